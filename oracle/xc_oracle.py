@@ -1,0 +1,433 @@
+"""CPU oracle for the extra-component method -- TEST INFRASTRUCTURE ONLY.
+
+Plain, slow, obviously-correct CPU implementation of what the B200 hot path
+computes, written from the paper (Terekhov, arXiv 2004.11610;
+``P:<n>`` = /root/reference/PAPER.md line n) and the readings listed in
+DESIGN.md ("R-<n>").  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+module.  It shares no code with ``paper_2004_11610_b200`` (the product); the
+only common module is the seeded input generator
+``paper_2004_11610_b200.inputs``, which holds none of the method's arithmetic.
+
+Two things are computed:
+
+* the plain definition, ``Y = A X`` (or ``diag(w~) A^T C``) with every entry
+  ``A[j,k] = phi_j(x_k)`` regenerated in double-double and rounded once
+  (``dense_apply``; C helper ``liborc.so``), and
+* the algorithm step by step in the paper's order: zeta, s,
+  block chain, extended/windowed rows, unitary DFT (Eq. 1, P:24;
+  library FFT as the DFT step), threshold, then the computation stage
+  of Algorithm 2 / its block form for the output axis and of
+  Algorithm 1 / block form for the input axis.
+
+Functions whose result is not pinned by a closed form or an independent
+library routine say so ("parity unpinned") in their docstring; see DESIGN.md.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse as sp
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+KIND_COS, KIND_JACOBI, KIND_LAGUERRE = 1, 2, 3
+
+
+def build_lib() -> str:
+    """Compile oracle/orc_special.c into oracle/liborc.so (plain gcc, OpenMP)."""
+    src = os.path.join(_HERE, "orc_special.c")
+    out = os.path.join(_HERE, "liborc.so")
+    if not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(src):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-ffp-contract=off",
+                               "-fno-fast-math", "-o", out, src, "-lm"])
+    return out
+
+
+def _lib():
+    global _LIB
+    if _LIB is None:
+        _LIB = ctypes.CDLL(build_lib())
+        dp = ctypes.POINTER(ctypes.c_double)
+        _LIB.orc_jacobi_entries.argtypes = [ctypes.c_double, ctypes.c_double, dp, ctypes.c_int64,
+                                            ctypes.c_int, ctypes.c_int, dp]
+        _LIB.orc_laguerre_entries.argtypes = [dp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, dp]
+        _LIB.orc_cos_entries.argtypes = [dp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         dp]
+        _LIB.orc_gauss_newton.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                          ctypes.c_int64, dp, dp, dp, ctypes.c_int]
+        _LIB.orc_dense_apply.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                         dp, ctypes.c_int64, ctypes.c_int64, dp, ctypes.c_int64, dp]
+        _LIB.orc_jacobi_mu0.restype = ctypes.c_double
+        _LIB.orc_jacobi_mu0.argtypes = [ctypes.c_double, ctypes.c_double]
+    return _LIB
+
+
+def _p(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+# ---------------------------------------------------------------------------
+# Special-function entries (double-double recurrences, rounded once)
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class Kind:
+    """Which special function generates A[j,k] = phi_j(x_k) (operator convention R-1).
+
+    kind COS:      phi_j(t) = cos(pi j t), nodes t in [0,1]
+    kind JACOBI:   phi_j(x) = p_j^(alpha,beta)(x), orthonormal on [-1,1] (R-4)
+    kind LAGUERRE: phi_j(x) = exp(-x/2) L_j(x), x >= 0
+    """
+    kind: int
+    alpha: float = 0.0
+    beta: float = 0.0
+
+
+def entries(kind: Kind, nodes: np.ndarray, m0: int, m1: int, m_off: int = 0) -> np.ndarray:
+    """E[k, m-m0] = phi_{m+m_off}(x_k) for m in [m0, m1) (node-major)."""
+    x = np.ascontiguousarray(nodes, dtype=np.float64)
+    out = np.empty((x.size, m1 - m0), dtype=np.float64)
+    lib = _lib()
+    if kind.kind == KIND_COS:
+        lib.orc_cos_entries(_p(x), x.size, m0, m1, m_off, _p(out))
+    elif kind.kind == KIND_JACOBI:
+        assert m_off == 0
+        lib.orc_jacobi_entries(kind.alpha, kind.beta, _p(x), x.size, m0, m1, _p(out))
+    elif kind.kind == KIND_LAGUERRE:
+        assert m_off == 0
+        lib.orc_laguerre_entries(_p(x), x.size, m0, m1, _p(out))
+    else:
+        raise ValueError(kind)
+    return out
+
+
+def jacobi_mu0(alpha: float, beta: float) -> float:
+    return _lib().orc_jacobi_mu0(alpha, beta)
+
+
+# ---------------------------------------------------------------------------
+# Gauss rules (inputs of the Legendre/Jacobi/Laguerre configs)
+# ---------------------------------------------------------------------------
+def gauss_rule(kind: Kind, N: int, newton: int = 2):
+    """Gauss nodes (ascending) and weights for the kind's orthogonality weight.
+
+    Initial guesses: a library routine (scipy's asymptotic Gauss-Legendre rule,
+    else the eigenvalues of the fp64 Jacobi matrix via scipy), then Newton in
+    double-double on p_N and weights by Christoffel-Darboux, all in liborc.
+    Returns (x, w, wt) where wt = w e^{x} (= 1/sum_j l_j(x)^2) for Laguerre,
+    wt = w otherwise.
+    """
+    import scipy.linalg
+    import scipy.special
+    if kind.kind == KIND_JACOBI and kind.alpha == 0.0 and kind.beta == 0.0:
+        x0, _ = scipy.special.roots_legendre(N)
+        iters = max(1, newton - 1)
+    elif kind.kind == KIND_JACOBI:
+        a, b = kind.alpha, kind.beta
+        n = np.arange(N, dtype=np.float64)
+        t = 2 * n + a + b
+        with np.errstate(divide="ignore", invalid="ignore"):
+            d = (b * b - a * a) / (t * (t + 2))
+        d[0] = (b - a) / (a + b + 2)
+        m = np.arange(1, N, dtype=np.float64)
+        t = 2 * m + a + b
+        e2 = 4 * m * (m + a) * (m + b) * (m + a + b) / (t * t * (t + 1) * (t - 1))
+        e2[0] = 4 * (1 + a) * (1 + b) / ((2 + a + b) ** 2 * (3 + a + b))
+        x0 = scipy.linalg.eigvalsh_tridiagonal(d, np.sqrt(e2))
+        iters = newton + 1
+    elif kind.kind == KIND_LAGUERRE:
+        n = np.arange(N, dtype=np.float64)
+        x0 = scipy.linalg.eigvalsh_tridiagonal(2 * n + 1, np.arange(1, N, dtype=np.float64))
+        iters = newton + 2
+    else:
+        raise ValueError("Gauss rule needs JACOBI or LAGUERRE")
+    x = np.ascontiguousarray(np.sort(x0), dtype=np.float64)
+    w = np.empty_like(x)
+    wt = np.empty_like(x)
+    bad = _lib().orc_gauss_newton(kind.kind, kind.alpha, kind.beta, N, _p(x), _p(w), _p(wt), iters)
+    if bad:
+        raise ArithmeticError("Gauss Newton produced non-finite nodes")
+    return x, w, wt
+
+
+# ---------------------------------------------------------------------------
+# Plain definition: the dense product (the paper's "direct method")
+# ---------------------------------------------------------------------------
+def dense_apply(kind: Kind, nodes: np.ndarray, X: np.ndarray) -> np.ndarray:
+    """Y[j,b] = sum_k phi_j(x_k) X[k,b], j < N (Y = A X; output indexed by degree)."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    N, B = X.shape
+    Y = np.empty((N, B), dtype=np.float64)
+    x = np.ascontiguousarray(nodes, dtype=np.float64)
+    rc = _lib().orc_dense_apply(kind.kind, kind.alpha, kind.beta, 1, _p(x), N, N, _p(X), B, _p(Y))
+    assert rc == 0
+    return Y
+
+
+def dense_apply_t(kind: Kind, nodes: np.ndarray, C: np.ndarray) -> np.ndarray:
+    """Y[k,b] = sum_j phi_j(x_k) C[j,b] (Y = A^T C; output indexed by node)."""
+    C = np.ascontiguousarray(C, dtype=np.float64)
+    N, B = C.shape
+    Y = np.empty((N, B), dtype=np.float64)
+    x = np.ascontiguousarray(nodes, dtype=np.float64)
+    rc = _lib().orc_dense_apply(kind.kind, kind.alpha, kind.beta, 2, _p(x), N, N, _p(C), B, _p(Y))
+    assert rc == 0
+    return Y
+
+
+# ---------------------------------------------------------------------------
+# Kaiser window, zeta(eps1), s(zeta, eps2)
+# ---------------------------------------------------------------------------
+def bessel_i0(x: float) -> float:
+    """I_0(x) = sum_k (x/2)^{2k} / (k!)^2 (power series, math.fsum)."""
+    x = float(x)
+    q = 0.25 * x * x
+    terms, t, k = [1.0], 1.0, 0
+    while True:
+        k += 1
+        t *= q / (k * k)
+        terms.append(t)
+        if t < 1e-18 * terms[0] and k > q:
+            break
+    return math.fsum(terms)
+
+
+def bessel_i1(x: float) -> float:
+    """I_1(x) = sum_k (x/2)^{2k+1} / (k! (k+1)!)."""
+    x = float(x)
+    q = 0.25 * x * x
+    t = 0.5 * x
+    terms, k = [t], 0
+    while True:
+        k += 1
+        t *= q / (k * (k + 1))
+        terms.append(t)
+        if t < 1e-18 * terms[0] and k > q:
+            break
+    return math.fsum(terms)
+
+
+def kaiser(zeta: float, npts: int) -> np.ndarray:
+    """w_n^{zeta,npts} = I0(zeta sqrt(1-(2n/npts-1)^2)) / I0(zeta), n = 0..npts.
+
+    A window over L positions uses npts = L - 1 (L samples; reading R-6).
+    """
+    n = np.arange(npts + 1, dtype=np.float64)
+    r = (2.0 * n - npts) / npts
+    arg = zeta * np.sqrt(np.maximum(0.0, 1.0 - r * r))
+    i0z = bessel_i0(zeta)
+    return np.array([bessel_i0(a) for a in arg]) / i0z
+
+
+def kaiser_at(zeta: float, npts: int, n: int) -> float:
+    r = (2.0 * n - npts) / npts
+    return bessel_i0(zeta * math.sqrt(max(0.0, 1.0 - r * r))) / bessel_i0(zeta)
+
+
+def solve_zeta(eps1: float, zeta0: float = 50.0, tol: float = 1e-14) -> float:
+    """zeta with 1/I0(zeta) = eps1, Newton from zeta0 = 50.
+
+    Newton is applied to the equivalent equation ln I0(zeta) = -ln eps1 (the
+    literal 1/I0 form diverges from zeta0 = 50; reading R-7).
+    """
+    z = zeta0
+    target = -math.log(eps1)
+    for _ in range(200):
+        g = math.log(bessel_i0(z)) - target
+        step = g / (bessel_i1(z) / bessel_i0(z))
+        z -= step
+        if abs(step) < tol * max(1.0, z):
+            return z
+    raise ArithmeticError("zeta Newton did not converge")
+
+
+def smooth5_even_at_least(n: int) -> int:
+    """Smallest even integer >= n whose only prime factors are 2, 3, 5 (R-9)."""
+    m = max(2, n + (n & 1))
+    while True:
+        r = m
+        for p in (2, 3, 5):
+            while r % p == 0:
+                r //= p
+        if r == 1:
+            return m
+        m += 2
+
+
+@dataclass
+class Block:
+    """One block of the (block) extra-component method.
+
+    Positions p in [0, L) carry degree p + m_off; the kept (real) degrees are
+    positions [keep_lo, keep_hi); the others are the extra components (P:131-180
+    for the trig form, P:281-301 for the block form).
+    """
+    L: int
+    m_off: int
+    keep_lo: int
+    keep_hi: int
+
+    @property
+    def H(self) -> int:
+        return self.L // 2 + 1
+
+
+@dataclass
+class Plan:
+    kind: Kind
+    N: int
+    eps1: float
+    eps2: float
+    zeta: float
+    blocks: list = field(default_factory=list)
+    tail: int = 0   # dense degrees [0, tail)
+
+
+def minimal_s(zeta: float, span: int, eps2: float, two_sided: bool) -> int:
+    """Smallest s >= 1 with w^{zeta, L-1}_s >= eps2, L = span + s (block) or span + 2s (trig).
+
+    Reading R-2 of P:184 (the printed '<' is satisfied by s = 0).
+    """
+    for s in range(1, 4 * span + 64):
+        L = span + (2 * s if two_sided else s)
+        if kaiser_at(zeta, L - 1, s) >= eps2:
+            return s
+    raise ArithmeticError("s search did not terminate (eps2 too close to 1?)")
+
+
+def make_plan(kind: Kind, N: int, eps: float, eps1: float | None = None, eps2: float | None = None,
+              dense_cutoff: int = 32) -> Plan:
+    """Block chain (R-2, R-3, R-8, R-9): see DESIGN.md."""
+    eps1 = eps if eps1 is None else eps1
+    eps2 = 1e-2 if eps2 is None else eps2
+    zeta = solve_zeta(eps1)
+    plan = Plan(kind, N, eps1, eps2, zeta)
+    if kind.kind == KIND_COS:
+        # trig form: extra components on both sides (Alg. 2)
+        s0 = minimal_s(zeta, N, eps2, two_sided=True)
+        L = smooth5_even_at_least(N + 2 * s0)
+        s = (L - N) // 2
+        plan.blocks.append(Block(L, -s, s, s + N))
+        plan.tail = 0
+        return plan
+    e = N
+    while e > dense_cutoff:
+        s0 = minimal_s(zeta, e, eps2, two_sided=False)
+        L = smooth5_even_at_least(e + s0)
+        s = L - e
+        plan.blocks.append(Block(L, 0, s, e))
+        e = s
+    plan.tail = e
+    return plan
+
+
+# ---------------------------------------------------------------------------
+# Compression (precomputation stage)
+# ---------------------------------------------------------------------------
+def node_spectra(plan: Plan, blk: Block, nodes: np.ndarray) -> np.ndarray:
+    """S[k, q] = (F W e_k)_q: unitary DFT (Eq. 1) of the windowed extended row of node k.
+
+    Returns the half spectrum q in [0, H) (real rows).  Bins 0 and L/2
+    are real by symmetry and their imaginary part is set to exactly 0.
+    """
+    w = kaiser(plan.zeta, blk.L - 1)
+    E = entries(plan.kind, nodes, 0, blk.L, blk.m_off)          # E[k, p] = phi_{p+m_off}(x_k)
+    S = np.fft.rfft(E * w[None, :], axis=1, norm="ortho")      # e^{-2 pi i p q / L} / sqrt(L)
+    S[:, 0] = S[:, 0].real
+    S[:, -1] = S[:, -1].real
+    return S
+
+
+def threshold(S: np.ndarray, eps1: float) -> np.ndarray:
+    """Per-node relative threshold (reading R-3): drop |S| < eps1 * max_q |S[k,q]|."""
+    mag2 = S.real ** 2 + S.imag ** 2
+    tau2 = (eps1 * eps1) * mag2.max(axis=1, keepdims=True)
+    return np.where(mag2 >= tau2, S, 0.0)
+
+
+@dataclass
+class Operator:
+    plan: Plan
+    S: list          # per block: scipy.sparse.csr_matrix (N x H) complex, kept entries
+    windows: list    # per block: Kaiser window on L points
+    P_tail: np.ndarray  # (tail x N) dense, phi_j(x_k) for j < tail
+
+
+def compress(plan: Plan, nodes: np.ndarray, node_chunk: int = 512) -> Operator:
+    S_list, W_list = [], []
+    for blk in plan.blocks:
+        parts = []
+        for k0 in range(0, plan.N, node_chunk):
+            Sk = threshold(node_spectra(plan, blk, nodes[k0:k0 + node_chunk]), plan.eps1)
+            parts.append(sp.csr_matrix(Sk))
+        S_list.append(sp.vstack(parts).tocsr())
+        W_list.append(kaiser(plan.zeta, blk.L - 1))
+    P_tail = entries(plan.kind, nodes, 0, plan.tail).T.copy() if plan.tail > 0 else np.zeros((0, plan.N))
+    return Operator(plan, S_list, W_list, P_tail)
+
+
+# ---------------------------------------------------------------------------
+# Computation stage
+# ---------------------------------------------------------------------------
+def apply_output_axis(op: Operator, X: np.ndarray) -> np.ndarray:
+    """Y = A X, output indexed by degree (Alg. 2; block form P:281).
+
+    Per block: u = S^T X (sparse), v = F* u (unitary inverse DFT, real
+    output), Y[kept] = v[kept] / w[kept]; the extra positions are discarded
+    (Fe2).  Tail degrees by the direct method.
+    """
+    X = np.asarray(X, dtype=np.float64)
+    N, B = X.shape
+    Y = np.zeros((N, B))
+    for blk, S, w in zip(op.plan.blocks, op.S, op.windows):
+        u = S.T @ X                                             # (H x B) complex
+        v = np.fft.irfft(u, n=blk.L, axis=0, norm="ortho")      # e^{+2 pi i p q / L} / sqrt(L)
+        lo, hi = blk.keep_lo, blk.keep_hi
+        Y[lo + blk.m_off:hi + blk.m_off] = v[lo:hi] / w[lo:hi, None]
+    if op.plan.tail:
+        Y[:op.plan.tail] = op.P_tail @ X
+    return Y
+
+
+def apply_input_axis(op: Operator, C: np.ndarray, wt: np.ndarray | None = None) -> np.ndarray:
+    """Y = diag(wt) A^T C, input indexed by degree (Alg. 1; block form P:281-301).
+
+    Per block: z = pad(C) / w (zeros outside the kept range, Fe1/Fe3), z' = F* z,
+    Y[k] += sum over the full spectrum of S[k,q] z'[q], evaluated on the half
+    spectrum as c_q Re(S z') with c_0 = c_{L/2} = 1, else 2 (real case).
+    """
+    C = np.asarray(C, dtype=np.float64)
+    N, B = C.shape
+    Y = np.zeros((N, B))
+    for blk, S, w in zip(op.plan.blocks, op.S, op.windows):
+        z = np.zeros((blk.L, B))
+        lo, hi = blk.keep_lo, blk.keep_hi
+        z[lo:hi] = C[lo + blk.m_off:hi + blk.m_off] / w[lo:hi, None]
+        zq = np.conj(np.fft.rfft(z, axis=0, norm="ortho"))     # (F* z)_q, q in [0, H)
+        c = np.full(blk.H, 2.0)
+        c[0] = 1.0
+        c[-1] = 1.0
+        Y += (S @ (c[:, None] * zq)).real
+    if op.plan.tail:
+        Y += op.P_tail.T @ C[:op.plan.tail]
+    if wt is not None:
+        Y *= wt[:, None]
+    return Y
+
+
+def rel_l2_cols(Y: np.ndarray, Yref: np.ndarray) -> np.ndarray:
+    """Per-column relative L2 error ||y - y_ref|| / ||y_ref|| (reading R-11)."""
+    num = np.linalg.norm(Y - Yref, axis=0)
+    den = np.linalg.norm(Yref, axis=0)
+    return num / np.where(den == 0, 1.0, den)
+
+
+def nnz(op: Operator) -> list:
+    return [int(S.nnz) for S in op.S]

@@ -1,0 +1,68 @@
+"""Seeded synthetic inputs shared by the tests, the oracle and bench.py.
+
+This module holds none of the method's arithmetic: only the workload shapes of
+BASELINE.json's configs and numpy PCG64 draws.
+Gauss nodes are NOT generated here: the tests take them from the oracle, the
+product computes its own (``xc.gauss_rule``).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+KIND_COS, KIND_JACOBI, KIND_LAGUERRE = 1, 2, 3
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    kind: int
+    N: int
+    B: int
+    eps: float
+    seed: int
+    alpha: float = 0.0
+    beta: float = 0.0
+    dirs: tuple = ("A",)
+    eps2: float = 1e-2
+
+
+CONFIGS = {
+    # BASELINE.json configs[0..4]; see DESIGN.md for the readings (R2 for c2, C-15 for c4)
+    "c1": Config("c1_legendre_512", KIND_JACOBI, 512, 1, 1e-12, 0),
+    "c2": Config("c2_noncos_4096", KIND_COS, 4096, 64, 1e-10, 1),
+    "c3": Config("c3_jacobi_16384", KIND_JACOBI, 16384, 256, 1e-12, 2, alpha=0.5, beta=-0.3),
+    "c4": Config("c4_laguerre_8192", KIND_LAGUERRE, 8192, 256, 1e-11, 3, dirs=("A", "WAT")),
+    "c5": Config("c5_legendre_65536", KIND_JACOBI, 65536, 4096, 1e-12, 4),
+}
+
+
+def cos_nodes(N: int, seed: int) -> np.ndarray:
+    """Non-uniform cosine nodes t_k = sort(U[0,1]) (first draw of the seed; c2 reading R2)."""
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.random(N))
+
+
+def rhs(N: int, B: int, seed: int, skip_cos_nodes: bool = False) -> np.ndarray:
+    """X ~ N(0,1), row-major N x B (RHS fastest).  For the cos config the node
+    draw comes first from the same stream (skip_cos_nodes=True)."""
+    rng = np.random.default_rng(seed)
+    if skip_cos_nodes:
+        rng.random(N)
+    return rng.standard_normal((N, B))
+
+
+def laguerre_coeffs(N: int, B: int, seed: int) -> np.ndarray:
+    """C[j,b] = N(0,1) / (1+j)^2 (BASELINE.json configs[3])."""
+    rng = np.random.default_rng(seed)
+    return rng.standard_normal((N, B)) / (1.0 + np.arange(N, dtype=np.float64))[:, None] ** 2
+
+
+def config_rhs(cfg: Config, B: int | None = None) -> np.ndarray:
+    B = cfg.B if B is None else B
+    if cfg.kind == KIND_COS:
+        return rhs(cfg.N, B, cfg.seed, skip_cos_nodes=True)
+    if cfg.kind == KIND_LAGUERRE:
+        return laguerre_coeffs(cfg.N, B, cfg.seed)
+    return rhs(cfg.N, B, cfg.seed)

@@ -1,0 +1,431 @@
+"""Pins for the CPU oracle: every part checked against something other than itself.
+
+Each test names the paper passage (P:<line> of /root/reference/PAPER.md) or the
+mathematical fact it uses.  Independent references: mpmath (arbitrary precision
+special functions), scipy (DCT-II, Gauss rules at small N, i0e+brentq), closed
+forms, and brute force at tiny N.  Runs on CPU (-m "not gpu").
+"""
+import json
+import math
+import os
+
+import mpmath as mp
+import numpy as np
+import pytest
+import scipy.fft
+import scipy.optimize
+import scipy.special
+
+import oracle as O
+from paper_2004_11610_b200 import inputs as I
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+LEG = O.Kind(O.KIND_JACOBI, 0.0, 0.0)
+JAC = O.Kind(O.KIND_JACOBI, 0.5, -0.3)
+CHEB = O.Kind(O.KIND_JACOBI, -0.5, -0.5)
+LAG = O.Kind(O.KIND_LAGUERRE)
+COS = O.Kind(O.KIND_COS)
+
+
+# --------------------------------------------------------------------------- Bessel / Kaiser
+@pytest.mark.parametrize("x", [0.0, 0.5, 3.0, 16.1, 25.56, 30.25, 50.0])
+def test_bessel_i0_i1_vs_mpmath(x):
+    """I0, I1 against mpmath's arbitrary-precision Bessel functions."""
+    mp.mp.dps = 40
+    assert abs(O.bessel_i0(x) / float(mp.besseli(0, x)) - 1) < 2e-15
+    if x > 0:
+        assert abs(O.bessel_i1(x) / float(mp.besseli(1, x)) - 1) < 2e-15
+
+
+def test_kaiser_closed_forms():
+    """w_0 = w_N = 1/I0(zeta); w_{N/2} = 1; symmetric; zeta = 0 gives ones."""
+    z = 25.5
+    w = O.kaiser(z, 100)
+    assert w[0] == pytest.approx(1 / float(mp.besseli(0, z)), rel=1e-15)
+    assert w[-1] == w[0]
+    assert w[50] == 1.0
+    np.testing.assert_array_equal(w, w[::-1])
+    np.testing.assert_array_equal(O.kaiser(0.0, 37), np.ones(38))
+    assert np.all(np.diff(w[:51]) > 0)
+
+
+@pytest.mark.parametrize("eps1", [1e-6, 1e-10, 1e-11, 1e-12, 1e-15])
+def test_zeta_solves_its_equation(eps1):
+    """1/I0(zeta) = eps1; checked with mpmath and against scipy brentq on i0e."""
+    z = O.solve_zeta(eps1)
+    mp.mp.dps = 40
+    assert abs(1 / float(mp.besseli(0, z)) / eps1 - 1) < 1e-12
+    zb = scipy.optimize.brentq(lambda t: math.log(scipy.special.i0e(t)) + t + math.log(eps1), 1, 100,
+                               xtol=1e-15)
+    assert z == pytest.approx(zb, abs=1e-10)
+
+
+@pytest.mark.parametrize("span,eps2,two", [(512, 1e-2, False), (16384, 1e-2, False), (4096, 1e-2, True),
+                                           (1000, 1e-3, False), (777, 1e-4, True)])
+def test_s_rule_definition(span, eps2, two):
+    """Reading R-2 of P:184: s is the smallest s >= 1 with w^{zeta,L-1}_s >= eps2."""
+    z = O.solve_zeta(1e-12)
+    s = O.minimal_s(z, span, eps2, two)
+    L = span + (2 * s if two else s)
+    assert O.kaiser_at(z, L - 1, s) >= eps2
+    if s > 1:
+        Lm = span + (2 * (s - 1) if two else s - 1)
+        assert O.kaiser_at(z, Lm - 1, s - 1) < eps2
+    # monotone: a larger eps2 needs at least as many extra components
+    assert O.minimal_s(z, span, eps2 * 3, two) >= s
+
+
+def test_smooth5_brute_force():
+    """R-9 (P:450 'locally optimal FFT size'): smallest even 2,3,5-smooth >= n."""
+    def smooth(m):
+        for p in (2, 3, 5):
+            while m % p == 0:
+                m //= p
+        return m == 1
+    for n in list(range(1, 400)) + [86399, 21601, 65537 + 20000]:
+        m = O.smooth5_even_at_least(n)
+        assert m >= n and m % 2 == 0 and smooth(m)
+        assert not any(smooth(k) and k % 2 == 0 for k in range(n, m))
+
+
+def test_block_chain_shape_vs_table1():
+    """P:491-518 (Table 1): first-block order N_1/N within 5 % and block count within 1,
+    for the minimal-s chain of reading R-2 (only the chain shape is pinned, C-9)."""
+    g = json.load(open(os.path.join(GOLD, "table1_block_orders.json")))
+    for col, e1, e2 in (("1e-6", g["eps1_1e-6"], g["eps2_1e-6"]), ("1e-10", g["eps1_1e-10"], g["eps2_1e-10"])):
+        z = O.solve_zeta(e1)
+        for Ns, row in g["rows"].items():
+            N = int(Ns)
+            if N < 1024:
+                continue
+            e, chain = N, []
+            while e > 32:
+                s = O.minimal_s(z, e, e2, False)
+                chain.append(e + s)
+                e = s
+            paper = row[col]
+            assert abs(chain[0] / paper[0] - 1) < 0.05, (N, col, chain, paper)
+            assert abs(len(chain) - len(paper)) <= 1, (N, col, chain, paper)
+
+
+def test_chain_is_self_consistent():
+    """R-8: block i keeps positions [s_i, s_{i-1}); L_i = s_{i-1} + s_i; tail <= cutoff."""
+    for cfg in ("c1", "c3", "c4", "c5"):
+        c = I.CONFIGS[cfg]
+        kind = O.Kind(c.kind, c.alpha, c.beta)
+        p = O.make_plan(kind, c.N, c.eps)
+        e = c.N
+        for b in p.blocks:
+            assert b.keep_hi == e and b.L == b.keep_hi + b.keep_lo and b.m_off == 0
+            assert O.kaiser_at(p.zeta, b.L - 1, b.keep_lo) >= p.eps2
+            e = b.keep_lo
+        assert p.tail == e <= 32
+
+
+# --------------------------------------------------------------------------- DFT convention
+def test_unitary_dft_convention():
+    """Eq. (1): unitary forward DFT with e^{-2 pi i jk/N}; F F* = I.
+    The oracle's DFT step is numpy's FFT with norm='ortho'; pin the convention."""
+    L = 30
+    e0 = np.zeros(L)
+    e0[0] = 1
+    np.testing.assert_allclose(np.fft.rfft(e0, norm="ortho"), np.full(L // 2 + 1, 1 / math.sqrt(L)), atol=1e-16)
+    x = np.random.default_rng(0).standard_normal(L)
+    direct = np.array([sum(x[j] * np.exp(-2j * np.pi * j * k / L) for j in range(L)) for k in range(L // 2 + 1)])
+    np.testing.assert_allclose(np.fft.rfft(x, norm="ortho"), direct / math.sqrt(L), atol=1e-14)
+    np.testing.assert_allclose(np.fft.irfft(np.fft.rfft(x, norm="ortho"), n=L, norm="ortho"), x, atol=1e-15)
+
+
+def test_convolution_theorem_appendix_a():
+    """(A.1) P:641-649: F(X . Y) = F X * F Y with the 1/sqrt(N) circular convolution."""
+    N = 24
+    rng = np.random.default_rng(1)
+    x, y = rng.standard_normal(N), rng.standard_normal(N)
+    F = lambda v: np.fft.fft(v, norm="ortho")
+    fx, fy = F(x), F(y)
+    conv = np.array([sum(fx[m] * fy[(n - m) % N] for m in range(N)) for n in range(N)]) / math.sqrt(N)
+    np.testing.assert_allclose(F(x * y), conv, atol=1e-14)
+
+
+def _closed_form_exp(theta, L):
+    """(y3) P:671: (1/sqrt(N)) sum_j e^{i j theta} w^{jk} = (e^{iN theta} - 1)/(e^{i theta} w^k - 1)/sqrt(N)."""
+    wk = np.exp(-2j * np.pi * np.arange(L) / L)
+    return (np.exp(1j * L * theta) - 1) / (np.exp(1j * theta) * wk - 1) / math.sqrt(L)
+
+
+def test_trig_row_spectrum_closed_form():
+    """Appendix A: with the window switched off (zeta = 0), the oracle's
+    per-node spectrum of a cos row equals the closed form
+    y^cos_k(theta) = (y^exp_k(theta) + y^exp_k(-theta)) / 2 built from (y3),
+    and the corrected (y1) of reading R-12."""
+    L = 48
+    plan = O.Plan(COS, 40, 1e-12, 1e-2, 0.0)
+    blk = O.Block(L, 0, 0, L)
+    t = np.array([0.1234, 0.4321, 0.77])
+    S = O.node_spectra(plan, blk, t)                     # (3, L/2+1)
+    for i, tk in enumerate(t):
+        th = math.pi * tk
+        y = 0.5 * (_closed_form_exp(th, L) + _closed_form_exp(-th, L))
+        np.testing.assert_allclose(S[i], y[:L // 2 + 1], atol=1e-14)
+        wk = np.exp(-2j * np.pi * np.arange(L) / L)
+        A = (math.cos(L * th) - 1) * math.cos(th) + math.sin(th) * math.sin(L * th)
+        y1 = (wk * A - (math.cos(L * th) - 1)) / (wk ** 2 - 2 * wk * math.cos(th) + 1) / math.sqrt(L)
+        np.testing.assert_allclose(S[i], y1[:L // 2 + 1], atol=1e-13)
+
+
+# --------------------------------------------------------------------------- special functions
+def test_legendre_closed_values():
+    """P_2(1/2) = -1/8; P_j(1) = 1, P_j(-1) = (-1)^j; orthonormal p_j = sqrt((2j+1)/2) P_j (R-4)."""
+    E = O.entries(LEG, np.array([0.5, 1.0, -1.0]), 0, 200)
+    j = np.arange(200)
+    nrm = np.sqrt((2 * j + 1) / 2)
+    assert E[0, 2] == pytest.approx(-0.125 * math.sqrt(2.5), rel=1e-15)
+    np.testing.assert_allclose(E[1], nrm, rtol=1e-15)
+    np.testing.assert_allclose(E[2], nrm * (-1.0) ** j, rtol=1e-15)
+
+
+def test_chebyshev_is_jacobi_minus_half():
+    """Jacobi(-1/2,-1/2) orthonormal = sqrt(2/pi) cos(j theta), 1/sqrt(pi) for j = 0."""
+    th = np.array([0.3, 1.1, 2.9])
+    E = O.entries(CHEB, np.cos(th), 0, 3000)
+    j = np.arange(3000)
+    ref = math.sqrt(2 / math.pi) * np.cos(np.outer(th, j))
+    ref[:, 0] = 1 / math.sqrt(math.pi)
+    np.testing.assert_allclose(E, ref, atol=2e-15)
+
+
+@pytest.mark.parametrize("a,b", [(0.0, 0.0), (0.5, -0.3), (1.0, 1.0), (-0.7, 2.5)])
+def test_jacobi_vs_mpmath(a, b):
+    """Orthonormal Jacobi p_n (chi read as the squared norm, R-4) vs mpmath.jacobi,
+    normalised by h_n = 2^{a+b+1}/(2n+a+b+1) G(n+a+1)G(n+b+1)/(G(n+a+b+1) n!), up to n = 3000."""
+    mp.mp.dps = 50
+    xs = [-0.999, -0.31, 0.0123, 0.77, 0.9999]
+    ns = [0, 1, 2, 7, 100, 1234, 2999]
+    E = O.entries(O.Kind(O.KIND_JACOBI, a, b), np.array(xs), 0, 3000)
+    for i, x in enumerate(xs):
+        for n in ns:
+            h = mp.mpf(2) ** (a + b + 1) / (2 * n + a + b + 1) * mp.gamma(n + a + 1) * mp.gamma(n + b + 1) / (
+                mp.gamma(n + a + b + 1) * mp.factorial(n))
+            ref = float(mp.jacobi(n, a, b, mp.mpf(x)) / mp.sqrt(h))
+            assert abs(E[i, n] - ref) <= 4e-15 * max(1.0, abs(ref)), (x, n, E[i, n], ref)
+
+
+def test_laguerre_vs_mpmath():
+    """l_n(t) = e^{-t/2} L_n(t) vs mpmath.laguerre, including t far beyond fp64's exp range."""
+    mp.mp.dps = 60
+    xs = [0.0, 0.5, 2.0, 37.0, 900.0, 3000.0, 20000.0]
+    E = O.entries(LAG, np.array(xs), 0, 2001)
+    assert E[2, 0] == pytest.approx(math.exp(-1), rel=1e-15)
+    assert E[2, 1] == pytest.approx(-math.exp(-1), rel=1e-15)   # l_1(2) = -e^{-1}
+    np.testing.assert_array_equal(E[0], np.ones(2001))          # l_n(0) = 1
+    for i, x in enumerate(xs):
+        for n in (0, 1, 5, 150, 1000, 2000):
+            ref = mp.exp(-mp.mpf(x) / 2) * mp.laguerre(n, 0, mp.mpf(x))
+            r = float(ref)
+            if abs(r) < 1e-300:
+                assert abs(E[i, n]) < 1e-290
+            else:
+                assert abs(E[i, n] - r) <= 1e-14 * abs(r) + 1e-300, (x, n, E[i, n], r)
+
+
+def test_cos_entries_exact_reduction():
+    """cos(pi m t) (P:68 with theta = pi t) vs mpmath at large m, negative m."""
+    mp.mp.dps = 50
+    t = np.array([0.1, 0.333333333333, 0.9999999])
+    E = O.entries(COS, t, 0, 20000, m_off=-5000)
+    for i, tk in enumerate(t):
+        for m in (-5000, -1, 0, 3, 9999, 14999):
+            ref = float(mp.cos(mp.pi * m * mp.mpf(tk)))
+            assert abs(E[i, m + 5000] - ref) < 3e-16
+
+
+# --------------------------------------------------------------------------- Gauss rules
+def test_gauss_small_closed_forms():
+    """N = 2: Gauss-Legendre +-1/sqrt(3), w = 1; Gauss-Laguerre 2 -+ sqrt(2), w = (2 +- sqrt 2)/4."""
+    x, w, _ = O.gauss_rule(LEG, 2)
+    np.testing.assert_allclose(x, [-1 / math.sqrt(3), 1 / math.sqrt(3)], rtol=1e-15)
+    np.testing.assert_allclose(w, [1, 1], rtol=1e-15)
+    x, w, wt = O.gauss_rule(LAG, 2)
+    np.testing.assert_allclose(x, [2 - math.sqrt(2), 2 + math.sqrt(2)], rtol=1e-15)
+    np.testing.assert_allclose(w, [(2 + math.sqrt(2)) / 4, (2 - math.sqrt(2)) / 4], rtol=1e-15)
+    np.testing.assert_allclose(wt, w * np.exp(x), rtol=1e-14)
+
+
+@pytest.mark.parametrize("kind", [LEG, JAC, CHEB, O.Kind(O.KIND_JACOBI, 2.0, 0.5)])
+def test_gauss_jacobi_identities(kind):
+    """sum w = 2^{a+b+1} G(a+1)G(b+1)/G(a+b+2); sum x = N(b-a)/(2N+a+b); p_N(x_k) = 0 (mpmath);
+    exact on monomials up to 2N-1; nodes match scipy at small N."""
+    a, b = kind.alpha, kind.beta
+    for N in (5, 64, 700):
+        x, w, _ = O.gauss_rule(kind, N)
+        mu0 = 2 ** (a + b + 1) * math.gamma(a + 1) * math.gamma(b + 1) / math.gamma(a + b + 2)
+        assert w.sum() == pytest.approx(mu0, rel=1e-13)
+        assert x.sum() == pytest.approx(N * (b - a) / (2 * N + a + b), abs=1e-12)
+        if N <= 64:
+            xs, ws = scipy.special.roots_jacobi(N, a, b)
+            np.testing.assert_allclose(x, xs, atol=1e-14)
+            np.testing.assert_allclose(w, ws, rtol=1e-11)   # scipy itself is ~1e-12
+            mp.mp.dps = 40
+            for deg in range(2 * N):
+                ex = mp.quad(lambda t: (1 - t) ** a * (1 + t) ** b * t ** deg, [-1, 0, 1])
+                assert float(np.dot(w, x ** deg)) == pytest.approx(float(ex), abs=1e-13)
+    mp.mp.dps = 40
+    N = 700
+    x, _, _ = O.gauss_rule(kind, N)
+    for k in (0, 1, N // 2, N - 1):
+        v = mp.jacobi(N, a, b, mp.mpf(x[k]))
+        d = mp.diff(lambda t: mp.jacobi(N, a, b, t), mp.mpf(x[k]))
+        assert abs(float(v / d)) <= 2 * np.spacing(abs(x[k])) + 1e-300
+
+
+def test_gauss_laguerre_identities():
+    """Gauss-Laguerre: sum w = 1, sum x = N^2, L_N(x_k) = 0 (mpmath), wt = 1/sum_j l_j(x_k)^2."""
+    N = 300
+    x, w, wt = O.gauss_rule(LAG, N)
+    assert w.sum() == pytest.approx(1.0, rel=1e-13)
+    assert x.sum() == pytest.approx(N * N, rel=1e-14)
+    mp.mp.dps = 60
+    for k in (0, 1, N // 2, N - 1):
+        v = mp.laguerre(N, 0, mp.mpf(x[k]))
+        d = mp.diff(lambda t: mp.laguerre(N, 0, t), mp.mpf(x[k]))
+        assert abs(float(v / d)) <= 2 * np.spacing(x[k])
+        s = sum((mp.exp(-mp.mpf(x[k]) / 2) * mp.laguerre(j, 0, mp.mpf(x[k]))) ** 2 for j in range(N))
+        assert wt[k] == pytest.approx(float(1 / s), rel=1e-13)
+
+
+@pytest.mark.parametrize("kind,N", [(LEG, 512), (JAC, 1024), (LAG, 512)])
+def test_discrete_orthogonality(kind, N):
+    """Gauss quadrature makes the transform orthogonal: A diag(w) A^T = I_N
+    (Laguerre functions with wt = w e^x)."""
+    x, w, wt = O.gauss_rule(kind, N)
+    E = O.entries(kind, x, 0, N)                 # E[k, j] = phi_j(x_k)
+    G = E.T @ (wt[:, None] * E)
+    assert np.abs(G - np.eye(N)).max() < 5e-13
+
+
+# --------------------------------------------------------------------------- dense product
+def test_dense_vs_mpmath_matrix():
+    """The plain definition Y = A X against a matrix built from mpmath entries (N = 24)."""
+    mp.mp.dps = 30
+    N = 24
+    x, _, _ = O.gauss_rule(LEG, N)
+    A = np.array([[float(mp.sqrt((2 * j + 1) / mp.mpf(2)) * mp.legendre(j, mp.mpf(xk))) for xk in x]
+                  for j in range(N)])
+    X = I.rhs(N, 3, 7)
+    np.testing.assert_allclose(O.dense_apply(LEG, x, X), A @ X, atol=1e-13)
+    np.testing.assert_allclose(O.dense_apply_t(LEG, x, X), A.T @ X, atol=1e-13)
+
+
+def test_dense_cos_is_dct2():
+    """at t_k = (k + 1/2)/N the cos transform is the DCT-II: y_j = (1/2) dct2(x)_j (scipy)."""
+    N = 300
+    t = (np.arange(N) + 0.5) / N
+    X = I.rhs(N, 4, 3)
+    np.testing.assert_allclose(O.dense_apply(COS, t, X), 0.5 * scipy.fft.dct(X, type=2, axis=0), atol=1e-12)
+
+
+def test_dense_chebyshev_gauss_is_dct2():
+    """Jacobi(-1/2,-1/2) at Gauss-Chebyshev nodes: y_j = sqrt(2/pi) (1/2) dct2(x reversed)_j, j >= 1;
+    y_0 = sum x / sqrt(pi); weights pi/N."""
+    N = 256
+    x, w, _ = O.gauss_rule(CHEB, N)
+    np.testing.assert_allclose(w, np.full(N, math.pi / N), rtol=1e-11)
+    X = I.rhs(N, 2, 4)
+    Y = O.dense_apply(CHEB, x, X)
+    d = 0.5 * scipy.fft.dct(X[::-1], type=2, axis=0)   # ascending x = descending theta
+    np.testing.assert_allclose(Y[1:], math.sqrt(2 / math.pi) * d[1:], atol=1e-12)
+    np.testing.assert_allclose(Y[0], X.sum(axis=0) / math.sqrt(math.pi), atol=1e-12)
+
+
+# --------------------------------------------------------------------------- compressed algorithm
+def test_threshold_soundness():
+    """P:106 per-node threshold (R-3): every dropped |S| < eps1 * node max, every kept one >=."""
+    x, _, _ = O.gauss_rule(JAC, 256)
+    plan = O.make_plan(JAC, 256, 1e-10)
+    blk = plan.blocks[0]
+    S = O.node_spectra(plan, blk, x)
+    K = O.threshold(S, plan.eps1)
+    m = np.abs(S).max(axis=1, keepdims=True)
+    assert np.all(np.abs(S[K == 0]) < (plan.eps1 * m * np.ones_like(S))[K == 0] * (1 + 1e-12))
+    assert np.all(np.abs(K[K != 0]) >= (plan.eps1 * m * np.ones_like(S))[K != 0] * (1 - 1e-12))
+    # Hermitian symmetry of real rows: bins 0 and L/2 real
+    assert np.all(S[:, 0].imag == 0) and np.all(S[:, -1].imag == 0)
+
+
+def test_spectrum_brute_force_tiny():
+    """Brute force (N = 16): the windowed-row spectrum equals the naive Eq.-(1) sum in mpmath."""
+    mp.mp.dps = 30
+    N = 16
+    x, _, _ = O.gauss_rule(LEG, N)
+    plan = O.make_plan(LEG, N, 1e-6, dense_cutoff=2)
+    blk = plan.blocks[0]
+    S = O.node_spectra(plan, blk, x)
+    w = O.kaiser(plan.zeta, blk.L - 1)
+    for k in (0, 5, 15):
+        for q in range(blk.H):
+            ref = sum(w[m] * mp.sqrt((2 * m + 1) / mp.mpf(2)) * mp.legendre(m, mp.mpf(x[k])) *
+                      mp.expj(-2 * mp.pi * m * q / blk.L) for m in range(blk.L)) / mp.sqrt(blk.L)
+            assert abs(complex(S[k, q]) - complex(ref)) < 1e-14
+
+
+@pytest.mark.parametrize("kind,N", [(LEG, 48), (JAC, 64), (LAG, 40), (COS, 50)])
+def test_keep_all_is_exact(kind, N):
+    """eps1 threshold -> 0 keeps every entry: both computation stages reproduce the dense
+    product (the extended identities comp1/comp2) to rounding x 1/eps2."""
+    if kind.kind == O.KIND_COS:
+        x = I.cos_nodes(N, 9)
+        wt = None
+    else:
+        x, _, wt = O.gauss_rule(kind, N)
+    plan = O.make_plan(kind, N, 1e-12, dense_cutoff=8)
+    plan.eps1 = 0.0                            # keep all (threshold only; zeta stays)
+    op = O.compress(plan, x)
+    X = I.rhs(N, 3, 11)
+    err = O.rel_l2_cols(O.apply_output_axis(op, X), O.dense_apply(kind, x, X))
+    assert err.max() < 1e-13
+    Yt = O.apply_input_axis(op, X)
+    err = O.rel_l2_cols(Yt, O.dense_apply_t(kind, x, X))
+    assert err.max() < 1e-13
+
+
+def test_compressed_cos_vs_dct2():
+    """P:74 + Alg. 2: the compressed non-uniform cos transform at DCT-II nodes meets 10 eps vs scipy."""
+    N = 512
+    t = (np.arange(N) + 0.5) / N
+    plan = O.make_plan(COS, N, 1e-10)
+    op = O.compress(plan, t)
+    X = I.rhs(N, 4, 6)
+    ref = 0.5 * scipy.fft.dct(X, type=2, axis=0)
+    assert O.rel_l2_cols(O.apply_output_axis(op, X), ref).max() < 1e-9
+
+
+@pytest.mark.parametrize("cfg,N", [("c1", 512), ("c2", 1024), ("c3", 1024), ("c4", 512)])
+def test_compressed_error_within_10eps(cfg, N):
+    """Calibration (parity unpinned by the paper, which states only 'accuracy ~ eps1/eps2'):
+    the oracle's compressed apply meets BASELINE's 10*eps bar against the dense product."""
+    c = I.CONFIGS[cfg]
+    kind = O.Kind(c.kind, c.alpha, c.beta)
+    if c.kind == O.KIND_COS:
+        x = I.cos_nodes(N, c.seed)
+    else:
+        x, _, wt = O.gauss_rule(kind, N)
+    plan = O.make_plan(kind, N, c.eps)
+    op = O.compress(plan, x)
+    X = I.rhs(N, 8, c.seed)
+    err = O.rel_l2_cols(O.apply_output_axis(op, X), O.dense_apply(kind, x, X))
+    assert err.max() < 10 * c.eps, err
+
+
+def test_laguerre_round_trip():
+    """C-15: with Gauss-Laguerre nodes, backward = diag(wt) A^T and forward = A are inverse
+    (Gauss exactness); the compressed pair reproduces C to ~eps."""
+    N = 384
+    x, _, wt = O.gauss_rule(LAG, N)
+    plan = O.make_plan(LAG, N, 1e-11)
+    op = O.compress(plan, x)
+    C = I.laguerre_coeffs(N, 4, 3)
+    Xf = O.apply_input_axis(op, C, wt)                   # backward (values at nodes)
+    Xd = wt[:, None] * O.dense_apply_t(LAG, x, C)
+    assert O.rel_l2_cols(Xf, Xd).max() < 1e-10
+    C2 = O.apply_output_axis(op, Xf)                     # forward
+    assert O.rel_l2_cols(C2, C).max() < 1e-9
