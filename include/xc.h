@@ -1,0 +1,165 @@
+/*
+ * xc.h -- C ABI of the B200-native extra-component transform library (libxc.so).
+ *
+ * Method: A. V. Terekhov, "An extra-component method for evaluating fast
+ * matrix-vector multiplication with special functions", arXiv 2004.11610.
+ * Citations "P:<n>" refer to lines of the paper's text; readings
+ * "R-<n>" are listed in DESIGN.md.
+ *
+ * Operator convention (R-1): A[j,k] = phi_j(x_k); row j = degree / frequency,
+ * column k = node.  All arithmetic is fp64.  Matrices X, Y are row-major with
+ * the right-hand-side (RHS) index fastest: element (row r, rhs b) at r*ld + b.
+ *
+ * Ownership: the handle owns the compressed operator, its plans, twiddle
+ * tables and an internal workspace; the caller owns X, Y and the nodes.
+ * Nodes and weights are copied at build time.
+ *
+ * Errors: every call returns an xc_status; xc_last_error() returns a
+ * thread-local message for the last failing call on the calling thread.
+ * CUDA errors are reported as XC_ECUDA (the library never aborts).
+ */
+#ifndef XC_H_
+#define XC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct xc_op* xc_handle;
+
+typedef enum {
+  XC_OK = 0,
+  XC_EINVAL = 1,        /* bad argument: N < 2, B < 1, ld < B, non-finite / unsorted /
+                           out-of-domain nodes, eps outside (0,1), eps1 >= eps2      */
+  XC_ENUMERIC = 2,      /* zeta Newton did not converge, s search did not terminate  */
+  XC_ESTATE = 3,        /* direction applied that was not built                       */
+  XC_ENOMEM = 4,        /* device allocation failed                                   */
+  XC_ECUDA = 5,         /* CUDA runtime error                                         */
+  XC_EUNSUPPORTED = 6   /* size beyond the FFT engine's range (L > 1024^2, ...)       */
+} xc_status;
+
+typedef enum {
+  XC_COS = 1,       /* A[j,k] = cos(pi j t_k), nodes t_k in [0,1] (P:66-70 with theta = pi t;
+                       non-block Algorithm 2/1 with extra components on both sides) */
+  XC_JACOBI = 2,    /* A[j,k] = p_j^(alpha,beta)(x_k), orthonormal on [-1,1]; Legendre = (0,0)
+                       (chi read as the squared norm, R-4; block form P:280-301)     */
+  XC_LAGUERRE = 3   /* A[j,k] = l_j(x_k) = exp(-x_k/2) L_j(x_k), x_k >= 0 (block form) */
+} xc_kind;
+
+typedef enum {
+  XC_DIR_A = 1,     /* Y = A X: output indexed by degree (Algorithm 2 / block form) */
+  XC_DIR_WAT = 2    /* Y = diag(wt) A^T X: input indexed by degree (Algorithm 1 / block form,
+                       P:188-204); wt are the weights passed at build time          */
+} xc_dir;
+
+typedef struct {
+  double alpha, beta;      /* XC_JACOBI parameters (> -1)                                    */
+  double eps1, eps2;       /* 0 => eps1 = eps (threshold), eps2 = 1e-2 (extra components, R-2) */
+  int dense_cutoff;        /* 0 => 32: degrees [0, t) with t <= cutoff done densely  */
+  int dirs;                /* bitmask of xc_dir layouts to build; 0 => XC_DIR_A only          */
+  const double* weights;   /* host, length N; required iff dirs & XC_DIR_WAT (copied)        */
+  int device;              /* CUDA device ordinal                                            */
+  void* stream;            /* cudaStream_t for the build (NULL = default stream)             */
+  int node_chunk;          /* 0 => auto: nodes per precompute chunk (device memory bound)    */
+} xc_params;
+
+typedef struct {
+  int64_t N;               /* transform size (degrees = nodes = N)                            */
+  int kind;
+  double zeta, eps1, eps2; /* Kaiser shape zeta(eps1) and thresholds                  */
+  int n_blocks;            /* number of compressed blocks (1 for XC_COS)                      */
+  int tail;                /* dense degrees [0, tail)                                         */
+  int dirs;                /* layouts built                                                   */
+  int64_t nnz;             /* kept complex entries over all blocks (half spectrum)            */
+  int64_t op_bytes_A;      /* device bytes of the XC_DIR_A apply operator (tiles + metadata)  */
+  int64_t op_bytes_WAT;    /* device bytes of the XC_DIR_WAT apply operator                   */
+  double flops_per_col_A;  /* algorithmic fp64 flops per RHS column, XC_DIR_A   */
+  double flops_per_col_WAT;
+  double dmma_flops_per_col_A;   /* flops the tensor-core (DMMA) tiles actually issue         */
+  double dmma_flops_per_col_WAT;
+} xc_info_t;
+
+typedef struct {
+  int L;            /* FFT length of the block (even, 2-3-5-smooth, R-9)                      */
+  int H;            /* half-spectrum bins L/2 + 1                                     */
+  int m_off;        /* position p carries degree p + m_off                                    */
+  int keep_lo;      /* kept positions [keep_lo, keep_hi) (Fe2/Fe3)      */
+  int keep_hi;
+  int64_t nnz;      /* kept complex entries                                                   */
+  int max_band;     /* widest kept run of any node (bins)                                     */
+} xc_block_info_t;
+
+/* Fill *p with defaults (all zero / NULL; device 0). */
+xc_status xc_params_default(xc_params* p);
+
+/* Precomputation stage (Alg. 1/2 step 1; block chain P:280-301):
+ * plans zeta/s/L_i on the host, then generates the special-function entries in
+ * double-double on the GPU, windows them, FFTs along the degree axis, thresholds
+ * per node (|S| >= eps1 * max_q |S[k,q]|, R-3) and builds the tensor-core tiles.
+ * nodes: host, length N, strictly ascending, finite, in the kind's domain.
+ * eps: accuracy parameter in (0,1); used as eps1 unless p->eps1 > 0.
+ * On success *out owns all device memory; destroy with xc_destroy. */
+xc_status xc_build_compressed(xc_kind kind, const xc_params* p, const double* nodes, int64_t N,
+                              double eps, xc_handle* out);
+
+/* Computation stage (Alg. 2 step 2 / Alg. 1 step 2 per block):
+ * X, Y: DEVICE pointers, row-major N x B with leading dimensions ldx, ldy >= B.
+ * Enqueues on `stream` only (no host synchronisation).  Allocates device
+ * workspace only if B exceeds the largest B reserved so far (xc_reserve).
+ * Not reentrant across streams on one handle (one workspace per handle). */
+xc_status xc_apply(xc_handle h, xc_dir dir, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                   int64_t B, void* stream);
+
+/* Same as xc_apply with HOST buffers X_host, Y_host (row-major N x B, ld = B):
+ * copies X to the device, applies, copies Y back, and synchronises `stream`.
+ * Host buffers should be pinned for full bandwidth. */
+xc_status xc_apply_host(xc_handle h, xc_dir dir, const double* X_host, double* Y_host, int64_t B,
+                        void* stream);
+
+/* Reserve workspace for up to B right-hand sides (may allocate). */
+xc_status xc_reserve(xc_handle h, int64_t B);
+
+/* Bytes of workspace xc_apply needs for B right-hand sides. */
+xc_status xc_workspace_query(xc_handle h, int64_t B, size_t* bytes);
+
+xc_status xc_info(xc_handle h, xc_info_t* out);
+xc_status xc_block_info(xc_handle h, int block, xc_block_info_t* out);
+
+/* Kaiser window of block `block` (host out, L values: w_p, p = 0..L-1, R-6). */
+xc_status xc_block_window(xc_handle h, int block, double* w_out);
+
+/* Kept spectrum of node k in block `block`: re/im host arrays of H values
+ * (dropped entries are 0).  For parity tests against the oracle. */
+xc_status xc_node_spectrum(xc_handle h, int block, int64_t k, double* re, double* im);
+
+/* Gauss rule of the kind's orthogonality weight, computed on device `device`
+ * (Sturm bisection on the Jacobi matrix + double-double Newton, Christoffel-Darboux
+ * weights).  nodes, weights: host out, length N (ascending).  wt (may be NULL):
+ * weights times e^{x} for XC_LAGUERRE (= 1/sum_j l_j(x)^2), else a copy of weights. */
+xc_status xc_gauss_rule(xc_kind kind, double alpha, double beta, int64_t N, double* nodes,
+                        double* weights, double* wt, int device);
+
+/* Host-only planning (no GPU needed): zeta(eps1), the block chain and
+ * FFT lengths (R-2, R-8, R-9).  Arrays L, m_off, keep_lo, keep_hi have room for
+ * max_blocks entries; *n_blocks receives the count, *tail the dense degrees.
+ * eps2 = 0 selects 1e-2, dense_cutoff = 0 selects 32. */
+xc_status xc_plan_chain(xc_kind kind, int64_t N, double eps1, double eps2, int dense_cutoff, double* zeta,
+                        int* n_blocks, int* L, int* m_off, int* keep_lo, int* keep_hi, int max_blocks,
+                        int* tail);
+
+/* Release all device memory of the handle (NULL is ignored). */
+void xc_destroy(xc_handle h);
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* xc_last_error(void);
+
+/* Library version string. */
+const char* xc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XC_H_ */

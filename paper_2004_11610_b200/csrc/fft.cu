@@ -1,0 +1,416 @@
+// fft.cu -- batched fp64 mixed-radix FFT for the extra-component method (sm_100a).
+//
+// The transform of Eq. (1) along the slow axis of a batch-fastest array
+// (element (n, col) at n*ld + col), for any 2-3-5-smooth length L (R-9).
+// Lengths up to 1024 run in one pass; longer ones as a four-step L = L1*L2:
+//   pass 1: for each n2, L1-point FFT over n = L2*n1 + n2, times w_L^{sigma n2 k1},
+//           stored at scratch[k1*L2 + n2]  (L2-resident: the scratch of one block)
+//   pass 2: for each k1, L2-point FFT over scratch[k1*L2 + n2], output k = k1 + L1*k2.
+// Each pass stages `cb` columns x `sc` sub-sequences in shared memory (ping-pong
+// buffers) and runs self-sorting Stockham radix-{8,4,5,3,2} stages with the
+// butterflies in registers; twiddles come from exact tables (long double on the
+// host), raised to the r-th power by complex multiplication.
+//
+// The prologue/epilogue of the first/last pass are fused with the method's
+// pre/post-processing (P:163-180 Fe2 truncate + W^{-1}, P:137-156 Fe1 pad + W^{-1}),
+// see FftPro / FftEpi in xc_internal.cuh.
+#include <math.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "xc_internal.cuh"
+
+namespace {
+
+__device__ __forceinline__ double2 c_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 c_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 c_mul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 c_scale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+// multiply by S*i
+template <int S>
+__device__ __forceinline__ double2 c_si(double2 a) {
+  return S > 0 ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+
+template <int S>
+__device__ __forceinline__ void bfly2(double2* v) {
+  double2 t = c_sub(v[0], v[1]);
+  v[0] = c_add(v[0], v[1]);
+  v[1] = t;
+}
+template <int S>
+__device__ __forceinline__ void bfly4(double2& v0, double2& v1, double2& v2, double2& v3) {
+  double2 a = c_add(v0, v2), b = c_sub(v0, v2), c = c_add(v1, v3), d = c_si<S>(c_sub(v1, v3));
+  v0 = c_add(a, c);
+  v2 = c_sub(a, c);
+  v1 = c_add(b, d);
+  v3 = c_sub(b, d);
+}
+template <int S>
+__device__ __forceinline__ void bfly8(double2* v) {
+  const double R2 = 0.70710678118654752440;
+  double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+  double2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+  bfly4<S>(e0, e1, e2, e3);
+  bfly4<S>(o0, o1, o2, o3);
+  // o1 *= e^{S i pi/4}, o2 *= S i, o3 *= e^{S 3 i pi/4}
+  o1 = make_double2(R2 * (o1.x - S * o1.y), R2 * (o1.y + S * o1.x));
+  o2 = c_si<S>(o2);
+  o3 = make_double2(R2 * (-o3.x - S * o3.y), R2 * (-o3.y + S * o3.x));
+  v[0] = c_add(e0, o0);
+  v[4] = c_sub(e0, o0);
+  v[1] = c_add(e1, o1);
+  v[5] = c_sub(e1, o1);
+  v[2] = c_add(e2, o2);
+  v[6] = c_sub(e2, o2);
+  v[3] = c_add(e3, o3);
+  v[7] = c_sub(e3, o3);
+}
+template <int S>
+__device__ __forceinline__ void bfly3(double2* v) {
+  const double C = -0.5, SN = S * 0.86602540378443864676;
+  double2 a = c_add(v[1], v[2]), b = c_sub(v[1], v[2]);
+  double2 m = make_double2(v[0].x + C * a.x, v[0].y + C * a.y);
+  double2 ib = make_double2(-SN * b.y, SN * b.x);  // i * SN * b
+  v[0] = c_add(v[0], a);
+  v[1] = c_add(m, ib);
+  v[2] = c_sub(m, ib);
+}
+template <int S>
+__device__ __forceinline__ void bfly5(double2* v) {
+  const double C1 = 0.30901699437494742410, C2 = -0.80901699437494742410;
+  const double S1 = S * 0.95105651629515357212, S2 = S * 0.58778525229247312917;
+  double2 a1 = c_add(v[1], v[4]), b1 = c_sub(v[1], v[4]);
+  double2 a2 = c_add(v[2], v[3]), b2 = c_sub(v[2], v[3]);
+  double2 x0 = v[0];
+  double2 m1 = make_double2(x0.x + C1 * a1.x + C2 * a2.x, x0.y + C1 * a1.y + C2 * a2.y);
+  double2 m2 = make_double2(x0.x + C2 * a1.x + C1 * a2.x, x0.y + C2 * a1.y + C1 * a2.y);
+  double2 t1 = make_double2(S1 * b1.x + S2 * b2.x, S1 * b1.y + S2 * b2.y);
+  double2 t2 = make_double2(S2 * b1.x - S1 * b2.x, S2 * b1.y - S1 * b2.y);
+  // i * t = (-t.y, t.x)
+  v[0] = make_double2(x0.x + a1.x + a2.x, x0.y + a1.y + a2.y);
+  v[1] = make_double2(m1.x - t1.y, m1.y + t1.x);
+  v[4] = make_double2(m1.x + t1.y, m1.y - t1.x);
+  v[2] = make_double2(m2.x - t2.y, m2.y + t2.x);
+  v[3] = make_double2(m2.x + t2.y, m2.y - t2.x);
+}
+
+// One self-sorting Stockham radix-r stage over nseq interleaved sequences of length R
+// (smem layout [n][seq]); twiddle w_{Ns r}^{k t} from the length-R table.
+template <int r, int SIG>
+__device__ __forceinline__ void stockham_stage(const double2* __restrict__ bin, double2* __restrict__ bout, int R,
+                                               int Ns, int nseq, const double2* __restrict__ tw, int tid, int nth) {
+  const int Rr = R / r;
+  const int twstep = R / (Ns * r);
+  for (int i = tid; i < Rr * nseq; i += nth) {
+    int j = i / nseq, sq = i - j * nseq;
+    int k = j % Ns;
+    double2 v[r];
+#pragma unroll
+    for (int t = 0; t < r; ++t) v[t] = bin[(j + t * Rr) * nseq + sq];
+    if (k > 0) {
+      double2 w = __ldg(tw + k * twstep);
+      if (SIG < 0) w.y = -w.y;
+      double2 wt = w;
+#pragma unroll
+      for (int t = 1; t < r; ++t) {
+        v[t] = c_mul(v[t], wt);
+        if (t + 1 < r) wt = c_mul(wt, w);
+      }
+    }
+    if (r == 2) bfly2<SIG>(v);
+    else if (r == 3) bfly3<SIG>(v);
+    else if (r == 4) bfly4<SIG>(v[0], v[1], v[2], v[3]);
+    else if (r == 5) bfly5<SIG>(v);
+    else bfly8<SIG>(v);
+    int idxD = (j / Ns) * Ns * r + k;
+#pragma unroll
+    for (int u = 0; u < r; ++u) bout[(idxD + u * Ns) * nseq + sq] = v[u];
+  }
+}
+
+struct PassArgs {
+  int R;             // sub-FFT length of this pass
+  int nf;            // number of radix stages
+  int f[12];         // radices
+  const double2* tw; // e^{+2 pi i n/R}
+  const double2* twL;// e^{+2 pi i n/L} (stage 0 only)
+  int L, L1, L2;
+  int stage;         // 0 = first of two, 1 = second of two, 2 = single
+  int S;             // number of sub-sequences per column
+  int ncol, cb, sc;
+  double2* scratch;  // two-pass intermediate, index (k1*L2 + n2)*ncol + col
+};
+
+template <int PRO>
+__device__ __forceinline__ double2 pro_load(const FftIO& io, int L, int n, int col) {
+  if (PRO == PRO_PLAIN) {
+    return io.src[(int64_t)n * io.lds + col];
+  } else if (PRO == PRO_UPART) {
+    // u[q] = sum of the partial sums of group q/4; Hermitian extension for n > L/2
+    int q = (n <= L / 2) ? n : L - n;
+    int g = q >> 2;
+    int r = 2 * (q & 3);
+    int nch = io.grp_nch[g];
+    int64_t row = io.grp_base[g] + r;
+    double re = 0.0, im = 0.0;
+    for (int c = 0; c < nch; ++c) {
+      re += io.part[row * io.ldp + col];
+      im += io.part[(row + 1) * io.ldp + col];
+      row += 8;
+    }
+    return make_double2(re, (n <= L / 2) ? im : -im);
+  } else {  // PRO_XREAL: pad + W^{-1} (Fe1 / Fe3)
+    if (n >= io.keep_lo && n < io.keep_hi)
+      return make_double2(io.X[(int64_t)(n + io.m_off) * io.ldx + col] * io.winv[n], 0.0);
+    return make_double2(0.0, 0.0);
+  }
+}
+
+template <int EPI>
+__device__ __forceinline__ void epi_store(const FftIO& io, int k, int col, double2 v) {
+  if (EPI == EPI_PLAIN) {
+    if (k < io.kmax) io.dst[(int64_t)k * io.ldd + col] = c_scale(v, io.scale);
+  } else if (EPI == EPI_YREAL) {
+    // Fe2 discard + W^{-1} (Alg. 2 step 2.1-2.2)
+    if (k >= io.keep_lo && k < io.keep_hi) io.Y[(int64_t)(k + io.m_off) * io.ldy + col] = v.x * io.yscale[k];
+  } else {
+    if (k < io.H) {
+      io.zre[(int64_t)k * io.ldz + col] = v.x * io.scale;
+      io.zim[(int64_t)k * io.ldz + col] = v.y * io.scale;
+    }
+  }
+}
+
+template <int PRO, int EPI, int SIG>
+__global__ void __launch_bounds__(256) fft_pass(PassArgs a, FftIO io) {
+  extern __shared__ double2 smem[];
+  const int nseq = a.cb * a.sc;
+  double2* bin = smem;
+  double2* bout = smem + a.R * nseq;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int sub0 = blockIdx.y * a.sc, col0 = blockIdx.x * a.cb;
+
+  // ---- load (prologue) ----
+  for (int i = tid; i < a.R * nseq; i += nth) {
+    int e = i / nseq, sq = i - e * nseq;
+    int sub = sub0 + sq / a.cb, col = col0 + sq % a.cb;
+    double2 v = make_double2(0.0, 0.0);
+    if (sub < a.S && col < a.ncol) {
+      if (a.stage == 1) {
+        v = a.scratch[((int64_t)sub * a.L2 + e) * a.ncol + col];
+      } else {
+        int n = (a.stage == 0) ? a.L2 * e + sub : e;
+        v = pro_load<PRO>(io, a.L, n, col);
+      }
+    }
+    bin[e * nseq + sq] = v;
+  }
+  __syncthreads();
+
+  // ---- Stockham stages ----
+  int Ns = 1;
+  for (int st = 0; st < a.nf; ++st) {
+    const int r = a.f[st];
+    switch (r) {
+      case 2: stockham_stage<2, SIG>(bin, bout, a.R, Ns, nseq, a.tw, tid, nth); break;
+      case 3: stockham_stage<3, SIG>(bin, bout, a.R, Ns, nseq, a.tw, tid, nth); break;
+      case 4: stockham_stage<4, SIG>(bin, bout, a.R, Ns, nseq, a.tw, tid, nth); break;
+      case 5: stockham_stage<5, SIG>(bin, bout, a.R, Ns, nseq, a.tw, tid, nth); break;
+      default: stockham_stage<8, SIG>(bin, bout, a.R, Ns, nseq, a.tw, tid, nth); break;
+    }
+    __syncthreads();
+    double2* t = bin;
+    bin = bout;
+    bout = t;
+    Ns *= r;
+  }
+
+  // ---- store (epilogue) ----
+  for (int i = tid; i < a.R * nseq; i += nth) {
+    int e = i / nseq, sq = i - e * nseq;
+    int sub = sub0 + sq / a.cb, col = col0 + sq % a.cb;
+    if (sub >= a.S || col >= a.ncol) continue;
+    double2 v = bin[e * nseq + sq];
+    if (a.stage == 0) {
+      // four-step twiddle w_L^{sigma n2 k1}: n2 = sub, k1 = e
+      int idx = (int)(((int64_t)sub * e) % a.L);
+      double2 w = a.twL[idx];
+      if (SIG < 0) w.y = -w.y;
+      a.scratch[((int64_t)e * a.L2 + sub) * a.ncol + col] = c_mul(v, w);
+    } else {
+      int k = (a.stage == 1) ? sub + a.L1 * e : e;
+      epi_store<EPI>(io, k, col, v);
+    }
+  }
+}
+
+void factorize(int R, int& nf, int* f) {
+  nf = 0;
+  while (R % 8 == 0) { f[nf++] = 8; R /= 8; }
+  while (R % 4 == 0) { f[nf++] = 4; R /= 4; }
+  while (R % 2 == 0) { f[nf++] = 2; R /= 2; }
+  while (R % 5 == 0) { f[nf++] = 5; R /= 5; }
+  while (R % 3 == 0) { f[nf++] = 3; R /= 3; }
+  if (R != 1) nf = -1;
+}
+
+void twiddle_table(int n, std::vector<double2>& t) {
+  t.resize(n);
+  const long double PI2 = 6.283185307179586476925286766559005768L;
+  for (int i = 0; i < n; ++i) {
+    // exact octant symmetry keeps the table symmetric to the bit
+    long double ang = PI2 * (long double)i / (long double)n;
+    t[i] = make_double2((double)cosl(ang), (double)sinl(ang));
+  }
+}
+
+template <int PRO, int EPI, int SIG>
+xc_status launch_pass(const PassArgs& a, const FftIO& io, cudaStream_t st) {
+  const int nseq = a.cb * a.sc;
+  size_t sm = 2ull * a.R * nseq * sizeof(double2);
+  static bool attr_set = false;
+  if (!attr_set) {
+    XC_CUDA(cudaFuncSetAttribute(fft_pass<PRO, EPI, SIG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 96 * 1024));
+    attr_set = true;
+  }
+  dim3 grid((a.ncol + a.cb - 1) / a.cb, (a.S + a.sc - 1) / a.sc);
+  int work = a.R * nseq / 2;
+  int th = work >= 256 ? 256 : (work >= 128 ? 128 : 64);
+  fft_pass<PRO, EPI, SIG><<<grid, th, sm, st>>>(a, io);
+  XC_CUDA(cudaGetLastError());
+  return XC_OK;
+}
+
+template <int SIG>
+xc_status dispatch(FftPro pro, FftEpi epi, const PassArgs& a, const FftIO& io, cudaStream_t st) {
+  // pass-1-of-2 uses only the prologue, pass-2-of-2 only the epilogue
+  if (a.stage == 0) {
+    if (pro == PRO_PLAIN) return launch_pass<PRO_PLAIN, EPI_PLAIN, SIG>(a, io, st);
+    if (pro == PRO_UPART) return launch_pass<PRO_UPART, EPI_PLAIN, SIG>(a, io, st);
+    return launch_pass<PRO_XREAL, EPI_PLAIN, SIG>(a, io, st);
+  }
+  if (a.stage == 1) {
+    if (epi == EPI_PLAIN) return launch_pass<PRO_PLAIN, EPI_PLAIN, SIG>(a, io, st);
+    if (epi == EPI_YREAL) return launch_pass<PRO_PLAIN, EPI_YREAL, SIG>(a, io, st);
+    return launch_pass<PRO_PLAIN, EPI_ZPLANES, SIG>(a, io, st);
+  }
+#define XC_CASE(P, E) \
+  if (pro == P && epi == E) return launch_pass<P, E, SIG>(a, io, st);
+  XC_CASE(PRO_PLAIN, EPI_PLAIN)
+  XC_CASE(PRO_PLAIN, EPI_YREAL)
+  XC_CASE(PRO_PLAIN, EPI_ZPLANES)
+  XC_CASE(PRO_UPART, EPI_PLAIN)
+  XC_CASE(PRO_UPART, EPI_YREAL)
+  XC_CASE(PRO_UPART, EPI_ZPLANES)
+  XC_CASE(PRO_XREAL, EPI_PLAIN)
+  XC_CASE(PRO_XREAL, EPI_YREAL)
+  XC_CASE(PRO_XREAL, EPI_ZPLANES)
+#undef XC_CASE
+  xc_set_error("fft: bad prologue/epilogue");
+  return XC_EINVAL;
+}
+
+void choose_tile(int R, int ncol, int& cb, int& sc) {
+  int nseq = 1;
+  while (nseq * 2 * R <= 2048 && nseq < 16) nseq *= 2;
+  cb = 1;
+  while (cb < nseq && cb < ncol && cb < 8) cb *= 2;
+  sc = nseq / cb;
+}
+
+}  // namespace
+
+xc_status fft_plan_make(FftPlan& p, int L) {
+  p.L = L;
+  if (L <= 1024) {
+    p.L1 = L;
+    p.L2 = 1;
+  } else {
+    int best = -1;
+    for (int d = 2; (int64_t)d * d <= L; ++d)
+      if (L % d == 0) best = d;
+    if (best < 0 || L / best > 1024) {
+      xc_set_error("fft: length " + std::to_string(L) + " not splittable into two factors <= 1024");
+      return XC_EUNSUPPORTED;
+    }
+    p.L1 = best;
+    p.L2 = L / best;
+  }
+  factorize(p.L1, p.nf1, p.f1);
+  factorize(p.L2, p.nf2, p.f2);
+  if (p.nf1 < 0 || p.nf2 < 0) {
+    xc_set_error("fft: length " + std::to_string(L) + " is not 2-3-5-smooth");
+    return XC_EUNSUPPORTED;
+  }
+  std::vector<double2> t1, t2, tL;
+  twiddle_table(p.L1, t1);
+  twiddle_table(p.L2, t2);
+  if (p.L2 > 1) twiddle_table(L, tL);
+  size_t bytes = (t1.size() + t2.size() + tL.size()) * sizeof(double2);
+  XC_TRY(dev_alloc(p.mem, bytes));
+  double2* base = (double2*)p.mem.p;
+  p.tw1 = base;
+  p.tw2 = base + t1.size();
+  p.twL = tL.empty() ? nullptr : base + t1.size() + t2.size();
+  XC_CUDA(cudaMemcpy(p.tw1, t1.data(), t1.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  XC_CUDA(cudaMemcpy(p.tw2, t2.data(), t2.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  if (!tL.empty()) XC_CUDA(cudaMemcpy(p.twL, tL.data(), tL.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  return XC_OK;
+}
+
+void fft_plan_free(FftPlan& p) { dev_free(p.mem); }
+
+xc_status fft_run(const FftPlan& p, int sigma, FftPro pro, FftEpi epi, const FftIO& io, int ncol,
+                  double2* scratch, cudaStream_t st) {
+  PassArgs a{};
+  a.L = p.L;
+  a.L1 = p.L1;
+  a.L2 = p.L2;
+  a.ncol = ncol;
+  a.scratch = scratch;
+  a.twL = p.twL;
+  if (p.L2 == 1) {
+    a.R = p.L1;
+    a.nf = p.nf1;
+    for (int i = 0; i < p.nf1; ++i) a.f[i] = p.f1[i];
+    a.tw = p.tw1;
+    a.stage = 2;
+    a.S = 1;
+    choose_tile(a.R, ncol, a.cb, a.sc);
+    a.sc = 1;  // single pass: one sub-sequence per column
+    {
+      int nseq = 1;
+      while (nseq * 2 * a.R <= 2048 && nseq < 16) nseq *= 2;
+      a.cb = std::min(nseq, 8);
+      while (a.cb > 1 && a.cb / 2 >= ncol) a.cb /= 2;
+    }
+    return sigma > 0 ? dispatch<1>(pro, epi, a, io, st) : dispatch<-1>(pro, epi, a, io, st);
+  }
+  if (!scratch) {
+    xc_set_error("fft: two-pass length needs scratch");
+    return XC_EINVAL;
+  }
+  // pass 1: L1-point FFTs, L2 sub-sequences per column
+  a.R = p.L1;
+  a.nf = p.nf1;
+  for (int i = 0; i < p.nf1; ++i) a.f[i] = p.f1[i];
+  a.tw = p.tw1;
+  a.stage = 0;
+  a.S = p.L2;
+  choose_tile(a.R, ncol, a.cb, a.sc);
+  XC_TRY(sigma > 0 ? dispatch<1>(pro, epi, a, io, st) : dispatch<-1>(pro, epi, a, io, st));
+  // pass 2: L2-point FFTs, L1 sub-sequences per column
+  a.R = p.L2;
+  a.nf = p.nf2;
+  for (int i = 0; i < p.nf2; ++i) a.f[i] = p.f2[i];
+  a.tw = p.tw2;
+  a.stage = 1;
+  a.S = p.L1;
+  choose_tile(a.R, ncol, a.cb, a.sc);
+  return sigma > 0 ? dispatch<1>(pro, epi, a, io, st) : dispatch<-1>(pro, epi, a, io, st);
+}

@@ -1,0 +1,193 @@
+// gen.cu -- GPU precomputation of the compressed operator (precomputation stage,
+// Alg. 1/2 steps 1.2-1.3; block form P:281).
+//
+//  * entry generation: phi_m(x_k) for all positions m of a block, one thread per
+//    node running the three-term recurrence in double-double and rounding once
+//    (R-5; "accumulation of errors when using the three-term recurrence"),
+//    times the Kaiser window (W_M);
+//  * band detection / compaction after the FFT: per node, keep |S| >= eps1 * max
+//    (R-3), one contiguous run per node (start, len) with the dropped
+//    entries inside the run stored as exact zeros;
+//  * tile fill for the tensor-core SpMM (spmm.cu).
+#include <math.h>
+
+#include "xc_internal.cuh"
+
+namespace {
+
+// 1/(2 ln 2) and ln 2 as double-double
+__device__ const double kI2L2_H = 0.7213475204444817, kI2L2_L = 1.0177636870465517e-17;
+__device__ const double kLN2_H = 0.6931471805599453, kLN2_L = 2.3190468138462996e-17;
+
+template <bool CPLX>
+__device__ __forceinline__ void put(void* F, int64_t idx, double v) {
+  if (CPLX)
+    reinterpret_cast<double2*>(F)[idx] = make_double2(v, 0.0);
+  else
+    reinterpret_cast<double*>(F)[idx] = v;
+}
+
+// Orthonormal Jacobi: x p_n = a_{n+1} p_{n+1} + b_n p_n + a_n p_{n-1}  (R-4)
+template <bool CPLX>
+__global__ void gen_jacobi(GenParams g, void* F, int64_t ld) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= g.nc) return;
+  const ddv x = dv(g.nodes[k]);
+  ddv p = g.p0, pm1 = dv(0.0);
+  for (int n = 0; n < g.L; ++n) {
+    double e = ddround(p);
+    put<CPLX>(F, (int64_t)n * ld + k, g.w ? g.w[n] * e : e);
+    const double2 bn = g.jab[3 * n + 0], an = g.jab[3 * n + 1], ia = g.jab[3 * (n + 1) + 2];
+    ddv t = ddsub(ddmul(ddsub(x, ddv{bn.x, bn.y}), p), ddmul(ddv{an.x, an.y}, pm1));
+    pm1 = p;
+    p = ddmul(t, ddv{ia.x, ia.y});
+  }
+}
+
+__device__ ddv dexp_neg_small(ddv gv) {
+  // exp(-g), 0 <= g < ln 2: Taylor series in double-double
+  ddv term = dv(1.0), sum = dv(1.0), mg = ddneg(gv);
+  for (int n = 1; n < 40; ++n) {
+    term = dddiv(ddmul(term, mg), dv((double)n));
+    sum = ddadd(sum, term);
+    if (fabs(term.h) < 1e-34) break;
+  }
+  return sum;
+}
+
+// Laguerre functions l_n = exp(-x/2) L_n(x) with a tracked binary exponent
+template <bool CPLX>
+__global__ void gen_laguerre(GenParams g, void* F, int64_t ld) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= g.nc) return;
+  const double xk = g.nodes[k];
+  ddv y = ddmuld(ddv{kI2L2_H, kI2L2_L}, xk);  // x / (2 ln 2)
+  double ny = floor(y.h);
+  ddv f = ddsub(y, dv(ny));
+  if (f.h < 0.0) {
+    ny -= 1.0;
+    f = ddadd(f, dv(1.0));
+  }
+  const ddv ef = dexp_neg_small(ddmul(f, ddv{kLN2_H, kLN2_L}));  // 2^{-f}
+  int E = -(int)ny;
+  const ddv x = dv(xk);
+  ddv Lc = dv(1.0), Lm = dv(0.0);
+  for (int n = 0; n < g.L; ++n) {
+    double r = ddround(ddmul(Lc, ef));
+    double v = (E < -2200) ? 0.0 : ldexp(r, E);
+    put<CPLX>(F, (int64_t)n * ld + k, g.w ? g.w[n] * v : v);
+    // L_{n+1} = ((2n+1-x) L_n - n L_{n-1}) / (n+1)
+    ddv t = ddsub(ddmul(ddsub(dv(2.0 * n + 1.0), x), Lc), ddmuld(Lm, (double)n));
+    ddv Ln = dddiv(t, dv((double)(n + 1)));
+    Lm = Lc;
+    Lc = Ln;
+    double a = fabs(Lc.h);
+    if (a > 0x1p512) {
+      Lc = ddv{ldexp(Lc.h, -512), ldexp(Lc.l, -512)};
+      Lm = ddv{ldexp(Lm.h, -512), ldexp(Lm.l, -512)};
+      E += 512;
+    }
+  }
+}
+
+// cos(pi m t), m = p + m_off: exact product and exact reduction mod 2
+template <bool CPLX>
+__global__ void gen_cos(GenParams g, void* F, int64_t ld) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t tot = (int64_t)g.L * g.nc;
+  if (idx >= tot) return;
+  int p = (int)(idx / g.nc), k = (int)(idx - (int64_t)p * g.nc);
+  double m = (double)(p + g.m_off);
+  ddv r = tprod(m, g.nodes[k]);
+  double n2 = 2.0 * rint(0.5 * r.h);
+  r = ddsub(r, dv(n2));
+  double s, c;
+  sincospi(r.h, &s, &c);
+  double v = fma(-3.141592653589793 * r.l, s, c);
+  put<CPLX>(F, (int64_t)p * ld + k, g.w ? g.w[p] * v : v);
+}
+
+// ---- band detection: per node, max |S|^2 then the kept run -------------------------
+__global__ void band_detect_k(const double2* __restrict__ spec, int H, int nc, double eps1, int* start, int* len) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nc) return;
+  double mx = 0.0;
+  for (int q = 0; q < H; ++q) {
+    double2 v = spec[(int64_t)q * nc + k];
+    mx = fmax(mx, v.x * v.x + v.y * v.y);
+  }
+  double thr = (eps1 * eps1) * mx;
+  int first = -1, last = -1;
+  if (mx > 0.0) {
+    for (int q = 0; q < H; ++q) {
+      double2 v = spec[(int64_t)q * nc + k];
+      if (v.x * v.x + v.y * v.y >= thr) {
+        if (first < 0) first = q;
+        last = q;
+      }
+    }
+  }
+  start[k] = first < 0 ? 0 : first;
+  len[k] = first < 0 ? 0 : last - first + 1;
+}
+
+__global__ void band_store_k(const double2* __restrict__ spec, int H, int nc, double eps1, const int* start,
+                             const int* len, const int64_t* off, double2* vals) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nc) return;
+  double mx = 0.0;
+  for (int q = 0; q < H; ++q) {
+    double2 v = spec[(int64_t)q * nc + k];
+    mx = fmax(mx, v.x * v.x + v.y * v.y);
+  }
+  double thr = (eps1 * eps1) * mx;
+  int s = start[k], n = len[k];
+  int64_t o = off[k];
+  for (int i = 0; i < n; ++i) {
+    int q = s + i;
+    double2 v = spec[(int64_t)q * nc + k];
+    if (q == 0 || q == H - 1) v.y = 0.0;  // bins 0 and L/2 of a real row are real
+    vals[o + i] = (v.x * v.x + v.y * v.y >= thr) ? v : make_double2(0.0, 0.0);
+  }
+}
+
+}  // namespace
+
+xc_status gen_entries(const GenParams& g, double2* F, cudaStream_t st) {
+  if (g.kind == XC_COS) {
+    int64_t tot = (int64_t)g.L * g.nc;
+    gen_cos<true><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(g, F, g.nc);
+  } else if (g.kind == XC_JACOBI) {
+    gen_jacobi<true><<<(g.nc + 127) / 128, 128, 0, st>>>(g, F, g.nc);
+  } else {
+    gen_laguerre<true><<<(g.nc + 127) / 128, 128, 0, st>>>(g, F, g.nc);
+  }
+  XC_CUDA(cudaGetLastError());
+  return XC_OK;
+}
+
+xc_status gen_entries_real(const GenParams& g, double* E, int64_t ldE, cudaStream_t st) {
+  if (g.kind == XC_COS) {
+    int64_t tot = (int64_t)g.L * g.nc;
+    gen_cos<false><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(g, E, ldE);
+  } else if (g.kind == XC_JACOBI) {
+    gen_jacobi<false><<<(g.nc + 127) / 128, 128, 0, st>>>(g, E, ldE);
+  } else {
+    gen_laguerre<false><<<(g.nc + 127) / 128, 128, 0, st>>>(g, E, ldE);
+  }
+  XC_CUDA(cudaGetLastError());
+  return XC_OK;
+}
+
+xc_status band_detect(const double2* spec, int H, int nc, double eps1, int* start, int* len, cudaStream_t st) {
+  band_detect_k<<<(nc + 127) / 128, 128, 0, st>>>(spec, H, nc, eps1, start, len);
+  XC_CUDA(cudaGetLastError());
+  return XC_OK;
+}
+
+xc_status band_store(const double2* spec, int H, int nc, double eps1, const int* start, const int* len,
+                     const int64_t* off, double2* vals, cudaStream_t st) {
+  band_store_k<<<(nc + 127) / 128, 128, 0, st>>>(spec, H, nc, eps1, start, len, off, vals);
+  XC_CUDA(cudaGetLastError());
+  return XC_OK;
+}

@@ -1,0 +1,179 @@
+// spmm.cu -- multiplication by the compressed operator on the FP64 tensor cores.
+//
+// The hot step of the computation stage (u = Ä_e^T F, Alg. 2 step 2.1, P:218;
+// F = Ä_e z, Alg. 1 step 2.2; per block P:281).  "The degree of compression
+// ... determines to a great extent the efficiency of the computation step".
+//
+// The band-sparse operator is pre-tiled (build.cu) into items: an item is an
+// 8 x (4*nsteps) dense slice A of the operator (8 output rows = 4 complex bins
+// as re/im, or 8 real rows) against 4*nsteps consecutive rows of the operand Bm.
+// One warp computes D = A * Bm for 8*NT right-hand sides with DMMA
+// (mma.sync.m8n8k4.f64: 37 TF/s measured on B200 vs 34 TF/s for DFMA):
+//   A fragment  : lane holds A[lane/4][lane%4]     (one coalesced 256 B load/step)
+//   B fragment  : lane holds Bm[lane%4][col], col = lane/4 -> RHS tile + (lane/4)*NT + nt
+//   D fragment  : lane holds D[lane/4][2(lane%4)+i] -> RHS tile + (2(lane%4)+i)*NT + nt,
+//                 i.e. 2*NT contiguous doubles per lane on store.
+// Partial sums of items that split one output group are reduced in fixed order by
+// the consumer (FFT prologue / reduce_rows8), so results are deterministic.
+#include <algorithm>
+
+#include "xc_internal.cuh"
+
+namespace {
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+constexpr int WPC = 4;  // warps (items) per CTA
+
+template <int NT>
+__global__ void __launch_bounds__(WPC * 32) spmm_dmma(const SpmmItem* __restrict__ items, int nitems,
+                                                       const double* __restrict__ tiles, SpmmSrcs srcs,
+                                                       double* __restrict__ part, int64_t ldp, int ncols) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int it_idx = blockIdx.y * WPC + warp;
+  if (it_idx >= nitems) return;
+  const SpmmItem it = items[it_idx];
+  const int t = lane & 3, g = lane >> 2;
+  const int tile0 = blockIdx.x * (8 * NT);
+  const int bcol = tile0 + g * NT;  // this lane's B-fragment columns [bcol, bcol+NT)
+
+  const double* re = srcs.re[it.src];
+  const double* im = srcs.im[it.src];
+  const int nrows = srcs.nrows[it.src];
+  const int64_t ld = srcs.ld[it.src];
+  const bool planes = (im != nullptr);
+  const bool full = (tile0 + 8 * NT <= ncols);
+
+  double acc[NT][2];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) acc[i][0] = acc[i][1] = 0.0;
+
+  const double* a_ptr = tiles + it.a_off + lane;
+  double a_cur = (it.nsteps > 0) ? __ldg(a_ptr) : 0.0;
+  double b_cur[NT];
+
+  auto load_b = [&](int s, double* bv) {
+    int r = 4 * s + t;
+    int row = planes ? it.k0 + (r >> 1) : it.k0 + r;
+    const double* src = (planes && (r & 1)) ? im : re;
+    if (row < nrows) {
+      const double* p = src + (int64_t)row * ld + bcol;
+      if (full) {
+        if ((NT % 2 == 0) && ((ld & 1) == 0) && ((((uintptr_t)p) & 15) == 0)) {
+#pragma unroll
+          for (int i = 0; i < NT; i += 2) {
+            double2 v = __ldg(reinterpret_cast<const double2*>(p + i));
+            bv[i] = v.x;
+            bv[i + 1] = v.y;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < NT; ++i) bv[i] = __ldg(p + i);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < NT; ++i) bv[i] = (bcol + i < ncols) ? __ldg(p + i) : 0.0;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < NT; ++i) bv[i] = 0.0;
+    }
+  };
+
+  if (it.nsteps > 0) load_b(0, b_cur);
+  for (int s = 0; s < it.nsteps; ++s) {
+    double a_nxt = 0.0;
+    double b_nxt[NT];
+    const bool more = (s + 1 < it.nsteps);
+    if (more) {
+      a_nxt = __ldg(a_ptr + 32 * (s + 1));
+      load_b(s + 1, b_nxt);
+    }
+#pragma unroll
+    for (int i = 0; i < NT; ++i) dmma(acc[i][0], acc[i][1], a_cur, b_cur[i]);
+    if (more) {
+      a_cur = a_nxt;
+#pragma unroll
+      for (int i = 0; i < NT; ++i) b_cur[i] = b_nxt[i];
+    }
+  }
+
+  // D[g][2t+i] -> RHS tile0 + (2t+i)*NT + nt: lane writes 2*NT contiguous doubles
+  double* out = part + (it.out_row + g) * ldp + tile0 + 2 * t * NT;
+  const int cstart = tile0 + 2 * t * NT;
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    if (cstart + i < ldp) out[i] = acc[i][0];
+    if (cstart + NT + i < ldp) out[NT + i] = acc[i][1];
+  }
+}
+
+template <int NT>
+xc_status launch(const SpmmItem* items, int nitems, const double* tiles, const SpmmSrcs& srcs, double* part,
+                 int64_t ldp, int ncols, cudaStream_t st) {
+  dim3 grid((ncols + 8 * NT - 1) / (8 * NT), (nitems + WPC - 1) / WPC);
+  if (grid.y > 65535) {
+    // fold very long item lists into several launches
+    int per = 65535 * WPC;
+    for (int i0 = 0; i0 < nitems; i0 += per) {
+      int n = std::min(per, nitems - i0);
+      XC_TRY(launch<NT>(items + i0, n, tiles, srcs, part, ldp, ncols, st));
+    }
+    return XC_OK;
+  }
+  spmm_dmma<NT><<<grid, WPC * 32, 0, st>>>(items, nitems, tiles, srcs, part, ldp, ncols);
+  XC_CUDA(cudaGetLastError());
+  return XC_OK;
+}
+
+__global__ void reduce_rows8_kernel(const double* __restrict__ part, int64_t ldp, const int64_t* __restrict__ base,
+                                    const int* __restrict__ nch, int nrows, const double* __restrict__ rowscale,
+                                    double* __restrict__ Y, int64_t ldy, int ncols) {
+  for (int row = blockIdx.y; row < nrows; row += gridDim.y) {
+    int g = row >> 3;
+    int n = nch[g];
+    int64_t r0 = base[g] + (row & 7);
+    double sc = rowscale ? rowscale[row] : 1.0;
+    for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < ncols; col += gridDim.x * blockDim.x) {
+      double s = 0.0;
+      for (int c = 0; c < n; ++c) s += part[(r0 + 8 * c) * ldp + col];
+      Y[(int64_t)row * ldy + col] = s * sc;
+    }
+  }
+}
+
+}  // namespace
+
+int spmm_nt_for(int64_t B) {
+  if (B >= 128) return 16;
+  if (B >= 64) return 8;
+  if (B >= 32) return 4;
+  if (B >= 16) return 2;
+  return 1;
+}
+
+xc_status spmm_run(const SpmmItem* items, int nitems, const double* tiles, const SpmmSrcs& srcs, double* part,
+                   int64_t ldp, int ncols, cudaStream_t st) {
+  if (nitems <= 0) return XC_OK;
+  switch (spmm_nt_for(ncols)) {
+    case 16: return launch<16>(items, nitems, tiles, srcs, part, ldp, ncols, st);
+    case 8: return launch<8>(items, nitems, tiles, srcs, part, ldp, ncols, st);
+    case 4: return launch<4>(items, nitems, tiles, srcs, part, ldp, ncols, st);
+    case 2: return launch<2>(items, nitems, tiles, srcs, part, ldp, ncols, st);
+    default: return launch<1>(items, nitems, tiles, srcs, part, ldp, ncols, st);
+  }
+}
+
+xc_status reduce_rows8(const double* part, int64_t ldp, const int64_t* base, const int* nch, int nrows,
+                       const double* rowscale, double* Y, int64_t ldy, int ncols, cudaStream_t st) {
+  if (nrows <= 0) return XC_OK;
+  int th = ncols >= 256 ? 256 : (ncols >= 64 ? 64 : 32);
+  dim3 grid(std::min((ncols + th - 1) / th, 64), std::min(nrows, 65535));
+  reduce_rows8_kernel<<<grid, th, 0, st>>>(part, ldp, base, nch, nrows, rowscale, Y, ldy, ncols);
+  XC_CUDA(cudaGetLastError());
+  return XC_OK;
+}

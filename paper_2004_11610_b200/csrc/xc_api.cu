@@ -1,0 +1,861 @@
+// xc_api.cu -- the C ABI (include/xc.h): build orchestration and apply.
+//
+// Precomputation (xc_build_compressed; Alg. 1/2 step 1):
+//   host plan (zeta, s_i, L_i, tail)  ->  per block, per node chunk on the GPU:
+//   entries (double-double) x window -> forward FFT (Eq. 1) -> per-node threshold ->
+//   node bands  ->  tensor-core tiles for the output axis (bin groups x nodes) and,
+//   if requested, the input axis (node groups x bins).
+// Computation (xc_apply):
+//   XC_DIR_A  : SpMM (all blocks + dense tail, one launch) -> per block inverse FFT
+//               with the partial-sum reduction fused in its prologue and the
+//               W^{-1}/truncation fused in its epilogue (Alg. 2 step 2);
+//               tail rows reduced directly.
+//   XC_DIR_WAT: per block inverse FFT of pad(X)/w (Alg. 1 step 2.2 / Fe1, Fe3) ->
+//               SpMM over all blocks + tail -> reduction times the weights.
+#include <math.h>
+#include <cmath>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "build.h"
+#include "plan.h"
+#include "xc_internal.cuh"
+
+static thread_local std::string g_err;
+void xc_set_error(const std::string& msg) { g_err = msg; }
+
+xc_status dev_alloc(DevBuf& b, size_t bytes) {
+  dev_free(b);
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(&b.p, bytes);
+  if (e != cudaSuccess) {
+    b.p = nullptr;
+    cudaGetLastError();
+    xc_set_error("cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    return XC_ENOMEM;
+  }
+  b.bytes = bytes;
+  return XC_OK;
+}
+void dev_free(DevBuf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+}
+
+namespace {
+
+constexpr int KC = 256;  // node chunk of an output-axis item (multiple of 4)
+constexpr int QC = 256;  // bin chunk of an input-axis item (multiple of 2)
+
+struct BlockData {
+  int L = 0, H = 0, m_off = 0, keep_lo = 0, keep_hi = 0;
+  FftPlan fft;
+  std::vector<double> h_w;
+  DevBuf w, yscale, winv;
+  std::vector<int> h_start, h_len;
+  std::vector<int64_t> h_off;
+  DevBuf start, len, off, vals;
+  int64_t nnz = 0;
+  int max_band = 0;
+  int ngroups = 0;
+  DevBuf grp_base, grp_nch;  // output axis groups
+};
+
+template <typename T>
+xc_status upload(DevBuf& b, const std::vector<T>& v) {
+  XC_TRY(dev_alloc(b, v.size() * sizeof(T)));
+  if (!v.empty()) XC_CUDA(cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return XC_OK;
+}
+
+}  // namespace
+
+struct xc_op {
+  int kind = 0;
+  double alpha = 0, beta = 0;
+  int64_t N = 0;
+  double eps1 = 0, eps2 = 0, zeta = 0;
+  int tail = 0, dirs = 0, device = 0;
+  std::vector<BlockData> blocks;
+  DevBuf nodes, wt, tailP;
+  // output axis
+  DevBuf itemsA, tilesA;
+  int nitemsA = 0;
+  int64_t rowsA = 0, tilesA_n = 0;
+  int ntailg = 0;
+  DevBuf tail_base, tail_nch;
+  // input axis
+  DevBuf itemsW, tilesW;
+  int nitemsW = 0;
+  int64_t rowsW = 0, tilesW_n = 0;
+  DevBuf nodeg_base, nodeg_nch;
+  // workspace
+  int64_t ws_B = 0;
+  DevBuf partA, partW, scratch, zpl, Xh, Yh;
+  std::vector<int64_t> zoff;  // per block offset (doubles) of its z' planes in zpl
+  xc_info_t info{};
+};
+
+namespace {
+
+int64_t pad_cols(int64_t B) {
+  int64_t t = 8 * spmm_nt_for(B);
+  return (B + t - 1) / t * t;
+}
+
+xc_status ensure_ws(xc_op* h, int64_t B) {
+  if (B <= h->ws_B) return XC_OK;
+  int64_t Bp = pad_cols(B);
+  size_t scratch_n = 0;
+  for (auto& b : h->blocks)
+    if (b.fft.L2 > 1) scratch_n = std::max(scratch_n, (size_t)b.L * (size_t)B);
+  XC_TRY(dev_alloc(h->scratch, std::max<size_t>(1, scratch_n) * sizeof(double2)));
+  if (h->dirs & XC_DIR_A) XC_TRY(dev_alloc(h->partA, (size_t)h->rowsA * Bp * sizeof(double)));
+  if (h->dirs & XC_DIR_WAT) {
+    XC_TRY(dev_alloc(h->partW, (size_t)h->rowsW * Bp * sizeof(double)));
+    h->zoff.clear();
+    int64_t tot = 0;
+    for (auto& b : h->blocks) {
+      h->zoff.push_back(tot);
+      tot += 2 * (int64_t)b.H * Bp;
+    }
+    XC_TRY(dev_alloc(h->zpl, (size_t)tot * sizeof(double)));
+  }
+  h->ws_B = B;
+  return XC_OK;
+}
+
+xc_status validate_nodes(int kind, const double* x, int64_t N) {
+  for (int64_t k = 0; k < N; ++k) {
+    if (!std::isfinite(x[k])) {
+      xc_set_error("nodes: non-finite value at " + std::to_string(k));
+      return XC_EINVAL;
+    }
+    if (k > 0 && !(x[k] > x[k - 1])) {
+      xc_set_error("nodes: not strictly ascending at " + std::to_string(k));
+      return XC_EINVAL;
+    }
+  }
+  bool ok = true;
+  if (kind == XC_COS) ok = x[0] >= 0.0 && x[N - 1] <= 1.0;
+  if (kind == XC_JACOBI) ok = x[0] >= -1.0 && x[N - 1] <= 1.0;
+  if (kind == XC_LAGUERRE) ok = x[0] >= 0.0;
+  if (!ok) {
+    xc_set_error("nodes: outside the domain of the kind");
+    return XC_EINVAL;
+  }
+  return XC_OK;
+}
+
+// --- the per-block precompute: entries -> FFT -> threshold -> node bands ------------
+xc_status build_block(xc_op* h, BlockData& b, const std::vector<double2>& jtab, const DevBuf& djtab, ddv p0,
+                      int node_chunk, cudaStream_t st) {
+  const int N = (int)h->N;
+  b.H = b.L / 2 + 1;
+  XC_TRY(fft_plan_make(b.fft, b.L));
+  kaiser_window(h->zeta, b.L, b.h_w);
+  std::vector<double> ys(b.L), wi(b.L);
+  const double isL = 1.0 / sqrt((double)b.L);
+  for (int p = 0; p < b.L; ++p) {
+    ys[p] = isL / b.h_w[p];
+    wi[p] = 1.0 / b.h_w[p];
+  }
+  XC_TRY(upload(b.w, b.h_w));
+  XC_TRY(upload(b.yscale, ys));
+  XC_TRY(upload(b.winv, wi));
+
+  // chunk the nodes so that F and the FFT scratch stay within ~3 GB
+  int nc = node_chunk > 0 ? node_chunk : (int)std::max<int64_t>(64, (3LL << 30) / ((int64_t)b.L * 48));
+  nc = std::min(nc, N);
+  DevBuf F, scr, spec, st_len, d_start, d_len;
+  XC_TRY(dev_alloc(F, (size_t)b.L * nc * sizeof(double2)));
+  if (b.fft.L2 > 1) XC_TRY(dev_alloc(scr, (size_t)b.L * nc * sizeof(double2)));
+  XC_TRY(dev_alloc(spec, (size_t)b.H * nc * sizeof(double2)));
+  XC_TRY(dev_alloc(b.start, (size_t)N * sizeof(int)));
+  XC_TRY(dev_alloc(b.len, (size_t)N * sizeof(int)));
+  b.h_start.assign(N, 0);
+  b.h_len.assign(N, 0);
+  b.h_off.assign(N + 1, 0);
+  std::vector<DevBuf> chunk_vals;
+  std::vector<int64_t> chunk_base;
+  DevBuf choff;
+
+  for (int k0 = 0; k0 < N; k0 += nc) {
+    int n = std::min(nc, N - k0);
+    GenParams g{};
+    g.kind = h->kind;
+    g.L = b.L;
+    g.m_off = b.m_off;
+    g.nodes = (const double*)h->nodes.p + k0;
+    g.nc = n;
+    g.w = (const double*)b.w.p;
+    g.jab = (const double2*)djtab.p;
+    g.p0 = p0;
+    XC_TRY(gen_entries(g, (double2*)F.p, st));
+    FftIO io{};
+    io.src = (const double2*)F.p;
+    io.lds = n;
+    io.dst = (double2*)spec.p;
+    io.ldd = n;
+    io.kmax = b.H;
+    io.scale = 1.0 / sqrt((double)b.L);  // unitary DFT of Eq. (1)
+    XC_TRY(fft_run(b.fft, -1, PRO_PLAIN, EPI_PLAIN, io, n, (double2*)scr.p, st));
+    int* ds = (int*)b.start.p + k0;
+    int* dl = (int*)b.len.p + k0;
+    XC_TRY(band_detect((const double2*)spec.p, b.H, n, h->eps1, ds, dl, st));
+    XC_CUDA(cudaMemcpyAsync(b.h_start.data() + k0, ds, n * sizeof(int), cudaMemcpyDeviceToHost, st));
+    XC_CUDA(cudaMemcpyAsync(b.h_len.data() + k0, dl, n * sizeof(int), cudaMemcpyDeviceToHost, st));
+    XC_CUDA(cudaStreamSynchronize(st));
+    std::vector<int64_t> loc(n);
+    int64_t tot = 0;
+    for (int i = 0; i < n; ++i) {
+      loc[i] = tot;
+      b.h_off[k0 + i] = b.h_off[k0] + tot;  // fixed below (global prefix)
+      tot += b.h_len[k0 + i];
+    }
+    DevBuf cv;
+    XC_TRY(dev_alloc(cv, (size_t)std::max<int64_t>(1, tot) * sizeof(double2)));
+    XC_TRY(upload(choff, loc));
+    XC_TRY(band_store((const double2*)spec.p, b.H, n, h->eps1, ds, dl, (const int64_t*)choff.p,
+                      (double2*)cv.p, st));
+    XC_CUDA(cudaStreamSynchronize(st));
+    chunk_vals.push_back(cv);
+    chunk_base.push_back(tot);
+  }
+  // global offsets and one contiguous value array
+  int64_t acc = 0;
+  b.max_band = 0;
+  for (int k = 0; k < N; ++k) {
+    b.h_off[k] = acc;
+    acc += b.h_len[k];
+    b.max_band = std::max(b.max_band, b.h_len[k]);
+  }
+  b.h_off[N] = acc;
+  XC_TRY(dev_alloc(b.vals, (size_t)std::max<int64_t>(1, acc) * sizeof(double2)));
+  int64_t pos = 0;
+  for (size_t c = 0; c < chunk_vals.size(); ++c) {
+    if (chunk_base[c] > 0)
+      XC_CUDA(cudaMemcpyAsync((double2*)b.vals.p + pos, chunk_vals[c].p, chunk_base[c] * sizeof(double2),
+                              cudaMemcpyDeviceToDevice, st));
+    pos += chunk_base[c];
+  }
+  XC_CUDA(cudaStreamSynchronize(st));
+  for (auto& cv : chunk_vals) dev_free(cv);
+  dev_free(choff);
+  XC_TRY(upload(b.off, b.h_off));
+  // kept nonzeros (the stored runs contain explicit zeros for dropped interior bins)
+  b.nnz = acc;
+  dev_free(F);
+  dev_free(scr);
+  dev_free(spec);
+  return XC_OK;
+}
+
+// --- output-axis items and tiles ---------------------------------------------------------
+xc_status build_output_axis(xc_op* h, cudaStream_t st) {
+  const int N = (int)h->N;
+  const int N4 = (N + 3) / 4 * 4;
+  std::vector<SpmmItem> items;
+  std::vector<FillItem> fills;
+  std::vector<int> fill_blk;  // block index, -1 = tail
+  int64_t rows = 0, aoff = 0;
+  for (size_t bi = 0; bi < h->blocks.size(); ++bi) {
+    BlockData& b = h->blocks[bi];
+    b.ngroups = (b.H + 3) / 4;
+    std::vector<int> klo(b.ngroups, N), khi(b.ngroups, 0);
+    for (int k = 0; k < N; ++k) {
+      if (b.h_len[k] == 0) continue;
+      int g0 = b.h_start[k] / 4, g1 = (b.h_start[k] + b.h_len[k] - 1) / 4;
+      for (int g = g0; g <= g1; ++g) {
+        klo[g] = std::min(klo[g], k);
+        khi[g] = std::max(khi[g], k + 1);
+      }
+    }
+    std::vector<int64_t> gbase(b.ngroups, 0);
+    std::vector<int> gnch(b.ngroups, 0);
+    std::vector<SpmmItem> bitems;
+    std::vector<FillItem> bfills;
+    for (int g = 0; g < b.ngroups; ++g) {
+      gbase[g] = rows;
+      if (klo[g] >= khi[g]) continue;
+      int a = klo[g] / 4 * 4, e = (khi[g] + 3) / 4 * 4;
+      for (int c = a / KC; c * KC < e; ++c) {
+        int k0 = std::max(a, c * KC), k1 = std::min(e, (c + 1) * KC);
+        if (k1 <= k0) continue;
+        SpmmItem it{};
+        it.a_off = aoff;
+        it.out_row = rows;
+        it.k0 = k0;
+        it.nsteps = (k1 - k0) / 4;
+        it.src = 0;
+        bitems.push_back(it);
+        bfills.push_back(FillItem{aoff, k0, it.nsteps, g, 0});
+        aoff += 32LL * it.nsteps;
+        rows += 8;
+        gnch[g]++;
+      }
+    }
+    XC_TRY(upload(b.grp_base, gbase));
+    XC_TRY(upload(b.grp_nch, gnch));
+    for (size_t i = 0; i < bitems.size(); ++i) {
+      items.push_back(bitems[i]);
+      fills.push_back(bfills[i]);
+      fill_blk.push_back((int)bi);
+    }
+  }
+  // dense tail: groups of 8 degrees x node chunks
+  h->ntailg = (h->tail + 7) / 8;
+  std::vector<int64_t> tbase(std::max(1, h->ntailg), 0);
+  std::vector<int> tnch(std::max(1, h->ntailg), 0);
+  for (int g = 0; g < h->ntailg; ++g) {
+    tbase[g] = rows;
+    for (int k0 = 0; k0 < N4; k0 += KC) {
+      int k1 = std::min(N4, k0 + KC);
+      SpmmItem it{};
+      it.a_off = aoff;
+      it.out_row = rows;
+      it.k0 = k0;
+      it.nsteps = (k1 - k0) / 4;
+      it.src = 0;
+      items.push_back(it);
+      fills.push_back(FillItem{aoff, k0, it.nsteps, g, 0});
+      fill_blk.push_back(-1);
+      aoff += 32LL * it.nsteps;
+      rows += 8;
+      tnch[g]++;
+    }
+  }
+  XC_TRY(upload(h->tail_base, tbase));
+  XC_TRY(upload(h->tail_nch, tnch));
+  h->rowsA = rows;
+  h->tilesA_n = aoff;
+  XC_TRY(dev_alloc(h->tilesA, (size_t)std::max<int64_t>(1, aoff) * sizeof(double)));
+  // fill per block
+  DevBuf dfill;
+  size_t i0 = 0;
+  while (i0 < fills.size()) {
+    size_t i1 = i0;
+    while (i1 < fills.size() && fill_blk[i1] == fill_blk[i0]) ++i1;
+    std::vector<FillItem> part(fills.begin() + i0, fills.begin() + i1);
+    XC_TRY(upload(dfill, part));
+    int bi = fill_blk[i0];
+    if (bi >= 0) {
+      BlockData& b = h->blocks[bi];
+      XC_TRY(fill_tiles(FILL_OUT_CPLX, (FillItem*)dfill.p, (int)part.size(), (int*)b.start.p, (int*)b.len.p,
+                        (int64_t*)b.off.p, (double2*)b.vals.p, nullptr, 0, N, b.H, (double*)h->tilesA.p, st));
+    } else {
+      XC_TRY(fill_tiles(FILL_OUT_REAL, (FillItem*)dfill.p, (int)part.size(), nullptr, nullptr, nullptr, nullptr,
+                        (double*)h->tailP.p, h->tail, N, 0, (double*)h->tilesA.p, st));
+    }
+    XC_CUDA(cudaStreamSynchronize(st));
+    i0 = i1;
+  }
+  dev_free(dfill);
+  // execution order: by (block, node chunk, group) so that a CTA's warps share X rows
+  std::vector<size_t> ord(items.size());
+  for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
+  std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+    if (fill_blk[a] != fill_blk[b]) return (unsigned)fill_blk[a] < (unsigned)fill_blk[b];
+    return items[a].k0 / KC < items[b].k0 / KC;
+  });
+  std::vector<SpmmItem> sorted(items.size());
+  for (size_t i = 0; i < ord.size(); ++i) sorted[i] = items[ord[i]];
+  XC_TRY(upload(h->itemsA, sorted));
+  h->nitemsA = (int)sorted.size();
+  return XC_OK;
+}
+
+// --- input-axis items and tiles ----------------------------------------------------------
+xc_status build_input_axis(xc_op* h, cudaStream_t st) {
+  const int N = (int)h->N;
+  const int NG = (N + 7) / 8;
+  const int nb = (int)h->blocks.size();
+  struct Tmp {
+    SpmmItem it;
+    FillItem f;
+    int blk;
+  };
+  std::vector<std::vector<Tmp>> per_group(NG);
+  for (int bi = 0; bi < nb; ++bi) {
+    BlockData& b = h->blocks[bi];
+    for (int G = 0; G < NG; ++G) {
+      int qlo = b.H, qhi = 0;
+      for (int k = 8 * G; k < std::min(N, 8 * G + 8); ++k) {
+        if (b.h_len[k] == 0) continue;
+        qlo = std::min(qlo, b.h_start[k]);
+        qhi = std::max(qhi, b.h_start[k] + b.h_len[k]);
+      }
+      if (qlo >= qhi) continue;
+      int a = qlo / 2 * 2, e = (qhi + 1) / 2 * 2;
+      for (int c = a / QC; c * QC < e; ++c) {
+        int q0 = std::max(a, c * QC), q1 = std::min(e, (c + 1) * QC);
+        if (q1 <= q0) continue;
+        Tmp t{};
+        t.it.k0 = q0;
+        t.it.nsteps = (q1 - q0) / 2;
+        t.it.src = bi;
+        t.f = FillItem{0, q0, t.it.nsteps, G, 0};
+        t.blk = bi;
+        per_group[G].push_back(t);
+      }
+    }
+  }
+  if (h->tail > 0) {
+    int t4 = (h->tail + 3) / 4 * 4;
+    for (int G = 0; G < NG; ++G) {
+      Tmp t{};
+      t.it.k0 = 0;
+      t.it.nsteps = t4 / 4;
+      t.it.src = nb;
+      t.f = FillItem{0, 0, t.it.nsteps, G, 0};
+      t.blk = -1;
+      per_group[G].push_back(t);
+    }
+  }
+  std::vector<int64_t> gbase(NG);
+  std::vector<int> gnch(NG);
+  std::vector<SpmmItem> items;
+  std::vector<FillItem> fills;
+  std::vector<int> fblk;
+  int64_t rows = 0, aoff = 0;
+  for (int G = 0; G < NG; ++G) {
+    gbase[G] = rows;
+    gnch[G] = (int)per_group[G].size();
+    for (auto& t : per_group[G]) {
+      t.it.a_off = aoff;
+      t.f.a_off = aoff;
+      t.it.out_row = rows;
+      aoff += 32LL * t.it.nsteps;
+      rows += 8;
+      items.push_back(t.it);
+      fills.push_back(t.f);
+      fblk.push_back(t.blk);
+    }
+  }
+  XC_TRY(upload(h->nodeg_base, gbase));
+  XC_TRY(upload(h->nodeg_nch, gnch));
+  h->rowsW = rows;
+  h->tilesW_n = aoff;
+  XC_TRY(dev_alloc(h->tilesW, (size_t)std::max<int64_t>(1, aoff) * sizeof(double)));
+  // fill, grouped by block
+  DevBuf dfill;
+  for (int bi = -1; bi < nb; ++bi) {
+    std::vector<FillItem> part;
+    for (size_t i = 0; i < fills.size(); ++i)
+      if (fblk[i] == bi) part.push_back(fills[i]);
+    if (part.empty()) continue;
+    XC_TRY(upload(dfill, part));
+    if (bi >= 0) {
+      BlockData& b = h->blocks[bi];
+      XC_TRY(fill_tiles(FILL_IN_CPLX, (FillItem*)dfill.p, (int)part.size(), (int*)b.start.p, (int*)b.len.p,
+                        (int64_t*)b.off.p, (double2*)b.vals.p, nullptr, 0, N, b.H, (double*)h->tilesW.p, st));
+    } else {
+      XC_TRY(fill_tiles(FILL_IN_REAL, (FillItem*)dfill.p, (int)part.size(), nullptr, nullptr, nullptr, nullptr,
+                        (double*)h->tailP.p, h->tail, N, 0, (double*)h->tilesW.p, st));
+    }
+    XC_CUDA(cudaStreamSynchronize(st));
+  }
+  dev_free(dfill);
+  // execution order: by (block, bin chunk, node group)
+  std::vector<size_t> ord(items.size());
+  for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
+  std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+    if (items[a].src != items[b].src) return items[a].src < items[b].src;
+    return items[a].k0 / QC < items[b].k0 / QC;
+  });
+  std::vector<SpmmItem> sorted(items.size());
+  for (size_t i = 0; i < ord.size(); ++i) sorted[i] = items[ord[i]];
+  XC_TRY(upload(h->itemsW, sorted));
+  h->nitemsW = (int)sorted.size();
+  return XC_OK;
+}
+
+double fft_flops(int L) { return 2.5 * L * log2((double)L); }  // real FFT = half of 5 L log2 L
+
+xc_status build_impl(xc_kind kind, const xc_params* prm, const double* nodes, int64_t N, double eps, xc_op* h) {
+  xc_params p;
+  xc_params_default(&p);
+  if (prm) p = *prm;
+  if (kind != XC_COS && kind != XC_JACOBI && kind != XC_LAGUERRE) {
+    xc_set_error("unknown kind");
+    return XC_EINVAL;
+  }
+  if (N < 2 || N > (1 << 24) || !nodes) {
+    xc_set_error("N must be in [2, 2^24] and nodes non-null");
+    return XC_EINVAL;
+  }
+  if (!(eps > 0.0 && eps < 1.0)) {
+    xc_set_error("eps must be in (0,1)");
+    return XC_EINVAL;
+  }
+  h->kind = kind;
+  h->alpha = p.alpha;
+  h->beta = p.beta;
+  h->N = N;
+  h->eps1 = p.eps1 > 0 ? p.eps1 : eps;
+  h->eps2 = p.eps2 > 0 ? p.eps2 : 1e-2;
+  h->dirs = p.dirs ? p.dirs : XC_DIR_A;
+  h->device = p.device;
+  if (!(h->eps1 < h->eps2) || !(h->eps2 < 1.0)) {
+    xc_set_error("need eps1 < eps2 < 1");
+    return XC_EINVAL;
+  }
+  if (kind == XC_JACOBI && !(p.alpha > -1.0 && p.beta > -1.0)) {
+    xc_set_error("Jacobi alpha, beta must be > -1");
+    return XC_EINVAL;
+  }
+  if ((h->dirs & XC_DIR_WAT) && !p.weights) {
+    xc_set_error("XC_DIR_WAT needs weights");
+    return XC_EINVAL;
+  }
+  XC_TRY(validate_nodes(kind, nodes, N));
+  XC_CUDA(cudaSetDevice(p.device));
+  cudaStream_t st = (cudaStream_t)p.stream;
+
+  PlanOut plan;
+  XC_TRY(make_chain(kind, N, h->eps1, h->eps2, p.dense_cutoff > 0 ? p.dense_cutoff : 32, plan));
+  h->zeta = plan.zeta;
+  h->tail = plan.tail;
+  h->blocks.resize(plan.blocks.size());
+  int Lmax = 0;
+  for (size_t i = 0; i < plan.blocks.size(); ++i) {
+    h->blocks[i].L = plan.blocks[i].L;
+    h->blocks[i].m_off = plan.blocks[i].m_off;
+    h->blocks[i].keep_lo = plan.blocks[i].keep_lo;
+    h->blocks[i].keep_hi = plan.blocks[i].keep_hi;
+    Lmax = std::max(Lmax, plan.blocks[i].L);
+  }
+  XC_TRY(upload(h->nodes, std::vector<double>(nodes, nodes + N)));
+  if (h->dirs & XC_DIR_WAT) XC_TRY(upload(h->wt, std::vector<double>(p.weights, p.weights + N)));
+
+  std::vector<double2> jtab;
+  ddv p0 = dv(1.0);
+  DevBuf djtab;
+  if (kind == XC_JACOBI) {
+    jacobi_coeffs(p.alpha, p.beta, std::max(Lmax, h->tail) + 2, jtab, p0);
+    XC_TRY(upload(djtab, jtab));
+  }
+  for (auto& b : h->blocks) XC_TRY(build_block(h, b, jtab, djtab, p0, p.node_chunk, st));
+  // dense tail entries P[j][k] = phi_j(x_k), j < t
+  if (h->tail > 0) {
+    XC_TRY(dev_alloc(h->tailP, (size_t)h->tail * N * sizeof(double)));
+    GenParams g{};
+    g.kind = kind;
+    g.L = h->tail;
+    g.m_off = 0;
+    g.nodes = (const double*)h->nodes.p;
+    g.nc = (int)N;
+    g.w = nullptr;
+    g.jab = (const double2*)djtab.p;
+    g.p0 = p0;
+    XC_TRY(gen_entries_real(g, (double*)h->tailP.p, N, st));
+    XC_CUDA(cudaStreamSynchronize(st));
+  }
+  if (h->dirs & XC_DIR_A) XC_TRY(build_output_axis(h, st));
+  if (h->dirs & XC_DIR_WAT) XC_TRY(build_input_axis(h, st));
+  dev_free(djtab);
+  XC_CUDA(cudaStreamSynchronize(st));
+
+  // info
+  xc_info_t& in = h->info;
+  in.N = N;
+  in.kind = kind;
+  in.zeta = h->zeta;
+  in.eps1 = h->eps1;
+  in.eps2 = h->eps2;
+  in.n_blocks = (int)h->blocks.size();
+  in.tail = h->tail;
+  in.dirs = h->dirs;
+  int64_t nnz = 0;
+  double fft = 0;
+  for (auto& b : h->blocks) {
+    nnz += b.nnz;
+    fft += fft_flops(b.L);
+  }
+  in.nnz = nnz;
+  in.flops_per_col_A = 4.0 * nnz + 2.0 * h->tail * N + fft;
+  in.flops_per_col_WAT = in.flops_per_col_A;
+  in.dmma_flops_per_col_A = 64.0 * (h->tilesA_n / 32);
+  in.dmma_flops_per_col_WAT = 64.0 * (h->tilesW_n / 32);
+  in.op_bytes_A = h->tilesA_n * 8 + (int64_t)h->nitemsA * sizeof(SpmmItem);
+  in.op_bytes_WAT = h->tilesW_n * 8 + (int64_t)h->nitemsW * sizeof(SpmmItem);
+  return XC_OK;
+}
+
+xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t B,
+                     cudaStream_t st) {
+  if (B < 1 || ldx < B || ldy < B || !X || !Y) {
+    xc_set_error("apply: need B >= 1, ldx >= B, ldy >= B, non-null X and Y");
+    return XC_EINVAL;
+  }
+  if (B > (1 << 24)) {
+    xc_set_error("apply: B too large");
+    return XC_EINVAL;
+  }
+  if (!(h->dirs & dir)) {
+    xc_set_error("apply: direction was not built");
+    return XC_ESTATE;
+  }
+  XC_TRY(ensure_ws(h, B));
+  const int64_t Bp = pad_cols(B);
+  const int N = (int)h->N;
+  if (dir == XC_DIR_A) {
+    SpmmSrcs s{};
+    s.re[0] = X;
+    s.im[0] = nullptr;
+    s.nrows[0] = N;
+    s.ld[0] = ldx;
+    XC_TRY(spmm_run((const SpmmItem*)h->itemsA.p, h->nitemsA, (const double*)h->tilesA.p, s,
+                    (double*)h->partA.p, Bp, (int)B, st));
+    for (auto& b : h->blocks) {
+      FftIO io{};
+      io.part = (const double*)h->partA.p;
+      io.ldp = Bp;
+      io.grp_base = (const int64_t*)b.grp_base.p;
+      io.grp_nch = (const int*)b.grp_nch.p;
+      io.H = b.H;
+      io.Y = Y;
+      io.ldy = ldy;
+      io.yscale = (const double*)b.yscale.p;
+      io.keep_lo = b.keep_lo;
+      io.keep_hi = b.keep_hi;
+      io.m_off = b.m_off;
+      XC_TRY(fft_run(b.fft, +1, PRO_UPART, EPI_YREAL, io, (int)B, (double2*)h->scratch.p, st));
+    }
+    if (h->tail > 0)
+      XC_TRY(reduce_rows8((const double*)h->partA.p, Bp, (const int64_t*)h->tail_base.p, (const int*)h->tail_nch.p,
+                          h->tail, nullptr, Y, ldy, (int)B, st));
+    return XC_OK;
+  }
+  // XC_DIR_WAT
+  SpmmSrcs s{};
+  const int nb = (int)h->blocks.size();
+  for (int i = 0; i < nb; ++i) {
+    BlockData& b = h->blocks[i];
+    double* zre = (double*)h->zpl.p + h->zoff[i];
+    double* zim = zre + (int64_t)b.H * Bp;
+    FftIO io{};
+    io.X = X;
+    io.ldx = ldx;
+    io.winv = (const double*)b.winv.p;
+    io.keep_lo = b.keep_lo;
+    io.keep_hi = b.keep_hi;
+    io.m_off = b.m_off;
+    io.zre = zre;
+    io.zim = zim;
+    io.ldz = Bp;
+    io.H = b.H;
+    io.scale = 1.0 / sqrt((double)b.L);
+    XC_TRY(fft_run(b.fft, +1, PRO_XREAL, EPI_ZPLANES, io, (int)B, (double2*)h->scratch.p, st));
+    s.re[i] = zre;
+    s.im[i] = zim;
+    s.nrows[i] = b.H;
+    s.ld[i] = Bp;
+  }
+  s.re[nb] = X;
+  s.im[nb] = nullptr;
+  s.nrows[nb] = h->tail;
+  s.ld[nb] = ldx;
+  XC_TRY(spmm_run((const SpmmItem*)h->itemsW.p, h->nitemsW, (const double*)h->tilesW.p, s, (double*)h->partW.p,
+                  Bp, (int)B, st));
+  return reduce_rows8((const double*)h->partW.p, Bp, (const int64_t*)h->nodeg_base.p, (const int*)h->nodeg_nch.p, N,
+                      (const double*)h->wt.p, Y, ldy, (int)B, st);
+}
+
+void destroy_impl(xc_op* h) {
+  for (auto& b : h->blocks) {
+    fft_plan_free(b.fft);
+    dev_free(b.w); dev_free(b.yscale); dev_free(b.winv);
+    dev_free(b.start); dev_free(b.len); dev_free(b.off); dev_free(b.vals);
+    dev_free(b.grp_base); dev_free(b.grp_nch);
+  }
+  DevBuf* all[] = {&h->nodes, &h->wt, &h->tailP, &h->itemsA, &h->tilesA, &h->tail_base, &h->tail_nch,
+                   &h->itemsW, &h->tilesW, &h->nodeg_base, &h->nodeg_nch, &h->partA, &h->partW,
+                   &h->scratch, &h->zpl, &h->Xh, &h->Yh};
+  for (DevBuf* b : all) dev_free(*b);
+}
+
+}  // namespace
+
+// =========================================================================== C ABI
+extern "C" {
+
+xc_status xc_params_default(xc_params* p) {
+  if (!p) return XC_EINVAL;
+  memset(p, 0, sizeof(*p));
+  return XC_OK;
+}
+
+xc_status xc_build_compressed(xc_kind kind, const xc_params* p, const double* nodes, int64_t N, double eps,
+                              xc_handle* out) {
+  if (!out) {
+    xc_set_error("out is null");
+    return XC_EINVAL;
+  }
+  *out = nullptr;
+  xc_op* h = new xc_op();
+  xc_status s = build_impl(kind, p, nodes, N, eps, h);
+  if (s != XC_OK) {
+    destroy_impl(h);
+    delete h;
+    return s;
+  }
+  *out = h;
+  return XC_OK;
+}
+
+xc_status xc_apply(xc_handle h, xc_dir dir, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t B,
+                   void* stream) {
+  if (!h) {
+    xc_set_error("null handle");
+    return XC_EINVAL;
+  }
+  XC_CUDA(cudaSetDevice(h->device));
+  return apply_impl(h, dir, X, ldx, Y, ldy, B, (cudaStream_t)stream);
+}
+
+xc_status xc_apply_host(xc_handle h, xc_dir dir, const double* Xh, double* Yh, int64_t B, void* stream) {
+  if (!h || !Xh || !Yh || B < 1) {
+    xc_set_error("apply_host: bad arguments");
+    return XC_EINVAL;
+  }
+  XC_CUDA(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  size_t bytes = (size_t)h->N * B * sizeof(double);
+  if (h->Xh.bytes < bytes) {
+    XC_TRY(dev_alloc(h->Xh, bytes));
+    XC_TRY(dev_alloc(h->Yh, bytes));
+  }
+  XC_CUDA(cudaMemcpyAsync(h->Xh.p, Xh, bytes, cudaMemcpyHostToDevice, st));
+  XC_TRY(apply_impl(h, dir, (const double*)h->Xh.p, B, (double*)h->Yh.p, B, B, st));
+  XC_CUDA(cudaMemcpyAsync(Yh, h->Yh.p, bytes, cudaMemcpyDeviceToHost, st));
+  XC_CUDA(cudaStreamSynchronize(st));
+  return XC_OK;
+}
+
+xc_status xc_reserve(xc_handle h, int64_t B) {
+  if (!h || B < 1) return XC_EINVAL;
+  XC_CUDA(cudaSetDevice(h->device));
+  return ensure_ws(h, B);
+}
+
+xc_status xc_workspace_query(xc_handle h, int64_t B, size_t* bytes) {
+  if (!h || !bytes || B < 1) return XC_EINVAL;
+  int64_t Bp = pad_cols(B);
+  size_t s = 0, scr = 0;
+  for (auto& b : h->blocks)
+    if (b.fft.L2 > 1) scr = std::max(scr, (size_t)b.L * B * sizeof(double2));
+  s += scr;
+  if (h->dirs & XC_DIR_A) s += (size_t)h->rowsA * Bp * 8;
+  if (h->dirs & XC_DIR_WAT) {
+    s += (size_t)h->rowsW * Bp * 8;
+    for (auto& b : h->blocks) s += (size_t)2 * b.H * Bp * 8;
+  }
+  *bytes = s;
+  return XC_OK;
+}
+
+xc_status xc_info(xc_handle h, xc_info_t* out) {
+  if (!h || !out) return XC_EINVAL;
+  *out = h->info;
+  return XC_OK;
+}
+
+xc_status xc_block_info(xc_handle h, int i, xc_block_info_t* out) {
+  if (!h || !out || i < 0 || i >= (int)h->blocks.size()) {
+    xc_set_error("block_info: bad block index");
+    return XC_EINVAL;
+  }
+  const BlockData& b = h->blocks[i];
+  out->L = b.L;
+  out->H = b.H;
+  out->m_off = b.m_off;
+  out->keep_lo = b.keep_lo;
+  out->keep_hi = b.keep_hi;
+  out->nnz = b.nnz;
+  out->max_band = b.max_band;
+  return XC_OK;
+}
+
+xc_status xc_block_window(xc_handle h, int i, double* w) {
+  if (!h || !w || i < 0 || i >= (int)h->blocks.size()) return XC_EINVAL;
+  memcpy(w, h->blocks[i].h_w.data(), h->blocks[i].h_w.size() * sizeof(double));
+  return XC_OK;
+}
+
+xc_status xc_node_spectrum(xc_handle h, int i, int64_t k, double* re, double* im) {
+  if (!h || !re || !im || i < 0 || i >= (int)h->blocks.size() || k < 0 || k >= h->N) {
+    xc_set_error("node_spectrum: bad arguments");
+    return XC_EINVAL;
+  }
+  const BlockData& b = h->blocks[i];
+  for (int q = 0; q < b.H; ++q) re[q] = im[q] = 0.0;
+  int n = b.h_len[k];
+  if (n == 0) return XC_OK;
+  std::vector<double2> v(n);
+  XC_CUDA(cudaSetDevice(h->device));
+  XC_CUDA(cudaMemcpy(v.data(), (double2*)b.vals.p + b.h_off[k], n * sizeof(double2), cudaMemcpyDeviceToHost));
+  for (int j = 0; j < n; ++j) {
+    re[b.h_start[k] + j] = v[j].x;
+    im[b.h_start[k] + j] = v[j].y;
+  }
+  return XC_OK;
+}
+
+xc_status xc_gauss_rule(xc_kind kind, double alpha, double beta, int64_t N, double* nodes, double* weights,
+                        double* wt, int device) {
+  if (!nodes) return XC_EINVAL;
+  std::vector<double> w(N), t(N);
+  xc_status s = gauss_rule_device(kind, alpha, beta, N, nodes, w.data(), t.data(), device);
+  if (s != XC_OK) return s;
+  if (weights) memcpy(weights, w.data(), N * sizeof(double));
+  if (wt) memcpy(wt, t.data(), N * sizeof(double));
+  return XC_OK;
+}
+
+xc_status xc_plan_chain(xc_kind kind, int64_t N, double eps1, double eps2, int cutoff, double* zeta, int* nb,
+                        int* L, int* m_off, int* keep_lo, int* keep_hi, int max_blocks, int* tail) {
+  if (!zeta || !nb || !L || !m_off || !keep_lo || !keep_hi || !tail || N < 2 || !(eps1 > 0 && eps1 < 1)) {
+    xc_set_error("plan_chain: bad arguments");
+    return XC_EINVAL;
+  }
+  if (eps2 <= 0) eps2 = 1e-2;
+  if (!(eps1 < eps2 && eps2 < 1)) {
+    xc_set_error("plan_chain: need eps1 < eps2 < 1");
+    return XC_EINVAL;
+  }
+  PlanOut p;
+  XC_TRY(make_chain(kind, N, eps1, eps2, cutoff > 0 ? cutoff : 32, p));
+  if ((int)p.blocks.size() > max_blocks) {
+    xc_set_error("plan_chain: too many blocks for the output arrays");
+    return XC_EINVAL;
+  }
+  *zeta = p.zeta;
+  *nb = (int)p.blocks.size();
+  *tail = p.tail;
+  for (size_t i = 0; i < p.blocks.size(); ++i) {
+    L[i] = p.blocks[i].L;
+    m_off[i] = p.blocks[i].m_off;
+    keep_lo[i] = p.blocks[i].keep_lo;
+    keep_hi[i] = p.blocks[i].keep_hi;
+  }
+  return XC_OK;
+}
+
+void xc_destroy(xc_handle h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  destroy_impl(h);
+  delete h;
+}
+
+const char* xc_last_error(void) { return g_err.c_str(); }
+
+const char* xc_version(void) { return "xc-b200 0.1 (sm_100a, fp64 DMMA)"; }
+
+}  // extern "C"

@@ -1,0 +1,215 @@
+// xc_internal.cuh -- shared declarations of the libxc CUDA sources (product side).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/xc.h"
+
+// ---------------------------------------------------------------------------
+// Error-free fp64 pairs ("double-double") for the entry generation (R-5).
+// Product-side implementation (host + device); independent of oracle/.
+// ---------------------------------------------------------------------------
+struct ddv {
+  double h, l;
+};
+
+__host__ __device__ __forceinline__ ddv dv(double a) { return ddv{a, 0.0}; }
+__host__ __device__ __forceinline__ ddv qsum(double a, double b) {
+  double s = a + b;
+  return ddv{s, b - (s - a)};
+}
+__host__ __device__ __forceinline__ ddv tsum(double a, double b) {
+  double s = a + b;
+  double v = s - a;
+  return ddv{s, (a - (s - v)) + (b - v)};
+}
+__host__ __device__ __forceinline__ ddv tprod(double a, double b) {
+  double p = a * b;
+#ifdef __CUDA_ARCH__
+  return ddv{p, __fma_rn(a, b, -p)};
+#else
+  return ddv{p, fma(a, b, -p)};
+#endif
+}
+__host__ __device__ __forceinline__ ddv ddadd(ddv a, ddv b) {
+  ddv s = tsum(a.h, b.h);
+  ddv t = tsum(a.l, b.l);
+  s.l += t.h;
+  s = qsum(s.h, s.l);
+  s.l += t.l;
+  return qsum(s.h, s.l);
+}
+__host__ __device__ __forceinline__ ddv ddneg(ddv a) { return ddv{-a.h, -a.l}; }
+__host__ __device__ __forceinline__ ddv ddsub(ddv a, ddv b) { return ddadd(a, ddneg(b)); }
+__host__ __device__ __forceinline__ ddv ddmul(ddv a, ddv b) {
+  ddv p = tprod(a.h, b.h);
+#ifdef __CUDA_ARCH__
+  p.l = __fma_rn(a.h, b.l, __fma_rn(a.l, b.h, p.l));
+#else
+  p.l += a.h * b.l + a.l * b.h;
+#endif
+  return qsum(p.h, p.l);
+}
+__host__ __device__ __forceinline__ ddv ddmuld(ddv a, double b) {
+  ddv p = tprod(a.h, b);
+#ifdef __CUDA_ARCH__
+  p.l = __fma_rn(a.l, b, p.l);
+#else
+  p.l += a.l * b;
+#endif
+  return qsum(p.h, p.l);
+}
+__host__ __device__ __forceinline__ ddv dddiv(ddv a, ddv b) {
+  double q1 = a.h / b.h;
+  ddv r = ddsub(a, ddmuld(b, q1));
+  double q2 = r.h / b.h;
+  r = ddsub(r, ddmuld(b, q2));
+  double q3 = r.h / b.h;
+  return ddadd(qsum(q1, q2), dv(q3));
+}
+__host__ __device__ __forceinline__ ddv ddsqrt(ddv a) {
+  if (a.h <= 0.0) return dv(0.0);
+  double s = sqrt(a.h);
+  ddv r = ddsub(a, tprod(s, s));
+  return ddadd(dv(s), dv(r.h / (2.0 * s)));
+}
+__host__ __device__ __forceinline__ double ddround(ddv a) { return a.h + a.l; }
+
+// ---------------------------------------------------------------------------
+// Error handling
+// ---------------------------------------------------------------------------
+void xc_set_error(const std::string& msg);
+
+#define XC_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e__ = (call);                                                          \
+    if (e__ != cudaSuccess) {                                                          \
+      xc_set_error(std::string(#call) + ": " + cudaGetErrorString(e__) + " @" +        \
+                   __FILE__ + ":" + std::to_string(__LINE__));                         \
+      return e__ == cudaErrorMemoryAllocation ? XC_ENOMEM : XC_ECUDA;                  \
+    }                                                                                  \
+  } while (0)
+
+#define XC_TRY(call)                  \
+  do {                                \
+    xc_status s__ = (call);           \
+    if (s__ != XC_OK) return s__;     \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Device buffers (owned by the handle)
+// ---------------------------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+xc_status dev_alloc(DevBuf& b, size_t bytes);
+void dev_free(DevBuf& b);
+
+// ---------------------------------------------------------------------------
+// FFT engine (fft.cu): batched complex FFT of 2-3-5-smooth length L along the
+// slow axis of a batch-fastest layout, 1 pass (L <= 1024) or 2 passes
+// (four-step, L = L1 * L2) through an L2-resident scratch.
+// ---------------------------------------------------------------------------
+enum FftPro { PRO_PLAIN = 0, PRO_UPART = 1, PRO_XREAL = 2 };
+enum FftEpi { EPI_PLAIN = 0, EPI_YREAL = 1, EPI_ZPLANES = 2 };
+
+struct FftPlan {
+  int L = 0, L1 = 0, L2 = 0;       // L = L1 * L2; single pass when L2 == 1
+  int nf1 = 0, f1[12] = {0};       // radices of the first (or only) pass
+  int nf2 = 0, f2[12] = {0};
+  double2* tw1 = nullptr;          // e^{+2 pi i n / L1}, n < L1
+  double2* tw2 = nullptr;          // e^{+2 pi i n / L2}
+  double2* twL = nullptr;          // e^{+2 pi i n / L}  (two-pass only)
+  DevBuf mem;
+};
+
+struct FftIO {
+  // prologue sources
+  const double2* src = nullptr; int64_t lds = 0;           // PRO_PLAIN
+  const double* part = nullptr; int64_t ldp = 0;           // PRO_UPART: partial sums
+  const int64_t* grp_base = nullptr; const int* grp_nch = nullptr; int H = 0;
+  const double* X = nullptr; int64_t ldx = 0;              // PRO_XREAL
+  const double* winv = nullptr;                            // 1/w_p (PRO_XREAL)
+  int keep_lo = 0, keep_hi = 0, m_off = 0;
+  // epilogue destinations
+  double2* dst = nullptr; int64_t ldd = 0; int kmax = 0;    // EPI_PLAIN: bins [0,kmax)
+  double* Y = nullptr; int64_t ldy = 0;                    // EPI_YREAL
+  const double* yscale = nullptr;                          // 1/(sqrt(L) w_p) (EPI_YREAL)
+  double* zre = nullptr; double* zim = nullptr; int64_t ldz = 0;  // EPI_ZPLANES
+  double scale = 1.0;                                      // EPI_PLAIN / EPI_ZPLANES
+};
+
+xc_status fft_plan_make(FftPlan& p, int L);
+void fft_plan_free(FftPlan& p);
+// sigma = -1 forward (Eq. 1), +1 inverse.  ncol columns.  scratch: L*ncol double2 (2-pass only).
+xc_status fft_run(const FftPlan& p, int sigma, FftPro pro, FftEpi epi, const FftIO& io, int ncol,
+                  double2* scratch, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// SpMM on the FP64 tensor cores (spmm.cu)
+// Each item computes an 8 x (8*NT) output tile  D = A_item (8 x 4*nsteps) * Bm,
+// where row r of Bm is gathered from a source (plain rows or re/im planes).
+// ---------------------------------------------------------------------------
+struct SpmmItem {
+  int64_t a_off;    // offset (doubles) of the A tile stream (32 doubles per step)
+  int64_t out_row;  // first of the 8 output rows in the partial-sum array
+  int k0;           // first B row (node, degree or bin) of the item
+  int nsteps;       // 4 B rows per step
+  int src;          // index into SpmmSrcs
+  int pad;
+};
+
+#define XC_MAX_SRC 40
+struct SpmmSrcs {
+  const double* re[XC_MAX_SRC];
+  const double* im[XC_MAX_SRC];   // null => plain rows (row r -> k0 + r)
+  int nrows[XC_MAX_SRC];          // rows available (loads beyond are zero)
+  int64_t ld[XC_MAX_SRC];
+};
+
+xc_status spmm_run(const SpmmItem* items, int nitems, const double* tiles, const SpmmSrcs& srcs,
+                   double* part, int64_t ldp, int ncols, cudaStream_t st);
+int spmm_nt_for(int64_t B);
+
+// ---------------------------------------------------------------------------
+// Reductions of the partial sums (spmm.cu)
+// ---------------------------------------------------------------------------
+// Y[deg][b] = sum_c part[(base(g) + 8c + deg % 8)][b], g = deg / 8, deg in [0, t)
+xc_status reduce_rows8(const double* part, int64_t ldp, const int64_t* base, const int* nch, int nrows,
+                       const double* rowscale, double* Y, int64_t ldy, int ncols, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// Precompute kernels (gen.cu)
+// ---------------------------------------------------------------------------
+struct GenParams {
+  int kind;            // XC_COS / XC_JACOBI / XC_LAGUERRE
+  int L;               // positions [0, L)
+  int m_off;           // degree = position + m_off
+  const double* nodes; // device, chunk
+  int nc;              // nodes in chunk
+  const double* w;     // window on L positions (device) or null (=1)
+  const double2* jab;  // Jacobi: per n: (b_n.h, b_n.l), (a_n.h, a_n.l), (inva_n.h, inva_n.l) = 3 double2
+  ddv p0;              // Jacobi p_0
+};
+// F[p * nc + k] = (w_p * phi_{p+m_off}(x_k), 0)   (complex, batch = nodes)
+xc_status gen_entries(const GenParams& g, double2* F, cudaStream_t st);
+// E[j * ldE + k] = phi_j(x_k) (real), j in [0, L)
+xc_status gen_entries_real(const GenParams& g, double* E, int64_t ldE, cudaStream_t st);
+
+// Band detection and compaction on a spectrum chunk Spec[q * nc + k], q < H.
+xc_status band_detect(const double2* spec, int H, int nc, double eps1, int* start, int* len,
+                      cudaStream_t st);
+xc_status band_store(const double2* spec, int H, int nc, double eps1, const int* start, const int* len,
+                     const int64_t* off, double2* vals, cudaStream_t st);
+
+// Gauss rules (gauss.cu)
+xc_status gauss_rule_device(int kind, double alpha, double beta, int64_t N, double* x, double* w,
+                            double* wt, int device);
+
+// Host-side Jacobi recurrence coefficients in double-double (plan.cu)
+void jacobi_coeffs(double alpha, double beta, int nmax, std::vector<double2>& tab, ddv& p0);
+double jacobi_mu0(double alpha, double beta);

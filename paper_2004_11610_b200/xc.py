@@ -1,0 +1,231 @@
+"""Thin ctypes binding of libxc.so (include/xc.h): argument marshalling only.
+
+Every step of the transform runs in the library's sm_100a kernels; PyTorch is
+used for device memory and streams.  There is no CPU fallback: if libxc.so is
+missing or no CUDA device is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libxc.so")
+
+XC_COS, XC_JACOBI, XC_LAGUERRE = 1, 2, 3
+XC_DIR_A, XC_DIR_WAT = 1, 2
+_STATUS = {0: "XC_OK", 1: "XC_EINVAL", 2: "XC_ENUMERIC", 3: "XC_ESTATE", 4: "XC_ENOMEM", 5: "XC_ECUDA",
+           6: "XC_EUNSUPPORTED"}
+
+_i64 = ctypes.c_int64
+_dp = ctypes.POINTER(ctypes.c_double)
+
+
+class XcParams(ctypes.Structure):
+    _fields_ = [("alpha", ctypes.c_double), ("beta", ctypes.c_double), ("eps1", ctypes.c_double),
+                ("eps2", ctypes.c_double), ("dense_cutoff", ctypes.c_int), ("dirs", ctypes.c_int),
+                ("weights", _dp), ("device", ctypes.c_int), ("stream", ctypes.c_void_p),
+                ("node_chunk", ctypes.c_int)]
+
+
+class XcInfo(ctypes.Structure):
+    _fields_ = [("N", _i64), ("kind", ctypes.c_int), ("zeta", ctypes.c_double), ("eps1", ctypes.c_double),
+                ("eps2", ctypes.c_double), ("n_blocks", ctypes.c_int), ("tail", ctypes.c_int),
+                ("dirs", ctypes.c_int), ("nnz", _i64), ("op_bytes_A", _i64), ("op_bytes_WAT", _i64),
+                ("flops_per_col_A", ctypes.c_double), ("flops_per_col_WAT", ctypes.c_double),
+                ("dmma_flops_per_col_A", ctypes.c_double), ("dmma_flops_per_col_WAT", ctypes.c_double)]
+
+
+class XcBlockInfo(ctypes.Structure):
+    _fields_ = [("L", ctypes.c_int), ("H", ctypes.c_int), ("m_off", ctypes.c_int), ("keep_lo", ctypes.c_int),
+                ("keep_hi", ctypes.c_int), ("nnz", _i64), ("max_band", ctypes.c_int)]
+
+
+EXPORTS = ["xc_params_default", "xc_build_compressed", "xc_apply", "xc_apply_host", "xc_reserve",
+           "xc_workspace_query", "xc_info", "xc_block_info", "xc_block_window", "xc_node_spectrum",
+           "xc_gauss_rule", "xc_plan_chain", "xc_destroy", "xc_last_error", "xc_version"]
+
+_lib = None
+
+
+class XcError(RuntimeError):
+    pass
+
+
+def load():
+    """Load libxc.so (built by __graft_entry__.build() / `make -C paper_2004_11610_b200/csrc`)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise XcError(f"libxc.so not built ({LIB_PATH}); run __graft_entry__.build()")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp = ctypes.c_void_p
+    lib.xc_params_default.argtypes = [ctypes.POINTER(XcParams)]
+    lib.xc_build_compressed.argtypes = [ctypes.c_int, ctypes.POINTER(XcParams), _dp, _i64, ctypes.c_double,
+                                        ctypes.POINTER(vp)]
+    lib.xc_apply.argtypes = [vp, ctypes.c_int, vp, _i64, vp, _i64, _i64, vp]
+    lib.xc_apply_host.argtypes = [vp, ctypes.c_int, vp, vp, _i64, vp]
+    lib.xc_reserve.argtypes = [vp, _i64]
+    lib.xc_workspace_query.argtypes = [vp, _i64, ctypes.POINTER(ctypes.c_size_t)]
+    lib.xc_info.argtypes = [vp, ctypes.POINTER(XcInfo)]
+    lib.xc_block_info.argtypes = [vp, ctypes.c_int, ctypes.POINTER(XcBlockInfo)]
+    lib.xc_block_window.argtypes = [vp, ctypes.c_int, _dp]
+    lib.xc_node_spectrum.argtypes = [vp, ctypes.c_int, _i64, _dp, _dp]
+    lib.xc_gauss_rule.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, _i64, _dp, _dp, _dp,
+                                  ctypes.c_int]
+    ip = ctypes.POINTER(ctypes.c_int)
+    lib.xc_plan_chain.argtypes = [ctypes.c_int, _i64, ctypes.c_double, ctypes.c_double, ctypes.c_int, _dp, ip,
+                                  ip, ip, ip, ip, ctypes.c_int, ip]
+    lib.xc_destroy.argtypes = [vp]
+    lib.xc_destroy.restype = None
+    lib.xc_last_error.restype = ctypes.c_char_p
+    lib.xc_version.restype = ctypes.c_char_p
+    for name in EXPORTS:
+        if name not in ("xc_destroy", "xc_last_error", "xc_version"):
+            getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = load().xc_last_error().decode(errors="replace")
+        raise XcError(f"{_STATUS.get(rc, rc)}: {msg}")
+
+
+def _np_ptr(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_dp)
+
+
+def gauss_rule(kind: int, N: int, alpha: float = 0.0, beta: float = 0.0, device: int = 0):
+    """Gauss nodes (ascending), weights and wt (= w e^x for Laguerre) computed on the GPU."""
+    lib = load()
+    x = np.empty(N)
+    w = np.empty(N)
+    wt = np.empty(N)
+    _check(lib.xc_gauss_rule(kind, alpha, beta, N, _np_ptr(x), _np_ptr(w), _np_ptr(wt), device))
+    return x, w, wt
+
+
+def plan_chain(kind: int, N: int, eps1: float, eps2: float = 0.0, dense_cutoff: int = 0):
+    """Host-only planning: (zeta, [(L, m_off, keep_lo, keep_hi)], tail)."""
+    lib = load()
+    M = 64
+    z = ctypes.c_double()
+    nb, tail = ctypes.c_int(), ctypes.c_int()
+    arrs = [(ctypes.c_int * M)() for _ in range(4)]
+    _check(lib.xc_plan_chain(kind, N, eps1, eps2, dense_cutoff, ctypes.byref(z), ctypes.byref(nb), *arrs, M,
+                             ctypes.byref(tail)))
+    blocks = [tuple(a[i] for a in arrs) for i in range(nb.value)]
+    return z.value, blocks, tail.value
+
+
+class Transform:
+    """A compressed special-function transform (handle of xc_build_compressed)."""
+
+    def __init__(self, kind: int, nodes, eps: float, alpha: float = 0.0, beta: float = 0.0,
+                 eps1: float = 0.0, eps2: float = 0.0, dense_cutoff: int = 0, dirs: int = XC_DIR_A,
+                 weights=None, device: int = 0, node_chunk: int = 0, stream=None):
+        lib = load()
+        self._lib = lib
+        self.kind = kind
+        x = np.ascontiguousarray(np.asarray(nodes, dtype=np.float64))
+        self.N = x.size
+        p = XcParams()
+        lib.xc_params_default(ctypes.byref(p))
+        p.alpha, p.beta, p.eps1, p.eps2 = alpha, beta, eps1, eps2
+        p.dense_cutoff, p.dirs, p.device, p.node_chunk = dense_cutoff, dirs, device, node_chunk
+        self._w = None
+        if weights is not None:
+            self._w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
+            p.weights = _np_ptr(self._w)
+        p.stream = ctypes.c_void_p(stream) if stream else None
+        h = ctypes.c_void_p()
+        _check(lib.xc_build_compressed(kind, ctypes.byref(p), _np_ptr(x), self.N, eps, ctypes.byref(h)))
+        self._h = h
+        self.device = device
+
+    # -- computation stage --------------------------------------------------------------
+    def apply(self, X, direction: int = XC_DIR_A, out=None, stream=None):
+        """Y = A X (XC_DIR_A) or diag(wt) A^T X (XC_DIR_WAT); X a CUDA fp64 tensor (N x B)."""
+        import torch
+        if not (isinstance(X, torch.Tensor) and X.is_cuda and X.dtype == torch.float64 and X.dim() == 2):
+            raise XcError("X must be a 2-D CUDA float64 tensor")
+        if X.stride(1) != 1:
+            X = X.contiguous()
+        N, B = X.shape
+        if N != self.N:
+            raise XcError(f"X has {N} rows, transform has N = {self.N}")
+        if out is None:
+            out = torch.empty((N, B), dtype=torch.float64, device=X.device)
+        st = stream if stream is not None else torch.cuda.current_stream(X.device).cuda_stream
+        _check(self._lib.xc_apply(self._h, direction, ctypes.c_void_p(X.data_ptr()), X.stride(0),
+                                  ctypes.c_void_p(out.data_ptr()), out.stride(0), B, ctypes.c_void_p(st)))
+        return out
+
+    def apply_host(self, X: np.ndarray, direction: int = XC_DIR_A, out: np.ndarray | None = None, stream=None):
+        """End-to-end call with host buffers (copies inside the library call)."""
+        X = np.ascontiguousarray(X, dtype=np.float64)
+        N, B = X.shape
+        if out is None:
+            out = np.empty_like(X)
+        _check(self._lib.xc_apply_host(self._h, direction, ctypes.c_void_p(X.ctypes.data),
+                                       ctypes.c_void_p(out.ctypes.data), B, ctypes.c_void_p(stream or 0)))
+        return out
+
+    def apply_host_ptr(self, x_ptr: int, y_ptr: int, B: int, direction: int = XC_DIR_A, stream=None):
+        _check(self._lib.xc_apply_host(self._h, direction, ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr), B,
+                                       ctypes.c_void_p(stream or 0)))
+
+    def reserve(self, B: int):
+        _check(self._lib.xc_reserve(self._h, B))
+
+    def workspace_bytes(self, B: int) -> int:
+        n = ctypes.c_size_t()
+        _check(self._lib.xc_workspace_query(self._h, B, ctypes.byref(n)))
+        return n.value
+
+    # -- introspection --------------------------------------------------------------------
+    def info(self) -> dict:
+        s = XcInfo()
+        _check(self._lib.xc_info(self._h, ctypes.byref(s)))
+        return {f: getattr(s, f) for f, _ in XcInfo._fields_}
+
+    def block_info(self, i: int) -> dict:
+        s = XcBlockInfo()
+        _check(self._lib.xc_block_info(self._h, i, ctypes.byref(s)))
+        return {f: getattr(s, f) for f, _ in XcBlockInfo._fields_}
+
+    def blocks(self) -> list:
+        return [self.block_info(i) for i in range(self.info()["n_blocks"])]
+
+    def window(self, i: int) -> np.ndarray:
+        L = self.block_info(i)["L"]
+        w = np.empty(L)
+        _check(self._lib.xc_block_window(self._h, i, _np_ptr(w)))
+        return w
+
+    def node_spectrum(self, i: int, k: int) -> np.ndarray:
+        H = self.block_info(i)["H"]
+        re, im = np.empty(H), np.empty(H)
+        _check(self._lib.xc_node_spectrum(self._h, i, k, _np_ptr(re), _np_ptr(im)))
+        return re + 1j * im
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.xc_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def version() -> str:
+    return load().xc_version().decode()

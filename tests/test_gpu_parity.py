@@ -1,0 +1,251 @@
+"""GPU parity: the CUDA path (through the C ABI, libxc.so) against the CPU oracle.
+
+Bars (BASELINE.json north_star): relative L2 per column <= 1e-12 against the
+oracle's compressed apply of the same inputs, <= 10*eps against the dense
+product.  Full BASELINE sizes run in the launch configuration bench.py times;
+c5 (N = 65536) is checked on 16 sampled columns against the dense product and
+on sampled nodes of the operator.
+"""
+import functools
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2004_11610_b200 import inputs as I
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _xc():
+    from paper_2004_11610_b200 import xc
+    return xc
+
+
+def _kind(c):
+    return O.Kind(c.kind, c.alpha, c.beta)
+
+
+@functools.lru_cache(maxsize=None)
+def _nodes(kind_t, N, seed):
+    kind = O.Kind(*kind_t)
+    if kind.kind == O.KIND_COS:
+        return I.cos_nodes(N, seed), None
+    x, _, wt = O.gauss_rule(kind, N)
+    return x, wt
+
+
+@functools.lru_cache(maxsize=None)
+def _oracle_op(kind_t, N, seed, eps):
+    kind = O.Kind(*kind_t)
+    x, _ = _nodes(kind_t, N, seed)
+    return O.compress(O.make_plan(kind, N, eps), x)
+
+
+def _gpu(X):
+    return torch.from_numpy(np.ascontiguousarray(X)).cuda()
+
+
+CASES = [
+    # name, kind tuple, N, B, eps, seed
+    ("c1", (O.KIND_JACOBI, 0.0, 0.0), 512, 1, 1e-12, 0),
+    ("c1_ragged", (O.KIND_JACOBI, 0.0, 0.0), 512, 37, 1e-12, 0),
+    ("c2", (O.KIND_COS, 0.0, 0.0), 4096, 64, 1e-10, 1),
+    ("c2_small_ragged", (O.KIND_COS, 0.0, 0.0), 1000, 130, 1e-10, 1),
+    ("c3_reduced", (O.KIND_JACOBI, 0.5, -0.3), 2048, 96, 1e-12, 2),
+    ("c3", (O.KIND_JACOBI, 0.5, -0.3), 16384, 256, 1e-12, 2),
+    ("c4_fwd", (O.KIND_LAGUERRE, 0.0, 0.0), 8192, 256, 1e-11, 3),
+    ("legendre_odd", (O.KIND_JACOBI, 0.0, 0.0), 777, 19, 1e-12, 5),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_output_axis_parity(case):
+    """XC_DIR_A (Alg. 2 / block form): GPU vs oracle compressed (<= 1e-12) and dense (<= 10 eps)."""
+    xc = _xc()
+    name, kt, N, B, eps, seed = case
+    kind = O.Kind(*kt)
+    x, _ = _nodes(kt, N, seed)
+    X = I.rhs(N, B, seed + 100)
+    T = xc.Transform(kt[0], x, eps, alpha=kt[1], beta=kt[2])
+    Y = T.apply(_gpu(X)).cpu().numpy()
+    op = _oracle_op(kt, N, seed, eps)
+    Ya = O.apply_output_axis(op, X)
+    e_alg = O.rel_l2_cols(Y, Ya)
+    assert e_alg.max() <= 1e-12, (name, e_alg.max())
+    cols = np.arange(B) if N <= 8192 else np.linspace(0, B - 1, 16).astype(int)
+    Yd = O.dense_apply(kind, x, X[:, cols])
+    e_d = O.rel_l2_cols(Y[:, cols], Yd)
+    assert e_d.max() <= 10 * eps, (name, e_d.max())
+    # the GPU plan is the oracle's plan
+    info = T.info()
+    assert info["n_blocks"] == len(op.plan.blocks) and info["tail"] == op.plan.tail
+    for i, b in enumerate(op.plan.blocks):
+        bi = T.block_info(i)
+        assert (bi["L"], bi["m_off"], bi["keep_lo"], bi["keep_hi"]) == (b.L, b.m_off, b.keep_lo, b.keep_hi)
+    T.close()
+
+
+@pytest.mark.parametrize("case", [CASES[0], CASES[2], CASES[4]], ids=["c1", "c2", "c3_reduced"])
+def test_operator_parity(case):
+    """Precompute (K1-K4): kept set equals the oracle's except within 1e-6 of the threshold;
+    values within 1e-13 of the node maximum."""
+    xc = _xc()
+    name, kt, N, B, eps, seed = case
+    x, _ = _nodes(kt, N, seed)
+    T = xc.Transform(kt[0], x, eps, alpha=kt[1], beta=kt[2])
+    op = _oracle_op(kt, N, seed, eps)
+    rng = np.random.default_rng(0)
+    ks = np.r_[0, N - 1, rng.integers(0, N, 14)]
+    for i, (blk, S) in enumerate(zip(op.plan.blocks, op.S)):
+        full = O.node_spectra(op.plan, blk, x[ks])
+        for j, k in enumerate(ks):
+            g = T.node_spectrum(i, int(k))
+            o = S[int(k)].toarray().ravel()
+            m = np.abs(full[j]).max()
+            tau = op.plan.eps1 * m
+            near = np.abs(np.abs(full[j]) - tau) <= 1e-6 * tau
+            assert np.all(((g != 0) == (o != 0)) | near), (name, i, k)
+            both = (g != 0) & (o != 0)
+            assert np.abs(g[both] - o[both]).max(initial=0) <= 1e-13 * m, (name, i, k)
+    T.close()
+
+
+def test_input_axis_parity_laguerre():
+    """XC_DIR_WAT (Alg. 1 / block form) for c4: backward = diag(wt) A^T C against the oracle, then
+    the round trip forward(backward(C)) ~ C (C-15)."""
+    xc = _xc()
+    kt = (O.KIND_LAGUERRE, 0.0, 0.0)
+    N, B, eps = 8192, 256, 1e-11
+    x, wt = _nodes(kt, N, 3)
+    C = I.laguerre_coeffs(N, B, 3)
+    T = xc.Transform(xc.XC_LAGUERRE, x, eps, dirs=xc.XC_DIR_A | xc.XC_DIR_WAT, weights=wt)
+    Xb = T.apply(_gpu(C), xc.XC_DIR_WAT).cpu().numpy()
+    op = _oracle_op(kt, N, 3, eps)
+    Xo = O.apply_input_axis(op, C, wt)
+    assert O.rel_l2_cols(Xb, Xo).max() <= 1e-12
+    cols = np.arange(0, B, 16)
+    Xd = wt[:, None] * O.dense_apply_t(O.Kind(*kt), x, C[:, cols])
+    assert O.rel_l2_cols(Xb[:, cols], Xd).max() <= 10 * eps
+    C2 = T.apply(_gpu(Xb), xc.XC_DIR_A).cpu().numpy()
+    assert O.rel_l2_cols(C2, C).max() <= 10 * eps
+    T.close()
+
+
+@pytest.mark.parametrize("kt,N", [((O.KIND_JACOBI, 0.0, 0.0), 1024), ((O.KIND_JACOBI, 0.5, -0.3), 2000),
+                                  ((O.KIND_COS, 0.0, 0.0), 640)])
+def test_input_axis_parity_small(kt, N):
+    """XC_DIR_WAT on Jacobi and cos operators (ragged B) vs the oracle's Algorithm 1."""
+    xc = _xc()
+    eps = 1e-12 if kt[0] == O.KIND_JACOBI else 1e-10
+    x, w = _nodes(kt, N, 7)
+    w = np.ones(N) if w is None else w
+    C = I.rhs(N, 21, 9)
+    T = xc.Transform(kt[0], x, eps, alpha=kt[1], beta=kt[2], dirs=xc.XC_DIR_WAT, weights=w)
+    Y = T.apply(_gpu(C), xc.XC_DIR_WAT).cpu().numpy()
+    op = O.compress(O.make_plan(O.Kind(*kt), N, eps), x)
+    assert O.rel_l2_cols(Y, O.apply_input_axis(op, C, w)).max() <= 1e-12
+    Yd = w[:, None] * O.dense_apply_t(O.Kind(*kt), x, C)
+    assert O.rel_l2_cols(Y, Yd).max() <= 10 * eps
+    T.close()
+
+
+@pytest.mark.slow
+def test_c5_sampled():
+    """c5 at full size (N = 65536, bench launch configuration B = 4096): 16 sampled columns
+    b = 256 i vs the dense product (10 eps), and sampled nodes of the operator vs the oracle."""
+    xc = _xc()
+    c = I.CONFIGS["c5"]
+    kt = (c.kind, c.alpha, c.beta)
+    x, _ = _nodes(kt, c.N, c.seed)
+    X = I.config_rhs(c)
+    T = xc.Transform(c.kind, x, c.eps)
+    Y = T.apply(_gpu(X)).cpu().numpy()
+    cols = 256 * np.arange(16)
+    Yd = O.dense_apply(O.Kind(*kt), x, X[:, cols])
+    e = O.rel_l2_cols(Y[:, cols], Yd)
+    assert e.max() <= 10 * c.eps, e
+    plan = O.make_plan(O.Kind(*kt), c.N, c.eps)
+    ks = np.r_[0, 1, c.N // 2, c.N - 1]
+    for i, blk in enumerate(plan.blocks):
+        S = O.threshold(O.node_spectra(plan, blk, x[ks]), plan.eps1)
+        for j, k in enumerate(ks):
+            g = T.node_spectrum(i, int(k))
+            m = np.abs(S[j]).max()
+            assert np.abs(g - S[j]).max() <= 1e-13 * m + 2 * plan.eps1 * m
+    T.close()
+
+
+def test_gauss_rule_vs_oracle():
+    """Product Gauss rules (GPU bisection + dd Newton) equal the oracle's to a few ulp."""
+    xc = _xc()
+    for kt, N in (((O.KIND_JACOBI, 0.0, 0.0), 1024), ((O.KIND_JACOBI, 0.5, -0.3), 2048),
+                  ((O.KIND_LAGUERRE, 0.0, 0.0), 1024)):
+        x, w, wt = xc.gauss_rule(kt[0], N, kt[1], kt[2])
+        xo, wo, wto = O.gauss_rule(O.Kind(*kt), N)
+        assert np.all(np.abs(x - xo) <= 4 * np.spacing(np.abs(xo)) + 1e-300)
+        np.testing.assert_allclose(w, wo, rtol=1e-12)
+        np.testing.assert_allclose(wt, wto, rtol=1e-12)
+
+
+def test_determinism_and_sharding():
+    """Bit-identical on repeat, and column shards (what each rank of a G-GPU run computes)
+    equal the corresponding columns of the single run."""
+    xc = _xc()
+    kt = (O.KIND_JACOBI, 0.5, -0.3)
+    N, B = 2048, 256
+    x, _ = _nodes(kt, N, 2)
+    X = _gpu(I.rhs(N, B, 4))
+    T = xc.Transform(kt[0], x, 1e-12, alpha=0.5, beta=-0.3)
+    Y1 = T.apply(X).cpu()
+    Y2 = T.apply(X).cpu()
+    assert torch.equal(Y1, Y2)
+    for G in (2, 4, 8):
+        for g in range(G):
+            sl = slice(g * B // G, (g + 1) * B // G)
+            Yg = T.apply(X[:, sl].contiguous()).cpu()
+            assert torch.equal(Yg, Y1[:, sl]), (G, g)
+    T.close()
+
+
+def test_strided_and_host_api():
+    """ldx, ldy > B (strided views) and the host-buffer entry point give the same numbers."""
+    xc = _xc()
+    kt = (O.KIND_JACOBI, 0.0, 0.0)
+    N, B = 512, 24
+    x, _ = _nodes(kt, N, 0)
+    Xn = I.rhs(N, B, 1)
+    T = xc.Transform(xc.XC_JACOBI, x, 1e-12)
+    Y = T.apply(_gpu(Xn)).cpu().numpy()
+    big = torch.zeros((N, 40), dtype=torch.float64, device="cuda")
+    big[:, 3:3 + B] = _gpu(Xn)
+    out = torch.full((N, 50), 7.0, dtype=torch.float64, device="cuda")
+    T.apply(big[:, 3:3 + B], out=out[:, 5:5 + B])
+    assert np.array_equal(out[:, 5:5 + B].cpu().numpy(), Y)
+    assert torch.all(out[:, :5] == 7.0) and torch.all(out[:, 5 + B:] == 7.0)
+    Yh = T.apply_host(Xn)
+    assert np.array_equal(Yh, Y)
+    T.close()
+
+
+def test_errors():
+    """Status codes of the boundary: EINVAL for bad nodes / eps / shapes, ESTATE for an unbuilt direction."""
+    xc = _xc()
+    x, _ = _nodes((O.KIND_JACOBI, 0.0, 0.0), 64, 0)
+    with pytest.raises(xc.XcError, match="XC_EINVAL"):
+        xc.Transform(xc.XC_JACOBI, x[::-1].copy(), 1e-12)
+    with pytest.raises(xc.XcError, match="XC_EINVAL"):
+        xc.Transform(xc.XC_JACOBI, x, 1.5)
+    with pytest.raises(xc.XcError, match="XC_EINVAL"):
+        bad = x.copy()
+        bad[3] = np.nan
+        xc.Transform(xc.XC_JACOBI, bad, 1e-12)
+    with pytest.raises(xc.XcError, match="XC_EINVAL"):
+        xc.Transform(xc.XC_LAGUERRE, x, 1e-12)          # negative nodes
+    T = xc.Transform(xc.XC_JACOBI, x, 1e-12)
+    with pytest.raises(xc.XcError, match="XC_ESTATE"):
+        T.apply(_gpu(np.ones((64, 2))), xc.XC_DIR_WAT)
+    with pytest.raises(xc.XcError):
+        T.apply(_gpu(np.ones((63, 2))))
+    T.close()
