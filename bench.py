@@ -1,0 +1,295 @@
+#!/usr/bin/env python
+"""bench.py -- fp64 transforms/s of the extra-component apply on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
+
+One "step" is one xc_apply of the whole hot path (SpMM on the FP64 tensor cores
+over every block + dense tail, then the per-block inverse FFTs with the fused
+W^{-1}/truncate epilogue) over one batch of B right-hand sides already resident
+in HBM.  Default workload: BASELINE.json configs[4] (c5: Legendre N = 65536,
+B = 4096 per GPU, eps = 1e-12; the config the metric's 1/2/4/8-GPU scaling is
+quoted on).  Multi-GPU: torchrun, one rank per GPU, the operator replicated and
+the RHS batch sharded with no collective on the data path (weak scaling: every
+rank applies B columns; --strong divides B by the world size).
+
+Prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2004_11610_b200 import inputs as I  # noqa: E402
+
+DMMA_PEAK_TFLOPS = 37.1   # measured: tools/fp64_peak.cu, mma.m8n8k4.f64 (profiles/fp64_peak_r01.txt)
+DFMA_PEAK_TFLOPS = 33.9   # measured: same microbenchmark, DFMA
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """nvidia-smi clock/throttle sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, device):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={device}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def _nodes(cfg, device):
+    from paper_2004_11610_b200 import xc
+    if cfg.kind == I.KIND_COS:
+        return I.cos_nodes(cfg.N, cfg.seed), None
+    x, w, wt = xc.gauss_rule(cfg.kind, cfg.N, cfg.alpha, cfg.beta, device=device)
+    return x, wt
+
+
+def cpu_oracle_rate(cfg, ncols, ndeg, threads):
+    """The oracle's dense direct product (the paper's 'direct method') on a bounded
+    sample: ncols columns x output degrees [0, ndeg); rate extrapolated per full transform."""
+    import oracle as O
+    os.environ["OMP_NUM_THREADS"] = str(threads)
+    kind = O.Kind(cfg.kind, cfg.alpha, cfg.beta)
+    if cfg.kind == I.KIND_COS:
+        x = I.cos_nodes(cfg.N, cfg.seed)
+    else:
+        x, _, _ = O.gauss_rule(kind, cfg.N)
+    X = I.config_rhs(cfg, B=max(ncols, 1))[:, :ncols]
+    t0 = time.perf_counter()
+    O.dense_apply_rows(kind, x, X, ndeg)
+    dt = time.perf_counter() - t0
+    return ncols * (ndeg / cfg.N) / dt, dt
+
+
+def run_reference(args, cfg, ws, rank):
+    """--impl reference: the CPU oracle timed on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    ncols, ndeg = 4, min(cfg.N, 4096)
+    rates = []
+    for i in range(args.warmup + args.steps):
+        r, dt = cpu_oracle_rate(cfg, ncols, ndeg, threads)
+        if i >= args.warmup:
+            rates.append(r)
+    v = float(np.median(rates))
+    sample = f"{ncols} columns x degrees [0,{ndeg}) of {cfg.N} per step (dense direct product, dd entries)"
+    line = {"impl": "reference", "metric": "fp64 transforms/s", "value": v, "unit": "transforms/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "N": cfg.N, "global_batch": cfg.B, "eps": cfg.eps},
+            "cpu_baseline": {"value": v, "unit": "transforms/s", "cores": threads, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "transforms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c5", choices=sorted(I.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--strong", action="store_true", help="divide the config's B over the ranks")
+    ap.add_argument("--batch", type=int, default=0, help="override RHS per rank")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--direction", default="", help="A or WAT (default: the config's first)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = I.CONFIGS[args.config]
+    ws, rank, local = _dist()
+
+    if args.impl == "reference":
+        run_reference(args, cfg, ws, rank)
+        return
+
+    import torch
+    from paper_2004_11610_b200 import xc
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    direction = xc.XC_DIR_WAT if (args.direction or cfg.dirs[0]) == "WAT" else xc.XC_DIR_A
+    B = args.batch or (cfg.B // ws if args.strong else cfg.B)
+    # ---- precompute (not timed in the metric) ----
+    t0 = time.perf_counter()
+    x, wt = _nodes(cfg, local)
+    t_nodes = time.perf_counter() - t0
+    dirs = xc.XC_DIR_A | (xc.XC_DIR_WAT if "WAT" in cfg.dirs else 0)
+    t0 = time.perf_counter()
+    T = xc.Transform(cfg.kind, x, cfg.eps, alpha=cfg.alpha, beta=cfg.beta, dirs=dirs, weights=wt, device=local)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    info = T.info()
+
+    # ---- inputs: seeded on the host, this rank's shard, resident in HBM ----
+    Xh = I.config_rhs(cfg, B=B)
+    if ws > 1:
+        # rank g applies its own shard: the same generator with a rank-offset seed
+        rng = np.random.default_rng(cfg.seed * 1000 + rank)
+        Xh = rng.standard_normal((cfg.N, B))
+    X = torch.from_numpy(Xh).cuda()
+    Y = torch.empty_like(X)
+    T.reserve(B)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        T.apply(X, direction, out=Y)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = Clocks(local) if rank == 0 else None
+    time.sleep(0.3 if clocks else 0)
+    T.profile(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        T.apply(X, direction, out=Y)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    prof = T.profile_read()
+    T.profile(False)
+    clk = clocks.stop() if clocks else None
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_cols = B * ws
+    value = total_cols / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (SpMM on the FP64 tensor cores) ----
+    nnz, tail, N = info["nnz"], info["tail"], info["N"]
+    spmm_flops = (4.0 * nnz + 2.0 * tail * N) * B          # algorithmic, per launch
+    spmm_ms = prof["ms_spmm"] / max(1, prof["n"])
+    fft_ms = prof["ms_fft"] / max(1, prof["n"])
+    achieved = spmm_flops / (spmm_ms / 1e3) / 1e12
+    alg_bytes = 16.0 * N * B + 20.0 * nnz + 8.0 * tail * N   # X in, Y out, operator once (SURVEY d.3)
+    peaks = _peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+
+    # ---- end to end: host buffers through xc_apply_host (copies inside the call) ----
+    e2e = None
+    if args.e2e_steps > 0:
+        Xp = torch.from_numpy(Xh).pin_memory()
+        Yp = torch.empty_like(Xp).pin_memory()
+        T.apply_host_ptr(Xp.data_ptr(), Yp.data_ptr(), B, direction, stream=stream.cuda_stream)
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            T.apply_host_ptr(Xp.data_ptr(), Yp.data_ptr(), B, direction, stream=stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / args.e2e_steps
+        if dist:
+            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": total_cols / (ems / 1e3), "unit": "transforms/s",
+               "h2d_bytes_per_step": int(Xh.nbytes) * ws, "d2h_bytes_per_step": int(Xh.nbytes) * ws,
+               "ms_per_step": ems, "api": "xc_apply_host (pinned host buffers)"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        ncols, ndeg = 16, min(cfg.N, 8192)
+        r, dt = cpu_oracle_rate(cfg, ncols, ndeg, threads)
+        cpu = {"value": r, "unit": "transforms/s", "cores": threads, "kind": "oracle",
+               "sample": f"{ncols} columns x output degrees [0,{ndeg}) of N={cfg.N}: dense direct product "
+                         f"with double-double entries ({dt:.1f} s), rate per full transform"}
+
+    if rank == 0:
+        line = {
+            "metric": "fp64 transforms/s", "value": value, "unit": "transforms/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded N(0,1) RHS, Gauss nodes computed on the GPU)",
+            "config": {"workload": cfg.name, "N": cfg.N, "B_per_gpu": B, "global_batch": total_cols,
+                       "eps": cfg.eps, "direction": "A" if direction == xc.XC_DIR_A else "WAT",
+                       "parallelism": f"rhs-shard x{ws}, operator replicated",
+                       "l2": "inputs larger than L2 (X = %.2f GB, partial sums %.2f GB)" % (
+                           Xh.nbytes / 1e9, T.workspace_bytes(B) / 1e9),
+                       "blocks": [b["L"] for b in T.blocks()], "tail": tail},
+            "hbm_gbs": alg_bytes / (ms / 1e3) / 1e9,
+            "hbm_frac": alg_bytes / (ms / 1e3) / 1e9 / hbm_peak,
+            "fp64_tflops": info["flops_per_col_A"] * B / (ms / 1e3) / 1e12,
+            "roofline": {"bound": "tensor", "kernel": "spmm_dmma (mma.m8n8k4.f64)", "achieved": achieved,
+                         "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / DMMA_PEAK_TFLOPS,
+                         "traffic": None, "peak_source": "measured DMMA microbenchmark (tools/fp64_peak.cu)",
+                         "spmm_ms": spmm_ms, "fft_ms": fft_ms, "spmm_share": spmm_ms / ms,
+                         "dmma_issue_efficiency": (4.0 * nnz + 2.0 * tail * N) / max(1.0, info["dmma_flops_per_col_A"])},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": info["launches_A" if direction == xc.XC_DIR_A else "launches_WAT"] * args.steps,
+            "clocks": clk,
+            "precompute_s": {"gauss_nodes": t_nodes, "build": t_build},
+            "nnz": nnz,
+        }
+        print(json.dumps(line), flush=True)
+    T.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -80,6 +80,8 @@ typedef struct {
   double flops_per_col_WAT;
   double dmma_flops_per_col_A;   /* flops the tensor-core (DMMA) tiles actually issue         */
   double dmma_flops_per_col_WAT;
+  int launches_A;          /* kernel launches per xc_apply(XC_DIR_A)                         */
+  int launches_WAT;        /* kernel launches per xc_apply(XC_DIR_WAT)                       */
 } xc_info_t;
 
 typedef struct {
@@ -141,6 +143,17 @@ xc_status xc_node_spectrum(xc_handle h, int block, int64_t k, double* re, double
  * weights times e^{x} for XC_LAGUERRE (= 1/sum_j l_j(x)^2), else a copy of weights. */
 xc_status xc_gauss_rule(xc_kind kind, double alpha, double beta, int64_t N, double* nodes,
                         double* weights, double* wt, int device);
+
+/* Per-phase timing of xc_apply: when enabled, each xc_apply records CUDA events on
+ * its own stream at the phase boundaries (no host synchronisation inside the call;
+ * a ring of 512 event sets is recycled).  enable != 0 turns it on, 0 off. */
+xc_status xc_profile_enable(xc_handle h, int enable);
+
+/* Waits for all recorded events, returns the summed milliseconds of the SpMM launch
+ * (FP64 tensor cores), of the FFT launches, of the reduction/tail launch and of the
+ * whole apply, plus the number of applies recorded; then resets the sums. */
+xc_status xc_profile_read(xc_handle h, double* ms_spmm, double* ms_fft, double* ms_reduce, double* ms_total,
+                          int64_t* n_applies);
 
 /* Host-only planning (no GPU needed): zeta(eps1), the block chain and
  * FFT lengths (R-2, R-8, R-9).  Arrays L, m_off, keep_lo, keep_hi have room for

@@ -171,6 +171,17 @@ def dense_apply(kind: Kind, nodes: np.ndarray, X: np.ndarray) -> np.ndarray:
     return Y
 
 
+def dense_apply_rows(kind: Kind, nodes: np.ndarray, X: np.ndarray, ndeg: int) -> np.ndarray:
+    """Rows [0, ndeg) of Y = A X (a row sample of the dense product; same arithmetic)."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    N, B = X.shape
+    Y = np.empty((ndeg, B), dtype=np.float64)
+    x = np.ascontiguousarray(nodes, dtype=np.float64)
+    rc = _lib().orc_dense_apply(kind.kind, kind.alpha, kind.beta, 1, _p(x), N, ndeg, _p(X), B, _p(Y))
+    assert rc == 0
+    return Y
+
+
 def dense_apply_t(kind: Kind, nodes: np.ndarray, C: np.ndarray) -> np.ndarray:
     """Y[k,b] = sum_j phi_j(x_k) C[j,b] (Y = A^T C; output indexed by node)."""
     C = np.ascontiguousarray(C, dtype=np.float64)

@@ -99,6 +99,14 @@ struct xc_op {
   DevBuf partA, partW, scratch, zpl, Xh, Yh;
   std::vector<int64_t> zoff;  // per block offset (doubles) of its z' planes in zpl
   xc_info_t info{};
+  // phase profiling (ring of event sets: start, after phase 1, after phase 2, end)
+  static constexpr int kRing = 512;
+  bool prof = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> ev_dir;     // direction recorded in the slot, 0 = free
+  int64_t ev_count = 0;
+  double ms_spmm = 0, ms_fft = 0, ms_red = 0, ms_tot = 0;
+  int64_t n_prof = 0;
 };
 
 namespace {
@@ -584,6 +592,34 @@ xc_status build_impl(xc_kind kind, const xc_params* prm, const double* nodes, in
   in.dmma_flops_per_col_WAT = 64.0 * (h->tilesW_n / 32);
   in.op_bytes_A = h->tilesA_n * 8 + (int64_t)h->nitemsA * sizeof(SpmmItem);
   in.op_bytes_WAT = h->tilesW_n * 8 + (int64_t)h->nitemsW * sizeof(SpmmItem);
+  int fl = 0;
+  for (auto& b : h->blocks) fl += (b.fft.L2 > 1) ? 2 : 1;
+  auto spmm_launches = [](int n) { return n <= 0 ? 0 : (n + 4 * 65535 - 1) / (4 * 65535); };
+  in.launches_A = (h->dirs & XC_DIR_A) ? spmm_launches(h->nitemsA) + fl + (h->tail > 0 ? 1 : 0) : 0;
+  in.launches_WAT = (h->dirs & XC_DIR_WAT) ? spmm_launches(h->nitemsW) + fl + 1 : 0;
+  return XC_OK;
+}
+
+xc_status prof_harvest(xc_op* h, int slot) {
+  if (h->ev_dir[slot] == 0) return XC_OK;
+  cudaEvent_t* e = &h->ev[4 * slot];
+  XC_CUDA(cudaEventSynchronize(e[3]));
+  float t01, t12, t23, t03;
+  XC_CUDA(cudaEventElapsedTime(&t01, e[0], e[1]));
+  XC_CUDA(cudaEventElapsedTime(&t12, e[1], e[2]));
+  XC_CUDA(cudaEventElapsedTime(&t23, e[2], e[3]));
+  XC_CUDA(cudaEventElapsedTime(&t03, e[0], e[3]));
+  if (h->ev_dir[slot] == XC_DIR_A) {
+    h->ms_spmm += t01;
+    h->ms_fft += t12;
+  } else {
+    h->ms_fft += t01;
+    h->ms_spmm += t12;
+  }
+  h->ms_red += t23;
+  h->ms_tot += t03;
+  h->n_prof++;
+  h->ev_dir[slot] = 0;
   return XC_OK;
 }
 
@@ -602,8 +638,20 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
     return XC_ESTATE;
   }
   XC_TRY(ensure_ws(h, B));
+  cudaEvent_t* ev = nullptr;
+  if (h->prof) {
+    int slot = (int)(h->ev_count++ % xc_op::kRing);
+    XC_TRY(prof_harvest(h, slot));
+    ev = &h->ev[4 * slot];
+    h->ev_dir[slot] = dir;
+  }
+  auto mark = [&](int i) -> xc_status {
+    if (ev) XC_CUDA(cudaEventRecord(ev[i], st));
+    return XC_OK;
+  };
   const int64_t Bp = pad_cols(B);
   const int N = (int)h->N;
+  XC_TRY(mark(0));
   if (dir == XC_DIR_A) {
     SpmmSrcs s{};
     s.re[0] = X;
@@ -612,6 +660,7 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
     s.ld[0] = ldx;
     XC_TRY(spmm_run((const SpmmItem*)h->itemsA.p, h->nitemsA, (const double*)h->tilesA.p, s,
                     (double*)h->partA.p, Bp, (int)B, st));
+    XC_TRY(mark(1));
     for (auto& b : h->blocks) {
       FftIO io{};
       io.part = (const double*)h->partA.p;
@@ -627,10 +676,11 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
       io.m_off = b.m_off;
       XC_TRY(fft_run(b.fft, +1, PRO_UPART, EPI_YREAL, io, (int)B, (double2*)h->scratch.p, st));
     }
+    XC_TRY(mark(2));
     if (h->tail > 0)
       XC_TRY(reduce_rows8((const double*)h->partA.p, Bp, (const int64_t*)h->tail_base.p, (const int*)h->tail_nch.p,
                           h->tail, nullptr, Y, ldy, (int)B, st));
-    return XC_OK;
+    return mark(3);
   }
   // XC_DIR_WAT
   SpmmSrcs s{};
@@ -661,13 +711,18 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
   s.im[nb] = nullptr;
   s.nrows[nb] = h->tail;
   s.ld[nb] = ldx;
+  XC_TRY(mark(1));
   XC_TRY(spmm_run((const SpmmItem*)h->itemsW.p, h->nitemsW, (const double*)h->tilesW.p, s, (double*)h->partW.p,
                   Bp, (int)B, st));
-  return reduce_rows8((const double*)h->partW.p, Bp, (const int64_t*)h->nodeg_base.p, (const int*)h->nodeg_nch.p, N,
-                      (const double*)h->wt.p, Y, ldy, (int)B, st);
+  XC_TRY(mark(2));
+  XC_TRY(reduce_rows8((const double*)h->partW.p, Bp, (const int64_t*)h->nodeg_base.p, (const int*)h->nodeg_nch.p, N,
+                      (const double*)h->wt.p, Y, ldy, (int)B, st));
+  return mark(3);
 }
 
 void destroy_impl(xc_op* h) {
+  for (auto& e : h->ev) cudaEventDestroy(e);
+  h->ev.clear();
   for (auto& b : h->blocks) {
     fft_plan_free(b.fft);
     dev_free(b.w); dev_free(b.yscale); dev_free(b.winv);
@@ -815,6 +870,33 @@ xc_status xc_gauss_rule(xc_kind kind, double alpha, double beta, int64_t N, doub
   if (s != XC_OK) return s;
   if (weights) memcpy(weights, w.data(), N * sizeof(double));
   if (wt) memcpy(wt, t.data(), N * sizeof(double));
+  return XC_OK;
+}
+
+xc_status xc_profile_enable(xc_handle h, int enable) {
+  if (!h) return XC_EINVAL;
+  XC_CUDA(cudaSetDevice(h->device));
+  if (enable && h->ev.empty()) {
+    h->ev.resize(4 * xc_op::kRing);
+    h->ev_dir.assign(xc_op::kRing, 0);
+    for (auto& e : h->ev) XC_CUDA(cudaEventCreate(&e));
+  }
+  h->prof = enable != 0;
+  return XC_OK;
+}
+
+xc_status xc_profile_read(xc_handle h, double* ms_spmm, double* ms_fft, double* ms_reduce, double* ms_total,
+                          int64_t* n) {
+  if (!h) return XC_EINVAL;
+  XC_CUDA(cudaSetDevice(h->device));
+  for (int slot = 0; slot < (int)h->ev_dir.size(); ++slot) XC_TRY(prof_harvest(h, slot));
+  if (ms_spmm) *ms_spmm = h->ms_spmm;
+  if (ms_fft) *ms_fft = h->ms_fft;
+  if (ms_reduce) *ms_reduce = h->ms_red;
+  if (ms_total) *ms_total = h->ms_tot;
+  if (n) *n = h->n_prof;
+  h->ms_spmm = h->ms_fft = h->ms_red = h->ms_tot = 0;
+  h->n_prof = 0;
   return XC_OK;
 }
 

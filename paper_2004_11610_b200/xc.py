@@ -35,7 +35,8 @@ class XcInfo(ctypes.Structure):
                 ("eps2", ctypes.c_double), ("n_blocks", ctypes.c_int), ("tail", ctypes.c_int),
                 ("dirs", ctypes.c_int), ("nnz", _i64), ("op_bytes_A", _i64), ("op_bytes_WAT", _i64),
                 ("flops_per_col_A", ctypes.c_double), ("flops_per_col_WAT", ctypes.c_double),
-                ("dmma_flops_per_col_A", ctypes.c_double), ("dmma_flops_per_col_WAT", ctypes.c_double)]
+                ("dmma_flops_per_col_A", ctypes.c_double), ("dmma_flops_per_col_WAT", ctypes.c_double),
+                ("launches_A", ctypes.c_int), ("launches_WAT", ctypes.c_int)]
 
 
 class XcBlockInfo(ctypes.Structure):
@@ -45,7 +46,8 @@ class XcBlockInfo(ctypes.Structure):
 
 EXPORTS = ["xc_params_default", "xc_build_compressed", "xc_apply", "xc_apply_host", "xc_reserve",
            "xc_workspace_query", "xc_info", "xc_block_info", "xc_block_window", "xc_node_spectrum",
-           "xc_gauss_rule", "xc_plan_chain", "xc_destroy", "xc_last_error", "xc_version"]
+           "xc_gauss_rule", "xc_plan_chain", "xc_profile_enable", "xc_profile_read", "xc_destroy",
+           "xc_last_error", "xc_version"]
 
 _lib = None
 
@@ -79,6 +81,8 @@ def load():
     ip = ctypes.POINTER(ctypes.c_int)
     lib.xc_plan_chain.argtypes = [ctypes.c_int, _i64, ctypes.c_double, ctypes.c_double, ctypes.c_int, _dp, ip,
                                   ip, ip, ip, ip, ctypes.c_int, ip]
+    lib.xc_profile_enable.argtypes = [vp, ctypes.c_int]
+    lib.xc_profile_read.argtypes = [vp, _dp, _dp, _dp, _dp, ctypes.POINTER(_i64)]
     lib.xc_destroy.argtypes = [vp]
     lib.xc_destroy.restype = None
     lib.xc_last_error.restype = ctypes.c_char_p
@@ -180,6 +184,16 @@ class Transform:
     def apply_host_ptr(self, x_ptr: int, y_ptr: int, B: int, direction: int = XC_DIR_A, stream=None):
         _check(self._lib.xc_apply_host(self._h, direction, ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr), B,
                                        ctypes.c_void_p(stream or 0)))
+
+    def profile(self, enable: bool = True):
+        _check(self._lib.xc_profile_enable(self._h, 1 if enable else 0))
+
+    def profile_read(self) -> dict:
+        v = [ctypes.c_double() for _ in range(4)]
+        n = _i64()
+        _check(self._lib.xc_profile_read(self._h, *[ctypes.byref(a) for a in v], ctypes.byref(n)))
+        return {"ms_spmm": v[0].value, "ms_fft": v[1].value, "ms_reduce": v[2].value, "ms_total": v[3].value,
+                "n": n.value}
 
     def reserve(self, B: int):
         _check(self._lib.xc_reserve(self._h, B))
