@@ -146,23 +146,22 @@ struct PassArgs {
 };
 
 template <int PRO>
-__device__ __forceinline__ double2 pro_load(const FftIO& io, int L, int n, int col) {
+__device__ __forceinline__ double2 pro_load(const FftIO& io, int n, int col) {
   if (PRO == PRO_PLAIN) {
     return io.src[(int64_t)n * io.lds + col];
-  } else if (PRO == PRO_UPART) {
-    // u[q] = sum of the partial sums of group q/4; Hermitian extension for n > L/2
-    int q = (n <= L / 2) ? n : L - n;
-    int g = q >> 2;
-    int r = 2 * (q & 3);
-    int nch = io.grp_nch[g];
-    int64_t row = io.grp_base[g] + r;
-    double re = 0.0, im = 0.0;
-    for (int c = 0; c < nch; ++c) {
-      re += io.part[row * io.ldp + col];
-      im += io.part[(row + 1) * io.ldp + col];
-      row += 8;
-    }
-    return make_double2(re, (n <= L / 2) ? im : -im);
+  } else if (PRO == PRO_C2R) {
+    // Real-output inverse DFT of length L = 2M from the half spectrum U[0..M]:
+    // Z[n] = (U[n] + conj U[M-n]) + i e^{2 pi i n/L} (U[n] - conj U[M-n]), n < M; then
+    // z = IDFT_M(Z) gives v[2k] = Re z[k], v[2k+1] = Im z[k].
+    const int nm = io.M - n;
+    const double* ur = io.U + col;
+    double ar = ur[(int64_t)(2 * n) * io.ldu], ai = ur[(int64_t)(2 * n + 1) * io.ldu];
+    double br = ur[(int64_t)(2 * nm) * io.ldu], bi = ur[(int64_t)(2 * nm + 1) * io.ldu];
+    double2 w = io.twh[n];
+    double evr = ar + br, evi = ai - bi;          // U[n] + conj U[M-n]
+    double dr = ar - br, di = ai + bi;            // U[n] - conj U[M-n]
+    double odr = dr * w.x - di * w.y, odi = dr * w.y + di * w.x;
+    return make_double2(evr - odi, evi + odr);    // Ev + i Od
   } else {  // PRO_XREAL: pad + W^{-1} (Fe1 / Fe3)
     if (n >= io.keep_lo && n < io.keep_hi)
       return make_double2(io.X[(int64_t)(n + io.m_off) * io.ldx + col] * io.winv[n], 0.0);
@@ -174,9 +173,12 @@ template <int EPI>
 __device__ __forceinline__ void epi_store(const FftIO& io, int k, int col, double2 v) {
   if (EPI == EPI_PLAIN) {
     if (k < io.kmax) io.dst[(int64_t)k * io.ldd + col] = c_scale(v, io.scale);
-  } else if (EPI == EPI_YREAL) {
-    // Fe2 discard + W^{-1} (Alg. 2 step 2.1-2.2)
-    if (k >= io.keep_lo && k < io.keep_hi) io.Y[(int64_t)(k + io.m_off) * io.ldy + col] = v.x * io.yscale[k];
+  } else if (EPI == EPI_C2R) {
+    // Fe2 discard + W^{-1} (Alg. 2 step 2.1-2.2): positions 2k and 2k+1
+    int p = 2 * k;
+    if (p >= io.keep_lo && p < io.keep_hi) io.Y[(int64_t)(p + io.m_off) * io.ldy + col] = v.x * io.yscale[p];
+    if (p + 1 >= io.keep_lo && p + 1 < io.keep_hi)
+      io.Y[(int64_t)(p + 1 + io.m_off) * io.ldy + col] = v.y * io.yscale[p + 1];
   } else {
     if (k < io.H) {
       io.zre[(int64_t)k * io.ldz + col] = v.x * io.scale;
@@ -194,20 +196,32 @@ __global__ void __launch_bounds__(256) fft_pass(PassArgs a, FftIO io) {
   const int tid = threadIdx.x, nth = blockDim.x;
   const int sub0 = blockIdx.y * a.sc, col0 = blockIdx.x * a.cb;
 
-  // ---- load (prologue) ----
-  for (int i = tid; i < a.R * nseq; i += nth) {
-    int e = i / nseq, sq = i - e * nseq;
-    int sub = sub0 + sq / a.cb, col = col0 + sq % a.cb;
-    double2 v = make_double2(0.0, 0.0);
-    if (sub < a.S && col < a.ncol) {
-      if (a.stage == 1) {
-        v = a.scratch[((int64_t)sub * a.L2 + e) * a.ncol + col];
-      } else {
-        int n = (a.stage == 0) ? a.L2 * e + sub : e;
-        v = pro_load<PRO>(io, a.L, n, col);
+  // ---- load (prologue): 4 independent global loads in flight per thread ----
+  const int total = a.R * nseq;
+  for (int base = tid; base < total; base += 4 * nth) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int i = base + u * nth;
+      v[u] = make_double2(0.0, 0.0);
+      if (i < total) {
+        int e = i / nseq, sq = i - e * nseq;
+        int sub = sub0 + sq / a.cb, col = col0 + sq % a.cb;
+        if (sub < a.S && col < a.ncol) {
+          if (a.stage == 1) {
+            v[u] = a.scratch[((int64_t)sub * a.L2 + e) * a.ncol + col];
+          } else {
+            int n = (a.stage == 0) ? a.L2 * e + sub : e;
+            v[u] = pro_load<PRO>(io, n, col);
+          }
+        }
       }
     }
-    bin[e * nseq + sq] = v;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int i = base + u * nth;
+      if (i < total) bin[i] = v[u];
+    }
   }
   __syncthreads();
 
@@ -230,11 +244,11 @@ __global__ void __launch_bounds__(256) fft_pass(PassArgs a, FftIO io) {
   }
 
   // ---- store (epilogue) ----
-  for (int i = tid; i < a.R * nseq; i += nth) {
+  for (int i = tid; i < total; i += nth) {
     int e = i / nseq, sq = i - e * nseq;
     int sub = sub0 + sq / a.cb, col = col0 + sq % a.cb;
     if (sub >= a.S || col >= a.ncol) continue;
-    double2 v = bin[e * nseq + sq];
+    double2 v = bin[i];
     if (a.stage == 0) {
       // four-step twiddle w_L^{sigma n2 k1}: n2 = sub, k1 = e
       int idx = (int)(((int64_t)sub * e) % a.L);
@@ -275,7 +289,7 @@ xc_status launch_pass(const PassArgs& a, const FftIO& io, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     XC_CUDA(cudaFuncSetAttribute(fft_pass<PRO, EPI, SIG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 96 * 1024));
+                                 120 * 1024));
     attr_set = true;
   }
   dim3 grid((a.ncol + a.cb - 1) / a.cb, (a.S + a.sc - 1) / a.sc);
@@ -291,24 +305,24 @@ xc_status dispatch(FftPro pro, FftEpi epi, const PassArgs& a, const FftIO& io, c
   // pass-1-of-2 uses only the prologue, pass-2-of-2 only the epilogue
   if (a.stage == 0) {
     if (pro == PRO_PLAIN) return launch_pass<PRO_PLAIN, EPI_PLAIN, SIG>(a, io, st);
-    if (pro == PRO_UPART) return launch_pass<PRO_UPART, EPI_PLAIN, SIG>(a, io, st);
+    if (pro == PRO_C2R) return launch_pass<PRO_C2R, EPI_PLAIN, SIG>(a, io, st);
     return launch_pass<PRO_XREAL, EPI_PLAIN, SIG>(a, io, st);
   }
   if (a.stage == 1) {
     if (epi == EPI_PLAIN) return launch_pass<PRO_PLAIN, EPI_PLAIN, SIG>(a, io, st);
-    if (epi == EPI_YREAL) return launch_pass<PRO_PLAIN, EPI_YREAL, SIG>(a, io, st);
+    if (epi == EPI_C2R) return launch_pass<PRO_PLAIN, EPI_C2R, SIG>(a, io, st);
     return launch_pass<PRO_PLAIN, EPI_ZPLANES, SIG>(a, io, st);
   }
 #define XC_CASE(P, E) \
   if (pro == P && epi == E) return launch_pass<P, E, SIG>(a, io, st);
   XC_CASE(PRO_PLAIN, EPI_PLAIN)
-  XC_CASE(PRO_PLAIN, EPI_YREAL)
+  XC_CASE(PRO_PLAIN, EPI_C2R)
   XC_CASE(PRO_PLAIN, EPI_ZPLANES)
-  XC_CASE(PRO_UPART, EPI_PLAIN)
-  XC_CASE(PRO_UPART, EPI_YREAL)
-  XC_CASE(PRO_UPART, EPI_ZPLANES)
+  XC_CASE(PRO_C2R, EPI_PLAIN)
+  XC_CASE(PRO_C2R, EPI_C2R)
+  XC_CASE(PRO_C2R, EPI_ZPLANES)
   XC_CASE(PRO_XREAL, EPI_PLAIN)
-  XC_CASE(PRO_XREAL, EPI_YREAL)
+  XC_CASE(PRO_XREAL, EPI_C2R)
   XC_CASE(PRO_XREAL, EPI_ZPLANES)
 #undef XC_CASE
   xc_set_error("fft: bad prologue/epilogue");
@@ -316,10 +330,11 @@ xc_status dispatch(FftPro pro, FftEpi epi, const PassArgs& a, const FftIO& io, c
 }
 
 void choose_tile(int R, int ncol, int& cb, int& sc) {
+  // ping-pong smem = 32 R nseq bytes <= 112 KB (two CTAs per SM)
   int nseq = 1;
-  while (nseq * 2 * R <= 2048 && nseq < 16) nseq *= 2;
+  while (nseq < 16 && 2 * nseq * R <= 3584) nseq *= 2;
   cb = 1;
-  while (cb < nseq && cb < ncol && cb < 8) cb *= 2;
+  while (cb < nseq && cb < ncol) cb *= 2;
   sc = nseq / cb;
 }
 
@@ -327,7 +342,7 @@ void choose_tile(int R, int ncol, int& cb, int& sc) {
 
 xc_status fft_plan_make(FftPlan& p, int L) {
   p.L = L;
-  if (L <= 1024) {
+  if (L <= 512) {
     p.L1 = L;
     p.L2 = 1;
   } else {
@@ -383,12 +398,6 @@ xc_status fft_run(const FftPlan& p, int sigma, FftPro pro, FftEpi epi, const Fft
     a.S = 1;
     choose_tile(a.R, ncol, a.cb, a.sc);
     a.sc = 1;  // single pass: one sub-sequence per column
-    {
-      int nseq = 1;
-      while (nseq * 2 * a.R <= 2048 && nseq < 16) nseq *= 2;
-      a.cb = std::min(nseq, 8);
-      while (a.cb > 1 && a.cb / 2 >= ncol) a.cb /= 2;
-    }
     return sigma > 0 ? dispatch<1>(pro, epi, a, io, st) : dispatch<-1>(pro, epi, a, io, st);
   }
   if (!scratch) {

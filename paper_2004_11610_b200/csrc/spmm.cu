@@ -10,9 +10,10 @@
 // One warp computes D = A * Bm for 8*NT right-hand sides with DMMA
 // (mma.sync.m8n8k4.f64: 37 TF/s measured on B200 vs 34 TF/s for DFMA):
 //   A fragment  : lane holds A[lane/4][lane%4]     (one coalesced 256 B load/step)
-//   B fragment  : lane holds Bm[lane%4][col], col = lane/4 -> RHS tile + (lane/4)*NT + nt
-//   D fragment  : lane holds D[lane/4][2(lane%4)+i] -> RHS tile + (2(lane%4)+i)*NT + nt,
-//                 i.e. 2*NT contiguous doubles per lane on store.
+//   B fragment  : lane holds Bm[lane%4][n], n = lane/4; for DMMA nt the column n is
+//                 RHS tile + 16*(nt/2) + 2n + (nt&1): each 16-byte load covers a 128-byte
+//                 contiguous run of a row across 8 lanes (coalesced);
+//   D fragment  : lane holds D[lane/4][2(lane%4)+i] -> 32 contiguous bytes per nt pair.
 // Partial sums of items that split one output group are reduced in fixed order by
 // the consumer (FFT prologue / reduce_rows8), so results are deterministic.
 #include <algorithm>
@@ -39,7 +40,6 @@ __global__ void __launch_bounds__(WPC * 32) spmm_dmma(const SpmmItem* __restrict
   const SpmmItem it = items[it_idx];
   const int t = lane & 3, g = lane >> 2;
   const int tile0 = blockIdx.x * (8 * NT);
-  const int bcol = tile0 + g * NT;  // this lane's B-fragment columns [bcol, bcol+NT)
 
   const double* re = srcs.re[it.src];
   const double* im = srcs.im[it.src];
@@ -47,11 +47,16 @@ __global__ void __launch_bounds__(WPC * 32) spmm_dmma(const SpmmItem* __restrict
   const int64_t ld = srcs.ld[it.src];
   const bool planes = (im != nullptr);
   const bool full = (tile0 + 8 * NT <= ncols);
+  const bool vec_ok = ((ld & 1) == 0) && ((((uintptr_t)re) & 15) == 0) && (!planes || (((uintptr_t)im) & 15) == 0);
 
   double acc[NT][2];
 #pragma unroll
   for (int i = 0; i < NT; ++i) acc[i][0] = acc[i][1] = 0.0;
 
+  // RHS of B-fragment column n for DMMA nt: tile0 + 16*(nt/2) + 2n + (nt&1)  (NT >= 2)
+  //                                         tile0 + n                     (NT == 1)
+  // so one 16-byte load per lane per nt pair covers 128 contiguous bytes per row.
+  const int bcol = (NT == 1) ? tile0 + g : tile0 + 2 * g;
   const double* a_ptr = tiles + it.a_off + lane;
   double a_cur = (it.nsteps > 0) ? __ldg(a_ptr) : 0.0;
   double b_cur[NT];
@@ -62,21 +67,22 @@ __global__ void __launch_bounds__(WPC * 32) spmm_dmma(const SpmmItem* __restrict
     const double* src = (planes && (r & 1)) ? im : re;
     if (row < nrows) {
       const double* p = src + (int64_t)row * ld + bcol;
-      if (full) {
-        if ((NT % 2 == 0) && ((ld & 1) == 0) && ((((uintptr_t)p) & 15) == 0)) {
+      if (NT == 1) {
+        bv[0] = (bcol < ncols) ? __ldg(p) : 0.0;
+      } else if (full && vec_ok) {
 #pragma unroll
-          for (int i = 0; i < NT; i += 2) {
-            double2 v = __ldg(reinterpret_cast<const double2*>(p + i));
-            bv[i] = v.x;
-            bv[i + 1] = v.y;
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < NT; ++i) bv[i] = __ldg(p + i);
+        for (int m = 0; m < NT / 2; ++m) {
+          double2 v = __ldg(reinterpret_cast<const double2*>(p + 16 * m));
+          bv[2 * m] = v.x;
+          bv[2 * m + 1] = v.y;
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < NT; ++i) bv[i] = (bcol + i < ncols) ? __ldg(p + i) : 0.0;
+        for (int m = 0; m < NT / 2; ++m) {
+          int c = bcol + 16 * m;
+          bv[2 * m] = (c < ncols) ? __ldg(p + 16 * m) : 0.0;
+          bv[2 * m + 1] = (c + 1 < ncols) ? __ldg(p + 16 * m + 1) : 0.0;
+        }
       }
     } else {
 #pragma unroll
@@ -102,13 +108,25 @@ __global__ void __launch_bounds__(WPC * 32) spmm_dmma(const SpmmItem* __restrict
     }
   }
 
-  // D[g][2t+i] -> RHS tile0 + (2t+i)*NT + nt: lane writes 2*NT contiguous doubles
-  double* out = part + (it.out_row + g) * ldp + tile0 + 2 * t * NT;
-  const int cstart = tile0 + 2 * t * NT;
+  // D[g][2t+i] of DMMA nt -> RHS tile0 + 16*(nt/2) + 4t + 2i + (nt&1): 32 contiguous bytes per
+  // lane per nt pair (NT == 1: RHS tile0 + 2t + i).
+  double* orow = part + (it.out_row + g) * ldp;
+  if (NT == 1) {
+    int c = tile0 + 2 * t;
+    if (c + 1 < ldp) {
+      *reinterpret_cast<double2*>(orow + c) = make_double2(acc[0][0], acc[0][1]);
+    } else if (c < ldp) {
+      orow[c] = acc[0][0];
+    }
+  } else {
 #pragma unroll
-  for (int i = 0; i < NT; ++i) {
-    if (cstart + i < ldp) out[i] = acc[i][0];
-    if (cstart + NT + i < ldp) out[NT + i] = acc[i][1];
+    for (int m = 0; m < NT / 2; ++m) {
+      int c = tile0 + 16 * m + 4 * t;
+      if (c + 3 < ldp) {
+        *reinterpret_cast<double2*>(orow + c) = make_double2(acc[2 * m][0], acc[2 * m + 1][0]);
+        *reinterpret_cast<double2*>(orow + c + 2) = make_double2(acc[2 * m][1], acc[2 * m + 1][1]);
+      }
+    }
   }
 }
 

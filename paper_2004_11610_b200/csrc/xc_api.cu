@@ -49,12 +49,17 @@ void dev_free(DevBuf& b) {
 
 namespace {
 
-constexpr int KC = 256;  // node chunk of an output-axis item (multiple of 4)
+constexpr int KC = 256;      // node chunk of a split output-axis item (multiple of 4)
+constexpr int KSPLIT = 1024; // blocks whose bin groups span more nodes than this are split
 constexpr int QC = 256;  // bin chunk of an input-axis item (multiple of 2)
 
 struct BlockData {
   int L = 0, H = 0, m_off = 0, keep_lo = 0, keep_hi = 0;
-  FftPlan fft;
+  FftPlan fft;   // length L: precompute (forward) and the input-axis prologue
+  FftPlan fftM;  // length M = L/2: output-axis real-output inverse (C2R)
+  DevBuf twh;    // e^{+2 pi i n / L}, n < M
+  bool split = false;
+  int64_t ubase = 0;  // first U row of the block in the output-axis partial array
   std::vector<double> h_w;
   DevBuf w, yscale, winv;
   std::vector<int> h_start, h_len;
@@ -120,8 +125,10 @@ xc_status ensure_ws(xc_op* h, int64_t B) {
   if (B <= h->ws_B) return XC_OK;
   int64_t Bp = pad_cols(B);
   size_t scratch_n = 0;
-  for (auto& b : h->blocks)
-    if (b.fft.L2 > 1) scratch_n = std::max(scratch_n, (size_t)b.L * (size_t)B);
+  for (auto& b : h->blocks) {
+    if ((h->dirs & XC_DIR_WAT) && b.fft.L2 > 1) scratch_n = std::max(scratch_n, (size_t)b.L * (size_t)B);
+    if ((h->dirs & XC_DIR_A) && b.fftM.L2 > 1) scratch_n = std::max(scratch_n, (size_t)b.fftM.L * (size_t)B);
+  }
   XC_TRY(dev_alloc(h->scratch, std::max<size_t>(1, scratch_n) * sizeof(double2)));
   if (h->dirs & XC_DIR_A) XC_TRY(dev_alloc(h->partA, (size_t)h->rowsA * Bp * sizeof(double)));
   if (h->dirs & XC_DIR_WAT) {
@@ -166,6 +173,16 @@ xc_status build_block(xc_op* h, BlockData& b, const std::vector<double2>& jtab, 
   const int N = (int)h->N;
   b.H = b.L / 2 + 1;
   XC_TRY(fft_plan_make(b.fft, b.L));
+  XC_TRY(fft_plan_make(b.fftM, b.L / 2));
+  {
+    std::vector<double2> tw(b.L / 2);
+    const long double PI2 = 6.283185307179586476925286766559005768L;
+    for (int n = 0; n < b.L / 2; ++n) {
+      long double a = PI2 * (long double)n / (long double)b.L;
+      tw[n] = make_double2((double)cosl(a), (double)sinl(a));
+    }
+    XC_TRY(upload(b.twh, tw));
+  }
   kaiser_window(h->zeta, b.L, b.h_w);
   std::vector<double> ys(b.L), wi(b.L);
   const double isL = 1.0 / sqrt((double)b.L);
@@ -265,12 +282,18 @@ xc_status build_block(xc_op* h, BlockData& b, const std::vector<double2>& jtab, 
 }
 
 // --- output-axis items and tiles ---------------------------------------------------------
+// Per block, bin group g = bins [4g, 4g+4) owns U rows ubase + 8g + 2(q%4) + comp, i.e. the
+// half spectrum u_q = (U[ubase + 2q], U[ubase + 2q + 1]).  Blocks whose groups span few nodes
+// (the large-L blocks) get one item per group writing its U rows directly; blocks whose
+// groups span many nodes (small L: ~18N nonzeros over few bins) are split into node chunks
+// whose partial sums are reduced into U in fixed order (deterministic split-K).
 xc_status build_output_axis(xc_op* h, cudaStream_t st) {
   const int N = (int)h->N;
   const int N4 = (N + 3) / 4 * 4;
   std::vector<SpmmItem> items;
   std::vector<FillItem> fills;
   std::vector<int> fill_blk;  // block index, -1 = tail
+  std::vector<int> chunk_of;  // node chunk index (execution order)
   int64_t rows = 0, aoff = 0;
   for (size_t bi = 0; bi < h->blocks.size(); ++bi) {
     BlockData& b = h->blocks[bi];
@@ -284,14 +307,35 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
         khi[g] = std::max(khi[g], k + 1);
       }
     }
+    int maxspan = 0;
+    for (int g = 0; g < b.ngroups; ++g)
+      if (klo[g] < khi[g]) maxspan = std::max(maxspan, (khi[g] + 3) / 4 * 4 - klo[g] / 4 * 4);
+    b.split = maxspan > KSPLIT;
+    b.ubase = rows;
+    rows += 8LL * b.ngroups;
     std::vector<int64_t> gbase(b.ngroups, 0);
     std::vector<int> gnch(b.ngroups, 0);
-    std::vector<SpmmItem> bitems;
-    std::vector<FillItem> bfills;
     for (int g = 0; g < b.ngroups; ++g) {
+      int a = 0, e = 0;
+      if (klo[g] < khi[g]) {
+        a = klo[g] / 4 * 4;
+        e = (khi[g] + 3) / 4 * 4;
+      }
+      if (!b.split) {
+        SpmmItem it{};
+        it.a_off = aoff;
+        it.out_row = b.ubase + 8LL * g;
+        it.k0 = a;
+        it.nsteps = (e - a) / 4;  // 0 for an empty group: writes zeros
+        it.src = 0;
+        items.push_back(it);
+        fills.push_back(FillItem{aoff, a, it.nsteps, g, 0});
+        fill_blk.push_back((int)bi);
+        chunk_of.push_back(a / KC);
+        aoff += 32LL * it.nsteps;
+        continue;
+      }
       gbase[g] = rows;
-      if (klo[g] >= khi[g]) continue;
-      int a = klo[g] / 4 * 4, e = (khi[g] + 3) / 4 * 4;
       for (int c = a / KC; c * KC < e; ++c) {
         int k0 = std::max(a, c * KC), k1 = std::min(e, (c + 1) * KC);
         if (k1 <= k0) continue;
@@ -301,19 +345,18 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
         it.k0 = k0;
         it.nsteps = (k1 - k0) / 4;
         it.src = 0;
-        bitems.push_back(it);
-        bfills.push_back(FillItem{aoff, k0, it.nsteps, g, 0});
+        items.push_back(it);
+        fills.push_back(FillItem{aoff, k0, it.nsteps, g, 0});
+        fill_blk.push_back((int)bi);
+        chunk_of.push_back(c);
         aoff += 32LL * it.nsteps;
         rows += 8;
         gnch[g]++;
       }
     }
-    XC_TRY(upload(b.grp_base, gbase));
-    XC_TRY(upload(b.grp_nch, gnch));
-    for (size_t i = 0; i < bitems.size(); ++i) {
-      items.push_back(bitems[i]);
-      fills.push_back(bfills[i]);
-      fill_blk.push_back((int)bi);
+    if (b.split) {
+      XC_TRY(upload(b.grp_base, gbase));
+      XC_TRY(upload(b.grp_nch, gnch));
     }
   }
   // dense tail: groups of 8 degrees x node chunks
@@ -333,6 +376,7 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
       items.push_back(it);
       fills.push_back(FillItem{aoff, k0, it.nsteps, g, 0});
       fill_blk.push_back(-1);
+      chunk_of.push_back(k0 / KC);
       aoff += 32LL * it.nsteps;
       rows += 8;
       tnch[g]++;
@@ -350,26 +394,33 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
     size_t i1 = i0;
     while (i1 < fills.size() && fill_blk[i1] == fill_blk[i0]) ++i1;
     std::vector<FillItem> part(fills.begin() + i0, fills.begin() + i1);
-    XC_TRY(upload(dfill, part));
+    std::vector<FillItem> nonempty;
+    for (auto& f : part)
+      if (f.nsteps > 0) nonempty.push_back(f);
     int bi = fill_blk[i0];
-    if (bi >= 0) {
-      BlockData& b = h->blocks[bi];
-      XC_TRY(fill_tiles(FILL_OUT_CPLX, (FillItem*)dfill.p, (int)part.size(), (int*)b.start.p, (int*)b.len.p,
-                        (int64_t*)b.off.p, (double2*)b.vals.p, nullptr, 0, N, b.H, (double*)h->tilesA.p, st));
-    } else {
-      XC_TRY(fill_tiles(FILL_OUT_REAL, (FillItem*)dfill.p, (int)part.size(), nullptr, nullptr, nullptr, nullptr,
-                        (double*)h->tailP.p, h->tail, N, 0, (double*)h->tilesA.p, st));
+    if (!nonempty.empty()) {
+      XC_TRY(upload(dfill, nonempty));
+      if (bi >= 0) {
+        BlockData& b = h->blocks[bi];
+        XC_TRY(fill_tiles(FILL_OUT_CPLX, (FillItem*)dfill.p, (int)nonempty.size(), (int*)b.start.p,
+                          (int*)b.len.p, (int64_t*)b.off.p, (double2*)b.vals.p, nullptr, 0, N, b.H,
+                          (double*)h->tilesA.p, st));
+      } else {
+        XC_TRY(fill_tiles(FILL_OUT_REAL, (FillItem*)dfill.p, (int)nonempty.size(), nullptr, nullptr, nullptr,
+                          nullptr, (double*)h->tailP.p, h->tail, N, 0, (double*)h->tilesA.p, st));
+      }
+      XC_CUDA(cudaStreamSynchronize(st));
     }
-    XC_CUDA(cudaStreamSynchronize(st));
     i0 = i1;
   }
   dev_free(dfill);
-  // execution order: by (block, node chunk, group) so that a CTA's warps share X rows
+  // execution order: by (block, node chunk, group) so that a CTA's warps share X rows;
+  // longest items of a block first within equal keys is not needed (items are short).
   std::vector<size_t> ord(items.size());
   for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
   std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
     if (fill_blk[a] != fill_blk[b]) return (unsigned)fill_blk[a] < (unsigned)fill_blk[b];
-    return items[a].k0 / KC < items[b].k0 / KC;
+    return chunk_of[a] < chunk_of[b];
   });
   std::vector<SpmmItem> sorted(items.size());
   for (size_t i = 0; i < ord.size(); ++i) sorted[i] = items[ord[i]];
@@ -592,10 +643,14 @@ xc_status build_impl(xc_kind kind, const xc_params* prm, const double* nodes, in
   in.dmma_flops_per_col_WAT = 64.0 * (h->tilesW_n / 32);
   in.op_bytes_A = h->tilesA_n * 8 + (int64_t)h->nitemsA * sizeof(SpmmItem);
   in.op_bytes_WAT = h->tilesW_n * 8 + (int64_t)h->nitemsW * sizeof(SpmmItem);
-  int fl = 0;
-  for (auto& b : h->blocks) fl += (b.fft.L2 > 1) ? 2 : 1;
+  int fl = 0, flM = 0, nsplit = 0;
+  for (auto& b : h->blocks) {
+    fl += (b.fft.L2 > 1) ? 2 : 1;
+    flM += (b.fftM.L2 > 1) ? 2 : 1;
+    nsplit += b.split ? 1 : 0;
+  }
   auto spmm_launches = [](int n) { return n <= 0 ? 0 : (n + 4 * 65535 - 1) / (4 * 65535); };
-  in.launches_A = (h->dirs & XC_DIR_A) ? spmm_launches(h->nitemsA) + fl + (h->tail > 0 ? 1 : 0) : 0;
+  in.launches_A = (h->dirs & XC_DIR_A) ? spmm_launches(h->nitemsA) + nsplit + flM + (h->tail > 0 ? 1 : 0) : 0;
   in.launches_WAT = (h->dirs & XC_DIR_WAT) ? spmm_launches(h->nitemsW) + fl + 1 : 0;
   return XC_OK;
 }
@@ -662,11 +717,15 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
                     (double*)h->partA.p, Bp, (int)B, st));
     XC_TRY(mark(1));
     for (auto& b : h->blocks) {
+      double* U = (double*)h->partA.p + b.ubase * Bp;
+      if (b.split)
+        XC_TRY(reduce_rows8((const double*)h->partA.p, Bp, (const int64_t*)b.grp_base.p, (const int*)b.grp_nch.p,
+                            8 * b.ngroups, nullptr, U, Bp, (int)B, st));
       FftIO io{};
-      io.part = (const double*)h->partA.p;
-      io.ldp = Bp;
-      io.grp_base = (const int64_t*)b.grp_base.p;
-      io.grp_nch = (const int*)b.grp_nch.p;
+      io.U = U;
+      io.ldu = Bp;
+      io.twh = (const double2*)b.twh.p;
+      io.M = b.L / 2;
       io.H = b.H;
       io.Y = Y;
       io.ldy = ldy;
@@ -674,7 +733,7 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
       io.keep_lo = b.keep_lo;
       io.keep_hi = b.keep_hi;
       io.m_off = b.m_off;
-      XC_TRY(fft_run(b.fft, +1, PRO_UPART, EPI_YREAL, io, (int)B, (double2*)h->scratch.p, st));
+      XC_TRY(fft_run(b.fftM, +1, PRO_C2R, EPI_C2R, io, (int)B, (double2*)h->scratch.p, st));
     }
     XC_TRY(mark(2));
     if (h->tail > 0)
@@ -725,6 +784,8 @@ void destroy_impl(xc_op* h) {
   h->ev.clear();
   for (auto& b : h->blocks) {
     fft_plan_free(b.fft);
+    fft_plan_free(b.fftM);
+    dev_free(b.twh);
     dev_free(b.w); dev_free(b.yscale); dev_free(b.winv);
     dev_free(b.start); dev_free(b.len); dev_free(b.off); dev_free(b.vals);
     dev_free(b.grp_base); dev_free(b.grp_nch);
@@ -803,8 +864,10 @@ xc_status xc_workspace_query(xc_handle h, int64_t B, size_t* bytes) {
   if (!h || !bytes || B < 1) return XC_EINVAL;
   int64_t Bp = pad_cols(B);
   size_t s = 0, scr = 0;
-  for (auto& b : h->blocks)
-    if (b.fft.L2 > 1) scr = std::max(scr, (size_t)b.L * B * sizeof(double2));
+  for (auto& b : h->blocks) {
+    if ((h->dirs & XC_DIR_WAT) && b.fft.L2 > 1) scr = std::max(scr, (size_t)b.L * B * sizeof(double2));
+    if ((h->dirs & XC_DIR_A) && b.fftM.L2 > 1) scr = std::max(scr, (size_t)b.fftM.L * B * sizeof(double2));
+  }
   s += scr;
   if (h->dirs & XC_DIR_A) s += (size_t)h->rowsA * Bp * 8;
   if (h->dirs & XC_DIR_WAT) {
