@@ -187,6 +187,7 @@ def main():
     T.reserve(B)
     stream = torch.cuda.current_stream()
 
+    torch.cuda.nvtx.range_push("xc_apply")
     for _ in range(args.warmup):
         T.apply(X, direction, out=Y)
     torch.cuda.synchronize()
@@ -202,6 +203,7 @@ def main():
         T.apply(X, direction, out=Y)
     ev1.record(stream)
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     if dist:
         dist.barrier()
     ms = ev0.elapsed_time(ev1) / args.steps

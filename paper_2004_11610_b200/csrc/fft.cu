@@ -98,19 +98,23 @@ __device__ __forceinline__ void bfly5(double2* v) {
   v[3] = make_double2(m2.x + t2.y, m2.y - t2.x);
 }
 
-// One self-sorting Stockham radix-r stage over nseq interleaved sequences of length R
-// (smem layout [n][seq]); twiddle w_{Ns r}^{k t} from the length-R table.
+// One self-sorting Stockham radix-r stage over nseq = 2^lgn interleaved sequences of length R
+// (smem layout [n][seq]); twiddle w_{Ns r}^{k t} from the length-R table.  j / Ns by a
+// precomputed multiplier (exact for j < 2^16).
 template <int r, int SIG>
 __device__ __forceinline__ void stockham_stage(const double2* __restrict__ bin, double2* __restrict__ bout, int R,
-                                               int Ns, int nseq, const double2* __restrict__ tw, int tid, int nth) {
+                                               int Ns, unsigned magic, int lgn, const double2* __restrict__ tw,
+                                               int tid, int nth) {
   const int Rr = R / r;
   const int twstep = R / (Ns * r);
-  for (int i = tid; i < Rr * nseq; i += nth) {
-    int j = i / nseq, sq = i - j * nseq;
-    int k = j % Ns;
+  const int nseq = 1 << lgn;
+  for (int i = tid; i < (Rr << lgn); i += nth) {
+    int j = i >> lgn, sq = i & (nseq - 1);
+    int jd = (Ns == 1) ? j : (int)__umulhi((unsigned)j, magic);  // j / Ns
+    int k = j - jd * Ns;
     double2 v[r];
 #pragma unroll
-    for (int t = 0; t < r; ++t) v[t] = bin[(j + t * Rr) * nseq + sq];
+    for (int t = 0; t < r; ++t) v[t] = bin[((j + t * Rr) << lgn) + sq];
     if (k > 0) {
       double2 w = __ldg(tw + k * twstep);
       if (SIG < 0) w.y = -w.y;
@@ -126,9 +130,9 @@ __device__ __forceinline__ void stockham_stage(const double2* __restrict__ bin, 
     else if (r == 4) bfly4<SIG>(v[0], v[1], v[2], v[3]);
     else if (r == 5) bfly5<SIG>(v);
     else bfly8<SIG>(v);
-    int idxD = (j / Ns) * Ns * r + k;
+    int idxD = jd * Ns * r + k;
 #pragma unroll
-    for (int u = 0; u < r; ++u) bout[(idxD + u * Ns) * nseq + sq] = v[u];
+    for (int u = 0; u < r; ++u) bout[((idxD + u * Ns) << lgn) + sq] = v[u];
   }
 }
 
@@ -136,12 +140,15 @@ struct PassArgs {
   int R;             // sub-FFT length of this pass
   int nf;            // number of radix stages
   int f[12];         // radices
+  unsigned magic[12];// ceil(2^32 / Ns) of each stage
   const double2* tw; // e^{+2 pi i n/R}
   const double2* twL;// e^{+2 pi i n/L} (stage 0 only)
   int L, L1, L2;
   int stage;         // 0 = first of two, 1 = second of two, 2 = single
   int S;             // number of sub-sequences per column
-  int ncol, cb, sc;
+  int ncol, cb, sc;  // cb, sc powers of two (sc = 2 for the paired C2R first pass)
+  int lgcb, lgn;     // log2(cb), log2(cb * sc)
+  int pairs;         // 1: slots are the sub-sequence pair {p, (S - p) % S}, p = blockIdx.y
   double2* scratch;  // two-pass intermediate, index (k1*L2 + n2)*ncol + col
 };
 
@@ -150,18 +157,7 @@ __device__ __forceinline__ double2 pro_load(const FftIO& io, int n, int col) {
   if (PRO == PRO_PLAIN) {
     return io.src[(int64_t)n * io.lds + col];
   } else if (PRO == PRO_C2R) {
-    // Real-output inverse DFT of length L = 2M from the half spectrum U[0..M] (P:444):
-    // Z[n] = (U[n] + conj U[M-n]) + i e^{2 pi i n/L} (U[n] - conj U[M-n]), n < M; then
-    // z = IDFT_M(Z) gives v[2k] = Re z[k], v[2k+1] = Im z[k].
-    const int nm = io.M - n;
-    const double* ur = io.U + col;
-    double ar = ur[(int64_t)(2 * n) * io.ldu], ai = ur[(int64_t)(2 * n + 1) * io.ldu];
-    double br = ur[(int64_t)(2 * nm) * io.ldu], bi = ur[(int64_t)(2 * nm + 1) * io.ldu];
-    double2 w = io.twh[n];
-    double evr = ar + br, evi = ai - bi;          // U[n] + conj U[M-n]
-    double dr = ar - br, di = ai + bi;            // U[n] - conj U[M-n]
-    double odr = dr * w.x - di * w.y, odi = dr * w.y + di * w.x;
-    return make_double2(evr - odi, evi + odr);    // Ev + i Od
+    return io.Uc[(int64_t)n * io.ldu + col];   // raw half-spectrum bin, paired later in smem
   } else {  // PRO_XREAL: pad + W^{-1} (Fe1 / Fe3)
     if (n >= io.keep_lo && n < io.keep_hi)
       return make_double2(io.X[(int64_t)(n + io.m_off) * io.ldx + col] * io.winv[n], 0.0);
@@ -190,14 +186,20 @@ __device__ __forceinline__ void epi_store(const FftIO& io, int k, int col, doubl
 template <int PRO, int EPI, int SIG>
 __global__ void __launch_bounds__(256) fft_pass(PassArgs a, FftIO io) {
   extern __shared__ double2 smem[];
-  const int nseq = a.cb * a.sc;
+  const int nseq = 1 << a.lgn;
   double2* bin = smem;
   double2* bout = smem + a.R * nseq;
+  double2* nyq = smem + 2 * a.R * nseq;  // C2R: U[M] per column (cb values)
   const int tid = threadIdx.x, nth = blockDim.x;
-  const int sub0 = blockIdx.y * a.sc, col0 = blockIdx.x * a.cb;
+  const int col0 = blockIdx.x * a.cb;
+  const int p = blockIdx.y;  // pair index (pairs) or first sub-sequence / sc
+  auto sub_of = [&](int slot) -> int {
+    if (a.pairs) return slot == 0 ? p : (a.S - p) % a.S;
+    return p * a.sc + slot;
+  };
 
   // ---- load (prologue): 4 independent global loads in flight per thread ----
-  const int total = a.R * nseq;
+  const int total = a.R << a.lgn;
   for (int base = tid; base < total; base += 4 * nth) {
     double2 v[4];
 #pragma unroll
@@ -205,8 +207,8 @@ __global__ void __launch_bounds__(256) fft_pass(PassArgs a, FftIO io) {
       int i = base + u * nth;
       v[u] = make_double2(0.0, 0.0);
       if (i < total) {
-        int e = i / nseq, sq = i - e * nseq;
-        int sub = sub0 + sq / a.cb, col = col0 + sq % a.cb;
+        int e = i >> a.lgn, sq = i & (nseq - 1);
+        int sub = sub_of(sq >> a.lgcb), col = col0 + (sq & (a.cb - 1));
         if (sub < a.S && col < a.ncol) {
           if (a.stage == 1) {
             v[u] = a.scratch[((int64_t)sub * a.L2 + e) * a.ncol + col];
@@ -223,18 +225,47 @@ __global__ void __launch_bounds__(256) fft_pass(PassArgs a, FftIO io) {
       if (i < total) bin[i] = v[u];
     }
   }
+  if (PRO == PRO_C2R && a.stage != 1) {
+    if (p == 0)
+      for (int c = tid; c < a.cb; c += nth)
+        nyq[c] = (col0 + c < a.ncol) ? io.Uc[(int64_t)io.M * io.ldu + col0 + c] : make_double2(0.0, 0.0);
+    __syncthreads();
+    // Real-output inverse DFT of length L = 2M from the half spectrum U[0..M] (P:444):
+    // Z[n] = (U[n] + conj U[M-n]) + i e^{2 pi i n/L} (U[n] - conj U[M-n]); then z = IDFT_M(Z)
+    // gives v[2k] = Re z[k], v[2k+1] = Im z[k].  U[M-n] lives in the paired slot of this CTA.
+    for (int i = tid; i < total; i += nth) {
+      int e = i >> a.lgn, sq = i & (nseq - 1);
+      int slot = sq >> a.lgcb, cl = sq & (a.cb - 1);
+      int sub = sub_of(slot);
+      int n = (a.stage == 0) ? a.L2 * e + sub : e;
+      double2 u = bin[i], v;
+      if (sub == 0)
+        v = (e == 0) ? nyq[cl] : bin[((a.R - e) << a.lgn) + sq];
+      else
+        v = bin[((a.R - 1 - e) << a.lgn) + ((slot ^ 1) << a.lgcb) + cl];
+      double2 w = __ldg(io.twh + n);
+      double evr = u.x + v.x, evi = u.y - v.y;  // U[n] + conj U[M-n]
+      double dr = u.x - v.x, di = u.y + v.y;    // U[n] - conj U[M-n]
+      double odr = dr * w.x - di * w.y, odi = dr * w.y + di * w.x;
+      bout[i] = make_double2(evr - odi, evi + odr);
+    }
+    double2* t = bin;
+    bin = bout;
+    bout = t;
+  }
   __syncthreads();
 
   // ---- Stockham stages ----
   int Ns = 1;
   for (int st = 0; st < a.nf; ++st) {
     const int r = a.f[st];
+    const unsigned mg = a.magic[st];
     switch (r) {
-      case 2: stockham_stage<2, SIG>(bin, bout, a.R, Ns, nseq, a.tw, tid, nth); break;
-      case 3: stockham_stage<3, SIG>(bin, bout, a.R, Ns, nseq, a.tw, tid, nth); break;
-      case 4: stockham_stage<4, SIG>(bin, bout, a.R, Ns, nseq, a.tw, tid, nth); break;
-      case 5: stockham_stage<5, SIG>(bin, bout, a.R, Ns, nseq, a.tw, tid, nth); break;
-      default: stockham_stage<8, SIG>(bin, bout, a.R, Ns, nseq, a.tw, tid, nth); break;
+      case 2: stockham_stage<2, SIG>(bin, bout, a.R, Ns, mg, a.lgn, a.tw, tid, nth); break;
+      case 3: stockham_stage<3, SIG>(bin, bout, a.R, Ns, mg, a.lgn, a.tw, tid, nth); break;
+      case 4: stockham_stage<4, SIG>(bin, bout, a.R, Ns, mg, a.lgn, a.tw, tid, nth); break;
+      case 5: stockham_stage<5, SIG>(bin, bout, a.R, Ns, mg, a.lgn, a.tw, tid, nth); break;
+      default: stockham_stage<8, SIG>(bin, bout, a.R, Ns, mg, a.lgn, a.tw, tid, nth); break;
     }
     __syncthreads();
     double2* t = bin;
@@ -245,9 +276,11 @@ __global__ void __launch_bounds__(256) fft_pass(PassArgs a, FftIO io) {
 
   // ---- store (epilogue) ----
   for (int i = tid; i < total; i += nth) {
-    int e = i / nseq, sq = i - e * nseq;
-    int sub = sub0 + sq / a.cb, col = col0 + sq % a.cb;
+    int e = i >> a.lgn, sq = i & (nseq - 1);
+    int slot = sq >> a.lgcb;
+    int sub = sub_of(slot), col = col0 + (sq & (a.cb - 1));
     if (sub >= a.S || col >= a.ncol) continue;
+    if (a.pairs && slot == 1 && sub == sub_of(0)) continue;  // self-paired sub-sequence
     double2 v = bin[i];
     if (a.stage == 0) {
       // four-step twiddle w_L^{sigma n2 k1}: n2 = sub, k1 = e
@@ -276,7 +309,6 @@ void twiddle_table(int n, std::vector<double2>& t) {
   t.resize(n);
   const long double PI2 = 6.283185307179586476925286766559005768L;
   for (int i = 0; i < n; ++i) {
-    // exact octant symmetry keeps the table symmetric to the bit
     long double ang = PI2 * (long double)i / (long double)n;
     t[i] = make_double2((double)cosl(ang), (double)sinl(ang));
   }
@@ -284,15 +316,16 @@ void twiddle_table(int n, std::vector<double2>& t) {
 
 template <int PRO, int EPI, int SIG>
 xc_status launch_pass(const PassArgs& a, const FftIO& io, cudaStream_t st) {
-  const int nseq = a.cb * a.sc;
-  size_t sm = 2ull * a.R * nseq * sizeof(double2);
+  const int nseq = 1 << a.lgn;
+  size_t sm = 2ull * a.R * nseq * sizeof(double2) + (PRO == PRO_C2R ? a.cb * sizeof(double2) : 0);
   static bool attr_set = false;
   if (!attr_set) {
     XC_CUDA(cudaFuncSetAttribute(fft_pass<PRO, EPI, SIG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  120 * 1024));
     attr_set = true;
   }
-  dim3 grid((a.ncol + a.cb - 1) / a.cb, (a.S + a.sc - 1) / a.sc);
+  int gy = a.pairs ? a.S / 2 + 1 : (a.S + a.sc - 1) / a.sc;
+  dim3 grid((a.ncol + a.cb - 1) / a.cb, gy);
   int work = a.R * nseq / 2;
   int th = work >= 256 ? 256 : (work >= 128 ? 128 : 64);
   fft_pass<PRO, EPI, SIG><<<grid, th, sm, st>>>(a, io);
@@ -329,13 +362,29 @@ xc_status dispatch(FftPro pro, FftEpi epi, const PassArgs& a, const FftIO& io, c
   return XC_EINVAL;
 }
 
-void choose_tile(int R, int ncol, int& cb, int& sc) {
-  // ping-pong smem = 32 R nseq bytes <= 112 KB (two CTAs per SM)
-  int nseq = 1;
-  while (nseq < 16 && 2 * nseq * R <= 3584) nseq *= 2;
-  cb = 1;
-  while (cb < nseq && cb < ncol) cb *= 2;
-  sc = nseq / cb;
+int ilog2(int v) {
+  int l = 0;
+  while ((1 << (l + 1)) <= v) ++l;
+  return l;
+}
+
+// Tile: nseq = cb * sc sequences of length R in ping-pong smem of 32 R nseq bytes <= 112 KB
+// (two CTAs per SM); cb, sc powers of two.
+void choose_tile(int R, int ncol, int sc, int& cb) {
+  int nseq = sc;
+  while (nseq < 16 * sc && 2 * nseq * R <= 3584) nseq *= 2;
+  cb = nseq / sc;
+  while (cb > 1 && cb / 2 >= ncol) cb /= 2;
+}
+
+void set_stages(PassArgs& a, int nf, const int* f) {
+  a.nf = nf;
+  int Ns = 1;
+  for (int i = 0; i < nf; ++i) {
+    a.f[i] = f[i];
+    a.magic[i] = (Ns == 1) ? 0u : (unsigned)((0x100000000ULL + Ns - 1) / Ns);
+    Ns *= f[i];
+  }
 }
 
 }  // namespace
@@ -389,37 +438,55 @@ xc_status fft_run(const FftPlan& p, int sigma, FftPro pro, FftEpi epi, const Fft
   a.ncol = ncol;
   a.scratch = scratch;
   a.twL = p.twL;
+  const bool c2r = (pro == PRO_C2R);
   if (p.L2 == 1) {
     a.R = p.L1;
-    a.nf = p.nf1;
-    for (int i = 0; i < p.nf1; ++i) a.f[i] = p.f1[i];
+    set_stages(a, p.nf1, p.f1);
     a.tw = p.tw1;
     a.stage = 2;
     a.S = 1;
-    choose_tile(a.R, ncol, a.cb, a.sc);
-    a.sc = 1;  // single pass: one sub-sequence per column
+    a.sc = 1;
+    a.pairs = c2r ? 1 : 0;
+    choose_tile(a.R, ncol, 1, a.cb);
+    a.lgcb = ilog2(a.cb);
+    a.lgn = a.lgcb;
     return sigma > 0 ? dispatch<1>(pro, epi, a, io, st) : dispatch<-1>(pro, epi, a, io, st);
   }
   if (!scratch) {
     xc_set_error("fft: two-pass length needs scratch");
     return XC_EINVAL;
   }
-  // pass 1: L1-point FFTs, L2 sub-sequences per column
+  // pass 1: L1-point FFTs, L2 sub-sequences per column (paired for the C2R prologue)
   a.R = p.L1;
-  a.nf = p.nf1;
-  for (int i = 0; i < p.nf1; ++i) a.f[i] = p.f1[i];
+  set_stages(a, p.nf1, p.f1);
   a.tw = p.tw1;
   a.stage = 0;
   a.S = p.L2;
-  choose_tile(a.R, ncol, a.cb, a.sc);
+  a.sc = c2r ? 2 : 1;
+  a.pairs = c2r ? 1 : 0;
+  choose_tile(a.R, ncol, a.sc, a.cb);
+  if (!c2r) {  // spread spare sequences over sub-sequences when there are few columns
+    int nseq = a.cb;
+    while (nseq < 16 && 2 * nseq * a.R <= 3584) nseq *= 2;
+    a.sc = nseq / a.cb;
+  }
+  a.lgcb = ilog2(a.cb);
+  a.lgn = ilog2(a.cb * a.sc);
   XC_TRY(sigma > 0 ? dispatch<1>(pro, epi, a, io, st) : dispatch<-1>(pro, epi, a, io, st));
   // pass 2: L2-point FFTs, L1 sub-sequences per column
   a.R = p.L2;
-  a.nf = p.nf2;
-  for (int i = 0; i < p.nf2; ++i) a.f[i] = p.f2[i];
+  set_stages(a, p.nf2, p.f2);
   a.tw = p.tw2;
   a.stage = 1;
   a.S = p.L1;
-  choose_tile(a.R, ncol, a.cb, a.sc);
+  a.pairs = 0;
+  choose_tile(a.R, ncol, 1, a.cb);
+  {
+    int nseq = a.cb;
+    while (nseq < 16 && 2 * nseq * a.R <= 3584) nseq *= 2;
+    a.sc = nseq / a.cb;
+  }
+  a.lgcb = ilog2(a.cb);
+  a.lgn = ilog2(a.cb * a.sc);
   return sigma > 0 ? dispatch<1>(pro, epi, a, io, st) : dispatch<-1>(pro, epi, a, io, st);
 }

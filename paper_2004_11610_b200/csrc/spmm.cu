@@ -110,6 +110,39 @@ __global__ void __launch_bounds__(WPC * 32) spmm_dmma(const SpmmItem* __restrict
 
   // D[g][2t+i] of DMMA nt -> RHS tile0 + 16*(nt/2) + 4t + 2i + (nt&1): 32 contiguous bytes per
   // lane per nt pair (NT == 1: RHS tile0 + 2t + i).
+  if (it.cplx) {
+    // rows g = 2*bin + comp of 4 complex bins: store u_bin interleaved (re, im) per column in
+    // the complex row out_row/2 + bin (= double rows out_row + 2 bin, +1).  Lanes g and g^1 (lane ^ 4)
+    // trade halves so that each writes whole complex numbers.
+    const bool odd = g & 1;
+    double2* crow = reinterpret_cast<double2*>(part + (it.out_row + (g & ~1)) * ldp);
+    if (NT == 1) {
+      int c = tile0 + 2 * t;
+      double snd = odd ? acc[0][0] : acc[0][1];
+      double rcv = __shfl_xor_sync(0xffffffffu, snd, 4);
+      if (!odd) {
+        if (c < ldp) crow[c] = make_double2(acc[0][0], rcv);
+      } else {
+        if (c + 1 < ldp) crow[c + 1] = make_double2(rcv, acc[0][1]);
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < NT / 2; ++m) {
+        int c = tile0 + 16 * m + 4 * t;
+        double v0 = acc[2 * m][0], v1 = acc[2 * m + 1][0], v2 = acc[2 * m][1], v3 = acc[2 * m + 1][1];
+        double s0 = odd ? v0 : v2, s1 = odd ? v1 : v3;
+        double r0 = __shfl_xor_sync(0xffffffffu, s0, 4), r1 = __shfl_xor_sync(0xffffffffu, s1, 4);
+        if (!odd) {
+          crow[c] = make_double2(v0, r0);
+          crow[c + 1] = make_double2(v1, r1);
+        } else {
+          crow[c + 2] = make_double2(r0, v2);
+          crow[c + 3] = make_double2(r1, v3);
+        }
+      }
+    }
+    return;
+  }
   double* orow = part + (it.out_row + g) * ldp;
   if (NT == 1) {
     int c = tile0 + 2 * t;

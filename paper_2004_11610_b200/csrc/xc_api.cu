@@ -328,6 +328,7 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
         it.k0 = a;
         it.nsteps = (e - a) / 4;  // 0 for an empty group: writes zeros
         it.src = 0;
+        it.cplx = 1;
         items.push_back(it);
         fills.push_back(FillItem{aoff, a, it.nsteps, g, 0});
         fill_blk.push_back((int)bi);
@@ -345,6 +346,7 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
         it.k0 = k0;
         it.nsteps = (k1 - k0) / 4;
         it.src = 0;
+        it.cplx = 1;
         items.push_back(it);
         fills.push_back(FillItem{aoff, k0, it.nsteps, g, 0});
         fill_blk.push_back((int)bi);
@@ -419,8 +421,8 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
   std::vector<size_t> ord(items.size());
   for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
   std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
-    if (fill_blk[a] != fill_blk[b]) return (unsigned)fill_blk[a] < (unsigned)fill_blk[b];
-    return chunk_of[a] < chunk_of[b];
+    if (chunk_of[a] != chunk_of[b]) return chunk_of[a] < chunk_of[b];
+    return (unsigned)fill_blk[a] < (unsigned)fill_blk[b];
   });
   std::vector<SpmmItem> sorted(items.size());
   for (size_t i = 0; i < ord.size(); ++i) sorted[i] = items[ord[i]];
@@ -718,11 +720,11 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
     XC_TRY(mark(1));
     for (auto& b : h->blocks) {
       double* U = (double*)h->partA.p + b.ubase * Bp;
-      if (b.split)
+      if (b.split)  // interleaved complex rows: reduce all Bp doubles of each double row
         XC_TRY(reduce_rows8((const double*)h->partA.p, Bp, (const int64_t*)b.grp_base.p, (const int*)b.grp_nch.p,
-                            8 * b.ngroups, nullptr, U, Bp, (int)B, st));
+                            8 * b.ngroups, nullptr, U, Bp, (int)Bp, st));
       FftIO io{};
-      io.U = U;
+      io.Uc = reinterpret_cast<const double2*>(U);
       io.ldu = Bp;
       io.twh = (const double2*)b.twh.p;
       io.M = b.L / 2;

@@ -130,7 +130,7 @@ struct FftPlan {
 struct FftIO {
   // prologue sources
   const double2* src = nullptr; int64_t lds = 0;           // PRO_PLAIN
-  const double* U = nullptr; int64_t ldu = 0;              // PRO_C2R: half spectrum, rows 2q (re), 2q+1 (im)
+  const double2* Uc = nullptr; int64_t ldu = 0;            // PRO_C2R: half spectrum u_q at Uc[q*ldu + col], q <= M
   const double2* twh = nullptr; int M = 0;                 // PRO_C2R: e^{+2 pi i n / (2M)}, n < M
   int H = 0;
   const double* X = nullptr; int64_t ldx = 0;              // PRO_XREAL
@@ -161,7 +161,7 @@ struct SpmmItem {
   int k0;           // first B row (node, degree or bin) of the item
   int nsteps;       // 4 B rows per step
   int src;          // index into SpmmSrcs
-  int pad;
+  int cplx;         // 1: output rows are 4 complex bins, stored interleaved (re, im) per column
 };
 
 #define XC_MAX_SRC 40
