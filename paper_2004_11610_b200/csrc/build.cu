@@ -10,7 +10,8 @@
 //     A[row][kk] = c_q Re S[node][q]   (kk even)  |  -c_q Im S[node][q]   (kk odd),
 //     node = 8g + row, q = k0 + 2s + kk/2
 // and its tail A[row][kk] = phi_{k0+4s+kk}(x_{8g+row}).
-// In every case lane l of a warp holds A[l/4][l%4] (spmm.cu).
+// In every case lane l of a warp holds A[l/4][l%4] (spmm.cu); an item carries two M-tiles
+// (adjacent groups sharing the B fragments), interleaved per lane.
 #include "build.h"
 #include "xc_internal.cuh"
 
@@ -24,55 +25,37 @@ __device__ __forceinline__ double band_val(int k, int q, int comp, const int* st
   return comp ? v.y : v.x;
 }
 
-__global__ void fill_out_cplx(const FillItem* fi, const int* start, const int* len, const int64_t* off,
-                              const double2* vals, int N, int H, double* tiles) {
+// lane l of a warp holds A[l/4][l%4] of each M-tile: row r = l/4, B row R = k0 + 4s + l%4
+template <int MODE>
+__global__ void fill_k(const FillItem* fi, const int* start, const int* len, const int64_t* off,
+                       const double2* vals, const double* P, int t, int N, int H, double* tiles) {
   const FillItem it = fi[blockIdx.x];
-  for (int idx = threadIdx.x; idx < it.nsteps * 32; idx += blockDim.x) {
-    int s = idx >> 5, lane = idx & 31;
-    int k = it.k0 + 4 * s + (lane & 3);
-    int row = lane >> 2;
-    int q = 4 * it.g + (row >> 1);
+  for (int idx = threadIdx.x; idx < it.nsteps * 64; idx += blockDim.x) {
+    int s = idx >> 6, lane = (idx >> 1) & 31, mt = idx & 1;
+    int gm = mt ? it.g1 : it.g0;
     double v = 0.0;
-    if (k < N && q < H) v = band_val(k, q, row & 1, start, len, off, vals);
-    tiles[it.a_off + idx] = v;
-  }
-}
-
-__global__ void fill_out_real(const FillItem* fi, const double* P, int t, int N, double* tiles) {
-  const FillItem it = fi[blockIdx.x];
-  for (int idx = threadIdx.x; idx < it.nsteps * 32; idx += blockDim.x) {
-    int s = idx >> 5, lane = idx & 31;
-    int k = it.k0 + 4 * s + (lane & 3);
-    int j = 8 * it.g + (lane >> 2);
-    tiles[it.a_off + idx] = (k < N && j < t) ? P[(int64_t)j * N + k] : 0.0;
-  }
-}
-
-__global__ void fill_in_cplx(const FillItem* fi, const int* start, const int* len, const int64_t* off,
-                             const double2* vals, int N, int H, double* tiles) {
-  const FillItem it = fi[blockIdx.x];
-  for (int idx = threadIdx.x; idx < it.nsteps * 32; idx += blockDim.x) {
-    int s = idx >> 5, lane = idx & 31;
-    int node = 8 * it.g + (lane >> 2);
-    int kk = lane & 3;
-    int q = it.k0 + 2 * s + (kk >> 1);
-    double v = 0.0;
-    if (node < N && q < H) {
-      double c = (q == 0 || q == H - 1) ? 1.0 : 2.0;
-      double a = band_val(node, q, kk & 1, start, len, off, vals);
-      v = (kk & 1) ? -c * a : c * a;
+    if (gm >= 0) {
+      int R = it.k0 + 4 * s + (lane & 3);
+      int r = lane >> 2;
+      if (MODE == FILL_OUT_CPLX) {        // node R, bin 4 gm + r/2, component r&1
+        int q = 4 * gm + (r >> 1);
+        if (R < N && q < H) v = band_val(R, q, r & 1, start, len, off, vals);
+      } else if (MODE == FILL_OUT_REAL) { // node R, degree 8 gm + r
+        int j = 8 * gm + r;
+        if (R < N && j < t) v = P[(int64_t)j * N + R];
+      } else if (MODE == FILL_IN_CPLX) {  // node 8 gm + r, bin R/2, (c Re S, -c Im S)
+        int node = 8 * gm + r, q = R >> 1;
+        if (node < N && q < H) {
+          double c = (q == 0 || q == H - 1) ? 1.0 : 2.0;
+          double a = band_val(node, q, R & 1, start, len, off, vals);
+          v = (R & 1) ? -c * a : c * a;
+        }
+      } else {                            // node 8 gm + r, degree R
+        int node = 8 * gm + r;
+        if (node < N && R < t) v = P[(int64_t)R * N + node];
+      }
     }
     tiles[it.a_off + idx] = v;
-  }
-}
-
-__global__ void fill_in_real(const FillItem* fi, const double* P, int t, int N, double* tiles) {
-  const FillItem it = fi[blockIdx.x];
-  for (int idx = threadIdx.x; idx < it.nsteps * 32; idx += blockDim.x) {
-    int s = idx >> 5, lane = idx & 31;
-    int node = 8 * it.g + (lane >> 2);
-    int j = it.k0 + 4 * s + (lane & 3);
-    tiles[it.a_off + idx] = (node < N && j < t) ? P[(int64_t)j * N + node] : 0.0;
   }
 }
 
@@ -82,10 +65,10 @@ xc_status fill_tiles(int mode, const FillItem* fi, int n, const int* start, cons
                      const double2* vals, const double* P, int t, int N, int H, double* tiles, cudaStream_t st) {
   if (n <= 0) return XC_OK;
   switch (mode) {
-    case FILL_OUT_CPLX: fill_out_cplx<<<n, 128, 0, st>>>(fi, start, len, off, vals, N, H, tiles); break;
-    case FILL_OUT_REAL: fill_out_real<<<n, 128, 0, st>>>(fi, P, t, N, tiles); break;
-    case FILL_IN_CPLX: fill_in_cplx<<<n, 128, 0, st>>>(fi, start, len, off, vals, N, H, tiles); break;
-    default: fill_in_real<<<n, 128, 0, st>>>(fi, P, t, N, tiles); break;
+    case FILL_OUT_CPLX: fill_k<FILL_OUT_CPLX><<<n, 128, 0, st>>>(fi, start, len, off, vals, P, t, N, H, tiles); break;
+    case FILL_OUT_REAL: fill_k<FILL_OUT_REAL><<<n, 128, 0, st>>>(fi, start, len, off, vals, P, t, N, H, tiles); break;
+    case FILL_IN_CPLX: fill_k<FILL_IN_CPLX><<<n, 128, 0, st>>>(fi, start, len, off, vals, P, t, N, H, tiles); break;
+    default: fill_k<FILL_IN_REAL><<<n, 128, 0, st>>>(fi, start, len, off, vals, P, t, N, H, tiles); break;
   }
   XC_CUDA(cudaGetLastError());
   return XC_OK;

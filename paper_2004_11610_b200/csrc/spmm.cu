@@ -4,9 +4,11 @@
 // F = Ä_e z, Alg. 1 step 2.2; per block P:281).  "The degree of compression
 // ... determines to a great extent the efficiency of the computation step".
 //
-// The band-sparse operator is pre-tiled (build.cu) into items: an item is an
-// 8 x (4*nsteps) dense slice A of the operator (8 output rows = 4 complex bins
-// as re/im, or 8 real rows) against 4*nsteps consecutive rows of the operand Bm.
+// The band-sparse operator is pre-tiled (build.cu) into items: an item is a pair of
+// 8 x (4*nsteps) dense slices A of the operator (8 output rows = 4 complex bins as re/im,
+// or 8 real rows) against 4*nsteps consecutive rows of the operand Bm; items are grouped
+// into windows of B rows that one CTA stages in shared memory (the X rows of a node window
+// are shared by every block's bins that touch those nodes).
 // One warp computes D = A * Bm for 8*NT right-hand sides with DMMA
 // (mma.sync.m8n8k4.f64: 37 TF/s measured on B200 vs 34 TF/s for DFMA):
 //   A fragment  : lane holds A[lane/4][lane%4]     (one coalesced 256 B load/step)
@@ -28,156 +30,175 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-constexpr int WPC = 4;  // warps (items) per CTA
+constexpr int WARPS = 8;  // warps per CTA
 
+// One CTA = one window of B rows [r0, r1) (<= XC_WMAX) x one tile of 8*NT right-hand sides.
+// The window's rows are staged once in shared memory; the window's items (all families whose
+// B rows lie inside it) are spread over the warps.  Each item holds 2 M-tiles sharing the B
+// fragments (2 x NT DMMAs per 4-row step).  B fragments come from shared memory (one step
+// ahead), A fragments stream from global memory two steps ahead.
 template <int NT>
-__global__ void __launch_bounds__(WPC * 32) spmm_dmma(const SpmmItem* __restrict__ items, int nitems,
-                                                       const double* __restrict__ tiles, SpmmSrcs srcs,
-                                                       double* __restrict__ part, int64_t ldp, int ncols) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int it_idx = blockIdx.y * WPC + warp;
-  if (it_idx >= nitems) return;
-  const SpmmItem it = items[it_idx];
+__global__ void __launch_bounds__(WARPS * 32, 2)
+    spmm_win(const SpmmWin* __restrict__ wins, const SpmmItem* __restrict__ items,
+             const double* __restrict__ tiles, SpmmSrcs srcs, double* __restrict__ part, int64_t ldp, int ncols) {
+  constexpr int CW = 8 * NT;  // columns per tile
+  extern __shared__ double2 xs2[];
+  const double* xs = reinterpret_cast<const double*>(xs2);
+  const SpmmWin W = wins[blockIdx.y];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = lane & 3, g = lane >> 2;
-  const int tile0 = blockIdx.x * (8 * NT);
+  const int tile0 = blockIdx.x * CW;
 
-  const double* re = srcs.re[it.src];
-  const double* im = srcs.im[it.src];
-  const int nrows = srcs.nrows[it.src];
-  const int64_t ld = srcs.ld[it.src];
-  const bool planes = (im != nullptr);
-  const bool full = (tile0 + 8 * NT <= ncols);
-  const bool vec_ok = ((ld & 1) == 0) && ((((uintptr_t)re) & 15) == 0) && (!planes || (((uintptr_t)im) & 15) == 0);
+  // ---- stage the window: rows [r0, r1) x columns [tile0, tile0 + CW) ----
+  {
+    const double* re = srcs.re[W.src];
+    const double* im = srcs.im[W.src];
+    const int nrows = srcs.nrows[W.src];
+    const int64_t ld = srcs.ld[W.src];
+    const int nr = W.r1 - W.r0;
+    const bool vec = (NT >= 2) && ((ld & 1) == 0) && ((((uintptr_t)re) & 15) == 0) &&
+                     (!im || (((uintptr_t)im) & 15) == 0) && (tile0 + CW <= ncols);
+    if (vec) {
+      for (int idx = tid; idx < nr * (CW / 2); idx += WARPS * 32) {
+        int rl = idx / (CW / 2), c2 = idx - rl * (CW / 2);
+        int R = W.r0 + rl;
+        int row = im ? (R >> 1) : R;
+        const double* src = (im && (R & 1)) ? im : re;
+        double2 v = make_double2(0.0, 0.0);
+        if (row < nrows) v = __ldg(reinterpret_cast<const double2*>(src + (int64_t)row * ld + tile0) + c2);
+        xs2[idx] = v;
+      }
+    } else {
+      double* xw = reinterpret_cast<double*>(xs2);
+      for (int idx = tid; idx < nr * CW; idx += WARPS * 32) {
+        int rl = idx / CW, c = idx - rl * CW;
+        int R = W.r0 + rl;
+        int row = im ? (R >> 1) : R;
+        const double* src = (im && (R & 1)) ? im : re;
+        xw[idx] = (row < nrows && tile0 + c < ncols) ? __ldg(src + (int64_t)row * ld + tile0 + c) : 0.0;
+      }
+    }
+  }
+  __syncthreads();
 
-  double acc[NT][2];
+  // B-fragment column n of DMMA nt: 16 (nt/2) + 2n + (nt&1) within the tile (NT >= 2), n (NT == 1)
+  const int bcol = (NT == 1) ? g : 2 * g;
+
+  for (int ii = W.i0 + warp; ii < W.i1; ii += WARPS) {
+    const SpmmItem it = items[ii];
+    double acc[2][NT][2];
 #pragma unroll
-  for (int i = 0; i < NT; ++i) acc[i][0] = acc[i][1] = 0.0;
-
-  // RHS of B-fragment column n for DMMA nt: tile0 + 16*(nt/2) + 2n + (nt&1)  (NT >= 2)
-  //                                         tile0 + n                     (NT == 1)
-  // so one 16-byte load per lane per nt pair covers 128 contiguous bytes per row.
-  const int bcol = (NT == 1) ? tile0 + g : tile0 + 2 * g;
-  const double* a_ptr = tiles + it.a_off + lane;
-  double a_cur = (it.nsteps > 0) ? __ldg(a_ptr) : 0.0;
-  double b_cur[NT];
-
-  auto load_b = [&](int s, double* bv) {
-    int r = 4 * s + t;
-    int row = planes ? it.k0 + (r >> 1) : it.k0 + r;
-    const double* src = (planes && (r & 1)) ? im : re;
-    if (row < nrows) {
-      const double* p = src + (int64_t)row * ld + bcol;
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int i = 0; i < NT; ++i) acc[m][i][0] = acc[m][i][1] = 0.0;
+    const double2* ap = reinterpret_cast<const double2*>(tiles + it.a_off) + lane;
+    const double* xb = xs + (it.k0 - W.r0 + t) * CW + bcol;
+    const int n = it.nsteps;
+    double2 a0 = n > 0 ? __ldg(ap) : make_double2(0.0, 0.0);
+    double2 a1 = n > 1 ? __ldg(ap + 32) : make_double2(0.0, 0.0);
+    double b0[NT], b1[NT];
+    auto lds_b = [&](int s, double* bv) {
+      const double* p = xb + 4 * s * CW;
       if (NT == 1) {
-        bv[0] = (bcol < ncols) ? __ldg(p) : 0.0;
-      } else if (full && vec_ok) {
+        bv[0] = p[0];
+      } else {
 #pragma unroll
         for (int m = 0; m < NT / 2; ++m) {
-          double2 v = __ldg(reinterpret_cast<const double2*>(p + 16 * m));
+          double2 v = *reinterpret_cast<const double2*>(p + 16 * m);
           bv[2 * m] = v.x;
           bv[2 * m + 1] = v.y;
         }
-      } else {
+      }
+    };
+    if (n > 0) lds_b(0, b0);
+    for (int s = 0; s < n; s += 2) {
+      if (s + 1 < n) lds_b(s + 1, b1);
 #pragma unroll
-        for (int m = 0; m < NT / 2; ++m) {
-          int c = bcol + 16 * m;
-          bv[2 * m] = (c < ncols) ? __ldg(p + 16 * m) : 0.0;
-          bv[2 * m + 1] = (c + 1 < ncols) ? __ldg(p + 16 * m + 1) : 0.0;
+      for (int i = 0; i < NT; ++i) {
+        dmma(acc[0][i][0], acc[0][i][1], a0.x, b0[i]);
+        dmma(acc[1][i][0], acc[1][i][1], a0.y, b0[i]);
+      }
+      a0 = (s + 2 < n) ? __ldg(ap + 32 * (s + 2)) : make_double2(0.0, 0.0);
+      if (s + 1 < n) {
+        if (s + 2 < n) lds_b(s + 2, b0);
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+          dmma(acc[0][i][0], acc[0][i][1], a1.x, b1[i]);
+          dmma(acc[1][i][0], acc[1][i][1], a1.y, b1[i]);
         }
+        a1 = (s + 3 < n) ? __ldg(ap + 32 * (s + 3)) : make_double2(0.0, 0.0);
       }
-    } else {
-#pragma unroll
-      for (int i = 0; i < NT; ++i) bv[i] = 0.0;
     }
-  };
 
-  if (it.nsteps > 0) load_b(0, b_cur);
-  for (int s = 0; s < it.nsteps; ++s) {
-    double a_nxt = 0.0;
-    double b_nxt[NT];
-    const bool more = (s + 1 < it.nsteps);
-    if (more) {
-      a_nxt = __ldg(a_ptr + 32 * (s + 1));
-      load_b(s + 1, b_nxt);
-    }
+    // ---- store the two 8 x CW output tiles ----
 #pragma unroll
-    for (int i = 0; i < NT; ++i) dmma(acc[i][0], acc[i][1], a_cur, b_cur[i]);
-    if (more) {
-      a_cur = a_nxt;
-#pragma unroll
-      for (int i = 0; i < NT; ++i) b_cur[i] = b_nxt[i];
-    }
-  }
-
-  // D[g][2t+i] of DMMA nt -> RHS tile0 + 16*(nt/2) + 4t + 2i + (nt&1): 32 contiguous bytes per
-  // lane per nt pair (NT == 1: RHS tile0 + 2t + i).
-  if (it.cplx) {
-    // rows g = 2*bin + comp of 4 complex bins: store u_bin interleaved (re, im) per column in
-    // the complex row out_row/2 + bin (= double rows out_row + 2 bin, +1).  Lanes g and g^1 (lane ^ 4)
-    // trade halves so that each writes whole complex numbers.
-    const bool odd = g & 1;
-    double2* crow = reinterpret_cast<double2*>(part + (it.out_row + (g & ~1)) * ldp);
-    if (NT == 1) {
-      int c = tile0 + 2 * t;
-      double snd = odd ? acc[0][0] : acc[0][1];
-      double rcv = __shfl_xor_sync(0xffffffffu, snd, 4);
-      if (!odd) {
-        if (c < ldp) crow[c] = make_double2(acc[0][0], rcv);
-      } else {
-        if (c + 1 < ldp) crow[c + 1] = make_double2(rcv, acc[0][1]);
-      }
-    } else {
-#pragma unroll
-      for (int m = 0; m < NT / 2; ++m) {
-        int c = tile0 + 16 * m + 4 * t;
-        double v0 = acc[2 * m][0], v1 = acc[2 * m + 1][0], v2 = acc[2 * m][1], v3 = acc[2 * m + 1][1];
-        double s0 = odd ? v0 : v2, s1 = odd ? v1 : v3;
-        double r0 = __shfl_xor_sync(0xffffffffu, s0, 4), r1 = __shfl_xor_sync(0xffffffffu, s1, 4);
-        if (!odd) {
-          crow[c] = make_double2(v0, r0);
-          crow[c + 1] = make_double2(v1, r1);
+    for (int mt = 0; mt < 2; ++mt) {
+      if (it.out_row[mt] < 0) continue;
+      if (it.cplx) {
+        // rows g = 2 bin + comp of 4 complex bins -> complex row (out_row + 2 bin) / 2, interleaved
+        // (re, im) per column; lanes g, g^1 (lane ^ 4) trade halves to write whole numbers.
+        const bool odd = g & 1;
+        double2* crow = reinterpret_cast<double2*>(part + (it.out_row[mt] + (g & ~1)) * ldp);
+        if (NT == 1) {
+          int c = tile0 + 2 * t;
+          double snd = odd ? acc[mt][0][0] : acc[mt][0][1];
+          double rcv = __shfl_xor_sync(0xffffffffu, snd, 4);
+          if (!odd) {
+            if (c < ldp) crow[c] = make_double2(acc[mt][0][0], rcv);
+          } else {
+            if (c + 1 < ldp) crow[c + 1] = make_double2(rcv, acc[mt][0][1]);
+          }
         } else {
-          crow[c + 2] = make_double2(r0, v2);
-          crow[c + 3] = make_double2(r1, v3);
-        }
-      }
-    }
-    return;
-  }
-  double* orow = part + (it.out_row + g) * ldp;
-  if (NT == 1) {
-    int c = tile0 + 2 * t;
-    if (c + 1 < ldp) {
-      *reinterpret_cast<double2*>(orow + c) = make_double2(acc[0][0], acc[0][1]);
-    } else if (c < ldp) {
-      orow[c] = acc[0][0];
-    }
-  } else {
 #pragma unroll
-    for (int m = 0; m < NT / 2; ++m) {
-      int c = tile0 + 16 * m + 4 * t;
-      if (c + 3 < ldp) {
-        *reinterpret_cast<double2*>(orow + c) = make_double2(acc[2 * m][0], acc[2 * m + 1][0]);
-        *reinterpret_cast<double2*>(orow + c + 2) = make_double2(acc[2 * m][1], acc[2 * m + 1][1]);
+          for (int m = 0; m < NT / 2; ++m) {
+            int c = tile0 + 16 * m + 4 * t;
+            double v0 = acc[mt][2 * m][0], v1 = acc[mt][2 * m + 1][0];
+            double v2 = acc[mt][2 * m][1], v3 = acc[mt][2 * m + 1][1];
+            double s0 = odd ? v0 : v2, s1 = odd ? v1 : v3;
+            double r0 = __shfl_xor_sync(0xffffffffu, s0, 4), r1 = __shfl_xor_sync(0xffffffffu, s1, 4);
+            if (!odd) {
+              crow[c] = make_double2(v0, r0);
+              crow[c + 1] = make_double2(v1, r1);
+            } else {
+              crow[c + 2] = make_double2(r0, v2);
+              crow[c + 3] = make_double2(r1, v3);
+            }
+          }
+        }
+      } else {
+        double* orow = part + (it.out_row[mt] + g) * ldp;
+        if (NT == 1) {
+          int c = tile0 + 2 * t;
+          if (c + 1 < ldp) *reinterpret_cast<double2*>(orow + c) = make_double2(acc[mt][0][0], acc[mt][0][1]);
+          else if (c < ldp) orow[c] = acc[mt][0][0];
+        } else {
+#pragma unroll
+          for (int m = 0; m < NT / 2; ++m) {
+            int c = tile0 + 16 * m + 4 * t;
+            *reinterpret_cast<double2*>(orow + c) = make_double2(acc[mt][2 * m][0], acc[mt][2 * m + 1][0]);
+            *reinterpret_cast<double2*>(orow + c + 2) = make_double2(acc[mt][2 * m][1], acc[mt][2 * m + 1][1]);
+          }
+        }
       }
     }
   }
 }
 
 template <int NT>
-xc_status launch(const SpmmItem* items, int nitems, const double* tiles, const SpmmSrcs& srcs, double* part,
-                 int64_t ldp, int ncols, cudaStream_t st) {
-  dim3 grid((ncols + 8 * NT - 1) / (8 * NT), (nitems + WPC - 1) / WPC);
-  if (grid.y > 65535) {
-    // fold very long item lists into several launches
-    int per = 65535 * WPC;
-    for (int i0 = 0; i0 < nitems; i0 += per) {
-      int n = std::min(per, nitems - i0);
-      XC_TRY(launch<NT>(items + i0, n, tiles, srcs, part, ldp, ncols, st));
-    }
-    return XC_OK;
+xc_status launch(const SpmmWin* wins, int nwins, const SpmmItem* items, const double* tiles, const SpmmSrcs& srcs,
+                 double* part, int64_t ldp, int ncols, cudaStream_t st) {
+  const size_t sm = (size_t)XC_WMAX * 8 * NT * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    XC_CUDA(cudaFuncSetAttribute(spmm_win<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr = true;
   }
-  spmm_dmma<NT><<<grid, WPC * 32, 0, st>>>(items, nitems, tiles, srcs, part, ldp, ncols);
-  XC_CUDA(cudaGetLastError());
+  for (int w0 = 0; w0 < nwins; w0 += 65535) {
+    int nw = std::min(65535, nwins - w0);
+    dim3 grid((ncols + 8 * NT - 1) / (8 * NT), nw);
+    spmm_win<NT><<<grid, WARPS * 32, sm, st>>>(wins + w0, items, tiles, srcs, part, ldp, ncols);
+    XC_CUDA(cudaGetLastError());
+  }
   return XC_OK;
 }
 
@@ -200,22 +221,20 @@ __global__ void reduce_rows8_kernel(const double* __restrict__ part, int64_t ldp
 }  // namespace
 
 int spmm_nt_for(int64_t B) {
-  if (B >= 128) return 16;
   if (B >= 64) return 8;
   if (B >= 32) return 4;
   if (B >= 16) return 2;
   return 1;
 }
 
-xc_status spmm_run(const SpmmItem* items, int nitems, const double* tiles, const SpmmSrcs& srcs, double* part,
-                   int64_t ldp, int ncols, cudaStream_t st) {
-  if (nitems <= 0) return XC_OK;
+xc_status spmm_run(const SpmmWin* wins, int nwins, const SpmmItem* items, const double* tiles,
+                   const SpmmSrcs& srcs, double* part, int64_t ldp, int ncols, cudaStream_t st) {
+  if (nwins <= 0) return XC_OK;
   switch (spmm_nt_for(ncols)) {
-    case 16: return launch<16>(items, nitems, tiles, srcs, part, ldp, ncols, st);
-    case 8: return launch<8>(items, nitems, tiles, srcs, part, ldp, ncols, st);
-    case 4: return launch<4>(items, nitems, tiles, srcs, part, ldp, ncols, st);
-    case 2: return launch<2>(items, nitems, tiles, srcs, part, ldp, ncols, st);
-    default: return launch<1>(items, nitems, tiles, srcs, part, ldp, ncols, st);
+    case 8: return launch<8>(wins, nwins, items, tiles, srcs, part, ldp, ncols, st);
+    case 4: return launch<4>(wins, nwins, items, tiles, srcs, part, ldp, ncols, st);
+    case 2: return launch<2>(wins, nwins, items, tiles, srcs, part, ldp, ncols, st);
+    default: return launch<1>(wins, nwins, items, tiles, srcs, part, ldp, ncols, st);
   }
 }
 

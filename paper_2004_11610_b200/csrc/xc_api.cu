@@ -49,9 +49,10 @@ void dev_free(DevBuf& b) {
 
 namespace {
 
-constexpr int KC = 256;      // node chunk of a split output-axis item (multiple of 4)
-constexpr int KSPLIT = 1024; // blocks whose bin groups span more nodes than this are split
-constexpr int QC = 256;  // bin chunk of an input-axis item (multiple of 2)
+constexpr int KC = 128;      // node chunk of a split output-axis item (multiple of 4, <= XC_WMAX)
+constexpr int KSPLIT = 128;  // blocks whose bin groups span more nodes than this are split
+constexpr int QC = 64;       // bin chunk of an input-axis item (2 QC B rows <= XC_WMAX)
+constexpr int WIN_ITEMS = 128;  // max items per SpMM window (CTA)
 
 struct BlockData {
   int L = 0, H = 0, m_off = 0, keep_lo = 0, keep_hi = 0;
@@ -89,14 +90,14 @@ struct xc_op {
   std::vector<BlockData> blocks;
   DevBuf nodes, wt, tailP;
   // output axis
-  DevBuf itemsA, tilesA;
-  int nitemsA = 0;
+  DevBuf itemsA, tilesA, winsA;
+  int nitemsA = 0, nwinsA = 0;
   int64_t rowsA = 0, tilesA_n = 0;
   int ntailg = 0;
   DevBuf tail_base, tail_nch;
   // input axis
-  DevBuf itemsW, tilesW;
-  int nitemsW = 0;
+  DevBuf itemsW, tilesW, winsW;
+  int nitemsW = 0, nwinsW = 0;
   int64_t rowsW = 0, tilesW_n = 0;
   DevBuf nodeg_base, nodeg_nch;
   // workspace
@@ -281,20 +282,140 @@ xc_status build_block(xc_op* h, BlockData& b, const std::vector<double2>& jtab, 
   return XC_OK;
 }
 
+// --- SpMM items: M-tiles paired into items ------------------------------------------------
+// An M-tile is one 8-row slice of the operator (a bin group, a degree group or a node group)
+// over a range of B rows [k0, k1) (multiples of 4) with its output rows.  Consecutive M-tiles
+// of the same family and chunk are paired into one item (they share the B fragments; the
+// union of their ranges is padded with zeros in each one's A stream).
+struct MTile {
+  int fam;        // block index, or -1 for the dense tail
+  int g;          // group index within the family
+  int chunk;      // execution-order key (B-row window)
+  int k0, k1;     // B rows
+  int64_t out_row;
+  int cplx;
+};
+
+struct ItemSet {
+  std::vector<SpmmItem> items;
+  std::vector<FillItem> fills;
+  std::vector<int> fam;
+  std::vector<int> chunk;
+  int64_t aoff = 0;
+};
+
+void pair_mtiles(const std::vector<MTile>& mt, int src, ItemSet& out) {
+  // mt is ordered by (fam, chunk, g)
+  size_t i = 0;
+  while (i < mt.size()) {
+    const MTile& a = mt[i];
+    const MTile* b = nullptr;
+    if (i + 1 < mt.size() && mt[i + 1].fam == a.fam && mt[i + 1].chunk == a.chunk) {
+      b = &mt[i + 1];
+      int u0 = std::min(a.k1 > a.k0 ? a.k0 : b->k0, b->k1 > b->k0 ? b->k0 : a.k0);
+      int u1 = std::max(a.k1, b->k1);
+      if (u1 - u0 > XC_WMAX) b = nullptr;  // the pair must fit one shared-memory window
+    }
+    int k0 = a.k0, k1 = a.k1;
+    if (b) {
+      if (b->k1 > b->k0) {
+        if (k1 > k0) {
+          k0 = std::min(k0, b->k0);
+          k1 = std::max(k1, b->k1);
+        } else {
+          k0 = b->k0;
+          k1 = b->k1;
+        }
+      }
+    }
+    SpmmItem it{};
+    it.a_off = out.aoff;
+    it.out_row[0] = a.out_row;
+    it.out_row[1] = b ? b->out_row : -1;
+    it.k0 = k0;
+    it.nsteps = std::max(0, (k1 - k0) / 4);
+    it.src = src < 0 ? (a.fam < 0 ? 0 : a.fam) : src;
+    it.cplx = a.cplx;
+    out.items.push_back(it);
+    out.fills.push_back(FillItem{out.aoff, k0, it.nsteps, a.g, b ? b->g : -1});
+    out.fam.push_back(a.fam);
+    out.chunk.push_back(a.chunk);
+    out.aoff += 64LL * it.nsteps;
+    i += b ? 2 : 1;
+  }
+}
+
+xc_status upload_and_fill(xc_op* h, ItemSet& S, bool input_axis, DevBuf& d_items, DevBuf& d_wins,
+                          DevBuf& d_tiles, int& nitems, int& nwins, int64_t& ntiles, cudaStream_t st) {
+  const int N = (int)h->N;
+  ntiles = S.aoff;
+  XC_TRY(dev_alloc(d_tiles, (size_t)std::max<int64_t>(1, S.aoff) * sizeof(double)));
+  DevBuf dfill;
+  for (int fam = -1; fam < (int)h->blocks.size(); ++fam) {
+    std::vector<FillItem> part;
+    for (size_t i = 0; i < S.fills.size(); ++i)
+      if (S.fam[i] == fam && S.fills[i].nsteps > 0) part.push_back(S.fills[i]);
+    if (part.empty()) continue;
+    XC_TRY(upload(dfill, part));
+    if (fam >= 0) {
+      BlockData& b = h->blocks[fam];
+      XC_TRY(fill_tiles(input_axis ? FILL_IN_CPLX : FILL_OUT_CPLX, (FillItem*)dfill.p, (int)part.size(),
+                        (int*)b.start.p, (int*)b.len.p, (int64_t*)b.off.p, (double2*)b.vals.p, nullptr, 0, N, b.H,
+                        (double*)d_tiles.p, st));
+    } else {
+      XC_TRY(fill_tiles(input_axis ? FILL_IN_REAL : FILL_OUT_REAL, (FillItem*)dfill.p, (int)part.size(), nullptr,
+                        nullptr, nullptr, nullptr, (double*)h->tailP.p, h->tail, N, 0, (double*)d_tiles.p, st));
+    }
+    XC_CUDA(cudaStreamSynchronize(st));
+  }
+  dev_free(dfill);
+  // windows: items sorted by (source, first B row); a window takes consecutive items while
+  // their B rows fit XC_WMAX rows (one CTA stages them in shared memory)
+  std::vector<size_t> ord(S.items.size());
+  for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
+  std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+    if (S.items[a].src != S.items[b].src) return S.items[a].src < S.items[b].src;
+    return S.items[a].k0 < S.items[b].k0;
+  });
+  std::vector<SpmmItem> sorted(S.items.size());
+  for (size_t i = 0; i < ord.size(); ++i) sorted[i] = S.items[ord[i]];
+  std::vector<SpmmWin> wins;
+  size_t i = 0;
+  while (i < sorted.size()) {
+    SpmmWin w{};
+    w.src = sorted[i].src;
+    w.r0 = sorted[i].k0;
+    w.r1 = sorted[i].k0 + 4 * sorted[i].nsteps;
+    w.i0 = (int)i;
+    size_t j = i + 1;
+    while (j < sorted.size() && sorted[j].src == w.src && (int)(j - i) < WIN_ITEMS) {
+      int e = sorted[j].k0 + 4 * sorted[j].nsteps;
+      if (std::max(e, w.r1) - w.r0 > XC_WMAX) break;
+      w.r1 = std::max(w.r1, e);
+      ++j;
+    }
+    w.i1 = (int)j;
+    wins.push_back(w);
+    i = j;
+  }
+  XC_TRY(upload(d_items, sorted));
+  XC_TRY(upload(d_wins, wins));
+  nitems = (int)sorted.size();
+  nwins = (int)wins.size();
+  return XC_OK;
+}
+
 // --- output-axis items and tiles ---------------------------------------------------------
 // Per block, bin group g = bins [4g, 4g+4) owns U rows ubase + 8g + 2(q%4) + comp, i.e. the
-// half spectrum u_q = (U[ubase + 2q], U[ubase + 2q + 1]).  Blocks whose groups span few nodes
-// (the large-L blocks) get one item per group writing its U rows directly; blocks whose
-// groups span many nodes (small L: ~18N nonzeros over few bins) are split into node chunks
-// whose partial sums are reduced into U in fixed order (deterministic split-K).
+// complex half spectrum u_q interleaved in double rows ubase + 2q, +1.  Blocks whose groups
+// span few nodes (the large-L blocks) get one M-tile per group writing U directly; blocks
+// whose groups span many nodes (small L: ~18N nonzeros over few bins) are split into node
+// chunks whose partial sums are reduced into U in fixed order (deterministic split-K).
 xc_status build_output_axis(xc_op* h, cudaStream_t st) {
   const int N = (int)h->N;
   const int N4 = (N + 3) / 4 * 4;
-  std::vector<SpmmItem> items;
-  std::vector<FillItem> fills;
-  std::vector<int> fill_blk;  // block index, -1 = tail
-  std::vector<int> chunk_of;  // node chunk index (execution order)
-  int64_t rows = 0, aoff = 0;
+  ItemSet S;
+  int64_t rows = 0;
   for (size_t bi = 0; bi < h->blocks.size(); ++bi) {
     BlockData& b = h->blocks[bi];
     b.ngroups = (b.H + 3) / 4;
@@ -315,6 +436,7 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
     rows += 8LL * b.ngroups;
     std::vector<int64_t> gbase(b.ngroups, 0);
     std::vector<int> gnch(b.ngroups, 0);
+    std::vector<MTile> mt;
     for (int g = 0; g < b.ngroups; ++g) {
       int a = 0, e = 0;
       if (klo[g] < khi[g]) {
@@ -322,36 +444,14 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
         e = (khi[g] + 3) / 4 * 4;
       }
       if (!b.split) {
-        SpmmItem it{};
-        it.a_off = aoff;
-        it.out_row = b.ubase + 8LL * g;
-        it.k0 = a;
-        it.nsteps = (e - a) / 4;  // 0 for an empty group: writes zeros
-        it.src = 0;
-        it.cplx = 1;
-        items.push_back(it);
-        fills.push_back(FillItem{aoff, a, it.nsteps, g, 0});
-        fill_blk.push_back((int)bi);
-        chunk_of.push_back(a / KC);
-        aoff += 32LL * it.nsteps;
+        mt.push_back(MTile{(int)bi, g, 0, a, e, b.ubase + 8LL * g, 1});  // empty group -> zeros
         continue;
       }
       gbase[g] = rows;
       for (int c = a / KC; c * KC < e; ++c) {
         int k0 = std::max(a, c * KC), k1 = std::min(e, (c + 1) * KC);
         if (k1 <= k0) continue;
-        SpmmItem it{};
-        it.a_off = aoff;
-        it.out_row = rows;
-        it.k0 = k0;
-        it.nsteps = (k1 - k0) / 4;
-        it.src = 0;
-        it.cplx = 1;
-        items.push_back(it);
-        fills.push_back(FillItem{aoff, k0, it.nsteps, g, 0});
-        fill_blk.push_back((int)bi);
-        chunk_of.push_back(c);
-        aoff += 32LL * it.nsteps;
+        mt.push_back(MTile{(int)bi, g, c, k0, k1, rows, 1});
         rows += 8;
         gnch[g]++;
       }
@@ -359,89 +459,59 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
     if (b.split) {
       XC_TRY(upload(b.grp_base, gbase));
       XC_TRY(upload(b.grp_nch, gnch));
+      std::stable_sort(mt.begin(), mt.end(), [](const MTile& x, const MTile& y) { return x.chunk < y.chunk; });
     }
+    // execution key of unsplit blocks: the node window of the first node
+    ItemSet tmp;
+    tmp.aoff = S.aoff;
+    pair_mtiles(mt, 0, tmp);
+    for (size_t i = 0; i < tmp.items.size(); ++i) {
+      S.items.push_back(tmp.items[i]);
+      S.fills.push_back(tmp.fills[i]);
+      S.fam.push_back(tmp.fam[i]);
+      S.chunk.push_back(b.split ? tmp.chunk[i] : tmp.items[i].k0 / KC);
+    }
+    S.aoff = tmp.aoff;
   }
-  // dense tail: groups of 8 degrees x node chunks
+  // dense tail: groups of 8 degrees x node chunks (P:301)
   h->ntailg = (h->tail + 7) / 8;
   std::vector<int64_t> tbase(std::max(1, h->ntailg), 0);
   std::vector<int> tnch(std::max(1, h->ntailg), 0);
+  std::vector<MTile> mt;
   for (int g = 0; g < h->ntailg; ++g) {
     tbase[g] = rows;
     for (int k0 = 0; k0 < N4; k0 += KC) {
-      int k1 = std::min(N4, k0 + KC);
-      SpmmItem it{};
-      it.a_off = aoff;
-      it.out_row = rows;
-      it.k0 = k0;
-      it.nsteps = (k1 - k0) / 4;
-      it.src = 0;
-      items.push_back(it);
-      fills.push_back(FillItem{aoff, k0, it.nsteps, g, 0});
-      fill_blk.push_back(-1);
-      chunk_of.push_back(k0 / KC);
-      aoff += 32LL * it.nsteps;
+      mt.push_back(MTile{-1, g, k0 / KC, k0, std::min(N4, k0 + KC), rows, 0});
       rows += 8;
       tnch[g]++;
     }
   }
+  std::stable_sort(mt.begin(), mt.end(), [](const MTile& x, const MTile& y) { return x.chunk < y.chunk; });
+  pair_mtiles(mt, 0, S);
   XC_TRY(upload(h->tail_base, tbase));
   XC_TRY(upload(h->tail_nch, tnch));
   h->rowsA = rows;
-  h->tilesA_n = aoff;
-  XC_TRY(dev_alloc(h->tilesA, (size_t)std::max<int64_t>(1, aoff) * sizeof(double)));
-  // fill per block
-  DevBuf dfill;
-  size_t i0 = 0;
-  while (i0 < fills.size()) {
-    size_t i1 = i0;
-    while (i1 < fills.size() && fill_blk[i1] == fill_blk[i0]) ++i1;
-    std::vector<FillItem> part(fills.begin() + i0, fills.begin() + i1);
-    std::vector<FillItem> nonempty;
-    for (auto& f : part)
-      if (f.nsteps > 0) nonempty.push_back(f);
-    int bi = fill_blk[i0];
-    if (!nonempty.empty()) {
-      XC_TRY(upload(dfill, nonempty));
-      if (bi >= 0) {
-        BlockData& b = h->blocks[bi];
-        XC_TRY(fill_tiles(FILL_OUT_CPLX, (FillItem*)dfill.p, (int)nonempty.size(), (int*)b.start.p,
-                          (int*)b.len.p, (int64_t*)b.off.p, (double2*)b.vals.p, nullptr, 0, N, b.H,
-                          (double*)h->tilesA.p, st));
-      } else {
-        XC_TRY(fill_tiles(FILL_OUT_REAL, (FillItem*)dfill.p, (int)nonempty.size(), nullptr, nullptr, nullptr,
-                          nullptr, (double*)h->tailP.p, h->tail, N, 0, (double*)h->tilesA.p, st));
-      }
-      XC_CUDA(cudaStreamSynchronize(st));
-    }
-    i0 = i1;
-  }
-  dev_free(dfill);
-  // execution order: by (block, node chunk, group) so that a CTA's warps share X rows;
-  // longest items of a block first within equal keys is not needed (items are short).
-  std::vector<size_t> ord(items.size());
-  for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
-  std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
-    if (chunk_of[a] != chunk_of[b]) return chunk_of[a] < chunk_of[b];
-    return (unsigned)fill_blk[a] < (unsigned)fill_blk[b];
-  });
-  std::vector<SpmmItem> sorted(items.size());
-  for (size_t i = 0; i < ord.size(); ++i) sorted[i] = items[ord[i]];
-  XC_TRY(upload(h->itemsA, sorted));
-  h->nitemsA = (int)sorted.size();
-  return XC_OK;
+  for (auto& it : S.items) it.src = 0;
+  return upload_and_fill(h, S, false, h->itemsA, h->winsA, h->tilesA, h->nitemsA, h->nwinsA, h->tilesA_n, st);
 }
 
 // --- input-axis items and tiles ----------------------------------------------------------
+// Node group G = nodes [8G, 8G+8); per block its bins are the union of the nodes' bands,
+// in B rows 2q (re plane) and 2q+1 (im plane) of that block's z' planes; split into bin
+// chunks.  Items of one node group are allocated consecutive output rows and reduced (times
+// the weights) in fixed order.
 xc_status build_input_axis(xc_op* h, cudaStream_t st) {
   const int N = (int)h->N;
   const int NG = (N + 7) / 8;
   const int nb = (int)h->blocks.size();
-  struct Tmp {
-    SpmmItem it;
-    FillItem f;
-    int blk;
+  std::vector<std::vector<MTile>> fam_tiles(nb + 1);
+  std::vector<int> gnch(NG, 0);
+  std::vector<int64_t> gbase(NG, 0);
+  // first pass: count M-tiles per node group (rows are allocated group-major)
+  struct Rng {
+    int fam, G, chunk, k0, k1;
   };
-  std::vector<std::vector<Tmp>> per_group(NG);
+  std::vector<Rng> rng;
   for (int bi = 0; bi < nb; ++bi) {
     BlockData& b = h->blocks[bi];
     for (int G = 0; G < NG; ++G) {
@@ -452,88 +522,44 @@ xc_status build_input_axis(xc_op* h, cudaStream_t st) {
         qhi = std::max(qhi, b.h_start[k] + b.h_len[k]);
       }
       if (qlo >= qhi) continue;
-      int a = qlo / 2 * 2, e = (qhi + 1) / 2 * 2;
+      int a = qlo / 2 * 2, e = (qhi + 1) / 2 * 2;  // 2 bins = 4 B rows per step
       for (int c = a / QC; c * QC < e; ++c) {
         int q0 = std::max(a, c * QC), q1 = std::min(e, (c + 1) * QC);
         if (q1 <= q0) continue;
-        Tmp t{};
-        t.it.k0 = q0;
-        t.it.nsteps = (q1 - q0) / 2;
-        t.it.src = bi;
-        t.f = FillItem{0, q0, t.it.nsteps, G, 0};
-        t.blk = bi;
-        per_group[G].push_back(t);
+        rng.push_back(Rng{bi, G, c, 2 * q0, 2 * q1});
+        gnch[G]++;
       }
     }
   }
   if (h->tail > 0) {
     int t4 = (h->tail + 3) / 4 * 4;
     for (int G = 0; G < NG; ++G) {
-      Tmp t{};
-      t.it.k0 = 0;
-      t.it.nsteps = t4 / 4;
-      t.it.src = nb;
-      t.f = FillItem{0, 0, t.it.nsteps, G, 0};
-      t.blk = -1;
-      per_group[G].push_back(t);
+      rng.push_back(Rng{-1, G, 0, 0, t4});
+      gnch[G]++;
     }
   }
-  std::vector<int64_t> gbase(NG);
-  std::vector<int> gnch(NG);
-  std::vector<SpmmItem> items;
-  std::vector<FillItem> fills;
-  std::vector<int> fblk;
-  int64_t rows = 0, aoff = 0;
+  int64_t rows = 0;
   for (int G = 0; G < NG; ++G) {
     gbase[G] = rows;
-    gnch[G] = (int)per_group[G].size();
-    for (auto& t : per_group[G]) {
-      t.it.a_off = aoff;
-      t.f.a_off = aoff;
-      t.it.out_row = rows;
-      aoff += 32LL * t.it.nsteps;
-      rows += 8;
-      items.push_back(t.it);
-      fills.push_back(t.f);
-      fblk.push_back(t.blk);
-    }
+    rows += 8LL * gnch[G];
+  }
+  std::vector<int> used(NG, 0);
+  for (auto& r : rng) {
+    int64_t orow = gbase[r.G] + 8LL * used[r.G]++;
+    fam_tiles[r.fam + 1].push_back(MTile{r.fam, r.G, r.chunk, r.k0, r.k1, orow, 0});
+  }
+  ItemSet S;
+  for (int f = 0; f <= nb; ++f) {
+    auto& mt = fam_tiles[f];
+    std::stable_sort(mt.begin(), mt.end(), [](const MTile& x, const MTile& y) {
+      return x.chunk != y.chunk ? x.chunk < y.chunk : x.g < y.g;
+    });
+    pair_mtiles(mt, f == 0 ? nb : f - 1, S);
   }
   XC_TRY(upload(h->nodeg_base, gbase));
   XC_TRY(upload(h->nodeg_nch, gnch));
   h->rowsW = rows;
-  h->tilesW_n = aoff;
-  XC_TRY(dev_alloc(h->tilesW, (size_t)std::max<int64_t>(1, aoff) * sizeof(double)));
-  // fill, grouped by block
-  DevBuf dfill;
-  for (int bi = -1; bi < nb; ++bi) {
-    std::vector<FillItem> part;
-    for (size_t i = 0; i < fills.size(); ++i)
-      if (fblk[i] == bi) part.push_back(fills[i]);
-    if (part.empty()) continue;
-    XC_TRY(upload(dfill, part));
-    if (bi >= 0) {
-      BlockData& b = h->blocks[bi];
-      XC_TRY(fill_tiles(FILL_IN_CPLX, (FillItem*)dfill.p, (int)part.size(), (int*)b.start.p, (int*)b.len.p,
-                        (int64_t*)b.off.p, (double2*)b.vals.p, nullptr, 0, N, b.H, (double*)h->tilesW.p, st));
-    } else {
-      XC_TRY(fill_tiles(FILL_IN_REAL, (FillItem*)dfill.p, (int)part.size(), nullptr, nullptr, nullptr, nullptr,
-                        (double*)h->tailP.p, h->tail, N, 0, (double*)h->tilesW.p, st));
-    }
-    XC_CUDA(cudaStreamSynchronize(st));
-  }
-  dev_free(dfill);
-  // execution order: by (block, bin chunk, node group)
-  std::vector<size_t> ord(items.size());
-  for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
-  std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
-    if (items[a].src != items[b].src) return items[a].src < items[b].src;
-    return items[a].k0 / QC < items[b].k0 / QC;
-  });
-  std::vector<SpmmItem> sorted(items.size());
-  for (size_t i = 0; i < ord.size(); ++i) sorted[i] = items[ord[i]];
-  XC_TRY(upload(h->itemsW, sorted));
-  h->nitemsW = (int)sorted.size();
-  return XC_OK;
+  return upload_and_fill(h, S, true, h->itemsW, h->winsW, h->tilesW, h->nitemsW, h->nwinsW, h->tilesW_n, st);
 }
 
 double fft_flops(int L) { return 2.5 * L * log2((double)L); }  // real FFT = half of 5 L log2 L
@@ -641,7 +667,7 @@ xc_status build_impl(xc_kind kind, const xc_params* prm, const double* nodes, in
   in.nnz = nnz;
   in.flops_per_col_A = 4.0 * nnz + 2.0 * h->tail * N + fft;
   in.flops_per_col_WAT = in.flops_per_col_A;
-  in.dmma_flops_per_col_A = 64.0 * (h->tilesA_n / 32);
+  in.dmma_flops_per_col_A = 64.0 * (h->tilesA_n / 32);   // 8x4 FMA pairs per lane-step per M-tile
   in.dmma_flops_per_col_WAT = 64.0 * (h->tilesW_n / 32);
   in.op_bytes_A = h->tilesA_n * 8 + (int64_t)h->nitemsA * sizeof(SpmmItem);
   in.op_bytes_WAT = h->tilesW_n * 8 + (int64_t)h->nitemsW * sizeof(SpmmItem);
@@ -651,9 +677,9 @@ xc_status build_impl(xc_kind kind, const xc_params* prm, const double* nodes, in
     flM += (b.fftM.L2 > 1) ? 2 : 1;
     nsplit += b.split ? 1 : 0;
   }
-  auto spmm_launches = [](int n) { return n <= 0 ? 0 : (n + 4 * 65535 - 1) / (4 * 65535); };
-  in.launches_A = (h->dirs & XC_DIR_A) ? spmm_launches(h->nitemsA) + nsplit + flM + (h->tail > 0 ? 1 : 0) : 0;
-  in.launches_WAT = (h->dirs & XC_DIR_WAT) ? spmm_launches(h->nitemsW) + fl + 1 : 0;
+  auto spmm_launches = [](int n) { return n <= 0 ? 0 : (n + 65535 - 1) / 65535; };
+  in.launches_A = (h->dirs & XC_DIR_A) ? spmm_launches(h->nwinsA) + nsplit + flM + (h->tail > 0 ? 1 : 0) : 0;
+  in.launches_WAT = (h->dirs & XC_DIR_WAT) ? spmm_launches(h->nwinsW) + fl + 1 : 0;
   return XC_OK;
 }
 
@@ -715,8 +741,8 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
     s.im[0] = nullptr;
     s.nrows[0] = N;
     s.ld[0] = ldx;
-    XC_TRY(spmm_run((const SpmmItem*)h->itemsA.p, h->nitemsA, (const double*)h->tilesA.p, s,
-                    (double*)h->partA.p, Bp, (int)B, st));
+    XC_TRY(spmm_run((const SpmmWin*)h->winsA.p, h->nwinsA, (const SpmmItem*)h->itemsA.p,
+                    (const double*)h->tilesA.p, s, (double*)h->partA.p, Bp, (int)B, st));
     XC_TRY(mark(1));
     for (auto& b : h->blocks) {
       double* U = (double*)h->partA.p + b.ubase * Bp;
@@ -773,8 +799,8 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
   s.nrows[nb] = h->tail;
   s.ld[nb] = ldx;
   XC_TRY(mark(1));
-  XC_TRY(spmm_run((const SpmmItem*)h->itemsW.p, h->nitemsW, (const double*)h->tilesW.p, s, (double*)h->partW.p,
-                  Bp, (int)B, st));
+  XC_TRY(spmm_run((const SpmmWin*)h->winsW.p, h->nwinsW, (const SpmmItem*)h->itemsW.p,
+                  (const double*)h->tilesW.p, s, (double*)h->partW.p, Bp, (int)B, st));
   XC_TRY(mark(2));
   XC_TRY(reduce_rows8((const double*)h->partW.p, Bp, (const int64_t*)h->nodeg_base.p, (const int*)h->nodeg_nch.p, N,
                       (const double*)h->wt.p, Y, ldy, (int)B, st));
@@ -792,8 +818,8 @@ void destroy_impl(xc_op* h) {
     dev_free(b.start); dev_free(b.len); dev_free(b.off); dev_free(b.vals);
     dev_free(b.grp_base); dev_free(b.grp_nch);
   }
-  DevBuf* all[] = {&h->nodes, &h->wt, &h->tailP, &h->itemsA, &h->tilesA, &h->tail_base, &h->tail_nch,
-                   &h->itemsW, &h->tilesW, &h->nodeg_base, &h->nodeg_nch, &h->partA, &h->partW,
+  DevBuf* all[] = {&h->nodes, &h->wt, &h->tailP, &h->itemsA, &h->tilesA, &h->winsA, &h->tail_base, &h->tail_nch,
+                   &h->itemsW, &h->tilesW, &h->winsW, &h->nodeg_base, &h->nodeg_nch, &h->partA, &h->partW,
                    &h->scratch, &h->zpl, &h->Xh, &h->Yh};
   for (DevBuf* b : all) dev_free(*b);
 }

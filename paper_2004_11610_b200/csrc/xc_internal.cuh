@@ -152,16 +152,25 @@ xc_status fft_run(const FftPlan& p, int sigma, FftPro pro, FftEpi epi, const Fft
 
 // ---------------------------------------------------------------------------
 // SpMM on the FP64 tensor cores (spmm.cu)
-// Each item computes an 8 x (8*NT) output tile  D = A_item (8 x 4*nsteps) * Bm,
-// where row r of Bm is gathered from a source (plain rows or re/im planes).
+// Each item computes two 8 x (8*NT) output tiles D_mt = A_mt (8 x 4*nsteps) * Bm (mt = 0, 1)
+// sharing the B fragments; row R of Bm is gathered from a source (plain rows or re/im planes).
 // ---------------------------------------------------------------------------
 struct SpmmItem {
-  int64_t a_off;    // offset (doubles) of the A tile stream (32 doubles per step)
-  int64_t out_row;  // first of the 8 output rows in the partial-sum array
-  int k0;           // first B row (node, degree or bin) of the item
-  int nsteps;       // 4 B rows per step
-  int src;          // index into SpmmSrcs
-  int cplx;         // 1: output rows are 4 complex bins, stored interleaved (re, im) per column
+  int64_t a_off;      // offset (doubles) of the A stream: 64 doubles per step (2 M-tiles x 32 lanes)
+  int64_t out_row[2]; // first of the 8 output rows of M-tile 0 / 1 (-1: M-tile absent)
+  int k0;             // first B row of the item (B row R -> plane R&1, row R>>1 for re/im sources)
+  int nsteps;         // 4 B rows per step
+  int src;            // index into SpmmSrcs
+  int cplx;           // 1: output rows are 4 complex bins, stored interleaved (re, im) per column
+};
+
+// A window of B rows [r0, r1) (r1 - r0 <= XC_WMAX) and the items [i0, i1) inside it.
+#define XC_WMAX 192
+struct SpmmWin {
+  int r0, r1;
+  int i0, i1;
+  int src;
+  int pad;
 };
 
 #define XC_MAX_SRC 40
@@ -172,8 +181,8 @@ struct SpmmSrcs {
   int64_t ld[XC_MAX_SRC];
 };
 
-xc_status spmm_run(const SpmmItem* items, int nitems, const double* tiles, const SpmmSrcs& srcs,
-                   double* part, int64_t ldp, int ncols, cudaStream_t st);
+xc_status spmm_run(const SpmmWin* wins, int nwins, const SpmmItem* items, const double* tiles,
+                   const SpmmSrcs& srcs, double* part, int64_t ldp, int ncols, cudaStream_t st);
 int spmm_nt_for(int64_t B);
 
 // ---------------------------------------------------------------------------
