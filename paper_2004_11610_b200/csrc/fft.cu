@@ -184,7 +184,7 @@ __device__ __forceinline__ void epi_store(const FftIO& io, int k, int col, doubl
 }
 
 template <int PRO, int EPI, int SIG>
-__global__ void __launch_bounds__(256) fft_pass(PassArgs a, FftIO io) {
+__global__ void __launch_bounds__(256, 3) fft_pass(PassArgs a, FftIO io) {
   extern __shared__ double2 smem[];
   const int nseq = 1 << a.lgn;
   double2* bin = smem;
@@ -198,32 +198,49 @@ __global__ void __launch_bounds__(256) fft_pass(PassArgs a, FftIO io) {
     return p * a.sc + slot;
   };
 
-  // ---- load (prologue): 4 independent global loads in flight per thread ----
+  // ---- load (prologue) ----
   const int total = a.R << a.lgn;
-  for (int base = tid; base < total; base += 4 * nth) {
-    double2 v[4];
+  if (PRO == PRO_XREAL && a.stage != 1) {
+    // real input scaled by W^{-1}: through registers, 4 loads in flight per thread
+    for (int base = tid; base < total; base += 4 * nth) {
+      double2 v[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      int i = base + u * nth;
-      v[u] = make_double2(0.0, 0.0);
-      if (i < total) {
-        int e = i >> a.lgn, sq = i & (nseq - 1);
-        int sub = sub_of(sq >> a.lgcb), col = col0 + (sq & (a.cb - 1));
-        if (sub < a.S && col < a.ncol) {
-          if (a.stage == 1) {
-            v[u] = a.scratch[((int64_t)sub * a.L2 + e) * a.ncol + col];
-          } else {
-            int n = (a.stage == 0) ? a.L2 * e + sub : e;
-            v[u] = pro_load<PRO>(io, n, col);
-          }
+      for (int u = 0; u < 4; ++u) {
+        int i = base + u * nth;
+        v[u] = make_double2(0.0, 0.0);
+        if (i < total) {
+          int e = i >> a.lgn, sq = i & (nseq - 1);
+          int sub = sub_of(sq >> a.lgcb), col = col0 + (sq & (a.cb - 1));
+          if (sub < a.S && col < a.ncol) v[u] = pro_load<PRO>(io, (a.stage == 0) ? a.L2 * e + sub : e, col);
         }
       }
-    }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      int i = base + u * nth;
-      if (i < total) bin[i] = v[u];
+      for (int u = 0; u < 4; ++u) {
+        int i = base + u * nth;
+        if (i < total) bin[i] = v[u];
+      }
     }
+  } else {
+    // complex input: asynchronous 16-byte copies global -> shared, all in flight at once
+    for (int i = tid; i < total; i += nth) {
+      int e = i >> a.lgn, sq = i & (nseq - 1);
+      int sub = sub_of(sq >> a.lgcb), col = col0 + (sq & (a.cb - 1));
+      if (sub < a.S && col < a.ncol) {
+        const double2* g;
+        if (a.stage == 1) {
+          g = a.scratch + ((int64_t)sub * a.L2 + e) * a.ncol + col;
+        } else {
+          int n = (a.stage == 0) ? a.L2 * e + sub : e;
+          g = (PRO == PRO_C2R) ? io.Uc + (int64_t)n * io.ldu + col : io.src + (int64_t)n * io.lds + col;
+        }
+        unsigned sa = (unsigned)__cvta_generic_to_shared(bin + i);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g));
+      } else {
+        bin[i] = make_double2(0.0, 0.0);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
   }
   if (PRO == PRO_C2R && a.stage != 1) {
     if (p == 0)
@@ -368,11 +385,13 @@ int ilog2(int v) {
   return l;
 }
 
-// Tile: nseq = cb * sc sequences of length R in ping-pong smem of 32 R nseq bytes <= 112 KB
-// (two CTAs per SM); cb, sc powers of two.
+// Tile: nseq = cb * sc sequences of length R in ping-pong smem of 32 R nseq bytes;
+// cb, sc powers of two.
+constexpr int kTileElems = 1792;  // R * nseq per CTA: 2 buffers x 16 B -> 56 KB, 3-4 CTAs per SM
+
 void choose_tile(int R, int ncol, int sc, int& cb) {
   int nseq = sc;
-  while (nseq < 16 * sc && 2 * nseq * R <= 3584) nseq *= 2;
+  while (nseq < 16 * sc && 2 * nseq * R <= kTileElems) nseq *= 2;
   cb = nseq / sc;
   while (cb > 1 && cb / 2 >= ncol) cb /= 2;
 }
@@ -467,7 +486,7 @@ xc_status fft_run(const FftPlan& p, int sigma, FftPro pro, FftEpi epi, const Fft
   choose_tile(a.R, ncol, a.sc, a.cb);
   if (!c2r) {  // spread spare sequences over sub-sequences when there are few columns
     int nseq = a.cb;
-    while (nseq < 16 && 2 * nseq * a.R <= 3584) nseq *= 2;
+    while (nseq < 16 && 2 * nseq * a.R <= kTileElems) nseq *= 2;
     a.sc = nseq / a.cb;
   }
   a.lgcb = ilog2(a.cb);
@@ -483,7 +502,7 @@ xc_status fft_run(const FftPlan& p, int sigma, FftPro pro, FftEpi epi, const Fft
   choose_tile(a.R, ncol, 1, a.cb);
   {
     int nseq = a.cb;
-    while (nseq < 16 && 2 * nseq * a.R <= 3584) nseq *= 2;
+    while (nseq < 16 && 2 * nseq * a.R <= kTileElems) nseq *= 2;
     a.sc = nseq / a.cb;
   }
   a.lgcb = ilog2(a.cb);
