@@ -104,12 +104,11 @@ __device__ __forceinline__ void bfly5(double2* v) {
 template <int r, int SIG>
 __device__ __forceinline__ void stockham_stage(const double2* __restrict__ bin, double2* __restrict__ bout, int R,
                                                int Ns, unsigned magic, int lgn, const double2* __restrict__ tw,
-                                               int tid, int nth) {
+                                               int sq, int j0, int jstep) {
+  // this thread's sequence sq is fixed (blockDim is a multiple of nseq); j runs over butterflies
   const int Rr = R / r;
   const int twstep = R / (Ns * r);
-  const int nseq = 1 << lgn;
-  for (int i = tid; i < (Rr << lgn); i += nth) {
-    int j = i >> lgn, sq = i & (nseq - 1);
+  for (int j = j0; j < Rr; j += jstep) {
     int jd = (Ns == 1) ? j : (int)__umulhi((unsigned)j, magic);  // j / Ns
     int k = j - jd * Ns;
     double2 v[r];
@@ -191,80 +190,84 @@ __global__ void __launch_bounds__(256, 3) fft_pass(PassArgs a, FftIO io) {
   double2* bout = smem + a.R * nseq;
   double2* nyq = smem + 2 * a.R * nseq;  // C2R: U[M] per column (cb values)
   const int tid = threadIdx.x, nth = blockDim.x;
-  const int col0 = blockIdx.x * a.cb;
+  // per-thread constants (nth is a multiple of nseq): sequence sq, its slot, sub-sequence and column
+  const int sq = tid & (nseq - 1);
+  const int e0 = tid >> a.lgn, estep = nth >> a.lgn;
+  const int slot = sq >> a.lgcb, cl = sq & (a.cb - 1);
   const int p = blockIdx.y;  // pair index (pairs) or first sub-sequence / sc
-  auto sub_of = [&](int slot) -> int {
-    if (a.pairs) return slot == 0 ? p : (a.S - p) % a.S;
-    return p * a.sc + slot;
-  };
+  int sub;
+  if (a.pairs) {
+    sub = p;
+    if (slot) sub = (p == 0) ? 0 : a.S - p;
+  } else {
+    sub = p * a.sc + slot;
+  }
+  const int col = blockIdx.x * a.cb + cl;
+  const bool valid = sub < a.S && col < a.ncol;
+  const bool dup = a.pairs && slot == 1 && sub == p;  // self-paired sub-sequence: store once
 
   // ---- load (prologue) ----
-  const int total = a.R << a.lgn;
   if (PRO == PRO_XREAL && a.stage != 1) {
-    // real input scaled by W^{-1}: through registers, 4 loads in flight per thread
-    for (int base = tid; base < total; base += 4 * nth) {
+    // real input scaled by W^{-1}: through registers
+    for (int e = e0; e < a.R; e += 4 * estep) {
       double2 v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        int i = base + u * nth;
+        int ee = e + u * estep;
         v[u] = make_double2(0.0, 0.0);
-        if (i < total) {
-          int e = i >> a.lgn, sq = i & (nseq - 1);
-          int sub = sub_of(sq >> a.lgcb), col = col0 + (sq & (a.cb - 1));
-          if (sub < a.S && col < a.ncol) v[u] = pro_load<PRO>(io, (a.stage == 0) ? a.L2 * e + sub : e, col);
-        }
+        if (valid && ee < a.R) v[u] = pro_load<PRO>(io, (a.stage == 0) ? a.L2 * ee + sub : ee, col);
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        int i = base + u * nth;
-        if (i < total) bin[i] = v[u];
+        int ee = e + u * estep;
+        if (ee < a.R) bin[(ee << a.lgn) + sq] = v[u];
       }
     }
-  } else {
+  } else if (valid) {
     // complex input: asynchronous 16-byte copies global -> shared, all in flight at once
-    for (int i = tid; i < total; i += nth) {
-      int e = i >> a.lgn, sq = i & (nseq - 1);
-      int sub = sub_of(sq >> a.lgcb), col = col0 + (sq & (a.cb - 1));
-      if (sub < a.S && col < a.ncol) {
-        const double2* g;
-        if (a.stage == 1) {
-          g = a.scratch + ((int64_t)sub * a.L2 + e) * a.ncol + col;
-        } else {
-          int n = (a.stage == 0) ? a.L2 * e + sub : e;
-          g = (PRO == PRO_C2R) ? io.Uc + (int64_t)n * io.ldu + col : io.src + (int64_t)n * io.lds + col;
-        }
-        unsigned sa = (unsigned)__cvta_generic_to_shared(bin + i);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g));
-      } else {
-        bin[i] = make_double2(0.0, 0.0);
-      }
+    const double2* g;
+    int64_t gstep;
+    if (a.stage == 1) {
+      g = a.scratch + ((int64_t)sub * a.L2) * a.ncol + col;
+      gstep = a.ncol;
+    } else {
+      const int64_t ld = (PRO == PRO_C2R) ? io.ldu : io.lds;
+      const int nstride = (a.stage == 0) ? a.L2 : 1;
+      g = ((PRO == PRO_C2R) ? io.Uc : io.src) + (int64_t)sub * ld + col;
+      gstep = (int64_t)nstride * ld;
+    }
+    for (int e = e0; e < a.R; e += estep) {
+      unsigned sa = (unsigned)__cvta_generic_to_shared(bin + (e << a.lgn) + sq);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g + e * gstep));
     }
     asm volatile("cp.async.commit_group;\n" ::);
     asm volatile("cp.async.wait_all;\n" ::: "memory");
+  } else {
+    for (int e = e0; e < a.R; e += estep) bin[(e << a.lgn) + sq] = make_double2(0.0, 0.0);
   }
   if (PRO == PRO_C2R && a.stage != 1) {
     if (p == 0)
       for (int c = tid; c < a.cb; c += nth)
-        nyq[c] = (col0 + c < a.ncol) ? io.Uc[(int64_t)io.M * io.ldu + col0 + c] : make_double2(0.0, 0.0);
+        nyq[c] = (blockIdx.x * a.cb + c < a.ncol) ? io.Uc[(int64_t)io.M * io.ldu + blockIdx.x * a.cb + c]
+                                                  : make_double2(0.0, 0.0);
     __syncthreads();
     // Real-output inverse DFT of length L = 2M from the half spectrum U[0..M]:
     // Z[n] = (U[n] + conj U[M-n]) + i e^{2 pi i n/L} (U[n] - conj U[M-n]); then z = IDFT_M(Z)
     // gives v[2k] = Re z[k], v[2k+1] = Im z[k].  U[M-n] lives in the paired slot of this CTA.
-    for (int i = tid; i < total; i += nth) {
-      int e = i >> a.lgn, sq = i & (nseq - 1);
-      int slot = sq >> a.lgcb, cl = sq & (a.cb - 1);
-      int sub = sub_of(slot);
-      int n = (a.stage == 0) ? a.L2 * e + sub : e;
-      double2 u = bin[i], v;
+    const int nstride = (a.stage == 0) ? a.L2 : 1;
+    const int osq = ((slot ^ 1) << a.lgcb) + cl;
+    for (int e = e0; e < a.R; e += estep) {
+      int n = nstride * e + sub;
+      double2 u = bin[(e << a.lgn) + sq], v;
       if (sub == 0)
         v = (e == 0) ? nyq[cl] : bin[((a.R - e) << a.lgn) + sq];
       else
-        v = bin[((a.R - 1 - e) << a.lgn) + ((slot ^ 1) << a.lgcb) + cl];
+        v = bin[((a.R - 1 - e) << a.lgn) + osq];
       double2 w = __ldg(io.twh + n);
       double evr = u.x + v.x, evi = u.y - v.y;  // U[n] + conj U[M-n]
       double dr = u.x - v.x, di = u.y + v.y;    // U[n] - conj U[M-n]
       double odr = dr * w.x - di * w.y, odi = dr * w.y + di * w.x;
-      bout[i] = make_double2(evr - odi, evi + odr);
+      bout[(e << a.lgn) + sq] = make_double2(evr - odi, evi + odr);
     }
     double2* t = bin;
     bin = bout;
@@ -278,11 +281,11 @@ __global__ void __launch_bounds__(256, 3) fft_pass(PassArgs a, FftIO io) {
     const int r = a.f[st];
     const unsigned mg = a.magic[st];
     switch (r) {
-      case 2: stockham_stage<2, SIG>(bin, bout, a.R, Ns, mg, a.lgn, a.tw, tid, nth); break;
-      case 3: stockham_stage<3, SIG>(bin, bout, a.R, Ns, mg, a.lgn, a.tw, tid, nth); break;
-      case 4: stockham_stage<4, SIG>(bin, bout, a.R, Ns, mg, a.lgn, a.tw, tid, nth); break;
-      case 5: stockham_stage<5, SIG>(bin, bout, a.R, Ns, mg, a.lgn, a.tw, tid, nth); break;
-      default: stockham_stage<8, SIG>(bin, bout, a.R, Ns, mg, a.lgn, a.tw, tid, nth); break;
+      case 2: stockham_stage<2, SIG>(bin, bout, a.R, Ns, mg, a.lgn, a.tw, sq, e0, estep); break;
+      case 3: stockham_stage<3, SIG>(bin, bout, a.R, Ns, mg, a.lgn, a.tw, sq, e0, estep); break;
+      case 4: stockham_stage<4, SIG>(bin, bout, a.R, Ns, mg, a.lgn, a.tw, sq, e0, estep); break;
+      case 5: stockham_stage<5, SIG>(bin, bout, a.R, Ns, mg, a.lgn, a.tw, sq, e0, estep); break;
+      default: stockham_stage<8, SIG>(bin, bout, a.R, Ns, mg, a.lgn, a.tw, sq, e0, estep); break;
     }
     __syncthreads();
     double2* t = bin;
@@ -292,23 +295,19 @@ __global__ void __launch_bounds__(256, 3) fft_pass(PassArgs a, FftIO io) {
   }
 
   // ---- store (epilogue) ----
-  for (int i = tid; i < total; i += nth) {
-    int e = i >> a.lgn, sq = i & (nseq - 1);
-    int slot = sq >> a.lgcb;
-    int sub = sub_of(slot), col = col0 + (sq & (a.cb - 1));
-    if (sub >= a.S || col >= a.ncol) continue;
-    if (a.pairs && slot == 1 && sub == sub_of(0)) continue;  // self-paired sub-sequence
-    double2 v = bin[i];
-    if (a.stage == 0) {
-      // four-step twiddle w_L^{sigma n2 k1}: n2 = sub, k1 = e
-      int idx = (int)(((int64_t)sub * e) % a.L);
-      double2 w = a.twL[idx];
+  if (!valid || dup) return;
+  if (a.stage == 0) {
+    // four-step twiddle w_L^{sigma n2 k1}, n2 = sub, k1 = e (n2 k1 < L)
+    double2* dstp = a.scratch + (int64_t)sub * a.ncol + col;
+    const int64_t dstep = (int64_t)a.L2 * a.ncol;
+    for (int e = e0; e < a.R; e += estep) {
+      double2 w = __ldg(a.twL + sub * e);
       if (SIG < 0) w.y = -w.y;
-      a.scratch[((int64_t)e * a.L2 + sub) * a.ncol + col] = c_mul(v, w);
-    } else {
-      int k = (a.stage == 1) ? sub + a.L1 * e : e;
-      epi_store<EPI>(io, k, col, v);
+      dstp[e * dstep] = c_mul(bin[(e << a.lgn) + sq], w);
     }
+  } else {
+    const int kstride = (a.stage == 1) ? a.L1 : 1;
+    for (int e = e0; e < a.R; e += estep) epi_store<EPI>(io, sub + kstride * e, col, bin[(e << a.lgn) + sq]);
   }
 }
 
