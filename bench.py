@@ -94,16 +94,27 @@ def _nodes(cfg, device):
     return x, wt
 
 
-def cpu_oracle_rate(cfg, ncols, ndeg, threads):
+def _timing_nodes(cfg):
+    """Nodes for the CPU timing legs only (the dense product's cost does not depend on node
+    accuracy): scipy's Gauss rules (library routines), not the product."""
+    import scipy.special
+    if cfg.kind == I.KIND_COS:
+        return I.cos_nodes(cfg.N, cfg.seed)
+    if cfg.kind == I.KIND_LAGUERRE:
+        return np.linspace(0.0, 4.0 * cfg.N, cfg.N)   # scipy's Laguerre rule overflows at this N
+    if cfg.alpha == 0.0 and cfg.beta == 0.0:
+        return scipy.special.roots_legendre(cfg.N)[0]
+    return scipy.special.roots_jacobi(cfg.N, cfg.alpha, cfg.beta)[0]
+
+
+def cpu_oracle_rate(cfg, ncols, ndeg, threads, x=None):
     """The oracle's dense direct product (the paper's 'direct method') on a bounded
     sample: ncols columns x output degrees [0, ndeg); rate extrapolated per full transform."""
     import oracle as O
     os.environ["OMP_NUM_THREADS"] = str(threads)
     kind = O.Kind(cfg.kind, cfg.alpha, cfg.beta)
-    if cfg.kind == I.KIND_COS:
-        x = I.cos_nodes(cfg.N, cfg.seed)
-    else:
-        x, _, _ = O.gauss_rule(kind, cfg.N)
+    if x is None:
+        x = _timing_nodes(cfg)
     X = I.config_rhs(cfg, B=max(ncols, 1))[:, :ncols]
     t0 = time.perf_counter()
     O.dense_apply_rows(kind, x, X, ndeg)
@@ -117,9 +128,10 @@ def run_reference(args, cfg, ws, rank):
         return
     threads = os.cpu_count() or 1
     ncols, ndeg = 4, min(cfg.N, 4096)
+    x = _timing_nodes(cfg)
     rates = []
     for i in range(args.warmup + args.steps):
-        r, dt = cpu_oracle_rate(cfg, ncols, ndeg, threads)
+        r, dt = cpu_oracle_rate(cfg, ncols, ndeg, threads, x)
         if i >= args.warmup:
             rates.append(r)
     v = float(np.median(rates))
@@ -132,6 +144,11 @@ def run_reference(args, cfg, ws, rank):
                              "sample": sample},
             "e2e": {"value": v, "unit": "transforms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def sum_cols(B):
+    from paper_2004_11610_b200.shard import sum_over_ranks
+    return sum_over_ranks(B, device="cuda")
 
 
 def main():
@@ -177,9 +194,14 @@ def main():
     info = T.info()
 
     # ---- inputs: seeded on the host, this rank's shard, resident in HBM ----
-    Xh = I.config_rhs(cfg, B=B)
-    if ws > 1:
-        # rank g applies its own shard: the same generator with a rank-offset seed
+    from paper_2004_11610_b200.shard import column_shard, max_over_ranks
+    if ws == 1:
+        Xh = I.config_rhs(cfg, B=B)
+    elif args.strong:
+        Xh = np.ascontiguousarray(I.config_rhs(cfg)[:, column_shard(cfg.B, rank, ws)])
+        B = Xh.shape[1]
+    else:
+        # weak scaling: rank g applies its own B columns (same generator, rank-offset seed)
         rng = np.random.default_rng(cfg.seed * 1000 + rank)
         Xh = rng.standard_normal((cfg.N, B))
     X = torch.from_numpy(Xh).cuda()
@@ -210,11 +232,8 @@ def main():
     prof = T.profile_read()
     T.profile(False)
     clk = clocks.stop() if clocks else None
-    if dist:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    total_cols = B * ws
+    ms = max_over_ranks(ms, device="cuda")
+    total_cols = int(round(sum_cols(B)))
     value = total_cols / (ms / 1e3)
 
     # ---- roofline of the dominant kernel (SpMM on the FP64 tensor cores) ----
@@ -242,12 +261,9 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1) / args.e2e_steps
-        if dist:
-            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = max_over_ranks(ems, device="cuda")
         e2e = {"value": total_cols / (ems / 1e3), "unit": "transforms/s",
-               "h2d_bytes_per_step": int(Xh.nbytes) * ws, "d2h_bytes_per_step": int(Xh.nbytes) * ws,
+               "h2d_bytes_per_step": int(sum_cols(Xh.nbytes)), "d2h_bytes_per_step": int(sum_cols(Xh.nbytes)),
                "ms_per_step": ems, "api": "xc_apply_host (pinned host buffers)"}
 
     cpu = None

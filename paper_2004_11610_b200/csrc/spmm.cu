@@ -41,7 +41,8 @@ template <int NT>
 __global__ void __launch_bounds__(WARPS * 32, 2)
     spmm_win(const SpmmWin* __restrict__ wins, const SpmmItem* __restrict__ items,
              const double* __restrict__ tiles, SpmmSrcs srcs, double* __restrict__ part, int64_t ldp, int ncols) {
-  constexpr int CW = 8 * NT;  // columns per tile
+  constexpr int CW = 8 * NT;   // columns per tile
+  constexpr int CWP = CW + 4;  // padded smem row: the 4 rows of a B fragment fall in distinct banks
   extern __shared__ double2 xs2[];
   const double* xs = reinterpret_cast<const double*>(xs2);
   const SpmmWin W = wins[blockIdx.y];
@@ -66,7 +67,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
         const double* src = (im && (R & 1)) ? im : re;
         double2 v = make_double2(0.0, 0.0);
         if (row < nrows) v = __ldg(reinterpret_cast<const double2*>(src + (int64_t)row * ld + tile0) + c2);
-        xs2[idx] = v;
+        xs2[rl * (CWP / 2) + c2] = v;
       }
     } else {
       double* xw = reinterpret_cast<double*>(xs2);
@@ -75,7 +76,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
         int R = W.r0 + rl;
         int row = im ? (R >> 1) : R;
         const double* src = (im && (R & 1)) ? im : re;
-        xw[idx] = (row < nrows && tile0 + c < ncols) ? __ldg(src + (int64_t)row * ld + tile0 + c) : 0.0;
+        xw[rl * CWP + c] = (row < nrows && tile0 + c < ncols) ? __ldg(src + (int64_t)row * ld + tile0 + c) : 0.0;
       }
     }
   }
@@ -92,13 +93,13 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
 #pragma unroll
       for (int i = 0; i < NT; ++i) acc[m][i][0] = acc[m][i][1] = 0.0;
     const double2* ap = reinterpret_cast<const double2*>(tiles + it.a_off) + lane;
-    const double* xb = xs + (it.k0 - W.r0 + t) * CW + bcol;
+    const double* xb = xs + (it.k0 - W.r0 + t) * CWP + bcol;
     const int n = it.nsteps;
     double2 a0 = n > 0 ? __ldg(ap) : make_double2(0.0, 0.0);
     double2 a1 = n > 1 ? __ldg(ap + 32) : make_double2(0.0, 0.0);
     double b0[NT], b1[NT];
     auto lds_b = [&](int s, double* bv) {
-      const double* p = xb + 4 * s * CW;
+      const double* p = xb + 4 * s * CWP;
       if (NT == 1) {
         bv[0] = p[0];
       } else {
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
 template <int NT>
 xc_status launch(const SpmmWin* wins, int nwins, const SpmmItem* items, const double* tiles, const SpmmSrcs& srcs,
                  double* part, int64_t ldp, int ncols, cudaStream_t st) {
-  const size_t sm = (size_t)XC_WMAX * 8 * NT * sizeof(double);
+  const size_t sm = (size_t)XC_WMAX * (8 * NT + 4) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     XC_CUDA(cudaFuncSetAttribute(spmm_win<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
