@@ -1,0 +1,470 @@
+// c2r.cu -- the output-axis inverse DFT of the computation stage (Alg. 2 steps 2.1-2.2,
+// P:217-219; real case P:444; Fe2 discard + W^{-1}), as persistent,
+// prefetching passes over the RHS batch.
+//
+// v = F*_L u for a real output of length L = 2M from the half spectrum u_0..u_M:
+//   Z[n] = (u_n + conj u_{M-n}) + i e^{2 pi i n/L} (u_n - conj u_{M-n}),  n < M
+//   z = IDFT_M(Z),  v[2k] = Re z_k,  v[2k+1] = Im z_k
+// and Y[p + m_off] = v[p] * yscale[p] for the kept positions p (yscale = 1/(sqrt(L) w_p)).
+// M <= 512 runs in one pass; longer M = L1 * L2 as a four-step pair of passes
+//   pass 0: for each n2, the L1-point IDFT over n = L2 n1 + n2 (pairing fused in its first
+//           radix stage), times e^{2 pi i n2 k1 / M}, to scratch row k1 L2 + n2;
+//   pass 1: for each k1, the L2-point IDFT over scratch rows k1 L2 + n2, output
+//           k = k1 + L1 k2 written as Y rows 2k, 2k+1 (scale, truncate).
+//
+// Design (sm_100a, HBM-bound): a tile is `nseq` = cb columns x sc sub-sequences of R
+// points (R * nseq <= 2048, 32 KB).  Each CTA is persistent over tiles and keeps two
+// buffers: LD (the tile being loaded by cp.async) and WK (the tile being transformed).
+// The first radix stage reads LD (and forms Z there), so LD is free after it and the
+// next tile's loads are issued immediately -- they stay in flight during the remaining
+// stages and the epilogue.  Middle stages run in place in WK (read, barrier, write);
+// the last stage writes global memory straight from registers (columns are the fast
+// index, so every store is a contiguous run of cb * 16 or cb * 8 bytes).
+#include <algorithm>
+
+#include "xc_internal.cuh"
+
+namespace {
+
+constexpr int NTH = 256;   // threads per CTA
+constexpr int TILE = 2048; // R * nseq per buffer (32 KB); 2 buffers -> 3 CTAs per SM
+
+__device__ __forceinline__ double2 c_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 c_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 c_mul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 c_ip(double2 a) { return make_double2(-a.y, a.x); }  // +i a
+
+// Inverse-direction (+) butterflies
+__device__ __forceinline__ void bf2(double2* v) {
+  double2 t = c_sub(v[0], v[1]);
+  v[0] = c_add(v[0], v[1]);
+  v[1] = t;
+}
+__device__ __forceinline__ void bf4(double2& v0, double2& v1, double2& v2, double2& v3) {
+  double2 a = c_add(v0, v2), b = c_sub(v0, v2), c = c_add(v1, v3), d = c_ip(c_sub(v1, v3));
+  v0 = c_add(a, c);
+  v2 = c_sub(a, c);
+  v1 = c_add(b, d);
+  v3 = c_sub(b, d);
+}
+__device__ __forceinline__ void bf8(double2* v) {
+  const double R2 = 0.70710678118654752440;
+  double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+  double2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+  bf4(e0, e1, e2, e3);
+  bf4(o0, o1, o2, o3);
+  o1 = make_double2(R2 * (o1.x - o1.y), R2 * (o1.y + o1.x));
+  o2 = c_ip(o2);
+  o3 = make_double2(R2 * (-o3.x - o3.y), R2 * (-o3.y + o3.x));
+  v[0] = c_add(e0, o0);
+  v[4] = c_sub(e0, o0);
+  v[1] = c_add(e1, o1);
+  v[5] = c_sub(e1, o1);
+  v[2] = c_add(e2, o2);
+  v[6] = c_sub(e2, o2);
+  v[3] = c_add(e3, o3);
+  v[7] = c_sub(e3, o3);
+}
+__device__ __forceinline__ void bf3(double2* v) {
+  const double C = -0.5, SN = 0.86602540378443864676;
+  double2 a = c_add(v[1], v[2]), b = c_sub(v[1], v[2]);
+  double2 m = make_double2(v[0].x + C * a.x, v[0].y + C * a.y);
+  double2 ib = make_double2(-SN * b.y, SN * b.x);
+  v[0] = c_add(v[0], a);
+  v[1] = c_add(m, ib);
+  v[2] = c_sub(m, ib);
+}
+__device__ __forceinline__ void bf5(double2* v) {
+  const double C1 = 0.30901699437494742410, C2 = -0.80901699437494742410;
+  const double S1 = 0.95105651629515357212, S2 = 0.58778525229247312917;
+  double2 a1 = c_add(v[1], v[4]), b1 = c_sub(v[1], v[4]);
+  double2 a2 = c_add(v[2], v[3]), b2 = c_sub(v[2], v[3]);
+  double2 x0 = v[0];
+  double2 m1 = make_double2(x0.x + C1 * a1.x + C2 * a2.x, x0.y + C1 * a1.y + C2 * a2.y);
+  double2 m2 = make_double2(x0.x + C2 * a1.x + C1 * a2.x, x0.y + C2 * a1.y + C1 * a2.y);
+  double2 t1 = make_double2(S1 * b1.x + S2 * b2.x, S1 * b1.y + S2 * b2.y);
+  double2 t2 = make_double2(S2 * b1.x - S1 * b2.x, S2 * b1.y - S1 * b2.y);
+  v[0] = make_double2(x0.x + a1.x + a2.x, x0.y + a1.y + a2.y);
+  v[1] = make_double2(m1.x - t1.y, m1.y + t1.x);
+  v[4] = make_double2(m1.x + t1.y, m1.y - t1.x);
+  v[2] = make_double2(m2.x - t2.y, m2.y + t2.x);
+  v[3] = make_double2(m2.x + t2.y, m2.y - t2.x);
+}
+template <int r>
+__device__ __forceinline__ void bfly(double2* v) {
+  if (r == 2) bf2(v);
+  else if (r == 3) bf3(v);
+  else if (r == 4) bf4(v[0], v[1], v[2], v[3]);
+  else if (r == 5) bf5(v);
+  else bf8(v);
+}
+
+struct StageC {
+  int r, Rr, Ns, twstep;  // radix, butterflies per sequence R/r, span Ns, twiddle stride R/(Ns r)
+  unsigned magic;         // ceil(2^32 / Ns): j / Ns by __umulhi (exact for j < 2^16)
+};
+
+struct C2RArgs {
+  int mode;              // 0: first of two, 1: second of two, 2: single pass
+  int R, nf;             // sub-transform length and its radix stages
+  StageC st[12];
+  const double2* tw;     // e^{+2 pi i n / R}
+  const double2* twL;    // e^{+2 pi i n / M} (pass 0 four-step twiddle)
+  int M, L1, L2;
+  int S;                 // sub-sequences per column
+  int P;                 // slot pairs per column (pass 0)
+  int ncol, cb, lgcb, sc, lgn;
+  int ntx, ntiles;
+  double2* scr;          // four-step scratch, row (k1 L2 + n2), ld = lds (offsets < 2^31)
+  int lds;
+};
+
+// Per-thread view of the current tile (offsets in elements; all < 2^31, checked on the host).
+struct Slot {
+  int sub;      // sub-sequence of this thread's sequence (clamped to 0 when invalid)
+  int col;
+  bool valid;
+  int pmode;    // 0: partner element R-e in own sequence (sub 0; e = 0 -> Nyquist), 1: R-1-e own, 2: R-1-e other slot
+  int psq;      // partner's sequence index (own or other slot)
+};
+
+template <int MODE>
+__device__ __forceinline__ Slot slot_of(const C2RArgs& a, int tile, int sq) {
+  Slot s;
+  const int gy = tile / a.ntx;
+  const int gx = tile - gy * a.ntx;
+  const int sl = sq >> a.lgcb, cl = sq & (a.cb - 1);
+  s.col = gx * a.cb + cl;
+  int sub;
+  if (MODE == 0) {
+    const int p = gy * (a.sc >> 1) + (sl >> 1);
+    const int which = sl & 1;
+    sub = -1;
+    if (p < a.P) {
+      if (p == 0) sub = which ? ((a.S & 1) ? -1 : a.S / 2) : 0;
+      else sub = which ? a.S - p : p;
+    }
+    s.pmode = (sub == 0) ? 0 : ((2 * sub == a.S) ? 1 : 2);
+  } else if (MODE == 1) {
+    sub = gy * a.sc + sl;
+    if (sub >= a.S) sub = -1;
+    s.pmode = 0;
+  } else {
+    sub = 0;
+    s.pmode = 0;
+  }
+  s.valid = sub >= 0 && s.col < a.ncol;
+  s.sub = s.valid ? sub : 0;
+  if (!s.valid) s.col = 0;
+  s.psq = (s.pmode == 2) ? (sq ^ a.cb) : sq;
+  return s;
+}
+
+__device__ __forceinline__ void cp16(double2* dst, const double2* src, bool v) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(v ? 16 : 0));
+}
+
+template <int MODE>
+__device__ __forceinline__ void issue_loads(const C2RArgs& a, const FftIO& io, int tile, double2* ld, double2* nyq,
+                                            int sq, int e0, int estep) {
+  Slot s = slot_of<MODE>(a, tile, sq);
+  const double2* g;
+  int gstep;
+  if (MODE == 0) {
+    g = io.Uc + (size_t)((unsigned)s.sub * (unsigned)io.ldu + s.col);
+    gstep = a.L2 * (int)io.ldu;
+  } else if (MODE == 1) {
+    g = a.scr + (size_t)((unsigned)s.sub * (unsigned)(a.L2 * a.lds) + s.col);
+    gstep = a.lds;
+  } else {
+    g = io.Uc + s.col;
+    gstep = (int)io.ldu;
+  }
+  double2* d = ld + (e0 << a.lgn) + sq;
+  const int dstep = estep << a.lgn;
+  for (int e = e0; e < a.R; e += estep, d += dstep) cp16(d, g + (size_t)((unsigned)e * (unsigned)gstep), s.valid);
+  if (MODE != 1 && e0 == 0) {
+    const bool v = s.valid && s.sub == 0;
+    cp16(nyq + sq, io.Uc + (size_t)((unsigned)a.M * (unsigned)io.ldu + s.col), v);
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+
+// Z[e] of this thread's sequence (pairing of the half spectrum); branch-free.
+template <int MODE>
+__device__ __forceinline__ double2 zval(const C2RArgs& a, const FftIO& io, const double2* ld, const double2* nyq,
+                                        const Slot& s, int sq, int e) {
+  double2 u = ld[(e << a.lgn) + sq];
+  const int pe = (s.pmode == 0) ? a.R - e : a.R - 1 - e;   // pe == R only for pmode 0, e == 0
+  const double2* pp = (pe == a.R) ? nyq + sq : ld + (pe << a.lgn) + s.psq;
+  double2 v = *pp;
+  const int n = (MODE == 0) ? a.L2 * e + s.sub : e;
+  double2 w = __ldg(io.twh + n);
+  double evr = u.x + v.x, evi = u.y - v.y;  // u_n + conj u_{M-n}
+  double dr = u.x - v.x, di = u.y + v.y;    // u_n - conj u_{M-n}
+  double odr = dr * w.x - di * w.y, odi = dr * w.y + di * w.x;
+  return make_double2(evr - odi, evi + odr);
+}
+
+// Epilogue context: per-tile base offsets so each store is one 32-bit multiply-add.
+struct Epi {
+  int base;   // MODE 0: sub * lds + col (scratch); MODE 1/2: column col of Y row 0 (+ m_off)
+  int kstep;  // MODE 0: L2 * lds;   MODE 1/2: output k advances by L1 (MODE 1) or 1 per kk
+};
+
+template <int MODE>
+__device__ __forceinline__ void store_out(const C2RArgs& a, const FftIO& io, const Slot& s, const Epi& ep, int kk,
+                                          double2 v, bool act) {
+  if (MODE == 0) {
+    double2 w = __ldg(a.twL + s.sub * kk);
+    if (act) a.scr[(unsigned)(ep.base + kk * ep.kstep)] = c_mul(v, w);
+  } else {
+    const int k = (MODE == 1) ? s.sub + a.L1 * kk : kk;
+    const int p = 2 * k;
+    double* y = io.Y + (size_t)(unsigned)(ep.base + p * (int)io.ldy);
+    if (act && p >= io.keep_lo && p < io.keep_hi) __stcs(y, v.x * __ldg(io.yscale + p));
+    if (act && p + 1 >= io.keep_lo && p + 1 < io.keep_hi) __stcs(y + io.ldy, v.y * __ldg(io.yscale + p + 1));
+  }
+}
+
+enum { IN_Z = 0, IN_LD = 1, IN_WK = 2 };
+enum { OUT_WK = 0, OUT_G = 1 };
+
+// One Stockham radix-r stage for this thread's sequence: butterflies j = e0 + b*estep < R/r.
+// Out-of-range butterflies of the last round are computed on a clamped (valid) index and
+// their stores suppressed, so there is no divergent control flow inside the stage.
+template <int r, int IN, int OUT, int MODE, bool FIRST>
+__device__ __forceinline__ void stage(const C2RArgs& a, const FftIO& io, const double2* ld, const double2* nyq,
+                                      double2* wk, const Slot& s, const Epi& ep, int sq, int e0, int estep,
+                                      const StageC& c) {
+  constexpr int MB = (TILE / NTH + r - 1) / r;  // butterflies per thread (R * nseq <= TILE)
+  const int lgn = a.lgn;
+  double2 v[MB][r];
+  bool act[MB];
+  int jj[MB];
+#pragma unroll
+  for (int b = 0; b < MB; ++b) {
+    const int j = e0 + b * estep;
+    act[b] = j < c.Rr;
+    jj[b] = act[b] ? j : c.Rr - 1;
+#pragma unroll
+    for (int t = 0; t < r; ++t) {
+      const int e = jj[b] + t * c.Rr;
+      if (IN == IN_Z) v[b][t] = zval<MODE>(a, io, ld, nyq, s, sq, e);
+      else if (IN == IN_LD) v[b][t] = ld[(e << lgn) + sq];
+      else v[b][t] = wk[(e << lgn) + sq];
+    }
+  }
+  if (IN == IN_WK && OUT == OUT_WK) __syncthreads();  // in place: all reads before any write
+#pragma unroll
+  for (int b = 0; b < MB; ++b) {
+    int jd = jj[b], k = 0;
+    if (!FIRST) {
+      jd = (int)__umulhi((unsigned)jj[b], c.magic);
+      k = jj[b] - jd * c.Ns;
+      const double2 w = __ldg(a.tw + k * c.twstep);  // tw[0] = 1
+      double2 wt = w;
+#pragma unroll
+      for (int t = 1; t < r; ++t) {
+        v[b][t] = c_mul(v[b][t], wt);
+        if (t + 1 < r) wt = c_mul(wt, w);
+      }
+    }
+    bfly<r>(v[b]);
+    const int idxD = FIRST ? jd * r : jd * c.Ns * r + k;
+    const int ustep = FIRST ? 1 : c.Ns;
+    const bool gact = act[b] && s.valid;
+#pragma unroll
+    for (int u = 0; u < r; ++u) {
+      if (OUT == OUT_WK) {
+        if (act[b]) wk[((idxD + u * ustep) << lgn) + sq] = v[b][u];
+      } else {
+        store_out<MODE>(a, io, s, ep, idxD + u * ustep, v[b][u], gact);
+      }
+    }
+  }
+}
+
+template <int IN, int OUT, int MODE, bool FIRST>
+__device__ __forceinline__ void stage_r(const C2RArgs& a, const FftIO& io, const double2* ld, const double2* nyq,
+                                        double2* wk, const Slot& s, const Epi& ep, int sq, int e0, int estep,
+                                        const StageC& c) {
+  switch (c.r) {
+    case 2: stage<2, IN, OUT, MODE, FIRST>(a, io, ld, nyq, wk, s, ep, sq, e0, estep, c); break;
+    case 3: stage<3, IN, OUT, MODE, FIRST>(a, io, ld, nyq, wk, s, ep, sq, e0, estep, c); break;
+    case 4: stage<4, IN, OUT, MODE, FIRST>(a, io, ld, nyq, wk, s, ep, sq, e0, estep, c); break;
+    case 5: stage<5, IN, OUT, MODE, FIRST>(a, io, ld, nyq, wk, s, ep, sq, e0, estep, c); break;
+    default: stage<8, IN, OUT, MODE, FIRST>(a, io, ld, nyq, wk, s, ep, sq, e0, estep, c); break;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(NTH, 3) c2r_pass(const __grid_constant__ C2RArgs a, const __grid_constant__ FftIO io) {
+  extern __shared__ double2 smem[];
+  double2* ld = smem;
+  double2* wk = smem + TILE;
+  double2* nyq = smem + 2 * TILE;  // nseq values
+  const int tid = threadIdx.x;
+  const int sq = tid & ((1 << a.lgn) - 1);
+  const int e0 = tid >> a.lgn, estep = NTH >> a.lgn;
+  constexpr int IN0 = (MODE == 1) ? IN_LD : IN_Z;
+
+  int tile = blockIdx.x;
+  if (tile < a.ntiles) issue_loads<MODE>(a, io, tile, ld, nyq, sq, e0, estep);
+  for (; tile < a.ntiles; tile += gridDim.x) {
+    const Slot s = slot_of<MODE>(a, tile, sq);
+    Epi ep;
+    if (MODE == 0) {
+      ep.base = s.sub * a.lds + s.col;
+      ep.kstep = a.L2 * a.lds;
+    } else {
+      ep.base = io.m_off * (int)io.ldy + s.col;
+      ep.kstep = 0;
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();  // LD (and nyq) complete for every thread; WK free (previous tile done)
+    if (a.nf == 1) {
+      stage_r<IN0, OUT_G, MODE, true>(a, io, ld, nyq, wk, s, ep, sq, e0, estep, a.st[0]);
+      __syncthreads();
+      if (tile + (int)gridDim.x < a.ntiles) issue_loads<MODE>(a, io, tile + gridDim.x, ld, nyq, sq, e0, estep);
+      continue;
+    }
+    stage_r<IN0, OUT_WK, MODE, true>(a, io, ld, nyq, wk, s, ep, sq, e0, estep, a.st[0]);
+    __syncthreads();  // LD consumed, WK written
+    if (tile + (int)gridDim.x < a.ntiles) issue_loads<MODE>(a, io, tile + gridDim.x, ld, nyq, sq, e0, estep);
+    for (int st = 1; st + 1 < a.nf; ++st) {
+      stage_r<IN_WK, OUT_WK, MODE, false>(a, io, ld, nyq, wk, s, ep, sq, e0, estep, a.st[st]);
+      __syncthreads();
+    }
+    stage_r<IN_WK, OUT_G, MODE, false>(a, io, ld, nyq, wk, s, ep, sq, e0, estep, a.st[a.nf - 1]);
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+int ilog2i(int v) {
+  int l = 0;
+  while ((1 << (l + 1)) <= v) ++l;
+  return l;
+}
+
+int g_nsm = 0;
+
+void set_radices(C2RArgs& a, int nf, const int* f) {
+  a.nf = nf;
+  int Ns = 1;
+  for (int i = 0; i < nf; ++i) {
+    StageC& c = a.st[i];
+    c.r = f[i];
+    c.Rr = a.R / f[i];
+    c.Ns = Ns;
+    c.twstep = a.R / (Ns * f[i]);
+    c.magic = (Ns == 1) ? 0u : (unsigned)((0x100000000ULL + Ns - 1) / Ns);
+    Ns *= f[i];
+  }
+}
+
+// nseq = cb * sc (powers of two) with R * nseq <= TILE; columns first (cb <= 16), sc >= smin.
+void choose(C2RArgs& a, int smin) {
+  int nseq = 1;
+  while (2 * nseq * a.R <= TILE && nseq < NTH && nseq < smin * a.S * std::max(1, a.ncol)) nseq *= 2;
+  int cb = 1;
+  while (cb < a.ncol && cb < 16 && 2 * cb * smin <= nseq) cb *= 2;
+  a.cb = cb;
+  a.sc = nseq / cb;
+  a.lgcb = ilog2i(cb);
+  a.lgn = ilog2i(nseq);
+}
+
+template <int MODE>
+xc_status launch(C2RArgs& a, const FftIO& io, cudaStream_t st) {
+  const size_t sm = (2 * TILE + 256) * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    XC_CUDA(cudaFuncSetAttribute(c2r_pass<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int dev = 0;
+    XC_CUDA(cudaGetDevice(&dev));
+    XC_CUDA(cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, dev));
+    attr = true;
+  }
+  a.ntx = (a.ncol + a.cb - 1) / a.cb;
+  int nty;
+  if (MODE == 0) nty = (a.P + a.sc / 2 - 1) / (a.sc / 2);
+  else if (MODE == 1) nty = (a.S + a.sc - 1) / a.sc;
+  else nty = 1;
+  a.ntiles = a.ntx * nty;
+  const int grid = std::min(a.ntiles, 3 * std::max(1, g_nsm));
+  c2r_pass<MODE><<<grid, NTH, sm, st>>>(a, io);
+  XC_CUDA(cudaGetLastError());
+  return XC_OK;
+}
+
+}  // namespace
+
+int c2r_launches(const FftPlan& p) { return p.L2 > 1 ? 2 : 1; }
+
+xc_status c2r_run(const FftPlan& p, const FftIO& io, int ncol, double2* scratch, cudaStream_t st) {
+  C2RArgs a{};
+  // 32-bit element offsets inside the kernels
+  if ((int64_t)p.L * ncol >= (1LL << 31) || (int64_t)(io.keep_hi + io.m_off + 1) * io.ldy >= (1LL << 31) ||
+      (int64_t)(p.L + 1) * io.ldu >= (1LL << 31)) {
+    xc_set_error("c2r: batch too large for 32-bit offsets (split the batch)");
+    return XC_EUNSUPPORTED;
+  }
+  a.M = p.L;
+  a.L1 = p.L1;
+  a.L2 = p.L2;
+  a.ncol = ncol;
+  a.scr = scratch;
+  a.lds = ncol;
+  a.twL = p.twL;
+  if (p.L2 == 1) {
+    a.mode = 2;
+    a.R = p.L1;
+    a.S = 1;
+    set_radices(a, p.nf1, p.f1);
+    a.tw = p.tw1;
+    // one sequence per column: every slot is a column
+    int nseq = 1;
+    while (2 * nseq * a.R <= TILE && nseq < NTH && nseq < ncol) nseq *= 2;
+    a.cb = nseq;
+    a.sc = 1;
+    a.lgcb = a.lgn = ilog2i(nseq);
+    if (a.R * nseq > TILE) {
+      xc_set_error("c2r: length too long for one pass");
+      return XC_EUNSUPPORTED;
+    }
+    return launch<2>(a, io, st);
+  }
+  if (!scratch) {
+    xc_set_error("c2r: two-pass length needs scratch");
+    return XC_EINVAL;
+  }
+  // pass 0: L1-point transforms over the L2 sub-sequences, slots paired {p, L2 - p}
+  a.mode = 0;
+  a.R = p.L1;
+  a.S = p.L2;
+  a.P = (a.S & 1) ? (a.S + 1) / 2 : a.S / 2;
+  set_radices(a, p.nf1, p.f1);
+  a.tw = p.tw1;
+  choose(a, 2);
+  if (a.sc < 2 || a.R * (1 << a.lgn) > TILE) {
+    xc_set_error("c2r: first-pass length too long");
+    return XC_EUNSUPPORTED;
+  }
+  XC_TRY(launch<0>(a, io, st));
+  // pass 1: L2-point transforms over the L1 sub-sequences
+  a.mode = 1;
+  a.R = p.L2;
+  a.S = p.L1;
+  set_radices(a, p.nf2, p.f2);
+  a.tw = p.tw2;
+  choose(a, 1);
+  if (a.R * (1 << a.lgn) > TILE) {
+    xc_set_error("c2r: second-pass length too long");
+    return XC_EUNSUPPORTED;
+  }
+  return launch<1>(a, io, st);
+}

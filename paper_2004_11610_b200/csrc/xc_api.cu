@@ -761,7 +761,7 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
       io.keep_lo = b.keep_lo;
       io.keep_hi = b.keep_hi;
       io.m_off = b.m_off;
-      XC_TRY(fft_run(b.fftM, +1, PRO_C2R, EPI_C2R, io, (int)B, (double2*)h->scratch.p, st));
+      XC_TRY(c2r_run(b.fftM, io, (int)B, (double2*)h->scratch.p, st));
     }
     XC_TRY(mark(2));
     if (h->tail > 0)

@@ -149,6 +149,9 @@ void fft_plan_free(FftPlan& p);
 // sigma = -1 forward (Eq. 1), +1 inverse.  ncol columns.  scratch: L*ncol double2 (2-pass only).
 xc_status fft_run(const FftPlan& p, int sigma, FftPro pro, FftEpi epi, const FftIO& io, int ncol,
                   double2* scratch, cudaStream_t st);
+// Output-axis real-output inverse (c2r.cu): persistent prefetching passes, half spectrum
+// io.Uc (ldu) -> Y rows (io.Y, ldy) with the W^{-1}/truncate epilogue.  scratch: M*ncol double2.
+xc_status c2r_run(const FftPlan& p, const FftIO& io, int ncol, double2* scratch, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // SpMM on the FP64 tensor cores (spmm.cu)
