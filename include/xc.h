@@ -117,7 +117,10 @@ xc_status xc_apply(xc_handle h, xc_dir dir, const double* X, int64_t ldx, double
 
 /* Same as xc_apply with HOST buffers X_host, Y_host (row-major N x B, ld = B):
  * copies X to the device, applies, copies Y back, and synchronises `stream`.
- * Host buffers should be pinned for full bandwidth. */
+ * The batch is processed in column chunks (about B/16 columns, a multiple of 64) through a
+ * pipeline: host-to-device copy, apply, device-to-host copy on three streams, so both copy
+ * directions and the apply overlap.  Work already queued on `stream` is ordered before it.
+ * Host buffers should be pinned for full bandwidth and must not overlap. */
 xc_status xc_apply_host(xc_handle h, xc_dir dir, const double* X_host, double* Y_host, int64_t B,
                         void* stream);
 

@@ -15,6 +15,7 @@
 #include <math.h>
 #include <cmath>
 #include <string.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <mutex>
@@ -103,6 +104,10 @@ struct xc_op {
   // workspace
   int64_t ws_B = 0;
   DevBuf partA, partW, scratch, zpl, Xh, Yh;
+  // xc_apply_host pipeline: copy-in / copy-out streams and per-slot events
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_cmp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  cudaEvent_t ev_start = nullptr;
   std::vector<int64_t> zoff;  // per block offset (doubles) of its z' planes in zpl
   xc_info_t info{};
   // phase profiling (ring of event sets: start, after phase 1, after phase 2, end)
@@ -810,6 +815,19 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
 void destroy_impl(xc_op* h) {
   for (auto& e : h->ev) cudaEventDestroy(e);
   h->ev.clear();
+  if (h->s_in) {
+    cudaStreamSynchronize(h->s_in);
+    cudaStreamSynchronize(h->s_out);
+    cudaStreamDestroy(h->s_in);
+    cudaStreamDestroy(h->s_out);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(h->ev_in[i]);
+      cudaEventDestroy(h->ev_cmp[i]);
+      cudaEventDestroy(h->ev_out[i]);
+    }
+    cudaEventDestroy(h->ev_start);
+    h->s_in = h->s_out = nullptr;
+  }
   for (auto& b : h->blocks) {
     fft_plan_free(b.fft);
     fft_plan_free(b.fftM);
@@ -863,6 +881,9 @@ xc_status xc_apply(xc_handle h, xc_dir dir, const double* X, int64_t ldx, double
   return apply_impl(h, dir, X, ldx, Y, ldy, B, (cudaStream_t)stream);
 }
 
+// Host buffers: the batch is cut into column chunks that flow through a 3-stage pipeline
+// (H2D on s_in, the apply on `stream`, D2H on s_out; two device slots), so the PCIe
+// copies in both directions overlap each other and the apply.
 xc_status xc_apply_host(xc_handle h, xc_dir dir, const double* Xh, double* Yh, int64_t B, void* stream) {
   if (!h || !Xh || !Yh || B < 1) {
     xc_set_error("apply_host: bad arguments");
@@ -870,14 +891,53 @@ xc_status xc_apply_host(xc_handle h, xc_dir dir, const double* Xh, double* Yh, i
   }
   XC_CUDA(cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
-  size_t bytes = (size_t)h->N * B * sizeof(double);
-  if (h->Xh.bytes < bytes) {
-    XC_TRY(dev_alloc(h->Xh, bytes));
-    XC_TRY(dev_alloc(h->Yh, bytes));
+  if (!h->s_in) {
+    int lo = 0, hi = 0;
+    XC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    XC_CUDA(cudaStreamCreateWithPriority(&h->s_in, cudaStreamNonBlocking, hi));
+    XC_CUDA(cudaStreamCreateWithPriority(&h->s_out, cudaStreamNonBlocking, hi));
+    for (int i = 0; i < 2; ++i) {
+      XC_CUDA(cudaEventCreateWithFlags(&h->ev_in[i], cudaEventDisableTiming));
+      XC_CUDA(cudaEventCreateWithFlags(&h->ev_cmp[i], cudaEventDisableTiming));
+      XC_CUDA(cudaEventCreateWithFlags(&h->ev_out[i], cudaEventDisableTiming));
+    }
+    XC_CUDA(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming));
   }
-  XC_CUDA(cudaMemcpyAsync(h->Xh.p, Xh, bytes, cudaMemcpyHostToDevice, st));
-  XC_TRY(apply_impl(h, dir, (const double*)h->Xh.p, B, (double*)h->Yh.p, B, B, st));
-  XC_CUDA(cudaMemcpyAsync(Yh, h->Yh.p, bytes, cudaMemcpyDeviceToHost, st));
+  const int64_t N = h->N;
+  // chunk: ~B/16 columns, a multiple of 64 (the SpMM column tile), at least 64
+  int64_t nparts = 8;
+  if (const char* e = getenv("XC_HOST_CHUNKS")) nparts = std::max(1, atoi(e));
+  int64_t Bc = std::min<int64_t>(B, std::max<int64_t>(64, ((B + nparts - 1) / nparts + 63) / 64 * 64));
+  const int64_t nchunk = (B + Bc - 1) / Bc;
+  const size_t slot = (size_t)N * Bc * sizeof(double);
+  if (h->Xh.bytes < 2 * slot) {
+    XC_TRY(dev_alloc(h->Xh, 2 * slot));
+    XC_TRY(dev_alloc(h->Yh, 2 * slot));
+  }
+  XC_TRY(ensure_ws(h, Bc));
+  // the copy streams start after the work already queued on `stream`
+  XC_CUDA(cudaEventRecord(h->ev_start, st));
+  XC_CUDA(cudaStreamWaitEvent(h->s_in, h->ev_start, 0));
+  XC_CUDA(cudaStreamWaitEvent(h->s_out, h->ev_start, 0));
+  for (int64_t c = 0; c < nchunk; ++c) {
+    const int i = (int)(c & 1);
+    const int64_t c0 = c * Bc, bc = std::min(Bc, B - c0);
+    double* xs = (double*)h->Xh.p + (size_t)i * N * Bc;
+    double* ys = (double*)h->Yh.p + (size_t)i * N * Bc;
+    if (c >= 2) XC_CUDA(cudaStreamWaitEvent(h->s_in, h->ev_cmp[i], 0));  // slot's X consumed
+    XC_CUDA(cudaMemcpy2DAsync(xs, bc * sizeof(double), Xh + c0, B * sizeof(double), bc * sizeof(double), N,
+                              cudaMemcpyHostToDevice, h->s_in));
+    XC_CUDA(cudaEventRecord(h->ev_in[i], h->s_in));
+    XC_CUDA(cudaStreamWaitEvent(st, h->ev_in[i], 0));
+    if (c >= 2) XC_CUDA(cudaStreamWaitEvent(st, h->ev_out[i], 0));     // slot's Y copied out
+    XC_TRY(apply_impl(h, dir, xs, bc, ys, bc, bc, st));
+    XC_CUDA(cudaEventRecord(h->ev_cmp[i], st));
+    XC_CUDA(cudaStreamWaitEvent(h->s_out, h->ev_cmp[i], 0));
+    XC_CUDA(cudaMemcpy2DAsync(Yh + c0, B * sizeof(double), ys, bc * sizeof(double), bc * sizeof(double), N,
+                              cudaMemcpyDeviceToHost, h->s_out));
+    XC_CUDA(cudaEventRecord(h->ev_out[i], h->s_out));
+  }
+  XC_CUDA(cudaStreamSynchronize(h->s_out));
   XC_CUDA(cudaStreamSynchronize(st));
   return XC_OK;
 }
