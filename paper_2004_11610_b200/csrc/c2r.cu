@@ -20,7 +20,11 @@
 // stages and the epilogue.  Middle stages run in place in WK (read, barrier, write);
 // the last stage writes global memory straight from registers (columns are the fast
 // index, so every store is a contiguous run of cb * 16 or cb * 8 bytes).
+#include <math.h>
+
 #include <algorithm>
+#include <mutex>
+#include <vector>
 
 #include "xc_internal.cuh"
 
@@ -102,7 +106,8 @@ __device__ __forceinline__ void bfly(double2* v) {
 }
 
 struct StageC {
-  int r, Rr, Ns, twstep;  // radix, butterflies per sequence R/r, span Ns, twiddle stride R/(Ns r)
+  int r, Rr, Ns;          // radix, butterflies per sequence R/r, span Ns
+  int twoff;              // offset of this stage's table w_{Ns r}^{k t}, [k][t-1], in C2RArgs::stw
   unsigned magic;         // ceil(2^32 / Ns): j / Ns by __umulhi (exact for j < 2^16)
 };
 
@@ -110,8 +115,9 @@ struct C2RArgs {
   int mode;              // 0: first of two, 1: second of two, 2: single pass
   int R, nf;             // sub-transform length and its radix stages
   StageC st[12];
-  const double2* tw;     // e^{+2 pi i n / R}
-  const double2* twL;    // e^{+2 pi i n / M} (pass 0 four-step twiddle)
+  const double2* stw;    // per-stage twiddle tables (exact, long double on the host)
+  const double2* ptw;    // pairing twiddle e^{i pi n / M}: pass 0 at [n2 L1 + e] (n = L2 e + n2), else [e]
+  const double2* ftw;    // pass 0 four-step twiddle e^{2 pi i n2 k1 / M} at [n2 L1 + k1]
   int M, L1, L2;
   int S;                 // sub-sequences per column
   int P;                 // slot pairs per column (pass 0)
@@ -201,8 +207,7 @@ __device__ __forceinline__ double2 zval(const C2RArgs& a, const FftIO& io, const
   const int pe = (s.pmode == 0) ? a.R - e : a.R - 1 - e;   // pe == R only for pmode 0, e == 0
   const double2* pp = (pe == a.R) ? nyq + sq : ld + (pe << a.lgn) + s.psq;
   double2 v = *pp;
-  const int n = (MODE == 0) ? a.L2 * e + s.sub : e;
-  double2 w = __ldg(io.twh + n);
+  const double2 w = __ldg(a.ptw + ((MODE == 0) ? s.sub * a.R + e : e));
   double evr = u.x + v.x, evi = u.y - v.y;  // u_n + conj u_{M-n}
   double dr = u.x - v.x, di = u.y + v.y;    // u_n - conj u_{M-n}
   double odr = dr * w.x - di * w.y, odi = dr * w.y + di * w.x;
@@ -219,14 +224,18 @@ template <int MODE>
 __device__ __forceinline__ void store_out(const C2RArgs& a, const FftIO& io, const Slot& s, const Epi& ep, int kk,
                                           double2 v, bool act) {
   if (MODE == 0) {
-    double2 w = __ldg(a.twL + s.sub * kk);
+    const double2 w = __ldg(a.ftw + s.sub * a.R + kk);
     if (act) a.scr[(unsigned)(ep.base + kk * ep.kstep)] = c_mul(v, w);
   } else {
     const int k = (MODE == 1) ? s.sub + a.L1 * kk : kk;
-    const int p = 2 * k;
+    const int p = 2 * k;  // p + 1 < L: yscale[p], yscale[p+1] always readable
+    const double2 ys = __ldg(reinterpret_cast<const double2*>(io.yscale) + k);
     double* y = io.Y + (size_t)(unsigned)(ep.base + p * (int)io.ldy);
-    if (act && p >= io.keep_lo && p < io.keep_hi) __stcs(y, v.x * __ldg(io.yscale + p));
-    if (act && p + 1 >= io.keep_lo && p + 1 < io.keep_hi) __stcs(y + io.ldy, v.y * __ldg(io.yscale + p + 1));
+    const bool k0 = act && p >= io.keep_lo && p < io.keep_hi;
+    const bool k1 = act && p + 1 >= io.keep_lo && p + 1 < io.keep_hi;
+    const double y0 = v.x * ys.x, y1 = v.y * ys.y;
+    if (k0) __stcs(y, y0);
+    if (k1) __stcs(y + io.ldy, y1);
   }
 }
 
@@ -265,13 +274,9 @@ __device__ __forceinline__ void stage(const C2RArgs& a, const FftIO& io, const d
     if (!FIRST) {
       jd = (int)__umulhi((unsigned)jj[b], c.magic);
       k = jj[b] - jd * c.Ns;
-      const double2 w = __ldg(a.tw + k * c.twstep);  // tw[0] = 1
-      double2 wt = w;
+      const double2* tw = a.stw + c.twoff + k * (r - 1);
 #pragma unroll
-      for (int t = 1; t < r; ++t) {
-        v[b][t] = c_mul(v[b][t], wt);
-        if (t + 1 < r) wt = c_mul(wt, w);
-      }
+      for (int t = 1; t < r; ++t) v[b][t] = c_mul(v[b][t], __ldg(tw + t - 1));
     }
     bfly<r>(v[b]);
     const int idxD = FIRST ? jd * r : jd * c.Ns * r + k;
@@ -354,16 +359,88 @@ int g_nsm = 0;
 
 void set_radices(C2RArgs& a, int nf, const int* f) {
   a.nf = nf;
-  int Ns = 1;
+  int Ns = 1, off = 0;
   for (int i = 0; i < nf; ++i) {
     StageC& c = a.st[i];
     c.r = f[i];
     c.Rr = a.R / f[i];
     c.Ns = Ns;
-    c.twstep = a.R / (Ns * f[i]);
+    c.twoff = off;
     c.magic = (Ns == 1) ? 0u : (unsigned)((0x100000000ULL + Ns - 1) / Ns);
+    off += Ns * (f[i] - 1);
     Ns *= f[i];
   }
+}
+
+// e^{+2 pi i m / n} with exact integer reduction of m
+double2 cis(int64_t m, int64_t n) {
+  const long double PI2 = 6.283185307179586476925286766559005768L;
+  m %= n;
+  if (m < 0) m += n;
+  const long double ang = PI2 * (long double)m / (long double)n;
+  return make_double2((double)cosl(ang), (double)sinl(ang));
+}
+
+void stage_table(int R, int nf, const int* f, std::vector<double2>& t) {
+  t.clear();
+  int Ns = 1;
+  for (int i = 0; i < nf; ++i) {
+    for (int k = 0; k < Ns; ++k)
+      for (int q = 1; q < f[i]; ++q) t.push_back(cis((int64_t)k * q, (int64_t)Ns * f[i]));
+    Ns *= f[i];
+  }
+  if (t.empty()) t.push_back(make_double2(1.0, 0.0));
+}
+
+// Twiddle tables of one length M (cached per device; a few MB at most per length).
+struct C2RTables {
+  int dev = -1, M = 0, L1 = 0, L2 = 0;
+  DevBuf stw0, stw1, ptw, ftw;
+};
+std::mutex g_tab_mu;
+std::vector<C2RTables*> g_tabs;
+
+template <typename T>
+xc_status put(DevBuf& b, const std::vector<T>& v) {
+  XC_TRY(dev_alloc(b, std::max<size_t>(1, v.size()) * sizeof(T)));
+  if (!v.empty()) XC_CUDA(cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return XC_OK;
+}
+
+xc_status tables_for(const FftPlan& p, const C2RTables** out) {
+  int dev = 0;
+  XC_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  for (auto* t : g_tabs)
+    if (t->dev == dev && t->M == p.L && t->L1 == p.L1 && t->L2 == p.L2) {
+      *out = t;
+      return XC_OK;
+    }
+  auto* t = new C2RTables();
+  t->dev = dev;
+  t->M = p.L;
+  t->L1 = p.L1;
+  t->L2 = p.L2;
+  std::vector<double2> v;
+  stage_table(p.L1, p.nf1, p.f1, v);
+  XC_TRY(put(t->stw0, v));
+  if (p.L2 > 1) {
+    stage_table(p.L2, p.nf2, p.f2, v);
+    XC_TRY(put(t->stw1, v));
+  }
+  const int64_t M = p.L, L1 = p.L1, L2 = p.L2;
+  v.assign(M, make_double2(0, 0));
+  for (int64_t n2 = 0; n2 < L2; ++n2)
+    for (int64_t e = 0; e < L1; ++e) v[n2 * L1 + e] = cis(L2 * e + n2, 2 * M);  // e^{i pi n / M}
+  XC_TRY(put(t->ptw, v));
+  if (p.L2 > 1) {
+    for (int64_t n2 = 0; n2 < L2; ++n2)
+      for (int64_t k1 = 0; k1 < L1; ++k1) v[n2 * L1 + k1] = cis(n2 * k1, M);
+    XC_TRY(put(t->ftw, v));
+  }
+  g_tabs.push_back(t);
+  *out = t;
+  return XC_OK;
 }
 
 // nseq = cb * sc (powers of two) with R * nseq <= TILE; columns first (cb <= 16), sc >= smin.
@@ -413,19 +490,22 @@ xc_status c2r_run(const FftPlan& p, const FftIO& io, int ncol, double2* scratch,
     xc_set_error("c2r: batch too large for 32-bit offsets (split the batch)");
     return XC_EUNSUPPORTED;
   }
+  const C2RTables* tb = nullptr;
+  XC_TRY(tables_for(p, &tb));
+  a.ptw = (const double2*)tb->ptw.p;
+  a.ftw = (const double2*)tb->ftw.p;
   a.M = p.L;
   a.L1 = p.L1;
   a.L2 = p.L2;
   a.ncol = ncol;
   a.scr = scratch;
   a.lds = ncol;
-  a.twL = p.twL;
   if (p.L2 == 1) {
     a.mode = 2;
     a.R = p.L1;
     a.S = 1;
     set_radices(a, p.nf1, p.f1);
-    a.tw = p.tw1;
+    a.stw = (const double2*)tb->stw0.p;
     // one sequence per column: every slot is a column
     int nseq = 1;
     while (2 * nseq * a.R <= TILE && nseq < NTH && nseq < ncol) nseq *= 2;
@@ -448,7 +528,7 @@ xc_status c2r_run(const FftPlan& p, const FftIO& io, int ncol, double2* scratch,
   a.S = p.L2;
   a.P = (a.S & 1) ? (a.S + 1) / 2 : a.S / 2;
   set_radices(a, p.nf1, p.f1);
-  a.tw = p.tw1;
+  a.stw = (const double2*)tb->stw0.p;
   choose(a, 2);
   if (a.sc < 2 || a.R * (1 << a.lgn) > TILE) {
     xc_set_error("c2r: first-pass length too long");
@@ -460,7 +540,7 @@ xc_status c2r_run(const FftPlan& p, const FftIO& io, int ncol, double2* scratch,
   a.R = p.L2;
   a.S = p.L1;
   set_radices(a, p.nf2, p.f2);
-  a.tw = p.tw2;
+  a.stw = (const double2*)tb->stw1.p;
   choose(a, 1);
   if (a.R * (1 << a.lgn) > TILE) {
     xc_set_error("c2r: second-pass length too long");
