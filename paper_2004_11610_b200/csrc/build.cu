@@ -11,7 +11,7 @@
 //     node = 8g + row, q = k0 + 2s + kk/2
 // and its tail A[row][kk] = phi_{k0+4s+kk}(x_{8g+row}).
 // In every case lane l of a warp holds A[l/4][l%4] (spmm.cu); an item carries two M-tiles
-// (adjacent groups sharing the B fragments), interleaved per lane.
+// (or one), interleaved per lane; each M-tile is filled from its own family's bands.
 #include "build.h"
 #include "xc_internal.cuh"
 
@@ -30,32 +30,33 @@ template <int MODE>
 __global__ void fill_k(const FillItem* fi, const int* start, const int* len, const int64_t* off,
                        const double2* vals, const double* P, int t, int N, int H, double* tiles) {
   const FillItem it = fi[blockIdx.x];
-  for (int idx = threadIdx.x; idx < it.nsteps * 64; idx += blockDim.x) {
-    int s = idx >> 6, lane = (idx >> 1) & 31, mt = idx & 1;
-    int gm = mt ? it.g1 : it.g0;
+  for (int idx = threadIdx.x; idx < it.nsteps * 32; idx += blockDim.x) {
+    const int s = idx >> 5, lane = idx & 31, gm = it.g;
     double v = 0.0;
-    if (gm >= 0) {
-      int R = it.k0 + 4 * s + (lane & 3);
-      int r = lane >> 2;
-      if (MODE == FILL_OUT_CPLX) {        // node R, bin 4 gm + r/2, component r&1
-        int q = 4 * gm + (r >> 1);
-        if (R < N && q < H) v = band_val(R, q, r & 1, start, len, off, vals);
-      } else if (MODE == FILL_OUT_REAL) { // node R, degree 8 gm + r
-        int j = 8 * gm + r;
-        if (R < N && j < t) v = P[(int64_t)j * N + R];
-      } else if (MODE == FILL_IN_CPLX) {  // node 8 gm + r, bin R/2, (c Re S, -c Im S)
-        int node = 8 * gm + r, q = R >> 1;
-        if (node < N && q < H) {
-          double c = (q == 0 || q == H - 1) ? 1.0 : 2.0;
-          double a = band_val(node, q, R & 1, start, len, off, vals);
-          v = (R & 1) ? -c * a : c * a;
-        }
-      } else {                            // node 8 gm + r, degree R
-        int node = 8 * gm + r;
-        if (node < N && R < t) v = P[(int64_t)R * N + node];
-      }
+    const int R = it.k0 + 4 * s + (lane & 3);
+    const int r = lane >> 2;
+    if (R < it.lo || R >= it.hi) {
+      tiles[it.a_off + 64 * s + 2 * lane + it.mt] = 0.0;
+      continue;
     }
-    tiles[it.a_off + idx] = v;
+    if (MODE == FILL_OUT_CPLX) {        // node R, bin 4 gm + r/2, component r&1
+      int q = 4 * gm + (r >> 1);
+      if (R < N && q < H) v = band_val(R, q, r & 1, start, len, off, vals);
+    } else if (MODE == FILL_OUT_REAL) { // node R, degree 8 gm + r
+      int j = 8 * gm + r;
+      if (R < N && j < t) v = P[(int64_t)j * N + R];
+    } else if (MODE == FILL_IN_CPLX) {  // node 8 gm + r, bin R/2, (c Re S, -c Im S)
+      int node = 8 * gm + r, q = R >> 1;
+      if (node < N && q < H) {
+        double c = (q == 0 || q == H - 1) ? 1.0 : 2.0;
+        double a = band_val(node, q, R & 1, start, len, off, vals);
+        v = (R & 1) ? -c * a : c * a;
+      }
+    } else {                            // node 8 gm + r, degree R
+      int node = 8 * gm + r;
+      if (node < N && R < t) v = P[(int64_t)R * N + node];
+    }
+    tiles[it.a_off + 64 * s + 2 * lane + it.mt] = v;
   }
 }
 

@@ -5,13 +5,16 @@
 
 #include "../../include/xc.h"
 
-// Fill descriptor of one SpMM item: two M-tiles (g0, g1; -1 = empty) over the B rows
-// [k0, k0 + 4 nsteps); tiles[a_off + 64 s + 2 lane + mt] is lane's A fragment of M-tile mt.
+// Fill descriptor of one M-tile of an SpMM item: group g over the B rows [k0, k0 + 4 nsteps)
+// in slot mt (0 or 1) of the item's A stream; tiles[a_off + 64 s + 2 lane + mt] is lane's A
+// fragment of that M-tile.
 struct FillItem {
   int64_t a_off;
-  int k0;
+  int k0;       // first B row of the item's stream
   int nsteps;
-  int g0, g1;
+  int g, mt;
+  int lo, hi;   // this M-tile's own B rows: entries outside [lo, hi) are zero (a chunked
+                // group must not count a row of its neighbouring chunk twice)
 };
 
 enum { FILL_OUT_CPLX = 0, FILL_OUT_REAL = 1, FILL_IN_CPLX = 2, FILL_IN_REAL = 3 };

@@ -92,11 +92,8 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
     for (int m = 0; m < 2; ++m)
 #pragma unroll
       for (int i = 0; i < NT; ++i) acc[m][i][0] = acc[m][i][1] = 0.0;
-    const double2* ap = reinterpret_cast<const double2*>(tiles + it.a_off) + lane;
     const double* xb = xs + (it.k0 - W.r0 + t) * CWP + bcol;
     const int n = it.nsteps;
-    double2 a0 = n > 0 ? __ldg(ap) : make_double2(0.0, 0.0);
-    double2 a1 = n > 1 ? __ldg(ap + 32) : make_double2(0.0, 0.0);
     double b0[NT], b1[NT];
     auto lds_b = [&](int s, double* bv) {
       const double* p = xb + 4 * s * CWP;
@@ -111,23 +108,50 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
         }
       }
     };
-    if (n > 0) lds_b(0, b0);
-    for (int s = 0; s < n; s += 2) {
-      if (s + 1 < n) lds_b(s + 1, b1);
 #pragma unroll
-      for (int i = 0; i < NT; ++i) {
-        dmma(acc[0][i][0], acc[0][i][1], a0.x, b0[i]);
-        dmma(acc[1][i][0], acc[1][i][1], a0.y, b0[i]);
-      }
-      a0 = (s + 2 < n) ? __ldg(ap + 32 * (s + 2)) : make_double2(0.0, 0.0);
-      if (s + 1 < n) {
-        if (s + 2 < n) lds_b(s + 2, b0);
+    for (int i = 0; i < NT; ++i) b0[i] = b1[i] = 0.0;
+    if (n > 0) lds_b(0, b0);
+    if (it.out_row[1] >= 0) {
+      // two M-tiles sharing the B fragments
+      const double2* ap = reinterpret_cast<const double2*>(tiles + it.a_off) + lane;
+      double2 a0 = n > 0 ? __ldg(ap) : make_double2(0.0, 0.0);
+      double2 a1 = n > 1 ? __ldg(ap + 32) : make_double2(0.0, 0.0);
+      for (int s = 0; s < n; s += 2) {
+        if (s + 1 < n) lds_b(s + 1, b1);
 #pragma unroll
         for (int i = 0; i < NT; ++i) {
-          dmma(acc[0][i][0], acc[0][i][1], a1.x, b1[i]);
-          dmma(acc[1][i][0], acc[1][i][1], a1.y, b1[i]);
+          dmma(acc[0][i][0], acc[0][i][1], a0.x, b0[i]);
+          dmma(acc[1][i][0], acc[1][i][1], a0.y, b0[i]);
         }
-        a1 = (s + 3 < n) ? __ldg(ap + 32 * (s + 3)) : make_double2(0.0, 0.0);
+        a0 = (s + 2 < n) ? __ldg(ap + 32 * (s + 2)) : make_double2(0.0, 0.0);
+        if (s + 1 < n) {
+          if (s + 2 < n) lds_b(s + 2, b0);
+#pragma unroll
+          for (int i = 0; i < NT; ++i) {
+            dmma(acc[0][i][0], acc[0][i][1], a1.x, b1[i]);
+            dmma(acc[1][i][0], acc[1][i][1], a1.y, b1[i]);
+          }
+          a1 = (s + 3 < n) ? __ldg(ap + 32 * (s + 3)) : make_double2(0.0, 0.0);
+        }
+      }
+    } else {
+      // one M-tile (slot 0 of the A stream), A fragments streamed 4 steps ahead
+      const double* ap = tiles + it.a_off + 2 * lane;
+      double a0 = n > 0 ? __ldg(ap) : 0.0, a1 = n > 1 ? __ldg(ap + 64) : 0.0;
+      double a2 = n > 2 ? __ldg(ap + 128) : 0.0, a3 = n > 3 ? __ldg(ap + 192) : 0.0;
+      for (int s = 0; s < n; s += 2) {
+        if (s + 1 < n) lds_b(s + 1, b1);
+#pragma unroll
+        for (int i = 0; i < NT; ++i) dmma(acc[0][i][0], acc[0][i][1], a0, b0[i]);
+        a0 = a2;
+        a2 = (s + 4 < n) ? __ldg(ap + 64 * (s + 4)) : 0.0;
+        if (s + 1 < n) {
+          if (s + 2 < n) lds_b(s + 2, b0);
+#pragma unroll
+          for (int i = 0; i < NT; ++i) dmma(acc[0][i][0], acc[0][i][1], a1, b1[i]);
+          a1 = a3;
+          a3 = (s + 5 < n) ? __ldg(ap + 64 * (s + 5)) : 0.0;
+        }
       }
     }
 

@@ -93,13 +93,13 @@ struct xc_op {
   // output axis
   DevBuf itemsA, tilesA, winsA;
   int nitemsA = 0, nwinsA = 0;
-  int64_t rowsA = 0, tilesA_n = 0;
+  int64_t rowsA = 0, tilesA_n = 0, mtstepsA = 0;  // M-tile steps issued (DMMA accounting)
   int ntailg = 0;
   DevBuf tail_base, tail_nch;
   // input axis
   DevBuf itemsW, tilesW, winsW;
   int nitemsW = 0, nwinsW = 0;
-  int64_t rowsW = 0, tilesW_n = 0;
+  int64_t rowsW = 0, tilesW_n = 0, mtstepsW = 0;
   DevBuf nodeg_base, nodeg_nch;
   // workspace
   int64_t ws_B = 0;
@@ -287,11 +287,14 @@ xc_status build_block(xc_op* h, BlockData& b, const std::vector<double2>& jtab, 
   return XC_OK;
 }
 
-// --- SpMM items: M-tiles paired into items ------------------------------------------------
+// --- SpMM items: M-tiles, single or paired ------------------------------------------------
 // An M-tile is one 8-row slice of the operator (a bin group, a degree group or a node group)
-// over a range of B rows [k0, k1) (multiples of 4) with its output rows.  Consecutive M-tiles
-// of the same family and chunk are paired into one item (they share the B fragments; the
-// union of their ranges is padded with zeros in each one's A stream).
+// over its exact range of B rows [k0, k1) with its output rows.  Two M-tiles over nearly the
+// same rows may be paired into one item: they then share the B fragments (half the shared-
+// memory traffic per DMMA) but both run over the union of the ranges.  Pairing is used only
+// where the union adds little (kPairSlack); otherwise the item carries one M-tile.
+constexpr double kPairSlack = 1.08;
+
 struct MTile {
   int fam;        // block index, or -1 for the dense tail
   int g;          // group index within the family
@@ -303,50 +306,55 @@ struct MTile {
 
 struct ItemSet {
   std::vector<SpmmItem> items;
-  std::vector<FillItem> fills;
-  std::vector<int> fam;
-  std::vector<int> chunk;
+  std::vector<FillItem> fills;  // one per M-tile
+  std::vector<int> fam;         // family of each fill
   int64_t aoff = 0;
 };
 
-void pair_mtiles(const std::vector<MTile>& mt, int src, ItemSet& out) {
-  // mt is ordered by (fam, chunk, g)
+bool worth_pairing(const MTile& a, const MTile& b) {
+  const int la = std::max(0, a.k1 - a.k0), lb = std::max(0, b.k1 - b.k0);
+  if (la == 0 || lb == 0) return false;
+  const int u0 = std::min(a.k0, b.k0), u1 = std::max(a.k1, b.k1);
+  if (u1 - u0 > XC_WMAX - 3) return false;  // the pair must fit one shared-memory window
+  return 2.0 * (u1 - u0) <= kPairSlack * (la + lb);
+}
+
+// Emit one item for M-tile a (and b, if non-null) reading operand source `src`.
+void emit_item(const MTile& a, const MTile* b, int src, ItemSet& out) {
+  int k0 = a.k0, k1 = a.k1;
+  if (b) {
+    k0 = std::min(k0, b->k0);
+    k1 = std::max(k1, b->k1);
+  }
+  SpmmItem it{};
+  it.a_off = out.aoff;
+  it.out_row[0] = a.out_row;
+  it.out_row[1] = b ? b->out_row : -1;
+  it.k0 = k1 > k0 ? k0 : 0;
+  it.nsteps = std::max(0, (k1 - k0 + 3) / 4);
+  it.src = src;
+  it.cplx = a.cplx;
+  out.items.push_back(it);
+  out.fills.push_back(FillItem{out.aoff, it.k0, it.nsteps, a.g, 0, a.k0, a.k1});
+  out.fam.push_back(a.fam);
+  if (b) {
+    out.fills.push_back(FillItem{out.aoff, it.k0, it.nsteps, b->g, 1, b->k0, b->k1});
+    out.fam.push_back(b->fam);
+  }
+  out.aoff += 64LL * it.nsteps;
+}
+
+// Pair neighbours of an ordered list greedily where worth it.
+void pair_list(const std::vector<MTile>& mt, int src, ItemSet& out) {
   size_t i = 0;
   while (i < mt.size()) {
-    const MTile& a = mt[i];
-    const MTile* b = nullptr;
-    if (i + 1 < mt.size() && mt[i + 1].fam == a.fam && mt[i + 1].chunk == a.chunk) {
-      b = &mt[i + 1];
-      int u0 = std::min(a.k1 > a.k0 ? a.k0 : b->k0, b->k1 > b->k0 ? b->k0 : a.k0);
-      int u1 = std::max(a.k1, b->k1);
-      if (u1 - u0 > XC_WMAX) b = nullptr;  // the pair must fit one shared-memory window
+    if (i + 1 < mt.size() && mt[i + 1].cplx == mt[i].cplx && worth_pairing(mt[i], mt[i + 1])) {
+      emit_item(mt[i], &mt[i + 1], src, out);
+      i += 2;
+    } else {
+      emit_item(mt[i], nullptr, src, out);
+      i += 1;
     }
-    int k0 = a.k0, k1 = a.k1;
-    if (b) {
-      if (b->k1 > b->k0) {
-        if (k1 > k0) {
-          k0 = std::min(k0, b->k0);
-          k1 = std::max(k1, b->k1);
-        } else {
-          k0 = b->k0;
-          k1 = b->k1;
-        }
-      }
-    }
-    SpmmItem it{};
-    it.a_off = out.aoff;
-    it.out_row[0] = a.out_row;
-    it.out_row[1] = b ? b->out_row : -1;
-    it.k0 = k0;
-    it.nsteps = std::max(0, (k1 - k0) / 4);
-    it.src = src < 0 ? (a.fam < 0 ? 0 : a.fam) : src;
-    it.cplx = a.cplx;
-    out.items.push_back(it);
-    out.fills.push_back(FillItem{out.aoff, k0, it.nsteps, a.g, b ? b->g : -1});
-    out.fam.push_back(a.fam);
-    out.chunk.push_back(a.chunk);
-    out.aoff += 64LL * it.nsteps;
-    i += b ? 2 : 1;
   }
 }
 
@@ -354,12 +362,16 @@ xc_status upload_and_fill(xc_op* h, ItemSet& S, bool input_axis, DevBuf& d_items
                           DevBuf& d_tiles, int& nitems, int& nwins, int64_t& ntiles, cudaStream_t st) {
   const int N = (int)h->N;
   ntiles = S.aoff;
+  int64_t& mts = input_axis ? h->mtstepsW : h->mtstepsA;
+  mts = 0;
+  for (auto& it : S.items) mts += (int64_t)it.nsteps * (it.out_row[1] >= 0 ? 2 : 1);
   XC_TRY(dev_alloc(d_tiles, (size_t)std::max<int64_t>(1, S.aoff) * sizeof(double)));
+  XC_CUDA(cudaMemsetAsync(d_tiles.p, 0, (size_t)std::max<int64_t>(1, S.aoff) * sizeof(double), st));  // unpaired slots
   DevBuf dfill;
   for (int fam = -1; fam < (int)h->blocks.size(); ++fam) {
     std::vector<FillItem> part;
     for (size_t i = 0; i < S.fills.size(); ++i)
-      if (S.fam[i] == fam && S.fills[i].nsteps > 0) part.push_back(S.fills[i]);
+      if (S.fam[i] == fam && S.fills[i].nsteps > 0) part.push_back(S.fills[i]);  // per M-tile
     if (part.empty()) continue;
     XC_TRY(upload(dfill, part));
     if (fam >= 0) {
@@ -421,6 +433,7 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
   const int N4 = (N + 3) / 4 * 4;
   ItemSet S;
   int64_t rows = 0;
+  std::vector<MTile> pool;  // split-block M-tiles of every block, paired across blocks per chunk
   for (size_t bi = 0; bi < h->blocks.size(); ++bi) {
     BlockData& b = h->blocks[bi];
     b.ngroups = (b.H + 3) / 4;
@@ -435,7 +448,7 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
     }
     int maxspan = 0;
     for (int g = 0; g < b.ngroups; ++g)
-      if (klo[g] < khi[g]) maxspan = std::max(maxspan, (khi[g] + 3) / 4 * 4 - klo[g] / 4 * 4);
+      if (klo[g] < khi[g]) maxspan = std::max(maxspan, khi[g] - klo[g]);
     b.split = maxspan > KSPLIT;
     b.ubase = rows;
     rows += 8LL * b.ngroups;
@@ -443,20 +456,16 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
     std::vector<int> gnch(b.ngroups, 0);
     std::vector<MTile> mt;
     for (int g = 0; g < b.ngroups; ++g) {
-      int a = 0, e = 0;
-      if (klo[g] < khi[g]) {
-        a = klo[g] / 4 * 4;
-        e = (khi[g] + 3) / 4 * 4;
-      }
+      const int a = klo[g] < khi[g] ? klo[g] : 0, e = klo[g] < khi[g] ? khi[g] : 0;
       if (!b.split) {
         mt.push_back(MTile{(int)bi, g, 0, a, e, b.ubase + 8LL * g, 1});  // empty group -> zeros
         continue;
       }
       gbase[g] = rows;
       for (int c = a / KC; c * KC < e; ++c) {
-        int k0 = std::max(a, c * KC), k1 = std::min(e, (c + 1) * KC);
+        const int k0 = std::max(a, c * KC), k1 = std::min(e, (c + 1) * KC);
         if (k1 <= k0) continue;
-        mt.push_back(MTile{(int)bi, g, c, k0, k1, rows, 1});
+        pool.push_back(MTile{(int)bi, g, c, k0, k1, rows, 1});
         rows += 8;
         gnch[g]++;
       }
@@ -464,20 +473,17 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
     if (b.split) {
       XC_TRY(upload(b.grp_base, gbase));
       XC_TRY(upload(b.grp_nch, gnch));
-      std::stable_sort(mt.begin(), mt.end(), [](const MTile& x, const MTile& y) { return x.chunk < y.chunk; });
+    } else {
+      pair_list(mt, 0, S);  // consecutive groups of one block (ordered by g)
     }
-    // execution key of unsplit blocks: the node window of the first node
-    ItemSet tmp;
-    tmp.aoff = S.aoff;
-    pair_mtiles(mt, 0, tmp);
-    for (size_t i = 0; i < tmp.items.size(); ++i) {
-      S.items.push_back(tmp.items[i]);
-      S.fills.push_back(tmp.fills[i]);
-      S.fam.push_back(tmp.fam[i]);
-      S.chunk.push_back(b.split ? tmp.chunk[i] : tmp.items[i].k0 / KC);
-    }
-    S.aoff = tmp.aoff;
   }
+  // split blocks: per node chunk, all blocks' M-tiles ordered by range, paired across blocks
+  std::stable_sort(pool.begin(), pool.end(), [](const MTile& x, const MTile& y) {
+    if (x.chunk != y.chunk) return x.chunk < y.chunk;
+    if (x.k0 != y.k0) return x.k0 < y.k0;
+    return x.k1 < y.k1;
+  });
+  pair_list(pool, 0, S);
   // dense tail: groups of 8 degrees x node chunks
   h->ntailg = (h->tail + 7) / 8;
   std::vector<int64_t> tbase(std::max(1, h->ntailg), 0);
@@ -486,17 +492,16 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
   for (int g = 0; g < h->ntailg; ++g) {
     tbase[g] = rows;
     for (int k0 = 0; k0 < N4; k0 += KC) {
-      mt.push_back(MTile{-1, g, k0 / KC, k0, std::min(N4, k0 + KC), rows, 0});
+      mt.push_back(MTile{-1, g, k0 / KC, k0, std::min(N, k0 + KC), rows, 0});
       rows += 8;
       tnch[g]++;
     }
   }
   std::stable_sort(mt.begin(), mt.end(), [](const MTile& x, const MTile& y) { return x.chunk < y.chunk; });
-  pair_mtiles(mt, 0, S);
+  pair_list(mt, 0, S);
   XC_TRY(upload(h->tail_base, tbase));
   XC_TRY(upload(h->tail_nch, tnch));
   h->rowsA = rows;
-  for (auto& it : S.items) it.src = 0;
   return upload_and_fill(h, S, false, h->itemsA, h->winsA, h->tilesA, h->nitemsA, h->nwinsA, h->tilesA_n, st);
 }
 
@@ -559,7 +564,7 @@ xc_status build_input_axis(xc_op* h, cudaStream_t st) {
     std::stable_sort(mt.begin(), mt.end(), [](const MTile& x, const MTile& y) {
       return x.chunk != y.chunk ? x.chunk < y.chunk : x.g < y.g;
     });
-    pair_mtiles(mt, f == 0 ? nb : f - 1, S);
+    pair_list(mt, f == 0 ? nb : f - 1, S);
   }
   XC_TRY(upload(h->nodeg_base, gbase));
   XC_TRY(upload(h->nodeg_nch, gnch));
@@ -672,8 +677,8 @@ xc_status build_impl(xc_kind kind, const xc_params* prm, const double* nodes, in
   in.nnz = nnz;
   in.flops_per_col_A = 4.0 * nnz + 2.0 * h->tail * N + fft;
   in.flops_per_col_WAT = in.flops_per_col_A;
-  in.dmma_flops_per_col_A = 64.0 * (h->tilesA_n / 32);   // 8x4 FMA pairs per lane-step per M-tile
-  in.dmma_flops_per_col_WAT = 64.0 * (h->tilesW_n / 32);
+  in.dmma_flops_per_col_A = 64.0 * h->mtstepsA;   // 8 x 4 FMA per M-tile step and column
+  in.dmma_flops_per_col_WAT = 64.0 * h->mtstepsW;
   in.op_bytes_A = h->tilesA_n * 8 + (int64_t)h->nitemsA * sizeof(SpmmItem);
   in.op_bytes_WAT = h->tilesW_n * 8 + (int64_t)h->nitemsW * sizeof(SpmmItem);
   int fl = 0, flM = 0, nsplit = 0;
