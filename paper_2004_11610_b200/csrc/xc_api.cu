@@ -50,8 +50,8 @@ void dev_free(DevBuf& b) {
 
 namespace {
 
-constexpr int KC = 128;      // node chunk of a split output-axis item (multiple of 4, <= XC_WMAX)
-constexpr int KSPLIT = 128;  // blocks whose bin groups span more nodes than this are split
+constexpr int KC = 184;      // node chunk of a split output-axis item (multiple of 4, <= XC_WMAX)
+constexpr int KSPLIT = 184;  // blocks whose bin groups span more nodes than this are split
 constexpr int QC = 64;       // bin chunk of an input-axis item (2 QC B rows <= XC_WMAX)
 constexpr int WIN_ITEMS = 128;  // max items per SpMM window (CTA)
 
