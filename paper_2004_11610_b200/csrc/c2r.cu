@@ -125,7 +125,30 @@ struct C2RArgs {
   int ntx, ntiles;
   double2* scr;          // four-step scratch, row (k1 L2 + n2), ld = lds (offsets < 2^31)
   int lds;
+  int nstw;              // entries of the stage-twiddle table (staged in smem once per CTA)
+  int naux;              // entries of one per-tile auxiliary slice (sc * R; MODE 2: R)
 };
+
+// Shared-memory partition (double2 units): LD | WK | nyq | stw | aux, where aux holds
+//   MODE 0: ptw slice [slot][e] (used by the first stage) + 2 x ftw slice [slot][k1]
+//   MODE 1: 2 x yscale slice [slot][k2] as (yscale[2k], yscale[2k+1])
+//   MODE 2: the whole ptw [e] and yscale [k] tables (loaded once per CTA)
+// The slices used by the last stage are double-buffered: the next tile's are prefetched
+// while the current tile's last stage still reads them.
+struct Smem {
+  double2 *ld, *wk, *nyq, *stw, *ptw, *aux2;  // aux2: two slices of a.naux
+};
+__device__ __forceinline__ Smem smem_parts(const C2RArgs& a, double2* base) {
+  Smem p;
+  const int tn = a.R << a.lgn;
+  p.ld = base;
+  p.wk = base + tn;
+  p.nyq = base + 2 * tn;
+  p.stw = p.nyq + (1 << a.lgn);
+  p.ptw = p.stw + a.nstw;
+  p.aux2 = p.ptw + ((a.mode == 1) ? 0 : a.naux);
+  return p;
+}
 
 // Per-thread view of the current tile (offsets in elements; all < 2^31, checked on the host).
 struct Slot {
@@ -134,7 +157,25 @@ struct Slot {
   bool valid;
   int pmode;    // 0: partner element R-e in own sequence (sub 0; e = 0 -> Nyquist), 1: R-1-e own, 2: R-1-e other slot
   int psq;      // partner's sequence index (own or other slot)
+  int sl;       // slot of this thread's sequence within the tile
 };
+
+// sub-sequence held by slot sl of sequence-group gy (-1: none)
+template <int MODE>
+__device__ __forceinline__ int slot_sub(const C2RArgs& a, int gy, int sl) {
+  if (MODE == 0) {
+    const int p = gy * (a.sc >> 1) + (sl >> 1);
+    const int which = sl & 1;
+    if (p >= a.P) return -1;
+    if (p == 0) return which ? ((a.S & 1) ? -1 : a.S / 2) : 0;
+    return which ? a.S - p : p;
+  }
+  if (MODE == 1) {
+    const int sub = gy * a.sc + sl;
+    return sub < a.S ? sub : -1;
+  }
+  return 0;
+}
 
 template <int MODE>
 __device__ __forceinline__ Slot slot_of(const C2RArgs& a, int tile, int sq) {
@@ -143,6 +184,7 @@ __device__ __forceinline__ Slot slot_of(const C2RArgs& a, int tile, int sq) {
   const int gx = tile - gy * a.ntx;
   const int sl = sq >> a.lgcb, cl = sq & (a.cb - 1);
   s.col = gx * a.cb + cl;
+  s.sl = sl;
   int sub;
   if (MODE == 0) {
     const int p = gy * (a.sc >> 1) + (sl >> 1);
@@ -174,7 +216,7 @@ __device__ __forceinline__ void cp16(double2* dst, const double2* src, bool v) {
 }
 
 template <int MODE>
-__device__ __forceinline__ void issue_loads(const C2RArgs& a, const FftIO& io, int tile, double2* ld, double2* nyq,
+__device__ __forceinline__ void issue_loads(const C2RArgs& a, const FftIO& io, int tile, const Smem& sp, int abuf,
                                             int sq, int e0, int estep) {
   Slot s = slot_of<MODE>(a, tile, sq);
   const double2* g;
@@ -189,25 +231,39 @@ __device__ __forceinline__ void issue_loads(const C2RArgs& a, const FftIO& io, i
     g = io.Uc + s.col;
     gstep = (int)io.ldu;
   }
-  double2* d = ld + (e0 << a.lgn) + sq;
+  double2* d = sp.ld + (e0 << a.lgn) + sq;
   const int dstep = estep << a.lgn;
   for (int e = e0; e < a.R; e += estep, d += dstep) cp16(d, g + (size_t)((unsigned)e * (unsigned)gstep), s.valid);
   if (MODE != 1 && e0 == 0) {
     const bool v = s.valid && s.sub == 0;
-    cp16(nyq + sq, io.Uc + (size_t)((unsigned)a.M * (unsigned)io.ldu + s.col), v);
+    cp16(sp.nyq + sq, io.Uc + (size_t)((unsigned)a.M * (unsigned)io.ldu + s.col), v);
+  }
+  if (MODE != 2) {  // this tile's twiddle / scale slices
+    const int gy = tile / a.ntx;
+    double2* aux = sp.aux2 + abuf * a.naux;
+    for (int idx = threadIdx.x; idx < a.naux; idx += NTH) {
+      const int sl = idx / a.R, e = idx - sl * a.R;
+      const int sub = slot_sub<MODE>(a, gy, sl);
+      const int su = sub < 0 ? 0 : sub;
+      if (MODE == 0) {
+        cp16(sp.ptw + idx, a.ptw + su * a.R + e, true);
+        cp16(aux + idx, a.ftw + su * a.R + e, true);
+      } else {
+        cp16(aux + idx, reinterpret_cast<const double2*>(io.yscale) + (su + a.L1 * e), true);
+      }
+    }
   }
   asm volatile("cp.async.commit_group;\n" ::);
 }
 
 // Z[e] of this thread's sequence (pairing of the half spectrum); branch-free.
 template <int MODE>
-__device__ __forceinline__ double2 zval(const C2RArgs& a, const FftIO& io, const double2* ld, const double2* nyq,
-                                        const Slot& s, int sq, int e) {
-  double2 u = ld[(e << a.lgn) + sq];
+__device__ __forceinline__ double2 zval(const C2RArgs& a, const Smem& sp, const Slot& s, int sq, int e) {
+  double2 u = sp.ld[(e << a.lgn) + sq];
   const int pe = (s.pmode == 0) ? a.R - e : a.R - 1 - e;   // pe == R only for pmode 0, e == 0
-  const double2* pp = (pe == a.R) ? nyq + sq : ld + (pe << a.lgn) + s.psq;
+  const double2* pp = (pe == a.R) ? sp.nyq + sq : sp.ld + (pe << a.lgn) + s.psq;
   double2 v = *pp;
-  const double2 w = __ldg(a.ptw + ((MODE == 0) ? s.sub * a.R + e : e));
+  const double2 w = sp.ptw[(MODE == 0) ? s.sl * a.R + e : e];
   double evr = u.x + v.x, evi = u.y - v.y;  // u_n + conj u_{M-n}
   double dr = u.x - v.x, di = u.y + v.y;    // u_n - conj u_{M-n}
   double odr = dr * w.x - di * w.y, odi = dr * w.y + di * w.x;
@@ -221,15 +277,15 @@ struct Epi {
 };
 
 template <int MODE>
-__device__ __forceinline__ void store_out(const C2RArgs& a, const FftIO& io, const Slot& s, const Epi& ep, int kk,
-                                          double2 v, bool act) {
+__device__ __forceinline__ void store_out(const C2RArgs& a, const FftIO& io, const Slot& s, const Epi& ep,
+                                          const double2* aux, int kk, double2 v, bool act) {
   if (MODE == 0) {
-    const double2 w = __ldg(a.ftw + s.sub * a.R + kk);
+    const double2 w = aux[s.sl * a.R + kk];
     if (act) a.scr[(unsigned)(ep.base + kk * ep.kstep)] = c_mul(v, w);
   } else {
     const int k = (MODE == 1) ? s.sub + a.L1 * kk : kk;
-    const int p = 2 * k;  // p + 1 < L: yscale[p], yscale[p+1] always readable
-    const double2 ys = __ldg(reinterpret_cast<const double2*>(io.yscale) + k);
+    const int p = 2 * k;
+    const double2 ys = aux[(MODE == 1) ? s.sl * a.R + kk : kk];  // (yscale[p], yscale[p+1])
     double* y = io.Y + (size_t)(unsigned)(ep.base + p * (int)io.ldy);
     const bool k0 = act && p >= io.keep_lo && p < io.keep_hi;
     const bool k1 = act && p + 1 >= io.keep_lo && p + 1 < io.keep_hi;
@@ -246,9 +302,10 @@ enum { OUT_WK = 0, OUT_G = 1 };
 // Out-of-range butterflies of the last round are computed on a clamped (valid) index and
 // their stores suppressed, so there is no divergent control flow inside the stage.
 template <int r, int IN, int OUT, int MODE, bool FIRST>
-__device__ __forceinline__ void stage(const C2RArgs& a, const FftIO& io, const double2* ld, const double2* nyq,
-                                      double2* wk, const Slot& s, const Epi& ep, int sq, int e0, int estep,
-                                      const StageC& c) {
+__device__ __forceinline__ void stage(const C2RArgs& a, const FftIO& io, const Smem& sp, const double2* aux,
+                                      const Slot& s, const Epi& ep, int sq, int e0, int estep, const StageC& c) {
+  const double2* ld = sp.ld;
+  double2* wk = sp.wk;
   constexpr int MB = (TILE / NTH + r - 1) / r;  // butterflies per thread (R * nseq <= TILE)
   const int lgn = a.lgn;
   double2 v[MB][r];
@@ -262,7 +319,7 @@ __device__ __forceinline__ void stage(const C2RArgs& a, const FftIO& io, const d
 #pragma unroll
     for (int t = 0; t < r; ++t) {
       const int e = jj[b] + t * c.Rr;
-      if (IN == IN_Z) v[b][t] = zval<MODE>(a, io, ld, nyq, s, sq, e);
+      if (IN == IN_Z) v[b][t] = zval<MODE>(a, sp, s, sq, e);
       else if (IN == IN_LD) v[b][t] = ld[(e << lgn) + sq];
       else v[b][t] = wk[(e << lgn) + sq];
     }
@@ -274,9 +331,9 @@ __device__ __forceinline__ void stage(const C2RArgs& a, const FftIO& io, const d
     if (!FIRST) {
       jd = (int)__umulhi((unsigned)jj[b], c.magic);
       k = jj[b] - jd * c.Ns;
-      const double2* tw = a.stw + c.twoff + k * (r - 1);
+      const double2* tw = sp.stw + c.twoff + k * (r - 1);
 #pragma unroll
-      for (int t = 1; t < r; ++t) v[b][t] = c_mul(v[b][t], __ldg(tw + t - 1));
+      for (int t = 1; t < r; ++t) v[b][t] = c_mul(v[b][t], tw[t - 1]);
     }
     bfly<r>(v[b]);
     const int idxD = FIRST ? jd * r : jd * c.Ns * r + k;
@@ -287,40 +344,45 @@ __device__ __forceinline__ void stage(const C2RArgs& a, const FftIO& io, const d
       if (OUT == OUT_WK) {
         if (act[b]) wk[((idxD + u * ustep) << lgn) + sq] = v[b][u];
       } else {
-        store_out<MODE>(a, io, s, ep, idxD + u * ustep, v[b][u], gact);
+        store_out<MODE>(a, io, s, ep, aux, idxD + u * ustep, v[b][u], gact);
       }
     }
   }
 }
 
 template <int IN, int OUT, int MODE, bool FIRST>
-__device__ __forceinline__ void stage_r(const C2RArgs& a, const FftIO& io, const double2* ld, const double2* nyq,
-                                        double2* wk, const Slot& s, const Epi& ep, int sq, int e0, int estep,
-                                        const StageC& c) {
+__device__ __forceinline__ void stage_r(const C2RArgs& a, const FftIO& io, const Smem& sp, const double2* aux,
+                                        const Slot& s, const Epi& ep, int sq, int e0, int estep, const StageC& c) {
   switch (c.r) {
-    case 2: stage<2, IN, OUT, MODE, FIRST>(a, io, ld, nyq, wk, s, ep, sq, e0, estep, c); break;
-    case 3: stage<3, IN, OUT, MODE, FIRST>(a, io, ld, nyq, wk, s, ep, sq, e0, estep, c); break;
-    case 4: stage<4, IN, OUT, MODE, FIRST>(a, io, ld, nyq, wk, s, ep, sq, e0, estep, c); break;
-    case 5: stage<5, IN, OUT, MODE, FIRST>(a, io, ld, nyq, wk, s, ep, sq, e0, estep, c); break;
-    default: stage<8, IN, OUT, MODE, FIRST>(a, io, ld, nyq, wk, s, ep, sq, e0, estep, c); break;
+    case 2: stage<2, IN, OUT, MODE, FIRST>(a, io, sp, aux, s, ep, sq, e0, estep, c); break;
+    case 3: stage<3, IN, OUT, MODE, FIRST>(a, io, sp, aux, s, ep, sq, e0, estep, c); break;
+    case 4: stage<4, IN, OUT, MODE, FIRST>(a, io, sp, aux, s, ep, sq, e0, estep, c); break;
+    case 5: stage<5, IN, OUT, MODE, FIRST>(a, io, sp, aux, s, ep, sq, e0, estep, c); break;
+    default: stage<8, IN, OUT, MODE, FIRST>(a, io, sp, aux, s, ep, sq, e0, estep, c); break;
   }
 }
 
 template <int MODE>
 __global__ void __launch_bounds__(NTH, 3) c2r_pass(const __grid_constant__ C2RArgs a, const __grid_constant__ FftIO io) {
   extern __shared__ double2 smem[];
-  double2* ld = smem;
-  double2* wk = smem + TILE;
-  double2* nyq = smem + 2 * TILE;  // nseq values
+  const Smem sp = smem_parts(a, smem);
   const int tid = threadIdx.x;
   const int sq = tid & ((1 << a.lgn) - 1);
   const int e0 = tid >> a.lgn, estep = NTH >> a.lgn;
   constexpr int IN0 = (MODE == 1) ? IN_LD : IN_Z;
 
-  int tile = blockIdx.x;
-  if (tile < a.ntiles) issue_loads<MODE>(a, io, tile, ld, nyq, sq, e0, estep);
-  for (; tile < a.ntiles; tile += gridDim.x) {
+  // once per CTA: the stage twiddles (and, single pass, the whole pairing / scale tables)
+  for (int i = tid; i < a.nstw; i += NTH) cp16(sp.stw + i, a.stw + i, true);
+  if (MODE == 2)
+    for (int i = tid; i < a.naux; i += NTH) {
+      cp16(sp.ptw + i, a.ptw + i, true);
+      cp16(sp.aux2 + i, reinterpret_cast<const double2*>(io.yscale) + i, true);
+    }
+  int tile = blockIdx.x, abuf = 0;
+  if (tile < a.ntiles) issue_loads<MODE>(a, io, tile, sp, abuf, sq, e0, estep);
+  for (; tile < a.ntiles; tile += gridDim.x, abuf ^= 1) {
     const Slot s = slot_of<MODE>(a, tile, sq);
+    const double2* aux = (MODE == 2) ? sp.aux2 : sp.aux2 + abuf * a.naux;
     Epi ep;
     if (MODE == 0) {
       ep.base = s.sub * a.lds + s.col;
@@ -330,21 +392,22 @@ __global__ void __launch_bounds__(NTH, 3) c2r_pass(const __grid_constant__ C2RAr
       ep.kstep = 0;
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
-    __syncthreads();  // LD (and nyq) complete for every thread; WK free (previous tile done)
+    __syncthreads();  // LD, nyq, slices complete for every thread; WK free (previous tile done)
+    const bool more = tile + (int)gridDim.x < a.ntiles;
     if (a.nf == 1) {
-      stage_r<IN0, OUT_G, MODE, true>(a, io, ld, nyq, wk, s, ep, sq, e0, estep, a.st[0]);
+      stage_r<IN0, OUT_G, MODE, true>(a, io, sp, aux, s, ep, sq, e0, estep, a.st[0]);
       __syncthreads();
-      if (tile + (int)gridDim.x < a.ntiles) issue_loads<MODE>(a, io, tile + gridDim.x, ld, nyq, sq, e0, estep);
+      if (more) issue_loads<MODE>(a, io, tile + gridDim.x, sp, abuf ^ 1, sq, e0, estep);
       continue;
     }
-    stage_r<IN0, OUT_WK, MODE, true>(a, io, ld, nyq, wk, s, ep, sq, e0, estep, a.st[0]);
-    __syncthreads();  // LD consumed, WK written
-    if (tile + (int)gridDim.x < a.ntiles) issue_loads<MODE>(a, io, tile + gridDim.x, ld, nyq, sq, e0, estep);
+    stage_r<IN0, OUT_WK, MODE, true>(a, io, sp, aux, s, ep, sq, e0, estep, a.st[0]);
+    __syncthreads();  // LD and the pairing slice consumed, WK written
+    if (more) issue_loads<MODE>(a, io, tile + gridDim.x, sp, abuf ^ 1, sq, e0, estep);
     for (int st = 1; st + 1 < a.nf; ++st) {
-      stage_r<IN_WK, OUT_WK, MODE, false>(a, io, ld, nyq, wk, s, ep, sq, e0, estep, a.st[st]);
+      stage_r<IN_WK, OUT_WK, MODE, false>(a, io, sp, aux, s, ep, sq, e0, estep, a.st[st]);
       __syncthreads();
     }
-    stage_r<IN_WK, OUT_G, MODE, false>(a, io, ld, nyq, wk, s, ep, sq, e0, estep, a.st[a.nf - 1]);
+    stage_r<IN_WK, OUT_G, MODE, false>(a, io, sp, aux, s, ep, sq, e0, estep, a.st[a.nf - 1]);
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
@@ -370,6 +433,7 @@ void set_radices(C2RArgs& a, int nf, const int* f) {
     off += Ns * (f[i] - 1);
     Ns *= f[i];
   }
+  a.nstw = std::max(off, 1);
 }
 
 // e^{+2 pi i m / n} with exact integer reduction of m
@@ -457,22 +521,33 @@ void choose(C2RArgs& a, int smin) {
 
 template <int MODE>
 xc_status launch(C2RArgs& a, const FftIO& io, cudaStream_t st) {
-  const size_t sm = (2 * TILE + 256) * sizeof(double2);
   static bool attr = false;
   if (!attr) {
-    XC_CUDA(cudaFuncSetAttribute(c2r_pass<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    XC_CUDA(cudaFuncSetAttribute(c2r_pass<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     int dev = 0;
     XC_CUDA(cudaGetDevice(&dev));
     XC_CUDA(cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, dev));
     attr = true;
   }
+  a.mode = MODE;
   a.ntx = (a.ncol + a.cb - 1) / a.cb;
   int nty;
   if (MODE == 0) nty = (a.P + a.sc / 2 - 1) / (a.sc / 2);
   else if (MODE == 1) nty = (a.S + a.sc - 1) / a.sc;
   else nty = 1;
   a.ntiles = a.ntx * nty;
-  const int grid = std::min(a.ntiles, 3 * std::max(1, g_nsm));
+  a.naux = (MODE == 2) ? a.R : a.sc * a.R;
+  const int nseq = 1 << a.lgn;
+  const size_t ent = 2 * (size_t)a.R * nseq + nseq + a.nstw + (MODE == 1 ? 0 : a.naux) +
+                     (MODE == 2 ? 1 : 2) * (size_t)a.naux;
+  const size_t sm = ent * sizeof(double2);
+  if (sm > 200 * 1024) {
+    xc_set_error("c2r: tile does not fit shared memory");
+    return XC_EUNSUPPORTED;
+  }
+  int per_sm = 0;
+  XC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c2r_pass<MODE>, NTH, sm));
+  const int grid = std::min(a.ntiles, std::max(1, per_sm) * std::max(1, g_nsm));
   c2r_pass<MODE><<<grid, NTH, sm, st>>>(a, io);
   XC_CUDA(cudaGetLastError());
   return XC_OK;
