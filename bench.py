@@ -188,7 +188,9 @@ def main():
     t_nodes = time.perf_counter() - t0
     dirs = xc.XC_DIR_A | (xc.XC_DIR_WAT if "WAT" in cfg.dirs else 0)
     t0 = time.perf_counter()
-    T = xc.Transform(cfg.kind, x, cfg.eps, alpha=cfg.alpha, beta=cfg.beta, dirs=dirs, weights=wt, device=local)
+    # N > 1: distributed precompute (node range per rank, NCCL all-gather of the node bands)
+    T = xc.Transform(cfg.kind, x, cfg.eps, alpha=cfg.alpha, beta=cfg.beta, dirs=dirs, weights=wt, device=local,
+                     dist=(rank, ws, xc.nccl_allgather()) if ws > 1 else None)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     info = T.info()
@@ -299,7 +301,8 @@ def main():
             "e2e": e2e,
             "gpu_launches": info["launches_A" if direction == xc.XC_DIR_A else "launches_WAT"] * args.steps,
             "clocks": clk,
-            "precompute_s": {"gauss_nodes": t_nodes, "build": t_build},
+            "precompute_s": {"gauss_nodes": t_nodes, "build": t_build,
+                             "mode": f"node range split over {ws} ranks + NCCL all-gather" if ws > 1 else "one GPU"},
             "nnz": nnz,
         }
         print(json.dumps(line), flush=True)

@@ -107,6 +107,28 @@ xc_status xc_params_default(xc_params* p);
 xc_status xc_build_compressed(xc_kind kind, const xc_params* p, const double* nodes, int64_t N,
                               double eps, xc_handle* out);
 
+/* Distributed precompute (the node range of the operator is split over ranks).
+ * One exchange: the caller copies `send` (bytes_per_rank device bytes) of every rank into
+ * `recv` in rank order (recv + r * bytes_per_rank), e.g. one NCCL all-gather.
+ * xc_build_local: phase 1 and the node bands (entries, FFT, threshold; p2-p4) of nodes
+ *   [rank * ceil(N/nranks), (rank + 1) * ceil(N/nranks)) only; *ex describes the first exchange
+ *   (every node's band start and length).  Same arguments as xc_build_compressed.
+ * xc_build_step: consumes the completed exchange; sets *ex to the next one (the kept values,
+ *   padded to the largest rank's count) or, after the last, finishes the build (tiles of the
+ *   whole operator, identical to xc_build_compressed's) and sets ex->bytes_per_rank = 0.
+ * The buffers in *ex are owned by the handle and valid until the next call on it.
+ * Errors: XC_EINVAL (bad rank / nranks, as xc_build_compressed), XC_ESTATE (step outside a
+ * distributed build).  The handle is unusable for xc_apply until the build has finished. */
+typedef struct {
+  void* send;             /* device, bytes_per_rank bytes                                   */
+  void* recv;             /* device, nranks * bytes_per_rank bytes, rank-major              */
+  size_t bytes_per_rank;  /* 0: no exchange pending (build finished)                        */
+} xc_exchange_t;
+
+xc_status xc_build_local(xc_kind kind, const xc_params* p, const double* nodes, int64_t N, double eps,
+                         int rank, int nranks, xc_handle* out, xc_exchange_t* ex);
+xc_status xc_build_step(xc_handle h, xc_exchange_t* ex);
+
 /* Computation stage (Alg. 2 step 2 / Alg. 1 step 2 per block):
  * X, Y: DEVICE pointers, row-major N x B with leading dimensions ldx, ldy >= B.
  * Enqueues on `stream` only (no host synchronisation).  Allocates device

@@ -309,17 +309,19 @@ __device__ __forceinline__ void stage(const C2RArgs& a, const FftIO& io, const S
   constexpr int MB = (TILE / NTH + r - 1) / r;  // butterflies per thread (R * nseq <= TILE)
   const int lgn = a.lgn;
   double2 v[MB][r];
-  bool act[MB];
+  bool act[MB], wact[MB];
   int jj[MB];
 #pragma unroll
   for (int b = 0; b < MB; ++b) {
     const int j = e0 + b * estep;
     act[b] = j < c.Rr;
+    wact[b] = __any_sync(0xffffffffu, act[b]);  // warp-uniform: rounds with no work are skipped
     jj[b] = act[b] ? j : c.Rr - 1;
 #pragma unroll
     for (int t = 0; t < r; ++t) {
       const int e = jj[b] + t * c.Rr;
-      if (IN == IN_Z) v[b][t] = zval<MODE>(a, sp, s, sq, e);
+      if (!wact[b]) v[b][t] = make_double2(0.0, 0.0);
+      else if (IN == IN_Z) v[b][t] = zval<MODE>(a, sp, s, sq, e);
       else if (IN == IN_LD) v[b][t] = ld[(e << lgn) + sq];
       else v[b][t] = wk[(e << lgn) + sq];
     }
@@ -327,6 +329,7 @@ __device__ __forceinline__ void stage(const C2RArgs& a, const FftIO& io, const S
   if (IN == IN_WK && OUT == OUT_WK) __syncthreads();  // in place: all reads before any write
 #pragma unroll
   for (int b = 0; b < MB; ++b) {
+    if (!wact[b]) continue;
     int jd = jj[b], k = 0;
     if (!FIRST) {
       jd = (int)__umulhi((unsigned)jj[b], c.magic);

@@ -407,15 +407,51 @@ void set_stages(PassArgs& a, int nf, const int* f) {
 
 }  // namespace
 
-xc_status fft_plan_make(FftPlan& p, int L) {
+// Warp-rounds per element of the C2R pass engine (c2r.cu: 256 threads, tiles of R * nseq <= 2048
+// points, nseq a power of two with at least smin sub-sequences, rounds without an active lane
+// skipped per warp) for a sub-transform of length R: the cost model of the four-step split.
+double c2r_pass_cost(int R, int smin) {
+  int f[12], nf;
+  factorize(R, nf, f);
+  if (nf < 0) return 1e30;
+  int nseq = 1;
+  while (2 * nseq * R <= 2048 && nseq < 256) nseq *= 2;
+  if (nseq < smin) return 1e30;
+  int lgn = ilog2(nseq);
+  const int estep = 256 >> lgn;
+  double warps = 0;
+  for (int i = 0; i < nf; ++i) {
+    const int r = f[i], Rr = R / r, MB = (8 + r - 1) / r;
+    for (int b = 0; b < MB; ++b)
+      for (int w = 0; w < 8; ++w) {
+        const int e0min = (32 * w) >> lgn;
+        if (e0min + b * estep < Rr) warps += 1;
+      }
+  }
+  return warps * 32.0 / ((double)R * nseq);
+}
+
+xc_status fft_plan_make(FftPlan& p, int L, bool c2r) {
   p.L = L;
   if (L <= 512) {
     p.L1 = L;
     p.L2 = 1;
   } else {
     int best = -1;
-    for (int d = 2; (int64_t)d * d <= L; ++d)
-      if (L % d == 0) best = d;
+    if (c2r) {  // the split with the cheapest pair of C2R passes (first pass pairs sub-sequences)
+      double bc = 1e30;
+      for (int d = 2; d <= 256; ++d) {
+        if (L % d || L / d > 256) continue;
+        const double c = c2r_pass_cost(d, 2) + c2r_pass_cost(L / d, 1);
+        if (c < bc - 1e-9) {
+          bc = c;
+          best = d;
+        }
+      }
+    }
+    if (best < 0)
+      for (int d = 2; (int64_t)d * d <= L; ++d)
+        if (L % d == 0) best = d;
     if (best < 0 || L / best > 1024) {
       xc_set_error("fft: length " + std::to_string(L) + " not splittable into two factors <= 1024");
       return XC_EUNSUPPORTED;

@@ -70,6 +70,7 @@ struct BlockData {
   int64_t nnz = 0;
   int max_band = 0;
   int ngroups = 0;
+  int64_t loc_count = 0;  // values of the locally computed node range (distributed precompute)
   DevBuf grp_base, grp_nch;  // output axis groups
 };
 
@@ -110,6 +111,14 @@ struct xc_op {
   cudaEvent_t ev_start = nullptr;
   std::vector<int64_t> zoff;  // per block offset (doubles) of its z' planes in zpl
   xc_info_t info{};
+  // build state (kept between the phases of a distributed precompute)
+  DevBuf djtab;
+  ddv p0{1.0, 0.0};
+  cudaStream_t bst = nullptr;
+  int node_chunk = 0;
+  int rank = 0, nranks = 1, npr = 0, xstage = 0;  // npr: nodes per rank (padded)
+  DevBuf xsend, xrecv;
+  std::vector<int64_t> xmaxc;  // per block: max over ranks of the local value count
   // phase profiling (ring of event sets: start, after phase 1, after phase 2, end)
   static constexpr int kRing = 512;
   bool prof = false;
@@ -174,12 +183,12 @@ xc_status validate_nodes(int kind, const double* x, int64_t N) {
 }
 
 // --- the per-block precompute: entries -> FFT -> threshold -> node bands ------------
-xc_status build_block(xc_op* h, BlockData& b, const std::vector<double2>& jtab, const DevBuf& djtab, ddv p0,
-                      int node_chunk, cudaStream_t st) {
+xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int node_chunk, int n0, int n1,
+                      cudaStream_t st) {
   const int N = (int)h->N;
   b.H = b.L / 2 + 1;
   XC_TRY(fft_plan_make(b.fft, b.L));
-  XC_TRY(fft_plan_make(b.fftM, b.L / 2));
+  XC_TRY(fft_plan_make(b.fftM, b.L / 2, true));
   {
     std::vector<double2> tw(b.L / 2);
     const long double PI2 = 6.283185307179586476925286766559005768L;
@@ -216,8 +225,8 @@ xc_status build_block(xc_op* h, BlockData& b, const std::vector<double2>& jtab, 
   std::vector<int64_t> chunk_base;
   DevBuf choff;
 
-  for (int k0 = 0; k0 < N; k0 += nc) {
-    int n = std::min(nc, N - k0);
+  for (int k0 = n0; k0 < n1; k0 += nc) {
+    int n = std::min(nc, n1 - k0);
     GenParams g{};
     g.kind = h->kind;
     g.L = b.L;
@@ -258,15 +267,9 @@ xc_status build_block(xc_op* h, BlockData& b, const std::vector<double2>& jtab, 
     chunk_vals.push_back(cv);
     chunk_base.push_back(tot);
   }
-  // global offsets and one contiguous value array
+  // the local node range's values, contiguous in node order
   int64_t acc = 0;
-  b.max_band = 0;
-  for (int k = 0; k < N; ++k) {
-    b.h_off[k] = acc;
-    acc += b.h_len[k];
-    b.max_band = std::max(b.max_band, b.h_len[k]);
-  }
-  b.h_off[N] = acc;
+  for (int64_t c : chunk_base) acc += c;
   XC_TRY(dev_alloc(b.vals, (size_t)std::max<int64_t>(1, acc) * sizeof(double2)));
   int64_t pos = 0;
   for (size_t c = 0; c < chunk_vals.size(); ++c) {
@@ -278,12 +281,28 @@ xc_status build_block(xc_op* h, BlockData& b, const std::vector<double2>& jtab, 
   XC_CUDA(cudaStreamSynchronize(st));
   for (auto& cv : chunk_vals) dev_free(cv);
   dev_free(choff);
-  XC_TRY(upload(b.off, b.h_off));
-  // kept nonzeros (the stored runs contain explicit zeros for dropped interior bins)
-  b.nnz = acc;
+  b.loc_count = acc;
   dev_free(F);
   dev_free(scr);
   dev_free(spec);
+  return XC_OK;
+}
+
+// Global band offsets once every node's band is known (h_start/h_len for all N nodes,
+// b.vals holding all values in node order).
+xc_status finalize_bands(xc_op* h, BlockData& b) {
+  const int N = (int)h->N;
+  int64_t acc = 0;
+  b.max_band = 0;
+  for (int k = 0; k < N; ++k) {
+    b.h_off[k] = acc;
+    acc += b.h_len[k];
+    b.max_band = std::max(b.max_band, b.h_len[k]);
+  }
+  b.h_off[N] = acc;
+  XC_TRY(upload(b.off, b.h_off));
+  // kept nonzeros (the stored runs contain explicit zeros for dropped interior bins)
+  b.nnz = acc;
   return XC_OK;
 }
 
@@ -574,7 +593,8 @@ xc_status build_input_axis(xc_op* h, cudaStream_t st) {
 
 double fft_flops(int L) { return 2.5 * L * log2((double)L); }  // real FFT = half of 5 L log2 L
 
-xc_status build_impl(xc_kind kind, const xc_params* prm, const double* nodes, int64_t N, double eps, xc_op* h) {
+// Phase 1 of the precompute: validation, plan (p1), per-block windows / FFT plans, nodes.
+xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, int64_t N, double eps, xc_op* h) {
   xc_params p;
   xc_params_default(&p);
   if (prm) p = *prm;
@@ -630,14 +650,28 @@ xc_status build_impl(xc_kind kind, const xc_params* prm, const double* nodes, in
   XC_TRY(upload(h->nodes, std::vector<double>(nodes, nodes + N)));
   if (h->dirs & XC_DIR_WAT) XC_TRY(upload(h->wt, std::vector<double>(p.weights, p.weights + N)));
 
-  std::vector<double2> jtab;
-  ddv p0 = dv(1.0);
-  DevBuf djtab;
+  h->bst = st;
+  h->node_chunk = p.node_chunk;
   if (kind == XC_JACOBI) {
-    jacobi_coeffs(p.alpha, p.beta, std::max(Lmax, h->tail) + 2, jtab, p0);
-    XC_TRY(upload(djtab, jtab));
+    std::vector<double2> jtab;
+    jacobi_coeffs(p.alpha, p.beta, std::max(Lmax, h->tail) + 2, jtab, h->p0);
+    XC_TRY(upload(h->djtab, jtab));
   }
-  for (auto& b : h->blocks) XC_TRY(build_block(h, b, jtab, djtab, p0, p.node_chunk, st));
+  return XC_OK;
+}
+
+// Phase 2 (p2-p4): node bands of the nodes [n0, n1) of every block.
+xc_status build_bands(xc_op* h, int n0, int n1) {
+  for (auto& b : h->blocks) XC_TRY(build_block(h, b, h->djtab, h->p0, h->node_chunk, n0, n1, h->bst));
+  return XC_OK;
+}
+
+// Phase 3: global band offsets, dense tail entries, tensor-core tiles, info.
+xc_status build_end(xc_op* h) {
+  const int64_t N = h->N;
+  const xc_kind kind = (xc_kind)h->kind;
+  cudaStream_t st = h->bst;
+  for (auto& b : h->blocks) XC_TRY(finalize_bands(h, b));
   // dense tail entries P[j][k] = phi_j(x_k), j < t
   if (h->tail > 0) {
     XC_TRY(dev_alloc(h->tailP, (size_t)h->tail * N * sizeof(double)));
@@ -648,14 +682,14 @@ xc_status build_impl(xc_kind kind, const xc_params* prm, const double* nodes, in
     g.nodes = (const double*)h->nodes.p;
     g.nc = (int)N;
     g.w = nullptr;
-    g.jab = (const double2*)djtab.p;
-    g.p0 = p0;
+    g.jab = (const double2*)h->djtab.p;
+    g.p0 = h->p0;
     XC_TRY(gen_entries_real(g, (double*)h->tailP.p, N, st));
     XC_CUDA(cudaStreamSynchronize(st));
   }
   if (h->dirs & XC_DIR_A) XC_TRY(build_output_axis(h, st));
   if (h->dirs & XC_DIR_WAT) XC_TRY(build_input_axis(h, st));
-  dev_free(djtab);
+  dev_free(h->djtab);
   XC_CUDA(cudaStreamSynchronize(st));
 
   // info
@@ -693,6 +727,12 @@ xc_status build_impl(xc_kind kind, const xc_params* prm, const double* nodes, in
   return XC_OK;
 }
 
+xc_status build_impl(xc_kind kind, const xc_params* prm, const double* nodes, int64_t N, double eps, xc_op* h) {
+  XC_TRY(build_begin(kind, prm, nodes, N, eps, h));
+  XC_TRY(build_bands(h, 0, (int)N));
+  return build_end(h);
+}
+
 xc_status prof_harvest(xc_op* h, int slot) {
   if (h->ev_dir[slot] == 0) return XC_OK;
   cudaEvent_t* e = &h->ev[4 * slot];
@@ -726,8 +766,8 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
     xc_set_error("apply: B too large");
     return XC_EINVAL;
   }
-  if (!(h->dirs & dir)) {
-    xc_set_error("apply: direction was not built");
+  if (!(h->dirs & dir) || h->xstage != 0) {
+    xc_set_error(h->xstage ? "apply: distributed build not finished" : "apply: direction was not built");
     return XC_ESTATE;
   }
   XC_TRY(ensure_ws(h, B));
@@ -843,7 +883,7 @@ void destroy_impl(xc_op* h) {
   }
   DevBuf* all[] = {&h->nodes, &h->wt, &h->tailP, &h->itemsA, &h->tilesA, &h->winsA, &h->tail_base, &h->tail_nch,
                    &h->itemsW, &h->tilesW, &h->winsW, &h->nodeg_base, &h->nodeg_nch, &h->partA, &h->partW,
-                   &h->scratch, &h->zpl, &h->Xh, &h->Yh};
+                   &h->scratch, &h->zpl, &h->Xh, &h->Yh, &h->xsend, &h->xrecv, &h->djtab};
   for (DevBuf* b : all) dev_free(*b);
 }
 
@@ -873,6 +913,148 @@ xc_status xc_build_compressed(xc_kind kind, const xc_params* p, const double* no
     return s;
   }
   *out = h;
+  return XC_OK;
+}
+
+// ---- distributed precompute: node range per rank + two all-gathers ----------
+namespace {
+
+// Exchange 1: per block, the (start, len) of this rank's nodes, padded to npr nodes.
+xc_status stage_exchange1(xc_op* h) {
+  const int nb = (int)h->blocks.size();
+  const int n0 = h->rank * h->npr, n1 = std::min<int>((int)h->N, n0 + h->npr);
+  std::vector<int> buf((size_t)nb * 2 * h->npr, 0);
+  for (int i = 0; i < nb; ++i) {
+    BlockData& b = h->blocks[i];
+    for (int k = n0; k < n1; ++k) {
+      buf[((size_t)i * 2 + 0) * h->npr + (k - n0)] = b.h_start[k];
+      buf[((size_t)i * 2 + 1) * h->npr + (k - n0)] = b.h_len[k];
+    }
+  }
+  const size_t bytes = buf.size() * sizeof(int);
+  XC_TRY(dev_alloc(h->xsend, bytes));
+  XC_TRY(dev_alloc(h->xrecv, bytes * h->nranks));
+  XC_CUDA(cudaMemcpy(h->xsend.p, buf.data(), bytes, cudaMemcpyHostToDevice));
+  return XC_OK;
+}
+
+// After exchange 1: every node's band; exchange 2 carries each rank's values per block,
+// padded to the largest rank's count.
+xc_status stage_exchange2(xc_op* h) {
+  const int nb = (int)h->blocks.size();
+  const int N = (int)h->N;
+  std::vector<int> all((size_t)h->nranks * nb * 2 * h->npr);
+  XC_CUDA(cudaMemcpy(all.data(), h->xrecv.p, all.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  h->xmaxc.assign(nb, 1);
+  for (int i = 0; i < nb; ++i) {
+    BlockData& b = h->blocks[i];
+    for (int r = 0; r < h->nranks; ++r) {
+      const int* st = all.data() + (((size_t)r * nb + i) * 2 + 0) * h->npr;
+      const int* ln = all.data() + (((size_t)r * nb + i) * 2 + 1) * h->npr;
+      int64_t cnt = 0;
+      for (int j = 0; j < h->npr && r * h->npr + j < N; ++j) {
+        b.h_start[r * h->npr + j] = st[j];
+        b.h_len[r * h->npr + j] = ln[j];
+        cnt += ln[j];
+      }
+      h->xmaxc[i] = std::max<int64_t>(h->xmaxc[i], cnt);
+    }
+  }
+  size_t per = 0;
+  for (int i = 0; i < nb; ++i) per += (size_t)h->xmaxc[i] * sizeof(double2);
+  XC_TRY(dev_alloc(h->xsend, per));
+  XC_TRY(dev_alloc(h->xrecv, per * h->nranks));
+  XC_CUDA(cudaMemset(h->xsend.p, 0, per));
+  size_t off = 0;
+  for (int i = 0; i < nb; ++i) {
+    BlockData& b = h->blocks[i];
+    if (b.loc_count > 0)
+      XC_CUDA(cudaMemcpy((char*)h->xsend.p + off, b.vals.p, b.loc_count * sizeof(double2), cudaMemcpyDeviceToDevice));
+    off += (size_t)h->xmaxc[i] * sizeof(double2);
+  }
+  return XC_OK;
+}
+
+// After exchange 2: the full value arrays, then the rest of the build.
+xc_status stage_finish(xc_op* h) {
+  const int nb = (int)h->blocks.size();
+  const int N = (int)h->N;
+  size_t per = 0;
+  for (int i = 0; i < nb; ++i) per += (size_t)h->xmaxc[i] * sizeof(double2);
+  size_t boff = 0;
+  for (int i = 0; i < nb; ++i) {
+    BlockData& b = h->blocks[i];
+    int64_t total = 0;
+    for (int k = 0; k < N; ++k) total += b.h_len[k];
+    XC_TRY(dev_alloc(b.vals, (size_t)std::max<int64_t>(1, total) * sizeof(double2)));
+    int64_t pos = 0;
+    for (int r = 0; r < h->nranks; ++r) {
+      int64_t cnt = 0;
+      for (int j = 0; j < h->npr && r * h->npr + j < N; ++j) cnt += b.h_len[r * h->npr + j];
+      if (cnt > 0)
+        XC_CUDA(cudaMemcpy((double2*)b.vals.p + pos, (const char*)h->xrecv.p + r * per + boff,
+                           cnt * sizeof(double2), cudaMemcpyDeviceToDevice));
+      pos += cnt;
+    }
+    boff += (size_t)h->xmaxc[i] * sizeof(double2);
+    XC_CUDA(cudaMemcpy(b.start.p, b.h_start.data(), N * sizeof(int), cudaMemcpyHostToDevice));
+    XC_CUDA(cudaMemcpy(b.len.p, b.h_len.data(), N * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  dev_free(h->xsend);
+  dev_free(h->xrecv);
+  return build_end(h);
+}
+
+void set_exchange(xc_op* h, xc_exchange_t* ex) {
+  ex->send = h->xsend.p;
+  ex->recv = h->xrecv.p;
+  ex->bytes_per_rank = h->xsend.p ? h->xsend.bytes : 0;
+}
+
+}  // namespace
+
+xc_status xc_build_local(xc_kind kind, const xc_params* p, const double* nodes, int64_t N, double eps, int rank,
+                         int nranks, xc_handle* out, xc_exchange_t* ex) {
+  if (!out || !ex || nranks < 1 || rank < 0 || rank >= nranks) {
+    xc_set_error("build_local: need out, ex and 0 <= rank < nranks");
+    return XC_EINVAL;
+  }
+  *out = nullptr;
+  xc_op* h = new xc_op();
+  auto fail = [&](xc_status s) {
+    destroy_impl(h);
+    delete h;
+    return s;
+  };
+  xc_status s = build_begin(kind, p, nodes, N, eps, h);
+  if (s != XC_OK) return fail(s);
+  h->rank = rank;
+  h->nranks = nranks;
+  h->npr = (int)((N + nranks - 1) / nranks);
+  const int n0 = std::min<int>((int)N, rank * h->npr), n1 = std::min<int>((int)N, n0 + h->npr);
+  if ((s = build_bands(h, n0, n1)) != XC_OK) return fail(s);
+  if ((s = stage_exchange1(h)) != XC_OK) return fail(s);
+  h->xstage = 1;
+  set_exchange(h, ex);
+  *out = h;
+  return XC_OK;
+}
+
+xc_status xc_build_step(xc_handle h, xc_exchange_t* ex) {
+  if (!h || !ex || h->xstage < 1 || h->xstage > 2) {
+    xc_set_error("build_step: handle is not in a distributed build");
+    return XC_ESTATE;
+  }
+  XC_CUDA(cudaSetDevice(h->device));
+  if (h->xstage == 1) {
+    XC_TRY(stage_exchange2(h));
+    h->xstage = 2;
+    set_exchange(h, ex);
+    return XC_OK;
+  }
+  XC_TRY(stage_finish(h));
+  h->xstage = 0;
+  set_exchange(h, ex);
   return XC_OK;
 }
 

@@ -144,7 +144,7 @@ struct FftIO {
   double scale = 1.0;                                      // EPI_PLAIN / EPI_ZPLANES
 };
 
-xc_status fft_plan_make(FftPlan& p, int L);
+xc_status fft_plan_make(FftPlan& p, int L, bool c2r = false);  // c2r: split chosen for c2r_run
 void fft_plan_free(FftPlan& p);
 // sigma = -1 forward (Eq. 1), +1 inverse.  ncol columns.  scratch: L*ncol double2 (2-pass only).
 xc_status fft_run(const FftPlan& p, int sigma, FftPro pro, FftEpi epi, const FftIO& io, int ncol,

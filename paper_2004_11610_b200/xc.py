@@ -39,12 +39,16 @@ class XcInfo(ctypes.Structure):
                 ("launches_A", ctypes.c_int), ("launches_WAT", ctypes.c_int)]
 
 
+class XcExchange(ctypes.Structure):
+    _fields_ = [("send", ctypes.c_void_p), ("recv", ctypes.c_void_p), ("bytes_per_rank", ctypes.c_size_t)]
+
+
 class XcBlockInfo(ctypes.Structure):
     _fields_ = [("L", ctypes.c_int), ("H", ctypes.c_int), ("m_off", ctypes.c_int), ("keep_lo", ctypes.c_int),
                 ("keep_hi", ctypes.c_int), ("nnz", _i64), ("max_band", ctypes.c_int)]
 
 
-EXPORTS = ["xc_params_default", "xc_build_compressed", "xc_apply", "xc_apply_host", "xc_reserve",
+EXPORTS = ["xc_params_default", "xc_build_compressed", "xc_build_local", "xc_build_step", "xc_apply", "xc_apply_host", "xc_reserve",
            "xc_workspace_query", "xc_info", "xc_block_info", "xc_block_window", "xc_node_spectrum",
            "xc_gauss_rule", "xc_plan_chain", "xc_profile_enable", "xc_profile_read", "xc_destroy",
            "xc_last_error", "xc_version"]
@@ -68,6 +72,9 @@ def load():
     lib.xc_params_default.argtypes = [ctypes.POINTER(XcParams)]
     lib.xc_build_compressed.argtypes = [ctypes.c_int, ctypes.POINTER(XcParams), _dp, _i64, ctypes.c_double,
                                         ctypes.POINTER(vp)]
+    lib.xc_build_local.argtypes = [ctypes.c_int, ctypes.POINTER(XcParams), _dp, _i64, ctypes.c_double, ctypes.c_int,
+                                   ctypes.c_int, ctypes.POINTER(vp), ctypes.POINTER(XcExchange)]
+    lib.xc_build_step.argtypes = [vp, ctypes.POINTER(XcExchange)]
     lib.xc_apply.argtypes = [vp, ctypes.c_int, vp, _i64, vp, _i64, _i64, vp]
     lib.xc_apply_host.argtypes = [vp, ctypes.c_int, vp, vp, _i64, vp]
     lib.xc_reserve.argtypes = [vp, _i64]
@@ -128,12 +135,40 @@ def plan_chain(kind: int, N: int, eps1: float, eps2: float = 0.0, dense_cutoff: 
     return z.value, blocks, tail.value
 
 
+def device_bytes(ptr: int, nbytes: int, device: int = 0):
+    """A uint8 CUDA tensor viewing `nbytes` of library-owned device memory (no copy)."""
+    import torch
+
+    class _View:
+        pass
+
+    v = _View()
+    v.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3,
+                                  "strides": None}
+    return torch.as_tensor(v, device=f"cuda:{device}")
+
+
+def nccl_allgather(group=None):
+    """The exchange of a distributed build as one torch.distributed all-gather (NCCL on GPUs):
+    recv[r * n : (r + 1) * n] = send of rank r."""
+    import torch.distributed as dist
+
+    def ag(send, recv):
+        dist.all_gather_into_tensor(recv, send, group=group)
+    return ag
+
+
 class Transform:
-    """A compressed special-function transform (handle of xc_build_compressed)."""
+    """A compressed special-function transform (handle of xc_build_compressed).
+
+    dist=(rank, nranks, allgather): distributed precompute -- this rank computes
+    the node bands of its node range, `allgather(send, recv)` (uint8 CUDA tensors, recv
+    rank-major; e.g. nccl_allgather()) exchanges them, and every rank ends with the whole
+    operator (identical to the single-process build)."""
 
     def __init__(self, kind: int, nodes, eps: float, alpha: float = 0.0, beta: float = 0.0,
                  eps1: float = 0.0, eps2: float = 0.0, dense_cutoff: int = 0, dirs: int = XC_DIR_A,
-                 weights=None, device: int = 0, node_chunk: int = 0, stream=None):
+                 weights=None, device: int = 0, node_chunk: int = 0, stream=None, dist=None):
         lib = load()
         self._lib = lib
         self.kind = kind
@@ -149,9 +184,27 @@ class Transform:
             p.weights = _np_ptr(self._w)
         p.stream = ctypes.c_void_p(stream) if stream else None
         h = ctypes.c_void_p()
-        _check(lib.xc_build_compressed(kind, ctypes.byref(p), _np_ptr(x), self.N, eps, ctypes.byref(h)))
-        self._h = h
         self.device = device
+        if dist is None:
+            _check(lib.xc_build_compressed(kind, ctypes.byref(p), _np_ptr(x), self.N, eps, ctypes.byref(h)))
+            self._h = h
+            return
+        import torch
+        rank, nranks, allgather = dist
+        ex = XcExchange()
+        _check(lib.xc_build_local(kind, ctypes.byref(p), _np_ptr(x), self.N, eps, rank, nranks, ctypes.byref(h),
+                                  ctypes.byref(ex)))
+        self._h = h
+        self.exchanges = []
+        while ex.bytes_per_rank:
+            n = ex.bytes_per_rank
+            send = device_bytes(ex.send, n, device)
+            recv = device_bytes(ex.recv, n * nranks, device)
+            torch.cuda.synchronize(device)
+            allgather(send, recv)
+            torch.cuda.synchronize(device)
+            self.exchanges.append(n)
+            _check(lib.xc_build_step(self._h, ctypes.byref(ex)))
 
     # -- computation stage --------------------------------------------------------------
     def apply(self, X, direction: int = XC_DIR_A, out=None, stream=None):

@@ -70,3 +70,29 @@ def test_two_rank_gloo_shards_equal_single_process(tmp_path):
     for r in range(2):
         mx, tot = np.load(tmp_path / f"m{r}.npy")
         assert mx == 11.0 and tot == B
+
+
+def _ag_worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+    from paper_2004_11610_b200 import xc
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 13 + 0  # bytes per rank (odd on purpose)
+    send = torch.arange(n, dtype=torch.uint8) + 100 * rank
+    recv = torch.empty(n * world, dtype=torch.uint8)
+    xc.nccl_allgather()(send, recv)   # the binding's exchange: rank-major all-gather
+    np.save(os.path.join(out_dir, f"ag{rank}.npy"), recv.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_exchange_layout(tmp_path):
+    """The distributed precompute's exchange contract (include/xc.h, xc_exchange_t): recv holds
+    rank r's send at offset r * bytes_per_rank on every rank."""
+    port = _free_port()
+    mp.spawn(_ag_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    want = np.concatenate([np.arange(13, dtype=np.uint8) + 100 * r for r in range(2)])
+    for r in range(2):
+        assert np.array_equal(np.load(tmp_path / f"ag{r}.npy"), want)

@@ -249,3 +249,86 @@ def test_errors():
     with pytest.raises(xc.XcError):
         T.apply(_gpu(np.ones((63, 2))))
     T.close()
+
+
+def _drive_ranks(lib, kind_t, x, eps, nranks):
+    """Distributed precompute with nranks emulated in one process: every rank's
+    xc_build_local / xc_build_step run in lockstep; the all-gather is done by concatenating the
+    ranks' send buffers (rank-major) into every rank's recv buffer."""
+    import ctypes
+    xc = _xc()
+    p = xc.XcParams()
+    lib.xc_params_default(ctypes.byref(p))
+    p.alpha, p.beta = kind_t[1], kind_t[2]
+    hs, exs = [], []
+    for r in range(nranks):
+        h, ex = ctypes.c_void_p(), xc.XcExchange()
+        xc._check(lib.xc_build_local(kind_t[0], ctypes.byref(p), xc._np_ptr(x), x.size, eps, r, nranks,
+                                     ctypes.byref(h), ctypes.byref(ex)))
+        hs.append(h)
+        exs.append(ex)
+    rounds = 0
+    while exs[0].bytes_per_rank:
+        n = exs[0].bytes_per_rank
+        assert all(e.bytes_per_rank == n for e in exs)
+        cat = torch.cat([xc.device_bytes(e.send, n) for e in exs])
+        for e in exs:
+            xc.device_bytes(e.recv, n * nranks).copy_(cat)
+        torch.cuda.synchronize()
+        for h, e in zip(hs, exs):
+            xc._check(lib.xc_build_step(h, ctypes.byref(e)))
+        rounds += 1
+    return hs, rounds
+
+
+@pytest.mark.parametrize("nranks", [1, 3])
+def test_distributed_build_equals_single(nranks):
+    """p5: node-range-split precompute + exchanges gives every rank the operator of the
+    single-process build (bit-identical applies and node spectra)."""
+    import ctypes
+    xc = _xc()
+    lib = xc.load()
+    kt = (O.KIND_JACOBI, 0.5, -0.3)
+    N, B, eps = 2000, 40, 1e-12
+    x, _ = _nodes(kt, N, 2)
+    X = _gpu(I.rhs(N, B, 8))
+    T = xc.Transform(kt[0], x, eps, alpha=kt[1], beta=kt[2])
+    Y = T.apply(X)
+    hs, rounds = _drive_ranks(lib, kt, x, eps, nranks)
+    assert rounds == 2
+    for h in hs:
+        Yd = torch.empty_like(Y)
+        xc._check(lib.xc_apply(h, xc.XC_DIR_A, ctypes.c_void_p(X.data_ptr()), B, ctypes.c_void_p(Yd.data_ptr()),
+                               B, B, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        torch.cuda.synchronize()
+        assert torch.equal(Yd, Y)
+        H = T.block_info(1)["H"]
+        re, im = np.empty(H), np.empty(H)
+        for k in (0, N // 3, N - 1):
+            xc._check(lib.xc_node_spectrum(h, 1, k, xc._np_ptr(re), xc._np_ptr(im)))
+            assert np.array_equal(re + 1j * im, T.node_spectrum(1, k))
+        lib.xc_destroy(h)
+    T.close()
+
+
+def test_distributed_build_via_process_group():
+    """The binding's distributed build through a 1-rank NCCL process group (torch.distributed
+    all-gather of the library's exchange buffers)."""
+    import os
+    import torch.distributed as dist
+    xc = _xc()
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    kt = (O.KIND_JACOBI, 0.0, 0.0)
+    N, eps = 1024, 1e-12
+    x, _ = _nodes(kt, N, 0)
+    X = _gpu(I.rhs(N, 8, 3))
+    T = xc.Transform(xc.XC_JACOBI, x, eps)
+    Td = xc.Transform(xc.XC_JACOBI, x, eps, dist=(0, 1, xc.nccl_allgather()))
+    assert len(Td.exchanges) == 2
+    assert torch.equal(T.apply(X), Td.apply(X))
+    T.close()
+    Td.close()
+    dist.destroy_process_group()
