@@ -21,6 +21,7 @@
 // the last stage writes global memory straight from registers (columns are the fast
 // index, so every store is a contiguous run of cb * 16 or cb * 8 bytes).
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <mutex>
@@ -110,6 +111,39 @@ struct StageC {
   int twoff;              // offset of this stage's table w_{Ns r}^{k t}, [k][t-1], in C2RArgs::stw
   unsigned magic;         // ceil(2^32 / Ns): j / Ns by __umulhi (exact for j < 2^16)
 };
+
+// Tile geometry: sub-transform length and log2(sequences per tile).  Compile-time constants
+// in the specialised kernels (all smem offsets fold to immediates), runtime in the generic one.
+struct Geo {
+  int R, lgn;
+};
+
+// The radix plan of a length (factorize() order: 8s, 4, 2, 5s, 3s) as compile-time data.
+struct StagePlan {
+  int nf;
+  StageC st[12];
+};
+constexpr StagePlan stages_of(int R) {
+  StagePlan p{};
+  int f[12] = {}, nf = 0, x = R;
+  while (x % 8 == 0) { f[nf++] = 8; x /= 8; }
+  while (x % 4 == 0) { f[nf++] = 4; x /= 4; }
+  while (x % 2 == 0) { f[nf++] = 2; x /= 2; }
+  while (x % 5 == 0) { f[nf++] = 5; x /= 5; }
+  while (x % 3 == 0) { f[nf++] = 3; x /= 3; }
+  p.nf = nf;
+  int Ns = 1, off = 0;
+  for (int i = 0; i < nf; ++i) {
+    p.st[i].r = f[i];
+    p.st[i].Rr = R / f[i];
+    p.st[i].Ns = Ns;
+    p.st[i].twoff = off;
+    p.st[i].magic = (Ns == 1) ? 0u : (unsigned)((0x100000000ULL + Ns - 1) / Ns);
+    off += Ns * (f[i] - 1);
+    Ns *= f[i];
+  }
+  return p;
+}
 
 struct C2RArgs {
   int mode;              // 0: first of two, 1: second of two, 2: single pass
@@ -258,12 +292,12 @@ __device__ __forceinline__ void issue_loads(const C2RArgs& a, const FftIO& io, i
 
 // Z[e] of this thread's sequence (pairing of the half spectrum); branch-free.
 template <int MODE>
-__device__ __forceinline__ double2 zval(const C2RArgs& a, const Smem& sp, const Slot& s, int sq, int e) {
-  double2 u = sp.ld[(e << a.lgn) + sq];
-  const int pe = (s.pmode == 0) ? a.R - e : a.R - 1 - e;   // pe == R only for pmode 0, e == 0
-  const double2* pp = (pe == a.R) ? sp.nyq + sq : sp.ld + (pe << a.lgn) + s.psq;
+__device__ __forceinline__ double2 zval(const Geo g, const Smem& sp, const Slot& s, int sq, int e) {
+  double2 u = sp.ld[(e << g.lgn) + sq];
+  const int pe = (s.pmode == 0) ? g.R - e : g.R - 1 - e;   // pe == R only for pmode 0, e == 0
+  const double2* pp = (pe == g.R) ? sp.nyq + sq : sp.ld + (pe << g.lgn) + s.psq;
   double2 v = *pp;
-  const double2 w = sp.ptw[(MODE == 0) ? s.sl * a.R + e : e];
+  const double2 w = sp.ptw[(MODE == 0) ? s.sl * g.R + e : e];
   double evr = u.x + v.x, evi = u.y - v.y;  // u_n + conj u_{M-n}
   double dr = u.x - v.x, di = u.y + v.y;    // u_n - conj u_{M-n}
   double odr = dr * w.x - di * w.y, odi = dr * w.y + di * w.x;
@@ -277,15 +311,15 @@ struct Epi {
 };
 
 template <int MODE>
-__device__ __forceinline__ void store_out(const C2RArgs& a, const FftIO& io, const Slot& s, const Epi& ep,
-                                          const double2* aux, int kk, double2 v, bool act) {
+__device__ __forceinline__ void store_out(const C2RArgs& a, const FftIO& io, const Geo g, const Slot& s,
+                                          const Epi& ep, const double2* aux, int kk, double2 v, bool act) {
   if (MODE == 0) {
-    const double2 w = aux[s.sl * a.R + kk];
+    const double2 w = aux[s.sl * g.R + kk];
     if (act) a.scr[(unsigned)(ep.base + kk * ep.kstep)] = c_mul(v, w);
   } else {
     const int k = (MODE == 1) ? s.sub + a.L1 * kk : kk;
     const int p = 2 * k;
-    const double2 ys = aux[(MODE == 1) ? s.sl * a.R + kk : kk];  // (yscale[p], yscale[p+1])
+    const double2 ys = aux[(MODE == 1) ? s.sl * g.R + kk : kk];  // (yscale[p], yscale[p+1])
     double* y = io.Y + (size_t)(unsigned)(ep.base + p * (int)io.ldy);
     const bool k0 = act && p >= io.keep_lo && p < io.keep_hi;
     const bool k1 = act && p + 1 >= io.keep_lo && p + 1 < io.keep_hi;
@@ -302,12 +336,13 @@ enum { OUT_WK = 0, OUT_G = 1 };
 // Out-of-range butterflies of the last round are computed on a clamped (valid) index and
 // their stores suppressed, so there is no divergent control flow inside the stage.
 template <int r, int IN, int OUT, int MODE, bool FIRST>
-__device__ __forceinline__ void stage(const C2RArgs& a, const FftIO& io, const Smem& sp, const double2* aux,
-                                      const Slot& s, const Epi& ep, int sq, int e0, int estep, const StageC& c) {
+__device__ __forceinline__ void stage(const C2RArgs& a, const FftIO& io, const Geo g, const Smem& sp,
+                                      const double2* aux, const Slot& s, const Epi& ep, int sq, int e0, int estep,
+                                      const StageC c) {
   const double2* ld = sp.ld;
   double2* wk = sp.wk;
   constexpr int MB = (TILE / NTH + r - 1) / r;  // butterflies per thread (R * nseq <= TILE)
-  const int lgn = a.lgn;
+  const int lgn = g.lgn;
   double2 v[MB][r];
   bool act[MB], wact[MB];
   int jj[MB];
@@ -321,7 +356,7 @@ __device__ __forceinline__ void stage(const C2RArgs& a, const FftIO& io, const S
     for (int t = 0; t < r; ++t) {
       const int e = jj[b] + t * c.Rr;
       if (!wact[b]) v[b][t] = make_double2(0.0, 0.0);
-      else if (IN == IN_Z) v[b][t] = zval<MODE>(a, sp, s, sq, e);
+      else if (IN == IN_Z) v[b][t] = zval<MODE>(g, sp, s, sq, e);
       else if (IN == IN_LD) v[b][t] = ld[(e << lgn) + sq];
       else v[b][t] = wk[(e << lgn) + sq];
     }
@@ -347,31 +382,51 @@ __device__ __forceinline__ void stage(const C2RArgs& a, const FftIO& io, const S
       if (OUT == OUT_WK) {
         if (act[b]) wk[((idxD + u * ustep) << lgn) + sq] = v[b][u];
       } else {
-        store_out<MODE>(a, io, s, ep, aux, idxD + u * ustep, v[b][u], gact);
+        store_out<MODE>(a, io, g, s, ep, aux, idxD + u * ustep, v[b][u], gact);
       }
     }
   }
 }
 
 template <int IN, int OUT, int MODE, bool FIRST>
-__device__ __forceinline__ void stage_r(const C2RArgs& a, const FftIO& io, const Smem& sp, const double2* aux,
-                                        const Slot& s, const Epi& ep, int sq, int e0, int estep, const StageC& c) {
+__device__ __forceinline__ void stage_r(const C2RArgs& a, const FftIO& io, const Geo g, const Smem& sp,
+                                        const double2* aux, const Slot& s, const Epi& ep, int sq, int e0, int estep,
+                                        const StageC& c) {
   switch (c.r) {
-    case 2: stage<2, IN, OUT, MODE, FIRST>(a, io, sp, aux, s, ep, sq, e0, estep, c); break;
-    case 3: stage<3, IN, OUT, MODE, FIRST>(a, io, sp, aux, s, ep, sq, e0, estep, c); break;
-    case 4: stage<4, IN, OUT, MODE, FIRST>(a, io, sp, aux, s, ep, sq, e0, estep, c); break;
-    case 5: stage<5, IN, OUT, MODE, FIRST>(a, io, sp, aux, s, ep, sq, e0, estep, c); break;
-    default: stage<8, IN, OUT, MODE, FIRST>(a, io, sp, aux, s, ep, sq, e0, estep, c); break;
+    case 2: stage<2, IN, OUT, MODE, FIRST>(a, io, g, sp, aux, s, ep, sq, e0, estep, c); break;
+    case 3: stage<3, IN, OUT, MODE, FIRST>(a, io, g, sp, aux, s, ep, sq, e0, estep, c); break;
+    case 4: stage<4, IN, OUT, MODE, FIRST>(a, io, g, sp, aux, s, ep, sq, e0, estep, c); break;
+    case 5: stage<5, IN, OUT, MODE, FIRST>(a, io, g, sp, aux, s, ep, sq, e0, estep, c); break;
+    default: stage<8, IN, OUT, MODE, FIRST>(a, io, g, sp, aux, s, ep, sq, e0, estep, c); break;
   }
 }
 
-template <int MODE>
+// Compile-time stage sequence (specialised kernels): stages ST .. NF-2 in place, then the last.
+template <int MODE, int RC, int ST>
+__device__ __forceinline__ void stages_ct(const C2RArgs& a, const FftIO& io, const Geo g, const Smem& sp,
+                                          const double2* aux, const Slot& s, const Epi& ep, int sq, int e0,
+                                          int estep) {
+  constexpr StagePlan P = stages_of(RC);
+  constexpr StageC c = P.st[ST];
+  if constexpr (ST + 1 < P.nf) {
+    stage<c.r, IN_WK, OUT_WK, MODE, false>(a, io, g, sp, aux, s, ep, sq, e0, estep, c);
+    __syncthreads();
+    stages_ct<MODE, RC, ST + 1>(a, io, g, sp, aux, s, ep, sq, e0, estep);
+  } else {
+    stage<c.r, IN_WK, OUT_G, MODE, false>(a, io, g, sp, aux, s, ep, sq, e0, estep, c);
+  }
+}
+
+// RC = 0: generic kernel (runtime length and radix plan); RC > 0: specialised for sub-length
+// RC with 2^LGNC sequences per tile.
+template <int MODE, int RC, int LGNC>
 __global__ void __launch_bounds__(NTH, 3) c2r_pass(const __grid_constant__ C2RArgs a, const __grid_constant__ FftIO io) {
   extern __shared__ double2 smem[];
   const Smem sp = smem_parts(a, smem);
+  const Geo g = RC ? Geo{RC, LGNC} : Geo{a.R, a.lgn};
   const int tid = threadIdx.x;
-  const int sq = tid & ((1 << a.lgn) - 1);
-  const int e0 = tid >> a.lgn, estep = NTH >> a.lgn;
+  const int sq = tid & ((1 << g.lgn) - 1);
+  const int e0 = tid >> g.lgn, estep = NTH >> g.lgn;
   constexpr int IN0 = (MODE == 1) ? IN_LD : IN_Z;
 
   // once per CTA: the stage twiddles (and, single pass, the whole pairing / scale tables)
@@ -397,20 +452,35 @@ __global__ void __launch_bounds__(NTH, 3) c2r_pass(const __grid_constant__ C2RAr
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();  // LD, nyq, slices complete for every thread; WK free (previous tile done)
     const bool more = tile + (int)gridDim.x < a.ntiles;
-    if (a.nf == 1) {
-      stage_r<IN0, OUT_G, MODE, true>(a, io, sp, aux, s, ep, sq, e0, estep, a.st[0]);
-      __syncthreads();
+    if constexpr (RC > 0) {
+      constexpr StagePlan P = stages_of(RC);
+      constexpr StageC c0 = P.st[0];
+      if constexpr (P.nf == 1) {
+        stage<c0.r, IN0, OUT_G, MODE, true>(a, io, g, sp, aux, s, ep, sq, e0, estep, c0);
+        __syncthreads();
+        if (more) issue_loads<MODE>(a, io, tile + gridDim.x, sp, abuf ^ 1, sq, e0, estep);
+      } else {
+        stage<c0.r, IN0, OUT_WK, MODE, true>(a, io, g, sp, aux, s, ep, sq, e0, estep, c0);
+        __syncthreads();  // LD and the pairing slice consumed, WK written
+        if (more) issue_loads<MODE>(a, io, tile + gridDim.x, sp, abuf ^ 1, sq, e0, estep);
+        stages_ct<MODE, RC, 1>(a, io, g, sp, aux, s, ep, sq, e0, estep);
+      }
+    } else {
+      if (a.nf == 1) {
+        stage_r<IN0, OUT_G, MODE, true>(a, io, g, sp, aux, s, ep, sq, e0, estep, a.st[0]);
+        __syncthreads();
+        if (more) issue_loads<MODE>(a, io, tile + gridDim.x, sp, abuf ^ 1, sq, e0, estep);
+        continue;
+      }
+      stage_r<IN0, OUT_WK, MODE, true>(a, io, g, sp, aux, s, ep, sq, e0, estep, a.st[0]);
+      __syncthreads();  // LD and the pairing slice consumed, WK written
       if (more) issue_loads<MODE>(a, io, tile + gridDim.x, sp, abuf ^ 1, sq, e0, estep);
-      continue;
+      for (int st = 1; st + 1 < a.nf; ++st) {
+        stage_r<IN_WK, OUT_WK, MODE, false>(a, io, g, sp, aux, s, ep, sq, e0, estep, a.st[st]);
+        __syncthreads();
+      }
+      stage_r<IN_WK, OUT_G, MODE, false>(a, io, g, sp, aux, s, ep, sq, e0, estep, a.st[a.nf - 1]);
     }
-    stage_r<IN0, OUT_WK, MODE, true>(a, io, sp, aux, s, ep, sq, e0, estep, a.st[0]);
-    __syncthreads();  // LD and the pairing slice consumed, WK written
-    if (more) issue_loads<MODE>(a, io, tile + gridDim.x, sp, abuf ^ 1, sq, e0, estep);
-    for (int st = 1; st + 1 < a.nf; ++st) {
-      stage_r<IN_WK, OUT_WK, MODE, false>(a, io, sp, aux, s, ep, sq, e0, estep, a.st[st]);
-      __syncthreads();
-    }
-    stage_r<IN_WK, OUT_G, MODE, false>(a, io, sp, aux, s, ep, sq, e0, estep, a.st[a.nf - 1]);
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
@@ -522,11 +592,32 @@ void choose(C2RArgs& a, int smin) {
   a.lgn = ilog2i(nseq);
 }
 
+typedef void (*C2RKernel)(C2RArgs, FftIO);
+
+// Specialised (mode, sub-length, log2 nseq) instances: the long passes of the configured
+// workloads (c5: 43200 = 200 x 216, 13824 = 64 x 216, 4500 = 45 x 100, 1458 = 27 x 54;
+// c3/c4: 10800 = 60 x 180, 5400 = 25 x 216, 3456 = 36 x 96, 1728 = 9 x 192).  Anything else
+// runs the generic kernel.
+struct Spec {
+  int mode, R, lgn;
+  C2RKernel k;
+};
+#define XC_SPEC(M, R, L) {M, R, L, (C2RKernel)c2r_pass<M, R, L>}
+const Spec kSpecs[] = {
+    XC_SPEC(0, 200, 3), XC_SPEC(1, 216, 3), XC_SPEC(0, 64, 5), XC_SPEC(0, 45, 5), XC_SPEC(1, 100, 4),
+    XC_SPEC(0, 27, 6),  XC_SPEC(1, 54, 5),  XC_SPEC(0, 60, 5), XC_SPEC(1, 180, 3), XC_SPEC(0, 25, 6),
+    XC_SPEC(0, 36, 5),  XC_SPEC(1, 96, 4),  XC_SPEC(0, 9, 7),  XC_SPEC(1, 192, 3),
+};
+#undef XC_SPEC
+
 template <int MODE>
 xc_status launch(C2RArgs& a, const FftIO& io, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    XC_CUDA(cudaFuncSetAttribute(c2r_pass<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    XC_CUDA(cudaFuncSetAttribute(c2r_pass<MODE, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    for (const Spec& sp : kSpecs)
+      if (sp.mode == MODE)
+        XC_CUDA(cudaFuncSetAttribute((const void*)sp.k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     int dev = 0;
     XC_CUDA(cudaGetDevice(&dev));
     XC_CUDA(cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -548,10 +639,14 @@ xc_status launch(C2RArgs& a, const FftIO& io, cudaStream_t st) {
     xc_set_error("c2r: tile does not fit shared memory");
     return XC_EUNSUPPORTED;
   }
+  C2RKernel k = (C2RKernel)c2r_pass<MODE, 0, 0>;
+  if (!getenv("XC_C2R_GENERIC"))
+    for (const Spec& sp : kSpecs)
+      if (sp.mode == MODE && sp.R == a.R && sp.lgn == a.lgn) k = sp.k;
   int per_sm = 0;
-  XC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c2r_pass<MODE>, NTH, sm));
+  XC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NTH, sm));
   const int grid = std::min(a.ntiles, std::max(1, per_sm) * std::max(1, g_nsm));
-  c2r_pass<MODE><<<grid, NTH, sm, st>>>(a, io);
+  k<<<grid, NTH, sm, st>>>(a, io);
   XC_CUDA(cudaGetLastError());
   return XC_OK;
 }
