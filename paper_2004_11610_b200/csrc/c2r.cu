@@ -159,6 +159,7 @@ struct C2RArgs {
   int ntx, ntiles;
   double2* scr;          // four-step scratch, row (k1 L2 + n2), ld = lds (offsets < 2^31)
   int lds;
+  int big;               // 1: 512-thread CTAs, tiles up to 2 TILE points
   int nstw;              // entries of the stage-twiddle table (staged in smem once per CTA)
   int naux;              // entries of one per-tile auxiliary slice (sc * R; MODE 2: R)
 };
@@ -251,7 +252,7 @@ __device__ __forceinline__ void cp16(double2* dst, const double2* src, bool v) {
 
 template <int MODE>
 __device__ __forceinline__ void issue_loads(const C2RArgs& a, const FftIO& io, int tile, const Smem& sp, int abuf,
-                                            int sq, int e0, int estep) {
+                                            int sq, int e0, int estep, int nth) {
   Slot s = slot_of<MODE>(a, tile, sq);
   const double2* g;
   int gstep;
@@ -275,7 +276,7 @@ __device__ __forceinline__ void issue_loads(const C2RArgs& a, const FftIO& io, i
   if (MODE != 2) {  // this tile's twiddle / scale slices
     const int gy = tile / a.ntx;
     double2* aux = sp.aux2 + abuf * a.naux;
-    for (int idx = threadIdx.x; idx < a.naux; idx += NTH) {
+    for (int idx = threadIdx.x; idx < a.naux; idx += nth) {
       const int sl = idx / a.R, e = idx - sl * a.R;
       const int sub = slot_sub<MODE>(a, gy, sl);
       const int su = sub < 0 ? 0 : sub;
@@ -419,25 +420,27 @@ __device__ __forceinline__ void stages_ct(const C2RArgs& a, const FftIO& io, con
 
 // RC = 0: generic kernel (runtime length and radix plan); RC > 0: specialised for sub-length
 // RC with 2^LGNC sequences per tile.
-template <int MODE, int RC, int LGNC>
-__global__ void __launch_bounds__(NTH, 3) c2r_pass(const __grid_constant__ C2RArgs a, const __grid_constant__ FftIO io) {
+template <int MODE, int RC, int LGNC, int BIG = 0>
+__global__ void __launch_bounds__(BIG ? 2 * NTH : NTH, BIG ? 1 : 3)
+    c2r_pass(const __grid_constant__ C2RArgs a, const __grid_constant__ FftIO io) {
+  constexpr int NT = BIG ? 2 * NTH : NTH;  // BIG: 512 threads, tiles up to 2 TILE (one CTA per SM)
   extern __shared__ double2 smem[];
   const Smem sp = smem_parts(a, smem);
   const Geo g = RC ? Geo{RC, LGNC} : Geo{a.R, a.lgn};
   const int tid = threadIdx.x;
   const int sq = tid & ((1 << g.lgn) - 1);
-  const int e0 = tid >> g.lgn, estep = NTH >> g.lgn;
+  const int e0 = tid >> g.lgn, estep = NT >> g.lgn;
   constexpr int IN0 = (MODE == 1) ? IN_LD : IN_Z;
 
   // once per CTA: the stage twiddles (and, single pass, the whole pairing / scale tables)
-  for (int i = tid; i < a.nstw; i += NTH) cp16(sp.stw + i, a.stw + i, true);
+  for (int i = tid; i < a.nstw; i += NT) cp16(sp.stw + i, a.stw + i, true);
   if (MODE == 2)
-    for (int i = tid; i < a.naux; i += NTH) {
+    for (int i = tid; i < a.naux; i += NT) {
       cp16(sp.ptw + i, a.ptw + i, true);
       cp16(sp.aux2 + i, reinterpret_cast<const double2*>(io.yscale) + i, true);
     }
   int tile = blockIdx.x, abuf = 0;
-  if (tile < a.ntiles) issue_loads<MODE>(a, io, tile, sp, abuf, sq, e0, estep);
+  if (tile < a.ntiles) issue_loads<MODE>(a, io, tile, sp, abuf, sq, e0, estep, NT);
   for (; tile < a.ntiles; tile += gridDim.x, abuf ^= 1) {
     const Slot s = slot_of<MODE>(a, tile, sq);
     const double2* aux = (MODE == 2) ? sp.aux2 : sp.aux2 + abuf * a.naux;
@@ -458,23 +461,23 @@ __global__ void __launch_bounds__(NTH, 3) c2r_pass(const __grid_constant__ C2RAr
       if constexpr (P.nf == 1) {
         stage<c0.r, IN0, OUT_G, MODE, true>(a, io, g, sp, aux, s, ep, sq, e0, estep, c0);
         __syncthreads();
-        if (more) issue_loads<MODE>(a, io, tile + gridDim.x, sp, abuf ^ 1, sq, e0, estep);
+        if (more) issue_loads<MODE>(a, io, tile + gridDim.x, sp, abuf ^ 1, sq, e0, estep, NT);
       } else {
         stage<c0.r, IN0, OUT_WK, MODE, true>(a, io, g, sp, aux, s, ep, sq, e0, estep, c0);
         __syncthreads();  // LD and the pairing slice consumed, WK written
-        if (more) issue_loads<MODE>(a, io, tile + gridDim.x, sp, abuf ^ 1, sq, e0, estep);
+        if (more) issue_loads<MODE>(a, io, tile + gridDim.x, sp, abuf ^ 1, sq, e0, estep, NT);
         stages_ct<MODE, RC, 1>(a, io, g, sp, aux, s, ep, sq, e0, estep);
       }
     } else {
       if (a.nf == 1) {
         stage_r<IN0, OUT_G, MODE, true>(a, io, g, sp, aux, s, ep, sq, e0, estep, a.st[0]);
         __syncthreads();
-        if (more) issue_loads<MODE>(a, io, tile + gridDim.x, sp, abuf ^ 1, sq, e0, estep);
+        if (more) issue_loads<MODE>(a, io, tile + gridDim.x, sp, abuf ^ 1, sq, e0, estep, NT);
         continue;
       }
       stage_r<IN0, OUT_WK, MODE, true>(a, io, g, sp, aux, s, ep, sq, e0, estep, a.st[0]);
       __syncthreads();  // LD and the pairing slice consumed, WK written
-      if (more) issue_loads<MODE>(a, io, tile + gridDim.x, sp, abuf ^ 1, sq, e0, estep);
+      if (more) issue_loads<MODE>(a, io, tile + gridDim.x, sp, abuf ^ 1, sq, e0, estep, NT);
       for (int st = 1; st + 1 < a.nf; ++st) {
         stage_r<IN_WK, OUT_WK, MODE, false>(a, io, g, sp, aux, s, ep, sq, e0, estep, a.st[st]);
         __syncthreads();
@@ -582,8 +585,9 @@ xc_status tables_for(const FftPlan& p, const C2RTables** out) {
 
 // nseq = cb * sc (powers of two) with R * nseq <= TILE; columns first (cb <= 16), sc >= smin.
 void choose(C2RArgs& a, int smin) {
+  const int tile = a.big ? 2 * TILE : TILE, nth = a.big ? 2 * NTH : NTH;
   int nseq = 1;
-  while (2 * nseq * a.R <= TILE && nseq < NTH && nseq < smin * a.S * std::max(1, a.ncol)) nseq *= 2;
+  while (2 * nseq * a.R <= tile && nseq < nth && nseq < smin * a.S * std::max(1, a.ncol)) nseq *= 2;
   int cb = 1;
   while (cb < a.ncol && cb < 16 && 2 * cb * smin <= nseq) cb *= 2;
   a.cb = cb;
@@ -599,16 +603,27 @@ typedef void (*C2RKernel)(C2RArgs, FftIO);
 // c3/c4: 10800 = 60 x 180, 5400 = 25 x 216, 3456 = 36 x 96, 1728 = 9 x 192).  Anything else
 // runs the generic kernel.
 struct Spec {
-  int mode, R, lgn;
+  int mode, R, lgn, big;
   C2RKernel k;
 };
-#define XC_SPEC(M, R, L) {M, R, L, (C2RKernel)c2r_pass<M, R, L>}
+#define XC_SPEC(M, R, L) {M, R, L, 0, (C2RKernel)c2r_pass<M, R, L>}
+#define XC_BIG(M, R, L) {M, R, L, 1, (C2RKernel)c2r_pass<M, R, L, 1>}
+// BIG (512 threads, 64 KB tiles, 1 CTA / SM): the longest passes, so that a tile row is >= 128 B
 const Spec kSpecs[] = {
+    XC_BIG(0, 200, 4),
     XC_SPEC(0, 200, 3), XC_SPEC(1, 216, 3), XC_SPEC(0, 64, 5), XC_SPEC(0, 45, 5), XC_SPEC(1, 100, 4),
     XC_SPEC(0, 27, 6),  XC_SPEC(1, 54, 5),  XC_SPEC(0, 60, 5), XC_SPEC(1, 180, 3), XC_SPEC(0, 25, 6),
     XC_SPEC(0, 36, 5),  XC_SPEC(1, 96, 4),  XC_SPEC(0, 9, 7),  XC_SPEC(1, 192, 3),
 };
 #undef XC_SPEC
+#undef XC_BIG
+
+bool has_big(int mode, int R) {
+  if (getenv("XC_C2R_GENERIC") || getenv("XC_C2R_NOBIG")) return false;
+  for (const Spec& sp : kSpecs)
+    if (sp.mode == mode && sp.R == R && sp.big) return true;
+  return false;
+}
 
 template <int MODE>
 xc_status launch(C2RArgs& a, const FftIO& io, cudaStream_t st) {
@@ -640,13 +655,21 @@ xc_status launch(C2RArgs& a, const FftIO& io, cudaStream_t st) {
     return XC_EUNSUPPORTED;
   }
   C2RKernel k = (C2RKernel)c2r_pass<MODE, 0, 0>;
+  int nt = NTH;
   if (!getenv("XC_C2R_GENERIC"))
     for (const Spec& sp : kSpecs)
-      if (sp.mode == MODE && sp.R == a.R && sp.lgn == a.lgn) k = sp.k;
+      if (sp.mode == MODE && sp.R == a.R && sp.lgn == a.lgn && sp.big == a.big) {
+        k = sp.k;
+        nt = sp.big ? 2 * NTH : NTH;
+      }
+  if (a.big && nt == NTH) {
+    xc_set_error("c2r: big tile without a big kernel");
+    return XC_EUNSUPPORTED;
+  }
   int per_sm = 0;
-  XC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NTH, sm));
+  XC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, nt, sm));
   const int grid = std::min(a.ntiles, std::max(1, per_sm) * std::max(1, g_nsm));
-  k<<<grid, NTH, sm, st>>>(a, io);
+  k<<<grid, nt, sm, st>>>(a, io);
   XC_CUDA(cudaGetLastError());
   return XC_OK;
 }
@@ -702,8 +725,9 @@ xc_status c2r_run(const FftPlan& p, const FftIO& io, int ncol, double2* scratch,
   a.P = (a.S & 1) ? (a.S + 1) / 2 : a.S / 2;
   set_radices(a, p.nf1, p.f1);
   a.stw = (const double2*)tb->stw0.p;
+  a.big = has_big(0, a.R) && ncol >= 64;
   choose(a, 2);
-  if (a.sc < 2 || a.R * (1 << a.lgn) > TILE) {
+  if (a.sc < 2 || a.R * (1 << a.lgn) > (a.big ? 2 : 1) * TILE) {
     xc_set_error("c2r: first-pass length too long");
     return XC_EUNSUPPORTED;
   }
@@ -714,8 +738,9 @@ xc_status c2r_run(const FftPlan& p, const FftIO& io, int ncol, double2* scratch,
   a.S = p.L1;
   set_radices(a, p.nf2, p.f2);
   a.stw = (const double2*)tb->stw1.p;
+  a.big = has_big(1, a.R) && ncol >= 64;
   choose(a, 1);
-  if (a.R * (1 << a.lgn) > TILE) {
+  if (a.R * (1 << a.lgn) > (a.big ? 2 : 1) * TILE) {
     xc_set_error("c2r: second-pass length too long");
     return XC_EUNSUPPORTED;
   }
