@@ -30,7 +30,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-constexpr int WARPS = 8;  // warps per CTA
+constexpr int WARPS = XC_WARPS;  // warps per CTA
 
 // One CTA = one window of B rows [r0, r1) (<= XC_WMAX) x one tile of 8*NT right-hand sides.
 // The window's rows are staged once in shared memory; the window's items (all families whose
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
   // B-fragment column n of DMMA nt: 16 (nt/2) + 2n + (nt&1) within the tile (NT >= 2), n (NT == 1)
   const int bcol = (NT == 1) ? g : 2 * g;
 
-  for (int ii = W.i0 + warp; ii < W.i1; ii += WARPS) {
+  for (int ii = W.i0 + W.wo[warp]; ii < W.i0 + W.wo[warp + 1]; ++ii) {
     const SpmmItem it = items[ii];
     double acc[2][NT][2];
 #pragma unroll
@@ -113,9 +113,11 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
     if (n > 0) lds_b(0, b0);
     if (it.out_row[1] >= 0) {
       // two M-tiles sharing the B fragments
+      // A fragments streamed four steps ahead
       const double2* ap = reinterpret_cast<const double2*>(tiles + it.a_off) + lane;
-      double2 a0 = n > 0 ? __ldg(ap) : make_double2(0.0, 0.0);
-      double2 a1 = n > 1 ? __ldg(ap + 32) : make_double2(0.0, 0.0);
+      const double2 z2 = make_double2(0.0, 0.0);
+      double2 a0 = n > 0 ? __ldg(ap) : z2, a1 = n > 1 ? __ldg(ap + 32) : z2;
+      double2 a2 = n > 2 ? __ldg(ap + 64) : z2, a3 = n > 3 ? __ldg(ap + 96) : z2;
       for (int s = 0; s < n; s += 2) {
         if (s + 1 < n) lds_b(s + 1, b1);
 #pragma unroll
@@ -123,7 +125,8 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
           dmma(acc[0][i][0], acc[0][i][1], a0.x, b0[i]);
           dmma(acc[1][i][0], acc[1][i][1], a0.y, b0[i]);
         }
-        a0 = (s + 2 < n) ? __ldg(ap + 32 * (s + 2)) : make_double2(0.0, 0.0);
+        a0 = a2;
+        a2 = (s + 4 < n) ? __ldg(ap + 32 * (s + 4)) : z2;
         if (s + 1 < n) {
           if (s + 2 < n) lds_b(s + 2, b0);
 #pragma unroll
@@ -131,7 +134,8 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
             dmma(acc[0][i][0], acc[0][i][1], a1.x, b1[i]);
             dmma(acc[1][i][0], acc[1][i][1], a1.y, b1[i]);
           }
-          a1 = (s + 3 < n) ? __ldg(ap + 32 * (s + 3)) : make_double2(0.0, 0.0);
+          a1 = a3;
+          a3 = (s + 5 < n) ? __ldg(ap + 32 * (s + 5)) : z2;
         }
       }
     } else {

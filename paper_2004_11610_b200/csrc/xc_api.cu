@@ -431,6 +431,34 @@ xc_status upload_and_fill(xc_op* h, ItemSet& S, bool input_axis, DevBuf& d_items
       ++j;
     }
     w.i1 = (int)j;
+    // balance the window's items over the CTA's warps: longest first onto the least-loaded
+    // warp (cost ~ M-tile steps + a fixed per-item overhead); each warp's items contiguous
+    {
+      const int n = w.i1 - w.i0;
+      std::vector<int> ord(n);
+      for (int q = 0; q < n; ++q) ord[q] = q;
+      auto cost = [&](int q) {
+        const SpmmItem& it = sorted[w.i0 + q];
+        return (int64_t)it.nsteps * (it.out_row[1] >= 0 ? 2 : 1) + 6;
+      };
+      std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return cost(x) > cost(y); });
+      std::vector<int64_t> load(XC_WARPS, 0);
+      std::vector<std::vector<int>> per(XC_WARPS);
+      for (int q : ord) {
+        int best = 0;
+        for (int k = 1; k < XC_WARPS; ++k)
+          if (load[k] < load[best]) best = k;
+        load[best] += cost(q);
+        per[best].push_back(q);
+      }
+      std::vector<SpmmItem> tmp;
+      w.wo[0] = 0;
+      for (int k = 0; k < XC_WARPS; ++k) {
+        for (int q : per[k]) tmp.push_back(sorted[w.i0 + q]);
+        w.wo[k + 1] = (int)tmp.size();
+      }
+      std::copy(tmp.begin(), tmp.end(), sorted.begin() + w.i0);
+    }
     wins.push_back(w);
     i = j;
   }

@@ -169,11 +169,13 @@ struct SpmmItem {
 
 // A window of B rows [r0, r1) (r1 - r0 <= XC_WMAX) and the items [i0, i1) inside it.
 #define XC_WMAX 192
+#define XC_WARPS 8  // warps per SpMM CTA
 struct SpmmWin {
   int r0, r1;
   int i0, i1;
   int src;
   int pad;
+  int wo[XC_WARPS + 1];  // items [i0 + wo[w], i0 + wo[w+1]) run on warp w (balanced on the host)
 };
 
 #define XC_MAX_SRC 40
