@@ -45,7 +45,11 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
   constexpr int CWP = CW + 4;  // padded smem row: the 4 rows of a B fragment fall in distinct banks
   extern __shared__ double2 xs2[];
   const double* xs = reinterpret_cast<const double*>(xs2);
-  const SpmmWin W = wins[blockIdx.y];
+  SpmmWin W;  // scalar fields only (the per-warp offsets are read where needed)
+  W.r0 = wins[blockIdx.y].r0;
+  W.r1 = wins[blockIdx.y].r1;
+  W.i0 = wins[blockIdx.y].i0;
+  W.src = wins[blockIdx.y].src;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = lane & 3, g = lane >> 2;
   const int tile0 = blockIdx.x * CW;
@@ -85,7 +89,8 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
   // B-fragment column n of DMMA nt: 16 (nt/2) + 2n + (nt&1) within the tile (NT >= 2), n (NT == 1)
   const int bcol = (NT == 1) ? g : 2 * g;
 
-  for (int ii = W.i0 + W.wo[warp]; ii < W.i0 + W.wo[warp + 1]; ++ii) {
+  const int iw0 = W.i0 + __ldg(&wins[blockIdx.y].wo[warp]), iw1 = W.i0 + __ldg(&wins[blockIdx.y].wo[warp + 1]);
+  for (int ii = iw0; ii < iw1; ++ii) {
     const SpmmItem it = items[ii];
     double acc[2][NT][2];
 #pragma unroll
