@@ -137,6 +137,12 @@ xc_status xc_build_step(xc_handle h, xc_exchange_t* ex);
 xc_status xc_apply(xc_handle h, xc_dir dir, const double* X, int64_t ldx, double* Y, int64_t ldy,
                    int64_t B, void* stream);
 
+/* CUDA graphs of xc_apply (default on): the second call with the same (X, Y, ldx, ldy, B,
+ * dir, stream) captures the apply's launches into a graph, later calls replay it with one
+ * launch.  Not used while profiling, on the legacy default stream, or when the caller is itself
+ * capturing.  Graphs are dropped when the workspace grows.  enable = 0 turns them off. */
+xc_status xc_set_graphs(xc_handle h, int enable);
+
 /* Same as xc_apply with HOST buffers X_host, Y_host (row-major N x B, ld = B):
  * copies X to the device, applies, copies Y back, and synchronises `stream`.
  * The batch is processed in column chunks (about B/16 columns, a multiple of 64) through a

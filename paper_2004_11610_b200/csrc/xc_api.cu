@@ -105,6 +105,19 @@ struct xc_op {
   // workspace
   int64_t ws_B = 0;
   DevBuf partA, partW, scratch, zpl, Xh, Yh;
+  // CUDA graphs of xc_apply, keyed on its arguments: a key seen twice is captured once and
+  // replayed from then on (one launch instead of ~20; matters for the small configs)
+  struct GraphEntry {
+    const void* X;
+    void* Y;
+    int64_t ldx, ldy, B;
+    int dir;
+    cudaStream_t st;
+    int seen;
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> graphs;
+  bool use_graphs = true;
   // xc_apply_host pipeline: copy-in / copy-out streams and per-slot events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_cmp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
@@ -136,6 +149,12 @@ int64_t pad_cols(int64_t B) {
   return (B + t - 1) / t * t;
 }
 
+void clear_graphs(xc_op* h) {
+  for (auto& g : h->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  h->graphs.clear();
+}
+
 xc_status ensure_ws(xc_op* h, int64_t B) {
   if (B <= h->ws_B) return XC_OK;
   int64_t Bp = pad_cols(B);
@@ -157,6 +176,7 @@ xc_status ensure_ws(xc_op* h, int64_t B) {
     XC_TRY(dev_alloc(h->zpl, (size_t)tot * sizeof(double)));
   }
   h->ws_B = B;
+  clear_graphs(h);  // captured graphs reference the old workspace
   return XC_OK;
 }
 
@@ -886,6 +906,7 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
 }
 
 void destroy_impl(xc_op* h) {
+  clear_graphs(h);
   for (auto& e : h->ev) cudaEventDestroy(e);
   h->ev.clear();
   if (h->s_in) {
@@ -1093,7 +1114,49 @@ xc_status xc_apply(xc_handle h, xc_dir dir, const double* X, int64_t ldx, double
     return XC_EINVAL;
   }
   XC_CUDA(cudaSetDevice(h->device));
-  return apply_impl(h, dir, X, ldx, Y, ldy, B, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!h->use_graphs || h->prof || h->xstage != 0) return apply_impl(h, dir, X, ldx, Y, ldy, B, st);
+  xc_op::GraphEntry* e = nullptr;
+  for (auto& g : h->graphs)
+    if (g.X == X && g.Y == Y && g.ldx == ldx && g.ldy == ldy && g.B == B && g.dir == dir && g.st == st) e = &g;
+  if (e && e->exec) {
+    XC_CUDA(cudaGraphLaunch(e->exec, st));
+    return XC_OK;
+  }
+  if (!e) {  // first call with these arguments: run directly (lazy tables, workspace, attributes)
+    XC_TRY(apply_impl(h, dir, X, ldx, Y, ldy, B, st));
+    if (h->graphs.size() >= 16) clear_graphs(h);
+    h->graphs.push_back(xc_op::GraphEntry{X, Y, ldx, ldy, B, (int)dir, st, 1, nullptr});
+    return XC_OK;
+  }
+  // second call: capture the apply once, then replay it
+  cudaStreamCaptureStatus cs;
+  XC_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs != cudaStreamCaptureStatusNone || st == nullptr)  // caller is capturing, or legacy stream
+    return apply_impl(h, dir, X, ldx, Y, ldy, B, st);
+  cudaGraph_t graph = nullptr;
+  XC_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  xc_status s = apply_impl(h, dir, X, ldx, Y, ldy, B, st);
+  cudaError_t ce = cudaStreamEndCapture(st, &graph);
+  if (s != XC_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return s;
+  }
+  XC_CUDA(ce);
+  cudaGraphExec_t exec = nullptr;
+  ce = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  XC_CUDA(ce);
+  e->exec = exec;
+  XC_CUDA(cudaGraphLaunch(exec, st));
+  return XC_OK;
+}
+
+xc_status xc_set_graphs(xc_handle h, int enable) {
+  if (!h) return XC_EINVAL;
+  h->use_graphs = enable != 0;
+  if (!enable) clear_graphs(h);
+  return XC_OK;
 }
 
 // Host buffers: the batch is cut into column chunks that flow through a 3-stage pipeline

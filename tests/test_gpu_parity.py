@@ -332,3 +332,54 @@ def test_distributed_build_via_process_group():
     T.close()
     Td.close()
     dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ab", [(-0.5, -0.5), (0.0, 0.0), (0.5, -0.3), (1.5, 0.25), (-0.7, 2.0)])
+def test_jacobi_sweep_round_trip(ab):
+    """NEXT-4 (the paper's Fig.test2 experiment): for several (alpha, beta), one operator
+    built for both directions; forward Y = A X and backward C = diag(w) A^T Y agree with the
+    oracle's compressed applies (1e-12) and backward(forward(X)) = X (Gauss exactness,
+    A diag(w) A^T = I) within 10 eps."""
+    xc = _xc()
+    kt = (O.KIND_JACOBI, ab[0], ab[1])
+    N, B, eps = 1536, 24, 1e-12
+    x, _ = _nodes(kt, N, 0)
+    _, w, _ = O.gauss_rule(O.Kind(*kt), N)
+    C = I.rhs(N, B, 31)
+    T = xc.Transform(kt[0], x, eps, alpha=ab[0], beta=ab[1], dirs=xc.XC_DIR_A | xc.XC_DIR_WAT, weights=w)
+    Xf = T.apply(_gpu(C), xc.XC_DIR_WAT)             # values at the nodes of the expansion C
+    Cb = T.apply(Xf, xc.XC_DIR_A).cpu().numpy()       # back to coefficients
+    op = O.compress(O.make_plan(O.Kind(*kt), N, eps), x)
+    Xo = O.apply_input_axis(op, C, w)
+    assert O.rel_l2_cols(Xf.cpu().numpy(), Xo).max() <= 1e-12
+    assert O.rel_l2_cols(Cb, O.apply_output_axis(op, Xf.cpu().numpy())).max() <= 1e-12
+    assert O.rel_l2_cols(Cb, C).max() <= 10 * eps
+    T.close()
+
+
+def test_graph_replay_identical():
+    """xc_set_graphs: the 1st call runs, the 2nd captures, later calls replay -- all bit-identical to
+    the uncaptured apply; a larger batch (workspace growth) drops and rebuilds the graphs."""
+    xc = _xc()
+    kt = (O.KIND_JACOBI, 0.0, 0.0)
+    N, eps = 512, 1e-12
+    x, _ = _nodes(kt, N, 0)
+    T = xc.Transform(xc.XC_JACOBI, x, eps)
+    s = torch.cuda.Stream()
+    for B in (8, 96):
+        X = _gpu(I.rhs(N, B, B))
+        T.graphs(False)
+        with torch.cuda.stream(s):
+            ref = T.apply(X).clone()
+        T.graphs(True)
+        Y = torch.empty_like(X)
+        outs = []
+        with torch.cuda.stream(s):
+            for _ in range(4):
+                Y.zero_()
+                T.apply(X, out=Y)
+                outs.append(Y.clone())
+        torch.cuda.synchronize()
+        for o in outs:
+            assert torch.equal(o, ref)
+    T.close()
