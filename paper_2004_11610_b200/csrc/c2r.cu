@@ -97,12 +97,55 @@ __device__ __forceinline__ void bf5(double2* v) {
   v[2] = make_double2(m2.x - t2.y, m2.y + t2.x);
   v[3] = make_double2(m2.x + t2.y, m2.y - t2.x);
 }
+// 6 = 2 x 3: DFT3 of the even and odd points, odd ones times e^{+i pi k/3}, then radix 2.
+__device__ __forceinline__ void bf6(double2* v) {
+  const double C = 0.5, SN = 0.86602540378443864676;
+  double2 a[3] = {v[0], v[2], v[4]}, b[3] = {v[1], v[3], v[5]};
+  bf3(a);
+  bf3(b);
+  b[1] = make_double2(C * b[1].x - SN * b[1].y, C * b[1].y + SN * b[1].x);     // e^{i pi/3}
+  b[2] = make_double2(-C * b[2].x - SN * b[2].y, -C * b[2].y + SN * b[2].x);   // e^{2 i pi/3}
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    v[k] = c_add(a[k], b[k]);
+    v[k + 3] = c_sub(a[k], b[k]);
+  }
+}
+// 9 = 3 x 3: inner DFT3 over m (x[j + 3m]), twiddle e^{+2 pi i j k1 / 9}, outer DFT3 over j,
+// output k1 + 3 k2.
+__device__ __forceinline__ void bf9(double2* v) {
+  const double C1 = 0.76604444311897803520, S1 = 0.64278760968653932632;   // 40 deg
+  const double C2 = 0.17364817766693034885, S2 = 0.98480775301220805936;   // 80 deg
+  const double C4 = -0.93969262078590838405, S4 = 0.34202014332566873304;  // 160 deg
+  double2 A[3][3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    A[j][0] = v[j];
+    A[j][1] = v[j + 3];
+    A[j][2] = v[j + 6];
+    bf3(A[j]);
+  }
+  A[1][1] = c_mul(A[1][1], make_double2(C1, S1));
+  A[1][2] = c_mul(A[1][2], make_double2(C2, S2));
+  A[2][1] = c_mul(A[2][1], make_double2(C2, S2));
+  A[2][2] = c_mul(A[2][2], make_double2(C4, S4));
+#pragma unroll
+  for (int k1 = 0; k1 < 3; ++k1) {
+    double2 t[3] = {A[0][k1], A[1][k1], A[2][k1]};
+    bf3(t);
+    v[k1] = t[0];
+    v[k1 + 3] = t[1];
+    v[k1 + 6] = t[2];
+  }
+}
 template <int r>
 __device__ __forceinline__ void bfly(double2* v) {
   if (r == 2) bf2(v);
   else if (r == 3) bf3(v);
   else if (r == 4) bf4(v[0], v[1], v[2], v[3]);
   else if (r == 5) bf5(v);
+  else if (r == 6) bf6(v);
+  else if (r == 9) bf9(v);
   else bf8(v);
 }
 
@@ -118,29 +161,24 @@ struct Geo {
   int R, lgn;
 };
 
-// The radix plan of a length (factorize() order: 8s, 4, 2, 5s, 3s) as compile-time data.
+// The radix plan of a length (c2r_radices) with spans, twiddle offsets and magic numbers.
 struct StagePlan {
   int nf;
-  StageC st[12];
+  StageC st[16];
 };
 constexpr StagePlan stages_of(int R) {
   StagePlan p{};
-  int f[12] = {}, nf = 0, x = R;
-  while (x % 8 == 0) { f[nf++] = 8; x /= 8; }
-  while (x % 4 == 0) { f[nf++] = 4; x /= 4; }
-  while (x % 2 == 0) { f[nf++] = 2; x /= 2; }
-  while (x % 5 == 0) { f[nf++] = 5; x /= 5; }
-  while (x % 3 == 0) { f[nf++] = 3; x /= 3; }
-  p.nf = nf;
+  const C2RRadices rp = c2r_radices(R);
+  p.nf = rp.nf;
   int Ns = 1, off = 0;
-  for (int i = 0; i < nf; ++i) {
-    p.st[i].r = f[i];
-    p.st[i].Rr = R / f[i];
+  for (int i = 0; i < rp.nf; ++i) {
+    p.st[i].r = rp.f[i];
+    p.st[i].Rr = R / rp.f[i];
     p.st[i].Ns = Ns;
     p.st[i].twoff = off;
     p.st[i].magic = (Ns == 1) ? 0u : (unsigned)((0x100000000ULL + Ns - 1) / Ns);
-    off += Ns * (f[i] - 1);
-    Ns *= f[i];
+    off += Ns * (rp.f[i] - 1);
+    Ns *= rp.f[i];
   }
   return p;
 }
@@ -148,7 +186,7 @@ constexpr StagePlan stages_of(int R) {
 struct C2RArgs {
   int mode;              // 0: first of two, 1: second of two, 2: single pass
   int R, nf;             // sub-transform length and its radix stages
-  StageC st[12];
+  StageC st[16];
   const double2* stw;    // per-stage twiddle tables (exact, long double on the host)
   const double2* ptw;    // pairing twiddle e^{i pi n / M}: pass 0 at [n2 L1 + e] (n = L2 e + n2), else [e]
   const double2* ftw;    // pass 0 four-step twiddle e^{2 pi i n2 k1 / M} at [n2 L1 + k1]
@@ -398,6 +436,8 @@ __device__ __forceinline__ void stage_r(const C2RArgs& a, const FftIO& io, const
     case 3: stage<3, IN, OUT, MODE, FIRST>(a, io, g, sp, aux, s, ep, sq, e0, estep, c); break;
     case 4: stage<4, IN, OUT, MODE, FIRST>(a, io, g, sp, aux, s, ep, sq, e0, estep, c); break;
     case 5: stage<5, IN, OUT, MODE, FIRST>(a, io, g, sp, aux, s, ep, sq, e0, estep, c); break;
+    case 6: stage<6, IN, OUT, MODE, FIRST>(a, io, g, sp, aux, s, ep, sq, e0, estep, c); break;
+    case 9: stage<9, IN, OUT, MODE, FIRST>(a, io, g, sp, aux, s, ep, sq, e0, estep, c); break;
     default: stage<8, IN, OUT, MODE, FIRST>(a, io, g, sp, aux, s, ep, sq, e0, estep, c); break;
   }
 }
@@ -496,18 +536,13 @@ int ilog2i(int v) {
 
 int g_nsm = 0;
 
-void set_radices(C2RArgs& a, int nf, const int* f) {
-  a.nf = nf;
-  int Ns = 1, off = 0;
-  for (int i = 0; i < nf; ++i) {
-    StageC& c = a.st[i];
-    c.r = f[i];
-    c.Rr = a.R / f[i];
-    c.Ns = Ns;
-    c.twoff = off;
-    c.magic = (Ns == 1) ? 0u : (unsigned)((0x100000000ULL + Ns - 1) / Ns);
-    off += Ns * (f[i] - 1);
-    Ns *= f[i];
+void set_radices(C2RArgs& a) {
+  const StagePlan P = stages_of(a.R);
+  a.nf = P.nf;
+  int off = 0;
+  for (int i = 0; i < P.nf; ++i) {
+    a.st[i] = P.st[i];
+    off = P.st[i].twoff + P.st[i].Ns * (P.st[i].r - 1);
   }
   a.nstw = std::max(off, 1);
 }
@@ -521,14 +556,12 @@ double2 cis(int64_t m, int64_t n) {
   return make_double2((double)cosl(ang), (double)sinl(ang));
 }
 
-void stage_table(int R, int nf, const int* f, std::vector<double2>& t) {
+void stage_table(int R, std::vector<double2>& t) {
   t.clear();
-  int Ns = 1;
-  for (int i = 0; i < nf; ++i) {
-    for (int k = 0; k < Ns; ++k)
-      for (int q = 1; q < f[i]; ++q) t.push_back(cis((int64_t)k * q, (int64_t)Ns * f[i]));
-    Ns *= f[i];
-  }
+  const StagePlan P = stages_of(R);
+  for (int i = 0; i < P.nf; ++i)
+    for (int k = 0; k < P.st[i].Ns; ++k)
+      for (int q = 1; q < P.st[i].r; ++q) t.push_back(cis((int64_t)k * q, (int64_t)P.st[i].Ns * P.st[i].r));
   if (t.empty()) t.push_back(make_double2(1.0, 0.0));
 }
 
@@ -562,10 +595,10 @@ xc_status tables_for(const FftPlan& p, const C2RTables** out) {
   t->L1 = p.L1;
   t->L2 = p.L2;
   std::vector<double2> v;
-  stage_table(p.L1, p.nf1, p.f1, v);
+  stage_table(p.L1, v);
   XC_TRY(put(t->stw0, v));
   if (p.L2 > 1) {
-    stage_table(p.L2, p.nf2, p.f2, v);
+    stage_table(p.L2, v);
     XC_TRY(put(t->stw1, v));
   }
   const int64_t M = p.L, L1 = p.L1, L2 = p.L2;
@@ -611,12 +644,22 @@ struct Spec {
 // BIG (512 threads, 64 KB tiles, 1 CTA / SM): the longest passes, so that a tile row is >= 128 B
 const Spec kSpecs[] = {
     XC_BIG(0, 200, 4),
-    XC_SPEC(0, 200, 3), XC_SPEC(1, 216, 3), XC_SPEC(0, 64, 5), XC_SPEC(0, 45, 5), XC_SPEC(1, 100, 4),
-    XC_SPEC(0, 27, 6),  XC_SPEC(1, 54, 5),  XC_SPEC(0, 60, 5), XC_SPEC(1, 180, 3), XC_SPEC(0, 25, 6),
-    XC_SPEC(0, 36, 5),  XC_SPEC(1, 96, 4),  XC_SPEC(0, 9, 7),  XC_SPEC(1, 192, 3),
+    XC_SPEC(1, 216, 3), XC_SPEC(0, 54, 5),  XC_SPEC(1, 256, 3), XC_SPEC(0, 45, 5), XC_SPEC(1, 100, 4),
+    XC_SPEC(0, 27, 6),  XC_SPEC(1, 54, 5),  XC_SPEC(1, 240, 3), XC_SPEC(1, 64, 5), XC_SPEC(0, 32, 6),
+    XC_SPEC(0, 36, 5),  XC_SPEC(0, 9, 7),
 };
 #undef XC_SPEC
 #undef XC_BIG
+
+}  // namespace
+
+bool c2r_has_big(int mode, int R) {
+  for (const Spec& sp : kSpecs)
+    if (sp.mode == mode && sp.R == R && sp.big) return true;
+  return false;
+}
+
+namespace {
 
 bool has_big(int mode, int R) {
   if (getenv("XC_C2R_GENERIC") || getenv("XC_C2R_NOBIG")) return false;
@@ -700,7 +743,7 @@ xc_status c2r_run(const FftPlan& p, const FftIO& io, int ncol, double2* scratch,
     a.mode = 2;
     a.R = p.L1;
     a.S = 1;
-    set_radices(a, p.nf1, p.f1);
+    set_radices(a);
     a.stw = (const double2*)tb->stw0.p;
     // one sequence per column: every slot is a column
     int nseq = 1;
@@ -723,7 +766,7 @@ xc_status c2r_run(const FftPlan& p, const FftIO& io, int ncol, double2* scratch,
   a.R = p.L1;
   a.S = p.L2;
   a.P = (a.S & 1) ? (a.S + 1) / 2 : a.S / 2;
-  set_radices(a, p.nf1, p.f1);
+  set_radices(a);
   a.stw = (const double2*)tb->stw0.p;
   a.big = has_big(0, a.R) && ncol >= 64;
   choose(a, 2);
@@ -736,7 +779,7 @@ xc_status c2r_run(const FftPlan& p, const FftIO& io, int ncol, double2* scratch,
   a.mode = 1;
   a.R = p.L2;
   a.S = p.L1;
-  set_radices(a, p.nf2, p.f2);
+  set_radices(a);
   a.stw = (const double2*)tb->stw1.p;
   a.big = has_big(1, a.R) && ncol >= 64;
   choose(a, 1);

@@ -407,28 +407,33 @@ void set_stages(PassArgs& a, int nf, const int* f) {
 
 }  // namespace
 
-// Warp-rounds per element of the C2R pass engine (c2r.cu: 256 threads, tiles of R * nseq <= 2048
-// points, nseq a power of two with at least smin sub-sequences, rounds without an active lane
-// skipped per warp) for a sub-transform of length R: the cost model of the four-step split.
-double c2r_pass_cost(int R, int smin) {
-  int f[12], nf;
-  factorize(R, nf, f);
-  if (nf < 0) return 1e30;
+// Cost model of one C2R pass (c2r.cu) per element: warp-rounds of its radix stages (256 threads,
+// tiles of R * nseq <= 2048 points -- 512 / 4096 for the big-tile kernels --, nseq a power of two
+// with at least smin sub-sequences, rounds without an active lane skipped per warp) times the
+// measured throughput penalty of its tile-row width (cb columns x 16 B: 64 B rows ran at 2.35,
+// 128 B at 3.75, 256 B at 5.8 TB/s on c5).
+double c2r_pass_cost(int R, int smin, int mode) {
+  const C2RRadices pl = c2r_radices(R);
+  if (pl.nf < 0) return 1e30;
+  const bool big = c2r_has_big(mode, R);
+  const int tile = big ? 4096 : 2048, nth = big ? 512 : 256;
   int nseq = 1;
-  while (2 * nseq * R <= 2048 && nseq < 256) nseq *= 2;
+  while (2 * nseq * R <= tile && nseq < nth) nseq *= 2;
   if (nseq < smin) return 1e30;
-  int lgn = ilog2(nseq);
-  const int estep = 256 >> lgn;
+  const int cb = std::min(16, nseq / smin);
+  const double pen = cb >= 16 ? 1.0 : cb >= 8 ? 1.55 : cb >= 4 ? 2.5 : cb >= 2 ? 4.0 : 6.0;
+  const int lgn = ilog2(nseq);
+  const int estep = nth >> lgn;
   double warps = 0;
-  for (int i = 0; i < nf; ++i) {
-    const int r = f[i], Rr = R / r, MB = (8 + r - 1) / r;
+  for (int i = 0; i < pl.nf; ++i) {
+    const int r = pl.f[i], Rr = R / r, MB = (8 + r - 1) / r;
     for (int b = 0; b < MB; ++b)
-      for (int w = 0; w < 8; ++w) {
+      for (int w = 0; w < nth / 32; ++w) {
         const int e0min = (32 * w) >> lgn;
         if (e0min + b * estep < Rr) warps += 1;
       }
   }
-  return warps * 32.0 / ((double)R * nseq);
+  return warps * 32.0 / ((double)R * nseq) * pen;
 }
 
 xc_status fft_plan_make(FftPlan& p, int L, bool c2r) {
@@ -442,7 +447,7 @@ xc_status fft_plan_make(FftPlan& p, int L, bool c2r) {
       double bc = 1e30;
       for (int d = 2; d <= 256; ++d) {
         if (L % d || L / d > 256) continue;
-        const double c = c2r_pass_cost(d, 2) + c2r_pass_cost(L / d, 1);
+        const double c = c2r_pass_cost(d, 2, 0) + c2r_pass_cost(L / d, 1, 1);
         if (c < bc - 1e-9) {
           bc = c;
           best = d;

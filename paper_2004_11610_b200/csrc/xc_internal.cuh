@@ -144,7 +144,27 @@ struct FftIO {
   double scale = 1.0;                                      // EPI_PLAIN / EPI_ZPLANES
 };
 
-xc_status fft_plan_make(FftPlan& p, int L, bool c2r = false);  // c2r: split chosen for c2r_run
+xc_status fft_plan_make(FftPlan& p, int L, bool c2r = false);
+
+// Radix plan of a C2R sub-transform (c2r.cu, and its cost model in fft.cu): 8s, then 9s, then 6s
+// (a 2 with a 3), then 4, 2, 5s, 3s -- few stages (every stage is a shared-memory round trip).
+struct C2RRadices {
+  int nf;
+  int f[16];
+};
+constexpr C2RRadices c2r_radices(int R) {
+  C2RRadices p{};
+  int x = R;
+  while (x % 8 == 0) { p.f[p.nf++] = 8; x /= 8; }
+  while (x % 9 == 0) { p.f[p.nf++] = 9; x /= 9; }
+  while (x % 6 == 0) { p.f[p.nf++] = 6; x /= 6; }
+  while (x % 4 == 0) { p.f[p.nf++] = 4; x /= 4; }
+  while (x % 2 == 0) { p.f[p.nf++] = 2; x /= 2; }
+  while (x % 5 == 0) { p.f[p.nf++] = 5; x /= 5; }
+  while (x % 3 == 0) { p.f[p.nf++] = 3; x /= 3; }
+  if (x != 1) p.nf = -1;
+  return p;
+}  // c2r: split chosen for c2r_run
 void fft_plan_free(FftPlan& p);
 // sigma = -1 forward (Eq. 1), +1 inverse.  ncol columns.  scratch: L*ncol double2 (2-pass only).
 xc_status fft_run(const FftPlan& p, int sigma, FftPro pro, FftEpi epi, const FftIO& io, int ncol,
@@ -152,6 +172,8 @@ xc_status fft_run(const FftPlan& p, int sigma, FftPro pro, FftEpi epi, const Fft
 // Output-axis real-output inverse (c2r.cu): persistent prefetching passes, half spectrum
 // io.Uc (ldu) -> Y rows (io.Y, ldy) with the W^{-1}/truncate epilogue.  scratch: M*ncol double2.
 xc_status c2r_run(const FftPlan& p, const FftIO& io, int ncol, double2* scratch, cudaStream_t st);
+// 1 if c2r.cu has a 512-thread big-tile kernel for this pass (mode 0 first / 1 second) and length
+bool c2r_has_big(int mode, int R);
 
 // ---------------------------------------------------------------------------
 // SpMM on the FP64 tensor cores (spmm.cu)
