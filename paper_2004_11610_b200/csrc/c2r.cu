@@ -359,7 +359,8 @@ __device__ __forceinline__ void store_out(const C2RArgs& a, const FftIO& io, con
     const int k = (MODE == 1) ? s.sub + a.L1 * kk : kk;
     const int p = 2 * k;
     const double2 ys = aux[(MODE == 1) ? s.sl * g.R + kk : kk];  // (yscale[p], yscale[p+1])
-    double* y = io.Y + (size_t)(unsigned)(ep.base + p * (int)io.ldy);
+    // signed: with m_off < 0 (trigonometric kind) rows below keep_lo give negative offsets (not stored)
+    double* y = io.Y + (ptrdiff_t)(ep.base + p * (int)io.ldy);
     const bool k0 = act && p >= io.keep_lo && p < io.keep_hi;
     const bool k1 = act && p + 1 >= io.keep_lo && p + 1 < io.keep_hi;
     const double y0 = v.x * ys.x, y1 = v.y * ys.y;

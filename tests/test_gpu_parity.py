@@ -383,3 +383,41 @@ def test_graph_replay_identical():
         for o in outs:
             assert torch.equal(o, ref)
     T.close()
+
+
+@pytest.mark.parametrize("kt,N,B", [((O.KIND_JACOBI, 0.0, 0.0), 2, 1), ((O.KIND_JACOBI, 0.5, -0.3), 3, 2),
+                                    ((O.KIND_JACOBI, 0.0, 0.0), 16, 5), ((O.KIND_LAGUERRE, 0.0, 0.0), 40, 3),
+                                    ((O.KIND_COS, 0.0, 0.0), 33, 7), ((O.KIND_JACOBI, -0.5, -0.5), 100, 65)])
+def test_degenerate_sizes(kt, N, B):
+    """Degenerate cases: N so small that the chain is empty (dense tail only) or has one block;
+    B = 1 and B one past a column tile.  Both directions against the oracle and the dense product."""
+    xc = _xc()
+    eps = 1e-12 if kt[0] != O.KIND_COS else 1e-10
+    x, w = _nodes(kt, N, 5)
+    if w is None:
+        w = np.ones(N)
+    X = I.rhs(N, B, 6)
+    T = xc.Transform(kt[0], x, eps, alpha=kt[1], beta=kt[2], dirs=xc.XC_DIR_A | xc.XC_DIR_WAT, weights=w)
+    op = O.compress(O.make_plan(O.Kind(*kt), N, eps), x)
+    Y = T.apply(_gpu(X)).cpu().numpy()
+    assert O.rel_l2_cols(Y, O.apply_output_axis(op, X)).max() <= 1e-12
+    assert O.rel_l2_cols(Y, O.dense_apply(O.Kind(*kt), x, X)).max() <= 10 * eps
+    Yw = T.apply(_gpu(X), xc.XC_DIR_WAT).cpu().numpy()
+    assert O.rel_l2_cols(Yw, O.apply_input_axis(op, X, w)).max() <= 1e-12
+    T.close()
+
+
+def test_empty_and_bad_batches():
+    """B = 0 and mismatched shapes are rejected (XC_EINVAL), never silently accepted."""
+    import ctypes
+    xc = _xc()
+    x, _ = _nodes((O.KIND_JACOBI, 0.0, 0.0), 64, 0)
+    T = xc.Transform(xc.XC_JACOBI, x, 1e-12)
+    X = _gpu(np.ones((64, 4)))
+    Y = torch.empty_like(X)
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for B, ldx, ldy in ((0, 4, 4), (4, 3, 4), (4, 4, 3)):
+        rc = T._lib.xc_apply(T._h, xc.XC_DIR_A, ctypes.c_void_p(X.data_ptr()), ldx, ctypes.c_void_p(Y.data_ptr()),
+                             ldy, B, st)
+        assert xc._STATUS[rc] == "XC_EINVAL"
+    T.close()
