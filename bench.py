@@ -263,6 +263,15 @@ def main():
     alg_bytes = 16.0 * N * B + 20.0 * nnz + 8.0 * tail * N   # X in, Y out, operator once (SURVEY d.3)
     peaks = _peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    # DRAM traffic of the SpMM launch from the committed ncu --set full capture (same workload)
+    traffic, traffic_src = None, None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r01_spmm_traffic.json")))
+        if tr.get("workload") == cfg.name and tr.get("B_per_gpu") == B and direction == xc.XC_DIR_A:
+            traffic = float(tr["dram_bytes_read_per_launch"] + tr["dram_bytes_write_per_launch"])
+            traffic_src = tr["source"]
+    except Exception:
+        traffic = None
 
     # ---- end to end: host buffers through xc_apply_host (copies inside the call) ----
     e2e = None
@@ -310,7 +319,8 @@ def main():
             "fp64_tflops": info["flops_per_col_A"] * B / (ms / 1e3) / 1e12,
             "roofline": {"bound": "tensor", "kernel": "spmm_dmma (mma.m8n8k4.f64)", "achieved": achieved,
                          "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / DMMA_PEAK_TFLOPS,
-                         "traffic": None, "peak_source": "measured DMMA microbenchmark (tools/fp64_peak.cu)",
+                         "traffic": traffic, "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
+                         "peak_source": "measured DMMA microbenchmark (tools/fp64_peak.cu)",
                          "spmm_ms": spmm_ms, "fft_ms": fft_ms, "spmm_share": spmm_ms / ms,
                          "dmma_issue_efficiency": (4.0 * nnz + 2.0 * tail * N) / max(1.0, info["dmma_flops_per_col_A"])},
             "cpu_baseline": cpu,
