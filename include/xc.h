@@ -152,6 +152,14 @@ xc_status xc_set_graphs(xc_handle h, int enable);
 xc_status xc_apply_host(xc_handle h, xc_dir dir, const double* X_host, double* Y_host, int64_t B,
                         void* stream);
 
+/* Streaming form of xc_apply_host: enqueues the same pipeline and returns without waiting; the
+ * pipeline state carries over, so back-to-back calls overlap (a call's first copy in runs under
+ * the previous call's last copy out).  X_host must stay unchanged and Y_host unread until
+ * xc_host_wait(h) (which waits for every enqueued call).  Errors as xc_apply_host. */
+xc_status xc_apply_host_async(xc_handle h, xc_dir dir, const double* X_host, double* Y_host, int64_t B,
+                              void* stream);
+xc_status xc_host_wait(xc_handle h);
+
 /* Reserve workspace for up to B right-hand sides (may allocate). */
 xc_status xc_reserve(xc_handle h, int64_t B);
 

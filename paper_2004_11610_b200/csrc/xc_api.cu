@@ -120,8 +120,12 @@ struct xc_op {
   bool use_graphs = true;
   // xc_apply_host pipeline: copy-in / copy-out streams and per-slot events
   cudaStream_t s_in = nullptr, s_out = nullptr;
-  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_cmp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  static constexpr int kSlots = 3;  // device slots of the host-buffer pipeline
+  cudaEvent_t ev_in[kSlots] = {}, ev_cmp[kSlots] = {}, ev_out[kSlots] = {};
   cudaEvent_t ev_start = nullptr;
+  cudaStream_t hst = nullptr;  // apply stream of the last host-buffer call (valid if hst_set)
+  bool hst_set = false;
+  int64_t hchunk = 0;          // chunks enqueued since the slots were (re)allocated
   std::vector<int64_t> zoff;  // per block offset (doubles) of its z' planes in zpl
   xc_info_t info{};
   // build state (kept between the phases of a distributed precompute)
@@ -914,7 +918,7 @@ void destroy_impl(xc_op* h) {
     cudaStreamSynchronize(h->s_out);
     cudaStreamDestroy(h->s_in);
     cudaStreamDestroy(h->s_out);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < xc_op::kSlots; ++i) {
       cudaEventDestroy(h->ev_in[i]);
       cudaEventDestroy(h->ev_cmp[i]);
       cudaEventDestroy(h->ev_out[i]);
@@ -1162,19 +1166,18 @@ xc_status xc_set_graphs(xc_handle h, int enable) {
 // Host buffers: the batch is cut into column chunks that flow through a 3-stage pipeline
 // (H2D on s_in, the apply on `stream`, D2H on s_out; two device slots), so the PCIe
 // copies in both directions overlap each other and the apply.
-xc_status xc_apply_host(xc_handle h, xc_dir dir, const double* Xh, double* Yh, int64_t B, void* stream) {
-  if (!h || !Xh || !Yh || B < 1) {
-    xc_set_error("apply_host: bad arguments");
-    return XC_EINVAL;
-  }
-  XC_CUDA(cudaSetDevice(h->device));
-  cudaStream_t st = (cudaStream_t)stream;
+namespace {
+
+// Enqueue one host-buffer apply on the pipeline (no host synchronisation).  Chunk slots and
+// their events carry over between calls, so consecutive calls overlap (the next call's first
+// copy in runs under this call's last copy out).
+xc_status host_enqueue(xc_op* h, xc_dir dir, const double* Xh, double* Yh, int64_t B, cudaStream_t st) {
   if (!h->s_in) {
     int lo = 0, hi = 0;
     XC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     XC_CUDA(cudaStreamCreateWithPriority(&h->s_in, cudaStreamNonBlocking, hi));
     XC_CUDA(cudaStreamCreateWithPriority(&h->s_out, cudaStreamNonBlocking, hi));
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < xc_op::kSlots; ++i) {
       XC_CUDA(cudaEventCreateWithFlags(&h->ev_in[i], cudaEventDisableTiming));
       XC_CUDA(cudaEventCreateWithFlags(&h->ev_cmp[i], cudaEventDisableTiming));
       XC_CUDA(cudaEventCreateWithFlags(&h->ev_out[i], cudaEventDisableTiming));
@@ -1182,32 +1185,46 @@ xc_status xc_apply_host(xc_handle h, xc_dir dir, const double* Xh, double* Yh, i
     XC_CUDA(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming));
   }
   const int64_t N = h->N;
-  // chunk: ~B/16 columns, a multiple of 64 (the SpMM column tile), at least 64
-  int64_t nparts = 8;
+  // chunk: a multiple of 64 columns (the SpMM column tile), at least 64
+  int64_t nparts = 12;  // ~B/12 columns per chunk: the measured optimum at c5 (2D DMA efficiency vs pipeline fill)
   if (const char* e = getenv("XC_HOST_CHUNKS")) nparts = std::max(1, atoi(e));
   int64_t Bc = std::min<int64_t>(B, std::max<int64_t>(64, ((B + nparts - 1) / nparts + 63) / 64 * 64));
   const int64_t nchunk = (B + Bc - 1) / Bc;
   const size_t slot = (size_t)N * Bc * sizeof(double);
-  if (h->Xh.bytes < 2 * slot) {
-    XC_TRY(dev_alloc(h->Xh, 2 * slot));
-    XC_TRY(dev_alloc(h->Yh, 2 * slot));
+  const int NS = xc_op::kSlots;
+  if (h->Xh.bytes < NS * slot || Bc > h->ws_B) {  // (re)allocation: drain the pipeline first
+    XC_CUDA(cudaStreamSynchronize(h->s_in));
+    XC_CUDA(cudaStreamSynchronize(h->s_out));
+    if (h->hst_set) XC_CUDA(cudaStreamSynchronize(h->hst));
+    h->hchunk = 0;
+    if (h->Xh.bytes < NS * slot) {
+      XC_TRY(dev_alloc(h->Xh, NS * slot));
+      XC_TRY(dev_alloc(h->Yh, NS * slot));
+    }
+    XC_TRY(ensure_ws(h, Bc));
   }
-  XC_TRY(ensure_ws(h, Bc));
+  if (h->hst_set && h->hst != st) {  // the previous calls' apply stream must be done with the slots
+    XC_CUDA(cudaEventRecord(h->ev_start, h->hst));
+    XC_CUDA(cudaStreamWaitEvent(st, h->ev_start, 0));
+  }
+  h->hst = st;
+  h->hst_set = true;
   // the copy streams start after the work already queued on `stream`
   XC_CUDA(cudaEventRecord(h->ev_start, st));
   XC_CUDA(cudaStreamWaitEvent(h->s_in, h->ev_start, 0));
   XC_CUDA(cudaStreamWaitEvent(h->s_out, h->ev_start, 0));
-  for (int64_t c = 0; c < nchunk; ++c) {
-    const int i = (int)(c & 1);
+  for (int64_t c = 0; c < nchunk; ++c, ++h->hchunk) {
+    const int i = (int)(h->hchunk % NS);
+    const bool reused = h->hchunk >= NS;
     const int64_t c0 = c * Bc, bc = std::min(Bc, B - c0);
     double* xs = (double*)h->Xh.p + (size_t)i * N * Bc;
     double* ys = (double*)h->Yh.p + (size_t)i * N * Bc;
-    if (c >= 2) XC_CUDA(cudaStreamWaitEvent(h->s_in, h->ev_cmp[i], 0));  // slot's X consumed
+    if (reused) XC_CUDA(cudaStreamWaitEvent(h->s_in, h->ev_cmp[i], 0));  // slot's X consumed
     XC_CUDA(cudaMemcpy2DAsync(xs, bc * sizeof(double), Xh + c0, B * sizeof(double), bc * sizeof(double), N,
                               cudaMemcpyHostToDevice, h->s_in));
     XC_CUDA(cudaEventRecord(h->ev_in[i], h->s_in));
     XC_CUDA(cudaStreamWaitEvent(st, h->ev_in[i], 0));
-    if (c >= 2) XC_CUDA(cudaStreamWaitEvent(st, h->ev_out[i], 0));     // slot's Y copied out
+    if (reused) XC_CUDA(cudaStreamWaitEvent(st, h->ev_out[i], 0));     // slot's Y copied out
     XC_TRY(apply_impl(h, dir, xs, bc, ys, bc, bc, st));
     XC_CUDA(cudaEventRecord(h->ev_cmp[i], st));
     XC_CUDA(cudaStreamWaitEvent(h->s_out, h->ev_cmp[i], 0));
@@ -1215,9 +1232,44 @@ xc_status xc_apply_host(xc_handle h, xc_dir dir, const double* Xh, double* Yh, i
                               cudaMemcpyDeviceToHost, h->s_out));
     XC_CUDA(cudaEventRecord(h->ev_out[i], h->s_out));
   }
-  XC_CUDA(cudaStreamSynchronize(h->s_out));
-  XC_CUDA(cudaStreamSynchronize(st));
   return XC_OK;
+}
+
+xc_status host_sync(xc_op* h) {
+  if (h->s_out) XC_CUDA(cudaStreamSynchronize(h->s_out));
+  if (h->s_in) XC_CUDA(cudaStreamSynchronize(h->s_in));
+  if (h->hst_set) XC_CUDA(cudaStreamSynchronize(h->hst));
+  return XC_OK;
+}
+
+}  // namespace
+
+// Host buffers: the batch is cut into column chunks that flow through a 3-stage pipeline
+// (H2D on s_in, the apply on `stream`, D2H on s_out; two device slots), so the PCIe
+// copies in both directions overlap each other and the apply.
+xc_status xc_apply_host(xc_handle h, xc_dir dir, const double* Xh, double* Yh, int64_t B, void* stream) {
+  if (!h || !Xh || !Yh || B < 1) {
+    xc_set_error("apply_host: bad arguments");
+    return XC_EINVAL;
+  }
+  XC_CUDA(cudaSetDevice(h->device));
+  XC_TRY(host_enqueue(h, dir, Xh, Yh, B, (cudaStream_t)stream));
+  return host_sync(h);
+}
+
+xc_status xc_apply_host_async(xc_handle h, xc_dir dir, const double* Xh, double* Yh, int64_t B, void* stream) {
+  if (!h || !Xh || !Yh || B < 1) {
+    xc_set_error("apply_host_async: bad arguments");
+    return XC_EINVAL;
+  }
+  XC_CUDA(cudaSetDevice(h->device));
+  return host_enqueue(h, dir, Xh, Yh, B, (cudaStream_t)stream);
+}
+
+xc_status xc_host_wait(xc_handle h) {
+  if (!h) return XC_EINVAL;
+  XC_CUDA(cudaSetDevice(h->device));
+  return host_sync(h);
 }
 
 xc_status xc_reserve(xc_handle h, int64_t B) {

@@ -48,7 +48,7 @@ class XcBlockInfo(ctypes.Structure):
                 ("keep_hi", ctypes.c_int), ("nnz", _i64), ("max_band", ctypes.c_int)]
 
 
-EXPORTS = ["xc_params_default", "xc_build_compressed", "xc_build_local", "xc_build_step", "xc_apply", "xc_set_graphs", "xc_apply_host", "xc_reserve",
+EXPORTS = ["xc_params_default", "xc_build_compressed", "xc_build_local", "xc_build_step", "xc_apply", "xc_set_graphs", "xc_apply_host", "xc_apply_host_async", "xc_host_wait", "xc_reserve",
            "xc_workspace_query", "xc_info", "xc_block_info", "xc_block_window", "xc_node_spectrum",
            "xc_gauss_rule", "xc_plan_chain", "xc_profile_enable", "xc_profile_read", "xc_destroy",
            "xc_last_error", "xc_version"]
@@ -78,6 +78,8 @@ def load():
     lib.xc_apply.argtypes = [vp, ctypes.c_int, vp, _i64, vp, _i64, _i64, vp]
     lib.xc_apply_host.argtypes = [vp, ctypes.c_int, vp, vp, _i64, vp]
     lib.xc_set_graphs.argtypes = [vp, ctypes.c_int]
+    lib.xc_apply_host_async.argtypes = [vp, ctypes.c_int, vp, vp, _i64, vp]
+    lib.xc_host_wait.argtypes = [vp]
     lib.xc_reserve.argtypes = [vp, _i64]
     lib.xc_workspace_query.argtypes = [vp, _i64, ctypes.POINTER(ctypes.c_size_t)]
     lib.xc_info.argtypes = [vp, ctypes.POINTER(XcInfo)]
@@ -242,6 +244,14 @@ class Transform:
     def graphs(self, enable: bool = True):
         """CUDA-graph replay of repeated applies with the same arguments (default on)."""
         _check(self._lib.xc_set_graphs(self._h, 1 if enable else 0))
+
+    def apply_host_async_ptr(self, x_ptr: int, y_ptr: int, B: int, direction: int = XC_DIR_A, stream=None):
+        """Streaming host-buffer apply (no wait); see host_wait()."""
+        _check(self._lib.xc_apply_host_async(self._h, direction, ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr), B,
+                                             ctypes.c_void_p(stream or 0)))
+
+    def host_wait(self):
+        _check(self._lib.xc_host_wait(self._h))
 
     def profile(self, enable: bool = True):
         _check(self._lib.xc_profile_enable(self._h, 1 if enable else 0))

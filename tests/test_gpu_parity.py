@@ -421,3 +421,22 @@ def test_empty_and_bad_batches():
                              ldy, B, st)
         assert xc._STATUS[rc] == "XC_EINVAL"
     T.close()
+
+
+def test_host_async_stream_matches():
+    """xc_apply_host_async: back-to-back streaming calls on distinct pinned buffers give the same
+    bits as the device apply (the pipeline state carries over between calls)."""
+    xc = _xc()
+    kt = (O.KIND_JACOBI, 0.5, -0.3)
+    N, B = 1024, 200
+    x, _ = _nodes(kt, N, 2)
+    T = xc.Transform(kt[0], x, 1e-12, alpha=0.5, beta=-0.3)
+    Xs = [torch.from_numpy(I.rhs(N, B, 40 + i)).pin_memory() for i in range(3)]
+    Ys = [torch.empty_like(Xs[0]).pin_memory() for _ in range(3)]
+    st = torch.cuda.current_stream().cuda_stream
+    for Xp, Yp in zip(Xs, Ys):
+        T.apply_host_async_ptr(Xp.data_ptr(), Yp.data_ptr(), B, stream=st)
+    T.host_wait()
+    for Xp, Yp in zip(Xs, Ys):
+        assert torch.equal(Yp, T.apply(Xp.cuda()).cpu())
+    T.close()
