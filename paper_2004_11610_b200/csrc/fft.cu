@@ -11,9 +11,10 @@
 // butterflies in registers; twiddles come from exact tables (long double on the
 // host), raised to the r-th power by complex multiplication.
 //
-// The prologue/epilogue of the first/last pass are fused with the method's
-// pre/post-processing (P:163-180 Fe2 truncate + W^{-1}, P:137-156 Fe1 pad + W^{-1}),
-// see FftPro / FftEpi in xc_internal.cuh.
+// The prologue of the first pass can fuse the input-axis pre-processing (P:137-156 Fe1 pad +
+// W^{-1}; PRO_XREAL) and the epilogue of the last the z' planes layout (EPI_ZPLANES), see
+// FftPro / FftEpi in xc_internal.cuh.  Serves the precompute (forward, Eq. 1) and the input
+// axis; the output-axis real-output inverse has its own engine (c2r.cu).
 #include <math.h>
 
 #include <algorithm>
@@ -145,9 +146,8 @@ struct PassArgs {
   int L, L1, L2;
   int stage;         // 0 = first of two, 1 = second of two, 2 = single
   int S;             // number of sub-sequences per column
-  int ncol, cb, sc;  // cb, sc powers of two (sc = 2 for the paired C2R first pass)
+  int ncol, cb, sc;  // cb, sc powers of two
   int lgcb, lgn;     // log2(cb), log2(cb * sc)
-  int pairs;         // 1: slots are the sub-sequence pair {p, (S - p) % S}, p = blockIdx.y
   double2* scratch;  // two-pass intermediate, index (k1*L2 + n2)*ncol + col
 };
 
@@ -155,8 +155,6 @@ template <int PRO>
 __device__ __forceinline__ double2 pro_load(const FftIO& io, int n, int col) {
   if (PRO == PRO_PLAIN) {
     return io.src[(int64_t)n * io.lds + col];
-  } else if (PRO == PRO_C2R) {
-    return io.Uc[(int64_t)n * io.ldu + col];   // raw half-spectrum bin, paired later in smem
   } else {  // PRO_XREAL: pad + W^{-1} (Fe1 / Fe3)
     if (n >= io.keep_lo && n < io.keep_hi)
       return make_double2(io.X[(int64_t)(n + io.m_off) * io.ldx + col] * io.winv[n], 0.0);
@@ -168,13 +166,7 @@ template <int EPI>
 __device__ __forceinline__ void epi_store(const FftIO& io, int k, int col, double2 v) {
   if (EPI == EPI_PLAIN) {
     if (k < io.kmax) io.dst[(int64_t)k * io.ldd + col] = c_scale(v, io.scale);
-  } else if (EPI == EPI_C2R) {
-    // Fe2 discard + W^{-1} (Alg. 2 step 2.1-2.2): positions 2k and 2k+1
-    int p = 2 * k;
-    if (p >= io.keep_lo && p < io.keep_hi) io.Y[(int64_t)(p + io.m_off) * io.ldy + col] = v.x * io.yscale[p];
-    if (p + 1 >= io.keep_lo && p + 1 < io.keep_hi)
-      io.Y[(int64_t)(p + 1 + io.m_off) * io.ldy + col] = v.y * io.yscale[p + 1];
-  } else {
+  } else {  // EPI_ZPLANES
     if (k < io.H) {
       io.zre[(int64_t)k * io.ldz + col] = v.x * io.scale;
       io.zim[(int64_t)k * io.ldz + col] = v.y * io.scale;
@@ -188,23 +180,14 @@ __global__ void __launch_bounds__(256, 3) fft_pass(PassArgs a, FftIO io) {
   const int nseq = 1 << a.lgn;
   double2* bin = smem;
   double2* bout = smem + a.R * nseq;
-  double2* nyq = smem + 2 * a.R * nseq;  // C2R: U[M] per column (cb values)
   const int tid = threadIdx.x, nth = blockDim.x;
   // per-thread constants (nth is a multiple of nseq): sequence sq, its slot, sub-sequence and column
   const int sq = tid & (nseq - 1);
   const int e0 = tid >> a.lgn, estep = nth >> a.lgn;
   const int slot = sq >> a.lgcb, cl = sq & (a.cb - 1);
-  const int p = blockIdx.y;  // pair index (pairs) or first sub-sequence / sc
-  int sub;
-  if (a.pairs) {
-    sub = p;
-    if (slot) sub = (p == 0) ? 0 : a.S - p;
-  } else {
-    sub = p * a.sc + slot;
-  }
+  const int sub = blockIdx.y * a.sc + slot;
   const int col = blockIdx.x * a.cb + cl;
   const bool valid = sub < a.S && col < a.ncol;
-  const bool dup = a.pairs && slot == 1 && sub == p;  // self-paired sub-sequence: store once
 
   // ---- load (prologue) ----
   if (PRO == PRO_XREAL && a.stage != 1) {
@@ -231,10 +214,9 @@ __global__ void __launch_bounds__(256, 3) fft_pass(PassArgs a, FftIO io) {
       g = a.scratch + ((int64_t)sub * a.L2) * a.ncol + col;
       gstep = a.ncol;
     } else {
-      const int64_t ld = (PRO == PRO_C2R) ? io.ldu : io.lds;
       const int nstride = (a.stage == 0) ? a.L2 : 1;
-      g = ((PRO == PRO_C2R) ? io.Uc : io.src) + (int64_t)sub * ld + col;
-      gstep = (int64_t)nstride * ld;
+      g = io.src + (int64_t)sub * io.lds + col;
+      gstep = (int64_t)nstride * io.lds;
     }
     for (int e = e0; e < a.R; e += estep) {
       unsigned sa = (unsigned)__cvta_generic_to_shared(bin + (e << a.lgn) + sq);
@@ -244,34 +226,6 @@ __global__ void __launch_bounds__(256, 3) fft_pass(PassArgs a, FftIO io) {
     asm volatile("cp.async.wait_all;\n" ::: "memory");
   } else {
     for (int e = e0; e < a.R; e += estep) bin[(e << a.lgn) + sq] = make_double2(0.0, 0.0);
-  }
-  if (PRO == PRO_C2R && a.stage != 1) {
-    if (p == 0)
-      for (int c = tid; c < a.cb; c += nth)
-        nyq[c] = (blockIdx.x * a.cb + c < a.ncol) ? io.Uc[(int64_t)io.M * io.ldu + blockIdx.x * a.cb + c]
-                                                  : make_double2(0.0, 0.0);
-    __syncthreads();
-    // Real-output inverse DFT of length L = 2M from the half spectrum U[0..M]:
-    // Z[n] = (U[n] + conj U[M-n]) + i e^{2 pi i n/L} (U[n] - conj U[M-n]); then z = IDFT_M(Z)
-    // gives v[2k] = Re z[k], v[2k+1] = Im z[k].  U[M-n] lives in the paired slot of this CTA.
-    const int nstride = (a.stage == 0) ? a.L2 : 1;
-    const int osq = ((slot ^ 1) << a.lgcb) + cl;
-    for (int e = e0; e < a.R; e += estep) {
-      int n = nstride * e + sub;
-      double2 u = bin[(e << a.lgn) + sq], v;
-      if (sub == 0)
-        v = (e == 0) ? nyq[cl] : bin[((a.R - e) << a.lgn) + sq];
-      else
-        v = bin[((a.R - 1 - e) << a.lgn) + osq];
-      double2 w = __ldg(io.twh + n);
-      double evr = u.x + v.x, evi = u.y - v.y;  // U[n] + conj U[M-n]
-      double dr = u.x - v.x, di = u.y + v.y;    // U[n] - conj U[M-n]
-      double odr = dr * w.x - di * w.y, odi = dr * w.y + di * w.x;
-      bout[(e << a.lgn) + sq] = make_double2(evr - odi, evi + odr);
-    }
-    double2* t = bin;
-    bin = bout;
-    bout = t;
   }
   __syncthreads();
 
@@ -295,7 +249,7 @@ __global__ void __launch_bounds__(256, 3) fft_pass(PassArgs a, FftIO io) {
   }
 
   // ---- store (epilogue) ----
-  if (!valid || dup) return;
+  if (!valid) return;
   if (a.stage == 0) {
     // four-step twiddle w_L^{sigma n2 k1}, n2 = sub, k1 = e (n2 k1 < L)
     double2* dstp = a.scratch + (int64_t)sub * a.ncol + col;
@@ -333,14 +287,14 @@ void twiddle_table(int n, std::vector<double2>& t) {
 template <int PRO, int EPI, int SIG>
 xc_status launch_pass(const PassArgs& a, const FftIO& io, cudaStream_t st) {
   const int nseq = 1 << a.lgn;
-  size_t sm = 2ull * a.R * nseq * sizeof(double2) + (PRO == PRO_C2R ? a.cb * sizeof(double2) : 0);
+  size_t sm = 2ull * a.R * nseq * sizeof(double2);
   static bool attr_set = false;
   if (!attr_set) {
     XC_CUDA(cudaFuncSetAttribute(fft_pass<PRO, EPI, SIG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  120 * 1024));
     attr_set = true;
   }
-  int gy = a.pairs ? a.S / 2 + 1 : (a.S + a.sc - 1) / a.sc;
+  int gy = (a.S + a.sc - 1) / a.sc;
   dim3 grid((a.ncol + a.cb - 1) / a.cb, gy);
   int work = a.R * nseq / 2;
   int th = work >= 256 ? 256 : (work >= 128 ? 128 : 64);
@@ -354,24 +308,17 @@ xc_status dispatch(FftPro pro, FftEpi epi, const PassArgs& a, const FftIO& io, c
   // pass-1-of-2 uses only the prologue, pass-2-of-2 only the epilogue
   if (a.stage == 0) {
     if (pro == PRO_PLAIN) return launch_pass<PRO_PLAIN, EPI_PLAIN, SIG>(a, io, st);
-    if (pro == PRO_C2R) return launch_pass<PRO_C2R, EPI_PLAIN, SIG>(a, io, st);
     return launch_pass<PRO_XREAL, EPI_PLAIN, SIG>(a, io, st);
   }
   if (a.stage == 1) {
     if (epi == EPI_PLAIN) return launch_pass<PRO_PLAIN, EPI_PLAIN, SIG>(a, io, st);
-    if (epi == EPI_C2R) return launch_pass<PRO_PLAIN, EPI_C2R, SIG>(a, io, st);
     return launch_pass<PRO_PLAIN, EPI_ZPLANES, SIG>(a, io, st);
   }
 #define XC_CASE(P, E) \
   if (pro == P && epi == E) return launch_pass<P, E, SIG>(a, io, st);
   XC_CASE(PRO_PLAIN, EPI_PLAIN)
-  XC_CASE(PRO_PLAIN, EPI_C2R)
   XC_CASE(PRO_PLAIN, EPI_ZPLANES)
-  XC_CASE(PRO_C2R, EPI_PLAIN)
-  XC_CASE(PRO_C2R, EPI_C2R)
-  XC_CASE(PRO_C2R, EPI_ZPLANES)
   XC_CASE(PRO_XREAL, EPI_PLAIN)
-  XC_CASE(PRO_XREAL, EPI_C2R)
   XC_CASE(PRO_XREAL, EPI_ZPLANES)
 #undef XC_CASE
   xc_set_error("fft: bad prologue/epilogue");
@@ -497,7 +444,10 @@ xc_status fft_run(const FftPlan& p, int sigma, FftPro pro, FftEpi epi, const Fft
   a.ncol = ncol;
   a.scratch = scratch;
   a.twL = p.twL;
-  const bool c2r = (pro == PRO_C2R);
+  if (pro != PRO_PLAIN && pro != PRO_XREAL) {
+    xc_set_error("fft_run: the output-axis inverse runs in c2r_run");
+    return XC_EINVAL;
+  }
   if (p.L2 == 1) {
     a.R = p.L1;
     set_stages(a, p.nf1, p.f1);
@@ -505,7 +455,6 @@ xc_status fft_run(const FftPlan& p, int sigma, FftPro pro, FftEpi epi, const Fft
     a.stage = 2;
     a.S = 1;
     a.sc = 1;
-    a.pairs = c2r ? 1 : 0;
     choose_tile(a.R, ncol, 1, a.cb);
     a.lgcb = ilog2(a.cb);
     a.lgn = a.lgcb;
@@ -515,16 +464,15 @@ xc_status fft_run(const FftPlan& p, int sigma, FftPro pro, FftEpi epi, const Fft
     xc_set_error("fft: two-pass length needs scratch");
     return XC_EINVAL;
   }
-  // pass 1: L1-point FFTs, L2 sub-sequences per column (paired for the C2R prologue)
+  // pass 1: L1-point FFTs, L2 sub-sequences per column
   a.R = p.L1;
   set_stages(a, p.nf1, p.f1);
   a.tw = p.tw1;
   a.stage = 0;
   a.S = p.L2;
-  a.sc = c2r ? 2 : 1;
-  a.pairs = c2r ? 1 : 0;
+  a.sc = 1;
   choose_tile(a.R, ncol, a.sc, a.cb);
-  if (!c2r) {  // spread spare sequences over sub-sequences when there are few columns
+  {  // spread spare sequences over sub-sequences when there are few columns
     int nseq = a.cb;
     while (nseq < 16 && 2 * nseq * a.R <= kTileElems) nseq *= 2;
     a.sc = nseq / a.cb;
@@ -538,7 +486,6 @@ xc_status fft_run(const FftPlan& p, int sigma, FftPro pro, FftEpi epi, const Fft
   a.tw = p.tw2;
   a.stage = 1;
   a.S = p.L1;
-  a.pairs = 0;
   choose_tile(a.R, ncol, 1, a.cb);
   {
     int nseq = a.cb;

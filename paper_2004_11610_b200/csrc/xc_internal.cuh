@@ -114,8 +114,8 @@ void dev_free(DevBuf& b);
 // slow axis of a batch-fastest layout, 1 pass (L <= 1024) or 2 passes
 // (four-step, L = L1 * L2) through an L2-resident scratch.
 // ---------------------------------------------------------------------------
-enum FftPro { PRO_PLAIN = 0, PRO_C2R = 1, PRO_XREAL = 2 };
-enum FftEpi { EPI_PLAIN = 0, EPI_C2R = 1, EPI_ZPLANES = 2 };
+enum FftPro { PRO_PLAIN = 0, PRO_XREAL = 2 };
+enum FftEpi { EPI_PLAIN = 0, EPI_ZPLANES = 2 };
 
 struct FftPlan {
   int L = 0, L1 = 0, L2 = 0;       // L = L1 * L2; single pass when L2 == 1
@@ -130,16 +130,16 @@ struct FftPlan {
 struct FftIO {
   // prologue sources
   const double2* src = nullptr; int64_t lds = 0;           // PRO_PLAIN
-  const double2* Uc = nullptr; int64_t ldu = 0;            // PRO_C2R: half spectrum u_q at Uc[q*ldu + col], q <= M
-  const double2* twh = nullptr; int M = 0;                 // PRO_C2R: e^{+2 pi i n / (2M)}, n < M
+  const double2* Uc = nullptr; int64_t ldu = 0;            // c2r_run: half spectrum u_q at Uc[q*ldu + col], q <= M
+  const double2* twh = nullptr; int M = 0;                 // c2r_run: e^{+2 pi i n / (2M)}, n < M
   int H = 0;
   const double* X = nullptr; int64_t ldx = 0;              // PRO_XREAL
   const double* winv = nullptr;                            // 1/w_p (PRO_XREAL)
   int keep_lo = 0, keep_hi = 0, m_off = 0;
   // epilogue destinations
   double2* dst = nullptr; int64_t ldd = 0; int kmax = 0;    // EPI_PLAIN: bins [0,kmax)
-  double* Y = nullptr; int64_t ldy = 0;                    // EPI_C2R
-  const double* yscale = nullptr;                          // 1/(sqrt(L) w_p) (EPI_C2R)
+  double* Y = nullptr; int64_t ldy = 0;                    // c2r_run: output rows
+  const double* yscale = nullptr;                          // c2r_run: 1/(sqrt(L) w_p)
   double* zre = nullptr; double* zim = nullptr; int64_t ldz = 0;  // EPI_ZPLANES
   double scale = 1.0;                                      // EPI_PLAIN / EPI_ZPLANES
 };
