@@ -18,6 +18,7 @@
  *   orc_jacobi_entries   p_m^(a,b)(x_k), orthonormal Jacobi (C-5)
  *   orc_laguerre_entries l_m(x_k) = exp(-x_k/2) L_m(x_k)
  *   orc_cos_entries      cos(pi * m * t_k)
+ *   orc_sin_entries      sin(pi * m * t_k)  (with cos: e^{i pi m t_k}, NEXT-3)
  *   orc_gauss_newton     Newton polish of Gauss nodes + Christoffel weights
  *   orc_dense_apply      Y = A X or Y = A^T C with entries regenerated on the fly
  */
@@ -239,6 +240,26 @@ static double cospi_exact_product(double m, double t) {
   long double a = (long double)r.hi + (long double)r.lo;
   const long double PI_L = 3.141592653589793238462643383279502884L;
   return (double)cosl(PI_L * a);
+}
+
+/* sin(pi * m * t_k), same exact argument reduction (the imaginary part of e^{i pi m t}). */
+static double sinpi_exact_product(double m, double t) {
+  dd r = two_prod(m, t);
+  double n2 = 2.0 * nearbyint(r.hi * 0.5);
+  r = dd_sub(r, d2dd(n2));
+  long double a = (long double)r.hi + (long double)r.lo;
+  const long double PI_L = 3.141592653589793238462643383279502884L;
+  return (double)sinl(PI_L * a);
+}
+
+int orc_sin_entries(const double *t, int64_t nx, int m0, int m1, int m_off, double *out) {
+  if (m1 <= m0 || nx <= 0) return 0;
+  int64_t W = m1 - m0;
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < nx; ++k)
+    for (int m = m0; m < m1; ++m)
+      out[k * W + (m - m0)] = sinpi_exact_product((double)(m + m_off), t[k]);
+  return 0;
 }
 
 int orc_cos_entries(const double *t, int64_t nx, int m0, int m1, int m_off, double *out) {

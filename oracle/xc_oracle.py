@@ -37,7 +37,7 @@ import scipy.sparse as sp
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = None
 
-KIND_COS, KIND_JACOBI, KIND_LAGUERRE = 1, 2, 3
+KIND_COS, KIND_JACOBI, KIND_LAGUERRE, KIND_EXP = 1, 2, 3, 4
 
 
 def build_lib() -> str:
@@ -59,6 +59,8 @@ def _lib():
                                             ctypes.c_int, ctypes.c_int, dp]
         _LIB.orc_laguerre_entries.argtypes = [dp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, dp]
         _LIB.orc_cos_entries.argtypes = [dp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         dp]
+        _LIB.orc_sin_entries.argtypes = [dp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                          dp]
         _LIB.orc_gauss_newton.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                           ctypes.c_int64, dp, dp, dp, ctypes.c_int]
@@ -82,6 +84,8 @@ class Kind:
     """Which special function generates A[j,k] = phi_j(x_k) (operator convention R-1).
 
     kind COS:      phi_j(t) = cos(pi j t), nodes t in [0,1]
+    kind EXP:      phi_j(t) = exp(i pi j t), nodes t in [0,2): the non-uniform DFT, complex
+                   (the exp row of Appendix A, Eq. A.4 / y3; NEXT-3)
     kind JACOBI:   phi_j(x) = p_j^(alpha,beta)(x), orthonormal on [-1,1] (R-4)
     kind LAGUERRE: phi_j(x) = exp(-x/2) L_j(x), x >= 0
     """
@@ -95,6 +99,11 @@ def entries(kind: Kind, nodes: np.ndarray, m0: int, m1: int, m_off: int = 0) -> 
     x = np.ascontiguousarray(nodes, dtype=np.float64)
     out = np.empty((x.size, m1 - m0), dtype=np.float64)
     lib = _lib()
+    if kind.kind == KIND_EXP:  # complex: e^{i pi m t} = cos + i sin, both exactly reduced
+        im = np.empty_like(out)
+        lib.orc_cos_entries(_p(x), x.size, m0, m1, m_off, _p(out))
+        lib.orc_sin_entries(_p(x), x.size, m0, m1, m_off, _p(im))
+        return out + 1j * im
     if kind.kind == KIND_COS:
         lib.orc_cos_entries(_p(x), x.size, m0, m1, m_off, _p(out))
     elif kind.kind == KIND_JACOBI:
@@ -162,6 +171,9 @@ def gauss_rule(kind: Kind, N: int, newton: int = 2):
 # ---------------------------------------------------------------------------
 def dense_apply(kind: Kind, nodes: np.ndarray, X: np.ndarray) -> np.ndarray:
     """Y[j,b] = sum_k phi_j(x_k) X[k,b], j < N (Y = A X; output indexed by degree)."""
+    if kind.kind == KIND_EXP:  # complex: the entries matrix (exactly reduced), a plain matmul
+        A = entries(kind, nodes, 0, len(nodes)).T                # A[j, k] = e^{i pi j t_k}
+        return A @ np.asarray(X, dtype=np.complex128)
     X = np.ascontiguousarray(X, dtype=np.float64)
     N, B = X.shape
     Y = np.empty((N, B), dtype=np.float64)
@@ -320,7 +332,7 @@ def make_plan(kind: Kind, N: int, eps: float, eps1: float | None = None, eps2: f
     eps2 = 1e-2 if eps2 is None else eps2
     zeta = solve_zeta(eps1)
     plan = Plan(kind, N, eps1, eps2, zeta)
-    if kind.kind == KIND_COS:
+    if kind.kind in (KIND_COS, KIND_EXP):
         # trig form: extra components on both sides (Alg. 2)
         s0 = minimal_s(zeta, N, eps2, two_sided=True)
         L = smooth5_even_at_least(N + 2 * s0)
@@ -346,10 +358,13 @@ def node_spectra(plan: Plan, blk: Block, nodes: np.ndarray) -> np.ndarray:
     """S[k, q] = (F W e_k)_q: unitary DFT (Eq. 1) of the windowed extended row of node k.
 
     Returns the half spectrum q in [0, H) (real rows).  Bins 0 and L/2
-    are real by symmetry and their imaginary part is set to exactly 0.
+    are real by symmetry and their imaginary part is set to exactly 0.  Kind EXP (complex
+    rows): the full spectrum q in [0, L).
     """
     w = kaiser(plan.zeta, blk.L - 1)
     E = entries(plan.kind, nodes, 0, blk.L, blk.m_off)          # E[k, p] = phi_{p+m_off}(x_k)
+    if plan.kind.kind == KIND_EXP:                              # complex rows: the full spectrum
+        return np.fft.fft(E * w[None, :], axis=1, norm="ortho")
     S = np.fft.rfft(E * w[None, :], axis=1, norm="ortho")      # e^{-2 pi i p q / L} / sqrt(L)
     S[:, 0] = S[:, 0].real
     S[:, -1] = S[:, -1].real
@@ -394,6 +409,15 @@ def apply_output_axis(op: Operator, X: np.ndarray) -> np.ndarray:
     output), Y[kept] = v[kept] / w[kept]; the extra positions are discarded
     (Fe2).  Tail degrees by the direct method.
     """
+    if op.plan.kind.kind == KIND_EXP:                           # complex input and output
+        X = np.asarray(X, dtype=np.complex128)
+        Y = np.zeros(X.shape, dtype=np.complex128)
+        for blk, S, w in zip(op.plan.blocks, op.S, op.windows):
+            u = S.T @ X                                         # (L x B): full spectrum
+            v = np.fft.ifft(u, axis=0, norm="ortho")            # e^{+2 pi i p q / L} / sqrt(L)
+            lo, hi = blk.keep_lo, blk.keep_hi
+            Y[lo + blk.m_off:hi + blk.m_off] = v[lo:hi] / w[lo:hi, None]
+        return Y
     X = np.asarray(X, dtype=np.float64)
     N, B = X.shape
     Y = np.zeros((N, B))

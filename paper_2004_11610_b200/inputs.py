@@ -11,7 +11,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-KIND_COS, KIND_JACOBI, KIND_LAGUERRE = 1, 2, 3
+KIND_COS, KIND_JACOBI, KIND_LAGUERRE, KIND_EXP = 1, 2, 3, 4
 
 
 @dataclass(frozen=True)
@@ -35,6 +35,9 @@ CONFIGS = {
     "c3": Config("c3_jacobi_16384", KIND_JACOBI, 16384, 256, 1e-12, 2, alpha=0.5, beta=-0.3),
     "c4": Config("c4_laguerre_8192", KIND_LAGUERRE, 8192, 256, 1e-11, 3, dirs=("A", "WAT")),
     "c5": Config("c5_legendre_65536", KIND_JACOBI, 65536, 4096, 1e-12, 4),
+    # NEXT-3: the complex exponential kind, non-uniform DFT e^{i pi j t_k}, t_k in [0,2);
+    # not a BASELINE config -- a parity / measurement case of the widened path
+    "c6": Config("c6_nonexp_4096", KIND_EXP, 4096, 64, 1e-10, 6),
 }
 
 
@@ -42,6 +45,21 @@ def cos_nodes(N: int, seed: int) -> np.ndarray:
     """Non-uniform cosine nodes t_k = sort(U[0,1]) (first draw of the seed; c2 reading R2)."""
     rng = np.random.default_rng(seed)
     return np.sort(rng.random(N))
+
+
+def exp_nodes(N: int, seed: int) -> np.ndarray:
+    """Non-uniform DFT nodes t_k = sort(U[0,2)) (theta_k = pi t_k on the whole circle)."""
+    rng = np.random.default_rng(seed)
+    return 2.0 * np.sort(rng.random(N))
+
+
+def complex_rhs(N: int, B: int, seed: int, skip_nodes: bool = True) -> np.ndarray:
+    """X = N(0,1) + i N(0,1) (complex128, N x B); the node draw first when skip_nodes."""
+    rng = np.random.default_rng(seed)
+    if skip_nodes:
+        rng.random(N)
+    re = rng.standard_normal((N, B))
+    return re + 1j * rng.standard_normal((N, B))
 
 
 def rhs(N: int, B: int, seed: int, skip_cos_nodes: bool = False) -> np.ndarray:
@@ -61,6 +79,8 @@ def laguerre_coeffs(N: int, B: int, seed: int) -> np.ndarray:
 
 def config_rhs(cfg: Config, B: int | None = None) -> np.ndarray:
     B = cfg.B if B is None else B
+    if cfg.kind == KIND_EXP:
+        return complex_rhs(cfg.N, B, cfg.seed)
     if cfg.kind == KIND_COS:
         return rhs(cfg.N, B, cfg.seed, skip_cos_nodes=True)
     if cfg.kind == KIND_LAGUERRE:

@@ -429,3 +429,64 @@ def test_laguerre_round_trip():
     assert O.rel_l2_cols(Xf, Xd).max() < 1e-10
     C2 = O.apply_output_axis(op, Xf)                     # forward
     assert O.rel_l2_cols(C2, C).max() < 1e-9
+
+
+# --------------------------------------------------------------------------- kind EXP (NEXT-3)
+EXPK = O.Kind(O.KIND_EXP)
+
+
+def test_exp_entries_vs_mpmath():
+    """phi_m(t) = e^{i pi m t}, exactly reduced (m may be negative): vs mpmath."""
+    mp.mp.dps = 30
+    t = np.array([0.0, 0.3, 1.0, 1.37, 1.999])
+    E = O.entries(EXPK, t, -40, 60)
+    for k, tk in enumerate(t):
+        for m in (-40, -1, 0, 7, 59):
+            ref = mp.expj(mp.pi * m * mp.mpf(tk))
+            assert abs(complex(E[k, m + 40]) - complex(ref)) < 2e-16
+
+
+def test_exp_row_spectrum_is_y3():
+    """Appendix A (y3): with the window off the oracle's spectrum of an exp row is the
+    closed form (e^{iL theta} - 1) / (e^{i theta} w^q - 1) / sqrt(L), all L bins (complex rows)."""
+    L = 40
+    plan = O.Plan(EXPK, 30, 1e-12, 1e-2, 0.0)
+    blk = O.Block(L, 0, 0, L)
+    t = np.array([0.11, 0.73, 1.41])
+    S = O.node_spectra(plan, blk, t)
+    assert S.shape == (3, L)
+    for i, tk in enumerate(t):
+        np.testing.assert_allclose(S[i], _closed_form_exp(math.pi * tk, L), atol=1e-14)
+
+
+def test_exp_dense_uniform_nodes_is_inverse_dft():
+    """At t_k = 2k/N the exp transform is the DFT matrix: A X = N ifft(X) (numpy)."""
+    N = 96
+    t = 2.0 * np.arange(N) / N
+    X = I.rhs(N, 3, 4) + 1j * I.rhs(N, 3, 5)
+    np.testing.assert_allclose(O.dense_apply(EXPK, t, X), N * np.fft.ifft(X, axis=0), atol=1e-11)
+
+
+def test_exp_compressed_uniform_nodes_vs_ifft():
+    """Alg. 2 with complex rows at uniform nodes meets 10 eps against numpy's inverse DFT."""
+    N = 256
+    t = 2.0 * np.arange(N) / N
+    op = O.compress(O.make_plan(EXPK, N, 1e-10), t)
+    X = I.rhs(N, 4, 7) + 1j * I.rhs(N, 4, 8)
+    ref = N * np.fft.ifft(X, axis=0)
+    assert O.rel_l2_cols(O.apply_output_axis(op, X), ref).max() < 1e-9
+
+
+def test_exp_keep_all_and_cos_consistency():
+    """Keep-all (eps1 -> 0) reproduces the dense complex product; and for t in [0,1] and real X
+    the real part of the exp transform is the cos transform (Re e^{i pi j t} = cos pi j t)."""
+    N = 60
+    t = np.sort(np.random.default_rng(3).random(N) * 2.0)
+    plan = O.make_plan(EXPK, N, 1e-12)
+    plan.eps1 = 0.0
+    op = O.compress(plan, t)
+    X = I.rhs(N, 2, 1) + 1j * I.rhs(N, 2, 2)
+    assert O.rel_l2_cols(O.apply_output_axis(op, X), O.dense_apply(EXPK, t, X)).max() < 1e-13
+    tc = I.cos_nodes(N, 4)
+    Xr = I.rhs(N, 2, 3)
+    np.testing.assert_allclose(O.dense_apply(EXPK, tc, Xr).real, O.dense_apply(COS, tc, Xr), atol=1e-12)
