@@ -90,6 +90,8 @@ def _nodes(cfg, device):
     from paper_2004_11610_b200 import xc
     if cfg.kind == I.KIND_COS:
         return I.cos_nodes(cfg.N, cfg.seed), None
+    if cfg.kind == I.KIND_EXP:
+        return I.exp_nodes(cfg.N, cfg.seed), None
     x, w, wt = xc.gauss_rule(cfg.kind, cfg.N, cfg.alpha, cfg.beta, device=device)
     return x, wt
 
@@ -100,6 +102,8 @@ def _timing_nodes(cfg):
     import scipy.special
     if cfg.kind == I.KIND_COS:
         return I.cos_nodes(cfg.N, cfg.seed)
+    if cfg.kind == I.KIND_EXP:
+        return I.exp_nodes(cfg.N, cfg.seed)
     if cfg.kind == I.KIND_LAGUERRE:
         return np.linspace(0.0, 4.0 * cfg.N, cfg.N)   # scipy's Laguerre rule overflows at this N
     if cfg.alpha == 0.0 and cfg.beta == 0.0:
@@ -117,7 +121,11 @@ def cpu_oracle_rate(cfg, ncols, ndeg, threads, x=None):
         x = _timing_nodes(cfg)
     X = I.config_rhs(cfg, B=max(ncols, 1))[:, :ncols]
     t0 = time.perf_counter()
-    O.dense_apply_rows(kind, x, X, ndeg)
+    if cfg.kind == I.KIND_EXP:   # complex: the oracle's dense product over all rows
+        O.dense_apply(kind, x, X)
+        ndeg = cfg.N
+    else:
+        O.dense_apply_rows(kind, x, X, ndeg)
     dt = time.perf_counter() - t0
     return ncols * (ndeg / cfg.N) / dt, dt
 
@@ -197,7 +205,10 @@ def main():
 
     # ---- inputs: seeded on the host, this rank's shard, resident in HBM ----
     from paper_2004_11610_b200.shard import column_shard, max_over_ranks
-    if ws == 1:
+    if cfg.kind == I.KIND_EXP:   # complex RHS in the planar layout of the C ABI (2N rows)
+        Xc = I.config_rhs(cfg, B=B)
+        Xh = np.ascontiguousarray(np.concatenate([Xc.real, Xc.imag]))
+    elif ws == 1:
         Xh = I.config_rhs(cfg, B=B)
     elif args.strong:
         Xh = np.ascontiguousarray(I.config_rhs(cfg)[:, column_shard(cfg.B, rank, ws)])
@@ -256,7 +267,8 @@ def main():
 
     # ---- roofline of the dominant kernel (SpMM on the FP64 tensor cores) ----
     nnz, tail, N = info["nnz"], info["tail"], info["N"]
-    spmm_flops = (4.0 * nnz + 2.0 * tail * N) * B          # algorithmic, per launch
+    cmul = 8.0 if cfg.kind == I.KIND_EXP else 4.0         # complex x complex / complex x real
+    spmm_flops = (cmul * nnz + 2.0 * tail * N) * B          # algorithmic, per launch
     spmm_ms = prof["ms_spmm"] / max(1, prof["n"])
     fft_ms = prof["ms_fft"] / max(1, prof["n"])
     achieved = spmm_flops / (spmm_ms / 1e3) / 1e12
@@ -326,7 +338,7 @@ def main():
                          "traffic": traffic, "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
                          "peak_source": "measured DMMA microbenchmark (tools/fp64_peak.cu)",
                          "spmm_ms": spmm_ms, "fft_ms": fft_ms, "spmm_share": spmm_ms / ms,
-                         "dmma_issue_efficiency": (4.0 * nnz + 2.0 * tail * N) / max(1.0, info["dmma_flops_per_col_A"])},
+                         "dmma_issue_efficiency": (cmul * nnz + 2.0 * tail * N) / max(1.0, info["dmma_flops_per_col_A"])},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "graph": graph,

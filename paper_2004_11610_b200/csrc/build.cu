@@ -17,11 +17,17 @@
 
 namespace {
 
-__device__ __forceinline__ double band_val(int k, int q, int comp, const int* start, const int* len,
+// entry of bin q of node k's run [s, s + len) -- taken mod H: runs of complex rows may wrap
+__device__ __forceinline__ double2 band_cval(int k, int q, int H, const int* start, const int* len,
+                                            const int64_t* off, const double2* vals) {
+  int d = q - start[k];
+  if (d < 0) d += H;
+  if (d >= len[k]) return make_double2(0.0, 0.0);
+  return vals[off[k] + d];
+}
+__device__ __forceinline__ double band_val(int k, int q, int comp, int H, const int* start, const int* len,
                                            const int64_t* off, const double2* vals) {
-  int s = start[k];
-  if (q < s || q >= s + len[k]) return 0.0;
-  double2 v = vals[off[k] + (q - s)];
+  const double2 v = band_cval(k, q, H, start, len, off, vals);
   return comp ? v.y : v.x;
 }
 
@@ -41,7 +47,14 @@ __global__ void fill_k(const FillItem* fi, const int* start, const int* len, con
     }
     if (MODE == FILL_OUT_CPLX) {        // node R, bin 4 gm + r/2, component r&1
       int q = 4 * gm + (r >> 1);
-      if (R < N && q < H) v = band_val(R, q, r & 1, start, len, off, vals);
+      if (R < N && q < H) v = band_val(R, q, r & 1, H, start, len, off, vals);
+    } else if (MODE == FILL_OUT_CC) {   // XC_EXP: B row R = (node R/2, re/im of X); row r = (bin, re/im of u)
+      const int node = R >> 1, xc = R & 1, q = 4 * gm + (r >> 1), uc = r & 1;
+      if (node < N && q < H) {
+        const double2 sv = band_cval(node, q, H, start, len, off, vals);
+        // u_re = S_re X_re - S_im X_im,  u_im = S_im X_re + S_re X_im
+        v = uc == 0 ? (xc == 0 ? sv.x : -sv.y) : (xc == 0 ? sv.y : sv.x);
+      }
     } else if (MODE == FILL_OUT_REAL) { // node R, degree 8 gm + r
       int j = 8 * gm + r;
       if (R < N && j < t) v = P[(int64_t)j * N + R];
@@ -49,7 +62,7 @@ __global__ void fill_k(const FillItem* fi, const int* start, const int* len, con
       int node = 8 * gm + r, q = R >> 1;
       if (node < N && q < H) {
         double c = (q == 0 || q == H - 1) ? 1.0 : 2.0;
-        double a = band_val(node, q, R & 1, start, len, off, vals);
+        double a = band_val(node, q, R & 1, H, start, len, off, vals);
         v = (R & 1) ? -c * a : c * a;
       }
     } else {                            // node 8 gm + r, degree R
@@ -69,6 +82,7 @@ xc_status fill_tiles(int mode, const FillItem* fi, int n, const int* start, cons
     case FILL_OUT_CPLX: fill_k<FILL_OUT_CPLX><<<n, 128, 0, st>>>(fi, start, len, off, vals, P, t, N, H, tiles); break;
     case FILL_OUT_REAL: fill_k<FILL_OUT_REAL><<<n, 128, 0, st>>>(fi, start, len, off, vals, P, t, N, H, tiles); break;
     case FILL_IN_CPLX: fill_k<FILL_IN_CPLX><<<n, 128, 0, st>>>(fi, start, len, off, vals, P, t, N, H, tiles); break;
+    case FILL_OUT_CC: fill_k<FILL_OUT_CC><<<n, 128, 0, st>>>(fi, start, len, off, vals, P, t, N, H, tiles); break;
     default: fill_k<FILL_IN_REAL><<<n, 128, 0, st>>>(fi, start, len, off, vals, P, t, N, H, tiles); break;
   }
   XC_CUDA(cudaGetLastError());

@@ -166,6 +166,13 @@ template <int EPI>
 __device__ __forceinline__ void epi_store(const FftIO& io, int k, int col, double2 v) {
   if (EPI == EPI_PLAIN) {
     if (k < io.kmax) io.dst[(int64_t)k * io.ldd + col] = c_scale(v, io.scale);
+  } else if (EPI == EPI_CY) {
+    // XC_EXP: complex output position k kept (Fe2), times 1/(sqrt(L) w_k); planar Y
+    if (k >= io.keep_lo && k < io.keep_hi) {
+      const int64_t o = (int64_t)(k + io.m_off) * io.ldy + col;
+      io.Y[o] = v.x * io.yscale[k];
+      io.Y[io.ypl + o] = v.y * io.yscale[k];
+    }
   } else {  // EPI_ZPLANES
     if (k < io.H) {
       io.zre[(int64_t)k * io.ldz + col] = v.x * io.scale;
@@ -312,12 +319,14 @@ xc_status dispatch(FftPro pro, FftEpi epi, const PassArgs& a, const FftIO& io, c
   }
   if (a.stage == 1) {
     if (epi == EPI_PLAIN) return launch_pass<PRO_PLAIN, EPI_PLAIN, SIG>(a, io, st);
+    if (epi == EPI_CY) return launch_pass<PRO_PLAIN, EPI_CY, SIG>(a, io, st);
     return launch_pass<PRO_PLAIN, EPI_ZPLANES, SIG>(a, io, st);
   }
 #define XC_CASE(P, E) \
   if (pro == P && epi == E) return launch_pass<P, E, SIG>(a, io, st);
   XC_CASE(PRO_PLAIN, EPI_PLAIN)
   XC_CASE(PRO_PLAIN, EPI_ZPLANES)
+  XC_CASE(PRO_PLAIN, EPI_CY)
   XC_CASE(PRO_XREAL, EPI_PLAIN)
   XC_CASE(PRO_XREAL, EPI_ZPLANES)
 #undef XC_CASE

@@ -107,7 +107,67 @@ __global__ void gen_cos(GenParams g, void* F, int64_t ld) {
   put<CPLX>(F, (int64_t)p * ld + k, g.w ? g.w[p] * v : v);
 }
 
+// e^{i pi m t} = (cos, sin)(pi m t), m = p + m_off: the same exact reduction (NEXT-3; the exp row
+// of Appendix A)
+__global__ void gen_exp(GenParams g, double2* F, int64_t ld) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t tot = (int64_t)g.L * g.nc;
+  if (idx >= tot) return;
+  int p = (int)(idx / g.nc), k = (int)(idx - (int64_t)p * g.nc);
+  double m = (double)(p + g.m_off);
+  ddv r = tprod(m, g.nodes[k]);
+  double n2 = 2.0 * rint(0.5 * r.h);
+  r = ddsub(r, dv(n2));
+  double s, c;
+  sincospi(r.h, &s, &c);
+  const double d = 3.141592653589793 * r.l;  // first-order correction for the low part
+  double vc = fma(-d, s, c), vs = fma(d, c, s);
+  const double wp = g.w ? g.w[p] : 1.0;
+  F[(int64_t)p * ld + k] = make_double2(wp * vc, wp * vs);
+}
+
 // ---- band detection: per node, max |S|^2 then the kept run -------------------------
+// circ (complex rows, full spectrum of L = H bins): the run is circular -- the shortest arc
+// holding every kept bin (the complement of the longest circular gap); start in [0, H),
+// start + len may exceed H (bins taken mod H).
+__global__ void band_detect_circ_k(const double2* __restrict__ spec, int H, int nc, double eps1, int* start,
+                                   int* len) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nc) return;
+  double mx = 0.0;
+  for (int q = 0; q < H; ++q) {
+    double2 v = spec[(int64_t)q * nc + k];
+    mx = fmax(mx, v.x * v.x + v.y * v.y);
+  }
+  const double thr = (eps1 * eps1) * mx;
+  int first = -1, prev = -1, gap = -1, gap_end = 0;
+  if (mx > 0.0)
+    for (int q = 0; q < H; ++q) {
+      double2 v = spec[(int64_t)q * nc + k];
+      if (v.x * v.x + v.y * v.y >= thr) {
+        if (first < 0) first = q;
+        if (prev >= 0 && q - prev - 1 > gap) {
+          gap = q - prev - 1;
+          gap_end = q;
+        }
+        prev = q;
+      }
+    }
+  if (first < 0) {
+    start[k] = 0;
+    len[k] = 0;
+    return;
+  }
+  const int wrap = first + (H - 1 - prev);  // unkept bins across the end of the spectrum
+  if (wrap >= gap) {                         // the longest gap wraps: run [first, prev]
+    start[k] = first;
+    len[k] = prev - first + 1;
+  } else {                                   // the longest gap is inside: run starts after it
+    start[k] = gap_end;
+    len[k] = H - gap;
+  }
+}
+
 __global__ void band_detect_k(const double2* __restrict__ spec, int H, int nc, double eps1, int* start, int* len) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nc) return;
@@ -132,7 +192,7 @@ __global__ void band_detect_k(const double2* __restrict__ spec, int H, int nc, d
 }
 
 __global__ void band_store_k(const double2* __restrict__ spec, int H, int nc, double eps1, const int* start,
-                             const int* len, const int64_t* off, double2* vals) {
+                             const int* len, const int64_t* off, double2* vals, bool circ) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nc) return;
   double mx = 0.0;
@@ -145,8 +205,9 @@ __global__ void band_store_k(const double2* __restrict__ spec, int H, int nc, do
   int64_t o = off[k];
   for (int i = 0; i < n; ++i) {
     int q = s + i;
+    if (circ && q >= H) q -= H;
     double2 v = spec[(int64_t)q * nc + k];
-    if (q == 0 || q == H - 1) v.y = 0.0;  // bins 0 and L/2 of a real row are real
+    if (!circ && (q == 0 || q == H - 1)) v.y = 0.0;  // bins 0 and L/2 of a real row are real
     vals[o + i] = (v.x * v.x + v.y * v.y >= thr) ? v : make_double2(0.0, 0.0);
   }
 }
@@ -154,7 +215,10 @@ __global__ void band_store_k(const double2* __restrict__ spec, int H, int nc, do
 }  // namespace
 
 xc_status gen_entries(const GenParams& g, double2* F, cudaStream_t st) {
-  if (g.kind == XC_COS) {
+  if (g.kind == XC_EXP) {
+    int64_t tot = (int64_t)g.L * g.nc;
+    gen_exp<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(g, F, g.nc);
+  } else if (g.kind == XC_COS) {
     int64_t tot = (int64_t)g.L * g.nc;
     gen_cos<true><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(g, F, g.nc);
   } else if (g.kind == XC_JACOBI) {
@@ -179,15 +243,17 @@ xc_status gen_entries_real(const GenParams& g, double* E, int64_t ldE, cudaStrea
   return XC_OK;
 }
 
-xc_status band_detect(const double2* spec, int H, int nc, double eps1, int* start, int* len, cudaStream_t st) {
-  band_detect_k<<<(nc + 127) / 128, 128, 0, st>>>(spec, H, nc, eps1, start, len);
+xc_status band_detect(const double2* spec, int H, int nc, double eps1, int* start, int* len, bool circ,
+                      cudaStream_t st) {
+  if (circ) band_detect_circ_k<<<(nc + 127) / 128, 128, 0, st>>>(spec, H, nc, eps1, start, len);
+  else band_detect_k<<<(nc + 127) / 128, 128, 0, st>>>(spec, H, nc, eps1, start, len);
   XC_CUDA(cudaGetLastError());
   return XC_OK;
 }
 
 xc_status band_store(const double2* spec, int H, int nc, double eps1, const int* start, const int* len,
-                     const int64_t* off, double2* vals, cudaStream_t st) {
-  band_store_k<<<(nc + 127) / 128, 128, 0, st>>>(spec, H, nc, eps1, start, len, off, vals);
+                     const int64_t* off, double2* vals, bool circ, cudaStream_t st) {
+  band_store_k<<<(nc + 127) / 128, 128, 0, st>>>(spec, H, nc, eps1, start, len, off, vals, circ);
   XC_CUDA(cudaGetLastError());
   return XC_OK;
 }

@@ -96,7 +96,7 @@ xc_status make_chain(int kind, int64_t N, double eps1, double eps2, int cutoff, 
     return XC_ENUMERIC;
   }
   out.blocks.clear();
-  if (kind == XC_COS) {
+  if (kind == XC_COS || kind == XC_EXP) {  // trigonometric: one block, extras on both sides
     int s0;
     if (!minimal_s(out.zeta, (int)N, eps2, true, s0)) {
       xc_set_error("s search did not terminate");

@@ -242,6 +242,7 @@ __global__ void reduce_rows8_kernel(const double* __restrict__ part, int64_t ldp
   for (int row = blockIdx.y; row < nrows; row += gridDim.y) {
     int g = row >> 3;
     int n = nch[g];
+    if (n < 0) continue;  // a group whose SpMM item wrote the rows directly
     int64_t r0 = base[g] + (row & 7);
     double sc = rowscale ? rowscale[row] : 1.0;
     for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < ncols; col += gridDim.x * blockDim.x) {

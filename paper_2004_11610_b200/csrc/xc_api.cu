@@ -166,6 +166,8 @@ xc_status ensure_ws(xc_op* h, int64_t B) {
   for (auto& b : h->blocks) {
     if ((h->dirs & XC_DIR_WAT) && b.fft.L2 > 1) scratch_n = std::max(scratch_n, (size_t)b.L * (size_t)B);
     if ((h->dirs & XC_DIR_A) && b.fftM.L2 > 1) scratch_n = std::max(scratch_n, (size_t)b.fftM.L * (size_t)B);
+    if ((h->dirs & XC_DIR_A) && h->kind == XC_EXP && b.fft.L2 > 1)  // C2C inverse of length L
+      scratch_n = std::max(scratch_n, (size_t)b.L * (size_t)B);
   }
   XC_TRY(dev_alloc(h->scratch, std::max<size_t>(1, scratch_n) * sizeof(double2)));
   if (h->dirs & XC_DIR_A) XC_TRY(dev_alloc(h->partA, (size_t)h->rowsA * Bp * sizeof(double)));
@@ -197,6 +199,7 @@ xc_status validate_nodes(int kind, const double* x, int64_t N) {
   }
   bool ok = true;
   if (kind == XC_COS) ok = x[0] >= 0.0 && x[N - 1] <= 1.0;
+  if (kind == XC_EXP) ok = x[0] >= 0.0 && x[N - 1] < 2.0;
   if (kind == XC_JACOBI) ok = x[0] >= -1.0 && x[N - 1] <= 1.0;
   if (kind == XC_LAGUERRE) ok = x[0] >= 0.0;
   if (!ok) {
@@ -210,9 +213,10 @@ xc_status validate_nodes(int kind, const double* x, int64_t N) {
 xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int node_chunk, int n0, int n1,
                       cudaStream_t st) {
   const int N = (int)h->N;
-  b.H = b.L / 2 + 1;
+  const bool cplx_rows = h->kind == XC_EXP;  // complex rows: the full spectrum (no Hermitian half)
+  b.H = cplx_rows ? b.L : b.L / 2 + 1;
   XC_TRY(fft_plan_make(b.fft, b.L));
-  XC_TRY(fft_plan_make(b.fftM, b.L / 2, true));
+  if (!cplx_rows) XC_TRY(fft_plan_make(b.fftM, b.L / 2, true));
   {
     std::vector<double2> tw(b.L / 2);
     const long double PI2 = 6.283185307179586476925286766559005768L;
@@ -271,7 +275,7 @@ xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int n
     XC_TRY(fft_run(b.fft, -1, PRO_PLAIN, EPI_PLAIN, io, n, (double2*)scr.p, st));
     int* ds = (int*)b.start.p + k0;
     int* dl = (int*)b.len.p + k0;
-    XC_TRY(band_detect((const double2*)spec.p, b.H, n, h->eps1, ds, dl, st));
+    XC_TRY(band_detect((const double2*)spec.p, b.H, n, h->eps1, ds, dl, cplx_rows, st));
     XC_CUDA(cudaMemcpyAsync(b.h_start.data() + k0, ds, n * sizeof(int), cudaMemcpyDeviceToHost, st));
     XC_CUDA(cudaMemcpyAsync(b.h_len.data() + k0, dl, n * sizeof(int), cudaMemcpyDeviceToHost, st));
     XC_CUDA(cudaStreamSynchronize(st));
@@ -286,7 +290,7 @@ xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int n
     XC_TRY(dev_alloc(cv, (size_t)std::max<int64_t>(1, tot) * sizeof(double2)));
     XC_TRY(upload(choff, loc));
     XC_TRY(band_store((const double2*)spec.p, b.H, n, h->eps1, ds, dl, (const int64_t*)choff.p,
-                      (double2*)cv.p, st));
+                      (double2*)cv.p, cplx_rows, st));
     XC_CUDA(cudaStreamSynchronize(st));
     chunk_vals.push_back(cv);
     chunk_base.push_back(tot);
@@ -419,7 +423,8 @@ xc_status upload_and_fill(xc_op* h, ItemSet& S, bool input_axis, DevBuf& d_items
     XC_TRY(upload(dfill, part));
     if (fam >= 0) {
       BlockData& b = h->blocks[fam];
-      XC_TRY(fill_tiles(input_axis ? FILL_IN_CPLX : FILL_OUT_CPLX, (FillItem*)dfill.p, (int)part.size(),
+      XC_TRY(fill_tiles(input_axis ? FILL_IN_CPLX : (h->kind == XC_EXP ? FILL_OUT_CC : FILL_OUT_CPLX),
+                        (FillItem*)dfill.p, (int)part.size(),
                         (int*)b.start.p, (int*)b.len.p, (int64_t*)b.off.p, (double2*)b.vals.p, nullptr, 0, N, b.H,
                         (double*)d_tiles.p, st));
     } else {
@@ -505,38 +510,50 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
   ItemSet S;
   int64_t rows = 0;
   std::vector<MTile> pool;  // split-block M-tiles of every block, paired across blocks per chunk
+  // B rows per node: 1 (real X), 2 for XC_EXP (planar complex X: row 2k real part, 2k+1 imag)
+  const int kb = h->kind == XC_EXP ? 2 : 1;
   for (size_t bi = 0; bi < h->blocks.size(); ++bi) {
     BlockData& b = h->blocks[bi];
     b.ngroups = (b.H + 3) / 4;
-    std::vector<int> klo(b.ngroups, N), khi(b.ngroups, 0);
+    // per group: the B-row range touched in each node chunk of KC B rows (chunks ascending)
+    struct Seg {
+      int c, lo, hi;
+    };
+    std::vector<std::vector<Seg>> seg(b.ngroups);
+    std::vector<int> last_node(b.ngroups, -1);
     for (int k = 0; k < N; ++k) {
-      if (b.h_len[k] == 0) continue;
-      int g0 = b.h_start[k] / 4, g1 = (b.h_start[k] + b.h_len[k] - 1) / 4;
-      for (int g = g0; g <= g1; ++g) {
-        klo[g] = std::min(klo[g], k);
-        khi[g] = std::max(khi[g], k + 1);
+      const int len = b.h_len[k];
+      if (len == 0) continue;
+      const int r0 = kb * k, r1 = kb * (k + 1), c = r0 / KC;
+      for (int j = 0; j < len; ++j) {
+        const int q = (b.h_start[k] + j) % b.H;  // complex rows may wrap around the spectrum
+        const int g = q / 4;
+        if (last_node[g] == k) continue;         // this node already counted for group g
+        last_node[g] = k;
+        auto& v = seg[g];
+        if (!v.empty() && v.back().c == c) v.back().hi = r1;
+        else v.push_back(Seg{c, r0, r1});
       }
     }
-    int maxspan = 0;
-    for (int g = 0; g < b.ngroups; ++g)
-      if (klo[g] < khi[g]) maxspan = std::max(maxspan, khi[g] - klo[g]);
-    b.split = maxspan > KSPLIT;
     b.ubase = rows;
     rows += 8LL * b.ngroups;
     std::vector<int64_t> gbase(b.ngroups, 0);
-    std::vector<int> gnch(b.ngroups, 0);
+    std::vector<int> gnch(b.ngroups, -1);  // -1: the group's items write U directly
     std::vector<MTile> mt;
+    b.split = false;
     for (int g = 0; g < b.ngroups; ++g) {
-      const int a = klo[g] < khi[g] ? klo[g] : 0, e = klo[g] < khi[g] ? khi[g] : 0;
-      if (!b.split) {
+      const auto& v = seg[g];
+      const int a = v.empty() ? 0 : v.front().lo, e = v.empty() ? 0 : v.back().hi;
+      if (e - a <= KSPLIT) {  // one item over the whole range writes the group's U rows
         mt.push_back(MTile{(int)bi, g, 0, a, e, b.ubase + 8LL * g, 1});  // empty group -> zeros
         continue;
       }
+      // long (or wrapping) group: one partial M-tile per touched chunk, reduced in fixed order
+      b.split = true;
       gbase[g] = rows;
-      for (int c = a / KC; c * KC < e; ++c) {
-        const int k0 = std::max(a, c * KC), k1 = std::min(e, (c + 1) * KC);
-        if (k1 <= k0) continue;
-        pool.push_back(MTile{(int)bi, g, c, k0, k1, rows, 1});
+      gnch[g] = 0;
+      for (const Seg& sg : v) {
+        pool.push_back(MTile{(int)bi, g, sg.c, sg.lo, sg.hi, rows, 1});
         rows += 8;
         gnch[g]++;
       }
@@ -544,9 +561,8 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
     if (b.split) {
       XC_TRY(upload(b.grp_base, gbase));
       XC_TRY(upload(b.grp_nch, gnch));
-    } else {
-      pair_list(mt, 0, S);  // consecutive groups of one block (ordered by g)
     }
+    pair_list(mt, 0, S);  // the direct groups, consecutive in g
   }
   // split blocks: per node chunk, all blocks' M-tiles ordered by range, paired across blocks
   std::stable_sort(pool.begin(), pool.end(), [](const MTile& x, const MTile& y) {
@@ -650,7 +666,7 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
   xc_params p;
   xc_params_default(&p);
   if (prm) p = *prm;
-  if (kind != XC_COS && kind != XC_JACOBI && kind != XC_LAGUERRE) {
+  if (kind != XC_COS && kind != XC_JACOBI && kind != XC_LAGUERRE && kind != XC_EXP) {
     xc_set_error("unknown kind");
     return XC_EINVAL;
   }
@@ -677,6 +693,10 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
   if (kind == XC_JACOBI && !(p.alpha > -1.0 && p.beta > -1.0)) {
     xc_set_error("Jacobi alpha, beta must be > -1");
     return XC_EINVAL;
+  }
+  if (kind == XC_EXP && (h->dirs & XC_DIR_WAT)) {
+    xc_set_error("XC_EXP: only XC_DIR_A is implemented");
+    return XC_EUNSUPPORTED;
   }
   if ((h->dirs & XC_DIR_WAT) && !p.weights) {
     xc_set_error("XC_DIR_WAT needs weights");
@@ -761,7 +781,8 @@ xc_status build_end(xc_op* h) {
     fft += fft_flops(b.L);
   }
   in.nnz = nnz;
-  in.flops_per_col_A = 4.0 * nnz + 2.0 * h->tail * N + fft;
+  // complex x real: 2 FMA per kept entry; XC_EXP complex x complex: 4 FMA (and a complex FFT)
+  in.flops_per_col_A = (kind == XC_EXP ? 8.0 : 4.0) * nnz + 2.0 * h->tail * N + (kind == XC_EXP ? 2.0 : 1.0) * fft;
   in.flops_per_col_WAT = in.flops_per_col_A;
   in.dmma_flops_per_col_A = 64.0 * h->mtstepsA;   // 8 x 4 FMA per M-tile step and column
   in.dmma_flops_per_col_WAT = 64.0 * h->mtstepsW;
@@ -770,7 +791,7 @@ xc_status build_end(xc_op* h) {
   int fl = 0, flM = 0, nsplit = 0;
   for (auto& b : h->blocks) {
     fl += (b.fft.L2 > 1) ? 2 : 1;
-    flM += (b.fftM.L2 > 1) ? 2 : 1;
+    flM += h->kind == XC_EXP ? ((b.fft.L2 > 1) ? 2 : 1) : ((b.fftM.L2 > 1) ? 2 : 1);
     nsplit += b.split ? 1 : 0;
   }
   auto spmm_launches = [](int n) { return n <= 0 ? 0 : (n + 65535 - 1) / 65535; };
@@ -837,6 +858,37 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
   const int64_t Bp = pad_cols(B);
   const int N = (int)h->N;
   XC_TRY(mark(0));
+  if (dir == XC_DIR_A && h->kind == XC_EXP) {
+    // complex input in planar form: B row 2k = Re X[k], 2k+1 = Im X[k] (rows N.. are the imag plane)
+    SpmmSrcs s{};
+    s.re[0] = X;
+    s.im[0] = X + (int64_t)N * ldx;
+    s.nrows[0] = N;
+    s.ld[0] = ldx;
+    XC_TRY(spmm_run((const SpmmWin*)h->winsA.p, h->nwinsA, (const SpmmItem*)h->itemsA.p,
+                    (const double*)h->tilesA.p, s, (double*)h->partA.p, Bp, (int)B, st));
+    XC_TRY(mark(1));
+    for (auto& b : h->blocks) {
+      double* U = (double*)h->partA.p + b.ubase * Bp;
+      if (b.split)
+        XC_TRY(reduce_rows8((const double*)h->partA.p, Bp, (const int64_t*)b.grp_base.p, (const int*)b.grp_nch.p,
+                            8 * b.ngroups, nullptr, U, Bp, (int)Bp, st));
+      // v = F* u over all L bins (complex inverse DFT), then Fe2 discard and W^{-1}
+      FftIO io{};
+      io.src = reinterpret_cast<const double2*>(U);
+      io.lds = Bp;
+      io.Y = Y;
+      io.ldy = ldy;
+      io.ypl = (int64_t)N * ldy;
+      io.yscale = (const double*)b.yscale.p;
+      io.keep_lo = b.keep_lo;
+      io.keep_hi = b.keep_hi;
+      io.m_off = b.m_off;
+      XC_TRY(fft_run(b.fft, +1, PRO_PLAIN, EPI_CY, io, (int)B, (double2*)h->scratch.p, st));
+    }
+    XC_TRY(mark(2));
+    return mark(3);
+  }
   if (dir == XC_DIR_A) {
     SpmmSrcs s{};
     s.re[0] = X;
@@ -1184,7 +1236,7 @@ xc_status host_enqueue(xc_op* h, xc_dir dir, const double* Xh, double* Yh, int64
     }
     XC_CUDA(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming));
   }
-  const int64_t N = h->N;
+  const int64_t N = h->kind == XC_EXP ? 2 * h->N : h->N;  // rows of X / Y (planar complex: 2N)
   // chunk: a multiple of 64 columns (the SpMM column tile), at least 64
   int64_t nparts = 12;  // ~B/12 columns per chunk: the measured optimum at c5 (2D DMA efficiency vs pipeline fill)
   if (const char* e = getenv("XC_HOST_CHUNKS")) nparts = std::max(1, atoi(e));
@@ -1285,6 +1337,7 @@ xc_status xc_workspace_query(xc_handle h, int64_t B, size_t* bytes) {
   for (auto& b : h->blocks) {
     if ((h->dirs & XC_DIR_WAT) && b.fft.L2 > 1) scr = std::max(scr, (size_t)b.L * B * sizeof(double2));
     if ((h->dirs & XC_DIR_A) && b.fftM.L2 > 1) scr = std::max(scr, (size_t)b.fftM.L * B * sizeof(double2));
+    if ((h->dirs & XC_DIR_A) && h->kind == XC_EXP && b.fft.L2 > 1) scr = std::max(scr, (size_t)b.L * B * sizeof(double2));
   }
   s += scr;
   if (h->dirs & XC_DIR_A) s += (size_t)h->rowsA * Bp * 8;
@@ -1337,8 +1390,9 @@ xc_status xc_node_spectrum(xc_handle h, int i, int64_t k, double* re, double* im
   XC_CUDA(cudaSetDevice(h->device));
   XC_CUDA(cudaMemcpy(v.data(), (double2*)b.vals.p + b.h_off[k], n * sizeof(double2), cudaMemcpyDeviceToHost));
   for (int j = 0; j < n; ++j) {
-    re[b.h_start[k] + j] = v[j].x;
-    im[b.h_start[k] + j] = v[j].y;
+    const int q = (b.h_start[k] + j) % b.H;  // runs of complex rows may wrap (XC_EXP)
+    re[q] = v[j].x;
+    im[q] = v[j].y;
   }
   return XC_OK;
 }

@@ -115,7 +115,7 @@ void dev_free(DevBuf& b);
 // (four-step, L = L1 * L2) through an L2-resident scratch.
 // ---------------------------------------------------------------------------
 enum FftPro { PRO_PLAIN = 0, PRO_XREAL = 2 };
-enum FftEpi { EPI_PLAIN = 0, EPI_ZPLANES = 2 };
+enum FftEpi { EPI_PLAIN = 0, EPI_ZPLANES = 2, EPI_CY = 3 };  // EPI_CY: XC_EXP output (planar, W^{-1}, Fe2)
 
 struct FftPlan {
   int L = 0, L1 = 0, L2 = 0;       // L = L1 * L2; single pass when L2 == 1
@@ -139,7 +139,8 @@ struct FftIO {
   // epilogue destinations
   double2* dst = nullptr; int64_t ldd = 0; int kmax = 0;    // EPI_PLAIN: bins [0,kmax)
   double* Y = nullptr; int64_t ldy = 0;                    // c2r_run: output rows
-  const double* yscale = nullptr;                          // c2r_run: 1/(sqrt(L) w_p)
+  const double* yscale = nullptr;                          // c2r_run / EPI_CY: 1/(sqrt(L) w_p)
+  int64_t ypl = 0;                                         // EPI_CY: offset of the imaginary plane of Y
   double* zre = nullptr; double* zim = nullptr; int64_t ldz = 0;  // EPI_ZPLANES
   double scale = 1.0;                                      // EPI_PLAIN / EPI_ZPLANES
 };
@@ -223,7 +224,7 @@ xc_status reduce_rows8(const double* part, int64_t ldp, const int64_t* base, con
 // Precompute kernels (gen.cu)
 // ---------------------------------------------------------------------------
 struct GenParams {
-  int kind;            // XC_COS / XC_JACOBI / XC_LAGUERRE
+  int kind;            // XC_COS / XC_JACOBI / XC_LAGUERRE / XC_EXP (complex entries)
   int L;               // positions [0, L)
   int m_off;           // degree = position + m_off
   const double* nodes; // device, chunk
@@ -238,10 +239,11 @@ xc_status gen_entries(const GenParams& g, double2* F, cudaStream_t st);
 xc_status gen_entries_real(const GenParams& g, double* E, int64_t ldE, cudaStream_t st);
 
 // Band detection and compaction on a spectrum chunk Spec[q * nc + k], q < H.
-xc_status band_detect(const double2* spec, int H, int nc, double eps1, int* start, int* len,
+// circ: complex rows (XC_EXP), full circular spectrum of H = L bins; runs may wrap (mod H).
+xc_status band_detect(const double2* spec, int H, int nc, double eps1, int* start, int* len, bool circ,
                       cudaStream_t st);
 xc_status band_store(const double2* spec, int H, int nc, double eps1, const int* start, const int* len,
-                     const int64_t* off, double2* vals, cudaStream_t st);
+                     const int64_t* off, double2* vals, bool circ, cudaStream_t st);
 
 // Gauss rules (gauss.cu)
 xc_status gauss_rule_device(int kind, double alpha, double beta, int64_t N, double* x, double* w,

@@ -14,7 +14,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libxc.so")
 
-XC_COS, XC_JACOBI, XC_LAGUERRE = 1, 2, 3
+XC_COS, XC_JACOBI, XC_LAGUERRE, XC_EXP = 1, 2, 3, 4
 XC_DIR_A, XC_DIR_WAT = 1, 2
 _STATUS = {0: "XC_OK", 1: "XC_EINVAL", 2: "XC_ENUMERIC", 3: "XC_ESTATE", 4: "XC_ENOMEM", 5: "XC_ECUDA",
            6: "XC_EUNSUPPORTED"}
@@ -218,14 +218,23 @@ class Transform:
         if X.stride(1) != 1:
             X = X.contiguous()
         N, B = X.shape
-        if N != self.N:
-            raise XcError(f"X has {N} rows, transform has N = {self.N}")
+        rows = 2 * self.N if self.kind == XC_EXP else self.N   # XC_EXP: planar complex (re rows, im rows)
+        if N != rows:
+            raise XcError(f"X has {N} rows, transform needs {rows}")
         if out is None:
             out = torch.empty((N, B), dtype=torch.float64, device=X.device)
         st = stream if stream is not None else torch.cuda.current_stream(X.device).cuda_stream
         _check(self._lib.xc_apply(self._h, direction, ctypes.c_void_p(X.data_ptr()), X.stride(0),
                                   ctypes.c_void_p(out.data_ptr()), out.stride(0), B, ctypes.c_void_p(st)))
         return out
+
+    def apply_complex(self, Xc, stream=None):
+        """XC_EXP with a complex128 CUDA tensor (N x B): marshalled to and from the planar layout
+        of the C ABI (real rows, then imaginary rows)."""
+        import torch
+        Xp = torch.cat([Xc.real, Xc.imag]).contiguous()
+        Yp = self.apply(Xp, XC_DIR_A, stream=stream)
+        return torch.complex(Yp[:self.N], Yp[self.N:])
 
     def apply_host(self, X: np.ndarray, direction: int = XC_DIR_A, out: np.ndarray | None = None, stream=None):
         """End-to-end call with host buffers (copies inside the library call)."""

@@ -440,3 +440,45 @@ def test_host_async_stream_matches():
     for Xp, Yp in zip(Xs, Ys):
         assert torch.equal(Yp, T.apply(Xp.cuda()).cpu())
     T.close()
+
+
+EXP_CASES = [("c6", 4096, 64, 1e-10, 6), ("exp_ragged", 1000, 37, 1e-10, 9), ("exp_small", 96, 3, 1e-12, 2)]
+
+
+@pytest.mark.parametrize("case", EXP_CASES, ids=[c[0] for c in EXP_CASES])
+def test_exp_kind_parity(case):
+    """NEXT-3, kind XC_EXP (complex rows, full circular spectrum, complex x complex DMMA SpMM, complex
+    inverse DFT): GPU vs the oracle's compressed apply (1e-12) and the dense product (10 eps)."""
+    xc = _xc()
+    name, N, B, eps, seed = case
+    t = I.exp_nodes(N, seed)
+    X = I.complex_rhs(N, B, seed)
+    T = xc.Transform(xc.XC_EXP, t, eps)
+    Xg = torch.from_numpy(X).cuda()
+    Y = T.apply_complex(Xg).cpu().numpy()
+    op = O.compress(O.make_plan(O.Kind(O.KIND_EXP), N, eps), t)
+    assert O.rel_l2_cols(Y, O.apply_output_axis(op, X)).max() <= 1e-12, name
+    cols = np.arange(min(B, 8))
+    assert O.rel_l2_cols(Y[:, cols], O.dense_apply(O.Kind(O.KIND_EXP), t, X[:, cols])).max() <= 10 * eps, name
+    # the operator: circular runs equal the oracle's kept entries (sampled nodes, incl. both ends)
+    full = O.node_spectra(op.plan, op.plan.blocks[0], t[[0, N // 2, N - 1]])
+    for j, k in enumerate((0, N // 2, N - 1)):
+        g = T.node_spectrum(0, k)
+        o = op.S[0][k].toarray().ravel()
+        m = np.abs(full[j]).max()
+        assert np.abs(g - o).max() <= 1e-13 * m, (name, k)
+    T.close()
+
+
+def test_exp_uniform_nodes_is_inverse_dft():
+    """XC_EXP at t_k = 2k/N is the DFT: A X = N ifft(X) (numpy) within 10 eps."""
+    xc = _xc()
+    N, B, eps = 512, 5, 1e-12
+    t = 2.0 * np.arange(N) / N
+    X = I.complex_rhs(N, B, 3)
+    T = xc.Transform(xc.XC_EXP, t, eps)
+    Y = T.apply_complex(torch.from_numpy(X).cuda()).cpu().numpy()
+    assert O.rel_l2_cols(Y, N * np.fft.ifft(X, axis=0)).max() <= 10 * eps
+    with pytest.raises(xc.XcError, match="XC_EUNSUPPORTED"):
+        xc.Transform(xc.XC_EXP, t, eps, dirs=xc.XC_DIR_A | xc.XC_DIR_WAT, weights=np.ones(N))
+    T.close()
