@@ -147,6 +147,13 @@ xc_status xc_apply(xc_handle h, xc_dir dir, const double* X, int64_t ldx, double
  * capturing.  Graphs are dropped when the workspace grows.  enable = 0 turns them off. */
 xc_status xc_set_graphs(xc_handle h, int enable);
 
+/* Test entry point: the computation stage's real-output inverse DFT engine alone, for the
+ * block length L (even) with the window switched off: Y[p] = (F*_L u)_p, p < L (unitary, P:24,
+ * real case P:444).  U: DEVICE, L/2 + 1 complex rows x B (interleaved re, im per column; row
+ * pitch ldu complex), the half spectrum u_0..u_{L/2}; Y: DEVICE, L x B, ld ldy.  Synchronises
+ * `stream`.  XC_EINVAL for odd L, L < 4, B < 1 or ld < B. */
+xc_status xc_c2r_check(int64_t L, const double* U, int64_t ldu, double* Y, int64_t ldy, int64_t B, void* stream);
+
 /* Same as xc_apply with HOST buffers X_host, Y_host (row-major N x B, ld = B):
  * copies X to the device, applies, copies Y back, and synchronises `stream`.
  * The batch is processed in column chunks (about B/16 columns, a multiple of 64) through a

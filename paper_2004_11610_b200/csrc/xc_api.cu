@@ -1163,6 +1163,53 @@ xc_status xc_build_step(xc_handle h, xc_exchange_t* ex) {
   return XC_OK;
 }
 
+// Test entry point: the output-axis real-output inverse DFT engine alone (c2r_run with the plan
+// a block of length L would use), W = 1: Y[p] = (F*_L u)_p (unitary) for p < L.
+xc_status xc_c2r_check(int64_t L, const double* U, int64_t ldu, double* Y, int64_t ldy, int64_t B, void* stream) {
+  if (L < 4 || (L & 1) || !U || !Y || B < 1 || ldu < B || ldy < B) {
+    xc_set_error("c2r_check: need even L >= 4, B >= 1, ld >= B");
+    return XC_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  FftPlan plan;
+  XC_TRY(fft_plan_make(plan, (int)(L / 2), true));
+  std::vector<double2> tw(L / 2);
+  const long double PI2 = 6.283185307179586476925286766559005768L;
+  for (int64_t n = 0; n < L / 2; ++n) {
+    long double a = PI2 * (long double)n / (long double)L;
+    tw[n] = make_double2((double)cosl(a), (double)sinl(a));
+  }
+  std::vector<double> ys(L, 1.0 / sqrt((double)L));
+  DevBuf dtw, dys, scr;
+  xc_status s = upload(dtw, tw);
+  if (s == XC_OK) s = upload(dys, ys);
+  if (s == XC_OK && plan.L2 > 1) s = dev_alloc(scr, (size_t)(L / 2) * B * sizeof(double2));
+  if (s == XC_OK) {
+    FftIO io{};
+    io.Uc = reinterpret_cast<const double2*>(U);
+    io.ldu = ldu;
+    io.twh = (const double2*)dtw.p;
+    io.M = (int)(L / 2);
+    io.H = (int)(L / 2 + 1);
+    io.Y = Y;
+    io.ldy = ldy;
+    io.yscale = (const double*)dys.p;
+    io.keep_lo = 0;
+    io.keep_hi = (int)L;
+    io.m_off = 0;
+    s = c2r_run(plan, io, (int)B, (double2*)scr.p, st);
+  }
+  if (s == XC_OK && cudaStreamSynchronize(st) != cudaSuccess) {
+    xc_set_error("c2r_check: kernel failed");
+    s = XC_ECUDA;
+  }
+  dev_free(dtw);
+  dev_free(dys);
+  dev_free(scr);
+  fft_plan_free(plan);
+  return s;
+}
+
 xc_status xc_apply(xc_handle h, xc_dir dir, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t B,
                    void* stream) {
   if (!h) {

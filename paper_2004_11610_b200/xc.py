@@ -48,7 +48,7 @@ class XcBlockInfo(ctypes.Structure):
                 ("keep_hi", ctypes.c_int), ("nnz", _i64), ("max_band", ctypes.c_int)]
 
 
-EXPORTS = ["xc_params_default", "xc_build_compressed", "xc_build_local", "xc_build_step", "xc_apply", "xc_set_graphs", "xc_apply_host", "xc_apply_host_async", "xc_host_wait", "xc_reserve",
+EXPORTS = ["xc_params_default", "xc_build_compressed", "xc_build_local", "xc_build_step", "xc_apply", "xc_c2r_check", "xc_set_graphs", "xc_apply_host", "xc_apply_host_async", "xc_host_wait", "xc_reserve",
            "xc_workspace_query", "xc_info", "xc_block_info", "xc_block_window", "xc_node_spectrum",
            "xc_gauss_rule", "xc_plan_chain", "xc_profile_enable", "xc_profile_read", "xc_destroy",
            "xc_last_error", "xc_version"]
@@ -78,6 +78,7 @@ def load():
     lib.xc_apply.argtypes = [vp, ctypes.c_int, vp, _i64, vp, _i64, _i64, vp]
     lib.xc_apply_host.argtypes = [vp, ctypes.c_int, vp, vp, _i64, vp]
     lib.xc_set_graphs.argtypes = [vp, ctypes.c_int]
+    lib.xc_c2r_check.argtypes = [_i64, vp, _i64, vp, _i64, _i64, vp]
     lib.xc_apply_host_async.argtypes = [vp, ctypes.c_int, vp, vp, _i64, vp]
     lib.xc_host_wait.argtypes = [vp]
     lib.xc_reserve.argtypes = [vp, _i64]
@@ -316,6 +317,19 @@ class Transform:
             self.close()
         except Exception:
             pass
+
+
+def c2r_check(L: int, U, stream=None):
+    """Test entry point: the real-output inverse DFT engine alone (xc_c2r_check); U a complex128
+    CUDA tensor (L/2 + 1, B), returns the (L, B) float64 unitary inverse."""
+    import torch
+    Ui = torch.view_as_real(U.contiguous()).contiguous()
+    B = U.shape[1]
+    Y = torch.empty((L, B), dtype=torch.float64, device=U.device)
+    st = stream if stream is not None else torch.cuda.current_stream(U.device).cuda_stream
+    _check(load().xc_c2r_check(L, ctypes.c_void_p(Ui.data_ptr()), B, ctypes.c_void_p(Y.data_ptr()), B, B,
+                               ctypes.c_void_p(st)))
+    return Y
 
 
 def version() -> str:

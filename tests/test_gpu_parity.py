@@ -482,3 +482,19 @@ def test_exp_uniform_nodes_is_inverse_dft():
     with pytest.raises(xc.XcError, match="XC_EUNSUPPORTED"):
         xc.Transform(xc.XC_EXP, t, eps, dirs=xc.XC_DIR_A | xc.XC_DIR_WAT, weights=np.ones(N))
     T.close()
+
+
+@pytest.mark.parametrize("L,B", [(86400, 64), (27648, 64), (9000, 96), (2916, 64), (960, 64), (360, 8),
+                                 (21600, 32), (10800, 64), (7200, 64), (1152, 40), (720, 1), (60, 3)])
+def test_c2r_engine_vs_numpy(L, B):
+    """The output-axis inverse DFT engine (c2r.cu) alone at the block lengths of c1-c5 -- including
+    the specialised and big-tile passes of c5 (86400 = 2 x 200 x 216, 27648, 9000, 2916) -- against
+    numpy's unitary irfft (Eq. 1 convention, pinned in test_oracle_pins), 1e-13 relative."""
+    xc = _xc()
+    rng = np.random.default_rng(L + B)
+    U = rng.standard_normal((L // 2 + 1, B)) + 1j * rng.standard_normal((L // 2 + 1, B))
+    U[0].imag = 0.0
+    U[-1].imag = 0.0
+    Y = xc.c2r_check(L, torch.from_numpy(U).cuda()).cpu().numpy()
+    ref = np.fft.irfft(U, n=L, axis=0, norm="ortho")
+    assert O.rel_l2_cols(Y, ref).max() <= 1e-13
