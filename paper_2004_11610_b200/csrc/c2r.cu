@@ -535,7 +535,6 @@ int ilog2i(int v) {
   return l;
 }
 
-int g_nsm = 0;
 
 void set_radices(C2RArgs& a) {
   const StagePlan P = stages_of(a.R);
@@ -671,17 +670,14 @@ bool has_big(int mode, int R) {
 
 template <int MODE>
 xc_status launch(C2RArgs& a, const FftIO& io, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> once{0};
+  if (first_on_device(once)) {
     XC_CUDA(cudaFuncSetAttribute(c2r_pass<MODE, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     for (const Spec& sp : kSpecs)
       if (sp.mode == MODE)
         XC_CUDA(cudaFuncSetAttribute((const void*)sp.k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    int dev = 0;
-    XC_CUDA(cudaGetDevice(&dev));
-    XC_CUDA(cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, dev));
-    attr = true;
   }
+  const int nsm = sm_count();
   a.mode = MODE;
   a.ntx = (a.ncol + a.cb - 1) / a.cb;
   int nty;
@@ -712,7 +708,7 @@ xc_status launch(C2RArgs& a, const FftIO& io, cudaStream_t st) {
   }
   int per_sm = 0;
   XC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, nt, sm));
-  const int grid = std::min(a.ntiles, std::max(1, per_sm) * std::max(1, g_nsm));
+  const int grid = std::min(a.ntiles, std::max(1, per_sm) * std::max(1, nsm));
   k<<<grid, nt, sm, st>>>(a, io);
   XC_CUDA(cudaGetLastError());
   return XC_OK;

@@ -295,12 +295,10 @@ template <int PRO, int EPI, int SIG>
 xc_status launch_pass(const PassArgs& a, const FftIO& io, cudaStream_t st) {
   const int nseq = 1 << a.lgn;
   size_t sm = 2ull * a.R * nseq * sizeof(double2);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<unsigned long long> once{0};
+  if (first_on_device(once))
     XC_CUDA(cudaFuncSetAttribute(fft_pass<PRO, EPI, SIG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  120 * 1024));
-    attr_set = true;
-  }
   int gy = (a.S + a.sc - 1) / a.sc;
   dim3 grid((a.ncol + a.cb - 1) / a.cb, gy);
   int work = a.R * nseq / 2;

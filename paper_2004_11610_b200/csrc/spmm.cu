@@ -222,11 +222,9 @@ template <int NT>
 xc_status launch(const SpmmWin* wins, int nwins, const SpmmItem* items, const double* tiles, const SpmmSrcs& srcs,
                  double* part, int64_t ldp, int ncols, cudaStream_t st) {
   const size_t sm = (size_t)XC_WMAX * (8 * NT + 4) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> once{0};
+  if (first_on_device(once))
     XC_CUDA(cudaFuncSetAttribute(spmm_win<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr = true;
-  }
   for (int w0 = 0; w0 < nwins; w0 += 65535) {
     int nw = std::min(65535, nwins - w0);
     dim3 grid((ncols + 8 * NT - 1) / (8 * NT), nw);

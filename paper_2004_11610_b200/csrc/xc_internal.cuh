@@ -109,6 +109,21 @@ struct DevBuf {
 xc_status dev_alloc(DevBuf& b, size_t bytes);
 void dev_free(DevBuf& b);
 
+// One-time per-device setup (function attributes are per device): true the first time it is
+// called for the current device with this mask.
+#include <atomic>
+inline bool first_on_device(std::atomic<unsigned long long>& mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return true;
+  const unsigned long long bit = 1ull << dev;
+  return (mask.fetch_or(bit) & bit) == 0;
+}
+inline int sm_count() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
 // ---------------------------------------------------------------------------
 // FFT engine (fft.cu): batched complex FFT of 2-3-5-smooth length L along the
 // slow axis of a batch-fastest layout, 1 pass (L <= 1024) or 2 passes
