@@ -196,6 +196,8 @@ def dense_apply_rows(kind: Kind, nodes: np.ndarray, X: np.ndarray, ndeg: int) ->
 
 def dense_apply_t(kind: Kind, nodes: np.ndarray, C: np.ndarray) -> np.ndarray:
     """Y[k,b] = sum_j phi_j(x_k) C[j,b] (Y = A^T C; output indexed by node)."""
+    if kind.kind == KIND_EXP:  # complex: Y[k] = sum_j e^{i pi j t_k} C[j] (no conjugate)
+        return entries(kind, nodes, 0, len(nodes)) @ np.asarray(C, dtype=np.complex128)
     C = np.ascontiguousarray(C, dtype=np.float64)
     N, B = C.shape
     Y = np.empty((N, B), dtype=np.float64)
@@ -438,6 +440,18 @@ def apply_input_axis(op: Operator, C: np.ndarray, wt: np.ndarray | None = None) 
     Y[k] += sum over the full spectrum of S[k,q] z'[q], evaluated on the half
     spectrum as c_q Re(S z') with c_0 = c_{L/2} = 1, else 2 (real case).
     """
+    if op.plan.kind.kind == KIND_EXP:  # complex rows: full spectrum, no fold, complex result
+        C = np.asarray(C, dtype=np.complex128)
+        N, B = C.shape
+        Y = np.zeros((N, B), dtype=np.complex128)
+        for blk, S, w in zip(op.plan.blocks, op.S, op.windows):
+            z = np.zeros((blk.L, B), dtype=np.complex128)
+            lo, hi = blk.keep_lo, blk.keep_hi
+            z[lo:hi] = C[lo + blk.m_off:hi + blk.m_off] / w[lo:hi, None]
+            Y += S @ np.fft.ifft(z, axis=0, norm="ortho")       # sum_q S[k,q] (F* z)_q
+        if wt is not None:
+            Y *= wt[:, None]
+        return Y
     C = np.asarray(C, dtype=np.float64)
     N, B = C.shape
     Y = np.zeros((N, B))

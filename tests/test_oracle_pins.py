@@ -490,3 +490,20 @@ def test_exp_keep_all_and_cos_consistency():
     tc = I.cos_nodes(N, 4)
     Xr = I.rhs(N, 2, 3)
     np.testing.assert_allclose(O.dense_apply(EXPK, tc, Xr).real, O.dense_apply(COS, tc, Xr), atol=1e-12)
+
+
+def test_exp_input_axis_closed_forms():
+    """Input axis of the exp kind (Alg. 1 with complex rows): at uniform nodes A^T C = N ifft(C)
+    (A symmetric there); keep-all reproduces the dense transpose; compressed meets 10 eps."""
+    N = 128
+    t = 2.0 * np.arange(N) / N
+    C = I.rhs(N, 3, 1) + 1j * I.rhs(N, 3, 2)
+    np.testing.assert_allclose(O.dense_apply_t(EXPK, t, C), N * np.fft.ifft(C, axis=0), atol=1e-11)
+    op = O.compress(O.make_plan(EXPK, N, 1e-10), t)
+    assert O.rel_l2_cols(O.apply_input_axis(op, C), N * np.fft.ifft(C, axis=0)).max() < 1e-9
+    tr = np.sort(np.random.default_rng(5).random(60) * 2.0)
+    plan = O.make_plan(EXPK, 60, 1e-12)
+    plan.eps1 = 0.0
+    op = O.compress(plan, tr)
+    C2 = I.rhs(60, 2, 3) + 1j * I.rhs(60, 2, 4)
+    assert O.rel_l2_cols(O.apply_input_axis(op, C2), O.dense_apply_t(EXPK, tr, C2)).max() < 1e-13
