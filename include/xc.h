@@ -48,7 +48,8 @@ typedef enum {
                        (chi read as the squared norm, R-4; block form P:280-301)     */
   XC_LAGUERRE = 3,  /* A[j,k] = l_j(x_k) = exp(-x_k/2) L_j(x_k), x_k >= 0 (block form) */
   XC_EXP = 4        /* A[j,k] = exp(i pi j t_k), nodes t_k in [0,2): the non-uniform DFT, complex
-                       (the exp row of Appendix A).  XC_DIR_A only.  X and Y
+                       (the exp row of Appendix A).  Both directions
+                       (XC_DIR_WAT: Y = diag(wts) A^T X, no conjugate).  X and Y
                        are complex in planar form: 2N rows, real parts in rows [0,N), imaginary
                        parts in rows [N,2N), same ld; the full spectrum of L bins is kept.        */
 } xc_kind;

@@ -58,6 +58,13 @@ __global__ void fill_k(const FillItem* fi, const int* start, const int* len, con
     } else if (MODE == FILL_OUT_REAL) { // node R, degree 8 gm + r
       int j = 8 * gm + r;
       if (R < N && j < t) v = P[(int64_t)j * N + R];
+    } else if (MODE == FILL_IN_CC) {    // XC_EXP input axis: gm = 2 G + part, node 8 G + r, bin R/2
+      // Y = sum_q S z'_q: part 0 rows Re Y = S_re z'_re - S_im z'_im, part 1 rows Im Y = S_im z'_re + S_re z'_im
+      const int node = 8 * (gm >> 1) + r, part = gm & 1, q = R >> 1, pl = R & 1;
+      if (node < N && q < H) {
+        const double2 sv = band_cval(node, q, H, start, len, off, vals);
+        v = part == 0 ? (pl == 0 ? sv.x : -sv.y) : (pl == 0 ? sv.y : sv.x);
+      }
     } else if (MODE == FILL_IN_CPLX) {  // node 8 gm + r, bin R/2, (c Re S, -c Im S)
       int node = 8 * gm + r, q = R >> 1;
       if (node < N && q < H) {
@@ -83,6 +90,7 @@ xc_status fill_tiles(int mode, const FillItem* fi, int n, const int* start, cons
     case FILL_OUT_REAL: fill_k<FILL_OUT_REAL><<<n, 128, 0, st>>>(fi, start, len, off, vals, P, t, N, H, tiles); break;
     case FILL_IN_CPLX: fill_k<FILL_IN_CPLX><<<n, 128, 0, st>>>(fi, start, len, off, vals, P, t, N, H, tiles); break;
     case FILL_OUT_CC: fill_k<FILL_OUT_CC><<<n, 128, 0, st>>>(fi, start, len, off, vals, P, t, N, H, tiles); break;
+    case FILL_IN_CC: fill_k<FILL_IN_CC><<<n, 128, 0, st>>>(fi, start, len, off, vals, P, t, N, H, tiles); break;
     default: fill_k<FILL_IN_REAL><<<n, 128, 0, st>>>(fi, start, len, off, vals, P, t, N, H, tiles); break;
   }
   XC_CUDA(cudaGetLastError());

@@ -17,7 +17,7 @@ struct FillItem {
                 // group must not count a row of its neighbouring chunk twice)
 };
 
-enum { FILL_OUT_CPLX = 0, FILL_OUT_REAL = 1, FILL_IN_CPLX = 2, FILL_IN_REAL = 3, FILL_OUT_CC = 4 };
+enum { FILL_OUT_CPLX = 0, FILL_OUT_REAL = 1, FILL_IN_CPLX = 2, FILL_IN_REAL = 3, FILL_OUT_CC = 4, FILL_IN_CC = 5 };
 
 xc_status fill_tiles(int mode, const FillItem* fi, int n, const int* start, const int* len, const int64_t* off,
                      const double2* vals, const double* P, int t, int N, int H, double* tiles, cudaStream_t st);

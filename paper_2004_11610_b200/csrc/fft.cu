@@ -155,6 +155,12 @@ template <int PRO>
 __device__ __forceinline__ double2 pro_load(const FftIO& io, int n, int col) {
   if (PRO == PRO_PLAIN) {
     return io.src[(int64_t)n * io.lds + col];
+  } else if (PRO == PRO_XCPLX) {  // XC_EXP: planar complex input (rows N.. imaginary), pad + W^{-1}
+    if (n >= io.keep_lo && n < io.keep_hi) {
+      const int64_t o = (int64_t)(n + io.m_off) * io.ldx + col;
+      return make_double2(io.X[o] * io.winv[n], io.X[io.xpl + o] * io.winv[n]);
+    }
+    return make_double2(0.0, 0.0);
   } else {  // PRO_XREAL: pad + W^{-1} (Fe1 / Fe3)
     if (n >= io.keep_lo && n < io.keep_hi)
       return make_double2(io.X[(int64_t)(n + io.m_off) * io.ldx + col] * io.winv[n], 0.0);
@@ -197,7 +203,7 @@ __global__ void __launch_bounds__(256, 3) fft_pass(PassArgs a, FftIO io) {
   const bool valid = sub < a.S && col < a.ncol;
 
   // ---- load (prologue) ----
-  if (PRO == PRO_XREAL && a.stage != 1) {
+  if ((PRO == PRO_XREAL || PRO == PRO_XCPLX) && a.stage != 1) {
     // real input scaled by W^{-1}: through registers
     for (int e = e0; e < a.R; e += 4 * estep) {
       double2 v[4];
@@ -313,6 +319,7 @@ xc_status dispatch(FftPro pro, FftEpi epi, const PassArgs& a, const FftIO& io, c
   // pass-1-of-2 uses only the prologue, pass-2-of-2 only the epilogue
   if (a.stage == 0) {
     if (pro == PRO_PLAIN) return launch_pass<PRO_PLAIN, EPI_PLAIN, SIG>(a, io, st);
+    if (pro == PRO_XCPLX) return launch_pass<PRO_XCPLX, EPI_PLAIN, SIG>(a, io, st);
     return launch_pass<PRO_XREAL, EPI_PLAIN, SIG>(a, io, st);
   }
   if (a.stage == 1) {
@@ -327,6 +334,7 @@ xc_status dispatch(FftPro pro, FftEpi epi, const PassArgs& a, const FftIO& io, c
   XC_CASE(PRO_PLAIN, EPI_CY)
   XC_CASE(PRO_XREAL, EPI_PLAIN)
   XC_CASE(PRO_XREAL, EPI_ZPLANES)
+  XC_CASE(PRO_XCPLX, EPI_ZPLANES)
 #undef XC_CASE
   xc_set_error("fft: bad prologue/epilogue");
   return XC_EINVAL;
@@ -451,7 +459,7 @@ xc_status fft_run(const FftPlan& p, int sigma, FftPro pro, FftEpi epi, const Fft
   a.ncol = ncol;
   a.scratch = scratch;
   a.twL = p.twL;
-  if (pro != PRO_PLAIN && pro != PRO_XREAL) {
+  if (pro != PRO_PLAIN && pro != PRO_XREAL && pro != PRO_XCPLX) {
     xc_set_error("fft_run: the output-axis inverse runs in c2r_run");
     return XC_EINVAL;
   }

@@ -102,6 +102,7 @@ struct xc_op {
   int nitemsW = 0, nwinsW = 0;
   int64_t rowsW = 0, tilesW_n = 0, mtstepsW = 0;
   DevBuf nodeg_base, nodeg_nch;
+  DevBuf nodeg_base_im;  // XC_EXP: partial rows of the imaginary parts per node group
   // workspace
   int64_t ws_B = 0;
   DevBuf partA, partW, scratch, zpl, Xh, Yh;
@@ -429,7 +430,8 @@ xc_status upload_and_fill(xc_op* h, ItemSet& S, bool input_axis, DevBuf& d_items
     XC_TRY(upload(dfill, part));
     if (fam >= 0) {
       BlockData& b = h->blocks[fam];
-      XC_TRY(fill_tiles(input_axis ? FILL_IN_CPLX : (h->kind == XC_EXP ? FILL_OUT_CC : FILL_OUT_CPLX),
+      XC_TRY(fill_tiles(input_axis ? (h->kind == XC_EXP ? FILL_IN_CC : FILL_IN_CPLX)
+                                   : (h->kind == XC_EXP ? FILL_OUT_CC : FILL_OUT_CPLX),
                         (FillItem*)dfill.p, (int)part.size(),
                         (int*)b.start.p, (int*)b.len.p, (int64_t*)b.off.p, (double2*)b.vals.p, nullptr, 0, N, b.H,
                         (double*)d_tiles.p, st));
@@ -603,7 +605,61 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
 // in B rows 2q (re plane) and 2q+1 (im plane) of that block's z' planes; split into bin
 // chunks.  Items of one node group are allocated consecutive output rows and reduced (times
 // the weights) in fixed order.
+// XC_EXP input axis (Alg. 1 with complex rows, R-20): node group G = nodes [8G, 8G+8), bins of
+// the full circular spectrum in chunks of QC; per (G, chunk) two M-tiles over the same B rows
+// (2q, 2q+1: the z' planes) -- the real and the imaginary parts of Y -- always paired.  Partial
+// rows of G: real parts at base[G] + 8c, imaginary parts at base_im[G] + 8c, c < nch[G].
+xc_status build_input_axis_cc(xc_op* h, cudaStream_t st) {
+  const int N = (int)h->N;
+  const int NG = (N + 7) / 8;
+  BlockData& b = h->blocks[0];  // the exp kind has one block and no tail
+  const int nch_bins = (b.H + QC - 1) / QC;
+  std::vector<int> gnch(NG, 0);
+  std::vector<int64_t> gbase(NG, 0), gbase_im(NG, 0);
+  struct Rng {
+    int G, c, q0, q1;
+  };
+  std::vector<Rng> rng;
+  std::vector<int> lo(nch_bins), hi(nch_bins);
+  for (int G = 0; G < NG; ++G) {
+    std::fill(lo.begin(), lo.end(), b.H);
+    std::fill(hi.begin(), hi.end(), -1);
+    for (int k = 8 * G; k < std::min(N, 8 * G + 8); ++k)
+      for (int j = 0; j < b.h_len[k]; ++j) {
+        const int q = (b.h_start[k] + j) % b.H, c = q / QC;
+        lo[c] = std::min(lo[c], q);
+        hi[c] = std::max(hi[c], q);
+      }
+    for (int c = 0; c < nch_bins; ++c)
+      if (hi[c] >= lo[c]) {
+        rng.push_back(Rng{G, c, lo[c] / 2 * 2, (hi[c] + 2) / 2 * 2});
+        gnch[G]++;
+      }
+  }
+  int64_t rows = 0;
+  for (int G = 0; G < NG; ++G) {
+    gbase[G] = rows;
+    gbase_im[G] = rows + 8LL * gnch[G];
+    rows += 16LL * gnch[G];
+  }
+  std::vector<int> used(NG, 0);
+  std::vector<MTile> mt;
+  for (auto& r : rng) {
+    const int u = used[r.G]++;
+    mt.push_back(MTile{0, 2 * r.G + 0, r.c, 2 * r.q0, 2 * r.q1, gbase[r.G] + 8LL * u, 0});
+    mt.push_back(MTile{0, 2 * r.G + 1, r.c, 2 * r.q0, 2 * r.q1, gbase_im[r.G] + 8LL * u, 0});
+  }
+  ItemSet S;
+  for (size_t i = 0; i + 1 < mt.size(); i += 2) emit_item(mt[i], &mt[i + 1], 0, S);  // re / im share B rows
+  XC_TRY(upload(h->nodeg_base, gbase));
+  XC_TRY(upload(h->nodeg_base_im, gbase_im));
+  XC_TRY(upload(h->nodeg_nch, gnch));
+  h->rowsW = rows;
+  return upload_and_fill(h, S, true, h->itemsW, h->winsW, h->tilesW, h->nitemsW, h->nwinsW, h->tilesW_n, st);
+}
+
 xc_status build_input_axis(xc_op* h, cudaStream_t st) {
+  if (h->kind == XC_EXP) return build_input_axis_cc(h, st);
   const int N = (int)h->N;
   const int NG = (N + 7) / 8;
   const int nb = (int)h->blocks.size();
@@ -699,10 +755,6 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
   if (kind == XC_JACOBI && !(p.alpha > -1.0 && p.beta > -1.0)) {
     xc_set_error("Jacobi alpha, beta must be > -1");
     return XC_EINVAL;
-  }
-  if (kind == XC_EXP && (h->dirs & XC_DIR_WAT)) {
-    xc_set_error("XC_EXP: only XC_DIR_A is implemented");
-    return XC_EUNSUPPORTED;
   }
   if ((h->dirs & XC_DIR_WAT) && !p.weights) {
     xc_set_error("XC_DIR_WAT needs weights");
@@ -930,6 +982,39 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
     return mark(3);
   }
   // XC_DIR_WAT
+  if (h->kind == XC_EXP) {
+    BlockData& b = h->blocks[0];
+    double* zre = (double*)h->zpl.p + h->zoff[0];
+    double* zim = zre + (int64_t)b.H * Bp;
+    FftIO io{};
+    io.X = X;
+    io.ldx = ldx;
+    io.xpl = (int64_t)N * ldx;  // planar complex input
+    io.winv = (const double*)b.winv.p;
+    io.keep_lo = b.keep_lo;
+    io.keep_hi = b.keep_hi;
+    io.m_off = b.m_off;
+    io.zre = zre;
+    io.zim = zim;
+    io.ldz = Bp;
+    io.H = b.H;
+    io.scale = 1.0 / sqrt((double)b.L);
+    XC_TRY(fft_run(b.fft, +1, PRO_XCPLX, EPI_ZPLANES, io, (int)B, (double2*)h->scratch.p, st));
+    SpmmSrcs s{};
+    s.re[0] = zre;
+    s.im[0] = zim;
+    s.nrows[0] = b.H;
+    s.ld[0] = Bp;
+    XC_TRY(mark(1));
+    XC_TRY(spmm_run((const SpmmWin*)h->winsW.p, h->nwinsW, (const SpmmItem*)h->itemsW.p,
+                    (const double*)h->tilesW.p, s, (double*)h->partW.p, Bp, (int)B, st));
+    XC_TRY(mark(2));
+    XC_TRY(reduce_rows8((const double*)h->partW.p, Bp, (const int64_t*)h->nodeg_base.p, (const int*)h->nodeg_nch.p,
+                        N, (const double*)h->wt.p, Y, ldy, (int)B, st));
+    XC_TRY(reduce_rows8((const double*)h->partW.p, Bp, (const int64_t*)h->nodeg_base_im.p,
+                        (const int*)h->nodeg_nch.p, N, (const double*)h->wt.p, Y + (int64_t)N * ldy, ldy, (int)B, st));
+    return mark(3);
+  }
   SpmmSrcs s{};
   const int nb = (int)h->blocks.size();
   for (int i = 0; i < nb; ++i) {
@@ -993,7 +1078,7 @@ void destroy_impl(xc_op* h) {
     dev_free(b.grp_base); dev_free(b.grp_nch);
   }
   DevBuf* all[] = {&h->nodes, &h->wt, &h->tailP, &h->itemsA, &h->tilesA, &h->winsA, &h->tail_base, &h->tail_nch,
-                   &h->itemsW, &h->tilesW, &h->winsW, &h->nodeg_base, &h->nodeg_nch, &h->partA, &h->partW,
+                   &h->itemsW, &h->tilesW, &h->winsW, &h->nodeg_base, &h->nodeg_nch, &h->nodeg_base_im, &h->partA, &h->partW,
                    &h->scratch, &h->zpl, &h->Xh, &h->Yh, &h->xsend, &h->xrecv, &h->djtab};
   for (DevBuf* b : all) dev_free(*b);
 }

@@ -129,7 +129,7 @@ inline int sm_count() {
 // slow axis of a batch-fastest layout, 1 pass (L <= 1024) or 2 passes
 // (four-step, L = L1 * L2) through an L2-resident scratch.
 // ---------------------------------------------------------------------------
-enum FftPro { PRO_PLAIN = 0, PRO_XREAL = 2 };
+enum FftPro { PRO_PLAIN = 0, PRO_XREAL = 2, PRO_XCPLX = 3 };  // PRO_XCPLX: XC_EXP input axis
 enum FftEpi { EPI_PLAIN = 0, EPI_ZPLANES = 2, EPI_CY = 3 };  // EPI_CY: XC_EXP output (planar, W^{-1}, Fe2)
 
 struct FftPlan {
@@ -149,7 +149,8 @@ struct FftIO {
   const double2* twh = nullptr; int M = 0;                 // c2r_run: e^{+2 pi i n / (2M)}, n < M
   int H = 0;
   const double* X = nullptr; int64_t ldx = 0;              // PRO_XREAL
-  const double* winv = nullptr;                            // 1/w_p (PRO_XREAL)
+  const double* winv = nullptr;                            // 1/w_p (PRO_XREAL, PRO_XCPLX)
+  int64_t xpl = 0;                                         // PRO_XCPLX: offset of the imaginary plane of X
   int keep_lo = 0, keep_hi = 0, m_off = 0;
   // epilogue destinations
   double2* dst = nullptr; int64_t ldd = 0; int kmax = 0;    // EPI_PLAIN: bins [0,kmax)

@@ -229,12 +229,12 @@ class Transform:
                                   ctypes.c_void_p(out.data_ptr()), out.stride(0), B, ctypes.c_void_p(st)))
         return out
 
-    def apply_complex(self, Xc, stream=None):
+    def apply_complex(self, Xc, direction: int = XC_DIR_A, stream=None):
         """XC_EXP with a complex128 CUDA tensor (N x B): marshalled to and from the planar layout
         of the C ABI (real rows, then imaginary rows)."""
         import torch
         Xp = torch.cat([Xc.real, Xc.imag]).contiguous()
-        Yp = self.apply(Xp, XC_DIR_A, stream=stream)
+        Yp = self.apply(Xp, direction, stream=stream)
         return torch.complex(Yp[:self.N], Yp[self.N:])
 
     def apply_host(self, X: np.ndarray, direction: int = XC_DIR_A, out: np.ndarray | None = None, stream=None):

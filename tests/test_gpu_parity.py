@@ -479,8 +479,30 @@ def test_exp_uniform_nodes_is_inverse_dft():
     T = xc.Transform(xc.XC_EXP, t, eps)
     Y = T.apply_complex(torch.from_numpy(X).cuda()).cpu().numpy()
     assert O.rel_l2_cols(Y, N * np.fft.ifft(X, axis=0)).max() <= 10 * eps
-    with pytest.raises(xc.XcError, match="XC_EUNSUPPORTED"):
-        xc.Transform(xc.XC_EXP, t, eps, dirs=xc.XC_DIR_A | xc.XC_DIR_WAT, weights=np.ones(N))
+    T.close()
+    # input axis (Alg. 1, complex): A^T C = N ifft(C) at uniform nodes (A symmetric there)
+    T = xc.Transform(xc.XC_EXP, t, eps, dirs=xc.XC_DIR_A | xc.XC_DIR_WAT, weights=np.ones(N))
+    Yw = T.apply_complex(torch.from_numpy(X).cuda(), xc.XC_DIR_WAT).cpu().numpy()
+    assert O.rel_l2_cols(Yw, N * np.fft.ifft(X, axis=0)).max() <= 10 * eps
+    T.close()
+
+
+@pytest.mark.parametrize("case", EXP_CASES, ids=[c[0] for c in EXP_CASES])
+def test_exp_kind_input_axis_parity(case):
+    """NEXT-3 both directions: XC_DIR_WAT of the exp kind, Y = diag(w) A^T C with complex rows
+    (full spectrum, no fold), vs the oracle's Alg. 1 (1e-12) and the dense transpose (10 eps)."""
+    xc = _xc()
+    name, N, B, eps, seed = case
+    t = I.exp_nodes(N, seed)
+    C = I.complex_rhs(N, B, seed + 50)
+    w = 0.5 + np.random.default_rng(seed).random(N)
+    T = xc.Transform(xc.XC_EXP, t, eps, dirs=xc.XC_DIR_A | xc.XC_DIR_WAT, weights=w)
+    Y = T.apply_complex(torch.from_numpy(C).cuda(), xc.XC_DIR_WAT).cpu().numpy()
+    op = O.compress(O.make_plan(O.Kind(O.KIND_EXP), N, eps), t)
+    assert O.rel_l2_cols(Y, O.apply_input_axis(op, C, w)).max() <= 1e-12, name
+    cols = np.arange(min(B, 8))
+    Yd = w[:, None] * O.dense_apply_t(O.Kind(O.KIND_EXP), t, C[:, cols])
+    assert O.rel_l2_cols(Y[:, cols], Yd).max() <= 10 * eps, name
     T.close()
 
 
