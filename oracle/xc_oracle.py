@@ -37,7 +37,12 @@ import scipy.sparse as sp
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = None
 
-KIND_COS, KIND_JACOBI, KIND_LAGUERRE, KIND_EXP = 1, 2, 3, 4
+KIND_COS, KIND_JACOBI, KIND_LAGUERRE, KIND_EXP, KIND_LAGSPEC = 1, 2, 3, 4, 5
+
+
+def is_complex(kind) -> bool:
+    """Complex rows (full spectrum of L bins, complex X and Y): kinds EXP and LAGSPEC."""
+    return kind.kind in (KIND_EXP, KIND_LAGSPEC)
 
 
 def build_lib() -> str:
@@ -88,10 +93,14 @@ class Kind:
                    (the exp row of Appendix A, Eq. A.4 / y3; NEXT-3)
     kind JACOBI:   phi_j(x) = p_j^(alpha,beta)(x), orthonormal on [-1,1] (R-4)
     kind LAGUERRE: phi_j(x) = exp(-x/2) L_j(x), x >= 0
+    kind LAGSPEC:  phi_m(k) = (-eta/2 - i k)^m / (eta/2 - i k)^(m+1): the matrix C^T of the
+                   spectral Laguerre forward transform V = C^T F (Eq. main_formula2 / lag_matrix,
+                   P:395-412); nodes = Fourier frequencies k_j (any real, ascending); complex
     """
     kind: int
     alpha: float = 0.0
     beta: float = 0.0
+    eta: float = 0.0   # LAGSPEC only: the Laguerre scale eta > 0 (P:395)
 
 
 def entries(kind: Kind, nodes: np.ndarray, m0: int, m1: int, m_off: int = 0) -> np.ndarray:
@@ -104,6 +113,15 @@ def entries(kind: Kind, nodes: np.ndarray, m0: int, m1: int, m_off: int = 0) -> 
         lib.orc_cos_entries(_p(x), x.size, m0, m1, m_off, _p(out))
         lib.orc_sin_entries(_p(x), x.size, m0, m1, m_off, _p(im))
         return out + 1j * im
+    if kind.kind == KIND_LAGSPEC:
+        # the power form of Eq. (main_formula2), evaluated as written in 80-bit complex
+        # arithmetic and rounded once; m < 0 (the left extra components) by the same formula
+        a = np.longdouble(kind.eta) / 2
+        kk = x.astype(np.longdouble)
+        den = a - 1j * kk
+        r = (-a - 1j * kk) / den
+        m = np.arange(m0 + m_off, m1 + m_off).astype(np.clongdouble)
+        return (np.power(r[:, None], m[None, :]) / den[:, None]).astype(np.complex128)
     if kind.kind == KIND_COS:
         lib.orc_cos_entries(_p(x), x.size, m0, m1, m_off, _p(out))
     elif kind.kind == KIND_JACOBI:
@@ -169,10 +187,11 @@ def gauss_rule(kind: Kind, N: int, newton: int = 2):
 # ---------------------------------------------------------------------------
 # Plain definition: the dense product (the paper's "direct method")
 # ---------------------------------------------------------------------------
-def dense_apply(kind: Kind, nodes: np.ndarray, X: np.ndarray) -> np.ndarray:
-    """Y[j,b] = sum_k phi_j(x_k) X[k,b], j < N (Y = A X; output indexed by degree)."""
-    if kind.kind == KIND_EXP:  # complex: the entries matrix (exactly reduced), a plain matmul
-        A = entries(kind, nodes, 0, len(nodes)).T                # A[j, k] = e^{i pi j t_k}
+def dense_apply(kind: Kind, nodes: np.ndarray, X: np.ndarray, M: int | None = None) -> np.ndarray:
+    """Y[j,b] = sum_k phi_j(x_k) X[k,b], j < M (Y = A X; output indexed by degree; M = N unless
+    given: rectangular for the complex kinds)."""
+    if is_complex(kind):  # complex: the entries matrix (rounded once), a plain matmul
+        A = entries(kind, nodes, 0, len(nodes) if M is None else M).T   # A[j, k] = phi_j(x_k)
         return A @ np.asarray(X, dtype=np.complex128)
     X = np.ascontiguousarray(X, dtype=np.float64)
     N, B = X.shape
@@ -195,9 +214,9 @@ def dense_apply_rows(kind: Kind, nodes: np.ndarray, X: np.ndarray, ndeg: int) ->
 
 
 def dense_apply_t(kind: Kind, nodes: np.ndarray, C: np.ndarray) -> np.ndarray:
-    """Y[k,b] = sum_j phi_j(x_k) C[j,b] (Y = A^T C; output indexed by node)."""
-    if kind.kind == KIND_EXP:  # complex: Y[k] = sum_j e^{i pi j t_k} C[j] (no conjugate)
-        return entries(kind, nodes, 0, len(nodes)) @ np.asarray(C, dtype=np.complex128)
+    """Y[k,b] = sum_j phi_j(x_k) C[j,b] (Y = A^T C; output indexed by node; j < rows of C)."""
+    if is_complex(kind):  # complex: Y[k] = sum_j phi_j(x_k) C[j] (no conjugate)
+        return entries(kind, nodes, 0, C.shape[0]) @ np.asarray(C, dtype=np.complex128)
     C = np.ascontiguousarray(C, dtype=np.float64)
     N, B = C.shape
     Y = np.empty((N, B), dtype=np.float64)
@@ -307,12 +326,17 @@ class Block:
 @dataclass
 class Plan:
     kind: Kind
-    N: int
+    N: int          # nodes (columns of A)
     eps1: float
     eps2: float
     zeta: float
     blocks: list = field(default_factory=list)
     tail: int = 0   # dense degrees [0, tail)
+    M: int = 0      # degrees (rows of A); 0 = N (square)
+
+    @property
+    def rows(self) -> int:
+        return self.M if self.M > 0 else self.N
 
 
 def minimal_s(zeta: float, span: int, eps2: float, two_sided: bool) -> int:
@@ -328,18 +352,23 @@ def minimal_s(zeta: float, span: int, eps2: float, two_sided: bool) -> int:
 
 
 def make_plan(kind: Kind, N: int, eps: float, eps1: float | None = None, eps2: float | None = None,
-              dense_cutoff: int = 32) -> Plan:
-    """Block chain (R-2, R-3, R-8, R-9): see DESIGN.md."""
+              dense_cutoff: int = 32, M: int | None = None) -> Plan:
+    """Block chain (R-2, R-3, R-8, R-9): see DESIGN.md.  M: degrees (rows) when they differ from
+    the N nodes -- complex kinds only (the C^T of P:412 is (M+1) x (Nx+1), R-21)."""
     eps1 = eps if eps1 is None else eps1
     eps2 = 1e-2 if eps2 is None else eps2
     zeta = solve_zeta(eps1)
     plan = Plan(kind, N, eps1, eps2, zeta)
-    if kind.kind in (KIND_COS, KIND_EXP):
-        # trig form: extra components on both sides (Alg. 2, P:208-222)
-        s0 = minimal_s(zeta, N, eps2, two_sided=True)
-        L = smooth5_even_at_least(N + 2 * s0)
-        s = (L - N) // 2
-        plan.blocks.append(Block(L, -s, s, s + N))
+    if M is not None and M != N:
+        assert is_complex(kind), "rectangular operators: complex kinds only"
+        plan.M = M
+    if kind.kind in (KIND_COS, KIND_EXP, KIND_LAGSPEC):
+        # trig form: extra components on both sides (Alg. 2, P:208-222); span = the degrees
+        R = plan.rows
+        s0 = minimal_s(zeta, R, eps2, two_sided=True)
+        L = smooth5_even_at_least(R + 2 * s0)
+        s = (L - R) // 2
+        plan.blocks.append(Block(L, -s, s, s + R))
         plan.tail = 0
         return plan
     e = N
@@ -365,7 +394,7 @@ def node_spectra(plan: Plan, blk: Block, nodes: np.ndarray) -> np.ndarray:
     """
     w = kaiser(plan.zeta, blk.L - 1)
     E = entries(plan.kind, nodes, 0, blk.L, blk.m_off)          # E[k, p] = phi_{p+m_off}(x_k)
-    if plan.kind.kind == KIND_EXP:                              # complex rows: the full spectrum
+    if is_complex(plan.kind):                                   # complex rows: the full spectrum
         return np.fft.fft(E * w[None, :], axis=1, norm="ortho")
     S = np.fft.rfft(E * w[None, :], axis=1, norm="ortho")      # e^{-2 pi i p q / L} / sqrt(L)
     S[:, 0] = S[:, 0].real
@@ -411,9 +440,9 @@ def apply_output_axis(op: Operator, X: np.ndarray) -> np.ndarray:
     output), Y[kept] = v[kept] / w[kept]; the extra positions are discarded
     (Fe2).  Tail degrees by the direct method.
     """
-    if op.plan.kind.kind == KIND_EXP:                           # complex input and output
+    if is_complex(op.plan.kind):                                # complex input and output
         X = np.asarray(X, dtype=np.complex128)
-        Y = np.zeros(X.shape, dtype=np.complex128)
+        Y = np.zeros((op.plan.rows, X.shape[1]), dtype=np.complex128)
         for blk, S, w in zip(op.plan.blocks, op.S, op.windows):
             u = S.T @ X                                         # (L x B): full spectrum
             v = np.fft.ifft(u, axis=0, norm="ortho")            # e^{+2 pi i p q / L} / sqrt(L)
@@ -440,10 +469,10 @@ def apply_input_axis(op: Operator, C: np.ndarray, wt: np.ndarray | None = None) 
     Y[k] += sum over the full spectrum of S[k,q] z'[q], evaluated on the half
     spectrum as c_q Re(S z') with c_0 = c_{L/2} = 1, else 2 (real case).
     """
-    if op.plan.kind.kind == KIND_EXP:  # complex rows: full spectrum, no fold, complex result
+    if is_complex(op.plan.kind):  # complex rows: full spectrum, no fold, complex result
         C = np.asarray(C, dtype=np.complex128)
-        N, B = C.shape
-        Y = np.zeros((N, B), dtype=np.complex128)
+        B = C.shape[1]
+        Y = np.zeros((op.plan.N, B), dtype=np.complex128)
         for blk, S, w in zip(op.plan.blocks, op.S, op.windows):
             z = np.zeros((blk.L, B), dtype=np.complex128)
             lo, hi = blk.keep_lo, blk.keep_hi

@@ -11,7 +11,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-KIND_COS, KIND_JACOBI, KIND_LAGUERRE, KIND_EXP = 1, 2, 3, 4
+KIND_COS, KIND_JACOBI, KIND_LAGUERRE, KIND_EXP, KIND_LAGSPEC = 1, 2, 3, 4, 5
 
 
 @dataclass(frozen=True)
@@ -26,6 +26,9 @@ class Config:
     beta: float = 0.0
     dirs: tuple = ("A",)
     eps2: float = 1e-2
+    M: int = 0          # degrees (rows) when != N (complex kinds); 0 = square
+    eta: float = 0.0    # LAGSPEC: Laguerre scale eta
+    T: float = 0.0      # LAGSPEC: Fourier period, frequencies k_j = 2 pi j / T
 
 
 CONFIGS = {
@@ -38,6 +41,9 @@ CONFIGS = {
     # NEXT-3: the complex exponential kind, non-uniform DFT e^{i pi j t_k}, t_k in [0,2);
     # not a BASELINE config -- a parity / measurement case of the widened path
     "c6": Config("c6_nonexp_4096", KIND_EXP, 4096, 64, 1e-10, 6),
+    # NEXT-3 second half: the spectral Laguerre forward V = C^T F at the sizes of the paper's
+    # Fig. lag_row: C^T is 649 x 501, eta = 2500, k_j = 2 pi j / T, T = 4 s
+    "c7": Config("c7_lagspec_649x501", KIND_LAGSPEC, 501, 64, 1e-10, 7, M=649, eta=2500.0, T=4.0),
 }
 
 
@@ -51,6 +57,11 @@ def exp_nodes(N: int, seed: int) -> np.ndarray:
     """Non-uniform DFT nodes t_k = sort(U[0,2)) (theta_k = pi t_k on the whole circle)."""
     rng = np.random.default_rng(seed)
     return 2.0 * np.sort(rng.random(N))
+
+
+def lagspec_freqs(N: int, T: float) -> np.ndarray:
+    """Fourier frequencies k_j = 2 pi j / T, j = 0..N-1 (Fig. lag_row caption); no draw."""
+    return 2.0 * np.pi * np.arange(N, dtype=np.float64) / T
 
 
 def complex_rhs(N: int, B: int, seed: int, skip_nodes: bool = True) -> np.ndarray:
@@ -81,6 +92,8 @@ def config_rhs(cfg: Config, B: int | None = None) -> np.ndarray:
     B = cfg.B if B is None else B
     if cfg.kind == KIND_EXP:
         return complex_rhs(cfg.N, B, cfg.seed)
+    if cfg.kind == KIND_LAGSPEC:  # Fourier coefficients F~ (no node draw: the k_j are a grid)
+        return complex_rhs(cfg.N, B, cfg.seed, skip_nodes=False)
     if cfg.kind == KIND_COS:
         return rhs(cfg.N, B, cfg.seed, skip_cos_nodes=True)
     if cfg.kind == KIND_LAGUERRE:

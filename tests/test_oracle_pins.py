@@ -507,3 +507,100 @@ def test_exp_input_axis_closed_forms():
     op = O.compress(plan, tr)
     C2 = I.rhs(60, 2, 3) + 1j * I.rhs(60, 2, 4)
     assert O.rel_l2_cols(O.apply_input_axis(op, C2), O.dense_apply_t(EXPK, tr, C2)).max() < 1e-13
+
+
+# --------------------------------------------------------------------------- rectangular / LAGSPEC
+def test_exp_rectangular_uniform_nodes():
+    """Rectangular exp operator (M degrees x N nodes, R-21): at t_k = 2k/N, A[m,k] = e^{2 pi i mk/N}
+    is periodic in m, so A X = N ifft(X)[m mod N] and A^T C = N ifft(sum of C's rows folded mod N)."""
+    N = 128
+    t = 2.0 * np.arange(N) / N
+    X = I.rhs(N, 3, 4) + 1j * I.rhs(N, 3, 5)
+    for M in (77, 200):
+        ref = (N * np.fft.ifft(X, axis=0))[np.arange(M) % N]
+        np.testing.assert_allclose(O.dense_apply(EXPK, t, X, M=M), ref, atol=1e-11)
+        op = O.compress(O.make_plan(EXPK, N, 1e-10, M=M), t)
+        assert op.plan.blocks[0].keep_hi - op.plan.blocks[0].keep_lo == M
+        assert O.rel_l2_cols(O.apply_output_axis(op, X), ref).max() < 1e-9
+        C = I.rhs(M, 3, 6) + 1j * I.rhs(M, 3, 7)
+        Cf = np.zeros((N, 3), dtype=np.complex128)
+        np.add.at(Cf, np.arange(M) % N, C)
+        reft = N * np.fft.ifft(Cf, axis=0)
+        np.testing.assert_allclose(O.dense_apply_t(EXPK, t, C), reft, atol=1e-10)
+        assert O.rel_l2_cols(O.apply_input_axis(op, C), reft).max() < 1e-9
+
+
+def _lagk(eta):
+    return O.Kind(O.KIND_LAGSPEC, eta=eta)
+
+
+def test_lagspec_entries_vs_mpmath_power_form():
+    """C^T[m,j] = (-eta/2 - i k_j)^m / (eta/2 - i k_j)^(m+1) (Eq. main_formula2) in 40-digit
+    arithmetic, including m < 0 (the left extra components of the trig form)."""
+    mp.mp.dps = 40
+    eta = 2500.0
+    k = I.lagspec_freqs(501, 4.0)[[0, 1, 7, 250, 500]]
+    E = O.entries(_lagk(eta), k, -300, 700)
+    for j, kj in enumerate(k):
+        for m in (-300, -1, 0, 1, 5, 345, 699):
+            ref = mp.mpc(-eta / 2, -kj) ** m / mp.mpc(eta / 2, -kj) ** (m + 1)
+            assert abs(complex(E[j, m + 300]) - complex(ref)) <= 2e-16 * abs(complex(ref))
+
+
+def test_lagspec_entries_are_laplace_transform_of_laguerre_functions():
+    """Where the formula comes from: v_m = int_0^inf e^{i k t} l_m(eta t) dt for one
+    Fourier mode, l_m(x) = e^{-x/2} L_m(x).  scipy quad (Fourier weight) with scipy's Laguerre
+    polynomials -- an independent route to every entry."""
+    import scipy.integrate as si
+    eta = 3.0
+    k = np.array([0.0, 0.7, 2.5])
+    E = O.entries(_lagk(eta), k, 0, 6)
+    for j, kj in enumerate(k):
+        for m in range(6):
+            f = lambda x, m=m: math.exp(-eta * x / 2) * scipy.special.eval_laguerre(m, eta * x)
+            # e^{-eta x / 2} < 1e-24 beyond x = 40: the finite interval is the integral
+            re = si.quad(lambda x: f(x) * math.cos(kj * x), 0, 40, epsabs=1e-15, epsrel=1e-13, limit=500)[0]
+            im = si.quad(lambda x: f(x) * math.sin(kj * x), 0, 40, epsabs=1e-15, epsrel=1e-13, limit=500)[0]
+            assert abs(E[j, m] - (re + 1j * im)) < 1e-10
+
+
+def test_lagspec_phase_reading():
+    """Reading R-21 of P:402-405: the ratio r_j = (-eta/2 - i k_j)/(eta/2 - i k_j) is unimodular with
+    argument pi + 2 atan(2 k_j / eta), so C^T[m,j] = e^{i m theta_j} / (eta/2 - i k_j): the exp kind at
+    t_j = 1 + (2/pi) atan(2 k_j/eta) in (0, 2), ascending in k_j, scaled per node.  The printed
+    i exp(-i m phi) / (eta/2 - i k_j) differs from the power form already at m = 0 (factor i)."""
+    eta = 2500.0
+    k = I.lagspec_freqs(501, 4.0)
+    E = O.entries(_lagk(eta), k, -5, 40)
+    d = 1.0 / (eta / 2 - 1j * k)
+    t = 1.0 + (2.0 / np.pi) * np.arctan(2.0 * k / eta)
+    assert np.all(np.diff(t) > 0) and t[0] == 1.0 and t[-1] < 2.0
+    Ee = O.entries(EXPK, t, -5, 40) * d[:, None]
+    # t_j rounded to fp64: phase error <= pi |m| 2 * 2^-53 (|m| <= 40 here)
+    np.testing.assert_allclose(E, Ee, rtol=0, atol=(np.pi * 40 * 2 ** -52 + 4e-16) * np.abs(d).max())
+    printed = 1j * d                                        # the printed form at m = 0
+    assert np.abs(printed - E[:, 5]).min() > 0.5 * np.abs(d).min()
+
+
+@pytest.mark.parametrize("eps", [1e-10, 1e-12])
+def test_lagspec_fig_lag_row_compressed(eps):
+    """The paper's Fig. lag_row operator: C^T is 649 x 501, eta = 2500, k_j = 2 pi j/T,
+    T = 4.  Compressed (Alg. 2 with complex rows, both directions) vs the dense C^T within 10 eps;
+    keep-all within 1e-13."""
+    cfg = I.CONFIGS["c7"]
+    k = I.lagspec_freqs(cfg.N, cfg.T)
+    kind = _lagk(cfg.eta)
+    F = I.config_rhs(cfg, 4)
+    op = O.compress(O.make_plan(kind, cfg.N, eps, M=cfg.M), k)
+    V = O.apply_output_axis(op, F)
+    assert V.shape == (cfg.M, 4)
+    assert O.rel_l2_cols(V, O.dense_apply(kind, k, F, M=cfg.M)).max() < 10 * eps
+    G = I.complex_rhs(cfg.M, 4, 70, skip_nodes=False)
+    Yt = O.apply_input_axis(op, G)
+    assert Yt.shape == (cfg.N, 4)
+    assert O.rel_l2_cols(Yt, O.dense_apply_t(kind, k, G)).max() < 10 * eps
+    plan = O.make_plan(kind, 60, 1e-12, M=85)
+    plan.eps1 = 0.0
+    kk = I.lagspec_freqs(60, 4.0)
+    op0 = O.compress(plan, kk)
+    assert O.rel_l2_cols(O.apply_output_axis(op0, F[:60]), O.dense_apply(kind, kk, F[:60], M=85)).max() < 1e-13
