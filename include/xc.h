@@ -47,11 +47,19 @@ typedef enum {
   XC_JACOBI = 2,    /* A[j,k] = p_j^(alpha,beta)(x_k), orthonormal on [-1,1]; Legendre = (0,0)
                        (chi read as the squared norm, R-4; block form P:280-301)     */
   XC_LAGUERRE = 3,  /* A[j,k] = l_j(x_k) = exp(-x_k/2) L_j(x_k), x_k >= 0 (block form) */
-  XC_EXP = 4        /* A[j,k] = exp(i pi j t_k), nodes t_k in [0,2): the non-uniform DFT, complex
+  XC_EXP = 4,       /* A[j,k] = exp(i pi j t_k), nodes t_k in [0,2): the non-uniform DFT, complex
                        (the exp row of Appendix A).  Both directions
                        (XC_DIR_WAT: Y = diag(wts) A^T X, no conjugate).  X and Y
                        are complex in planar form: 2N rows, real parts in rows [0,N), imaginary
-                       parts in rows [N,2N), same ld; the full spectrum of L bins is kept.        */
+                       parts in rows [N,2N), same ld; the full spectrum of L bins is kept.
+                       May be rectangular: p->n_rows = M degrees (rows) != N nodes; then
+                       XC_DIR_A maps 2N planar rows to 2M, XC_DIR_WAT 2M to 2N.                  */
+  XC_LAGSPEC = 5    /* the spectral Laguerre forward V = C^T F (Fig. lag_row):
+                       A[m,j] = (-eta/2 - i k_j)^m / (eta/2 - i k_j)^(m+1), m < M = p->n_rows
+                       (0 => N), nodes = frequencies k_j (finite, strictly ascending, any sign),
+                       eta = p->eta > 0.  Computed as XC_EXP at t_j = 1 + (2/pi) atan(2 k_j/eta)
+                       with the per-node scale 1/(eta/2 - i k_j) folded into the operator (R-21);
+                       complex planar X / Y as XC_EXP, both directions.                          */
 } xc_kind;
 
 typedef enum {
@@ -69,6 +77,8 @@ typedef struct {
   int device;              /* CUDA device ordinal                                            */
   void* stream;            /* cudaStream_t for the build (NULL = default stream)             */
   int node_chunk;          /* 0 => auto: nodes per precompute chunk (device memory bound)    */
+  double eta;              /* XC_LAGSPEC: Laguerre scale eta > 0                      */
+  int64_t n_rows;          /* XC_EXP / XC_LAGSPEC: degrees M (rows of A); 0 => N (square)     */
 } xc_params;
 
 typedef struct {
@@ -87,6 +97,7 @@ typedef struct {
   double dmma_flops_per_col_WAT;
   int launches_A;          /* kernel launches per xc_apply(XC_DIR_A)                         */
   int launches_WAT;        /* kernel launches per xc_apply(XC_DIR_WAT)                       */
+  int64_t M;               /* degrees (rows of A): N unless rectangular (complex kinds)       */
 } xc_info_t;
 
 typedef struct {

@@ -116,6 +116,7 @@ __global__ void gen_exp(GenParams g, double2* F, int64_t ld) {
   int p = (int)(idx / g.nc), k = (int)(idx - (int64_t)p * g.nc);
   double m = (double)(p + g.m_off);
   ddv r = tprod(m, g.nodes[k]);
+  if (g.nodes_lo) r = ddadd(r, dv(m * g.nodes_lo[k]));  // t = hi + lo (XC_LAGSPEC phases)
   double n2 = 2.0 * rint(0.5 * r.h);
   r = ddsub(r, dv(n2));
   double s, c;
@@ -123,6 +124,12 @@ __global__ void gen_exp(GenParams g, double2* F, int64_t ld) {
   const double d = 3.141592653589793 * r.l;  // first-order correction for the low part
   double vc = fma(-d, s, c), vs = fma(d, c, s);
   const double wp = g.w ? g.w[p] : 1.0;
+  if (g.cscale) {  // per-node complex scale d_k (XC_LAGSPEC: 1 / (eta/2 - i k))
+    const double2 sc = g.cscale[k];
+    const double re = vc * sc.x - vs * sc.y, im = vc * sc.y + vs * sc.x;
+    vc = re;
+    vs = im;
+  }
   F[(int64_t)p * ld + k] = make_double2(wp * vc, wp * vs);
 }
 

@@ -84,9 +84,12 @@ xc_status upload(DevBuf& b, const std::vector<T>& v) {
 }  // namespace
 
 struct xc_op {
-  int kind = 0;
+  int kind = 0;   // machinery kind (XC_LAGSPEC runs as XC_EXP, R-21)
+  int ukind = 0;  // the kind the caller built
   double alpha = 0, beta = 0;
-  int64_t N = 0;
+  int64_t N = 0;  // nodes
+  int64_t M = 0;  // degrees (rows of A); == N unless rectangular
+  DevBuf nodes_lo, cscale;  // XC_LAGSPEC: low parts of t_j, per-node scale 1/(eta/2 - i k_j)
   double eps1 = 0, eps2 = 0, zeta = 0;
   int tail = 0, dirs = 0, device = 0;
   std::vector<BlockData> blocks;
@@ -202,7 +205,7 @@ xc_status validate_nodes(int kind, const double* x, int64_t N) {
   if (kind == XC_COS) ok = x[0] >= 0.0 && x[N - 1] <= 1.0;
   if (kind == XC_EXP) ok = x[0] >= 0.0 && x[N - 1] < 2.0;
   if (kind == XC_JACOBI) ok = x[0] >= -1.0 && x[N - 1] <= 1.0;
-  if (kind == XC_LAGUERRE) ok = x[0] >= 0.0;
+  if (kind == XC_LAGUERRE) ok = x[0] >= 0.0;  // XC_LAGSPEC: any real frequency
   if (!ok) {
     xc_set_error("nodes: outside the domain of the kind");
     return XC_EINVAL;
@@ -267,6 +270,8 @@ xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int n
     g.L = b.L;
     g.m_off = b.m_off;
     g.nodes = (const double*)h->nodes.p + k0;
+    if (h->nodes_lo.p) g.nodes_lo = (const double*)h->nodes_lo.p + k0;
+    if (h->cscale.p) g.cscale = (const double2*)h->cscale.p + k0;
     g.nc = n;
     g.w = (const double*)b.w.p;
     g.jab = (const double2*)djtab.p;
@@ -728,8 +733,18 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
   xc_params p;
   xc_params_default(&p);
   if (prm) p = *prm;
-  if (kind != XC_COS && kind != XC_JACOBI && kind != XC_LAGUERRE && kind != XC_EXP) {
+  if (kind != XC_COS && kind != XC_JACOBI && kind != XC_LAGUERRE && kind != XC_EXP && kind != XC_LAGSPEC) {
     xc_set_error("unknown kind");
+    return XC_EINVAL;
+  }
+  const bool cplx = kind == XC_EXP || kind == XC_LAGSPEC;
+  const int64_t M = p.n_rows > 0 ? p.n_rows : N;
+  if (p.n_rows < 0 || (M != N && !cplx) || M < 2 || M > (1 << 24)) {
+    xc_set_error("n_rows: 0, or in [2, 2^24] for the complex kinds (XC_EXP, XC_LAGSPEC)");
+    return XC_EINVAL;
+  }
+  if (kind == XC_LAGSPEC && !(std::isfinite(p.eta) && p.eta > 0.0)) {
+    xc_set_error("XC_LAGSPEC needs eta > 0");
     return XC_EINVAL;
   }
   if (N < 2 || N > (1 << 24) || !nodes) {
@@ -740,10 +755,12 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
     xc_set_error("eps must be in (0,1)");
     return XC_EINVAL;
   }
-  h->kind = kind;
+  h->kind = kind == XC_LAGSPEC ? XC_EXP : kind;
+  h->ukind = kind;
   h->alpha = p.alpha;
   h->beta = p.beta;
   h->N = N;
+  h->M = M;
   h->eps1 = p.eps1 > 0 ? p.eps1 : eps;
   h->eps2 = p.eps2 > 0 ? p.eps2 : 1e-2;
   h->dirs = p.dirs ? p.dirs : XC_DIR_A;
@@ -765,7 +782,7 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
   cudaStream_t st = (cudaStream_t)p.stream;
 
   PlanOut plan;
-  XC_TRY(make_chain(kind, N, h->eps1, h->eps2, p.dense_cutoff > 0 ? p.dense_cutoff : 32, plan));
+  XC_TRY(make_chain(h->kind, M, h->eps1, h->eps2, p.dense_cutoff > 0 ? p.dense_cutoff : 32, plan));
   h->zeta = plan.zeta;
   h->tail = plan.tail;
   h->blocks.resize(plan.blocks.size());
@@ -777,7 +794,30 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
     h->blocks[i].keep_hi = plan.blocks[i].keep_hi;
     Lmax = std::max(Lmax, plan.blocks[i].L);
   }
-  XC_TRY(upload(h->nodes, std::vector<double>(nodes, nodes + N)));
+  if (kind == XC_LAGSPEC) {
+    // R-21: C^T[m,j] = r_j^m / (eta/2 - i k_j), r_j = e^{i pi t_j}, t_j = 1 + (2/pi) atan(2 k_j / eta)
+    // in (0, 2), ascending in k_j; t_j carried as hi + lo (80-bit), the scale folded into the entries
+    std::vector<double> th(N), tl(N);
+    std::vector<double2> sc(N);
+    const long double PI = 3.141592653589793238462643383279502884L, e2 = 0.5L * (long double)p.eta;
+    for (int64_t j = 0; j < N; ++j) {
+      const long double kj = nodes[j];
+      const long double t = 1.0L + (2.0L / PI) * atanl(kj / e2);
+      th[j] = (double)t;
+      tl[j] = (double)(t - (long double)th[j]);
+      const long double den = e2 * e2 + kj * kj;
+      sc[j] = make_double2((double)(e2 / den), (double)(kj / den));  // 1/(e2 - i k) = (e2 + i k)/den
+    }
+    if (!(th[0] > 0.0) || !(th[N - 1] < 2.0)) {
+      xc_set_error("XC_LAGSPEC: |k| / eta too large (phase node at the circle's seam)");
+      return XC_EINVAL;
+    }
+    XC_TRY(upload(h->nodes, th));
+    XC_TRY(upload(h->nodes_lo, tl));
+    XC_TRY(upload(h->cscale, sc));
+  } else {
+    XC_TRY(upload(h->nodes, std::vector<double>(nodes, nodes + N)));
+  }
   if (h->dirs & XC_DIR_WAT) XC_TRY(upload(h->wt, std::vector<double>(p.weights, p.weights + N)));
 
   h->bst = st;
@@ -825,7 +865,8 @@ xc_status build_end(xc_op* h) {
   // info
   xc_info_t& in = h->info;
   in.N = N;
-  in.kind = kind;
+  in.M = h->M;
+  in.kind = h->ukind;
   in.zeta = h->zeta;
   in.eps1 = h->eps1;
   in.eps2 = h->eps2;
@@ -937,7 +978,7 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
       io.lds = Bp;
       io.Y = Y;
       io.ldy = ldy;
-      io.ypl = (int64_t)N * ldy;
+      io.ypl = h->M * ldy;  // planar complex output: M degree rows
       io.yscale = (const double*)b.yscale.p;
       io.keep_lo = b.keep_lo;
       io.keep_hi = b.keep_hi;
@@ -989,7 +1030,7 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
     FftIO io{};
     io.X = X;
     io.ldx = ldx;
-    io.xpl = (int64_t)N * ldx;  // planar complex input
+    io.xpl = h->M * ldx;  // planar complex input: M degree rows
     io.winv = (const double*)b.winv.p;
     io.keep_lo = b.keep_lo;
     io.keep_hi = b.keep_hi;
@@ -1079,7 +1120,7 @@ void destroy_impl(xc_op* h) {
   }
   DevBuf* all[] = {&h->nodes, &h->wt, &h->tailP, &h->itemsA, &h->tilesA, &h->winsA, &h->tail_base, &h->tail_nch,
                    &h->itemsW, &h->tilesW, &h->winsW, &h->nodeg_base, &h->nodeg_nch, &h->nodeg_base_im, &h->partA, &h->partW,
-                   &h->scratch, &h->zpl, &h->Xh, &h->Yh, &h->xsend, &h->xrecv, &h->djtab};
+                   &h->scratch, &h->zpl, &h->Xh, &h->Yh, &h->xsend, &h->xrecv, &h->djtab, &h->nodes_lo, &h->cscale};
   for (DevBuf* b : all) dev_free(*b);
 }
 
@@ -1374,7 +1415,10 @@ xc_status host_enqueue(xc_op* h, xc_dir dir, const double* Xh, double* Yh, int64
     }
     XC_CUDA(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming));
   }
-  const int64_t N = h->kind == XC_EXP ? 2 * h->N : h->N;  // rows of X / Y (planar complex: 2N)
+  // rows of X and Y: nodes N / degrees M by direction (planar complex: twice)
+  const int64_t cf = h->kind == XC_EXP ? 2 : 1;
+  const int64_t NI = cf * (dir == XC_DIR_A ? h->N : h->M), NO = cf * (dir == XC_DIR_A ? h->M : h->N);
+  const int64_t N = std::max(NI, NO);
   // chunk: a multiple of 64 columns (the SpMM column tile), at least 64
   int64_t nparts = 12;  // ~B/12 columns per chunk: the measured optimum at c5 (2D DMA efficiency vs pipeline fill)
   if (const char* e = getenv("XC_HOST_CHUNKS")) nparts = std::max(1, atoi(e));
@@ -1410,7 +1454,7 @@ xc_status host_enqueue(xc_op* h, xc_dir dir, const double* Xh, double* Yh, int64
     double* xs = (double*)h->Xh.p + (size_t)i * N * Bc;
     double* ys = (double*)h->Yh.p + (size_t)i * N * Bc;
     if (reused) XC_CUDA(cudaStreamWaitEvent(h->s_in, h->ev_cmp[i], 0));  // slot's X consumed
-    XC_CUDA(cudaMemcpy2DAsync(xs, bc * sizeof(double), Xh + c0, B * sizeof(double), bc * sizeof(double), N,
+    XC_CUDA(cudaMemcpy2DAsync(xs, bc * sizeof(double), Xh + c0, B * sizeof(double), bc * sizeof(double), NI,
                               cudaMemcpyHostToDevice, h->s_in));
     XC_CUDA(cudaEventRecord(h->ev_in[i], h->s_in));
     XC_CUDA(cudaStreamWaitEvent(st, h->ev_in[i], 0));
@@ -1418,7 +1462,7 @@ xc_status host_enqueue(xc_op* h, xc_dir dir, const double* Xh, double* Yh, int64
     XC_TRY(apply_impl(h, dir, xs, bc, ys, bc, bc, st));
     XC_CUDA(cudaEventRecord(h->ev_cmp[i], st));
     XC_CUDA(cudaStreamWaitEvent(h->s_out, h->ev_cmp[i], 0));
-    XC_CUDA(cudaMemcpy2DAsync(Yh + c0, B * sizeof(double), ys, bc * sizeof(double), bc * sizeof(double), N,
+    XC_CUDA(cudaMemcpy2DAsync(Yh + c0, B * sizeof(double), ys, bc * sizeof(double), bc * sizeof(double), NO,
                               cudaMemcpyDeviceToHost, h->s_out));
     XC_CUDA(cudaEventRecord(h->ev_out[i], h->s_out));
   }

@@ -248,6 +248,8 @@ struct GenParams {
   const double* w;     // window on L positions (device) or null (=1)
   const double2* jab;  // Jacobi: per n: (b_n.h, b_n.l), (a_n.h, a_n.l), (inva_n.h, inva_n.l) = 3 double2
   ddv p0;              // Jacobi p_0
+  const double* nodes_lo = nullptr;  // XC_EXP: low parts of the nodes (t = hi + lo), or null
+  const double2* cscale = nullptr;   // XC_EXP: per-node complex scale of the entries, or null
 };
 // F[p * nc + k] = (w_p * phi_{p+m_off}(x_k), 0)   (complex, batch = nodes)
 xc_status gen_entries(const GenParams& g, double2* F, cudaStream_t st);

@@ -14,7 +14,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libxc.so")
 
-XC_COS, XC_JACOBI, XC_LAGUERRE, XC_EXP = 1, 2, 3, 4
+XC_COS, XC_JACOBI, XC_LAGUERRE, XC_EXP, XC_LAGSPEC = 1, 2, 3, 4, 5
+COMPLEX_KINDS = (XC_EXP, XC_LAGSPEC)  # planar complex X / Y (real rows, then imaginary rows)
 XC_DIR_A, XC_DIR_WAT = 1, 2
 _STATUS = {0: "XC_OK", 1: "XC_EINVAL", 2: "XC_ENUMERIC", 3: "XC_ESTATE", 4: "XC_ENOMEM", 5: "XC_ECUDA",
            6: "XC_EUNSUPPORTED"}
@@ -27,7 +28,7 @@ class XcParams(ctypes.Structure):
     _fields_ = [("alpha", ctypes.c_double), ("beta", ctypes.c_double), ("eps1", ctypes.c_double),
                 ("eps2", ctypes.c_double), ("dense_cutoff", ctypes.c_int), ("dirs", ctypes.c_int),
                 ("weights", _dp), ("device", ctypes.c_int), ("stream", ctypes.c_void_p),
-                ("node_chunk", ctypes.c_int)]
+                ("node_chunk", ctypes.c_int), ("eta", ctypes.c_double), ("n_rows", _i64)]
 
 
 class XcInfo(ctypes.Structure):
@@ -36,7 +37,7 @@ class XcInfo(ctypes.Structure):
                 ("dirs", ctypes.c_int), ("nnz", _i64), ("op_bytes_A", _i64), ("op_bytes_WAT", _i64),
                 ("flops_per_col_A", ctypes.c_double), ("flops_per_col_WAT", ctypes.c_double),
                 ("dmma_flops_per_col_A", ctypes.c_double), ("dmma_flops_per_col_WAT", ctypes.c_double),
-                ("launches_A", ctypes.c_int), ("launches_WAT", ctypes.c_int)]
+                ("launches_A", ctypes.c_int), ("launches_WAT", ctypes.c_int), ("M", _i64)]
 
 
 class XcExchange(ctypes.Structure):
@@ -172,16 +173,19 @@ class Transform:
 
     def __init__(self, kind: int, nodes, eps: float, alpha: float = 0.0, beta: float = 0.0,
                  eps1: float = 0.0, eps2: float = 0.0, dense_cutoff: int = 0, dirs: int = XC_DIR_A,
-                 weights=None, device: int = 0, node_chunk: int = 0, stream=None, dist=None):
+                 weights=None, device: int = 0, node_chunk: int = 0, stream=None, dist=None,
+                 eta: float = 0.0, n_rows: int = 0):
         lib = load()
         self._lib = lib
         self.kind = kind
         x = np.ascontiguousarray(np.asarray(nodes, dtype=np.float64))
         self.N = x.size
+        self.M = n_rows if n_rows > 0 else self.N   # degrees (rows of A)
         p = XcParams()
         lib.xc_params_default(ctypes.byref(p))
         p.alpha, p.beta, p.eps1, p.eps2 = alpha, beta, eps1, eps2
         p.dense_cutoff, p.dirs, p.device, p.node_chunk = dense_cutoff, dirs, device, node_chunk
+        p.eta, p.n_rows = eta, n_rows
         self._w = None
         if weights is not None:
             self._w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
@@ -219,30 +223,40 @@ class Transform:
         if X.stride(1) != 1:
             X = X.contiguous()
         N, B = X.shape
-        rows = 2 * self.N if self.kind == XC_EXP else self.N   # XC_EXP: planar complex (re rows, im rows)
-        if N != rows:
-            raise XcError(f"X has {N} rows, transform needs {rows}")
+        rin, rout = self.rows(direction)
+        if N != rin:
+            raise XcError(f"X has {N} rows, transform needs {rin}")
         if out is None:
-            out = torch.empty((N, B), dtype=torch.float64, device=X.device)
+            out = torch.empty((rout, B), dtype=torch.float64, device=X.device)
         st = stream if stream is not None else torch.cuda.current_stream(X.device).cuda_stream
         _check(self._lib.xc_apply(self._h, direction, ctypes.c_void_p(X.data_ptr()), X.stride(0),
                                   ctypes.c_void_p(out.data_ptr()), out.stride(0), B, ctypes.c_void_p(st)))
         return out
 
+    def rows(self, direction: int = XC_DIR_A):
+        """(rows of X, rows of Y) of an apply: nodes N / degrees M by direction, twice for the
+        planar complex kinds."""
+        cf = 2 if self.kind in COMPLEX_KINDS else 1
+        return (cf * self.N, cf * self.M) if direction == XC_DIR_A else (cf * self.M, cf * self.N)
+
     def apply_complex(self, Xc, direction: int = XC_DIR_A, stream=None):
-        """XC_EXP with a complex128 CUDA tensor (N x B): marshalled to and from the planar layout
+        """Complex kinds with a complex128 CUDA tensor: marshalled to and from the planar layout
         of the C ABI (real rows, then imaginary rows)."""
         import torch
         Xp = torch.cat([Xc.real, Xc.imag]).contiguous()
         Yp = self.apply(Xp, direction, stream=stream)
-        return torch.complex(Yp[:self.N], Yp[self.N:])
+        h = Yp.shape[0] // 2
+        return torch.complex(Yp[:h], Yp[h:])
 
     def apply_host(self, X: np.ndarray, direction: int = XC_DIR_A, out: np.ndarray | None = None, stream=None):
         """End-to-end call with host buffers (copies inside the library call)."""
         X = np.ascontiguousarray(X, dtype=np.float64)
         N, B = X.shape
+        rin, rout = self.rows(direction)
+        if N != rin:
+            raise XcError(f"X has {N} rows, transform needs {rin}")
         if out is None:
-            out = np.empty_like(X)
+            out = np.empty((rout, B), dtype=np.float64)
         _check(self._lib.xc_apply_host(self._h, direction, ctypes.c_void_p(X.ctypes.data),
                                        ctypes.c_void_p(out.ctypes.data), B, ctypes.c_void_p(stream or 0)))
         return out

@@ -506,6 +506,98 @@ def test_exp_kind_input_axis_parity(case):
     T.close()
 
 
+RECT_CASES = [("exp_wide", 700, 1000, 5, 1e-10, 11), ("exp_tall", 1000, 643, 7, 1e-12, 12)]
+
+
+@pytest.mark.parametrize("case", RECT_CASES, ids=[c[0] for c in RECT_CASES])
+def test_exp_rectangular_parity(case):
+    """Rectangular complex operator (M degrees x N nodes, R-21): both directions vs the oracle's
+    compressed apply (1e-12) and the dense product / transpose (10 eps); device and host buffers."""
+    xc = _xc()
+    name, M, N, B, eps, seed = case
+    t = I.exp_nodes(N, seed)
+    X = I.complex_rhs(N, B, seed)
+    C = I.complex_rhs(M, B, seed + 1, skip_nodes=False)
+    w = 0.5 + np.random.default_rng(seed).random(N)
+    T = xc.Transform(xc.XC_EXP, t, eps, dirs=xc.XC_DIR_A | xc.XC_DIR_WAT, weights=w, n_rows=M)
+    assert T.info()["M"] == M and T.rows(xc.XC_DIR_A) == (2 * N, 2 * M)
+    op = O.compress(O.make_plan(O.Kind(O.KIND_EXP), N, eps, M=M), t)
+    Y = T.apply_complex(torch.from_numpy(X).cuda()).cpu().numpy()
+    assert Y.shape == (M, B)
+    assert O.rel_l2_cols(Y, O.apply_output_axis(op, X)).max() <= 1e-12, name
+    assert O.rel_l2_cols(Y, O.dense_apply(O.Kind(O.KIND_EXP), t, X, M=M)).max() <= 10 * eps, name
+    Yw = T.apply_complex(torch.from_numpy(C).cuda(), xc.XC_DIR_WAT).cpu().numpy()
+    assert Yw.shape == (N, B)
+    assert O.rel_l2_cols(Yw, O.apply_input_axis(op, C, w)).max() <= 1e-12, name
+    assert O.rel_l2_cols(Yw, w[:, None] * O.dense_apply_t(O.Kind(O.KIND_EXP), t, C)).max() <= 10 * eps, name
+    # host buffers (pipeline copies 2N rows in, 2M rows out)
+    Yh = T.apply_host(np.concatenate([X.real, X.imag]))
+    assert Yh.shape == (2 * M, B)
+    assert O.rel_l2_cols(Yh[:M] + 1j * Yh[M:], Y).max() <= 1e-14, name
+    Ywh = T.apply_host(np.concatenate([C.real, C.imag]), xc.XC_DIR_WAT)
+    assert O.rel_l2_cols(Ywh[:N] + 1j * Ywh[N:], Yw).max() <= 1e-14, name
+    T.close()
+
+
+LAGSPEC_CASES = [("c7", None), ("lagspec_ragged", (333, 517, 19, 1e-12, 800.0, 3.0)),
+                 ("lagspec_4k", (4097, 3001, 64, 1e-10, 2500.0, 40.0))]
+
+
+@pytest.mark.parametrize("case", LAGSPEC_CASES, ids=[c[0] for c in LAGSPEC_CASES])
+def test_lagspec_parity(case):
+    """NEXT-3 second half: the spectral Laguerre forward V = C^T F (c7 = the paper's
+    Fig. lag_row sizes 649 x 501, eta = 2500, T = 4) and its transpose, vs the oracle's power-form
+    operator (compressed 1e-12, dense 10 eps).  The GPU builds it as the exp kind at phase nodes
+    with a per-node scale (R-21); the oracle from Eq. main_formula2 as written."""
+    xc = _xc()
+    name, sz = case
+    if sz is None:
+        cfg = I.CONFIGS["c7"]
+        M, N, B, eps, eta, Tp = cfg.M, cfg.N, cfg.B, cfg.eps, cfg.eta, cfg.T
+        F = I.config_rhs(cfg)
+    else:
+        M, N, B, eps, eta, Tp = sz
+        F = I.complex_rhs(N, B, 21, skip_nodes=False)
+    k = I.lagspec_freqs(N, Tp)
+    kind = O.Kind(O.KIND_LAGSPEC, eta=eta)
+    w = np.ones(N)
+    T = xc.Transform(xc.XC_LAGSPEC, k, eps, dirs=xc.XC_DIR_A | xc.XC_DIR_WAT, weights=w, eta=eta, n_rows=M)
+    assert T.info()["kind"] == xc.XC_LAGSPEC
+    op = O.compress(O.make_plan(kind, N, eps, M=M), k)
+    V = T.apply_complex(torch.from_numpy(F).cuda()).cpu().numpy()
+    assert V.shape == (M, B)
+    assert O.rel_l2_cols(V, O.apply_output_axis(op, F)).max() <= 1e-12, name
+    cols = np.arange(min(B, 8))
+    assert O.rel_l2_cols(V[:, cols], O.dense_apply(kind, k, F[:, cols], M=M)).max() <= 10 * eps, name
+    G = I.complex_rhs(M, B, 22, skip_nodes=False)
+    Vt = T.apply_complex(torch.from_numpy(G).cuda(), xc.XC_DIR_WAT).cpu().numpy()
+    assert O.rel_l2_cols(Vt, O.apply_input_axis(op, G)).max() <= 1e-12, name
+    assert O.rel_l2_cols(Vt[:, cols], O.dense_apply_t(kind, k, G[:, cols])).max() <= 10 * eps, name
+    # the operator: kept runs equal the oracle's (sampled nodes incl. both ends)
+    full = O.node_spectra(op.plan, op.plan.blocks[0], k[[0, N // 2, N - 1]])
+    for j, kk in enumerate((0, N // 2, N - 1)):
+        g = T.node_spectrum(0, kk)
+        o = op.S[0][kk].toarray().ravel()
+        assert np.abs(g - o).max() <= 1e-13 * np.abs(full[j]).max(), (name, kk)
+    T.close()
+
+
+def test_rectangular_and_lagspec_errors():
+    xc = _xc()
+    x = np.linspace(-0.9, 0.9, 64)
+    with pytest.raises(xc.XcError, match="XC_EINVAL"):
+        xc.Transform(xc.XC_JACOBI, x, 1e-10, n_rows=80)        # rectangular: complex kinds only
+    k = np.linspace(0.0, 10.0, 64)
+    with pytest.raises(xc.XcError, match="XC_EINVAL"):
+        xc.Transform(xc.XC_LAGSPEC, k, 1e-10)                  # eta missing
+    with pytest.raises(xc.XcError, match="XC_EINVAL"):
+        xc.Transform(xc.XC_LAGSPEC, k[::-1].copy(), 1e-10, eta=10.0)   # not ascending
+    T = xc.Transform(xc.XC_LAGSPEC, k, 1e-10, eta=10.0, n_rows=50)
+    with pytest.raises(xc.XcError):
+        T.apply(torch.zeros(100, 2, dtype=torch.float64, device="cuda"))  # needs 2N = 128 rows
+    T.close()
+
+
 @pytest.mark.parametrize("L,B", [(86400, 64), (27648, 64), (9000, 96), (2916, 64), (960, 64), (360, 8),
                                  (21600, 32), (10800, 64), (7200, 64), (1152, 40), (720, 1), (60, 3)])
 def test_c2r_engine_vs_numpy(L, B):
