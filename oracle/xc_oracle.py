@@ -431,6 +431,97 @@ def compress(plan: Plan, nodes: np.ndarray, node_chunk: int = 512) -> Operator:
 
 
 # ---------------------------------------------------------------------------
+# Appendix A: fast precompute of the trig kinds (NEXT-2, reading R-22)
+# ---------------------------------------------------------------------------
+def window_spectrum_truncated(zeta: float, L: int, eps1: float):
+    """Step 1 of Appendix A: the Kaiser window's unitary DFT x~ = F w (one library FFT,
+    "performed once for all rows"), truncated to the q = 2Q+1 coefficients |m| <= Q, Q the largest
+    |m| <= L/2 with |x~_m| >= eps1 |x~_0| (R-22).  Returns (Q, x~ truncated (length L), w' = F* x~
+    truncated): w' is the window of the whole method (divided out in the computation stage)."""
+    w = kaiser(zeta, L - 1)
+    xt = np.fft.fft(w, norm="ortho")
+    m = np.minimum(np.arange(L), L - np.arange(L))
+    big = np.abs(xt) >= eps1 * abs(xt[0])
+    Q = int(m[big].max())
+    xq = np.where(m <= Q, xt, 0.0)
+    wq = np.fft.ifft(xq, norm="ortho").real        # x~ Hermitian (w real) => w' real
+    return Q, xq, wq
+
+
+def _dirichlet_exp(t, L: int, m_off: int) -> np.ndarray:
+    """Eq. (y3) for the extended row p -> e^{i pi (p + m_off) t}, p in [0, L): all L bins,
+    y~_k = L^-1/2 e^{i pi m_off t} (e^{i L theta} - 1) / (e^{i theta} w_L^k - 1), theta = pi t, written in
+    its equivalent Dirichlet form e^{i pi (L-1) s / L} sin(pi s) / sin(pi s / L), s = L t / 2 - k
+    (reduced to (-L/2, L/2]; the limit L at s = 0) so that it is exact near resonance.  80-bit."""
+    t = np.asarray(t, dtype=np.longdouble)
+    k = np.arange(L, dtype=np.longdouble)
+    Ld = np.longdouble(L)
+    s = Ld * t[:, None] / 2 - k[None, :]
+    s = s - Ld * np.round(s / Ld)
+    pi = np.longdouble(np.pi)
+    den = np.sin(pi * s / Ld)
+    ratio = np.where(s == 0, Ld, np.sin(pi * s) / np.where(s == 0, 1, den))
+    a = (Ld - 1) * s / Ld + np.longdouble(m_off) * t[:, None]   # phase / pi
+    a = a - 2 * np.round(a / 2)
+    y = ratio * (np.cos(pi * a) + 1j * np.sin(pi * a)) / np.sqrt(Ld)
+    return y.astype(np.complex128)
+
+
+def row_spectra_closed(kind: Kind, nodes: np.ndarray, L: int, m_off: int) -> np.ndarray:
+    """Step 3 of Appendix A: the unitary DFT of every extended (unwindowed) row in closed form,
+    all L bins.  exp: (y3); cos: (y3(theta) + y3(-theta)) / 2 (the printed (y1) is the complex
+    conjugate of the sum it names, R-22); LAGSPEC: (y3) at e^{i theta_j} = r_j times 1/(eta/2 - i k_j)."""
+    x = np.asarray(nodes, dtype=np.float64)
+    if kind.kind == KIND_EXP:
+        return _dirichlet_exp(x, L, m_off)
+    if kind.kind == KIND_COS:
+        return 0.5 * (_dirichlet_exp(x, L, m_off) + _dirichlet_exp(-x, L, m_off))
+    if kind.kind == KIND_LAGSPEC:
+        a = np.longdouble(kind.eta) / 2
+        kk = x.astype(np.longdouble)
+        r = (-a - 1j * kk) / (a - 1j * kk)
+        th = np.angle(r) / np.longdouble(np.pi)        # r = e^{i pi th}
+        d = (1 / (a - 1j * kk)).astype(np.complex128)
+        return _dirichlet_exp(th, L, m_off) * d[:, None]
+    raise ValueError("Appendix A covers the trigonometric kinds only")
+
+
+def node_spectra_appA(plan: Plan, blk: Block, nodes: np.ndarray, xq: np.ndarray) -> np.ndarray:
+    """Step 2 of Appendix A: F(w' . row) = x~ * y~ (Eq. A.1: (x~*y~)_n =
+    L^-1/2 sum_m x~_m y~_{(n-m) mod L}) over the 2Q+1 nonzero x~_m, every bin (the oracle does
+    not skip bins; the product evaluates only a window around each node's peak)."""
+    L = blk.L
+    y = row_spectra_closed(plan.kind, nodes, L, blk.m_off)
+    S = np.zeros_like(y)
+    for m in np.nonzero(xq)[0]:
+        S += xq[m] * np.roll(y, m, axis=1)            # y~_{(n - m) mod L}
+    S /= np.sqrt(L)
+    if is_complex(plan.kind):
+        return S
+    S = S[:, :blk.H].copy()
+    S[:, 0] = S[:, 0].real
+    S[:, -1] = S[:, -1].real
+    return S
+
+
+def compress_appA(plan: Plan, nodes: np.ndarray, node_chunk: int = 256) -> Operator:
+    """The trig operator by Appendix A: per block the truncated window spectrum, closed-form row
+    spectra, convolution, then the same per-node threshold; the window the computation
+    stage divides by is w' (R-22)."""
+    assert plan.kind.kind in (KIND_COS, KIND_EXP, KIND_LAGSPEC)
+    S_list, W_list = [], []
+    for blk in plan.blocks:
+        Q, xq, wq = window_spectrum_truncated(plan.zeta, blk.L, plan.eps1)
+        parts = []
+        for k0 in range(0, plan.N, node_chunk):
+            Sk = threshold(node_spectra_appA(plan, blk, nodes[k0:k0 + node_chunk], xq), plan.eps1)
+            parts.append(sp.csr_matrix(Sk))
+        S_list.append(sp.vstack(parts).tocsr())
+        W_list.append(wq)
+    return Operator(plan, S_list, W_list, np.zeros((0, plan.N)))
+
+
+# ---------------------------------------------------------------------------
 # Computation stage
 # ---------------------------------------------------------------------------
 def apply_output_axis(op: Operator, X: np.ndarray) -> np.ndarray:

@@ -604,3 +604,99 @@ def test_lagspec_fig_lag_row_compressed(eps):
     kk = I.lagspec_freqs(60, 4.0)
     op0 = O.compress(plan, kk)
     assert O.rel_l2_cols(O.apply_output_axis(op0, F[:60]), O.dense_apply(kind, kk, F[:60], M=85)).max() < 1e-13
+
+
+# --------------------------------------------------------------------------- Appendix A (NEXT-2)
+def test_appA_closed_row_spectra_vs_fft():
+    """(y3) / the cos and LAGSPEC rows in closed form = numpy's FFT of the extended rows."""
+    L, m_off = 90, -13
+    t = np.array([0.0, 0.013, 0.5, 0.77, 1.0])
+    for kind, nodes in ((COS, t), (EXPK, np.r_[t, 1.31, 1.999]), (_lagk(40.0), np.array([-30.0, 0.0, 2.5, 90.0]))):
+        y = O.row_spectra_closed(kind, nodes, L, m_off)
+        E = O.entries(kind, nodes, 0, L, m_off)
+        np.testing.assert_allclose(y, np.fft.fft(E, axis=1, norm="ortho"), atol=1e-13 * np.sqrt(L))
+
+
+def test_appA_closed_form_at_resonance_vs_mpmath():
+    """Near and at resonance (theta = 2 pi k / L, where (y3) is 0/0) the Dirichlet form is exact: vs
+    the 40-digit geometric sum."""
+    mp.mp.dps = 40
+    L, m_off = 64, -5
+    for t in (2 * 7 / L, 2 * 7 / L + 1e-13, 2 * 7 / L - 3e-16, 2 * 63 / L):
+        y = O.row_spectra_closed(EXPK, np.array([t]), L, m_off)[0]
+        for k in (6, 7, 8, 63):
+            ref = mp.fsum(mp.expj(mp.pi * (p + m_off) * mp.mpf(t)) * mp.expj(-2 * mp.pi * p * k / L) for p in range(L))
+            assert abs(complex(y[k]) - complex(ref) / math.sqrt(L)) < 1e-14 * math.sqrt(L), (t, k)
+
+
+def test_appA_printed_y1_is_conjugated():
+    """Reading R-22: the printed (y1) equals the sum with w_N^{-jk}, i.e. the conjugate of the sum it
+    names (the oracle uses (y3(theta) + y3(-theta))/2); (y3) as printed is right."""
+    N, th = 50, 0.7123
+    k = np.arange(N)
+    om = np.exp(-2j * np.pi / N)
+    c, s_ = np.cos(N * th), np.sin(N * th)
+    y1 = om ** k * (((c - 1) * np.cos(th) + np.sin(th) * s_) - (c - 1) * om ** k) / (om ** (2 * k) - 2 * om ** k * np.cos(th) + 1) / np.sqrt(N)
+    y = O.row_spectra_closed(COS, np.array([th / np.pi]), N, 0)[0]
+    np.testing.assert_allclose(y1, np.conj(y), atol=1e-12)
+    assert np.abs(y1 - y).max() > 1.0
+    y3 = (np.exp(1j * N * th) - 1) / (np.exp(1j * th) * om ** k - 1) / np.sqrt(N)
+    np.testing.assert_allclose(y3, O.row_spectra_closed(EXPK, np.array([th / np.pi]), N, 0)[0], atol=1e-12)
+
+
+def test_appA_untruncated_convolution_is_the_direct_dft():
+    """Eq. (A.1) with every window coefficient (Q = L/2) reproduces the direct windowed DFT
+    (node_spectra) -- the convolution theorem with the 1/sqrt(N) of P:645."""
+    N, eps = 40, 1e-10
+    t = I.cos_nodes(N, 3)
+    for kind, nodes in ((COS, t), (EXPK, 2 * t)):
+        plan = O.make_plan(kind, N, eps)
+        blk = plan.blocks[0]
+        xt = np.fft.fft(O.kaiser(plan.zeta, blk.L - 1), norm="ortho")
+        S = O.node_spectra_appA(plan, blk, nodes, xt)
+        np.testing.assert_allclose(S, O.node_spectra(plan, blk, nodes), atol=1e-13)
+
+
+def test_appA_window_truncation():
+    """Q, x~ and w' (R-22): w' = F* of the kept coefficients, real; |w' - w| <= L^-1/2 sum of the
+    dropped |x~_m|; q = 2Q + 1 is small (the paper: "a small number of coefficients")."""
+    for eps, L in ((1e-10, 7200), (1e-12, 1080)):
+        z = O.solve_zeta(eps)
+        Q, xq, wq = O.window_spectrum_truncated(z, L, eps)
+        w = O.kaiser(z, L - 1)
+        xt = np.fft.fft(w, norm="ortho")
+        assert 6 <= Q <= 16
+        assert np.count_nonzero(xq) == 2 * Q + 1
+        assert np.abs(xt[Q + 1:L - Q]).max() < eps * abs(xt[0]) <= np.abs(xt[Q])
+        bound = np.abs(xt[Q + 1:L - Q]).sum() / np.sqrt(L)
+        assert np.abs(wq - w).max() <= bound * (1 + 1e-9) + 1e-15
+
+
+@pytest.mark.parametrize("which", ["cos", "exp", "lagspec"])
+def test_appA_operator_meets_10eps(which):
+    """The Appendix-A operator (closed-form rows, q-term convolution, w' divided out) meets 10 eps
+    against the dense product, with the kept-entry count of the direct build (+-2 %)."""
+    eps = 1e-10
+    if which == "cos":
+        kind, N, M = COS, 1024, None
+        nodes = I.cos_nodes(N, 1)
+        X = I.rhs(N, 3, 1, skip_cos_nodes=True)
+    elif which == "exp":
+        kind, N, M = EXPK, 1024, None
+        nodes = I.exp_nodes(N, 6)
+        X = I.complex_rhs(N, 3, 6)
+    else:
+        cfg = I.CONFIGS["c7"]
+        kind, N, M = _lagk(cfg.eta), cfg.N, cfg.M
+        nodes = I.lagspec_freqs(N, cfg.T)
+        X = I.config_rhs(cfg, 3)
+    plan = O.make_plan(kind, N, eps, M=M)
+    opA = O.compress_appA(plan, nodes)
+    Y = O.apply_output_axis(opA, X)
+    Yd = O.dense_apply(kind, nodes, X, M=M) if M else O.dense_apply(kind, nodes, X)
+    assert O.rel_l2_cols(Y, Yd).max() < 10 * eps
+    op = O.compress(plan, nodes)
+    assert abs(O.nnz(opA)[0] / O.nnz(op)[0] - 1) < 0.02
+    if which == "exp":
+        C = I.complex_rhs(N, 2, 60, skip_nodes=False)
+        assert O.rel_l2_cols(O.apply_input_axis(opA, C), O.dense_apply_t(kind, nodes, C)).max() < 10 * eps
