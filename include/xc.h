@@ -79,6 +79,11 @@ typedef struct {
   int node_chunk;          /* 0 => auto: nodes per precompute chunk (device memory bound)    */
   double eta;              /* XC_LAGSPEC: Laguerre scale eta > 0                      */
   int64_t n_rows;          /* XC_EXP / XC_LAGSPEC: degrees M (rows of A); 0 => N (square)     */
+  int trig_precompute;     /* trig kinds (XC_COS, XC_EXP, XC_LAGSPEC): 0 = entries + FFT per node;
+                              1 = Appendix A (R-22): closed-form row spectra convolved
+                              with the 2Q+1 leading window coefficients, only the bins around each
+                              node's peak evaluated; the truncated window W' is then the method's
+                              window (xc_block_window returns it).  XC_EINVAL for other kinds.  */
 } xc_params;
 
 typedef struct {
@@ -108,6 +113,7 @@ typedef struct {
   int keep_hi;
   int64_t nnz;      /* kept complex entries                                                   */
   int max_band;     /* widest kept run of any node (bins)                                     */
+  int q_taps;       /* Appendix A precompute: window coefficients 2Q+1 (0: direct precompute) */
 } xc_block_info_t;
 
 /* Fill *p with defaults (all zero / NULL; device 0). */

@@ -69,6 +69,7 @@ struct BlockData {
   DevBuf start, len, off, vals;
   int64_t nnz = 0;
   int max_band = 0;
+  int appQ = -1;  // Appendix A precompute: Q of the truncated window spectrum (-1: direct)
   int ngroups = 0;
   int64_t loc_count = 0;  // values of the locally computed node range (distributed precompute)
   DevBuf grp_base, grp_nch;  // output axis groups
@@ -86,6 +87,7 @@ xc_status upload(DevBuf& b, const std::vector<T>& v) {
 struct xc_op {
   int kind = 0;   // machinery kind (XC_LAGSPEC runs as XC_EXP, R-21)
   int ukind = 0;  // the kind the caller built
+  bool appA = false;  // Appendix A trig precompute (R-22)
   double alpha = 0, beta = 0;
   int64_t N = 0;  // nodes
   int64_t M = 0;  // degrees (rows of A); == N unless rectangular
@@ -231,6 +233,14 @@ xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int n
     XC_TRY(upload(b.twh, tw));
   }
   kaiser_window(h->zeta, b.L, b.h_w);
+  DevBuf dxq;
+  if (h->appA) {  // R-22: the truncated window W' = F* xq is the method's window from here on
+    std::vector<double2> xq;
+    std::vector<double> wq;
+    XC_TRY(appa_window(b.h_w, b.L, h->eps1, xq, b.appQ, wq));
+    b.h_w = wq;
+    XC_TRY(upload(dxq, xq));
+  }
   std::vector<double> ys(b.L), wi(b.L);
   const double isL = 1.0 / sqrt((double)b.L);
   for (int p = 0; p < b.L; ++p) {
@@ -248,12 +258,28 @@ xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int n
   size_t fr = 0, tot = 0;
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = 3ull << 30;
   const int64_t budget = std::max<int64_t>(1LL << 30, std::min<int64_t>((int64_t)(fr / 3), 48LL << 30));
-  int nc = node_chunk > 0 ? node_chunk : (int)std::max<int64_t>(64, budget / ((int64_t)b.L * 48));
+  // Appendix A, window mode: only 2W+1 bins per node are evaluated and kept in memory; for
+  // complex rows the window must stay under half the circle (its linear span is then the
+  // shortest arc holding the kept bins, R-18); short blocks take the full-spectrum mode
+  int appW = b.appQ + 16;
+  const int appWmax = cplx_rows ? (b.L / 2 - 1) / 2 : b.H;
+  const bool app_win = h->appA && appW <= appWmax;
+  int64_t per_node = app_win ? (int64_t)16 * 4 * (2 * appW + 1) + 32 : (int64_t)b.L * 48;
+  int nc = node_chunk > 0 ? node_chunk : (int)std::max<int64_t>(64, std::min<int64_t>(budget / per_node, 1 << 24));
   nc = std::min(nc, N);
-  DevBuf F, scr, spec, st_len, d_start, d_len;
-  XC_TRY(dev_alloc(F, (size_t)b.L * nc * sizeof(double2)));
-  if (b.fft.L2 > 1) XC_TRY(dev_alloc(scr, (size_t)b.L * nc * sizeof(double2)));
-  XC_TRY(dev_alloc(spec, (size_t)b.H * nc * sizeof(double2)));
+  DevBuf F, scr, spec, st_len, d_start, d_len, dflag, dwin, dwfirst, dthr;
+  if (!h->appA) {
+    XC_TRY(dev_alloc(F, (size_t)b.L * nc * sizeof(double2)));
+    if (b.fft.L2 > 1) XC_TRY(dev_alloc(scr, (size_t)b.L * nc * sizeof(double2)));
+  } else {
+    XC_TRY(dev_alloc(dflag, sizeof(int)));
+  }
+  if (app_win) {
+    XC_TRY(dev_alloc(dwfirst, (size_t)nc * sizeof(int)));
+    XC_TRY(dev_alloc(dthr, (size_t)nc * sizeof(double)));
+  } else {
+    XC_TRY(dev_alloc(spec, (size_t)b.H * nc * sizeof(double2)));
+  }
   XC_TRY(dev_alloc(b.start, (size_t)N * sizeof(int)));
   XC_TRY(dev_alloc(b.len, (size_t)N * sizeof(int)));
   b.h_start.assign(N, 0);
@@ -265,29 +291,66 @@ xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int n
 
   for (int k0 = n0; k0 < n1; k0 += nc) {
     int n = std::min(nc, n1 - k0);
-    GenParams g{};
-    g.kind = h->kind;
-    g.L = b.L;
-    g.m_off = b.m_off;
-    g.nodes = (const double*)h->nodes.p + k0;
-    if (h->nodes_lo.p) g.nodes_lo = (const double*)h->nodes_lo.p + k0;
-    if (h->cscale.p) g.cscale = (const double2*)h->cscale.p + k0;
-    g.nc = n;
-    g.w = (const double*)b.w.p;
-    g.jab = (const double2*)djtab.p;
-    g.p0 = p0;
-    XC_TRY(gen_entries(g, (double2*)F.p, st));
-    FftIO io{};
-    io.src = (const double2*)F.p;
-    io.lds = n;
-    io.dst = (double2*)spec.p;
-    io.ldd = n;
-    io.kmax = b.H;
-    io.scale = 1.0 / sqrt((double)b.L);  // unitary DFT of Eq. (1)
-    XC_TRY(fft_run(b.fft, -1, PRO_PLAIN, EPI_PLAIN, io, n, (double2*)scr.p, st));
+    int W = 0;  // Appendix A: evaluated half-window around the peak (kept runs lie within Q + 3, R-22)
+    AppAWin wm{};
+    if (h->appA) {
+      for (;;) {
+        const int Wmax = app_win ? appWmax : (cplx_rows ? (b.L - 1) / 2 : b.H);  // no bin evaluated twice
+        W = std::min(appW, Wmax);
+        int flag = 0;
+        XC_CUDA(cudaMemsetAsync(dflag.p, 0, sizeof(int), st));
+        const double* th = (const double*)h->nodes.p + k0;
+        const double* tl = h->nodes_lo.p ? (const double*)h->nodes_lo.p + k0 : nullptr;
+        const double2* cs = h->cscale.p ? (const double2*)h->cscale.p + k0 : nullptr;
+        if (app_win) {
+          const size_t wb = (size_t)n * (2 * W + 1) * sizeof(double2);
+          if (dwin.bytes < wb) {
+            dev_free(dwin);
+            XC_TRY(dev_alloc(dwin, wb));
+          }
+          wm = AppAWin{(double2*)dwin.p, (int*)b.start.p + k0, (int*)b.len.p + k0, (int*)dwfirst.p, (double*)dthr.p};
+          XC_TRY(appa_spectra(h->kind, b.L, b.H, b.m_off, b.appQ, W, th, tl, cs, (const double2*)dxq.p, n, h->eps1,
+                              nullptr, (int*)dflag.p, st, &wm));
+        } else {
+          XC_CUDA(cudaMemsetAsync(spec.p, 0, (size_t)b.H * n * sizeof(double2), st));
+          XC_TRY(appa_spectra(h->kind, b.L, b.H, b.m_off, b.appQ, W, th, tl, cs, (const double2*)dxq.p, n, h->eps1,
+                              (double2*)spec.p, (int*)dflag.p, st));
+        }
+        XC_CUDA(cudaMemcpyAsync(&flag, dflag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        XC_CUDA(cudaStreamSynchronize(st));
+        if (!flag) break;
+        if (W == Wmax) {
+          if (!app_win) break;  // every bin evaluated
+          xc_set_error("Appendix A: a kept run spans a quarter of the circle; use trig_precompute = 0");
+          return XC_ENUMERIC;
+        }
+        appW = 2 * appW;  // a kept bin on the window's edge: widen and redo the chunk
+      }
+    } else {
+      GenParams g{};
+      g.kind = h->kind;
+      g.L = b.L;
+      g.m_off = b.m_off;
+      g.nodes = (const double*)h->nodes.p + k0;
+      if (h->nodes_lo.p) g.nodes_lo = (const double*)h->nodes_lo.p + k0;
+      if (h->cscale.p) g.cscale = (const double2*)h->cscale.p + k0;
+      g.nc = n;
+      g.w = (const double*)b.w.p;
+      g.jab = (const double2*)djtab.p;
+      g.p0 = p0;
+      XC_TRY(gen_entries(g, (double2*)F.p, st));
+      FftIO io{};
+      io.src = (const double2*)F.p;
+      io.lds = n;
+      io.dst = (double2*)spec.p;
+      io.ldd = n;
+      io.kmax = b.H;
+      io.scale = 1.0 / sqrt((double)b.L);  // unitary DFT of Eq. (1)
+      XC_TRY(fft_run(b.fft, -1, PRO_PLAIN, EPI_PLAIN, io, n, (double2*)scr.p, st));
+    }
     int* ds = (int*)b.start.p + k0;
     int* dl = (int*)b.len.p + k0;
-    XC_TRY(band_detect((const double2*)spec.p, b.H, n, h->eps1, ds, dl, cplx_rows, st));
+    if (!app_win) XC_TRY(band_detect((const double2*)spec.p, b.H, n, h->eps1, ds, dl, cplx_rows, st));
     XC_CUDA(cudaMemcpyAsync(b.h_start.data() + k0, ds, n * sizeof(int), cudaMemcpyDeviceToHost, st));
     XC_CUDA(cudaMemcpyAsync(b.h_len.data() + k0, dl, n * sizeof(int), cudaMemcpyDeviceToHost, st));
     XC_CUDA(cudaStreamSynchronize(st));
@@ -301,8 +364,11 @@ xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int n
     DevBuf cv;
     XC_TRY(dev_alloc(cv, (size_t)std::max<int64_t>(1, tot) * sizeof(double2)));
     XC_TRY(upload(choff, loc));
-    XC_TRY(band_store((const double2*)spec.p, b.H, n, h->eps1, ds, dl, (const int64_t*)choff.p,
-                      (double2*)cv.p, cplx_rows, st));
+    if (app_win)
+      XC_TRY(appa_store(wm, W, (const int64_t*)choff.p, (double2*)cv.p, n, st));
+    else
+      XC_TRY(band_store((const double2*)spec.p, b.H, n, h->eps1, ds, dl, (const int64_t*)choff.p,
+                        (double2*)cv.p, cplx_rows, st));
     XC_CUDA(cudaStreamSynchronize(st));
     chunk_vals.push_back(cv);
     chunk_base.push_back(tot);
@@ -325,6 +391,11 @@ xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int n
   dev_free(F);
   dev_free(scr);
   dev_free(spec);
+  dev_free(dflag);
+  dev_free(dxq);
+  dev_free(dwin);
+  dev_free(dwfirst);
+  dev_free(dthr);
   return XC_OK;
 }
 
@@ -743,6 +814,10 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
     xc_set_error("n_rows: 0, or in [2, 2^24] for the complex kinds (XC_EXP, XC_LAGSPEC)");
     return XC_EINVAL;
   }
+  if (p.trig_precompute != 0 && (p.trig_precompute != 1 || !(cplx || kind == XC_COS))) {
+    xc_set_error("trig_precompute: 0, or 1 (Appendix A) for XC_COS / XC_EXP / XC_LAGSPEC");
+    return XC_EINVAL;
+  }
   if (kind == XC_LAGSPEC && !(std::isfinite(p.eta) && p.eta > 0.0)) {
     xc_set_error("XC_LAGSPEC needs eta > 0");
     return XC_EINVAL;
@@ -757,6 +832,7 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
   }
   h->kind = kind == XC_LAGSPEC ? XC_EXP : kind;
   h->ukind = kind;
+  h->appA = p.trig_precompute == 1;
   h->alpha = p.alpha;
   h->beta = p.beta;
   h->N = N;
@@ -1550,6 +1626,7 @@ xc_status xc_block_info(xc_handle h, int i, xc_block_info_t* out) {
   out->keep_hi = b.keep_hi;
   out->nnz = b.nnz;
   out->max_band = b.max_band;
+  out->q_taps = b.appQ >= 0 ? 2 * b.appQ + 1 : 0;
   return XC_OK;
 }
 

@@ -258,6 +258,23 @@ xc_status gen_entries_real(const GenParams& g, double* E, int64_t ldE, cudaStrea
 
 // Band detection and compaction on a spectrum chunk Spec[q * nc + k], q < H.
 // circ: complex rows (XC_EXP), full circular spectrum of H = L bins; runs may wrap (mod H).
+// Appendix A (appa.cu): truncated window spectrum xq (2Q+1, index m+Q) and W' = F* xq on the host;
+// the per-node windowed spectra around each node's peak into spec (zeroed by the caller).
+xc_status appa_window(const std::vector<double>& w, int L, double eps1, std::vector<double2>& xq, int& Q,
+                      std::vector<double>& wq);
+// Window mode (wm != null): only the 2W+1 bins around each node's peak, the kept run (start, len)
+// found in the window, then appa_store copies it; spec may then be null.
+struct AppAWin {
+  double2* win;   // nc x (2W+1)
+  int* start;
+  int* len;
+  int* wfirst;
+  double* thr;
+};
+xc_status appa_spectra(int kind, int L, int H, int m_off, int Q, int W, const double* th, const double* tl,
+                       const double2* cscale, const double2* xq, int nc, double eps1, double2* spec, int* flag,
+                       cudaStream_t st, AppAWin* wm = nullptr);
+xc_status appa_store(const AppAWin& wm, int W, const int64_t* off, double2* vals, int nc, cudaStream_t st);
 xc_status band_detect(const double2* spec, int H, int nc, double eps1, int* start, int* len, bool circ,
                       cudaStream_t st);
 xc_status band_store(const double2* spec, int H, int nc, double eps1, const int* start, const int* len,

@@ -28,7 +28,8 @@ class XcParams(ctypes.Structure):
     _fields_ = [("alpha", ctypes.c_double), ("beta", ctypes.c_double), ("eps1", ctypes.c_double),
                 ("eps2", ctypes.c_double), ("dense_cutoff", ctypes.c_int), ("dirs", ctypes.c_int),
                 ("weights", _dp), ("device", ctypes.c_int), ("stream", ctypes.c_void_p),
-                ("node_chunk", ctypes.c_int), ("eta", ctypes.c_double), ("n_rows", _i64)]
+                ("node_chunk", ctypes.c_int), ("eta", ctypes.c_double), ("n_rows", _i64),
+                ("trig_precompute", ctypes.c_int)]
 
 
 class XcInfo(ctypes.Structure):
@@ -46,7 +47,7 @@ class XcExchange(ctypes.Structure):
 
 class XcBlockInfo(ctypes.Structure):
     _fields_ = [("L", ctypes.c_int), ("H", ctypes.c_int), ("m_off", ctypes.c_int), ("keep_lo", ctypes.c_int),
-                ("keep_hi", ctypes.c_int), ("nnz", _i64), ("max_band", ctypes.c_int)]
+                ("keep_hi", ctypes.c_int), ("nnz", _i64), ("max_band", ctypes.c_int), ("q_taps", ctypes.c_int)]
 
 
 EXPORTS = ["xc_params_default", "xc_build_compressed", "xc_build_local", "xc_build_step", "xc_apply", "xc_c2r_check", "xc_set_graphs", "xc_apply_host", "xc_apply_host_async", "xc_host_wait", "xc_reserve",
@@ -174,7 +175,7 @@ class Transform:
     def __init__(self, kind: int, nodes, eps: float, alpha: float = 0.0, beta: float = 0.0,
                  eps1: float = 0.0, eps2: float = 0.0, dense_cutoff: int = 0, dirs: int = XC_DIR_A,
                  weights=None, device: int = 0, node_chunk: int = 0, stream=None, dist=None,
-                 eta: float = 0.0, n_rows: int = 0):
+                 eta: float = 0.0, n_rows: int = 0, trig_precompute: int = 0):
         lib = load()
         self._lib = lib
         self.kind = kind
@@ -185,7 +186,7 @@ class Transform:
         lib.xc_params_default(ctypes.byref(p))
         p.alpha, p.beta, p.eps1, p.eps2 = alpha, beta, eps1, eps2
         p.dense_cutoff, p.dirs, p.device, p.node_chunk = dense_cutoff, dirs, device, node_chunk
-        p.eta, p.n_rows = eta, n_rows
+        p.eta, p.n_rows, p.trig_precompute = eta, n_rows, trig_precompute
         self._w = None
         if weights is not None:
             self._w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))

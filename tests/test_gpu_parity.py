@@ -598,6 +598,61 @@ def test_rectangular_and_lagspec_errors():
     T.close()
 
 
+APPA_CASES = [("c2", "cos", 4096, 64, 1e-10, 1), ("cos_small", "cos", 33, 3, 1e-12, 5),
+              ("exp_ragged", "exp", 1000, 37, 1e-10, 9), ("exp_1e-12", "exp", 2048, 16, 1e-12, 2),
+              ("c7", "lagspec", 501, 64, 1e-10, 7)]
+
+
+@pytest.mark.parametrize("case", APPA_CASES, ids=[c[0] for c in APPA_CASES])
+def test_appA_precompute_parity(case):
+    """NEXT-2: the Appendix A precompute (trig_precompute=1, R-22) on the GPU vs the oracle's
+    Appendix A operator: same truncated window W' (1e-14) and q, sampled node spectra (1e-13 of
+    the node max), applies within 1e-12 of the oracle's and 10 eps of the dense product; the kept
+    count within 2 % of the direct build's."""
+    xc = _xc()
+    name, which, N, B, eps, seed = case
+    M = None
+    if which == "cos":
+        kind, kx, nodes = O.Kind(O.KIND_COS), xc.XC_COS, I.cos_nodes(N, seed)
+        X = I.rhs(N, B, seed, skip_cos_nodes=True)
+        extra = {}
+    elif which == "exp":
+        kind, kx, nodes = O.Kind(O.KIND_EXP), xc.XC_EXP, I.exp_nodes(N, seed)
+        X = I.complex_rhs(N, B, seed)
+        extra = {}
+    else:
+        cfg = I.CONFIGS["c7"]
+        kind, kx, nodes = O.Kind(O.KIND_LAGSPEC, eta=cfg.eta), xc.XC_LAGSPEC, I.lagspec_freqs(N, cfg.T)
+        M = cfg.M
+        X = I.config_rhs(cfg, B)
+        extra = {"eta": cfg.eta, "n_rows": M}
+    T = xc.Transform(kx, nodes, eps, trig_precompute=1, **extra)
+    Td = xc.Transform(kx, nodes, eps, **extra)
+    plan = O.make_plan(kind, N, eps, M=M)
+    opA = O.compress_appA(plan, nodes)
+    Q, xq, wq = O.window_spectrum_truncated(plan.zeta, plan.blocks[0].L, plan.eps1)
+    bi = T.block_info(0)
+    assert bi["q_taps"] == 2 * Q + 1 and Td.block_info(0)["q_taps"] == 0
+    np.testing.assert_allclose(T.window(0), wq, rtol=0, atol=1e-14)   # two evaluation orders of F* xq
+    assert abs(bi["nnz"] / Td.block_info(0)["nnz"] - 1) < 0.02
+    blk = plan.blocks[0]
+    ks = [0, N // 3, N - 1]
+    full = O.node_spectra_appA(plan, blk, nodes[ks], xq)
+    for j, k in enumerate(ks):
+        g = T.node_spectrum(0, k)
+        o = opA.S[0][k].toarray().ravel()
+        assert np.abs(g - o).max() <= 1e-13 * np.abs(full[j]).max(), (name, k)
+    cplx = which != "cos"
+    Xg = torch.from_numpy(X).cuda()
+    Y = (T.apply_complex(Xg) if cplx else T.apply(Xg)).cpu().numpy()
+    assert O.rel_l2_cols(Y, O.apply_output_axis(opA, X)).max() <= 1e-12, name
+    cols = np.arange(min(B, 8))
+    Yd = O.dense_apply(kind, nodes, X[:, cols], M=M) if M else O.dense_apply(kind, nodes, X[:, cols])
+    assert O.rel_l2_cols(Y[:, cols], Yd).max() <= 10 * eps, name
+    T.close()
+    Td.close()
+
+
 @pytest.mark.parametrize("L,B", [(86400, 64), (27648, 64), (9000, 96), (2916, 64), (960, 64), (360, 8),
                                  (21600, 32), (10800, 64), (7200, 64), (1152, 40), (720, 1), (60, 3)])
 def test_c2r_engine_vs_numpy(L, B):
