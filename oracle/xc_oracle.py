@@ -37,7 +37,7 @@ import scipy.sparse as sp
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = None
 
-KIND_COS, KIND_JACOBI, KIND_LAGUERRE, KIND_EXP, KIND_LAGSPEC = 1, 2, 3, 4, 5
+KIND_COS, KIND_JACOBI, KIND_LAGUERRE, KIND_EXP, KIND_LAGSPEC, KIND_LAG2D = 1, 2, 3, 4, 5, 6
 
 
 def is_complex(kind) -> bool:
@@ -519,6 +519,90 @@ def compress_appA(plan: Plan, nodes: np.ndarray, node_chunk: int = 256) -> Opera
         S_list.append(sp.vstack(parts).tocsr())
         W_list.append(wq)
     return Operator(plan, S_list, W_list, np.zeros((0, plan.N)))
+
+
+# ---------------------------------------------------------------------------
+# 2D (both-sided) block extra-component method, time-domain Laguerre (NEXT-1, reading R-23)
+# ---------------------------------------------------------------------------
+def lag2d_nodes_ext(nodes: np.ndarray, n: int) -> np.ndarray:
+    """The equispaced grid x_i (t_i = 12 i / (N-1)) continued to n points: the given
+    N nodes, then x_{N-1} + i h, h = (x_{N-1} - x_0) / (N - 1) (the extra rows of the 2D blocks)."""
+    x = np.asarray(nodes, dtype=np.float64)
+    N = x.size
+    if n <= N:
+        return x[:n].copy()
+    h = (x[-1] - x[0]) / (N - 1)
+    return np.concatenate([x, x[-1] + h * np.arange(1, n - N + 1, dtype=np.float64)])
+
+
+@dataclass
+class Operator2D:
+    plan: Plan        # the block chain, used on both axes (square N x N)
+    D2: list          # D2[b][a]: scipy.sparse (L_b x L_a) complex, thresholded 2D spectrum
+    windows: list     # Kaiser window of each block
+    tail_rows: np.ndarray   # D[i, j], i < t (all degrees)
+    tail_cols: np.ndarray   # D[i, j], i >= t, j < t
+
+
+def compress_2d(plan: Plan, nodes: np.ndarray) -> Operator2D:
+    """D[i,j] = l_j(x_i) on the equispaced grid, compressed per block pair (a, b) of the chain used
+    on both axes (Fig. test322; R-23): the extended block E_ab[p, q] =
+    l_q(x_p), p in [0, L_b) (time positions; extra rows continue the grid), q in [0, L_a) (degrees;
+    extra degrees continue the recurrence), then D2_ab = F W_b E_ab W_a F (Eq. comp_2d, P:428;
+    unitary 2D DFT), thresholded at eps1 * max |D2_ab| (the global form of P:198)."""
+    assert plan.kind.kind == KIND_LAGUERRE
+    N, t = plan.N, plan.tail
+    Lmax = max(b.L for b in plan.blocks)
+    W = [kaiser(plan.zeta, b.L - 1) for b in plan.blocks]
+    D2 = []
+    for b, wb in zip(plan.blocks, W):
+        Et = entries(plan.kind, lag2d_nodes_ext(nodes, b.L), 0, Lmax)   # Et[p, q] = l_q(x_p)
+        row = []
+        for a, wa in zip(plan.blocks, W):
+            S = np.fft.fft2(wb[:, None] * Et[:, :a.L] * wa[None, :], norm="ortho")
+            S = np.where(np.abs(S) >= plan.eps1 * np.abs(S).max(), S, 0.0)
+            row.append(sp.csr_matrix(S))
+        D2.append(row)
+    x = np.asarray(nodes, dtype=np.float64)
+    tail_rows = entries(plan.kind, x[:t], 0, N) if t > 0 else np.zeros((0, N))
+    tail_cols = entries(plan.kind, x[t:], 0, t) if t > 0 else np.zeros((N, 0))
+    return Operator2D(plan, D2, W, tail_rows, tail_cols)
+
+
+def apply_2d(op: Operator2D, C: np.ndarray) -> np.ndarray:
+    """Y = D C (values at the grid from Laguerre coefficients, the backward transform of P:528):
+    per degree block a, z_a = F* W_a^-1 pad_a(C) (Alg. 1 prologue); per time block b,
+    u_b = sum_a D2_ab z_a, v_b = F* u_b, Y[kept_b] = v_b / w_b (Alg. 2 epilogue, P:218);
+    tails by the direct method: rows i < t in full, columns j < t for i >= t."""
+    plan = op.plan
+    C = np.asarray(C, dtype=np.float64)
+    N, B = C.shape
+    Y = np.zeros((N, B))
+    zs = []
+    for a, wa in zip(plan.blocks, op.windows):
+        z = np.zeros((a.L, B))
+        z[a.keep_lo:a.keep_hi] = C[a.keep_lo:a.keep_hi] / wa[a.keep_lo:a.keep_hi, None]
+        zs.append(np.fft.ifft(z, axis=0, norm="ortho"))
+    for b, wb, row in zip(plan.blocks, op.windows, op.D2):
+        u = np.zeros((b.L, B), dtype=np.complex128)
+        for S, z in zip(row, zs):
+            u += S @ z
+        v = np.fft.ifft(u, axis=0, norm="ortho").real      # Hermitian u: real up to rounding
+        Y[b.keep_lo:b.keep_hi] = v[b.keep_lo:b.keep_hi] / wb[b.keep_lo:b.keep_hi, None]
+    t = plan.tail
+    if t > 0:
+        Y[t:] += op.tail_cols @ C[:t]
+        Y[:t] = op.tail_rows @ C
+    return Y
+
+
+def nnz_2d(op: Operator2D, half: bool = True) -> int:
+    """Kept entries of all block pairs (half: rows k <= L_b/2 only, the Hermitian half stored)."""
+    tot = 0
+    for b, row in zip(op.plan.blocks, op.D2):
+        for S in row:
+            tot += S[:b.L // 2 + 1].nnz if half else S.nnz
+    return tot
 
 
 # ---------------------------------------------------------------------------

@@ -11,7 +11,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-KIND_COS, KIND_JACOBI, KIND_LAGUERRE, KIND_EXP, KIND_LAGSPEC = 1, 2, 3, 4, 5
+KIND_COS, KIND_JACOBI, KIND_LAGUERRE, KIND_EXP, KIND_LAGSPEC, KIND_LAG2D = 1, 2, 3, 4, 5, 6
 
 
 @dataclass(frozen=True)
@@ -44,6 +44,9 @@ CONFIGS = {
     # NEXT-3 second half: the spectral Laguerre forward V = C^T F at the sizes of the paper's
     # Fig. lag_row: C^T is 649 x 501, eta = 2500, k_j = 2 pi j / T, T = 4 s
     "c7": Config("c7_lagspec_649x501", KIND_LAGSPEC, 501, 64, 1e-10, 7, M=649, eta=2500.0, T=4.0),
+    # NEXT-1: the time-domain Laguerre series sum D c, D[i,j] = l_j(eta t_i), t_i = 12 i / (N-1)
+    # (P:528), by the 2D block method; eps2 = 0.1 (R-23: errors pass two window divisions)
+    "c8": Config("c8_lag2d_4096", KIND_LAG2D, 4096, 256, 1e-10, 8, eps2=0.1, eta=100.0),
 }
 
 
@@ -62,6 +65,11 @@ def exp_nodes(N: int, seed: int) -> np.ndarray:
 def lagspec_freqs(N: int, T: float) -> np.ndarray:
     """Fourier frequencies k_j = 2 pi j / T, j = 0..N-1 (Fig. lag_row caption); no draw."""
     return 2.0 * np.pi * np.arange(N, dtype=np.float64) / T
+
+
+def lag2d_grid(N: int, eta: float) -> np.ndarray:
+    """x_i = eta t_i, t_i = 12 i / (N - 1), i = 1..N; no draw."""
+    return eta * 12.0 * np.arange(1, N + 1, dtype=np.float64) / (N - 1)
 
 
 def complex_rhs(N: int, B: int, seed: int, skip_nodes: bool = True) -> np.ndarray:
