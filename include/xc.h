@@ -54,12 +54,17 @@ typedef enum {
                        parts in rows [N,2N), same ld; the full spectrum of L bins is kept.
                        May be rectangular: p->n_rows = M degrees (rows) != N nodes; then
                        XC_DIR_A maps 2N planar rows to 2M, XC_DIR_WAT 2M to 2N.                  */
-  XC_LAGSPEC = 5    /* the spectral Laguerre forward V = C^T F (Fig. lag_row):
+  XC_LAGSPEC = 5,   /* the spectral Laguerre forward V = C^T F (Fig. lag_row):
                        A[m,j] = (-eta/2 - i k_j)^m / (eta/2 - i k_j)^(m+1), m < M = p->n_rows
                        (0 => N), nodes = frequencies k_j (finite, strictly ascending, any sign),
                        eta = p->eta > 0.  Computed as XC_EXP at t_j = 1 + (2/pi) atan(2 k_j/eta)
                        with the per-node scale 1/(eta/2 - i k_j) folded into the operator (R-21);
                        complex planar X / Y as XC_EXP, both directions.                          */
+  XC_LAG2D = 6      /* the time-domain Laguerre sum Y = D X, D[i,j] = l_j(x_i) = exp(-x_i/2) L_j(x_i),
+                       i, j < N, on an EQUISPACED grid x_i >= 0 (nodes ascending, spacing equal to
+                       1e-9 relative), by the 2D block method (R-23): the
+                       block chain on both axes, D2 = F W D W F per block pair.  XC_DIR_A only
+                       (output indexed by node); eps2 defaults to 0.1 for this kind.             */
 } xc_kind;
 
 typedef enum {

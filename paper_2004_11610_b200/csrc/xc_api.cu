@@ -70,6 +70,7 @@ struct BlockData {
   int64_t nnz = 0;
   int max_band = 0;
   int appQ = -1;  // Appendix A precompute: Q of the truncated window spectrum (-1: direct)
+  DevBuf ptr2d, ent2d;  // XC_LAG2D: CSR of the Hermitian half of sum_a D2_ab (this block = b)
   int ngroups = 0;
   int64_t loc_count = 0;  // values of the locally computed node range (distributed precompute)
   DevBuf grp_base, grp_nch;  // output axis groups
@@ -88,6 +89,7 @@ struct xc_op {
   int kind = 0;   // machinery kind (XC_LAGSPEC runs as XC_EXP, R-21)
   int ukind = 0;  // the kind the caller built
   bool appA = false;  // Appendix A trig precompute (R-22)
+  DevBuf tailR, tailC;  // XC_LAG2D: direct-method tails (rows i < t: N x t; columns j < t: t x (N-t))
   double alpha = 0, beta = 0;
   int64_t N = 0;  // nodes
   int64_t M = 0;  // degrees (rows of A); == N unless rectangular
@@ -169,16 +171,17 @@ xc_status ensure_ws(xc_op* h, int64_t B) {
   if (B <= h->ws_B) return XC_OK;
   int64_t Bp = pad_cols(B);
   size_t scratch_n = 0;
+  const bool two_d = h->ukind == XC_LAG2D;  // prologue planes (as XC_DIR_WAT) + C2R (as XC_DIR_A)
   for (auto& b : h->blocks) {
-    if ((h->dirs & XC_DIR_WAT) && b.fft.L2 > 1) scratch_n = std::max(scratch_n, (size_t)b.L * (size_t)B);
+    if ((two_d || (h->dirs & XC_DIR_WAT)) && b.fft.L2 > 1) scratch_n = std::max(scratch_n, (size_t)b.L * (size_t)B);
     if ((h->dirs & XC_DIR_A) && b.fftM.L2 > 1) scratch_n = std::max(scratch_n, (size_t)b.fftM.L * (size_t)B);
     if ((h->dirs & XC_DIR_A) && h->kind == XC_EXP && b.fft.L2 > 1)  // C2C inverse of length L
       scratch_n = std::max(scratch_n, (size_t)b.L * (size_t)B);
   }
   XC_TRY(dev_alloc(h->scratch, std::max<size_t>(1, scratch_n) * sizeof(double2)));
   if (h->dirs & XC_DIR_A) XC_TRY(dev_alloc(h->partA, (size_t)h->rowsA * Bp * sizeof(double)));
-  if (h->dirs & XC_DIR_WAT) {
-    XC_TRY(dev_alloc(h->partW, (size_t)h->rowsW * Bp * sizeof(double)));
+  if ((h->dirs & XC_DIR_WAT) || two_d) {
+    if (!two_d) XC_TRY(dev_alloc(h->partW, (size_t)h->rowsW * Bp * sizeof(double)));
     h->zoff.clear();
     int64_t tot = 0;
     for (auto& b : h->blocks) {
@@ -207,7 +210,15 @@ xc_status validate_nodes(int kind, const double* x, int64_t N) {
   if (kind == XC_COS) ok = x[0] >= 0.0 && x[N - 1] <= 1.0;
   if (kind == XC_EXP) ok = x[0] >= 0.0 && x[N - 1] < 2.0;
   if (kind == XC_JACOBI) ok = x[0] >= -1.0 && x[N - 1] <= 1.0;
-  if (kind == XC_LAGUERRE) ok = x[0] >= 0.0;  // XC_LAGSPEC: any real frequency
+  if (kind == XC_LAGUERRE || kind == XC_LAG2D) ok = x[0] >= 0.0;  // XC_LAGSPEC: any real frequency
+  if (ok && kind == XC_LAG2D && N > 2) {  // equispaced (the extra rows continue the grid, R-23)
+    const double hh = (x[N - 1] - x[0]) / (double)(N - 1);
+    for (int64_t k = 1; k < N && ok; ++k) ok = fabs((x[k] - x[k - 1]) - hh) <= 1e-9 * fmax(hh, fabs(x[k]));
+    if (!ok) {
+      xc_set_error("XC_LAG2D: nodes must be equispaced");
+      return XC_EINVAL;
+    }
+  }
   if (!ok) {
     xc_set_error("nodes: outside the domain of the kind");
     return XC_EINVAL;
@@ -216,9 +227,9 @@ xc_status validate_nodes(int kind, const double* x, int64_t N) {
 }
 
 // --- the per-block precompute: entries -> FFT -> threshold -> node bands ------------
-xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int node_chunk, int n0, int n1,
-                      cudaStream_t st) {
-  const int N = (int)h->N;
+// Per block: FFT plans, twiddles, the window and its derived scales (and, for the Appendix A
+// precompute, the truncated window spectrum in dxq).
+xc_status block_setup(xc_op* h, BlockData& b, DevBuf& dxq) {
   const bool cplx_rows = h->kind == XC_EXP;  // complex rows: the full spectrum (no Hermitian half)
   b.H = cplx_rows ? b.L : b.L / 2 + 1;
   XC_TRY(fft_plan_make(b.fft, b.L));
@@ -233,7 +244,6 @@ xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int n
     XC_TRY(upload(b.twh, tw));
   }
   kaiser_window(h->zeta, b.L, b.h_w);
-  DevBuf dxq;
   if (h->appA) {  // R-22: the truncated window W' = F* xq is the method's window from here on
     std::vector<double2> xq;
     std::vector<double> wq;
@@ -250,6 +260,15 @@ xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int n
   XC_TRY(upload(b.w, b.h_w));
   XC_TRY(upload(b.yscale, ys));
   XC_TRY(upload(b.winv, wi));
+  return XC_OK;
+}
+
+xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int node_chunk, int n0, int n1,
+                      cudaStream_t st) {
+  const int N = (int)h->N;
+  const bool cplx_rows = h->kind == XC_EXP;
+  DevBuf dxq;
+  XC_TRY(block_setup(h, b, dxq));
 
   // chunk the nodes so that F, the FFT scratch and the spectra (48 B per position and node) take
   // at most a third of the free device memory (capped at 48 GB): the entry recurrence runs one
@@ -804,7 +823,8 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
   xc_params p;
   xc_params_default(&p);
   if (prm) p = *prm;
-  if (kind != XC_COS && kind != XC_JACOBI && kind != XC_LAGUERRE && kind != XC_EXP && kind != XC_LAGSPEC) {
+  if (kind != XC_COS && kind != XC_JACOBI && kind != XC_LAGUERRE && kind != XC_EXP && kind != XC_LAGSPEC &&
+      kind != XC_LAG2D) {
     xc_set_error("unknown kind");
     return XC_EINVAL;
   }
@@ -830,7 +850,7 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
     xc_set_error("eps must be in (0,1)");
     return XC_EINVAL;
   }
-  h->kind = kind == XC_LAGSPEC ? XC_EXP : kind;
+  h->kind = kind == XC_LAGSPEC ? XC_EXP : (kind == XC_LAG2D ? XC_LAGUERRE : kind);
   h->ukind = kind;
   h->appA = p.trig_precompute == 1;
   h->alpha = p.alpha;
@@ -838,8 +858,12 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
   h->N = N;
   h->M = M;
   h->eps1 = p.eps1 > 0 ? p.eps1 : eps;
-  h->eps2 = p.eps2 > 0 ? p.eps2 : 1e-2;
+  h->eps2 = p.eps2 > 0 ? p.eps2 : (kind == XC_LAG2D ? 0.1 : 1e-2);
   h->dirs = p.dirs ? p.dirs : XC_DIR_A;
+  if (kind == XC_LAG2D && h->dirs != XC_DIR_A) {
+    xc_set_error("XC_LAG2D: XC_DIR_A only");
+    return XC_EUNSUPPORTED;
+  }
   h->device = p.device;
   if (!(h->eps1 < h->eps2) || !(h->eps2 < 1.0)) {
     xc_set_error("need eps1 < eps2 < 1");
@@ -891,6 +915,16 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
     XC_TRY(upload(h->nodes, th));
     XC_TRY(upload(h->nodes_lo, tl));
     XC_TRY(upload(h->cscale, sc));
+  } else if (kind == XC_LAG2D) {
+    // the grid continued past x_{N-1} for the extra rows of the 2D blocks (as the oracle's
+    // lag2d_nodes_ext: x_{N-1} + i h, h = (x_{N-1} - x_0) / (N - 1))
+    std::vector<double> xe(nodes, nodes + N);
+    const double hh = (nodes[N - 1] - nodes[0]) / (double)(N - 1);
+    for (int64_t i = 1; N - 1 + i < std::max<int64_t>(N, Lmax); ++i) {
+      volatile double d = hh * (double)i;  // no contraction: the same two roundings as the oracle
+      xe.push_back(nodes[N - 1] + d);
+    }
+    XC_TRY(upload(h->nodes, xe));
   } else {
     XC_TRY(upload(h->nodes, std::vector<double>(nodes, nodes + N)));
   }
@@ -975,8 +1009,161 @@ xc_status build_end(xc_op* h) {
   return XC_OK;
 }
 
+// XC_LAG2D (R-23): per block pair (a = degree block, b = time block) the extended block E_ab,
+// windowed on both axes, its 2D DFT (degree axis, transpose, time axis; rows k <= L_b/2 kept),
+// the global threshold, then per time block the rows of all pairs merged into one CSR whose
+// entries point at the prologue planes of their degree block.
+xc_status build_2d(xc_op* h) {
+  cudaStream_t st = h->bst;
+  const int N = (int)h->N, t = h->tail, nb = (int)h->blocks.size();
+  DevBuf none;
+  for (auto& b : h->blocks) XC_TRY(block_setup(h, b, none));
+  std::vector<int64_t> zrow(nb + 1, 0);  // prologue plane rows of degree block a: re then im
+  for (int a = 0; a < nb; ++a) zrow[a + 1] = zrow[a] + 2 * (int64_t)h->blocks[a].H;
+  int Lmax = 0;
+  for (auto& b : h->blocks) Lmax = std::max(Lmax, b.L);
+  DevBuf F, S1, T, S2, scr, dmx, dcnt;
+  const size_t big = (size_t)Lmax * Lmax * sizeof(double2);
+  XC_TRY(dev_alloc(F, big));
+  XC_TRY(dev_alloc(S1, big));
+  XC_TRY(dev_alloc(T, big));
+  XC_TRY(dev_alloc(S2, big));
+  XC_TRY(dev_alloc(scr, big));
+  XC_TRY(dev_alloc(dmx, sizeof(unsigned long long)));
+  XC_TRY(dev_alloc(dcnt, (size_t)Lmax * sizeof(int)));
+  int64_t total = 0;
+  h->rowsA = 0;  // the apply's u_b buffer (Hermitian half, complex): 2 H_b double rows
+  for (auto& b : h->blocks) h->rowsA = std::max<int64_t>(h->rowsA, 2 * (int64_t)b.H);
+  for (int ib = 0; ib < nb; ++ib) {
+    BlockData& bb = h->blocks[ib];
+    const int Lb = bb.L, Hb = bb.H;
+    std::vector<std::vector<int64_t>> pptr(nb);
+    std::vector<std::vector<int>> pq(nb);
+    std::vector<std::vector<double2>> pv(nb);
+    for (int ia = 0; ia < nb; ++ia) {
+      BlockData& ba = h->blocks[ia];
+      const int La = ba.L;
+      GenParams g{};
+      g.kind = XC_LAGUERRE;
+      g.L = La;
+      g.m_off = 0;
+      g.nodes = (const double*)h->nodes.p;  // time positions p < L_b: x_p of the continued grid
+      g.nc = Lb;
+      g.w = (const double*)ba.w.p;           // degree window W_a
+      XC_TRY(gen_entries(g, (double2*)F.p, st));  // F[q * L_b + p] = w_a[q] l_q(x_p)
+      XC_TRY(lag2d_scale_nodes((double2*)F.p, La, Lb, (const double*)bb.w.p, st));  // W_b
+      FftIO io{};
+      io.src = (const double2*)F.p;
+      io.lds = Lb;
+      io.dst = (double2*)S1.p;
+      io.ldd = Lb;
+      io.kmax = La;
+      io.scale = 1.0 / sqrt((double)La);
+      XC_TRY(fft_run(ba.fft, -1, PRO_PLAIN, EPI_PLAIN, io, Lb, (double2*)scr.p, st));  // degree axis
+      XC_TRY(lag2d_transpose((const double2*)S1.p, (double2*)T.p, La, Lb, st));    // T[p * L_a + q]
+      FftIO io2{};
+      io2.src = (const double2*)T.p;
+      io2.lds = La;
+      io2.dst = (double2*)S2.p;
+      io2.ldd = La;
+      io2.kmax = Hb;  // the Hermitian half of the time axis
+      io2.scale = 1.0 / sqrt((double)Lb);
+      XC_TRY(fft_run(bb.fft, -1, PRO_PLAIN, EPI_PLAIN, io2, La, (double2*)scr.p, st));  // time axis
+      DevBuf dq, dv;
+      XC_TRY(lag2d_compact_rows((const double2*)S2.p, Hb, La, h->eps1, (unsigned long long*)dmx.p, (int*)dcnt.p,
+                                pptr[ia], dq, dv, st));
+      const int64_t n = pptr[ia][Hb];
+      pq[ia].resize(n);
+      pv[ia].resize(n);
+      if (n > 0) {
+        XC_CUDA(cudaMemcpy(pq[ia].data(), dq.p, n * sizeof(int), cudaMemcpyDeviceToHost));
+        XC_CUDA(cudaMemcpy(pv[ia].data(), dv.p, n * sizeof(double2), cudaMemcpyDeviceToHost));
+      }
+      dev_free(dq);
+      dev_free(dv);
+    }
+    // merge the pairs row by row (degree blocks in order, q ascending)
+    std::vector<int64_t> ptr(Hb + 1, 0);
+    for (int k = 0; k < Hb; ++k) {
+      int64_t c = 0;
+      for (int ia = 0; ia < nb; ++ia) c += pptr[ia][k + 1] - pptr[ia][k];
+      ptr[k + 1] = ptr[k] + c;
+    }
+    std::vector<Ent2D> ent(ptr[Hb]);
+    for (int k = 0; k < Hb; ++k) {
+      int64_t o = ptr[k];
+      for (int ia = 0; ia < nb; ++ia) {
+        const int La = h->blocks[ia].L, Ha = h->blocks[ia].H;
+        for (int64_t e = pptr[ia][k]; e < pptr[ia][k + 1]; ++e) {
+          const int q = pq[ia][e];
+          const bool cj = q >= Ha;  // z_a[q] = conj z_a[L_a - q] (real input)
+          const int r = cj ? La - q : q;
+          Ent2D en;
+          en.v = pv[ia][e];
+          en.re = (int)(zrow[ia] + r);
+          en.im = (int)(zrow[ia] + Ha + r);
+          if (cj) en.im = -en.im - 1;
+          ent[o++] = en;
+        }
+      }
+    }
+    XC_TRY(upload(bb.ptr2d, ptr));
+    XC_TRY(upload(bb.ent2d, ent));
+    bb.nnz = ptr[Hb];
+    total += bb.nnz;
+  }
+  dev_free(F);
+  dev_free(S1);
+  dev_free(T);
+  dev_free(S2);
+  dev_free(scr);
+  dev_free(dmx);
+  dev_free(dcnt);
+  // direct-method tails: E[j * ld + k] = l_j(x_k)
+  if (t > 0) {
+    XC_TRY(dev_alloc(h->tailR, (size_t)N * t * sizeof(double)));
+    XC_TRY(dev_alloc(h->tailC, (size_t)t * (N - t) * sizeof(double)));
+    GenParams g{};
+    g.kind = XC_LAGUERRE;
+    g.m_off = 0;
+    g.w = nullptr;
+    g.L = N;
+    g.nodes = (const double*)h->nodes.p;
+    g.nc = t;
+    XC_TRY(gen_entries_real(g, (double*)h->tailR.p, t, st));
+    g.L = t;
+    g.nodes = (const double*)h->nodes.p + t;
+    g.nc = N - t;
+    XC_TRY(gen_entries_real(g, (double*)h->tailC.p, N - t, st));
+  }
+  XC_CUDA(cudaStreamSynchronize(st));
+  // info
+  xc_info_t& in = h->info;
+  in.N = N;
+  in.M = N;
+  in.kind = XC_LAG2D;
+  in.zeta = h->zeta;
+  in.eps1 = h->eps1;
+  in.eps2 = h->eps2;
+  in.n_blocks = nb;
+  in.tail = t;
+  in.dirs = h->dirs;
+  in.nnz = total;
+  double fft = 0;
+  for (auto& b : h->blocks) fft += 2.0 * fft_flops(b.L);  // the prologue and the C2R epilogue
+  // complex x complex: 4 FMA per stored entry; tails: 2 t N - t^2 FMA
+  in.flops_per_col_A = 8.0 * total + 2.0 * (2.0 * t * N - (double)t * t) + fft;
+  in.flops_per_col_WAT = 0;
+  in.op_bytes_A = total * (int64_t)sizeof(Ent2D);
+  int fl = 0;
+  for (auto& b : h->blocks) fl += ((b.fft.L2 > 1) ? 2 : 1) + ((b.fftM.L2 > 1) ? 2 : 1) + 1;
+  in.launches_A = fl + (t > 0 ? 2 : 0);
+  return XC_OK;
+}
+
 xc_status build_impl(xc_kind kind, const xc_params* prm, const double* nodes, int64_t N, double eps, xc_op* h) {
   XC_TRY(build_begin(kind, prm, nodes, N, eps, h));
+  if (h->ukind == XC_LAG2D) return build_2d(h);
   XC_TRY(build_bands(h, 0, (int)N));
   return build_end(h);
 }
@@ -1033,6 +1220,54 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
   const int64_t Bp = pad_cols(B);
   const int N = (int)h->N;
   XC_TRY(mark(0));
+  if (h->ukind == XC_LAG2D) {  // R-23: prologues, merged 2D products + C2R per time block, tails
+    const int nb = (int)h->blocks.size();
+    int64_t zrow = 0;  // plane rows of the degree blocks, stacked with the row stride Bp of this call
+    for (int a = 0; a < nb; ++a) {
+      BlockData& b = h->blocks[a];
+      FftIO io{};
+      io.X = X;
+      io.ldx = ldx;
+      io.winv = (const double*)b.winv.p;
+      io.keep_lo = b.keep_lo;
+      io.keep_hi = b.keep_hi;
+      io.m_off = b.m_off;
+      io.zre = (double*)h->zpl.p + zrow * Bp;  // the rows the CSR entries address (build_2d)
+      zrow += 2 * (int64_t)b.H;
+      io.zim = io.zre + (int64_t)b.H * Bp;
+      io.ldz = Bp;
+      io.H = b.H;
+      io.scale = 1.0 / sqrt((double)b.L);
+      XC_TRY(fft_run(b.fft, +1, PRO_XREAL, EPI_ZPLANES, io, (int)B, (double2*)h->scratch.p, st));
+    }
+    XC_TRY(mark(1));
+    double2* U = (double2*)h->partA.p;
+    for (int ib = 0; ib < nb; ++ib) {
+      BlockData& b = h->blocks[ib];
+      XC_TRY(lag2d_spmm((const int64_t*)b.ptr2d.p, (const Ent2D*)b.ent2d.p, b.H, (const double*)h->zpl.p, Bp, U,
+                        Bp, (int)B, st));
+      FftIO io{};
+      io.Uc = U;
+      io.ldu = Bp;
+      io.twh = (const double2*)b.twh.p;
+      io.M = b.L / 2;
+      io.H = b.H;
+      io.Y = Y;
+      io.ldy = ldy;
+      io.yscale = (const double*)b.yscale.p;
+      io.keep_lo = b.keep_lo;
+      io.keep_hi = b.keep_hi;
+      io.m_off = b.m_off;
+      XC_TRY(c2r_run(b.fftM, io, (int)B, (double2*)h->scratch.p, st));
+    }
+    XC_TRY(mark(2));
+    const int t = h->tail;
+    if (t > 0) {
+      XC_TRY(dense_tn((const double*)h->tailR.p, N, t, t, X, ldx, Y, ldy, (int)B, false, st));
+      XC_TRY(dense_tn((const double*)h->tailC.p, t, N - t, N - t, X, ldx, Y + (int64_t)t * ldy, ldy, (int)B, true, st));
+    }
+    return mark(3);
+  }
   if (dir == XC_DIR_A && h->kind == XC_EXP) {
     // complex input in planar form: B row 2k = Re X[k], 2k+1 = Im X[k] (rows N.. are the imag plane)
     SpmmSrcs s{};
@@ -1192,11 +1427,12 @@ void destroy_impl(xc_op* h) {
     dev_free(b.twh);
     dev_free(b.w); dev_free(b.yscale); dev_free(b.winv);
     dev_free(b.start); dev_free(b.len); dev_free(b.off); dev_free(b.vals);
-    dev_free(b.grp_base); dev_free(b.grp_nch);
+    dev_free(b.grp_base); dev_free(b.grp_nch); dev_free(b.ptr2d); dev_free(b.ent2d);
   }
   DevBuf* all[] = {&h->nodes, &h->wt, &h->tailP, &h->itemsA, &h->tilesA, &h->winsA, &h->tail_base, &h->tail_nch,
                    &h->itemsW, &h->tilesW, &h->winsW, &h->nodeg_base, &h->nodeg_nch, &h->nodeg_base_im, &h->partA, &h->partW,
-                   &h->scratch, &h->zpl, &h->Xh, &h->Yh, &h->xsend, &h->xrecv, &h->djtab, &h->nodes_lo, &h->cscale};
+                   &h->scratch, &h->zpl, &h->Xh, &h->Yh, &h->xsend, &h->xrecv, &h->djtab, &h->nodes_lo, &h->cscale,
+                   &h->tailR, &h->tailC};
   for (DevBuf* b : all) dev_free(*b);
 }
 
@@ -1339,6 +1575,10 @@ xc_status xc_build_local(xc_kind kind, const xc_params* p, const double* nodes, 
     delete h;
     return s;
   };
+  if (kind == XC_LAG2D) {
+    xc_set_error("build_local: XC_LAG2D has no distributed precompute");
+    return fail(XC_EUNSUPPORTED);
+  }
   xc_status s = build_begin(kind, p, nodes, N, eps, h);
   if (s != XC_OK) return fail(s);
   h->rank = rank;
@@ -1592,15 +1832,16 @@ xc_status xc_workspace_query(xc_handle h, int64_t B, size_t* bytes) {
   if (!h || !bytes || B < 1) return XC_EINVAL;
   int64_t Bp = pad_cols(B);
   size_t s = 0, scr = 0;
+  const bool two_d = h->ukind == XC_LAG2D;
   for (auto& b : h->blocks) {
-    if ((h->dirs & XC_DIR_WAT) && b.fft.L2 > 1) scr = std::max(scr, (size_t)b.L * B * sizeof(double2));
+    if ((two_d || (h->dirs & XC_DIR_WAT)) && b.fft.L2 > 1) scr = std::max(scr, (size_t)b.L * B * sizeof(double2));
     if ((h->dirs & XC_DIR_A) && b.fftM.L2 > 1) scr = std::max(scr, (size_t)b.fftM.L * B * sizeof(double2));
     if ((h->dirs & XC_DIR_A) && h->kind == XC_EXP && b.fft.L2 > 1) scr = std::max(scr, (size_t)b.L * B * sizeof(double2));
   }
   s += scr;
   if (h->dirs & XC_DIR_A) s += (size_t)h->rowsA * Bp * 8;
-  if (h->dirs & XC_DIR_WAT) {
-    s += (size_t)h->rowsW * Bp * 8;
+  if ((h->dirs & XC_DIR_WAT) || two_d) {
+    if (!two_d) s += (size_t)h->rowsW * Bp * 8;
     for (auto& b : h->blocks) s += (size_t)2 * b.H * Bp * 8;
   }
   *bytes = s;
@@ -1637,7 +1878,7 @@ xc_status xc_block_window(xc_handle h, int i, double* w) {
 }
 
 xc_status xc_node_spectrum(xc_handle h, int i, int64_t k, double* re, double* im) {
-  if (!h || !re || !im || i < 0 || i >= (int)h->blocks.size() || k < 0 || k >= h->N) {
+  if (!h || !re || !im || i < 0 || i >= (int)h->blocks.size() || k < 0 || k >= h->N || h->ukind == XC_LAG2D) {
     xc_set_error("node_spectrum: bad arguments");
     return XC_EINVAL;
   }

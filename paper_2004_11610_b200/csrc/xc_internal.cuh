@@ -275,6 +275,20 @@ xc_status appa_spectra(int kind, int L, int H, int m_off, int Q, int W, const do
                        const double2* cscale, const double2* xq, int nc, double eps1, double2* spec, int* flag,
                        cudaStream_t st, AppAWin* wm = nullptr);
 xc_status appa_store(const AppAWin& wm, int W, const int64_t* off, double2* vals, int nc, cudaStream_t st);
+// 2D block method (lag2d.cu, R-23): one kept entry of a D2 row: value and the rows of the
+// prologue planes it multiplies (re plane row; im plane row, negative -r-1 = conjugate)
+struct Ent2D {
+  double2 v;
+  int re, im;
+};
+xc_status lag2d_scale_nodes(double2* F, int L, int nc, const double* w, cudaStream_t st);
+xc_status lag2d_transpose(const double2* in, double2* out, int R, int C, cudaStream_t st);
+xc_status lag2d_compact_rows(const double2* S, int rows, int cols, double eps1, unsigned long long* dmx, int* dcnt,
+                             std::vector<int64_t>& ptr, DevBuf& q, DevBuf& v, cudaStream_t st);
+xc_status lag2d_spmm(const int64_t* ptr, const Ent2D* ent, int rows, const double* z, int64_t ldz, double2* U,
+                     int64_t ldu, int B, cudaStream_t st);
+xc_status dense_tn(const double* E, int J, int K, int64_t ldE, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                   int B, bool acc, cudaStream_t st);
 xc_status band_detect(const double2* spec, int H, int nc, double eps1, int* start, int* len, bool circ,
                       cudaStream_t st);
 xc_status band_store(const double2* spec, int H, int nc, double eps1, const int* start, const int* len,

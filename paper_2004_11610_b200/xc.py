@@ -14,7 +14,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libxc.so")
 
-XC_COS, XC_JACOBI, XC_LAGUERRE, XC_EXP, XC_LAGSPEC = 1, 2, 3, 4, 5
+XC_COS, XC_JACOBI, XC_LAGUERRE, XC_EXP, XC_LAGSPEC, XC_LAG2D = 1, 2, 3, 4, 5, 6
 COMPLEX_KINDS = (XC_EXP, XC_LAGSPEC)  # planar complex X / Y (real rows, then imaginary rows)
 XC_DIR_A, XC_DIR_WAT = 1, 2
 _STATUS = {0: "XC_OK", 1: "XC_EINVAL", 2: "XC_ENUMERIC", 3: "XC_ESTATE", 4: "XC_ENOMEM", 5: "XC_ECUDA",

@@ -653,6 +653,45 @@ def test_appA_precompute_parity(case):
     Td.close()
 
 
+LAG2D_CASES = [("c8", 4096, 256, 1e-10, 100.0), ("lag2d_small", 200, 5, 1e-12, 1000.0),
+               ("lag2d_ragged", 1000, 37, 1e-10, 500.0)]
+
+
+@pytest.mark.parametrize("case", LAG2D_CASES, ids=[c[0] for c in LAG2D_CASES])
+def test_lag2d_parity(case):
+    """NEXT-1: the time-domain Laguerre sum Y = D C (D[i,j] = l_j(eta t_i), t_i = 12 i/(N-1))
+    by the 2D block method (R-23) on the GPU vs the oracle's 2D operator (1e-12) and the dense
+    sum (10 eps); the kept count (Hermitian half) equals the oracle's up to threshold ties."""
+    xc = _xc()
+    name, N, B, eps, eta = case
+    x = I.lag2d_grid(N, eta)
+    C = I.rhs(N, B, 8)
+    T = xc.Transform(xc.XC_LAG2D, x, eps)
+    info = T.info()
+    assert info["kind"] == xc.XC_LAG2D and info["eps2"] == 0.1
+    plan = O.make_plan(O.Kind(O.KIND_LAGUERRE), N, eps, eps2=0.1)
+    op = O.compress_2d(plan, x)
+    assert abs(info["nnz"] - O.nnz_2d(op)) <= 1e-3 * O.nnz_2d(op) + 2
+    Y = T.apply(torch.from_numpy(C).cuda()).cpu().numpy()
+    assert O.rel_l2_cols(Y, O.apply_2d(op, C)).max() <= 1e-12, name
+    cols = np.arange(min(B, 8))
+    assert O.rel_l2_cols(Y[:, cols], O.dense_apply_t(O.Kind(O.KIND_LAGUERRE), x, C[:, cols])).max() <= 10 * eps
+    Yh = T.apply_host(C)
+    assert O.rel_l2_cols(Yh, Y).max() <= 1e-15
+    T.close()
+
+
+def test_lag2d_errors():
+    xc = _xc()
+    x = I.lag2d_grid(100, 100.0)
+    xb = x.copy()
+    xb[50] += 1e-3
+    with pytest.raises(xc.XcError, match="XC_EINVAL"):
+        xc.Transform(xc.XC_LAG2D, xb, 1e-10)                   # not equispaced
+    with pytest.raises(xc.XcError, match="XC_EUNSUPPORTED"):
+        xc.Transform(xc.XC_LAG2D, x, 1e-10, dirs=xc.XC_DIR_A | xc.XC_DIR_WAT, weights=np.ones(100))
+
+
 @pytest.mark.parametrize("L,B", [(86400, 64), (27648, 64), (9000, 96), (2916, 64), (960, 64), (360, 8),
                                  (21600, 32), (10800, 64), (7200, 64), (1152, 40), (720, 1), (60, 3)])
 def test_c2r_engine_vs_numpy(L, B):
