@@ -92,6 +92,10 @@ def _nodes(cfg, device):
         return I.cos_nodes(cfg.N, cfg.seed), None
     if cfg.kind == I.KIND_EXP:
         return I.exp_nodes(cfg.N, cfg.seed), None
+    if cfg.kind == I.KIND_LAGSPEC:
+        return I.lagspec_freqs(cfg.N, cfg.T), None
+    if cfg.kind == I.KIND_LAG2D:
+        return I.lag2d_grid(cfg.N, cfg.eta), None
     x, w, wt = xc.gauss_rule(cfg.kind, cfg.N, cfg.alpha, cfg.beta, device=device)
     return x, wt
 
@@ -104,6 +108,10 @@ def _timing_nodes(cfg):
         return I.cos_nodes(cfg.N, cfg.seed)
     if cfg.kind == I.KIND_EXP:
         return I.exp_nodes(cfg.N, cfg.seed)
+    if cfg.kind == I.KIND_LAGSPEC:
+        return I.lagspec_freqs(cfg.N, cfg.T)
+    if cfg.kind == I.KIND_LAG2D:
+        return I.lag2d_grid(cfg.N, cfg.eta)
     if cfg.kind == I.KIND_LAGUERRE:
         return np.linspace(0.0, 4.0 * cfg.N, cfg.N)   # scipy's Laguerre rule overflows at this N
     if cfg.alpha == 0.0 and cfg.beta == 0.0:
@@ -116,13 +124,16 @@ def cpu_oracle_rate(cfg, ncols, ndeg, threads, x=None):
     sample: ncols columns x output degrees [0, ndeg); rate extrapolated per full transform."""
     import oracle as O
     os.environ["OMP_NUM_THREADS"] = str(threads)
-    kind = O.Kind(cfg.kind, cfg.alpha, cfg.beta)
+    kind = O.Kind(cfg.kind, cfg.alpha, cfg.beta, eta=cfg.eta)
     if x is None:
         x = _timing_nodes(cfg)
     X = I.config_rhs(cfg, B=max(ncols, 1))[:, :ncols]
     t0 = time.perf_counter()
-    if cfg.kind == I.KIND_EXP:   # complex: the oracle's dense product over all rows
-        O.dense_apply(kind, x, X)
+    if cfg.kind in (I.KIND_EXP, I.KIND_LAGSPEC):   # complex: the oracle's dense product over all rows
+        O.dense_apply(kind, x, X, M=cfg.M or None)
+        ndeg = cfg.N
+    elif cfg.kind == I.KIND_LAG2D:   # the series sum D C = the transposed Laguerre product, all rows
+        O.dense_apply_t(O.Kind(O.KIND_LAGUERRE), x, X)
         ndeg = cfg.N
     else:
         O.dense_apply_rows(kind, x, X, ndeg)
@@ -198,14 +209,15 @@ def main():
     t0 = time.perf_counter()
     # N > 1: distributed precompute (node range per rank, NCCL all-gather of the node bands)
     T = xc.Transform(cfg.kind, x, cfg.eps, alpha=cfg.alpha, beta=cfg.beta, dirs=dirs, weights=wt, device=local,
-                     dist=(rank, ws, xc.nccl_allgather()) if ws > 1 else None)
+                     dist=(rank, ws, xc.nccl_allgather()) if ws > 1 else None,
+                     eta=cfg.eta, n_rows=cfg.M, eps2=cfg.eps2 if cfg.eps2 != 1e-2 else 0.0)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     info = T.info()
 
     # ---- inputs: seeded on the host, this rank's shard, resident in HBM ----
     from paper_2004_11610_b200.shard import column_shard, max_over_ranks
-    if cfg.kind == I.KIND_EXP:   # complex RHS in the planar layout of the C ABI (2N rows)
+    if cfg.kind in (I.KIND_EXP, I.KIND_LAGSPEC):   # complex RHS, planar layout of the C ABI (2N rows)
         Xc = I.config_rhs(cfg, B=B)
         Xh = np.ascontiguousarray(np.concatenate([Xc.real, Xc.imag]))
     elif ws == 1:
@@ -218,7 +230,7 @@ def main():
         rng = np.random.default_rng(cfg.seed * 1000 + rank)
         Xh = rng.standard_normal((cfg.N, B))
     X = torch.from_numpy(Xh).cuda()
-    Y = torch.empty_like(X)
+    Y = torch.empty((T.rows(direction)[1], B), dtype=torch.float64, device=X.device)
     T.reserve(B)
     stream = torch.cuda.current_stream()
 
@@ -267,11 +279,13 @@ def main():
 
     # ---- roofline of the dominant kernel (SpMM on the FP64 tensor cores) ----
     nnz, tail, N = info["nnz"], info["tail"], info["N"]
-    cmul = 8.0 if cfg.kind == I.KIND_EXP else 4.0         # complex x complex / complex x real
+    cmul = 8.0 if cfg.kind in (I.KIND_EXP, I.KIND_LAGSPEC, I.KIND_LAG2D) else 4.0   # complex x complex / x real
     spmm_flops = (cmul * nnz + 2.0 * tail * N) * B          # algorithmic, per launch
     spmm_ms = prof["ms_spmm"] / max(1, prof["n"])
     fft_ms = prof["ms_fft"] / max(1, prof["n"])
     achieved = spmm_flops / (spmm_ms / 1e3) / 1e12
+    if cfg.kind == I.KIND_LAG2D:   # no dense tail inside the product launch (separate kernels)
+        spmm_flops = 8.0 * nnz * B
     alg_bytes = 16.0 * N * B + 20.0 * nnz + 8.0 * tail * N   # X in, Y out, operator once (SURVEY d.3)
     peaks = _peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
@@ -289,7 +303,7 @@ def main():
     e2e = None
     if args.e2e_steps > 0:
         Xp = torch.from_numpy(Xh).pin_memory()
-        Yp = torch.empty_like(Xp).pin_memory()
+        Yp = torch.empty(tuple(Y.shape), dtype=torch.float64).pin_memory()
         T.apply_host_ptr(Xp.data_ptr(), Yp.data_ptr(), B, direction, stream=stream.cuda_stream)
         if dist:
             dist.barrier()
@@ -305,7 +319,7 @@ def main():
         ems = (time.perf_counter() - tw0) * 1e3 / args.e2e_steps
         ems = max_over_ranks(ems, device="cuda")
         e2e = {"value": total_cols / (ems / 1e3), "unit": "transforms/s",
-               "h2d_bytes_per_step": int(sum_cols(Xh.nbytes)), "d2h_bytes_per_step": int(sum_cols(Xh.nbytes)),
+               "h2d_bytes_per_step": int(sum_cols(Xh.nbytes)), "d2h_bytes_per_step": int(sum_cols(8 * Y.numel())),
                "ms_per_step": ems,
                    "api": "xc_apply_host_async x steps + xc_host_wait (pinned host buffers; host wall clock)"}
 
@@ -333,10 +347,14 @@ def main():
             "hbm_gbs": alg_bytes / (ms / 1e3) / 1e9,
             "hbm_frac": alg_bytes / (ms / 1e3) / 1e9 / hbm_peak,
             "fp64_tflops": info["flops_per_col_A"] * B / (ms / 1e3) / 1e12,
-            "roofline": {"bound": "tensor", "kernel": "spmm_dmma (mma.m8n8k4.f64)", "achieved": achieved,
-                         "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / DMMA_PEAK_TFLOPS,
+            "roofline": ({"bound": "alu", "kernel": "csr2d (complex CSR product, DFMA)", "achieved": achieved,
+                          "peak": DFMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / DFMA_PEAK_TFLOPS,
+                          "peak_source": "measured DFMA microbenchmark (tools/fp64_peak.cu)"}
+                         if cfg.kind == I.KIND_LAG2D else
+                         {"bound": "tensor", "kernel": "spmm_dmma (mma.m8n8k4.f64)", "achieved": achieved,
+                          "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / DMMA_PEAK_TFLOPS,
+                          "peak_source": "measured DMMA microbenchmark (tools/fp64_peak.cu)"}) | {
                          "traffic": traffic, "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
-                         "peak_source": "measured DMMA microbenchmark (tools/fp64_peak.cu)",
                          "spmm_ms": spmm_ms, "fft_ms": fft_ms, "spmm_share": spmm_ms / ms,
                          "dmma_issue_efficiency": (cmul * nnz + 2.0 * tail * N) / max(1.0, info["dmma_flops_per_col_A"])},
             "cpu_baseline": cpu,

@@ -85,49 +85,71 @@ __global__ void scatter_rows_k(const double2* __restrict__ S, int rows, int cols
 }
 
 // u[k][col] = sum_e v_e * z_e[col]; z_e = zre[re_e] + i zim-row, conjugated when im_e < 0
-// (row index -im_e - 1).  One warp per row, lanes over columns (2 per lane per 64-column tile).
+// (row index -im_e - 1).  One warp per row; each lane owns CPL columns (lane + 32 c) of a
+// 32*CPL-column tile; the row's entries are fetched 32 at a time (one per lane, coalesced) and
+// broadcast with shuffles, so the z gathers of consecutive entries are independent loads.
+template <int CPL>
 __global__ void __launch_bounds__(256) csr2d_k(const int64_t* __restrict__ ptr, const Ent2D* __restrict__ ent,
                                                 int rows, const double* __restrict__ z, int64_t ldz,
                                                 double2* __restrict__ U, int64_t ldu, int B) {
   const int k = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (k >= rows) return;
-  const int c0 = blockIdx.y * 64 + lane, c1 = c0 + 32;
-  const bool a0 = c0 < B, a1 = c1 < B;
-  double r0 = 0, i0 = 0, r1 = 0, i1 = 0;
-  const int64_t e1 = ptr[k + 1];
-  for (int64_t e = ptr[k]; e < e1; ++e) {
-    const Ent2D en = ent[e];
-    const bool cj = en.im < 0;
-    const int64_t ri = cj ? -(int64_t)en.im - 1 : en.im;
-    const double* zr = z + (int64_t)en.re * ldz;
-    const double* zi = z + ri * ldz;
-    const double sg = cj ? -1.0 : 1.0;
-    if (a0) {
-      const double xr = zr[c0], xi = sg * zi[c0];
-      r0 = fma(en.v.x, xr, fma(-en.v.y, xi, r0));
-      i0 = fma(en.v.x, xi, fma(en.v.y, xr, i0));
-    }
-    if (a1) {
-      const double xr = zr[c1], xi = sg * zi[c1];
-      r1 = fma(en.v.x, xr, fma(-en.v.y, xi, r1));
-      i1 = fma(en.v.x, xi, fma(en.v.y, xr, i1));
+  const int cb = blockIdx.y * 32 * CPL + lane;
+  double ar[CPL], ai[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) ar[c] = ai[c] = 0.0;
+  const int64_t e0 = ptr[k], e1 = ptr[k + 1];
+  for (int64_t eb = e0; eb < e1; eb += 32) {
+    const int n = (e1 - eb) < 32 ? (int)(e1 - eb) : 32;
+    Ent2D mine = {make_double2(0.0, 0.0), 0, 0};
+    if (lane < n) mine = ent[eb + lane];
+    for (int j = 0; j < n; ++j) {
+      const double vx = __shfl_sync(0xffffffffu, mine.v.x, j), vy = __shfl_sync(0xffffffffu, mine.v.y, j);
+      const int re = __shfl_sync(0xffffffffu, mine.re, j), im = __shfl_sync(0xffffffffu, mine.im, j);
+      const bool cj = im < 0;
+      const double* zr = z + (int64_t)re * ldz;
+      const double* zi = z + (cj ? -(int64_t)im - 1 : (int64_t)im) * ldz;
+      const double sy = cj ? -vy : vy;  // conj(z): (xr, -xi); fold the sign into the value
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int col = cb + 32 * c;
+        if (col < B) {
+          const double xr = __ldg(zr + col), xi = __ldg(zi + col);
+          // (vx + i vy)(xr + i s xi), s = +-1:  re = vx xr - s vy xi,  im = s vx xi + vy xr
+          ar[c] = fma(vx, xr, fma(-sy, xi, ar[c]));
+          ai[c] = fma(cj ? -vx : vx, xi, fma(vy, xr, ai[c]));
+        }
+      }
     }
   }
-  if (a0) U[(int64_t)k * ldu + c0] = make_double2(r0, i0);
-  if (a1) U[(int64_t)k * ldu + c1] = make_double2(r1, i1);
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int col = cb + 32 * c;
+    if (col < B) U[(int64_t)k * ldu + col] = make_double2(ar[c], ai[c]);
+  }
 }
 
-// Y[k][col] (+)= sum_j E[j * ldE + k] X[j][col]   (the direct method for the tails)
+// Y[k][col] (+)= sum_j E[j * ldE + k] X[j][col]   (the direct method for the tails).
+// One CTA per (row k, 32 columns); its 8 warps split j and are summed in a fixed order.
 __global__ void __launch_bounds__(256) dense_tn_k(const double* __restrict__ E, int J, int K, int64_t ldE,
                                                    const double* __restrict__ X, int64_t ldx, double* Y,
                                                    int64_t ldy, int B, int acc) {
-  const int col = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int k = blockIdx.y * 8 + (threadIdx.x >> 5);
-  if (k >= K || col >= B) return;
+  __shared__ double part[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int col = blockIdx.x * 32 + lane;
+  const int k = blockIdx.y;
   double s = 0.0;
-  for (int j = 0; j < J; ++j) s = fma(E[(int64_t)j * ldE + k], X[(int64_t)j * ldx + col], s);
-  double* y = Y + (int64_t)k * ldy + col;
-  *y = acc ? *y + s : s;
+  if (col < B)
+    for (int j = w; j < J; j += 8) s = fma(__ldg(E + (int64_t)j * ldE + k), __ldg(X + (int64_t)j * ldx + col), s);
+  part[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && col < B) {
+    double t = part[0][lane];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) t += part[i][lane];
+    double* y = Y + (int64_t)k * ldy + col;
+    *y = acc ? *y + t : t;
+  }
 }
 
 }  // namespace
@@ -173,7 +195,7 @@ xc_status lag2d_compact_rows(const double2* S, int rows, int cols, double eps1, 
 xc_status lag2d_spmm(const int64_t* ptr, const Ent2D* ent, int rows, const double* z, int64_t ldz, double2* U,
                      int64_t ldu, int B, cudaStream_t st) {
   if (rows <= 0) return XC_OK;
-  csr2d_k<<<dim3((rows + 7) / 8, (B + 63) / 64), 256, 0, st>>>(ptr, ent, rows, z, ldz, U, ldu, B);
+  csr2d_k<2><<<dim3((rows + 7) / 8, (B + 63) / 64), 256, 0, st>>>(ptr, ent, rows, z, ldz, U, ldu, B);
   XC_CUDA(cudaGetLastError());
   return XC_OK;
 }
@@ -181,7 +203,7 @@ xc_status lag2d_spmm(const int64_t* ptr, const Ent2D* ent, int rows, const doubl
 xc_status dense_tn(const double* E, int J, int K, int64_t ldE, const double* X, int64_t ldx, double* Y, int64_t ldy,
                    int B, bool acc, cudaStream_t st) {
   if (K <= 0 || J <= 0) return XC_OK;
-  dense_tn_k<<<dim3((B + 31) / 32, (K + 7) / 8), 256, 0, st>>>(E, J, K, ldE, X, ldx, Y, ldy, B, acc ? 1 : 0);
+  dense_tn_k<<<dim3((B + 31) / 32, K), 256, 0, st>>>(E, J, K, ldE, X, ldx, Y, ldy, B, acc ? 1 : 0);
   XC_CUDA(cudaGetLastError());
   return XC_OK;
 }

@@ -70,7 +70,6 @@ struct BlockData {
   int64_t nnz = 0;
   int max_band = 0;
   int appQ = -1;  // Appendix A precompute: Q of the truncated window spectrum (-1: direct)
-  DevBuf ptr2d, ent2d;  // XC_LAG2D: CSR of the Hermitian half of sum_a D2_ab (this block = b)
   int ngroups = 0;
   int64_t loc_count = 0;  // values of the locally computed node range (distributed precompute)
   DevBuf grp_base, grp_nch;  // output axis groups
@@ -90,6 +89,8 @@ struct xc_op {
   int ukind = 0;  // the kind the caller built
   bool appA = false;  // Appendix A trig precompute (R-22)
   DevBuf tailR, tailC;  // XC_LAG2D: direct-method tails (rows i < t: N x t; columns j < t: t x (N-t))
+  DevBuf ptr2d, ent2d;  // XC_LAG2D: CSR of the Hermitian halves of sum_a D2_ab, time blocks b stacked
+  int rows2d = 0;
   double alpha = 0, beta = 0;
   int64_t N = 0;  // nodes
   int64_t M = 0;  // degrees (rows of A); == N unless rectangular
@@ -1032,8 +1033,10 @@ xc_status build_2d(xc_op* h) {
   XC_TRY(dev_alloc(dmx, sizeof(unsigned long long)));
   XC_TRY(dev_alloc(dcnt, (size_t)Lmax * sizeof(int)));
   int64_t total = 0;
-  h->rowsA = 0;  // the apply's u_b buffer (Hermitian half, complex): 2 H_b double rows
-  for (auto& b : h->blocks) h->rowsA = std::max<int64_t>(h->rowsA, 2 * (int64_t)b.H);
+  std::vector<int64_t> gptr(1, 0);  // all time blocks' rows stacked (one launch of the product)
+  std::vector<Ent2D> gent;
+  h->rowsA = 0;  // the apply's u_b buffers (Hermitian half, complex): 2 H_b double rows each
+  for (auto& b : h->blocks) h->rowsA += 2 * (int64_t)b.H;
   for (int ib = 0; ib < nb; ++ib) {
     BlockData& bb = h->blocks[ib];
     const int Lb = bb.L, Hb = bb.H;
@@ -1107,11 +1110,14 @@ xc_status build_2d(xc_op* h) {
         }
       }
     }
-    XC_TRY(upload(bb.ptr2d, ptr));
-    XC_TRY(upload(bb.ent2d, ent));
+    for (int k = 0; k < Hb; ++k) gptr.push_back(gptr.back() + (ptr[k + 1] - ptr[k]));
+    gent.insert(gent.end(), ent.begin(), ent.end());
     bb.nnz = ptr[Hb];
     total += bb.nnz;
   }
+  XC_TRY(upload(h->ptr2d, gptr));
+  XC_TRY(upload(h->ent2d, gent));
+  h->rows2d = (int)gptr.size() - 1;
   dev_free(F);
   dev_free(S1);
   dev_free(T);
@@ -1156,8 +1162,8 @@ xc_status build_2d(xc_op* h) {
   in.flops_per_col_WAT = 0;
   in.op_bytes_A = total * (int64_t)sizeof(Ent2D);
   int fl = 0;
-  for (auto& b : h->blocks) fl += ((b.fft.L2 > 1) ? 2 : 1) + ((b.fftM.L2 > 1) ? 2 : 1) + 1;
-  in.launches_A = fl + (t > 0 ? 2 : 0);
+  for (auto& b : h->blocks) fl += ((b.fft.L2 > 1) ? 2 : 1) + ((b.fftM.L2 > 1) ? 2 : 1);
+  in.launches_A = fl + 1 + (t > 0 ? 2 : 0);
   return XC_OK;
 }
 
@@ -1211,7 +1217,8 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
     int slot = (int)(h->ev_count++ % xc_op::kRing);
     XC_TRY(prof_harvest(h, slot));
     ev = &h->ev[4 * slot];
-    h->ev_dir[slot] = dir;
+    // XC_LAG2D phases: prologue FFTs, products, C2R + tails -- the input axis's order
+    h->ev_dir[slot] = h->ukind == XC_LAG2D ? XC_DIR_WAT : dir;
   }
   auto mark = [&](int i) -> xc_status {
     if (ev) XC_CUDA(cudaEventRecord(ev[i], st));
@@ -1241,11 +1248,16 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
       XC_TRY(fft_run(b.fft, +1, PRO_XREAL, EPI_ZPLANES, io, (int)B, (double2*)h->scratch.p, st));
     }
     XC_TRY(mark(1));
-    double2* U = (double2*)h->partA.p;
+    // the products of all time blocks in one launch (u_b stacked in partA), then the C2R
+    // epilogues and the tails
+    XC_TRY(lag2d_spmm((const int64_t*)h->ptr2d.p, (const Ent2D*)h->ent2d.p, h->rows2d, (const double*)h->zpl.p, Bp,
+                      (double2*)h->partA.p, Bp, (int)B, st));
+    XC_TRY(mark(2));
+    int64_t uoff = 0;
     for (int ib = 0; ib < nb; ++ib) {
       BlockData& b = h->blocks[ib];
-      XC_TRY(lag2d_spmm((const int64_t*)b.ptr2d.p, (const Ent2D*)b.ent2d.p, b.H, (const double*)h->zpl.p, Bp, U,
-                        Bp, (int)B, st));
+      double2* U = (double2*)h->partA.p + uoff * Bp;
+      uoff += b.H;
       FftIO io{};
       io.Uc = U;
       io.ldu = Bp;
@@ -1260,7 +1272,6 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
       io.m_off = b.m_off;
       XC_TRY(c2r_run(b.fftM, io, (int)B, (double2*)h->scratch.p, st));
     }
-    XC_TRY(mark(2));
     const int t = h->tail;
     if (t > 0) {
       XC_TRY(dense_tn((const double*)h->tailR.p, N, t, t, X, ldx, Y, ldy, (int)B, false, st));
@@ -1427,12 +1438,12 @@ void destroy_impl(xc_op* h) {
     dev_free(b.twh);
     dev_free(b.w); dev_free(b.yscale); dev_free(b.winv);
     dev_free(b.start); dev_free(b.len); dev_free(b.off); dev_free(b.vals);
-    dev_free(b.grp_base); dev_free(b.grp_nch); dev_free(b.ptr2d); dev_free(b.ent2d);
+    dev_free(b.grp_base); dev_free(b.grp_nch);
   }
   DevBuf* all[] = {&h->nodes, &h->wt, &h->tailP, &h->itemsA, &h->tilesA, &h->winsA, &h->tail_base, &h->tail_nch,
                    &h->itemsW, &h->tilesW, &h->winsW, &h->nodeg_base, &h->nodeg_nch, &h->nodeg_base_im, &h->partA, &h->partW,
                    &h->scratch, &h->zpl, &h->Xh, &h->Yh, &h->xsend, &h->xrecv, &h->djtab, &h->nodes_lo, &h->cscale,
-                   &h->tailR, &h->tailC};
+                   &h->tailR, &h->tailC, &h->ptr2d, &h->ent2d};
   for (DevBuf* b : all) dev_free(*b);
 }
 
