@@ -347,9 +347,10 @@ def main():
             "hbm_gbs": alg_bytes / (ms / 1e3) / 1e9,
             "hbm_frac": alg_bytes / (ms / 1e3) / 1e9 / hbm_peak,
             "fp64_tflops": info["flops_per_col_A"] * B / (ms / 1e3) / 1e12,
-            "roofline": ({"bound": "alu", "kernel": "csr2d (complex CSR product, DFMA)", "achieved": achieved,
-                          "peak": DFMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / DFMA_PEAK_TFLOPS,
-                          "peak_source": "measured DFMA microbenchmark (tools/fp64_peak.cu)"}
+            "roofline": ({"bound": "tensor", "kernel": "bsr2d (8x4 complex blocks, mma.m8n8k4.f64)",
+                          "achieved": achieved, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                          "frac": achieved / DMMA_PEAK_TFLOPS,
+                          "peak_source": "measured DMMA microbenchmark (tools/fp64_peak.cu)"}
                          if cfg.kind == I.KIND_LAG2D else
                          {"bound": "tensor", "kernel": "spmm_dmma (mma.m8n8k4.f64)", "achieved": achieved,
                           "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / DMMA_PEAK_TFLOPS,

@@ -18,6 +18,8 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <array>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -89,8 +91,13 @@ struct xc_op {
   int ukind = 0;  // the kind the caller built
   bool appA = false;  // Appendix A trig precompute (R-22)
   DevBuf tailR, tailC;  // XC_LAG2D: direct-method tails (rows i < t: N x t; columns j < t: t x (N-t))
-  DevBuf ptr2d, ent2d;  // XC_LAG2D: CSR of the Hermitian halves of sum_a D2_ab, time blocks b stacked
-  int rows2d = 0;
+  DevBuf ptr2d, ent2d, order2d;  // XC_LAG2D: CSR of the Hermitian halves of sum_a D2_ab, time blocks
+  int rows2d = 0;                 // stacked; order2d: rows longest first
+  DevBuf tailpart;                // XC_LAG2D: split-j partial sums of the tails
+  DevBuf bsr_sptr, bsr_r4, bsr_tiles, bsr_srow, bsr_snv, bsr_sslot, bsr_order;  // XC_LAG2D: 8 x 4
+  DevBuf bsr_rrow, bsr_rnv, bsr_rslot, bsr_rcnt, bsr_part;                       // DMMA blocks
+  int bsr_nseg = 0, bsr_nred = 0, bsr_nslots = 0;
+  int64_t zrows2d = 0;  // rows of the stacked prologue spectra
   double alpha = 0, beta = 0;
   int64_t N = 0;  // nodes
   int64_t M = 0;  // degrees (rows of A); == N unless rectangular
@@ -181,6 +188,10 @@ xc_status ensure_ws(xc_op* h, int64_t B) {
   }
   XC_TRY(dev_alloc(h->scratch, std::max<size_t>(1, scratch_n) * sizeof(double2)));
   if (h->dirs & XC_DIR_A) XC_TRY(dev_alloc(h->partA, (size_t)h->rowsA * Bp * sizeof(double)));
+  if (two_d && h->bsr_nslots > 0)  // partial rows of the split DMMA groups
+    XC_TRY(dev_alloc(h->bsr_part, (size_t)h->bsr_nslots * 8 * Bp * sizeof(double2)));
+  if (two_d && h->tail > 0)  // split-j partial sums of the tail rows: ceil(N/128) x t x B
+    XC_TRY(dev_alloc(h->tailpart, (size_t)((h->N + 127) / 128) * h->tail * Bp * sizeof(double)));
   if ((h->dirs & XC_DIR_WAT) || two_d) {
     if (!two_d) XC_TRY(dev_alloc(h->partW, (size_t)h->rowsW * Bp * sizeof(double)));
     h->zoff.clear();
@@ -189,7 +200,9 @@ xc_status ensure_ws(xc_op* h, int64_t B) {
       h->zoff.push_back(tot);
       tot += 2 * (int64_t)b.H * Bp;
     }
+    if (two_d) tot += 2 * 4 * Bp;  // the DMMA blocks may reach 3 rows past the last spectrum row
     XC_TRY(dev_alloc(h->zpl, (size_t)tot * sizeof(double)));
+    if (two_d) XC_CUDA(cudaMemset(h->zpl.p, 0, (size_t)tot * sizeof(double)));  // finite padding
   }
   h->ws_B = B;
   clear_graphs(h);  // captured graphs reference the old workspace
@@ -1019,8 +1032,8 @@ xc_status build_2d(xc_op* h) {
   const int N = (int)h->N, t = h->tail, nb = (int)h->blocks.size();
   DevBuf none;
   for (auto& b : h->blocks) XC_TRY(block_setup(h, b, none));
-  std::vector<int64_t> zrow(nb + 1, 0);  // prologue plane rows of degree block a: re then im
-  for (int a = 0; a < nb; ++a) zrow[a + 1] = zrow[a] + 2 * (int64_t)h->blocks[a].H;
+  std::vector<int64_t> zrow(nb + 1, 0);  // rows of degree block a's prologue spectrum (interleaved)
+  for (int a = 0; a < nb; ++a) zrow[a + 1] = zrow[a] + (int64_t)h->blocks[a].H;
   int Lmax = 0;
   for (auto& b : h->blocks) Lmax = std::max(Lmax, b.L);
   DevBuf F, S1, T, S2, scr, dmx, dcnt;
@@ -1035,6 +1048,11 @@ xc_status build_2d(xc_op* h) {
   int64_t total = 0;
   std::vector<int64_t> gptr(1, 0);  // all time blocks' rows stacked (one launch of the product)
   std::vector<Ent2D> gent;
+  // the BSR form: groups of 8 rows of one time block, 8 x 4 blocks over z rows r4..r4+3
+  std::vector<int64_t> bptr(1, 0);
+  std::vector<int> br4, bgrow, bgnv;
+  std::vector<double> btiles;
+  int64_t urow = 0;  // first stacked u row of the current time block
   h->rowsA = 0;  // the apply's u_b buffers (Hermitian half, complex): 2 H_b double rows each
   for (auto& b : h->blocks) h->rowsA += 2 * (int64_t)b.H;
   for (int ib = 0; ib < nb; ++ib) {
@@ -1104,20 +1122,93 @@ xc_status build_2d(xc_op* h) {
           Ent2D en;
           en.v = pv[ia][e];
           en.re = (int)(zrow[ia] + r);
-          en.im = (int)(zrow[ia] + Ha + r);
-          if (cj) en.im = -en.im - 1;
+          en.im = cj ? 1 : 0;
           ent[o++] = en;
         }
       }
     }
     for (int k = 0; k < Hb; ++k) gptr.push_back(gptr.back() + (ptr[k + 1] - ptr[k]));
     gent.insert(gent.end(), ent.begin(), ent.end());
+    for (int k0 = 0; k0 < Hb; k0 += 8) {
+      std::map<int, std::array<double, 128>> blk;  // r4 -> Crr | Cri | Cir | Cii (ordered: deterministic)
+      for (int i = 0; i < 8 && k0 + i < Hb; ++i)
+        for (int64_t e = ptr[k0 + i]; e < ptr[k0 + i + 1]; ++e) {
+          const Ent2D& en = ent[e];
+          const int r4 = en.re & ~3, j = en.re - r4;
+          auto it = blk.find(r4);
+          if (it == blk.end()) {
+            std::array<double, 128> z{};
+            it = blk.emplace(r4, z).first;
+          }
+          double* T = it->second.data();
+          const double vr = en.v.x, vi = en.v.y;
+          const int f = 4 * i + j;
+          T[f] += vr;                          // Crr
+          T[32 + f] += en.im ? vi : -vi;       // Cri
+          T[64 + f] += vi;                     // Cir
+          T[96 + f] += en.im ? -vr : vr;       // Cii
+        }
+      for (auto& kv : blk) {
+        br4.push_back(kv.first);
+        btiles.insert(btiles.end(), kv.second.begin(), kv.second.end());
+      }
+      bptr.push_back(bptr.back() + (int64_t)blk.size());
+      bgrow.push_back((int)(urow + k0));
+      bgnv.push_back(std::min(8, Hb - k0));
+    }
+    urow += Hb;
     bb.nnz = ptr[Hb];
     total += bb.nnz;
   }
   XC_TRY(upload(h->ptr2d, gptr));
   XC_TRY(upload(h->ent2d, gent));
   h->rows2d = (int)gptr.size() - 1;
+  std::vector<int> order(h->rows2d);
+  for (int r = 0; r < h->rows2d; ++r) order[r] = r;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return gptr[a + 1] - gptr[a] > gptr[b + 1] - gptr[b]; });
+  XC_TRY(upload(h->order2d, order));
+  // segments of at most kBsrSeg blocks (one warp each); groups cut in several are summed in order
+  std::vector<int64_t> sptr(1, 0);
+  std::vector<int> srow, snv, sslot, rrow, rnv, rslot, rcnt;
+  int nslots = 0;
+  for (size_t g = 0; g + 1 < bptr.size(); ++g) {
+    const int64_t nbk = bptr[g + 1] - bptr[g];
+    const int ns = std::max<int64_t>(1, (nbk + kBsrSeg - 1) / kBsrSeg);
+    for (int c = 0; c < ns; ++c) {
+      sptr.push_back(std::min(bptr[g + 1], bptr[g] + (int64_t)(c + 1) * kBsrSeg));
+      srow.push_back(bgrow[g]);
+      snv.push_back(bgnv[g]);
+      sslot.push_back(ns == 1 ? -1 : nslots + c);
+    }
+    if (ns > 1) {
+      rrow.push_back(bgrow[g]);
+      rnv.push_back(bgnv[g]);
+      rslot.push_back(nslots);
+      rcnt.push_back(ns);
+      nslots += ns;
+    }
+  }
+  sptr.back() = bptr.back();
+  h->bsr_nseg = (int)srow.size();
+  h->bsr_nred = (int)rrow.size();
+  h->bsr_nslots = nslots;
+  std::vector<int> sorder(h->bsr_nseg);
+  for (int g = 0; g < h->bsr_nseg; ++g) sorder[g] = g;
+  std::stable_sort(sorder.begin(), sorder.end(),
+                   [&](int a, int b) { return sptr[a + 1] - sptr[a] > sptr[b + 1] - sptr[b]; });
+  XC_TRY(upload(h->bsr_sptr, sptr));
+  XC_TRY(upload(h->bsr_r4, br4));
+  XC_TRY(upload(h->bsr_tiles, btiles));
+  XC_TRY(upload(h->bsr_srow, srow));
+  XC_TRY(upload(h->bsr_snv, snv));
+  XC_TRY(upload(h->bsr_sslot, sslot));
+  XC_TRY(upload(h->bsr_order, sorder));
+  XC_TRY(upload(h->bsr_rrow, rrow));
+  XC_TRY(upload(h->bsr_rnv, rnv));
+  XC_TRY(upload(h->bsr_rslot, rslot));
+  XC_TRY(upload(h->bsr_rcnt, rcnt));
+  h->zrows2d = zrow[nb];
   dev_free(F);
   dev_free(S1);
   dev_free(T);
@@ -1163,7 +1254,7 @@ xc_status build_2d(xc_op* h) {
   in.op_bytes_A = total * (int64_t)sizeof(Ent2D);
   int fl = 0;
   for (auto& b : h->blocks) fl += ((b.fft.L2 > 1) ? 2 : 1) + ((b.fftM.L2 > 1) ? 2 : 1);
-  in.launches_A = fl + 1 + (t > 0 ? 2 : 0);
+  in.launches_A = fl + 1 + (h->bsr_nred > 0 ? 1 : 0) + (t > 0 ? 2 + (N > 128 ? 1 : 0) : 0);
   return XC_OK;
 }
 
@@ -1239,19 +1330,29 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
       io.keep_lo = b.keep_lo;
       io.keep_hi = b.keep_hi;
       io.m_off = b.m_off;
-      io.zre = (double*)h->zpl.p + zrow * Bp;  // the rows the CSR entries address (build_2d)
-      zrow += 2 * (int64_t)b.H;
-      io.zim = io.zre + (int64_t)b.H * Bp;
-      io.ldz = Bp;
-      io.H = b.H;
+      io.dst = (double2*)h->zpl.p + zrow * Bp;  // the rows the CSR entries address (build_2d)
+      zrow += b.H;
+      io.ldd = Bp;
+      io.kmax = b.H;
       io.scale = 1.0 / sqrt((double)b.L);
-      XC_TRY(fft_run(b.fft, +1, PRO_XREAL, EPI_ZPLANES, io, (int)B, (double2*)h->scratch.p, st));
+      XC_TRY(fft_run(b.fft, +1, PRO_XREAL, EPI_PLAIN, io, (int)B, (double2*)h->scratch.p, st));
     }
     XC_TRY(mark(1));
     // the products of all time blocks in one launch (u_b stacked in partA), then the C2R
     // epilogues and the tails
-    XC_TRY(lag2d_spmm((const int64_t*)h->ptr2d.p, (const Ent2D*)h->ent2d.p, h->rows2d, (const double*)h->zpl.p, Bp,
-                      (double2*)h->partA.p, Bp, (int)B, st));
+    static const bool use_csr = getenv("XC_2D_CSR") != nullptr;  // the DFMA CSR product (comparison)
+    if (use_csr) {
+      XC_TRY(lag2d_spmm((const int64_t*)h->ptr2d.p, (const Ent2D*)h->ent2d.p, (const int*)h->order2d.p, h->rows2d,
+                        (const double2*)h->zpl.p, Bp, (double2*)h->partA.p, Bp, (int)B, st));
+    } else {
+      Bsr2D m{(const int64_t*)h->bsr_sptr.p, (const int*)h->bsr_r4.p,  (const double*)h->bsr_tiles.p,
+              (const int*)h->bsr_srow.p,     (const int*)h->bsr_snv.p, (const int*)h->bsr_sslot.p,
+              (const int*)h->bsr_order.p,    h->bsr_nseg,              (const int*)h->bsr_rrow.p,
+              (const int*)h->bsr_rnv.p,      (const int*)h->bsr_rslot.p, (const int*)h->bsr_rcnt.p,
+              h->bsr_nred,                   h->bsr_nslots};
+      XC_TRY(lag2d_bsr(m, (const double2*)h->zpl.p, Bp, (double2*)h->partA.p, Bp, (double2*)h->bsr_part.p, (int)B,
+                       st));
+    }
     XC_TRY(mark(2));
     int64_t uoff = 0;
     for (int ib = 0; ib < nb; ++ib) {
@@ -1274,8 +1375,11 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
     }
     const int t = h->tail;
     if (t > 0) {
-      XC_TRY(dense_tn((const double*)h->tailR.p, N, t, t, X, ldx, Y, ldy, (int)B, false, st));
-      XC_TRY(dense_tn((const double*)h->tailC.p, t, N - t, N - t, X, ldx, Y + (int64_t)t * ldy, ldy, (int)B, true, st));
+      const int64_t cap = (int64_t)(h->tailpart.bytes / sizeof(double));
+      XC_TRY(dense_tn((const double*)h->tailR.p, N, t, t, X, ldx, Y, ldy, (int)B, false, (double*)h->tailpart.p, cap,
+                      st));
+      XC_TRY(dense_tn((const double*)h->tailC.p, t, N - t, N - t, X, ldx, Y + (int64_t)t * ldy, ldy, (int)B, true,
+                      (double*)h->tailpart.p, cap, st));
     }
     return mark(3);
   }
@@ -1443,7 +1547,9 @@ void destroy_impl(xc_op* h) {
   DevBuf* all[] = {&h->nodes, &h->wt, &h->tailP, &h->itemsA, &h->tilesA, &h->winsA, &h->tail_base, &h->tail_nch,
                    &h->itemsW, &h->tilesW, &h->winsW, &h->nodeg_base, &h->nodeg_nch, &h->nodeg_base_im, &h->partA, &h->partW,
                    &h->scratch, &h->zpl, &h->Xh, &h->Yh, &h->xsend, &h->xrecv, &h->djtab, &h->nodes_lo, &h->cscale,
-                   &h->tailR, &h->tailC, &h->ptr2d, &h->ent2d};
+                   &h->tailR, &h->tailC, &h->ptr2d, &h->ent2d, &h->order2d, &h->tailpart,
+                   &h->bsr_sptr, &h->bsr_r4, &h->bsr_tiles, &h->bsr_srow, &h->bsr_snv, &h->bsr_sslot,
+                   &h->bsr_order, &h->bsr_rrow, &h->bsr_rnv, &h->bsr_rslot, &h->bsr_rcnt, &h->bsr_part};
   for (DevBuf* b : all) dev_free(*b);
 }
 

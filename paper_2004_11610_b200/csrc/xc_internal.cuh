@@ -275,8 +275,8 @@ xc_status appa_spectra(int kind, int L, int H, int m_off, int Q, int W, const do
                        const double2* cscale, const double2* xq, int nc, double eps1, double2* spec, int* flag,
                        cudaStream_t st, AppAWin* wm = nullptr);
 xc_status appa_store(const AppAWin& wm, int W, const int64_t* off, double2* vals, int nc, cudaStream_t st);
-// 2D block method (lag2d.cu, R-23): one kept entry of a D2 row: value and the rows of the
-// prologue planes it multiplies (re plane row; im plane row, negative -r-1 = conjugate)
+// 2D block method (lag2d.cu, R-23): one kept entry of a D2 row: value, the row of the interleaved
+// prologue spectra it multiplies (re) and whether that spectrum value is conjugated (im != 0)
 struct Ent2D {
   double2 v;
   int re, im;
@@ -285,10 +285,33 @@ xc_status lag2d_scale_nodes(double2* F, int L, int nc, const double* w, cudaStre
 xc_status lag2d_transpose(const double2* in, double2* out, int R, int C, cudaStream_t st);
 xc_status lag2d_compact_rows(const double2* S, int rows, int cols, double eps1, unsigned long long* dmx, int* dcnt,
                              std::vector<int64_t>& ptr, DevBuf& q, DevBuf& v, cudaStream_t st);
-xc_status lag2d_spmm(const int64_t* ptr, const Ent2D* ent, int rows, const double* z, int64_t ldz, double2* U,
-                     int64_t ldu, int B, cudaStream_t st);
+xc_status lag2d_spmm(const int64_t* ptr, const Ent2D* ent, const int* order, int rows, const double2* z, int64_t ldz,
+                     double2* U, int64_t ldu, int B, cudaStream_t st);
+// The same product in 8 x 4 blocks on the FP64 tensor cores (device pointers, built by build_2d):
+// groups of 8 u rows, their blocks cut into segments of at most kBsrSeg blocks (one warp each)
+constexpr int kBsrSeg = 24;
+struct Bsr2D {
+  const int64_t* sptr;  // blocks of segment s: [sptr[s], sptr[s+1])
+  const int* r4s;       // first z row of each block
+  const double* tiles;  // 128 doubles per block: the Crr, Cri, Cir, Cii A fragments
+  const int* srow;      // first u row of the segment's group
+  const int* snv;       // valid rows of the group (<= 8)
+  const int* sslot;     // -1: the group's only segment; else its partial slot
+  const int* order;     // segments, most blocks first
+  int nseg;
+  const int* rrow;      // groups with several segments: u row, valid rows, first slot, slots
+  const int* rnv;
+  const int* rslot;
+  const int* rcnt;
+  int nred;
+  int nslots;
+};
+xc_status lag2d_bsr(const Bsr2D& m, const double2* z, int64_t ldz, double2* U, int64_t ldu, double2* part, int B,
+                    cudaStream_t st);
+// Y[k][col] (+)= sum_j E[j * ldE + k] X[j][col]; part: optional scratch (part_cap doubles) for
+// a split-j pass with a deterministic second-pass reduction
 xc_status dense_tn(const double* E, int J, int K, int64_t ldE, const double* X, int64_t ldx, double* Y, int64_t ldy,
-                   int B, bool acc, cudaStream_t st);
+                   int B, bool acc, double* part, int64_t part_cap, cudaStream_t st);
 xc_status band_detect(const double2* spec, int H, int nc, double eps1, int* start, int* len, bool circ,
                       cudaStream_t st);
 xc_status band_store(const double2* spec, int H, int nc, double eps1, const int* start, const int* len,
