@@ -231,33 +231,6 @@ __global__ void bsr_reduce_k(const int* __restrict__ rrow, const int* __restrict
   U[(int64_t)(rrow[g] + i) * ldu + col] = s;
 }
 
-// Y[k][col] (+)= sum_j E[j * ldE + k] X[j][col]   (the direct method for the tails).
-// Warp per (k, 32 columns) over the j-chunk blockIdx.z; with several chunks the partial sums go
-// to part[(chunk * K + k) * B + col] and tail_reduce_k adds them in chunk order (deterministic).
-__global__ void __launch_bounds__(256) dense_tn_k(const double* __restrict__ E, int J, int K, int64_t ldE,
-                                                   const double* __restrict__ X, int64_t ldx, double* Y,
-                                                   int64_t ldy, int B, int acc, int JC, double* part) {
-  const int lane = threadIdx.x & 31;
-  const int col = blockIdx.x * 32 + lane;
-  const int k = blockIdx.y * 8 + (threadIdx.x >> 5);
-  if (k >= K || col >= B) return;
-  const int j0 = blockIdx.z * JC, j1 = min(J, j0 + JC);
-  double s0 = 0.0, s1 = 0.0;
-  int j = j0;
-  for (; j + 1 < j1; j += 2) {
-    s0 = fma(__ldg(E + (int64_t)j * ldE + k), __ldg(X + (int64_t)j * ldx + col), s0);
-    s1 = fma(__ldg(E + (int64_t)(j + 1) * ldE + k), __ldg(X + (int64_t)(j + 1) * ldx + col), s1);
-  }
-  if (j < j1) s0 = fma(__ldg(E + (int64_t)j * ldE + k), __ldg(X + (int64_t)j * ldx + col), s0);
-  const double s = s0 + s1;
-  if (part) {
-    part[((int64_t)blockIdx.z * K + k) * B + col] = s;
-  } else {
-    double* y = Y + (int64_t)k * ldy + col;
-    *y = acc ? *y + s : s;
-  }
-}
-
 __global__ void tail_reduce_k(const double* __restrict__ part, int nch, int K, int B, double* Y, int64_t ldy,
                               int acc) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -267,6 +240,49 @@ __global__ void tail_reduce_k(const double* __restrict__ part, int nch, int K, i
   for (int c = 0; c < nch; ++c) s += part[((int64_t)c * K + k) * B + col];
   double* y = Y + (int64_t)k * ldy + col;
   *y = acc ? *y + s : s;
+}
+
+// The tails (the direct method) on the FP64 tensor cores: Y[m][col] (+)= sum_j E[j * ldE + m] X[j][col], j in the
+// chunk blockIdx.z (length JC, a multiple of 4).  One warp per 8 rows x 32 columns (4 DMMA column
+// tiles): A fragment lane = E[k0 + lane%4][m0 + lane/4], B fragment lane = X[k0 + lane%4][col].
+__global__ void __launch_bounds__(256) dense_tn_mma_k(const double* __restrict__ E, int J, int K, int64_t ldE,
+                                                       const double* __restrict__ X, int64_t ldx, double* Y,
+                                                       int64_t ldy, int B, int acc, int JC, double* part) {
+  const int lane = threadIdx.x & 31;
+  const int m0 = (blockIdx.y * 8 + (threadIdx.x >> 5)) * 8;
+  if (m0 >= K) return;
+  const int c0 = blockIdx.x * 32;
+  const int j0 = blockIdx.z * JC, j1 = min(J, j0 + JC);
+  const int am = m0 + (lane >> 2), kk = lane & 3;
+  double d[4][2];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) d[t][0] = d[t][1] = 0.0;
+  for (int k = j0; k < j1; k += 4) {
+    const int kr = k + kk;
+    const double a = (kr < j1 && am < K) ? __ldg(E + (int64_t)kr * ldE + am) : 0.0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int col = c0 + 8 * t + (lane >> 2);
+      const double b = (kr < j1 && col < B) ? __ldg(X + (int64_t)kr * ldx + col) : 0.0;
+      dmma2(d[t][0], d[t][1], a, b);
+    }
+  }
+  const int m = m0 + (lane >> 2);
+  if (m >= K) return;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int col = c0 + 8 * t + 2 * (lane & 3) + q;
+      if (col >= B) continue;
+      if (part) {
+        part[((int64_t)blockIdx.z * K + m) * B + col] = d[t][q];
+      } else {
+        double* y = Y + (int64_t)m * ldy + col;
+        *y = acc ? *y + d[t][q] : d[t][q];
+      }
+    }
+  }
 }
 
 }  // namespace
@@ -342,9 +358,10 @@ xc_status dense_tn(const double* E, int J, int K, int64_t ldE, const double* X, 
   // long sums are cut into chunks of 128 (grid parallelism), reduced in a second pass
   int nch = (J + 127) / 128;
   if (nch > 1 && (!part || (int64_t)nch * K * B > part_cap)) nch = 1;
-  const int JC = (J + nch - 1) / nch;
-  dense_tn_k<<<dim3((B + 31) / 32, (K + 7) / 8, nch), 256, 0, st>>>(E, J, K, ldE, X, ldx, Y, ldy, B, acc ? 1 : 0, JC,
-                                                                      nch > 1 ? part : nullptr);
+  const int JC = ((J + nch - 1) / nch + 3) / 4 * 4;
+  nch = (J + JC - 1) / JC;
+  dense_tn_mma_k<<<dim3((B + 31) / 32, (K + 63) / 64, nch), 256, 0, st>>>(E, J, K, ldE, X, ldx, Y, ldy, B, acc ? 1 : 0,
+                                                                          JC, nch > 1 ? part : nullptr);
   XC_CUDA(cudaGetLastError());
   if (nch > 1) {
     const int64_t n = (int64_t)K * B;
