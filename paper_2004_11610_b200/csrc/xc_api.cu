@@ -136,6 +136,12 @@ struct xc_op {
   bool use_graphs = true;
   // xc_apply_host pipeline: copy-in / copy-out streams and per-slot events
   cudaStream_t s_in = nullptr, s_out = nullptr;
+  // XC_DIR_A of the block kinds: after the SpMM the blocks are independent; block 2 and the
+  // smaller blocks run on two forked streams beside block 1 (own C2R scratch each)
+  cudaStream_t s_aux[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  DevBuf scratch_aux[2];
+  bool use_fork = true;
   static constexpr int kSlots = 3;  // device slots of the host-buffer pipeline
   cudaEvent_t ev_in[kSlots] = {}, ev_cmp[kSlots] = {}, ev_out[kSlots] = {};
   cudaEvent_t ev_start = nullptr;
@@ -187,6 +193,17 @@ xc_status ensure_ws(xc_op* h, int64_t B) {
       scratch_n = std::max(scratch_n, (size_t)b.L * (size_t)B);
   }
   XC_TRY(dev_alloc(h->scratch, std::max<size_t>(1, scratch_n) * sizeof(double2)));
+  if ((h->dirs & XC_DIR_A) && h->kind != XC_EXP && !two_d && h->blocks.size() > 1) {
+    size_t a0 = 0, a1 = 0;  // block 2 on s_aux[0], blocks 3.. on s_aux[1]
+    for (size_t i = 1; i < h->blocks.size(); ++i) {
+      const BlockData& b = h->blocks[i];
+      const size_t n = b.fftM.L2 > 1 ? (size_t)b.fftM.L * (size_t)B : 1;
+      if (i == 1) a0 = std::max(a0, n);
+      else a1 = std::max(a1, n);
+    }
+    XC_TRY(dev_alloc(h->scratch_aux[0], std::max<size_t>(1, a0) * sizeof(double2)));
+    XC_TRY(dev_alloc(h->scratch_aux[1], std::max<size_t>(1, a1) * sizeof(double2)));
+  }
   if (h->dirs & XC_DIR_A) XC_TRY(dev_alloc(h->partA, (size_t)h->rowsA * Bp * sizeof(double)));
   if (two_d && h->bsr_nslots > 0)  // partial rows of the split DMMA groups
     XC_TRY(dev_alloc(h->bsr_part, (size_t)h->bsr_nslots * 8 * Bp * sizeof(double2)));
@@ -867,6 +884,7 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
   h->kind = kind == XC_LAGSPEC ? XC_EXP : (kind == XC_LAG2D ? XC_LAGUERRE : kind);
   h->ukind = kind;
   h->appA = p.trig_precompute == 1;
+  h->use_fork = getenv("XC_NO_FORK") == nullptr;  // A/B switch for measurements
   h->alpha = p.alpha;
   h->beta = p.beta;
   h->N = N;
@@ -1423,11 +1441,34 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
     XC_TRY(spmm_run((const SpmmWin*)h->winsA.p, h->nwinsA, (const SpmmItem*)h->itemsA.p,
                     (const double*)h->tilesA.p, s, (double*)h->partA.p, Bp, (int)B, st));
     XC_TRY(mark(1));
-    for (auto& b : h->blocks) {
+    const int nb = (int)h->blocks.size();
+    const bool fork = h->use_fork && nb > 1 && h->scratch_aux[0].p;
+    if (fork) {
+      if (!h->s_aux[0]) {
+        int lo = 0, hi = 0;  // the small blocks first: their CTAs are dispatched before block 1's
+        XC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        const int pr = getenv("XC_FORK_LOWPRIO") ? lo : hi;
+        for (int i = 0; i < 2; ++i) {
+          XC_CUDA(cudaStreamCreateWithPriority(&h->s_aux[i], cudaStreamNonBlocking, pr));
+          XC_CUDA(cudaEventCreateWithFlags(&h->ev_join[i], cudaEventDisableTiming));
+        }
+        XC_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+      }
+      XC_CUDA(cudaEventRecord(h->ev_fork, st));
+      for (int i = 0; i < 2; ++i) XC_CUDA(cudaStreamWaitEvent(h->s_aux[i], h->ev_fork, 0));
+    }
+    for (int ib = 0; ib < nb; ++ib) {
+      BlockData& b = h->blocks[ib];
+      cudaStream_t sb = st;
+      double2* scr = (double2*)h->scratch.p;
+      if (fork && ib > 0) {
+        sb = h->s_aux[ib == 1 ? 0 : 1];
+        scr = (double2*)h->scratch_aux[ib == 1 ? 0 : 1].p;
+      }
       double* U = (double*)h->partA.p + b.ubase * Bp;
       if (b.split)  // interleaved complex rows: reduce all Bp doubles of each double row
         XC_TRY(reduce_rows8((const double*)h->partA.p, Bp, (const int64_t*)b.grp_base.p, (const int*)b.grp_nch.p,
-                            8 * b.ngroups, nullptr, U, Bp, (int)Bp, st));
+                            8 * b.ngroups, nullptr, U, Bp, (int)Bp, sb));
       FftIO io{};
       io.Uc = reinterpret_cast<const double2*>(U);
       io.ldu = Bp;
@@ -1440,7 +1481,13 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
       io.keep_lo = b.keep_lo;
       io.keep_hi = b.keep_hi;
       io.m_off = b.m_off;
-      XC_TRY(c2r_run(b.fftM, io, (int)B, (double2*)h->scratch.p, st));
+      XC_TRY(c2r_run(b.fftM, io, (int)B, scr, sb));
+    }
+    if (fork) {
+      for (int i = 0; i < 2; ++i) {
+        XC_CUDA(cudaEventRecord(h->ev_join[i], h->s_aux[i]));
+        XC_CUDA(cudaStreamWaitEvent(st, h->ev_join[i], 0));
+      }
     }
     XC_TRY(mark(2));
     if (h->tail > 0)
@@ -1523,6 +1570,15 @@ void destroy_impl(xc_op* h) {
   clear_graphs(h);
   for (auto& e : h->ev) cudaEventDestroy(e);
   h->ev.clear();
+  for (int i = 0; i < 2; ++i) {
+    if (h->s_aux[i]) {
+      cudaStreamSynchronize(h->s_aux[i]);
+      cudaStreamDestroy(h->s_aux[i]);
+      cudaEventDestroy(h->ev_join[i]);
+    }
+    dev_free(h->scratch_aux[i]);
+  }
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->s_in) {
     cudaStreamSynchronize(h->s_in);
     cudaStreamSynchronize(h->s_out);
@@ -1956,6 +2012,16 @@ xc_status xc_workspace_query(xc_handle h, int64_t B, size_t* bytes) {
     if ((h->dirs & XC_DIR_A) && h->kind == XC_EXP && b.fft.L2 > 1) scr = std::max(scr, (size_t)b.L * B * sizeof(double2));
   }
   s += scr;
+  if ((h->dirs & XC_DIR_A) && h->kind != XC_EXP && !two_d && h->blocks.size() > 1) {
+    size_t a0 = 0, a1 = 0;  // the forked blocks' C2R scratch (ensure_ws)
+    for (size_t i = 1; i < h->blocks.size(); ++i) {
+      const BlockData& b = h->blocks[i];
+      const size_t n = b.fftM.L2 > 1 ? (size_t)b.fftM.L * B * sizeof(double2) : 0;
+      if (i == 1) a0 = std::max(a0, n);
+      else a1 = std::max(a1, n);
+    }
+    s += a0 + a1;
+  }
   if (h->dirs & XC_DIR_A) s += (size_t)h->rowsA * Bp * 8;
   if ((h->dirs & XC_DIR_WAT) || two_d) {
     if (!two_d) s += (size_t)h->rowsW * Bp * 8;
