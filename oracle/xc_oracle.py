@@ -552,7 +552,7 @@ def compress_2d(plan: Plan, nodes: np.ndarray) -> Operator2D:
     unitary 2D DFT), thresholded at eps1 * max |D2_ab| (the global form of P:198)."""
     assert plan.kind.kind == KIND_LAGUERRE
     N, t = plan.N, plan.tail
-    Lmax = max(b.L for b in plan.blocks)
+    Lmax = max((b.L for b in plan.blocks), default=0)   # N <= cutoff: no block, all direct (P:301)
     W = [kaiser(plan.zeta, b.L - 1) for b in plan.blocks]
     D2 = []
     for b, wb in zip(plan.blocks, W):

@@ -222,6 +222,7 @@ __global__ void band_store_k(const double2* __restrict__ spec, int H, int nc, do
 }  // namespace
 
 xc_status gen_entries(const GenParams& g, double2* F, cudaStream_t st) {
+  if (g.nc <= 0 || g.L <= 0) return XC_OK;
   if (g.kind == XC_EXP) {
     int64_t tot = (int64_t)g.L * g.nc;
     gen_exp<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(g, F, g.nc);
@@ -238,6 +239,7 @@ xc_status gen_entries(const GenParams& g, double2* F, cudaStream_t st) {
 }
 
 xc_status gen_entries_real(const GenParams& g, double* E, int64_t ldE, cudaStream_t st) {
+  if (g.nc <= 0 || g.L <= 0) return XC_OK;  // nothing to generate (e.g. an empty tail part)
   if (g.kind == XC_COS) {
     int64_t tot = (int64_t)g.L * g.nc;
     gen_cos<false><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(g, E, ldE);

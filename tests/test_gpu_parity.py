@@ -681,6 +681,38 @@ def test_lag2d_parity(case):
     T.close()
 
 
+@pytest.mark.parametrize("N", [2, 20, 33, 64])
+def test_lag2d_degenerate_sizes(N):
+    """2D method at the degenerate sizes: all tail (N <= cutoff), one block pair plus tails; B = 1."""
+    xc = _xc()
+    x = I.lag2d_grid(N, 100.0)
+    C = I.rhs(N, 1, 9)
+    T = xc.Transform(xc.XC_LAG2D, x, 1e-12)
+    Y = T.apply(torch.from_numpy(C).cuda()).cpu().numpy()
+    plan = O.make_plan(O.Kind(O.KIND_LAGUERRE), N, 1e-12, eps2=0.1)
+    assert O.rel_l2_cols(Y, O.apply_2d(O.compress_2d(plan, x), C)).max() <= 1e-12
+    assert O.rel_l2_cols(Y, O.dense_apply_t(O.Kind(O.KIND_LAGUERRE), x, C)).max() <= 1e-11
+    T.close()
+
+
+@pytest.mark.parametrize("M,N", [(2, 50), (50, 2), (2, 2), (1, 40)])
+def test_rectangular_degenerate_sizes(M, N):
+    """Rectangular complex operators at the smallest sizes (M = 1 is rejected: n_rows >= 2)."""
+    xc = _xc()
+    t = I.exp_nodes(N, 3)
+    if M < 2:
+        with pytest.raises(xc.XcError, match="XC_EINVAL"):
+            xc.Transform(xc.XC_EXP, t, 1e-12, n_rows=M)
+        return
+    X = I.complex_rhs(N, 3, 4)
+    T = xc.Transform(xc.XC_EXP, t, 1e-12, n_rows=M)
+    Y = T.apply_complex(torch.from_numpy(X).cuda()).cpu().numpy()
+    op = O.compress(O.make_plan(O.Kind(O.KIND_EXP), N, 1e-12, M=M), t)
+    assert O.rel_l2_cols(Y, O.apply_output_axis(op, X)).max() <= 1e-12
+    assert O.rel_l2_cols(Y, O.dense_apply(O.Kind(O.KIND_EXP), t, X, M=M)).max() <= 1e-11
+    T.close()
+
+
 def test_lag2d_errors():
     xc = _xc()
     x = I.lag2d_grid(100, 100.0)

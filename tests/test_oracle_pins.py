@@ -762,3 +762,13 @@ def test_2d_compression_paper_claims():
     N = 4096
     op = O.compress_2d(_plan2d(N, eps), I.lag2d_grid(N, 100.0))
     assert O.nnz_2d(op) / N ** 2 < 0.05
+
+
+def test_2d_all_tail_is_the_direct_sum():
+    """N <= the cutoff: no block pair, the 2D method is the direct method exactly."""
+    N = 20
+    x = I.lag2d_grid(N, 100.0)
+    op = O.compress_2d(_plan2d(N, 1e-12), x)
+    assert not op.D2
+    C = I.rhs(N, 2, 3)
+    np.testing.assert_allclose(O.apply_2d(op, C), O.dense_apply_t(LAG, x, C), rtol=0, atol=1e-12)
