@@ -193,11 +193,13 @@ xc_status ensure_ws(xc_op* h, int64_t B) {
       scratch_n = std::max(scratch_n, (size_t)b.L * (size_t)B);
   }
   XC_TRY(dev_alloc(h->scratch, std::max<size_t>(1, scratch_n) * sizeof(double2)));
-  if ((h->dirs & XC_DIR_A) && h->kind != XC_EXP && !two_d && h->blocks.size() > 1) {
-    size_t a0 = 0, a1 = 0;  // block 2 on s_aux[0], blocks 3.. on s_aux[1]
+  if (h->kind != XC_EXP && h->blocks.size() > 1) {
+    size_t a0 = 0, a1 = 0;  // block 2 on s_aux[0], blocks 3.. on s_aux[1] (fork_stream)
     for (size_t i = 1; i < h->blocks.size(); ++i) {
       const BlockData& b = h->blocks[i];
-      const size_t n = b.fftM.L2 > 1 ? (size_t)b.fftM.L * (size_t)B : 1;
+      size_t n = 1;
+      if (((h->dirs & XC_DIR_A) || two_d) && b.fftM.L2 > 1) n = std::max(n, (size_t)b.fftM.L * (size_t)B);
+      if (((h->dirs & XC_DIR_WAT) || two_d) && b.fft.L2 > 1) n = std::max(n, (size_t)b.L * (size_t)B);
       if (i == 1) a0 = std::max(a0, n);
       else a1 = std::max(a1, n);
     }
@@ -1306,6 +1308,51 @@ xc_status prof_harvest(xc_op* h, int slot) {
   return XC_OK;
 }
 
+// Per-block phases (the blocks are independent there): block 1 stays on the caller's stream,
+// block 2 goes to s_aux[0], blocks 3.. to s_aux[1] (high priority: their few CTAs are dispatched
+// ahead of block 1's persistent grid), each with its own FFT scratch; fork/join by events, so
+// the phase also works under CUDA-graph capture.
+bool fork_begin(xc_op* h, cudaStream_t st, xc_status& err) {
+  err = XC_OK;
+  if (!h->use_fork || h->blocks.size() < 2 || !h->scratch_aux[0].p) return false;
+  auto fail = [&](cudaError_t e) {
+    xc_set_error(std::string("fork: ") + cudaGetErrorString(e));
+    err = XC_ECUDA;
+    return false;
+  };
+  cudaError_t e;
+  if (!h->s_aux[0]) {
+    int lo = 0, hi = 0;
+    if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return fail(e);
+    for (int i = 0; i < 2; ++i) {
+      if ((e = cudaStreamCreateWithPriority(&h->s_aux[i], cudaStreamNonBlocking, hi)) != cudaSuccess) return fail(e);
+      if ((e = cudaEventCreateWithFlags(&h->ev_join[i], cudaEventDisableTiming)) != cudaSuccess) return fail(e);
+    }
+    if ((e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
+  }
+  if ((e = cudaEventRecord(h->ev_fork, st)) != cudaSuccess) return fail(e);
+  for (int i = 0; i < 2; ++i)
+    if ((e = cudaStreamWaitEvent(h->s_aux[i], h->ev_fork, 0)) != cudaSuccess) return fail(e);
+  return true;
+}
+
+xc_status fork_end(xc_op* h, cudaStream_t st, bool fork) {
+  if (!fork) return XC_OK;
+  for (int i = 0; i < 2; ++i) {
+    XC_CUDA(cudaEventRecord(h->ev_join[i], h->s_aux[i]));
+    XC_CUDA(cudaStreamWaitEvent(st, h->ev_join[i], 0));
+  }
+  return XC_OK;
+}
+
+cudaStream_t fork_stream(xc_op* h, cudaStream_t st, bool fork, int ib) {
+  return (fork && ib > 0) ? h->s_aux[ib == 1 ? 0 : 1] : st;
+}
+
+double2* fork_scratch(xc_op* h, bool fork, int ib) {
+  return (double2*)((fork && ib > 0) ? h->scratch_aux[ib == 1 ? 0 : 1].p : h->scratch.p);
+}
+
 xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t B,
                      cudaStream_t st) {
   if (B < 1 || ldx < B || ldy < B || !X || !Y) {
@@ -1338,6 +1385,9 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
   XC_TRY(mark(0));
   if (h->ukind == XC_LAG2D) {  // R-23: prologues, merged 2D products + C2R per time block, tails
     const int nb = (int)h->blocks.size();
+    xc_status ferr;
+    bool fork = fork_begin(h, st, ferr);
+    XC_TRY(ferr);
     int64_t zrow = 0;  // plane rows of the degree blocks, stacked with the row stride Bp of this call
     for (int a = 0; a < nb; ++a) {
       BlockData& b = h->blocks[a];
@@ -1353,8 +1403,10 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
       io.ldd = Bp;
       io.kmax = b.H;
       io.scale = 1.0 / sqrt((double)b.L);
-      XC_TRY(fft_run(b.fft, +1, PRO_XREAL, EPI_PLAIN, io, (int)B, (double2*)h->scratch.p, st));
+      XC_TRY(fft_run(b.fft, +1, PRO_XREAL, EPI_PLAIN, io, (int)B, fork_scratch(h, fork, a),
+                     fork_stream(h, st, fork, a)));
     }
+    XC_TRY(fork_end(h, st, fork));
     XC_TRY(mark(1));
     // the products of all time blocks in one launch (u_b stacked in partA), then the C2R
     // epilogues and the tails
@@ -1372,6 +1424,8 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
                        st));
     }
     XC_TRY(mark(2));
+    fork = fork_begin(h, st, ferr);
+    XC_TRY(ferr);
     int64_t uoff = 0;
     for (int ib = 0; ib < nb; ++ib) {
       BlockData& b = h->blocks[ib];
@@ -1389,8 +1443,9 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
       io.keep_lo = b.keep_lo;
       io.keep_hi = b.keep_hi;
       io.m_off = b.m_off;
-      XC_TRY(c2r_run(b.fftM, io, (int)B, (double2*)h->scratch.p, st));
+      XC_TRY(c2r_run(b.fftM, io, (int)B, fork_scratch(h, fork, ib), fork_stream(h, st, fork, ib)));
     }
+    XC_TRY(fork_end(h, st, fork));  // the tail columns add into rows the epilogues wrote
     const int t = h->tail;
     if (t > 0) {
       const int64_t cap = (int64_t)(h->tailpart.bytes / sizeof(double));
@@ -1442,29 +1497,13 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
                     (const double*)h->tilesA.p, s, (double*)h->partA.p, Bp, (int)B, st));
     XC_TRY(mark(1));
     const int nb = (int)h->blocks.size();
-    const bool fork = h->use_fork && nb > 1 && h->scratch_aux[0].p;
-    if (fork) {
-      if (!h->s_aux[0]) {
-        int lo = 0, hi = 0;  // the small blocks first: their CTAs are dispatched before block 1's
-        XC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        const int pr = getenv("XC_FORK_LOWPRIO") ? lo : hi;
-        for (int i = 0; i < 2; ++i) {
-          XC_CUDA(cudaStreamCreateWithPriority(&h->s_aux[i], cudaStreamNonBlocking, pr));
-          XC_CUDA(cudaEventCreateWithFlags(&h->ev_join[i], cudaEventDisableTiming));
-        }
-        XC_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
-      }
-      XC_CUDA(cudaEventRecord(h->ev_fork, st));
-      for (int i = 0; i < 2; ++i) XC_CUDA(cudaStreamWaitEvent(h->s_aux[i], h->ev_fork, 0));
-    }
+    xc_status ferr;
+    const bool fork = fork_begin(h, st, ferr);
+    XC_TRY(ferr);
     for (int ib = 0; ib < nb; ++ib) {
       BlockData& b = h->blocks[ib];
-      cudaStream_t sb = st;
-      double2* scr = (double2*)h->scratch.p;
-      if (fork && ib > 0) {
-        sb = h->s_aux[ib == 1 ? 0 : 1];
-        scr = (double2*)h->scratch_aux[ib == 1 ? 0 : 1].p;
-      }
+      cudaStream_t sb = fork_stream(h, st, fork, ib);
+      double2* scr = fork_scratch(h, fork, ib);
       double* U = (double*)h->partA.p + b.ubase * Bp;
       if (b.split)  // interleaved complex rows: reduce all Bp doubles of each double row
         XC_TRY(reduce_rows8((const double*)h->partA.p, Bp, (const int64_t*)b.grp_base.p, (const int*)b.grp_nch.p,
@@ -1483,12 +1522,7 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
       io.m_off = b.m_off;
       XC_TRY(c2r_run(b.fftM, io, (int)B, scr, sb));
     }
-    if (fork) {
-      for (int i = 0; i < 2; ++i) {
-        XC_CUDA(cudaEventRecord(h->ev_join[i], h->s_aux[i]));
-        XC_CUDA(cudaStreamWaitEvent(st, h->ev_join[i], 0));
-      }
-    }
+    XC_TRY(fork_end(h, st, fork));
     XC_TRY(mark(2));
     if (h->tail > 0)
       XC_TRY(reduce_rows8((const double*)h->partA.p, Bp, (const int64_t*)h->tail_base.p, (const int*)h->tail_nch.p,
@@ -1531,6 +1565,9 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
   }
   SpmmSrcs s{};
   const int nb = (int)h->blocks.size();
+  xc_status ferr;
+  const bool fork = fork_begin(h, st, ferr);
+  XC_TRY(ferr);
   for (int i = 0; i < nb; ++i) {
     BlockData& b = h->blocks[i];
     double* zre = (double*)h->zpl.p + h->zoff[i];
@@ -1547,12 +1584,14 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
     io.ldz = Bp;
     io.H = b.H;
     io.scale = 1.0 / sqrt((double)b.L);
-    XC_TRY(fft_run(b.fft, +1, PRO_XREAL, EPI_ZPLANES, io, (int)B, (double2*)h->scratch.p, st));
+    XC_TRY(fft_run(b.fft, +1, PRO_XREAL, EPI_ZPLANES, io, (int)B, fork_scratch(h, fork, i),
+                   fork_stream(h, st, fork, i)));
     s.re[i] = zre;
     s.im[i] = zim;
     s.nrows[i] = b.H;
     s.ld[i] = Bp;
   }
+  XC_TRY(fork_end(h, st, fork));
   s.re[nb] = X;
   s.im[nb] = nullptr;
   s.nrows[nb] = h->tail;
@@ -2012,11 +2051,13 @@ xc_status xc_workspace_query(xc_handle h, int64_t B, size_t* bytes) {
     if ((h->dirs & XC_DIR_A) && h->kind == XC_EXP && b.fft.L2 > 1) scr = std::max(scr, (size_t)b.L * B * sizeof(double2));
   }
   s += scr;
-  if ((h->dirs & XC_DIR_A) && h->kind != XC_EXP && !two_d && h->blocks.size() > 1) {
-    size_t a0 = 0, a1 = 0;  // the forked blocks' C2R scratch (ensure_ws)
+  if (h->kind != XC_EXP && h->blocks.size() > 1) {
+    size_t a0 = 0, a1 = 0;  // the forked blocks' FFT scratch (ensure_ws)
     for (size_t i = 1; i < h->blocks.size(); ++i) {
       const BlockData& b = h->blocks[i];
-      const size_t n = b.fftM.L2 > 1 ? (size_t)b.fftM.L * B * sizeof(double2) : 0;
+      size_t n = 0;
+      if (((h->dirs & XC_DIR_A) || two_d) && b.fftM.L2 > 1) n = std::max(n, (size_t)b.fftM.L * B * sizeof(double2));
+      if (((h->dirs & XC_DIR_WAT) || two_d) && b.fft.L2 > 1) n = std::max(n, (size_t)b.L * B * sizeof(double2));
       if (i == 1) a0 = std::max(a0, n);
       else a1 = std::max(a1, n);
     }
