@@ -251,7 +251,7 @@ def test_errors():
     T.close()
 
 
-def _drive_ranks(lib, kind_t, x, eps, nranks):
+def _drive_ranks(lib, kind_t, x, eps, nranks, **extra):
     """Distributed precompute with nranks emulated in one process: every rank's
     xc_build_local / xc_build_step run in lockstep; the all-gather is done by concatenating the
     ranks' send buffers (rank-major) into every rank's recv buffer."""
@@ -260,6 +260,8 @@ def _drive_ranks(lib, kind_t, x, eps, nranks):
     p = xc.XcParams()
     lib.xc_params_default(ctypes.byref(p))
     p.alpha, p.beta = kind_t[1], kind_t[2]
+    for k, v in extra.items():   # e.g. eta, n_rows, trig_precompute
+        setattr(p, k, v)
     hs, exs = [], []
     for r in range(nranks):
         h, ex = ctypes.c_void_p(), xc.XcExchange()
@@ -307,6 +309,33 @@ def test_distributed_build_equals_single(nranks):
         for k in (0, N // 3, N - 1):
             xc._check(lib.xc_node_spectrum(h, 1, k, xc._np_ptr(re), xc._np_ptr(im)))
             assert np.array_equal(re + 1j * im, T.node_spectrum(1, k))
+        lib.xc_destroy(h)
+    T.close()
+
+
+@pytest.mark.parametrize("appA", [0, 1])
+def test_distributed_build_lagspec(appA):
+    """p5 for the spectral Laguerre kind (rectangular, complex rows, circular bands), with the
+    direct and the Appendix-A precompute: 3 emulated ranks give the single build's operator
+    (bit-identical applies)."""
+    import ctypes
+    xc = _xc()
+    lib = xc.load()
+    cfg = I.CONFIGS["c7"]
+    k = I.lagspec_freqs(cfg.N, cfg.T)
+    extra = {"eta": cfg.eta, "n_rows": cfg.M, "trig_precompute": appA}
+    T = xc.Transform(xc.XC_LAGSPEC, k, cfg.eps, **extra)
+    F = I.config_rhs(cfg, 16)
+    Xp = _gpu(np.concatenate([F.real, F.imag]))
+    Y = T.apply(Xp)
+    hs, rounds = _drive_ranks(lib, (xc.XC_LAGSPEC, 0.0, 0.0), k, cfg.eps, 3, **extra)
+    assert rounds == 2
+    for h in hs:
+        Yd = torch.empty_like(Y)
+        xc._check(lib.xc_apply(h, xc.XC_DIR_A, ctypes.c_void_p(Xp.data_ptr()), 16, ctypes.c_void_p(Yd.data_ptr()),
+                               16, 16, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        torch.cuda.synchronize()
+        assert torch.equal(Yd, Y)
         lib.xc_destroy(h)
     T.close()
 
