@@ -7,7 +7,7 @@ timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_ou
 tail -3 gpurun_out/pytest_gpu.log
 timeout 600 python bench.py > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err; echo "bench rc=$?"
 cat gpurun_out/bench_c5.json
-for c in c1 c2 c3 c4; do
+for c in c1 c2 c3 c4 c6 c7 c8; do
   timeout 300 python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
 done
 timeout 300 python bench.py --config c4 --direction WAT --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_c4_wat.json 2>&1
