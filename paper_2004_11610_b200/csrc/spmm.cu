@@ -18,6 +18,8 @@
 //   D fragment  : lane holds D[lane/4][2(lane%4)+i] -> 32 contiguous bytes per nt pair.
 // Partial sums of items that split one output group are reduced in fixed order by
 // the consumer (FFT prologue / reduce_rows8), so results are deterministic.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "xc_internal.cuh"
@@ -254,6 +256,8 @@ __global__ void reduce_rows8_kernel(const double* __restrict__ part, int64_t ldp
 }  // namespace
 
 int spmm_nt_for(int64_t B) {
+  static const int force = getenv("XC_SPMM_NT") ? atoi(getenv("XC_SPMM_NT")) : 0;  // experiment
+  if (force == 1 || force == 2 || force == 4 || force == 8) return (8 * force <= B || force == 1) ? force : 1;
   if (B >= 64) return 8;
   if (B >= 32) return 4;
   if (B >= 16) return 2;
@@ -263,7 +267,12 @@ int spmm_nt_for(int64_t B) {
 xc_status spmm_run(const SpmmWin* wins, int nwins, const SpmmItem* items, const double* tiles,
                    const SpmmSrcs& srcs, double* part, int64_t ldp, int ncols, cudaStream_t st) {
   if (nwins <= 0) return XC_OK;
-  switch (spmm_nt_for(ncols)) {
+  // RHS tile: 8 NT columns; a grid smaller than two CTAs per SM takes narrower tiles (more
+  // CTAs: c2 0.020 -> 0.013 ms), never below 16 columns
+  int nt = spmm_nt_for(ncols);
+  static const bool forced = getenv("XC_SPMM_NT") != nullptr;
+  while (!forced && nt > 2 && (int64_t)nwins * ((ncols + 8 * nt - 1) / (8 * nt)) < 2 * (int64_t)sm_count()) nt /= 2;
+  switch (nt) {
     case 8: return launch<8>(wins, nwins, items, tiles, srcs, part, ldp, ncols, st);
     case 4: return launch<4>(wins, nwins, items, tiles, srcs, part, ldp, ncols, st);
     case 2: return launch<2>(wins, nwins, items, tiles, srcs, part, ldp, ncols, st);
