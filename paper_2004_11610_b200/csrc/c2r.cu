@@ -662,7 +662,8 @@ bool c2r_has_big(int mode, int R) {
 namespace {
 
 bool has_big(int mode, int R) {
-  if (getenv("XC_C2R_GENERIC") || getenv("XC_C2R_NOBIG")) return false;
+  static const bool off = getenv("XC_C2R_GENERIC") || getenv("XC_C2R_NOBIG");  // measurement switches
+  if (off) return false;
   for (const Spec& sp : kSpecs)
     if (sp.mode == mode && sp.R == R && sp.big) return true;
   return false;
@@ -696,7 +697,8 @@ xc_status launch(C2RArgs& a, const FftIO& io, cudaStream_t st) {
   }
   C2RKernel k = (C2RKernel)c2r_pass<MODE, 0, 0>;
   int nt = NTH;
-  if (!getenv("XC_C2R_GENERIC"))
+  static const bool generic = getenv("XC_C2R_GENERIC") != nullptr;
+  if (!generic)
     for (const Spec& sp : kSpecs)
       if (sp.mode == MODE && sp.R == a.R && sp.lgn == a.lgn && sp.big == a.big) {
         k = sp.k;

@@ -1968,7 +1968,8 @@ xc_status host_enqueue(xc_op* h, xc_dir dir, const double* Xh, double* Yh, int64
   const int64_t N = std::max(NI, NO);
   // chunk: a multiple of 64 columns (the SpMM column tile), at least 64
   int64_t nparts = 12;  // ~B/12 columns per chunk: the measured optimum at c5 (2D DMA efficiency vs pipeline fill)
-  if (const char* e = getenv("XC_HOST_CHUNKS")) nparts = std::max(1, atoi(e));
+  static const int env_parts = getenv("XC_HOST_CHUNKS") ? atoi(getenv("XC_HOST_CHUNKS")) : 0;
+  if (env_parts > 0) nparts = env_parts;
   int64_t Bc = std::min<int64_t>(B, std::max<int64_t>(64, ((B + nparts - 1) / nparts + 63) / 64 * 64));
   const int64_t nchunk = (B + Bc - 1) / Bc;
   const size_t slot = (size_t)N * Bc * sizeof(double);
