@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(32 * kWarps) appa_spectra_k(AppAArgs a) {
   for (int i = lane; i < Wn; i += 32) {
     const int64_t n = c - a.W + i;
     int64_t q = n;
-    const bool valid = !cosk || (n >= 0 && n < a.H);
+    // complex rows with 2W + 1 = L + 1 (full circle): the last bin repeats the first -- skipped
+    const bool valid = cosk ? (n >= 0 && n < a.H) : !(2 * a.W + 1 > a.L && i == Wn - 1);
     double re = 0.0, im = 0.0;
     if (valid) {
       if (!cosk) q = ((n % a.L) + a.L) % a.L;

@@ -347,7 +347,9 @@ xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int n
     AppAWin wm{};
     if (h->appA) {
       for (;;) {
-        const int Wmax = app_win ? appWmax : (cplx_rows ? (b.L - 1) / 2 : b.H);  // no bin evaluated twice
+        // full-spectrum mode: 2 Wmax + 1 >= L covers every bin of the circle (for even L one bin
+        // is evaluated twice, with the same value); window mode: under half the circle
+        const int Wmax = app_win ? appWmax : (cplx_rows ? b.L / 2 : b.H);
         W = std::min(appW, Wmax);
         int flag = 0;
         XC_CUDA(cudaMemsetAsync(dflag.p, 0, sizeof(int), st));

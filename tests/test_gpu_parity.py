@@ -767,3 +767,78 @@ def test_c2r_engine_vs_numpy(L, B):
     Y = xc.c2r_check(L, torch.from_numpy(U).cuda()).cpu().numpy()
     ref = np.fft.irfft(U, n=L, axis=0, norm="ortho")
     assert O.rel_l2_cols(Y, ref).max() <= 1e-13
+
+
+def _fuzz_case(i):
+    """Case i of the seeded sweep: kind, sizes, eps, direction, options drawn from PCG64(1000 + i)."""
+    rng = np.random.default_rng(1000 + i)
+    kinds = ["cos", "exp", "jacobi", "laguerre", "lagspec", "lag2d"]
+    which = kinds[i % len(kinds)]
+    N = int(rng.integers(2, 1500))
+    B = int(rng.integers(1, 72))
+    eps = float(rng.choice([1e-8, 1e-10, 1e-12]))
+    return which, N, B, eps, rng
+
+
+@pytest.mark.parametrize("i", range(72))
+def test_seeded_sweep(i):
+    """Seeded sweep over kinds x ragged sizes x eps x direction x precompute options (72 cases):
+    the GPU apply against the oracle's compressed apply on its own operator (1e-12 relative L2
+    per column; 2e-12 for the input axis of the real kinds, whose fold doubles the rounding)."""
+    xc = _xc()
+    which, N, B, eps, rng = _fuzz_case(i)
+    wat = bool(rng.integers(0, 2)) and which not in ("lag2d",)
+    dirs = xc.XC_DIR_A | (xc.XC_DIR_WAT if wat else 0)
+    d = xc.XC_DIR_WAT if wat else xc.XC_DIR_A
+    extra = {}
+    M = None
+    if which == "cos":
+        kind, kx, x = O.Kind(O.KIND_COS), xc.XC_COS, I.cos_nodes(N, i)
+        extra["trig_precompute"] = int(rng.integers(0, 2))
+    elif which == "exp":
+        kind, kx, x = O.Kind(O.KIND_EXP), xc.XC_EXP, I.exp_nodes(N, i)
+        M = int(rng.integers(2, 1500)) if rng.integers(0, 2) else None
+        extra["trig_precompute"] = int(rng.integers(0, 2))
+    elif which == "jacobi":
+        a, b = float(rng.uniform(-0.9, 2.0)), float(rng.uniform(-0.9, 2.0))
+        kind, kx = O.Kind(O.KIND_JACOBI, a, b), xc.XC_JACOBI
+        x, _, _ = O.gauss_rule(kind, N)
+        extra.update(alpha=a, beta=b)
+    elif which == "laguerre":
+        kind, kx = O.Kind(O.KIND_LAGUERRE), xc.XC_LAGUERRE
+        x, _, _ = O.gauss_rule(kind, N)
+    elif which == "lagspec":
+        eta = float(rng.uniform(10.0, 3000.0))
+        kind, kx, x = O.Kind(O.KIND_LAGSPEC, eta=eta), xc.XC_LAGSPEC, I.lagspec_freqs(N, float(rng.uniform(1, 8)))
+        M = int(rng.integers(2, 1500))
+        extra.update(eta=eta, trig_precompute=int(rng.integers(0, 2)))
+    else:
+        eta = float(rng.choice([100.0, 500.0]))
+        kind, kx, x = O.Kind(O.KIND_LAGUERRE), xc.XC_LAG2D, I.lag2d_grid(N, eta)
+    if M is not None:
+        extra["n_rows"] = M
+    w = 0.5 + rng.random(N) if wat else None
+    T = xc.Transform(kx, x, eps, dirs=dirs, weights=w, **extra)
+    cplx = which in ("exp", "lagspec")
+    rows_in = (M or N) if wat else N
+    if which == "lag2d":
+        plan = O.make_plan(kind, N, eps, eps2=0.1)
+        op = O.compress_2d(plan, x)
+        X = I.rhs(N, B, i)
+        Y = T.apply(_gpu(X)).cpu().numpy()
+        ref = O.apply_2d(op, X)
+        tol = 1e-12
+    else:
+        plan = O.make_plan(kind, N, eps, M=M) if cplx else O.make_plan(kind, N, eps)
+        op = O.compress_appA(plan, x) if extra.get("trig_precompute") else O.compress(plan, x)
+        if cplx:
+            X = I.complex_rhs(rows_in, B, i, skip_nodes=False)
+            Y = T.apply_complex(_gpu(X), d).cpu().numpy()
+        else:
+            X = I.rhs(rows_in, B, i)
+            Y = T.apply(_gpu(X), d).cpu().numpy()
+        ref = O.apply_input_axis(op, X, w) if wat else O.apply_output_axis(op, X)
+        tol = 2e-12 if (wat and not cplx) else 1e-12
+    err = O.rel_l2_cols(Y, ref).max()
+    assert err <= tol, (which, N, B, eps, wat, extra, err)
+    T.close()
