@@ -246,8 +246,20 @@ __global__ void reduce_rows8_kernel(const double* __restrict__ part, int64_t ldp
     int64_t r0 = base[g] + (row & 7);
     double sc = rowscale ? rowscale[row] : 1.0;
     for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < ncols; col += gridDim.x * blockDim.x) {
+      // four loads in flight, summed in chunk order (the same rounding as the plain loop)
+      const double* p = part + r0 * ldp + col;
+      const int64_t st = 8 * ldp;
       double s = 0.0;
-      for (int c = 0; c < n; ++c) s += part[(r0 + 8 * c) * ldp + col];
+      int c = 0;
+      for (; c + 4 <= n; c += 4) {
+        const double v0 = __ldcs(p + c * st), v1 = __ldcs(p + (c + 1) * st);
+        const double v2 = __ldcs(p + (c + 2) * st), v3 = __ldcs(p + (c + 3) * st);
+        s += v0;
+        s += v1;
+        s += v2;
+        s += v3;
+      }
+      for (; c < n; ++c) s += __ldcs(p + c * st);
       Y[(int64_t)row * ldy + col] = s * sc;
     }
   }
