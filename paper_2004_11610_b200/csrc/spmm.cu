@@ -180,9 +180,9 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
           double snd = odd ? acc[mt][0][0] : acc[mt][0][1];
           double rcv = __shfl_xor_sync(0xffffffffu, snd, 4);
           if (!odd) {
-            if (c < ldp) crow[c] = make_double2(acc[mt][0][0], rcv);
+            if (c < ldp) __stcs(crow + c, make_double2(acc[mt][0][0], rcv));
           } else {
-            if (c + 1 < ldp) crow[c + 1] = make_double2(rcv, acc[mt][0][1]);
+            if (c + 1 < ldp) __stcs(crow + c + 1, make_double2(rcv, acc[mt][0][1]));
           }
         } else {
 #pragma unroll
@@ -193,11 +193,11 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
             double s0 = odd ? v0 : v2, s1 = odd ? v1 : v3;
             double r0 = __shfl_xor_sync(0xffffffffu, s0, 4), r1 = __shfl_xor_sync(0xffffffffu, s1, 4);
             if (!odd) {
-              crow[c] = make_double2(v0, r0);
-              crow[c + 1] = make_double2(v1, r1);
+              __stcs(crow + c, make_double2(v0, r0));
+              __stcs(crow + c + 1, make_double2(v1, r1));
             } else {
-              crow[c + 2] = make_double2(r0, v2);
-              crow[c + 3] = make_double2(r1, v3);
+              __stcs(crow + c + 2, make_double2(r0, v2));
+              __stcs(crow + c + 3, make_double2(r1, v3));
             }
           }
         }
@@ -211,8 +211,8 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
 #pragma unroll
           for (int m = 0; m < NT / 2; ++m) {
             int c = tile0 + 16 * m + 4 * t;
-            *reinterpret_cast<double2*>(orow + c) = make_double2(acc[mt][2 * m][0], acc[mt][2 * m + 1][0]);
-            *reinterpret_cast<double2*>(orow + c + 2) = make_double2(acc[mt][2 * m][1], acc[mt][2 * m + 1][1]);
+            __stcs(reinterpret_cast<double2*>(orow + c), make_double2(acc[mt][2 * m][0], acc[mt][2 * m + 1][0]));
+            __stcs(reinterpret_cast<double2*>(orow + c + 2), make_double2(acc[mt][2 * m][1], acc[mt][2 * m + 1][1]));
           }
         }
       }
