@@ -66,15 +66,19 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
     const bool vec = (NT >= 2) && ((ld & 1) == 0) && ((((uintptr_t)re) & 15) == 0) &&
                      (!im || (((uintptr_t)im) & 15) == 0) && (tile0 + CW <= ncols);
     if (vec) {
+      // cp.async: every 16-byte piece of the window in flight at once (no register round trip;
+      // rows past the source are zero-filled)
       for (int idx = tid; idx < nr * (CW / 2); idx += WARPS * 32) {
         int rl = idx / (CW / 2), c2 = idx - rl * (CW / 2);
         int R = W.r0 + rl;
         int row = im ? (R >> 1) : R;
         const double* src = (im && (R & 1)) ? im : re;
-        double2 v = make_double2(0.0, 0.0);
-        if (row < nrows) v = __ldg(reinterpret_cast<const double2*>(src + (int64_t)row * ld + tile0) + c2);
-        xs2[rl * (CWP / 2) + c2] = v;
+        const bool ok = row < nrows;
+        const double2* g = reinterpret_cast<const double2*>(src + (int64_t)(ok ? row : 0) * ld + tile0) + c2;
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(&xs2[rl * (CWP / 2) + c2]);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 16 : 0));
       }
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
     } else {
       double* xw = reinterpret_cast<double*>(xs2);
       for (int idx = tid; idx < nr * CW; idx += WARPS * 32) {
