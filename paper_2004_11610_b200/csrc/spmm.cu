@@ -51,7 +51,10 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
   W.r0 = wins[blockIdx.y].r0;
   W.r1 = wins[blockIdx.y].r1;
   W.i0 = wins[blockIdx.y].i0;
+  W.i1 = wins[blockIdx.y].i1;
   W.src = wins[blockIdx.y].src;
+  // the window's item descriptors, staged next to the X window (8-byte cp.async pieces)
+  SpmmItem* its = reinterpret_cast<SpmmItem*>(xs2 + XC_WMAX * ((8 * NT + 4) / 2));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = lane & 3, g = lane >> 2;
   const int tile0 = blockIdx.x * CW;
@@ -78,7 +81,6 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
         const unsigned sa = (unsigned)__cvta_generic_to_shared(&xs2[rl * (CWP / 2) + c2]);
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 16 : 0));
       }
-      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
     } else {
       double* xw = reinterpret_cast<double*>(xs2);
       for (int idx = tid; idx < nr * CW; idx += WARPS * 32) {
@@ -89,6 +91,15 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
         xw[rl * CWP + c] = (row < nrows && tile0 + c < ncols) ? __ldg(src + (int64_t)row * ld + tile0 + c) : 0.0;
       }
     }
+    constexpr int IW = sizeof(SpmmItem) / 8;
+    const int nit = (W.i1 - W.i0) * IW;
+    const double* isrc = reinterpret_cast<const double*>(items + W.i0);
+    double* idst = reinterpret_cast<double*>(its);
+    for (int q = tid; q < nit; q += WARPS * 32) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(idst + q);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(isrc + q));
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
   }
   __syncthreads();
 
@@ -97,7 +108,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
 
   const int iw0 = W.i0 + __ldg(&wins[blockIdx.y].wo[warp]), iw1 = W.i0 + __ldg(&wins[blockIdx.y].wo[warp + 1]);
   for (int ii = iw0; ii < iw1; ++ii) {
-    const SpmmItem it = items[ii];
+    const SpmmItem it = its[ii - W.i0];
     double acc[2][NT][2];
 #pragma unroll
     for (int m = 0; m < 2; ++m)
@@ -227,7 +238,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
 template <int NT>
 xc_status launch(const SpmmWin* wins, int nwins, const SpmmItem* items, const double* tiles, const SpmmSrcs& srcs,
                  double* part, int64_t ldp, int ncols, cudaStream_t st) {
-  const size_t sm = (size_t)XC_WMAX * (8 * NT + 4) * sizeof(double);
+  const size_t sm = (size_t)XC_WMAX * (8 * NT + 4) * sizeof(double) + (size_t)XC_WIN_ITEMS * sizeof(SpmmItem);
   static std::atomic<unsigned long long> once{0};
   if (first_on_device(once))
     XC_CUDA(cudaFuncSetAttribute(spmm_win<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));

@@ -55,7 +55,7 @@ namespace {
 constexpr int KC = 184;      // node chunk of a split output-axis item (multiple of 4, <= XC_WMAX)
 constexpr int KSPLIT = 184;  // blocks whose bin groups span more nodes than this are split
 constexpr int QC = 64;       // bin chunk of an input-axis item (2 QC B rows <= XC_WMAX)
-constexpr int WIN_ITEMS = 128;  // max items per SpMM window (CTA)
+constexpr int WIN_ITEMS = XC_WIN_ITEMS;  // max items per SpMM window (CTA)
 
 struct BlockData {
   int L = 0, H = 0, m_off = 0, keep_lo = 0, keep_hi = 0;

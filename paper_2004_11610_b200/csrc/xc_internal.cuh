@@ -209,6 +209,7 @@ struct SpmmItem {
 // A window of B rows [r0, r1) (r1 - r0 <= XC_WMAX) and the items [i0, i1) inside it.
 #define XC_WMAX 192
 #define XC_WARPS 8  // warps per SpMM CTA
+#define XC_WIN_ITEMS 128  // max items per SpMM window (the CTA stages them in shared memory)
 struct SpmmWin {
   int r0, r1;
   int i0, i1;
