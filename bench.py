@@ -179,7 +179,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--strong", action="store_true", help="divide the config's B over the ranks")
     ap.add_argument("--batch", type=int, default=0, help="override RHS per rank")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--direction", default="", help="A or WAT (default: the config's first)")
     args = ap.parse_args()
