@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(BIG ? 2 * NTH : NTH, BIG ? 1 : 3)
   constexpr int NT = BIG ? 2 * NTH : NTH;  // BIG: 512 threads, tiles up to 2 TILE (one CTA per SM)
   extern __shared__ double2 smem[];
   const Smem sp = smem_parts(a, smem);
-  const Geo g = RC ? Geo{RC, LGNC} : Geo{a.R, a.lgn};
+  const Geo g = RC ? Geo{RC, LGNC >= 0 ? LGNC : a.lgn} : Geo{a.R, a.lgn};  // LGNC < 0: runtime
   const int tid = threadIdx.x;
   const int sq = tid & ((1 << g.lgn) - 1);
   const int e0 = tid >> g.lgn, estep = NT >> g.lgn;
@@ -647,6 +647,12 @@ const Spec kSpecs[] = {
     XC_SPEC(1, 216, 3), XC_SPEC(0, 54, 5),  XC_SPEC(1, 256, 3), XC_SPEC(0, 45, 5), XC_SPEC(1, 100, 4),
     XC_SPEC(0, 27, 6),  XC_SPEC(1, 54, 5),  XC_SPEC(1, 240, 3), XC_SPEC(1, 64, 5), XC_SPEC(0, 32, 6),
     XC_SPEC(0, 36, 5),  XC_SPEC(0, 9, 7),
+    // single-pass lengths (M <= 512) of the configured workloads, any sequences per tile: a
+    // compact kernel instead of the generic one (12.7K instructions; a one-CTA launch at B = 1
+    // spends most of its 15 us fetching them)
+    XC_SPEC(2, 360, -1), XC_SPEC(2, 144, -1), XC_SPEC(2, 54, -1),  XC_SPEC(2, 375, -1), XC_SPEC(2, 128, -1),
+    XC_SPEC(2, 40, -1),  XC_SPEC(2, 200, -1), XC_SPEC(2, 64, -1),  XC_SPEC(2, 480, -1), XC_SPEC(2, 180, -1),
+    XC_SPEC(2, 72, -1),  XC_SPEC(2, 30, -1),  XC_SPEC(2, 225, -1), XC_SPEC(2, 96, -1),  XC_SPEC(2, 45, -1),
 };
 #undef XC_SPEC
 #undef XC_BIG
@@ -700,7 +706,7 @@ xc_status launch(C2RArgs& a, const FftIO& io, cudaStream_t st) {
   static const bool generic = getenv("XC_C2R_GENERIC") != nullptr;
   if (!generic)
     for (const Spec& sp : kSpecs)
-      if (sp.mode == MODE && sp.R == a.R && sp.lgn == a.lgn && sp.big == a.big) {
+      if (sp.mode == MODE && sp.R == a.R && (sp.lgn == a.lgn || sp.lgn < 0) && sp.big == a.big) {
         k = sp.k;
         nt = sp.big ? 2 * NTH : NTH;
       }
