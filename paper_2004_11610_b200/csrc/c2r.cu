@@ -21,6 +21,7 @@
 // the last stage writes global memory straight from registers (columns are the fast
 // index, so every store is a contiguous run of cb * 16 or cb * 8 bytes).
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -647,6 +648,7 @@ const Spec kSpecs[] = {
     XC_SPEC(1, 216, 3), XC_SPEC(0, 54, 5),  XC_SPEC(1, 256, 3), XC_SPEC(0, 45, 5), XC_SPEC(1, 100, 4),
     XC_SPEC(0, 27, 6),  XC_SPEC(1, 54, 5),  XC_SPEC(1, 240, 3), XC_SPEC(1, 64, 5), XC_SPEC(0, 32, 6),
     XC_SPEC(0, 36, 5),  XC_SPEC(0, 9, 7),
+    XC_SPEC(0, 25, 6),  XC_SPEC(1, 45, 5),  XC_SPEC(0, 15, 7),  XC_SPEC(1, 36, 5), XC_SPEC(1, 50, 5),  // c3, c8
     // single-pass lengths (M <= 512) of the configured workloads, any sequences per tile: a
     // compact kernel instead of the generic one (12.7K instructions; a one-CTA launch at B = 1
     // spends most of its 15 us fetching them)
@@ -710,6 +712,9 @@ xc_status launch(C2RArgs& a, const FftIO& io, cudaStream_t st) {
         k = sp.k;
         nt = sp.big ? 2 * NTH : NTH;
       }
+  static const bool log_generic = getenv("XC_C2R_LOG") != nullptr;  // which passes run generic
+  if (log_generic && k == (C2RKernel)c2r_pass<MODE, 0, 0>)
+    fprintf(stderr, "c2r generic: mode %d R %d lgn %d big %d\n", MODE, a.R, a.lgn, a.big);
   if (a.big && nt == NTH) {
     xc_set_error("c2r: big tile without a big kernel");
     return XC_EUNSUPPORTED;
