@@ -134,6 +134,18 @@ xc_status xc_params_default(xc_params* p);
 xc_status xc_build_compressed(xc_kind kind, const xc_params* p, const double* nodes, int64_t N,
                               double eps, xc_handle* out);
 
+/* The computation stage on node bands given by the caller instead of the GPU precompute (p2-p4):
+ * the plan (zeta, chain, windows) is this library's for (kind, p, nodes, N, eps) -- query it with
+ * xc_plan_chain -- and for block i node k keeps bins [start[i][k], start[i][k] + len[i][k]) of the
+ * block's spectrum (real rows: half spectrum, start + len <= L/2 + 1; XC_EXP / XC_LAGSPEC: all L
+ * bins, the run taken mod L), values vals[i] = (re, im) pairs, the runs of all nodes concatenated
+ * in node order (len[i][k] pairs per node; zeros allowed).  Host pointers, copied.  The tests use
+ * it to apply the oracle's own operator (same kept entries).  XC_EUNSUPPORTED for
+ * XC_LAG2D and trig_precompute = 1; XC_EINVAL for runs out of range. */
+xc_status xc_build_from_bands(xc_kind kind, const xc_params* p, const double* nodes, int64_t N, double eps,
+                              const int* const* start, const int* const* len, const double* const* vals,
+                              xc_handle* out);
+
 /* Distributed precompute (the node range of the operator is split over ranks).
  * One exchange: the caller copies `send` (bytes_per_rank device bytes) of every rank into
  * `recv` in rank order (recv + r * bytes_per_rank), e.g. one NCCL all-gather.

@@ -1698,6 +1698,59 @@ xc_status xc_build_compressed(xc_kind kind, const xc_params* p, const double* no
   return XC_OK;
 }
 
+xc_status xc_build_from_bands(xc_kind kind, const xc_params* p, const double* nodes, int64_t N, double eps,
+                              const int* const* start, const int* const* len, const double* const* vals,
+                              xc_handle* out) {
+  if (!out || !start || !len || !vals) {
+    xc_set_error("build_from_bands: null argument");
+    return XC_EINVAL;
+  }
+  *out = nullptr;
+  if (kind == XC_LAG2D || (p && p->trig_precompute != 0)) {
+    xc_set_error("build_from_bands: node bands of the 1D operators with the Kaiser window only");
+    return XC_EUNSUPPORTED;
+  }
+  xc_op* h = new xc_op();
+  auto fail = [&](xc_status s) {
+    destroy_impl(h);
+    delete h;
+    return s;
+  };
+  xc_status s = build_begin(kind, p, nodes, N, eps, h);
+  if (s != XC_OK) return fail(s);
+  for (size_t i = 0; i < h->blocks.size(); ++i) {
+    BlockData& b = h->blocks[i];
+    DevBuf none;
+    if ((s = block_setup(h, b, none)) != XC_OK) return fail(s);
+    if (!start[i] || !len[i] || !vals[i]) {
+      xc_set_error("build_from_bands: null band arrays of block " + std::to_string(i));
+      return fail(XC_EINVAL);
+    }
+    b.h_start.assign(start[i], start[i] + N);
+    b.h_len.assign(len[i], len[i] + N);
+    b.h_off.assign(N + 1, 0);
+    int64_t tot = 0;
+    for (int64_t k = 0; k < N; ++k) {
+      if (b.h_len[k] < 0 || b.h_len[k] > b.H || b.h_start[k] < 0 || b.h_start[k] >= std::max(1, b.H) ||
+          (h->kind != XC_EXP && b.h_start[k] + b.h_len[k] > b.H)) {
+        xc_set_error("build_from_bands: band out of range at block " + std::to_string(i) + ", node " +
+                     std::to_string(k));
+        return fail(XC_EINVAL);
+      }
+      tot += b.h_len[k];
+    }
+    std::vector<double2> v(std::max<int64_t>(1, tot));
+    for (int64_t q = 0; q < tot; ++q) v[q] = make_double2(vals[i][2 * q], vals[i][2 * q + 1]);
+    if ((s = upload(b.vals, v)) != XC_OK) return fail(s);
+    if ((s = upload(b.start, b.h_start)) != XC_OK) return fail(s);
+    if ((s = upload(b.len, b.h_len)) != XC_OK) return fail(s);
+    b.loc_count = tot;
+  }
+  if ((s = build_end(h)) != XC_OK) return fail(s);
+  *out = h;
+  return XC_OK;
+}
+
 // ---- distributed precompute: node range per rank + two all-gathers ----------
 namespace {
 

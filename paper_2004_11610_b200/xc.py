@@ -50,7 +50,7 @@ class XcBlockInfo(ctypes.Structure):
                 ("keep_hi", ctypes.c_int), ("nnz", _i64), ("max_band", ctypes.c_int), ("q_taps", ctypes.c_int)]
 
 
-EXPORTS = ["xc_params_default", "xc_build_compressed", "xc_build_local", "xc_build_step", "xc_apply", "xc_c2r_check", "xc_set_graphs", "xc_apply_host", "xc_apply_host_async", "xc_host_wait", "xc_reserve",
+EXPORTS = ["xc_params_default", "xc_build_compressed", "xc_build_from_bands", "xc_build_local", "xc_build_step", "xc_apply", "xc_c2r_check", "xc_set_graphs", "xc_apply_host", "xc_apply_host_async", "xc_host_wait", "xc_reserve",
            "xc_workspace_query", "xc_info", "xc_block_info", "xc_block_window", "xc_node_spectrum",
            "xc_gauss_rule", "xc_plan_chain", "xc_profile_enable", "xc_profile_read", "xc_destroy",
            "xc_last_error", "xc_version"]
@@ -77,6 +77,10 @@ def load():
     lib.xc_build_local.argtypes = [ctypes.c_int, ctypes.POINTER(XcParams), _dp, _i64, ctypes.c_double, ctypes.c_int,
                                    ctypes.c_int, ctypes.POINTER(vp), ctypes.POINTER(XcExchange)]
     lib.xc_build_step.argtypes = [vp, ctypes.POINTER(XcExchange)]
+    lib.xc_build_from_bands.argtypes = [ctypes.c_int, ctypes.POINTER(XcParams), _dp, _i64, ctypes.c_double,
+                                        ctypes.POINTER(ctypes.POINTER(ctypes.c_int)),
+                                        ctypes.POINTER(ctypes.POINTER(ctypes.c_int)), ctypes.POINTER(_dp),
+                                        ctypes.POINTER(vp)]
     lib.xc_apply.argtypes = [vp, ctypes.c_int, vp, _i64, vp, _i64, _i64, vp]
     lib.xc_apply_host.argtypes = [vp, ctypes.c_int, vp, vp, _i64, vp]
     lib.xc_set_graphs.argtypes = [vp, ctypes.c_int]
@@ -214,6 +218,44 @@ class Transform:
             torch.cuda.synchronize(device)
             self.exchanges.append(n)
             _check(lib.xc_build_step(self._h, ctypes.byref(ex)))
+
+    @classmethod
+    def from_bands(cls, kind: int, nodes, eps: float, bands, **kw):
+        """xc_build_from_bands: the computation stage on caller-supplied node bands, one
+        (start int32[N], len int32[N], vals complex128[sum len]) triple per block of the plan."""
+        lib = load()
+        self = cls.__new__(cls)
+        self._lib = lib
+        self.kind = kind
+        x = np.ascontiguousarray(np.asarray(nodes, dtype=np.float64))
+        self.N = x.size
+        self.M = kw.get("n_rows", 0) or self.N
+        p = XcParams()
+        lib.xc_params_default(ctypes.byref(p))
+        for k, v in kw.items():
+            if k == "weights":
+                self._w = np.ascontiguousarray(np.asarray(v, dtype=np.float64))
+                p.weights = _np_ptr(self._w)
+            else:
+                setattr(p, k, v)
+        nb = len(bands)
+        keep = []
+        st = (ctypes.POINTER(ctypes.c_int) * nb)()
+        ln = (ctypes.POINTER(ctypes.c_int) * nb)()
+        vl = (_dp * nb)()
+        for i, (s0, l0, v0) in enumerate(bands):
+            s0 = np.ascontiguousarray(s0, dtype=np.int32)
+            l0 = np.ascontiguousarray(l0, dtype=np.int32)
+            v0 = np.ascontiguousarray(np.asarray(v0, dtype=np.complex128)).view(np.float64)
+            keep += [s0, l0, v0]
+            st[i] = s0.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
+            ln[i] = l0.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
+            vl[i] = _np_ptr(v0) if v0.size else _np_ptr(np.zeros(2))
+        h = ctypes.c_void_p()
+        self.device = kw.get("device", 0)
+        _check(lib.xc_build_from_bands(kind, ctypes.byref(p), _np_ptr(x), self.N, eps, st, ln, vl, ctypes.byref(h)))
+        self._h = h
+        return self
 
     # -- computation stage --------------------------------------------------------------
     def apply(self, X, direction: int = XC_DIR_A, out=None, stream=None):

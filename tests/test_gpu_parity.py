@@ -866,3 +866,91 @@ def test_seeded_sweep(i):
         err = min(errs)
     assert err <= tol, (which, N, B, eps, wat, extra, err)
     T.close()
+
+
+def _bands_of(op, circ):
+    """The oracle operator's kept entries as one run per node (test glue, no method arithmetic):
+    real rows [first, last] kept bin; complex rows the shortest circular arc holding them."""
+    out = []
+    for S in op.S:
+        S = S.tocsr()
+        N, H = S.shape
+        start = np.zeros(N, np.int32)
+        ln = np.zeros(N, np.int32)
+        vals = []
+        for k in range(N):
+            idx = S.indices[S.indptr[k]:S.indptr[k + 1]]
+            if idx.size == 0:
+                continue
+            idx = np.sort(idx)
+            if circ:
+                gaps = np.diff(np.r_[idx, idx[0] + H]) - 1          # gap after each kept bin
+                g = int(np.argmax(gaps))
+                s0 = int(idx[(g + 1) % idx.size])
+                n = H - int(gaps[g])
+            else:
+                s0, n = int(idx[0]), int(idx[-1] - idx[0] + 1)
+            row = S[k].toarray().ravel()
+            start[k], ln[k] = s0, n
+            vals.append(row[(s0 + np.arange(n)) % H])
+        out.append((start, ln, np.concatenate(vals) if vals else np.zeros(0, np.complex128)))
+    return out
+
+
+IMPORT_CASES = [("c1", "jacobi", 512, 7, 1e-12), ("c2", "cos", 4096, 64, 1e-10), ("c3_red", "jac", 2048, 40, 1e-12),
+                ("lag", "laguerre", 1932, 33, 1e-10), ("exp", "exp", 1000, 21, 1e-10),
+                ("lagspec", "lagspec", 501, 16, 1e-10)]
+
+
+@pytest.mark.parametrize("case", IMPORT_CASES, ids=[c[0] for c in IMPORT_CASES])
+def test_same_operator_parity(case):
+    """BASELINE's first bar on the SAME operator: the oracle's kept entries imported as node bands
+    (xc_build_from_bands), the GPU computation stage vs the oracle's compressed apply at 1e-12 in
+    both directions -- no threshold tie can differ."""
+    xc = _xc()
+    name, which, N, B, eps = case
+    extra, M = {}, None
+    if which == "jacobi":
+        kind, kx = O.Kind(O.KIND_JACOBI, 0.0, 0.0), xc.XC_JACOBI
+        x, _, _ = O.gauss_rule(kind, N)
+    elif which == "jac":
+        kind, kx = O.Kind(O.KIND_JACOBI, 0.5, -0.3), xc.XC_JACOBI
+        x, _, _ = O.gauss_rule(kind, N)
+        extra.update(alpha=0.5, beta=-0.3)
+    elif which == "cos":
+        kind, kx, x = O.Kind(O.KIND_COS), xc.XC_COS, I.cos_nodes(N, 1)
+    elif which == "laguerre":
+        kind, kx = O.Kind(O.KIND_LAGUERRE), xc.XC_LAGUERRE
+        x, _, _ = O.gauss_rule(kind, N)
+    elif which == "exp":
+        kind, kx, x = O.Kind(O.KIND_EXP), xc.XC_EXP, I.exp_nodes(N, 9)
+        M = 777
+    else:
+        cfg = I.CONFIGS["c7"]
+        kind, kx, x = O.Kind(O.KIND_LAGSPEC, eta=cfg.eta), xc.XC_LAGSPEC, I.lagspec_freqs(N, cfg.T)
+        M = cfg.M
+        extra["eta"] = cfg.eta
+    if M:
+        extra["n_rows"] = M
+    cplx = which in ("exp", "lagspec")
+    plan = O.make_plan(kind, N, eps, M=M) if cplx else O.make_plan(kind, N, eps)
+    op = O.compress(plan, x)
+    w = 0.5 + np.random.default_rng(3).random(N)
+    T = xc.Transform.from_bands(kx, x, eps, _bands_of(op, cplx), dirs=xc.XC_DIR_A | xc.XC_DIR_WAT, weights=w,
+                                **extra)
+    assert [(b["L"], b["keep_lo"], b["keep_hi"]) for b in T.blocks()] == \
+        [(b.L, b.keep_lo, b.keep_hi) for b in plan.blocks]
+    rows = M or N
+    if cplx:
+        X = I.complex_rhs(N, B, 5, skip_nodes=False)
+        C = I.complex_rhs(rows, B, 6, skip_nodes=False)
+        Y = T.apply_complex(_gpu(X)).cpu().numpy()
+        Yw = T.apply_complex(_gpu(C), xc.XC_DIR_WAT).cpu().numpy()
+    else:
+        X = I.rhs(N, B, 5)
+        C = I.rhs(rows, B, 6)
+        Y = T.apply(_gpu(X)).cpu().numpy()
+        Yw = T.apply(_gpu(C), xc.XC_DIR_WAT).cpu().numpy()
+    assert O.rel_l2_cols(Y, O.apply_output_axis(op, X)).max() <= 1e-12, name
+    assert O.rel_l2_cols(Yw, O.apply_input_axis(op, C, w)).max() <= 1e-12, name
+    T.close()
