@@ -954,3 +954,31 @@ def test_same_operator_parity(case):
     assert O.rel_l2_cols(Y, O.apply_output_axis(op, X)).max() <= 1e-12, name
     assert O.rel_l2_cols(Yw, O.apply_input_axis(op, C, w)).max() <= 1e-12, name
     T.close()
+
+
+EXTREME = [("legendre_1e-14", (O.KIND_JACOBI, 0.0, 0.0), 1500, 40, 1e-14, False),
+           ("cos_1e-6_wat", (O.KIND_COS, 0.0, 0.0), 2000, 70, 1e-6, True),
+           ("jacobi_-0.95", (O.KIND_JACOBI, -0.95, -0.95), 1200, 33, 1e-12, True),
+           ("jacobi_4_4", (O.KIND_JACOBI, 4.0, 4.0), 1200, 33, 1e-12, True)]
+
+
+@pytest.mark.parametrize("case", EXTREME, ids=[c[0] for c in EXTREME])
+def test_extreme_parameters(case):
+    """Thresholds at the ends of the range (eps 1e-14: zeta ~ 35, wider bands; eps 1e-6) and
+    Jacobi parameters near -1 and large, against the oracle (1e-12) and the dense product (10 eps)."""
+    xc = _xc()
+    name, kt, N, B, eps, wat = case
+    kind = O.Kind(*kt)
+    x = I.cos_nodes(N, 4) if kt[0] == O.KIND_COS else O.gauss_rule(kind, N)[0]
+    w = 0.5 + np.random.default_rng(1).random(N) if wat else None
+    T = xc.Transform(kt[0], x, eps, alpha=kt[1], beta=kt[2], dirs=xc.XC_DIR_A | (xc.XC_DIR_WAT if wat else 0),
+                     weights=w)
+    op = O.compress(O.make_plan(kind, N, eps), x)
+    X = I.rhs(N, B, 3)
+    d = xc.XC_DIR_WAT if wat else xc.XC_DIR_A
+    Y = T.apply(_gpu(X), d).cpu().numpy()
+    ref = O.apply_input_axis(op, X, w) if wat else O.apply_output_axis(op, X)
+    assert O.rel_l2_cols(Y, ref).max() <= 1e-12, name
+    dense = (w[:, None] * O.dense_apply_t(kind, x, X[:, :4])) if wat else O.dense_apply(kind, x, X[:, :4])
+    assert O.rel_l2_cols(Y[:, :4], dense).max() <= 10 * eps, name
+    T.close()
