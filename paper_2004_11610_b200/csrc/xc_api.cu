@@ -582,6 +582,12 @@ xc_status upload_and_fill(xc_op* h, ItemSet& S, bool input_axis, DevBuf& d_items
   });
   std::vector<SpmmItem> sorted(S.items.size());
   for (size_t i = 0; i < ord.size(); ++i) sorted[i] = S.items[ord[i]];
+  // tiny operators (fewer than 16 items per SM, e.g. c1): fewer items per window, so that the
+  // single-column-tile grid still has >= 2 CTAs per SM
+  const int64_t nsm = sm_count();
+  const int win_items = (int64_t)sorted.size() < 16 * nsm
+                            ? (int)std::max<int64_t>(8, ((int64_t)sorted.size() + 2 * nsm - 1) / (2 * nsm))
+                            : WIN_ITEMS;
   std::vector<SpmmWin> wins;
   std::vector<int64_t> wcost;  // the window's critical path: its most loaded warp
   size_t i = 0;
@@ -592,7 +598,7 @@ xc_status upload_and_fill(xc_op* h, ItemSet& S, bool input_axis, DevBuf& d_items
     w.r1 = sorted[i].k0 + 4 * sorted[i].nsteps;
     w.i0 = (int)i;
     size_t j = i + 1;
-    while (j < sorted.size() && sorted[j].src == w.src && (int)(j - i) < WIN_ITEMS) {
+    while (j < sorted.size() && sorted[j].src == w.src && (int)(j - i) < win_items) {
       int e = sorted[j].k0 + 4 * sorted[j].nsteps;
       if (std::max(e, w.r1) - w.r0 > XC_WMAX) break;
       w.r1 = std::max(w.r1, e);
