@@ -138,9 +138,11 @@ struct xc_op {
   cudaStream_t s_in = nullptr, s_out = nullptr;
   // XC_DIR_A of the block kinds: after the SpMM the blocks are independent; block 2 and the
   // smaller blocks run on two forked streams beside block 1 (own C2R scratch each)
-  cudaStream_t s_aux[2] = {nullptr, nullptr};
-  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
-  DevBuf scratch_aux[2];
+  static constexpr int kAux = 4;  // forked streams: block 2 alone, blocks 3.. round robin over 3
+  cudaStream_t s_aux[kAux] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[kAux] = {};
+  DevBuf scratch_aux[kAux];
+  int naux = 2;  // forked streams of the current apply (naux_for)
   bool use_fork = true;
   static constexpr int kSlots = 3;  // device slots of the host-buffer pipeline
   cudaEvent_t ev_in[kSlots] = {}, ev_cmp[kSlots] = {}, ev_out[kSlots] = {};
@@ -181,6 +183,12 @@ void clear_graphs(xc_op* h) {
   h->graphs.clear();
 }
 
+// Forked stream of block ib >= 1 (fork_stream): block 2 on its own, blocks 3.. round robin over
+// naux - 1 streams.  Large batches use naux = 2 (blocks 3.. in one stream: more concurrent
+// streams slowed c5's FFT phase 3.94 -> 4.09 ms), small ones all four (c3 0.255 -> 0.225 ms).
+inline int aux_of(int ib, int naux) { return ib == 1 ? 0 : 1 + (ib - 2) % (naux - 1); }
+inline int naux_for(int64_t N, int64_t B) { return N * B <= (32LL << 20) ? xc_op::kAux : 2; }
+
 xc_status ensure_ws(xc_op* h, int64_t B) {
   if (B <= h->ws_B) return XC_OK;
   int64_t Bp = pad_cols(B);
@@ -194,17 +202,17 @@ xc_status ensure_ws(xc_op* h, int64_t B) {
   }
   XC_TRY(dev_alloc(h->scratch, std::max<size_t>(1, scratch_n) * sizeof(double2)));
   if (h->kind != XC_EXP && h->blocks.size() > 1) {
-    size_t a0 = 0, a1 = 0;  // block 2 on s_aux[0], blocks 3.. on s_aux[1] (fork_stream)
+    size_t an[xc_op::kAux] = {};  // each forked stream's FFT scratch: the max over its blocks
     for (size_t i = 1; i < h->blocks.size(); ++i) {
       const BlockData& b = h->blocks[i];
       size_t n = 1;
       if (((h->dirs & XC_DIR_A) || two_d) && b.fftM.L2 > 1) n = std::max(n, (size_t)b.fftM.L * (size_t)B);
       if (((h->dirs & XC_DIR_WAT) || two_d) && b.fft.L2 > 1) n = std::max(n, (size_t)b.L * (size_t)B);
-      if (i == 1) a0 = std::max(a0, n);
-      else a1 = std::max(a1, n);
+      for (int na : {2, (int)xc_op::kAux})  // scratch for either stream assignment (naux_for)
+        an[aux_of((int)i, na)] = std::max(an[aux_of((int)i, na)], n);
     }
-    XC_TRY(dev_alloc(h->scratch_aux[0], std::max<size_t>(1, a0) * sizeof(double2)));
-    XC_TRY(dev_alloc(h->scratch_aux[1], std::max<size_t>(1, a1) * sizeof(double2)));
+    for (int i = 0; i < xc_op::kAux; ++i)
+      XC_TRY(dev_alloc(h->scratch_aux[i], std::max<size_t>(1, an[i]) * sizeof(double2)));
   }
   if (h->dirs & XC_DIR_A) XC_TRY(dev_alloc(h->partA, (size_t)h->rowsA * Bp * sizeof(double)));
   if (two_d && h->bsr_nslots > 0)  // partial rows of the split DMMA groups
@@ -1336,11 +1344,12 @@ const SpmmWin* wins_for(const DevBuf& w, int nwins, int64_t B) {
 }
 
 // Per-block phases (the blocks are independent there): block 1 stays on the caller's stream,
-// block 2 goes to s_aux[0], blocks 3.. to s_aux[1] (high priority: their few CTAs are dispatched
-// ahead of block 1's persistent grid), each with its own FFT scratch; fork/join by events, so
-// the phase also works under CUDA-graph capture.
-bool fork_begin(xc_op* h, cudaStream_t st, xc_status& err) {
+// block 2 goes to s_aux[0], blocks 3.. round robin to s_aux[1..3] (high priority: their few CTAs
+// are dispatched ahead of block 1's persistent grid), each stream with its own FFT scratch;
+// fork/join by events, so the phase also works under CUDA-graph capture.
+bool fork_begin(xc_op* h, cudaStream_t st, int64_t B, xc_status& err) {
   err = XC_OK;
+  h->naux = naux_for(h->N, B);
   if (!h->use_fork || h->blocks.size() < 2 || !h->scratch_aux[0].p) return false;
   auto fail = [&](cudaError_t e) {
     xc_set_error(std::string("fork: ") + cudaGetErrorString(e));
@@ -1351,21 +1360,23 @@ bool fork_begin(xc_op* h, cudaStream_t st, xc_status& err) {
   if (!h->s_aux[0]) {
     int lo = 0, hi = 0;
     if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return fail(e);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < xc_op::kAux; ++i) {
       if ((e = cudaStreamCreateWithPriority(&h->s_aux[i], cudaStreamNonBlocking, hi)) != cudaSuccess) return fail(e);
       if ((e = cudaEventCreateWithFlags(&h->ev_join[i], cudaEventDisableTiming)) != cudaSuccess) return fail(e);
     }
     if ((e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
   }
   if ((e = cudaEventRecord(h->ev_fork, st)) != cudaSuccess) return fail(e);
-  for (int i = 0; i < 2; ++i)
+  const int na = std::min<int>(h->naux, (int)h->blocks.size() - 1);  // streams in use
+  for (int i = 0; i < na; ++i)
     if ((e = cudaStreamWaitEvent(h->s_aux[i], h->ev_fork, 0)) != cudaSuccess) return fail(e);
   return true;
 }
 
 xc_status fork_end(xc_op* h, cudaStream_t st, bool fork) {
   if (!fork) return XC_OK;
-  for (int i = 0; i < 2; ++i) {
+  const int na = std::min<int>(h->naux, (int)h->blocks.size() - 1);
+  for (int i = 0; i < na; ++i) {
     XC_CUDA(cudaEventRecord(h->ev_join[i], h->s_aux[i]));
     XC_CUDA(cudaStreamWaitEvent(st, h->ev_join[i], 0));
   }
@@ -1373,11 +1384,11 @@ xc_status fork_end(xc_op* h, cudaStream_t st, bool fork) {
 }
 
 cudaStream_t fork_stream(xc_op* h, cudaStream_t st, bool fork, int ib) {
-  return (fork && ib > 0) ? h->s_aux[ib == 1 ? 0 : 1] : st;
+  return (fork && ib > 0) ? h->s_aux[aux_of(ib, h->naux)] : st;
 }
 
 double2* fork_scratch(xc_op* h, bool fork, int ib) {
-  return (double2*)((fork && ib > 0) ? h->scratch_aux[ib == 1 ? 0 : 1].p : h->scratch.p);
+  return (double2*)((fork && ib > 0) ? h->scratch_aux[aux_of(ib, h->naux)].p : h->scratch.p);
 }
 
 xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t B,
@@ -1413,7 +1424,7 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
   if (h->ukind == XC_LAG2D) {  // R-23: prologues, merged 2D products + C2R per time block, tails
     const int nb = (int)h->blocks.size();
     xc_status ferr;
-    bool fork = fork_begin(h, st, ferr);
+    bool fork = fork_begin(h, st, B, ferr);
     XC_TRY(ferr);
     int64_t zrow = 0;  // plane rows of the degree blocks, stacked with the row stride Bp of this call
     for (int a = 0; a < nb; ++a) {
@@ -1451,7 +1462,7 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
                        st));
     }
     XC_TRY(mark(2));
-    fork = fork_begin(h, st, ferr);
+    fork = fork_begin(h, st, B, ferr);
     XC_TRY(ferr);
     int64_t uoff = 0;
     for (int ib = 0; ib < nb; ++ib) {
@@ -1525,7 +1536,7 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
     XC_TRY(mark(1));
     const int nb = (int)h->blocks.size();
     xc_status ferr;
-    const bool fork = fork_begin(h, st, ferr);
+    const bool fork = fork_begin(h, st, B, ferr);
     XC_TRY(ferr);
     for (int ib = 0; ib < nb; ++ib) {
       BlockData& b = h->blocks[ib];
@@ -1593,7 +1604,7 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
   SpmmSrcs s{};
   const int nb = (int)h->blocks.size();
   xc_status ferr;
-  const bool fork = fork_begin(h, st, ferr);
+  const bool fork = fork_begin(h, st, B, ferr);
   XC_TRY(ferr);
   for (int i = 0; i < nb; ++i) {
     BlockData& b = h->blocks[i];
@@ -1636,7 +1647,7 @@ void destroy_impl(xc_op* h) {
   clear_graphs(h);
   for (auto& e : h->ev) cudaEventDestroy(e);
   h->ev.clear();
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < xc_op::kAux; ++i) {
     if (h->s_aux[i]) {
       cudaStreamSynchronize(h->s_aux[i]);
       cudaStreamDestroy(h->s_aux[i]);
@@ -2133,16 +2144,16 @@ xc_status xc_workspace_query(xc_handle h, int64_t B, size_t* bytes) {
   }
   s += scr;
   if (h->kind != XC_EXP && h->blocks.size() > 1) {
-    size_t a0 = 0, a1 = 0;  // the forked blocks' FFT scratch (ensure_ws)
+    size_t an[xc_op::kAux] = {};  // the forked streams' FFT scratch (ensure_ws)
     for (size_t i = 1; i < h->blocks.size(); ++i) {
       const BlockData& b = h->blocks[i];
       size_t n = 0;
       if (((h->dirs & XC_DIR_A) || two_d) && b.fftM.L2 > 1) n = std::max(n, (size_t)b.fftM.L * B * sizeof(double2));
       if (((h->dirs & XC_DIR_WAT) || two_d) && b.fft.L2 > 1) n = std::max(n, (size_t)b.L * B * sizeof(double2));
-      if (i == 1) a0 = std::max(a0, n);
-      else a1 = std::max(a1, n);
+      for (int na : {2, (int)xc_op::kAux})  // scratch for either stream assignment (naux_for)
+        an[aux_of((int)i, na)] = std::max(an[aux_of((int)i, na)], n);
     }
-    s += a0 + a1;
+    for (size_t a : an) s += a;
   }
   if (h->dirs & XC_DIR_A) s += (size_t)h->rowsA * Bp * 8;
   if ((h->dirs & XC_DIR_WAT) || two_d) {
