@@ -2,7 +2,9 @@
 import collections, csv, sys
 
 path = sys.argv[1]
-napply = float(sys.argv[2]) if len(sys.argv) > 2 else 5.0
+# applies executed inside the NVTX range of `bench.py --steps 2 --warmup 3`: 3 warm-up + 2 graph
+# + 2 timed (graph replay) + 2 profiled (eager) = 9 (5 before the graph-replay headline)
+napply = float(sys.argv[2]) if len(sys.argv) > 2 else 9.0
 rows = list(csv.reader(open(path)))
 hdr = None
 agg = collections.OrderedDict()
