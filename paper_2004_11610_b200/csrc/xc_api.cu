@@ -593,9 +593,12 @@ xc_status upload_and_fill(xc_op* h, ItemSet& S, bool input_axis, DevBuf& d_items
   // tiny operators (fewer than 16 items per SM, e.g. c1): fewer items per window, so that the
   // single-column-tile grid still has >= 2 CTAs per SM
   const int64_t nsm = sm_count();
+  // otherwise the output axis takes at most 64 items per window (c4 forward SpMM 1.366 -> 1.314
+  // ms; c5 unchanged, its windows are bounded by their 192 rows), the input axis 128 (64 there
+  // made c4 backward 2.5 % slower)
   const int win_items = (int64_t)sorted.size() < 16 * nsm
                             ? (int)std::max<int64_t>(8, ((int64_t)sorted.size() + 2 * nsm - 1) / (2 * nsm))
-                            : WIN_ITEMS;
+                            : (input_axis ? WIN_ITEMS : std::min(64, WIN_ITEMS));
   std::vector<SpmmWin> wins;
   std::vector<int64_t> wcost;  // the window's critical path: its most loaded warp
   size_t i = 0;
