@@ -8,9 +8,12 @@ over every block + dense tail, then the per-block inverse FFTs with the fused
 W^{-1}/truncate epilogue) over one batch of B right-hand sides already resident
 in HBM.  Default workload: BASELINE.json configs[4] (c5: Legendre N = 65536,
 B = 4096 per GPU, eps = 1e-12; the config the metric's 1/2/4/8-GPU scaling is
-quoted on).  Multi-GPU: torchrun, one rank per GPU, the operator replicated and
-the RHS batch sharded with no collective on the data path (weak scaling: every
-rank applies B columns; --strong divides B by the world size).
+quoted on).  Multi-GPU: one rank per GPU (torchrun; `--gpus N` without a
+launcher re-launches itself under torch.distributed.run), the operator replicated
+(built by the distributed precompute: node range per rank + NCCL all-gather) and
+the config's seeded batch sharded by column with no collective on the data path
+(strong scaling of the global B = 4096, the default; --weak gives every rank the
+whole batch).
 
 Prints ONE JSON line on rank 0.
 """
@@ -38,13 +41,6 @@ def _peaks():
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         return {"hbm_gbs": 6650.0, "_fallback": True}
-
-
-def _dist():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
 
 
 class Clocks:
@@ -119,48 +115,131 @@ def _timing_nodes(cfg):
     return scipy.special.roots_jacobi(cfg.N, cfg.alpha, cfg.beta)[0]
 
 
-def cpu_oracle_rate(cfg, ncols, ndeg, threads, x=None):
-    """The oracle's dense direct product (the paper's 'direct method') on a bounded
-    sample: ncols columns x output degrees [0, ndeg); rate extrapolated per full transform."""
+CPU_COLS = 16   # the oracle's timed column count (the c5 check columns), fixed for both CPU legs
+
+
+def _oracle_op_cached(cfg):
+    """The oracle's c5 operator from tools/make_c5_oracle.py's cache (bands -> the oracle's sparse
+    node-by-bin form), or None."""
+    path = os.path.join(ROOT, "oracle_cache", "c5_oracle.npz")
+    if cfg.name != I.CONFIGS["c5"].name or not os.path.exists(path):
+        return None
+    import scipy.sparse as sp
+
+    import oracle as O
+    z = np.load(path)
+    kind = O.Kind(cfg.kind, cfg.alpha, cfg.beta)
+    plan = O.make_plan(kind, cfg.N, cfg.eps)
+    S = []
+    for i, b in enumerate(plan.blocks):
+        st, ln, v = z[f"start{i}"].astype(np.int64), z[f"len{i}"].astype(np.int64), z[f"vals{i}"]
+        row = np.repeat(np.arange(cfg.N), ln)
+        off = np.concatenate([[0], np.cumsum(ln)])
+        col = st[row] + (np.arange(v.size) - off[row])
+        S.append(sp.csr_matrix((v, (row, col)), shape=(cfg.N, b.H)))
+    P = O.entries(kind, z["x"], 0, plan.tail).T.copy()
+    return O.Operator(plan, S, [O.kaiser(plan.zeta, b.L - 1) for b in plan.blocks], P), z["x"]
+
+
+def _dense_sample(cfg, threads):
+    """The oracle's dense direct product (the paper's 'direct method'; entries regenerated in
+    double-double) on CPU_COLS columns of the seeded batch and output rows [0, ndeg): (rate per full
+    transform, seconds, ndeg, rows, nodes, X)."""
     import oracle as O
     os.environ["OMP_NUM_THREADS"] = str(threads)
     kind = O.Kind(cfg.kind, cfg.alpha, cfg.beta, eta=cfg.eta)
-    if x is None:
-        x = _timing_nodes(cfg)
-    X = I.config_rhs(cfg, B=max(ncols, 1))[:, :ncols]
+    x = _timing_nodes(cfg)
+    X = I.config_rhs(cfg, B=CPU_COLS)
+    cplx = cfg.kind in (I.KIND_EXP, I.KIND_LAGSPEC)
+    rows_total = (cfg.M or cfg.N) if cplx else cfg.N
+    ndeg = rows_total if (cplx or cfg.kind == I.KIND_LAG2D or cfg.N <= 16384) else 8192
     t0 = time.perf_counter()
-    if cfg.kind in (I.KIND_EXP, I.KIND_LAGSPEC):   # complex: the oracle's dense product over all rows
+    if cplx:
         O.dense_apply(kind, x, X, M=cfg.M or None)
-        ndeg = cfg.N
-    elif cfg.kind == I.KIND_LAG2D:   # the series sum D C = the transposed Laguerre product, all rows
+    elif cfg.kind == I.KIND_LAG2D:   # the series sum D C = the transposed Laguerre product
         O.dense_apply_t(O.Kind(O.KIND_LAGUERRE), x, X)
-        ndeg = cfg.N
     else:
         O.dense_apply_rows(kind, x, X, ndeg)
-    dt = time.perf_counter() - t0
-    return ncols * (ndeg / cfg.N) / dt, dt
+    t = time.perf_counter() - t0
+    return CPU_COLS * (ndeg / rows_total) / t, t, ndeg, rows_total, x, X
+
+
+def cpu_oracle_timing(cfg, threads, direction="A"):
+    """The oracle as it stands, on CPU_COLS columns of the config's seeded batch, all host cores:
+    (1) the dense direct product on output rows [0, ndeg) (_dense_sample; rate per full transform),
+        with the double-double generation of the same entries timed alone beside it;
+    (2) the oracle's compressed apply (Alg. 2 / Alg. 1 block form, library FFT) on the same
+        columns, when its operator is at hand (built here for N <= 16384; c5 from the cache of
+        tools/make_c5_oracle.py).
+    Returns the cpu_baseline object; value = (1)."""
+    import oracle as O
+    kind = O.Kind(cfg.kind, cfg.alpha, cfg.beta, eta=cfg.eta)
+    v, t_dense, ndeg, rows_total, x, X = _dense_sample(cfg, threads)
+    cplx = cfg.kind in (I.KIND_EXP, I.KIND_LAGSPEC)
+    t_gen = None
+    if not cplx:   # the entry generation alone: the same rows x all nodes, node chunks of 4096
+        gk = O.Kind(O.KIND_LAGUERRE) if cfg.kind == I.KIND_LAG2D else kind
+        t0 = time.perf_counter()
+        for k0 in range(0, cfg.N, 4096):
+            O.entries(gk, x[k0:k0 + 4096], 0, ndeg)
+        t_gen = time.perf_counter() - t0
+    out = {"value": v, "unit": "transforms/s", "cores": threads, "kind": "oracle",
+           "sample": f"dense direct product (double-double entries regenerated), {CPU_COLS} columns x "
+                     f"output rows [0,{ndeg}) of {rows_total}: {t_dense:.2f} s; rate per full transform",
+           "dense_s": t_dense, "entry_generation_s": t_gen, "columns": CPU_COLS, "rows": ndeg}
+    comp = None
+    try:
+        op, t_build = None, None
+        if cfg.kind != I.KIND_LAG2D and not cplx and cfg.N <= 16384:
+            t0 = time.perf_counter()
+            op = O.compress(O.make_plan(kind, cfg.N, cfg.eps, eps2=cfg.eps2), x)
+            t_build = time.perf_counter() - t0
+        elif cfg.kind != I.KIND_LAG2D and not cplx:
+            got = _oracle_op_cached(cfg)
+            if got is not None:
+                op, _ = got
+        if op is not None:
+            n, t0 = 0, time.perf_counter()
+            while True:
+                if direction == "WAT":
+                    O.apply_input_axis(op, X, np.ones(cfg.N))
+                else:
+                    O.apply_output_axis(op, X)
+                n += 1
+                if time.perf_counter() - t0 >= 2.0:
+                    break
+            t_ap = (time.perf_counter() - t0) / n
+            comp = {"value": CPU_COLS / t_ap, "unit": "transforms/s", "seconds_per_apply": t_ap, "repeats": n,
+                    "precompute_s": t_build,
+                    "sample": f"oracle compressed apply ({'input' if direction == 'WAT' else 'output'} axis, "
+                              f"library FFT) on the same {CPU_COLS} columns"}
+    except Exception as e:  # pragma: no cover - reported, not fatal
+        comp = {"error": repr(e)[:200]}
+    out["compressed"] = comp
+    return out
 
 
 def run_reference(args, cfg, ws, rank):
-    """--impl reference: the CPU oracle timed on the host cores (rank 0 only)."""
+    """--impl reference: the CPU oracle timed on the host cores (rank 0 only): per step the dense
+    direct product on the fixed column sample, median over the timed steps; the first step also
+    times the entry generation and the oracle's compressed apply (cpu_oracle_timing)."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    ncols, ndeg = 4, min(cfg.N, 4096)
-    x = _timing_nodes(cfg)
-    rates = []
-    for i in range(args.warmup + args.steps):
-        r, dt = cpu_oracle_rate(cfg, ncols, ndeg, threads, x)
-        if i >= args.warmup:
-            rates.append(r)
-    v = float(np.median(rates))
-    sample = f"{ncols} columns x degrees [0,{ndeg}) of {cfg.N} per step (dense direct product, dd entries)"
+    direction = args.direction or cfg.dirs[0]
+    first = cpu_oracle_timing(cfg, threads, direction)
+    vals = [first["value"]]
+    for _ in range(args.warmup + args.steps - 1):
+        vals.append(_dense_sample(cfg, threads)[0])
+    v = float(np.median(vals[args.warmup:] if len(vals) > args.warmup else vals))
+    base = dict(first)
+    base["value"] = v
     line = {"impl": "reference", "metric": "fp64 transforms/s", "value": v, "unit": "transforms/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "N": cfg.N, "global_batch": cfg.B, "eps": cfg.eps},
-            "cpu_baseline": {"value": v, "unit": "transforms/s", "cores": threads, "kind": "oracle",
-                             "sample": sample},
+            "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "N": cfg.N, "global_batch": cfg.B, "eps": cfg.eps,
+                       "direction": direction},
+            "cpu_baseline": base,
             "e2e": {"value": v, "unit": "transforms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -177,15 +256,28 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c5", choices=sorted(I.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--strong", action="store_true", help="divide the config's B over the ranks")
-    ap.add_argument("--batch", type=int, default=0, help="override RHS per rank")
+    ap.add_argument("--weak", action="store_true", help="every rank applies the whole batch (default: strong "
+                    "scaling, the config's global batch sharded by column)")
+    ap.add_argument("--batch", type=int, default=0, help="override the global batch (strong) / per-rank batch (weak)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--direction", default="", help="A or WAT (default: the config's first)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = I.CONFIGS[args.config]
-    ws, rank, local = _dist()
+    from paper_2004_11610_b200.shard import rank_columns, relaunch_cmd, world_from
+    ws, rank, local, relaunch = world_from(os.environ, args.gpus)
+    if relaunch:   # `bench.py --gpus N` without a launcher: one rank per GPU under torch.distributed.run
+        import socket
+        so = socket.socket()
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+        so.close()
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")            # communicator lines (ranks, transport) on stderr
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        sys.exit(subprocess.call(relaunch_cmd(os.path.abspath(__file__), sys.argv[1:], args.gpus, port,
+                                              sys.executable), env=env))
 
     if args.impl == "reference":
         run_reference(args, cfg, ws, rank)
@@ -200,7 +292,9 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     direction = xc.XC_DIR_WAT if (args.direction or cfg.dirs[0]) == "WAT" else xc.XC_DIR_A
-    B = args.batch or (cfg.B // ws if args.strong else cfg.B)
+    B_global = args.batch or cfg.B
+    cols = rank_columns(B_global, rank, ws, strong=not args.weak)
+    B = cols.stop - cols.start
     # ---- precompute (not timed in the metric) ----
     t0 = time.perf_counter()
     x, wt = _nodes(cfg, local)
@@ -216,19 +310,13 @@ def main():
     info = T.info()
 
     # ---- inputs: seeded on the host, this rank's shard, resident in HBM ----
-    from paper_2004_11610_b200.shard import column_shard, max_over_ranks
+    from paper_2004_11610_b200.shard import max_over_ranks
+    Xfull = I.config_rhs(cfg, B=B_global)   # the config's seeded batch; this rank's column shard
     if cfg.kind in (I.KIND_EXP, I.KIND_LAGSPEC):   # complex RHS, planar layout of the C ABI (2N rows)
-        Xc = I.config_rhs(cfg, B=B)
-        Xh = np.ascontiguousarray(np.concatenate([Xc.real, Xc.imag]))
-    elif ws == 1:
-        Xh = I.config_rhs(cfg, B=B)
-    elif args.strong:
-        Xh = np.ascontiguousarray(I.config_rhs(cfg)[:, column_shard(cfg.B, rank, ws)])
-        B = Xh.shape[1]
+        Xh = np.ascontiguousarray(np.concatenate([Xfull.real[:, cols], Xfull.imag[:, cols]]))
     else:
-        # weak scaling: rank g applies its own B columns (same generator, rank-offset seed)
-        rng = np.random.default_rng(cfg.seed * 1000 + rank)
-        Xh = rng.standard_normal((cfg.N, B))
+        Xh = np.ascontiguousarray(Xfull[:, cols])
+    del Xfull
     X = torch.from_numpy(Xh).cuda()
     Y = torch.empty((T.rows(direction)[1], B), dtype=torch.float64, device=X.device)
     T.reserve(B)
@@ -288,9 +376,9 @@ def main():
     spmm_flops = (cmul * nnz + 2.0 * tail * N) * B          # algorithmic, per launch
     spmm_ms = prof["ms_spmm"] / max(1, prof["n"])
     fft_ms = prof["ms_fft"] / max(1, prof["n"])
-    achieved = spmm_flops / (spmm_ms / 1e3) / 1e12
     if cfg.kind == I.KIND_LAG2D:   # no dense tail inside the product launch (separate kernels)
         spmm_flops = 8.0 * nnz * B
+    achieved = spmm_flops / (spmm_ms / 1e3) / 1e12
     alg_bytes = 16.0 * N * B + 20.0 * nnz + 8.0 * tail * N   # X in, Y out, operator once (SURVEY d.3)
     peaks = _peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
@@ -330,20 +418,16 @@ def main():
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        ncols, ndeg = 16, min(cfg.N, 8192)
-        r, dt = cpu_oracle_rate(cfg, ncols, ndeg, threads)
-        cpu = {"value": r, "unit": "transforms/s", "cores": threads, "kind": "oracle",
-               "sample": f"{ncols} columns x output degrees [0,{ndeg}) of N={cfg.N}: dense direct product "
-                         f"with double-double entries ({dt:.1f} s), rate per full transform"}
+        cpu = cpu_oracle_timing(cfg, os.cpu_count() or 1, "WAT" if direction == xc.XC_DIR_WAT else "A")
 
     if rank == 0:
         line = {
             "metric": "fp64 transforms/s", "value": value, "unit": "transforms/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded N(0,1) RHS, Gauss nodes computed on the GPU)",
             "config": {"workload": cfg.name, "N": cfg.N, "B_per_gpu": B, "global_batch": total_cols,
+                       "columns_of_rank0": [cols.start, cols.stop],
                        "eps": cfg.eps, "direction": "A" if direction == xc.XC_DIR_A else "WAT",
                        "parallelism": f"rhs-shard x{ws}, operator replicated",
                        "l2": "inputs larger than L2 (X = %.2f GB, partial sums %.2f GB)" % (
@@ -362,12 +446,19 @@ def main():
                           "peak_source": "measured DMMA microbenchmark (tools/fp64_peak.cu)"}) | {
                          "traffic": traffic, "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
                          "spmm_ms": spmm_ms, "fft_ms": fft_ms, "spmm_share": spmm_ms / ms,
+                         # the whole step against the fp64 roof: SURVEY 8d.3 flops (SpMM + tail + FFTs)
+                         # per column x B / the measured DMMA peak / ms_per_step
+                         "step_frac": info["flops_per_col_A" if direction == xc.XC_DIR_A else "flops_per_col_WAT"]
+                                      * B / (DMMA_PEAK_TFLOPS * 1e12) / (ms / 1e3),
                          "dmma_issue_efficiency": (cmul * nnz + 2.0 * tail * N) / max(1.0, info["dmma_flops_per_col_A"])},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "graph": graph,
             "gpu_launches": info["launches_A" if direction == xc.XC_DIR_A else "launches_WAT"] * args.steps,
             "clocks": clk,
+            "comm": ({"backend": "nccl", "world_size": ws, "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
+                      "data_path_collectives": 0, "precompute": "2 all-gathers of node bands (xc_build_local/step)"}
+                     if ws > 1 else None),
             "precompute_s": {"gauss_nodes": t_nodes, "build": t_build,
                              "mode": f"node range split over {ws} ranks + NCCL all-gather" if ws > 1 else "one GPU"},
             "nnz": nnz,

@@ -26,6 +26,7 @@ library routine say so ("parity unpinned") in their docstring; see DESIGN.md.
 from __future__ import annotations
 
 import ctypes
+import functools
 import math
 import os
 import subprocess
@@ -261,8 +262,15 @@ def bessel_i1(x: float) -> float:
 def kaiser(zeta: float, npts: int) -> np.ndarray:
     """w_n^{zeta,npts} = I0(zeta sqrt(1-(2n/npts-1)^2)) / I0(zeta), n = 0..npts.
 
-    A window over L positions uses npts = L - 1 (L samples; reading R-6).
+    A window over L positions uses npts = L - 1 (L samples; reading R-6).  The values of one
+    (zeta, npts) are computed once and memoised (the per-point series is slow in Python; a node
+    chunk of c5's first block would otherwise spend 4 s recomputing its 86400-point window).
     """
+    return _kaiser_memo(float(zeta), int(npts)).copy()
+
+
+@functools.lru_cache(maxsize=64)
+def _kaiser_memo(zeta: float, npts: int) -> np.ndarray:
     n = np.arange(npts + 1, dtype=np.float64)
     r = (2.0 * n - npts) / npts
     arg = zeta * np.sqrt(np.maximum(0.0, 1.0 - r * r))
@@ -376,6 +384,8 @@ def make_plan(kind: Kind, N: int, eps: float, eps1: float | None = None, eps2: f
         s0 = minimal_s(zeta, e, eps2, two_sided=False)
         L = smooth5_even_at_least(e + s0)
         s = L - e
+        if s >= e:   # the next block's span [s_{i+1}, s_i) must shrink (R-8)
+            raise ArithmeticError("block chain does not shrink (eps2 too close to 1)")
         plan.blocks.append(Block(L, 0, s, e))
         e = s
     plan.tail = e

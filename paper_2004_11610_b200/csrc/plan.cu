@@ -117,6 +117,16 @@ xc_status make_chain(int kind, int64_t N, double eps1, double eps2, int cutoff, 
     }
     int L = smooth5_even_ge(e + s0);
     int s = L - e;
+    // the chain must shrink (the next block holds the first s_i degrees of this one);
+    // s >= e happens only for eps2 close to 1 -- reject instead of looping
+    if (s >= e) {
+      xc_set_error("block chain does not shrink (s >= span): eps2 too close to 1");
+      return XC_ENUMERIC;
+    }
+    if ((int)out.blocks.size() + 1 >= XC_MAX_BLOCKS) {
+      xc_set_error("block chain longer than " + std::to_string(XC_MAX_BLOCKS - 1) + " blocks");
+      return XC_ENUMERIC;
+    }
     out.blocks.push_back(PlanBlock{L, 0, s, e});
     e = s;
   }

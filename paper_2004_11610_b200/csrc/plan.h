@@ -6,6 +6,9 @@
 
 #include "../../include/xc.h"
 
+// longest block chain (+ the dense tail) the apply's per-source tables hold (XC_MAX_SRC)
+constexpr int XC_MAX_BLOCKS = 40;
+
 struct PlanBlock {
   int L, m_off, keep_lo, keep_hi;
 };

@@ -28,6 +28,8 @@
 #include "plan.h"
 #include "xc_internal.cuh"
 
+static_assert(XC_MAX_BLOCKS == XC_MAX_SRC, "block chain bound = apply source table size");
+
 static thread_local std::string g_err;
 void xc_set_error(const std::string& msg) { g_err = msg; }
 
@@ -150,6 +152,7 @@ struct xc_op {
   cudaStream_t hst = nullptr;  // apply stream of the last host-buffer call (valid if hst_set)
   bool hst_set = false;
   int64_t hchunk = 0;          // chunks enqueued since the slots were (re)allocated
+  int64_t hBc = 0, hN = 0;     // chunk shape (columns, rows) the slots are laid out for
   std::vector<int64_t> zoff;  // per block offset (doubles) of its z' planes in zpl
   xc_info_t info{};
   // build state (kept between the phases of a distributed precompute)
@@ -940,6 +943,12 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
   }
   if ((h->dirs & XC_DIR_WAT) && !p.weights) {
     xc_set_error("XC_DIR_WAT needs weights");
+    return XC_EINVAL;
+  }
+  // the input axis's tail items stage the t dense degrees as B rows of one shared-memory window
+  // (<= XC_WMAX rows), so the cutoff is bounded
+  if (p.dense_cutoff < 0 || p.dense_cutoff > XC_WMAX - 4) {
+    xc_set_error("dense_cutoff: 0 (default 32) or in [1, " + std::to_string(XC_WMAX - 4) + "]");
     return XC_EINVAL;
   }
   XC_TRY(validate_nodes(kind, nodes, N));
@@ -2049,11 +2058,16 @@ xc_status host_enqueue(xc_op* h, xc_dir dir, const double* Xh, double* Yh, int64
   const int64_t nchunk = (B + Bc - 1) / Bc;
   const size_t slot = (size_t)N * Bc * sizeof(double);
   const int NS = xc_op::kSlots;
-  if (h->Xh.bytes < NS * slot || Bc > h->ws_B) {  // (re)allocation: drain the pipeline first
+  // slot i sits at i * N * Bc: a call with another chunk shape (B or direction) would move the
+  // slots under chunks still in flight, so a shape change drains the pipeline first (as does a
+  // reallocation)
+  if (h->Xh.bytes < NS * slot || Bc > h->ws_B || Bc != h->hBc || N != h->hN) {
     XC_CUDA(cudaStreamSynchronize(h->s_in));
     XC_CUDA(cudaStreamSynchronize(h->s_out));
     if (h->hst_set) XC_CUDA(cudaStreamSynchronize(h->hst));
     h->hchunk = 0;
+    h->hBc = Bc;
+    h->hN = N;
     if (h->Xh.bytes < NS * slot) {
       XC_TRY(dev_alloc(h->Xh, NS * slot));
       XC_TRY(dev_alloc(h->Yh, NS * slot));

@@ -271,6 +271,11 @@ class Transform:
             raise XcError(f"X has {N} rows, transform needs {rin}")
         if out is None:
             out = torch.empty((rout, B), dtype=torch.float64, device=X.device)
+        elif not (isinstance(out, torch.Tensor) and out.is_cuda and out.dtype == torch.float64 and out.dim() == 2
+                  and tuple(out.shape) == (rout, B) and out.device == X.device and out.stride(1) == 1
+                  and out.stride(0) >= B):
+            raise XcError(f"out must be a CUDA float64 tensor of shape ({rout}, {B}) on {X.device} with "
+                          f"unit column stride")
         st = stream if stream is not None else torch.cuda.current_stream(X.device).cuda_stream
         _check(self._lib.xc_apply(self._h, direction, ctypes.c_void_p(X.data_ptr()), X.stride(0),
                                   ctypes.c_void_p(out.data_ptr()), out.stride(0), B, ctypes.c_void_p(st)))

@@ -45,3 +45,33 @@ def test_plan_rejects_bad_eps():
         xc.plan_chain(xc.XC_JACOBI, 512, 0.5, 0.1)
     with pytest.raises(xc.XcError, match="XC_EINVAL"):
         xc.plan_chain(xc.XC_JACOBI, 1, 1e-12)
+
+
+def test_plan_rejects_non_shrinking_chain():
+    """eps2 close to 1: the block chain would not shrink (s >= span; P:281 needs s_{i+1} < s_i):
+    XC_ENUMERIC from the product's planner and ArithmeticError from the oracle's, no endless loop."""
+    from paper_2004_11610_b200 import xc
+    with pytest.raises(xc.XcError, match="XC_ENUMERIC"):
+        xc.plan_chain(xc.XC_JACOBI, 65536, 1e-12, 0.9)
+    with pytest.raises(ArithmeticError):
+        O.make_plan(O.Kind(O.KIND_JACOBI), 65536, 1e-12, eps2=0.9)
+
+
+def test_bench_multi_gpu_launch_plan():
+    """bench.py --gpus N without a launcher re-launches itself as N ranks (torch.distributed.run on
+    127.0.0.1); under the launcher the ranks split the config's global batch (strong scaling)."""
+    from paper_2004_11610_b200.shard import rank_columns, relaunch_cmd, world_from
+    assert world_from({}, 1) == (1, 0, 0, False)
+    assert world_from({}, 2) == (1, 0, 0, True)
+    assert world_from({"WORLD_SIZE": "2", "RANK": "1", "LOCAL_RANK": "1"}, 2) == (2, 1, 1, False)
+    assert world_from({"WORLD_SIZE": "4", "RANK": "3", "LOCAL_RANK": "3"}, 1) == (4, 3, 3, False)
+    with pytest.raises(ValueError):
+        world_from({"WORLD_SIZE": "2"}, 8)
+    cmd = relaunch_cmd("bench.py", ["--gpus", "2", "--steps", "3"], 2, 29500)
+    assert "--nproc-per-node=2" in cmd and "127.0.0.1" in cmd and cmd[-4:] == ["--gpus", "2", "--steps", "3"]
+    B = I.CONFIGS["c5"].B
+    for G in (1, 2, 4, 8):
+        sh = [rank_columns(B, g, G) for g in range(G)]
+        assert sum(s.stop - s.start for s in sh) == B == 4096 and sh[0].start == 0 and sh[-1].stop == B
+        assert all(sh[g].stop == sh[g + 1].start for g in range(G - 1))
+        assert rank_columns(B, G - 1, G, strong=False) == slice(0, B)

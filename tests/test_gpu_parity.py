@@ -471,6 +471,29 @@ def test_host_async_stream_matches():
     T.close()
 
 
+def test_host_async_shape_change():
+    """Streaming host-buffer calls whose chunk shape changes (B = 4096 then B = 200, and a call of
+    the other direction) while earlier chunks are still in flight: every result equals the device
+    apply (a shape change drains the pipeline before the slots move)."""
+    xc = _xc()
+    kt = (O.KIND_LAGUERRE, 0.0, 0.0)
+    N = 512
+    x, wt = _nodes(kt, N, 3)
+    T = xc.Transform(kt[0], x, 1e-12, dirs=xc.XC_DIR_A | xc.XC_DIR_WAT, weights=wt)
+    st = torch.cuda.current_stream().cuda_stream
+    calls = [(4096, xc.XC_DIR_A, 50), (200, xc.XC_DIR_A, 51), (4096, xc.XC_DIR_WAT, 52), (64, xc.XC_DIR_A, 53)]
+    bufs = []
+    for B, d, seed in calls:
+        Xp = torch.from_numpy(I.rhs(N, B, seed)).pin_memory()
+        Yp = torch.full((N, B), float("nan"), dtype=torch.float64).pin_memory()
+        T.apply_host_async_ptr(Xp.data_ptr(), Yp.data_ptr(), B, d, stream=st)
+        bufs.append((Xp, Yp, d))
+    T.host_wait()
+    for Xp, Yp, d in bufs:
+        assert torch.equal(Yp, T.apply(Xp.cuda(), d).cpu())
+    T.close()
+
+
 EXP_CASES = [("c6", 4096, 64, 1e-10, 6), ("exp_ragged", 1000, 37, 1e-10, 9), ("exp_small", 96, 3, 1e-12, 2)]
 
 
