@@ -170,11 +170,22 @@ xc_status xc_build_step(xc_handle h, xc_exchange_t* ex);
 
 /* Computation stage (Alg. 2 step 2 / Alg. 1 step 2 per block):
  * X, Y: DEVICE pointers, row-major N x B with leading dimensions ldx, ldy >= B.
- * Enqueues on `stream` only (no host synchronisation).  Allocates device
- * workspace only if B exceeds the largest B reserved so far (xc_reserve).
- * Not reentrant across streams on one handle (one workspace per handle). */
+ * Enqueues on `stream` only: no host synchronisation and no allocation.  The workspace is the
+ * one attached to `stream` (xc_attach_workspace) or else the handle's own, reserved beforehand
+ * with xc_reserve(h, >= B) -- XC_ESTATE if B exceeds it, XC_ENOMEM if an attached workspace is
+ * shorter than xc_workspace_query(h, B).  Reentrant across streams that have distinct workspaces
+ * (one attached per stream; concurrent calls from several host threads are allowed then); calls
+ * sharing one workspace must be ordered on one stream.  The handle's operator is read-only here. */
 xc_status xc_apply(xc_handle h, xc_dir dir, const double* X, int64_t ldx, double* Y, int64_t ldy,
                    int64_t B, void* stream);
+
+/* Bind a caller-owned DEVICE workspace [dptr, dptr + bytes) (256-byte aligned) to `stream`:
+ * xc_apply on that stream uses it instead of the handle's own (size it with xc_workspace_query;
+ * the caller keeps ownership and must not free it before detaching).  dptr = NULL detaches the
+ * stream's workspace; attaching to a stream that has one replaces it.  Both wait for the work
+ * queued on `stream`.  Creates the workspace's forked block streams (no device allocation).
+ * Errors: XC_EINVAL (null handle, misaligned or tiny range). */
+xc_status xc_attach_workspace(xc_handle h, void* stream, void* dptr, size_t bytes);
 
 /* CUDA graphs of xc_apply (default on): the second call with the same (X, Y, ldx, ldy, B,
  * dir, stream) captures the apply's launches into a graph, later calls replay it with one
@@ -206,10 +217,15 @@ xc_status xc_apply_host_async(xc_handle h, xc_dir dir, const double* X_host, dou
                               void* stream);
 xc_status xc_host_wait(xc_handle h);
 
-/* Reserve workspace for up to B right-hand sides (may allocate). */
+/* Reserve the handle's own workspace for up to B right-hand sides (allocates if B exceeds the
+ * reserve so far; the host-buffer calls reserve their chunk width themselves). */
 xc_status xc_reserve(xc_handle h, int64_t B);
 
-/* Bytes of workspace xc_apply needs for B right-hand sides. */
+/* Kernel launches one xc_apply(dir) of B columns makes (xc_info's launches_* are for B = 1;
+ * the two-pass inverse DFTs run in column chunks, so the count grows with B). */
+xc_status xc_launches(xc_handle h, xc_dir dir, int64_t B, int64_t* n);
+
+/* Bytes of workspace xc_apply needs for B right-hand sides (what xc_attach_workspace must get). */
 xc_status xc_workspace_query(xc_handle h, int64_t B, size_t* bytes);
 
 xc_status xc_info(xc_handle h, xc_info_t* out);

@@ -731,7 +731,38 @@ xc_status launch(C2RArgs& a, const FftIO& io, cudaStream_t st) {
 
 int c2r_launches(const FftPlan& p) { return p.L2 > 1 ? 2 : 1; }
 
+// Column chunk of a two-pass length: the four-step scratch of one chunk (M x chunk complex) is held
+// near XC_C2R_CHUNK_MB (default 40) MB so that pass 1 reads it from L2 (126 MB) right after pass 0
+// wrote it, instead of a round trip through HBM (c5 block 1: 5.6 GB per apply at B = 4096).
+// XC_C2R_CHUNK_MB=0: one chunk (the whole batch) -- the measurement switch.
+int64_t c2r_chunk_cols(const FftPlan& p, int64_t B) {
+  if (p.L2 <= 1 || B <= 64) return B;
+  static const int64_t mb = getenv("XC_C2R_CHUNK_MB") ? atoll(getenv("XC_C2R_CHUNK_MB")) : 40;
+  if (mb <= 0) return B;
+  int64_t c = (mb << 20) / (16 * (int64_t)p.L) / 64 * 64;
+  return std::min<int64_t>(B, std::max<int64_t>(64, c));
+}
+
+xc_status c2r_prepare(const FftPlan& p) {
+  const C2RTables* tb = nullptr;
+  return tables_for(p, &tb);
+}
+
+static xc_status c2r_run_cols(const FftPlan& p, const FftIO& io, int ncol, double2* scratch, cudaStream_t st);
+
 xc_status c2r_run(const FftPlan& p, const FftIO& io, int ncol, double2* scratch, cudaStream_t st) {
+  const int64_t cw = c2r_chunk_cols(p, ncol);
+  if (cw >= ncol) return c2r_run_cols(p, io, ncol, scratch, st);
+  for (int64_t c0 = 0; c0 < ncol; c0 += cw) {  // columns are independent: chunk by chunk
+    FftIO ic = io;
+    ic.Uc = io.Uc + c0;
+    ic.Y = io.Y + c0;
+    XC_TRY(c2r_run_cols(p, ic, (int)std::min<int64_t>(cw, ncol - c0), scratch, st));
+  }
+  return XC_OK;
+}
+
+static xc_status c2r_run_cols(const FftPlan& p, const FftIO& io, int ncol, double2* scratch, cudaStream_t st) {
   C2RArgs a{};
   // 32-bit element offsets inside the kernels
   if ((int64_t)p.L * ncol >= (1LL << 31) || (int64_t)(io.keep_hi + io.m_off + 1) * io.ldy >= (1LL << 31) ||

@@ -88,6 +88,38 @@ xc_status upload(DevBuf& b, const std::vector<T>& v) {
 
 }  // namespace
 
+// One workspace of xc_apply: the per-call scratch arrays for up to B columns, carved from one
+// device range (ws_layout), plus the forked block streams and the captured graphs that use them.
+constexpr int kAux = 4;  // forked streams: block 2 alone, blocks 3.. round robin over 3
+struct GraphEntry {      // CUDA graph of one xc_apply argument set (captured at its 2nd call)
+  const void* X;
+  void* Y;
+  int64_t ldx, ldy, B;
+  int dir;
+  cudaStream_t st;
+  int seen;
+  cudaGraphExec_t exec;
+};
+struct Ws {
+  int64_t B = 0;              // columns the layout is carved for (0: none yet)
+  DevBuf own;                 // the handle's own workspace; empty for an attached one
+  char* base = nullptr;       // device range (own.p or the caller's)
+  size_t bytes = 0;
+  cudaStream_t bound = nullptr;  // attached: the stream it serves
+  double* partA = nullptr;    // output axis: SpMM rows (u of every block, split-K partials, tail)
+  double* partW = nullptr;    // input axis: SpMM partial rows
+  double* zpl = nullptr;      // input axis / 2D: prologue spectra (z' planes)
+  double* tailpart = nullptr; // 2D: split-j partial sums of the tails
+  double2* bsr_part = nullptr;  // 2D: partial rows of the split DMMA groups
+  double2* scratch = nullptr;   // FFT scratch of the caller's stream
+  double2* scratch_aux[kAux] = {};  // ... and of each forked stream
+  std::vector<int64_t> zoff;  // per block offset (doubles) of its z' planes in zpl
+  cudaStream_t s_aux[kAux] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[kAux] = {};
+  int naux = 2;               // forked streams of the current apply (naux_for)
+  std::vector<GraphEntry> graphs;
+};
+
 struct xc_op {
   int kind = 0;   // machinery kind (XC_LAGSPEC runs as XC_EXP, R-21)
   int ukind = 0;  // the kind the caller built
@@ -95,9 +127,8 @@ struct xc_op {
   DevBuf tailR, tailC;  // XC_LAG2D: direct-method tails (rows i < t: N x t; columns j < t: t x (N-t))
   DevBuf ptr2d, ent2d, order2d;  // XC_LAG2D: CSR of the Hermitian halves of sum_a D2_ab, time blocks
   int rows2d = 0;                 // stacked; order2d: rows longest first
-  DevBuf tailpart;                // XC_LAG2D: split-j partial sums of the tails
   DevBuf bsr_sptr, bsr_r4, bsr_tiles, bsr_srow, bsr_snv, bsr_sslot, bsr_order;  // XC_LAG2D: 8 x 4
-  DevBuf bsr_rrow, bsr_rnv, bsr_rslot, bsr_rcnt, bsr_part;                       // DMMA blocks
+  DevBuf bsr_rrow, bsr_rnv, bsr_rslot, bsr_rcnt;                       // DMMA blocks
   int bsr_nseg = 0, bsr_nred = 0, bsr_nslots = 0;
   int64_t zrows2d = 0;  // rows of the stacked prologue spectra
   double alpha = 0, beta = 0;
@@ -120,31 +151,15 @@ struct xc_op {
   int64_t rowsW = 0, tilesW_n = 0, mtstepsW = 0;
   DevBuf nodeg_base, nodeg_nch;
   DevBuf nodeg_base_im;  // XC_EXP: partial rows of the imaginary parts per node group
-  // workspace
-  int64_t ws_B = 0;
-  DevBuf partA, partW, scratch, zpl, Xh, Yh;
-  // CUDA graphs of xc_apply, keyed on its arguments: a key seen twice is captured once and
-  // replayed from then on (one launch instead of ~20; matters for the small configs)
-  struct GraphEntry {
-    const void* X;
-    void* Y;
-    int64_t ldx, ldy, B;
-    int dir;
-    cudaStream_t st;
-    int seen;
-    cudaGraphExec_t exec;
-  };
-  std::vector<GraphEntry> graphs;
+  // workspaces: the handle's own (xc_reserve; also the host-buffer pipeline's) and the ones the
+  // caller attaches to streams (xc_attach_workspace); xc_apply uses the one bound to its stream
+  Ws def;
+  std::vector<Ws*> att;
+  std::mutex att_mu;
+  DevBuf Xh, Yh;  // host-buffer pipeline slots
   bool use_graphs = true;
   // xc_apply_host pipeline: copy-in / copy-out streams and per-slot events
   cudaStream_t s_in = nullptr, s_out = nullptr;
-  // XC_DIR_A of the block kinds: after the SpMM the blocks are independent; block 2 and the
-  // smaller blocks run on two forked streams beside block 1 (own C2R scratch each)
-  static constexpr int kAux = 4;  // forked streams: block 2 alone, blocks 3.. round robin over 3
-  cudaStream_t s_aux[kAux] = {};
-  cudaEvent_t ev_fork = nullptr, ev_join[kAux] = {};
-  DevBuf scratch_aux[kAux];
-  int naux = 2;  // forked streams of the current apply (naux_for)
   bool use_fork = true;
   static constexpr int kSlots = 3;  // device slots of the host-buffer pipeline
   cudaEvent_t ev_in[kSlots] = {}, ev_cmp[kSlots] = {}, ev_out[kSlots] = {};
@@ -153,7 +168,6 @@ struct xc_op {
   bool hst_set = false;
   int64_t hchunk = 0;          // chunks enqueued since the slots were (re)allocated
   int64_t hBc = 0, hN = 0;     // chunk shape (columns, rows) the slots are laid out for
-  std::vector<int64_t> zoff;  // per block offset (doubles) of its z' planes in zpl
   xc_info_t info{};
   // build state (kept between the phases of a distributed precompute)
   DevBuf djtab;
@@ -180,63 +194,157 @@ int64_t pad_cols(int64_t B) {
   return (B + t - 1) / t * t;
 }
 
-void clear_graphs(xc_op* h) {
-  for (auto& g : h->graphs)
+void clear_graphs(Ws& w) {
+  for (auto& g : w.graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
-  h->graphs.clear();
+  w.graphs.clear();
 }
 
 // Forked stream of block ib >= 1 (fork_stream): block 2 on its own, blocks 3.. round robin over
 // naux - 1 streams.  Large batches use naux = 2 (blocks 3.. in one stream: more concurrent
 // streams slowed c5's FFT phase 3.94 -> 4.09 ms), small ones all four (c3 0.255 -> 0.225 ms).
 inline int aux_of(int ib, int naux) { return ib == 1 ? 0 : 1 + (ib - 2) % (naux - 1); }
-inline int naux_for(int64_t N, int64_t B) { return N * B <= (32LL << 20) ? xc_op::kAux : 2; }
+inline int naux_for(int64_t N, int64_t B) { return N * B <= (32LL << 20) ? kAux : 2; }
 
-xc_status ensure_ws(xc_op* h, int64_t B) {
-  if (B <= h->ws_B) return XC_OK;
-  int64_t Bp = pad_cols(B);
-  size_t scratch_n = 0;
+// Columns of one C2R column chunk of a two-pass block (c2r_run): the four-step scratch of a chunk
+// (M x chunk complex) is kept near 40 MB so that it stays in L2 between the two passes.
+int64_t c2r_cols(const BlockData& b, int64_t B) { return c2r_chunk_cols(b.fftM, B); }
+
+// FFT scratch (double2 elements) one block needs on its stream for B columns
+size_t block_scratch(const xc_op* h, const BlockData& b, int64_t B) {
   const bool two_d = h->ukind == XC_LAG2D;  // prologue planes (as XC_DIR_WAT) + C2R (as XC_DIR_A)
-  for (auto& b : h->blocks) {
-    if ((two_d || (h->dirs & XC_DIR_WAT)) && b.fft.L2 > 1) scratch_n = std::max(scratch_n, (size_t)b.L * (size_t)B);
-    if ((h->dirs & XC_DIR_A) && b.fftM.L2 > 1) scratch_n = std::max(scratch_n, (size_t)b.fftM.L * (size_t)B);
-    if ((h->dirs & XC_DIR_A) && h->kind == XC_EXP && b.fft.L2 > 1)  // C2C inverse of length L
-      scratch_n = std::max(scratch_n, (size_t)b.L * (size_t)B);
-  }
-  XC_TRY(dev_alloc(h->scratch, std::max<size_t>(1, scratch_n) * sizeof(double2)));
-  if (h->kind != XC_EXP && h->blocks.size() > 1) {
-    size_t an[xc_op::kAux] = {};  // each forked stream's FFT scratch: the max over its blocks
+  size_t n = 0;
+  if ((two_d || (h->dirs & XC_DIR_WAT)) && b.fft.L2 > 1) n = std::max(n, (size_t)b.L * (size_t)B);
+  if (((h->dirs & XC_DIR_A) || two_d) && h->kind != XC_EXP && b.fftM.L2 > 1)
+    n = std::max(n, (size_t)b.fftM.L * (size_t)c2r_cols(b, B));
+  if ((h->dirs & XC_DIR_A) && h->kind == XC_EXP && b.fft.L2 > 1)  // C2C inverse of length L
+    n = std::max(n, (size_t)b.L * (size_t)B);
+  return n;
+}
+
+// The workspace of B columns: part sizes in carve order (256-byte aligned), total returned.  With
+// w and base it also sets w's pointers into [base, base + total).  xc_workspace_query is this total.
+size_t ws_layout(const xc_op* h, int64_t B, Ws* w, char* base) {
+  const int64_t Bp = pad_cols(B);
+  const bool two_d = h->ukind == XC_LAG2D;
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> char* {
+    char* p = base ? base + off : nullptr;
+    off += (std::max<size_t>(bytes, 16) + 255) / 256 * 256;
+    return p;
+  };
+  size_t scr = 1;
+  for (size_t i = 0; i < h->blocks.size(); ++i)
+    if (i == 0 || h->kind == XC_EXP) scr = std::max(scr, block_scratch(h, h->blocks[i], B));
+  size_t an[kAux] = {};
+  if (h->kind != XC_EXP)
     for (size_t i = 1; i < h->blocks.size(); ++i) {
-      const BlockData& b = h->blocks[i];
-      size_t n = 1;
-      if (((h->dirs & XC_DIR_A) || two_d) && b.fftM.L2 > 1) n = std::max(n, (size_t)b.fftM.L * (size_t)B);
-      if (((h->dirs & XC_DIR_WAT) || two_d) && b.fft.L2 > 1) n = std::max(n, (size_t)b.L * (size_t)B);
-      for (int na : {2, (int)xc_op::kAux})  // scratch for either stream assignment (naux_for)
+      const size_t n = block_scratch(h, h->blocks[i], B);
+      scr = std::max(scr, n);  // without forked streams every block runs on the caller's
+      for (int na : {2, (int)kAux})  // scratch for either stream assignment (naux_for)
         an[aux_of((int)i, na)] = std::max(an[aux_of((int)i, na)], n);
     }
-    for (int i = 0; i < xc_op::kAux; ++i)
-      XC_TRY(dev_alloc(h->scratch_aux[i], std::max<size_t>(1, an[i]) * sizeof(double2)));
-  }
-  if (h->dirs & XC_DIR_A) XC_TRY(dev_alloc(h->partA, (size_t)h->rowsA * Bp * sizeof(double)));
-  if (two_d && h->bsr_nslots > 0)  // partial rows of the split DMMA groups
-    XC_TRY(dev_alloc(h->bsr_part, (size_t)h->bsr_nslots * 8 * Bp * sizeof(double2)));
-  if (two_d && h->tail > 0)  // split-j partial sums of the tail rows: ceil(N/128) x t x B
-    XC_TRY(dev_alloc(h->tailpart, (size_t)((h->N + 127) / 128) * h->tail * Bp * sizeof(double)));
+  double2* p_scr = (double2*)take(scr * sizeof(double2));
+  double2* p_aux[kAux];
+  for (int i = 0; i < kAux; ++i) p_aux[i] = an[i] ? (double2*)take(an[i] * sizeof(double2)) : nullptr;
+  double* p_partA = (h->dirs & XC_DIR_A) ? (double*)take((size_t)h->rowsA * Bp * sizeof(double)) : nullptr;
+  double2* p_bsr = (two_d && h->bsr_nslots > 0) ? (double2*)take((size_t)h->bsr_nslots * 8 * Bp * sizeof(double2))
+                                                 : nullptr;
+  double* p_tail = (two_d && h->tail > 0)
+                       ? (double*)take((size_t)((h->N + 127) / 128) * h->tail * Bp * sizeof(double))
+                       : nullptr;
+  double* p_partW = ((h->dirs & XC_DIR_WAT) && !two_d) ? (double*)take((size_t)h->rowsW * Bp * sizeof(double))
+                                                      : nullptr;
+  std::vector<int64_t> zoff;
+  double* p_zpl = nullptr;
   if ((h->dirs & XC_DIR_WAT) || two_d) {
-    if (!two_d) XC_TRY(dev_alloc(h->partW, (size_t)h->rowsW * Bp * sizeof(double)));
-    h->zoff.clear();
     int64_t tot = 0;
     for (auto& b : h->blocks) {
-      h->zoff.push_back(tot);
+      zoff.push_back(tot);
       tot += 2 * (int64_t)b.H * Bp;
     }
     if (two_d) tot += 2 * 4 * Bp;  // the DMMA blocks may reach 3 rows past the last spectrum row
-    XC_TRY(dev_alloc(h->zpl, (size_t)tot * sizeof(double)));
-    if (two_d) XC_CUDA(cudaMemset(h->zpl.p, 0, (size_t)tot * sizeof(double)));  // finite padding
+    p_zpl = (double*)take((size_t)tot * sizeof(double));
   }
-  h->ws_B = B;
-  clear_graphs(h);  // captured graphs reference the old workspace
+  if (w && base) {
+    w->scratch = p_scr;
+    for (int i = 0; i < kAux; ++i) w->scratch_aux[i] = p_aux[i];
+    w->partA = p_partA;
+    w->bsr_part = p_bsr;
+    w->tailpart = p_tail;
+    w->partW = p_partW;
+    w->zpl = p_zpl;
+    w->zoff = zoff;
+  }
+  return off;
+}
+
+// The forked-stream events and streams of a workspace (created once, before any apply uses it).
+xc_status ws_streams(Ws& w) {
+  if (w.s_aux[0]) return XC_OK;
+  int lo = 0, hi = 0;
+  XC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  for (int i = 0; i < kAux; ++i) {
+    XC_CUDA(cudaStreamCreateWithPriority(&w.s_aux[i], cudaStreamNonBlocking, hi));
+    XC_CUDA(cudaEventCreateWithFlags(&w.ev_join[i], cudaEventDisableTiming));
+  }
+  XC_CUDA(cudaEventCreateWithFlags(&w.ev_fork, cudaEventDisableTiming));
   return XC_OK;
+}
+
+// Carve workspace w for B columns from [w.base, w.base + w.bytes) (no allocation).
+xc_status ws_carve(const xc_op* h, Ws& w, int64_t B) {
+  const size_t need = ws_layout(h, B, nullptr, nullptr);
+  if (need > w.bytes) {
+    xc_set_error("workspace of " + std::to_string(w.bytes) + " bytes is short of the " + std::to_string(need) +
+                 " needed for B = " + std::to_string(B) + " (xc_workspace_query)");
+    return XC_ENOMEM;
+  }
+  ws_layout(h, B, &w, w.base);
+  w.B = B;
+  clear_graphs(w);  // captured graphs reference the old layout
+  return XC_OK;
+}
+
+// The handle's own workspace for up to B columns (allocates: xc_reserve, the host pipeline).
+xc_status ensure_ws(xc_op* h, int64_t B) {
+  XC_TRY(ws_streams(h->def));
+  if (B <= h->def.B) return XC_OK;
+  const size_t need = ws_layout(h, B, nullptr, nullptr);
+  clear_graphs(h->def);
+  XC_TRY(dev_alloc(h->def.own, need));
+  h->def.base = (char*)h->def.own.p;
+  h->def.bytes = need;
+  XC_TRY(ws_carve(h, h->def, B));
+  if (h->def.zpl && h->ukind == XC_LAG2D)  // finite padding rows (read by the DMMA blocks, times 0)
+    XC_CUDA(cudaMemset(h->def.zpl, 0, need - (size_t)((char*)h->def.zpl - h->def.base)));
+  return XC_OK;
+}
+
+// Kernel launches of one apply of B columns (xc_launches; xc_info's counts are for B = 1).
+int64_t c2r_launches_b(const BlockData& b, int64_t B) {
+  if (b.fftM.L2 <= 1) return 1;
+  const int64_t cw = c2r_cols(b, B);
+  return 2 * ((B + cw - 1) / cw);
+}
+int64_t count_launches(const xc_op* h, int dir, int64_t B) {
+  auto spmm_launches = [](int n) -> int64_t { return n <= 0 ? 0 : (n + 65535 - 1) / 65535; };
+  int64_t n = 0;
+  if (h->ukind == XC_LAG2D) {
+    for (auto& b : h->blocks) n += ((b.fft.L2 > 1) ? 2 : 1) + c2r_launches_b(b, B);
+    return n + 1 + (h->bsr_nred > 0 ? 1 : 0) + (h->tail > 0 ? 2 + (h->N > 128 ? 1 : 0) : 0);
+  }
+  if (dir == XC_DIR_A) {
+    if (!(h->dirs & XC_DIR_A)) return 0;
+    n = spmm_launches(h->nwinsA) + (h->tail > 0 ? 1 : 0);
+    for (auto& b : h->blocks)
+      n += (b.split ? 1 : 0) + (h->kind == XC_EXP ? ((b.fft.L2 > 1) ? 2 : 1) : c2r_launches_b(b, B));
+    return n;
+  }
+  if (!(h->dirs & XC_DIR_WAT)) return 0;
+  n = spmm_launches(h->nwinsW) + (h->kind == XC_EXP ? 2 : 1);
+  for (auto& b : h->blocks) n += (b.fft.L2 > 1) ? 2 : 1;
+  return n;
 }
 
 xc_status validate_nodes(int kind, const double* x, int64_t N) {
@@ -1043,6 +1151,8 @@ xc_status build_end(xc_op* h) {
   }
   if (h->dirs & XC_DIR_A) XC_TRY(build_output_axis(h, st));
   if (h->dirs & XC_DIR_WAT) XC_TRY(build_input_axis(h, st));
+  if ((h->dirs & XC_DIR_A) && h->kind != XC_EXP)  // C2R twiddle tables now, not inside an apply
+    for (auto& b : h->blocks) XC_TRY(c2r_prepare(b.fftM));
   dev_free(h->djtab);
   XC_CUDA(cudaStreamSynchronize(st));
 
@@ -1071,15 +1181,8 @@ xc_status build_end(xc_op* h) {
   in.dmma_flops_per_col_WAT = 64.0 * h->mtstepsW;
   in.op_bytes_A = h->tilesA_n * 8 + (int64_t)h->nitemsA * sizeof(SpmmItem);
   in.op_bytes_WAT = h->tilesW_n * 8 + (int64_t)h->nitemsW * sizeof(SpmmItem);
-  int fl = 0, flM = 0, nsplit = 0;
-  for (auto& b : h->blocks) {
-    fl += (b.fft.L2 > 1) ? 2 : 1;
-    flM += h->kind == XC_EXP ? ((b.fft.L2 > 1) ? 2 : 1) : ((b.fftM.L2 > 1) ? 2 : 1);
-    nsplit += b.split ? 1 : 0;
-  }
-  auto spmm_launches = [](int n) { return n <= 0 ? 0 : (n + 65535 - 1) / 65535; };
-  in.launches_A = (h->dirs & XC_DIR_A) ? spmm_launches(h->nwinsA) + nsplit + flM + (h->tail > 0 ? 1 : 0) : 0;
-  in.launches_WAT = (h->dirs & XC_DIR_WAT) ? spmm_launches(h->nwinsW) + fl + 1 : 0;
+  in.launches_A = (int)count_launches(h, XC_DIR_A, 1);
+  in.launches_WAT = (int)count_launches(h, XC_DIR_WAT, 1);
   return XC_OK;
 }
 
@@ -1220,6 +1323,7 @@ xc_status build_2d(xc_op* h) {
     bb.nnz = ptr[Hb];
     total += bb.nnz;
   }
+  for (auto& b : h->blocks) XC_TRY(c2r_prepare(b.fftM));  // C2R twiddle tables (not in an apply)
   XC_TRY(upload(h->ptr2d, gptr));
   XC_TRY(upload(h->ent2d, gent));
   h->rows2d = (int)gptr.size() - 1;
@@ -1312,9 +1416,7 @@ xc_status build_2d(xc_op* h) {
   in.flops_per_col_A = 8.0 * total + 2.0 * (2.0 * t * N - (double)t * t) + fft;
   in.flops_per_col_WAT = 0;
   in.op_bytes_A = total * (int64_t)sizeof(Ent2D);
-  int fl = 0;
-  for (auto& b : h->blocks) fl += ((b.fft.L2 > 1) ? 2 : 1) + ((b.fftM.L2 > 1) ? 2 : 1);
-  in.launches_A = fl + 1 + (h->bsr_nred > 0 ? 1 : 0) + (t > 0 ? 2 + (N > 128 ? 1 : 0) : 0);
+  in.launches_A = (int)count_launches(h, XC_DIR_A, 1);
   return XC_OK;
 }
 
@@ -1359,51 +1461,42 @@ const SpmmWin* wins_for(const DevBuf& w, int nwins, int64_t B) {
 // block 2 goes to s_aux[0], blocks 3.. round robin to s_aux[1..3] (high priority: their few CTAs
 // are dispatched ahead of block 1's persistent grid), each stream with its own FFT scratch;
 // fork/join by events, so the phase also works under CUDA-graph capture.
-bool fork_begin(xc_op* h, cudaStream_t st, int64_t B, xc_status& err) {
+bool fork_begin(xc_op* h, Ws& w, cudaStream_t st, int64_t B, xc_status& err) {
   err = XC_OK;
-  h->naux = naux_for(h->N, B);
-  if (!h->use_fork || h->blocks.size() < 2 || !h->scratch_aux[0].p) return false;
+  w.naux = naux_for(h->N, B);
+  if (!h->use_fork || h->blocks.size() < 2 || !w.scratch_aux[0] || !w.s_aux[0]) return false;
   auto fail = [&](cudaError_t e) {
     xc_set_error(std::string("fork: ") + cudaGetErrorString(e));
     err = XC_ECUDA;
     return false;
   };
   cudaError_t e;
-  if (!h->s_aux[0]) {
-    int lo = 0, hi = 0;
-    if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return fail(e);
-    for (int i = 0; i < xc_op::kAux; ++i) {
-      if ((e = cudaStreamCreateWithPriority(&h->s_aux[i], cudaStreamNonBlocking, hi)) != cudaSuccess) return fail(e);
-      if ((e = cudaEventCreateWithFlags(&h->ev_join[i], cudaEventDisableTiming)) != cudaSuccess) return fail(e);
-    }
-    if ((e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
-  }
-  if ((e = cudaEventRecord(h->ev_fork, st)) != cudaSuccess) return fail(e);
-  const int na = std::min<int>(h->naux, (int)h->blocks.size() - 1);  // streams in use
+  if ((e = cudaEventRecord(w.ev_fork, st)) != cudaSuccess) return fail(e);
+  const int na = std::min<int>(w.naux, (int)h->blocks.size() - 1);  // streams in use
   for (int i = 0; i < na; ++i)
-    if ((e = cudaStreamWaitEvent(h->s_aux[i], h->ev_fork, 0)) != cudaSuccess) return fail(e);
+    if ((e = cudaStreamWaitEvent(w.s_aux[i], w.ev_fork, 0)) != cudaSuccess) return fail(e);
   return true;
 }
 
-xc_status fork_end(xc_op* h, cudaStream_t st, bool fork) {
+xc_status fork_end(xc_op* h, Ws& w, cudaStream_t st, bool fork) {
   if (!fork) return XC_OK;
-  const int na = std::min<int>(h->naux, (int)h->blocks.size() - 1);
+  const int na = std::min<int>(w.naux, (int)h->blocks.size() - 1);
   for (int i = 0; i < na; ++i) {
-    XC_CUDA(cudaEventRecord(h->ev_join[i], h->s_aux[i]));
-    XC_CUDA(cudaStreamWaitEvent(st, h->ev_join[i], 0));
+    XC_CUDA(cudaEventRecord(w.ev_join[i], w.s_aux[i]));
+    XC_CUDA(cudaStreamWaitEvent(st, w.ev_join[i], 0));
   }
   return XC_OK;
 }
 
-cudaStream_t fork_stream(xc_op* h, cudaStream_t st, bool fork, int ib) {
-  return (fork && ib > 0) ? h->s_aux[aux_of(ib, h->naux)] : st;
+cudaStream_t fork_stream(const Ws& w, cudaStream_t st, bool fork, int ib) {
+  return (fork && ib > 0) ? w.s_aux[aux_of(ib, w.naux)] : st;
 }
 
-double2* fork_scratch(xc_op* h, bool fork, int ib) {
-  return (double2*)((fork && ib > 0) ? h->scratch_aux[aux_of(ib, h->naux)].p : h->scratch.p);
+double2* fork_scratch(const Ws& w, bool fork, int ib) {
+  return (fork && ib > 0) ? w.scratch_aux[aux_of(ib, w.naux)] : w.scratch;
 }
 
-xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t B,
+xc_status apply_impl(xc_op* h, Ws& w, xc_dir dir, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t B,
                      cudaStream_t st) {
   if (B < 1 || ldx < B || ldy < B || !X || !Y) {
     xc_set_error("apply: need B >= 1, ldx >= B, ldy >= B, non-null X and Y");
@@ -1417,7 +1510,10 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
     xc_set_error(h->xstage ? "apply: distributed build not finished" : "apply: direction was not built");
     return XC_ESTATE;
   }
-  XC_TRY(ensure_ws(h, B));
+  if (B > w.B) {
+    xc_set_error("apply: B exceeds the workspace (xc_reserve / xc_attach_workspace first)");
+    return XC_ESTATE;
+  }
   cudaEvent_t* ev = nullptr;
   if (h->prof) {
     int slot = (int)(h->ev_count++ % xc_op::kRing);
@@ -1436,7 +1532,7 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
   if (h->ukind == XC_LAG2D) {  // R-23: prologues, merged 2D products + C2R per time block, tails
     const int nb = (int)h->blocks.size();
     xc_status ferr;
-    bool fork = fork_begin(h, st, B, ferr);
+    bool fork = fork_begin(h, w, st, B, ferr);
     XC_TRY(ferr);
     int64_t zrow = 0;  // plane rows of the degree blocks, stacked with the row stride Bp of this call
     for (int a = 0; a < nb; ++a) {
@@ -1448,38 +1544,40 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
       io.keep_lo = b.keep_lo;
       io.keep_hi = b.keep_hi;
       io.m_off = b.m_off;
-      io.dst = (double2*)h->zpl.p + zrow * Bp;  // the rows the CSR entries address (build_2d)
+      io.dst = (double2*)w.zpl + zrow * Bp;  // the rows the CSR entries address (build_2d)
       zrow += b.H;
       io.ldd = Bp;
       io.kmax = b.H;
       io.scale = 1.0 / sqrt((double)b.L);
-      XC_TRY(fft_run(b.fft, +1, PRO_XREAL, EPI_PLAIN, io, (int)B, fork_scratch(h, fork, a),
-                     fork_stream(h, st, fork, a)));
+      XC_TRY(fft_run(b.fft, +1, PRO_XREAL, EPI_PLAIN, io, (int)B, fork_scratch(w, fork, a),
+                     fork_stream(w, st, fork, a)));
     }
-    XC_TRY(fork_end(h, st, fork));
+    XC_TRY(fork_end(h, w, st, fork));
+    // the 4 rows past the last spectrum row: read by the DMMA blocks (times zero), so finite
+    XC_CUDA(cudaMemsetAsync(w.zpl + 2 * zrow * Bp, 0, 8 * Bp * sizeof(double), st));
     XC_TRY(mark(1));
     // the products of all time blocks in one launch (u_b stacked in partA), then the C2R
     // epilogues and the tails
     static const bool use_csr = getenv("XC_2D_CSR") != nullptr;  // the DFMA CSR product (comparison)
     if (use_csr) {
       XC_TRY(lag2d_spmm((const int64_t*)h->ptr2d.p, (const Ent2D*)h->ent2d.p, (const int*)h->order2d.p, h->rows2d,
-                        (const double2*)h->zpl.p, Bp, (double2*)h->partA.p, Bp, (int)B, st));
+                        (const double2*)w.zpl, Bp, (double2*)w.partA, Bp, (int)B, st));
     } else {
       Bsr2D m{(const int64_t*)h->bsr_sptr.p, (const int*)h->bsr_r4.p,  (const double*)h->bsr_tiles.p,
               (const int*)h->bsr_srow.p,     (const int*)h->bsr_snv.p, (const int*)h->bsr_sslot.p,
               (const int*)h->bsr_order.p,    h->bsr_nseg,              (const int*)h->bsr_rrow.p,
               (const int*)h->bsr_rnv.p,      (const int*)h->bsr_rslot.p, (const int*)h->bsr_rcnt.p,
               h->bsr_nred,                   h->bsr_nslots};
-      XC_TRY(lag2d_bsr(m, (const double2*)h->zpl.p, Bp, (double2*)h->partA.p, Bp, (double2*)h->bsr_part.p, (int)B,
+      XC_TRY(lag2d_bsr(m, (const double2*)w.zpl, Bp, (double2*)w.partA, Bp, w.bsr_part, (int)B,
                        st));
     }
     XC_TRY(mark(2));
-    fork = fork_begin(h, st, B, ferr);
+    fork = fork_begin(h, w, st, B, ferr);
     XC_TRY(ferr);
     int64_t uoff = 0;
     for (int ib = 0; ib < nb; ++ib) {
       BlockData& b = h->blocks[ib];
-      double2* U = (double2*)h->partA.p + uoff * Bp;
+      double2* U = (double2*)w.partA + uoff * Bp;
       uoff += b.H;
       FftIO io{};
       io.Uc = U;
@@ -1493,16 +1591,16 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
       io.keep_lo = b.keep_lo;
       io.keep_hi = b.keep_hi;
       io.m_off = b.m_off;
-      XC_TRY(c2r_run(b.fftM, io, (int)B, fork_scratch(h, fork, ib), fork_stream(h, st, fork, ib)));
+      XC_TRY(c2r_run(b.fftM, io, (int)B, fork_scratch(w, fork, ib), fork_stream(w, st, fork, ib)));
     }
-    XC_TRY(fork_end(h, st, fork));  // the tail columns add into rows the epilogues wrote
+    XC_TRY(fork_end(h, w, st, fork));  // the tail columns add into rows the epilogues wrote
     const int t = h->tail;
     if (t > 0) {
-      const int64_t cap = (int64_t)(h->tailpart.bytes / sizeof(double));
-      XC_TRY(dense_tn((const double*)h->tailR.p, N, t, t, X, ldx, Y, ldy, (int)B, false, (double*)h->tailpart.p, cap,
+      const int64_t cap = (int64_t)((h->N + 127) / 128) * h->tail * Bp;
+      XC_TRY(dense_tn((const double*)h->tailR.p, N, t, t, X, ldx, Y, ldy, (int)B, false, w.tailpart, cap,
                       st));
       XC_TRY(dense_tn((const double*)h->tailC.p, t, N - t, N - t, X, ldx, Y + (int64_t)t * ldy, ldy, (int)B, true,
-                      (double*)h->tailpart.p, cap, st));
+                      w.tailpart, cap, st));
     }
     return mark(3);
   }
@@ -1514,12 +1612,12 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
     s.nrows[0] = N;
     s.ld[0] = ldx;
     XC_TRY(spmm_run(wins_for(h->winsA, h->nwinsA, B), h->nwinsA, (const SpmmItem*)h->itemsA.p,
-                    (const double*)h->tilesA.p, s, (double*)h->partA.p, Bp, (int)B, st));
+                    (const double*)h->tilesA.p, s, w.partA, Bp, (int)B, st));
     XC_TRY(mark(1));
     for (auto& b : h->blocks) {
-      double* U = (double*)h->partA.p + b.ubase * Bp;
+      double* U = w.partA + b.ubase * Bp;
       if (b.split)
-        XC_TRY(reduce_rows8((const double*)h->partA.p, Bp, (const int64_t*)b.grp_base.p, (const int*)b.grp_nch.p,
+        XC_TRY(reduce_rows8(w.partA, Bp, (const int64_t*)b.grp_base.p, (const int*)b.grp_nch.p,
                             8 * b.ngroups, nullptr, U, Bp, (int)Bp, st));
       // v = F* u over all L bins (complex inverse DFT), then Fe2 discard and W^{-1}
       FftIO io{};
@@ -1532,7 +1630,7 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
       io.keep_lo = b.keep_lo;
       io.keep_hi = b.keep_hi;
       io.m_off = b.m_off;
-      XC_TRY(fft_run(b.fft, +1, PRO_PLAIN, EPI_CY, io, (int)B, (double2*)h->scratch.p, st));
+      XC_TRY(fft_run(b.fft, +1, PRO_PLAIN, EPI_CY, io, (int)B, w.scratch, st));
     }
     XC_TRY(mark(2));
     return mark(3);
@@ -1544,19 +1642,19 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
     s.nrows[0] = N;
     s.ld[0] = ldx;
     XC_TRY(spmm_run(wins_for(h->winsA, h->nwinsA, B), h->nwinsA, (const SpmmItem*)h->itemsA.p,
-                    (const double*)h->tilesA.p, s, (double*)h->partA.p, Bp, (int)B, st));
+                    (const double*)h->tilesA.p, s, w.partA, Bp, (int)B, st));
     XC_TRY(mark(1));
     const int nb = (int)h->blocks.size();
     xc_status ferr;
-    const bool fork = fork_begin(h, st, B, ferr);
+    const bool fork = fork_begin(h, w, st, B, ferr);
     XC_TRY(ferr);
     for (int ib = 0; ib < nb; ++ib) {
       BlockData& b = h->blocks[ib];
-      cudaStream_t sb = fork_stream(h, st, fork, ib);
-      double2* scr = fork_scratch(h, fork, ib);
-      double* U = (double*)h->partA.p + b.ubase * Bp;
+      cudaStream_t sb = fork_stream(w, st, fork, ib);
+      double2* scr = fork_scratch(w, fork, ib);
+      double* U = w.partA + b.ubase * Bp;
       if (b.split)  // interleaved complex rows: reduce all Bp doubles of each double row
-        XC_TRY(reduce_rows8((const double*)h->partA.p, Bp, (const int64_t*)b.grp_base.p, (const int*)b.grp_nch.p,
+        XC_TRY(reduce_rows8(w.partA, Bp, (const int64_t*)b.grp_base.p, (const int*)b.grp_nch.p,
                             8 * b.ngroups, nullptr, U, Bp, (int)Bp, sb));
       FftIO io{};
       io.Uc = reinterpret_cast<const double2*>(U);
@@ -1572,17 +1670,17 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
       io.m_off = b.m_off;
       XC_TRY(c2r_run(b.fftM, io, (int)B, scr, sb));
     }
-    XC_TRY(fork_end(h, st, fork));
+    XC_TRY(fork_end(h, w, st, fork));
     XC_TRY(mark(2));
     if (h->tail > 0)
-      XC_TRY(reduce_rows8((const double*)h->partA.p, Bp, (const int64_t*)h->tail_base.p, (const int*)h->tail_nch.p,
+      XC_TRY(reduce_rows8(w.partA, Bp, (const int64_t*)h->tail_base.p, (const int*)h->tail_nch.p,
                           h->tail, nullptr, Y, ldy, (int)B, st));
     return mark(3);
   }
   // XC_DIR_WAT
   if (h->kind == XC_EXP) {
     BlockData& b = h->blocks[0];
-    double* zre = (double*)h->zpl.p + h->zoff[0];
+    double* zre = w.zpl + w.zoff[0];
     double* zim = zre + (int64_t)b.H * Bp;
     FftIO io{};
     io.X = X;
@@ -1597,7 +1695,7 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
     io.ldz = Bp;
     io.H = b.H;
     io.scale = 1.0 / sqrt((double)b.L);
-    XC_TRY(fft_run(b.fft, +1, PRO_XCPLX, EPI_ZPLANES, io, (int)B, (double2*)h->scratch.p, st));
+    XC_TRY(fft_run(b.fft, +1, PRO_XCPLX, EPI_ZPLANES, io, (int)B, w.scratch, st));
     SpmmSrcs s{};
     s.re[0] = zre;
     s.im[0] = zim;
@@ -1605,22 +1703,22 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
     s.ld[0] = Bp;
     XC_TRY(mark(1));
     XC_TRY(spmm_run(wins_for(h->winsW, h->nwinsW, B), h->nwinsW, (const SpmmItem*)h->itemsW.p,
-                    (const double*)h->tilesW.p, s, (double*)h->partW.p, Bp, (int)B, st));
+                    (const double*)h->tilesW.p, s, w.partW, Bp, (int)B, st));
     XC_TRY(mark(2));
-    XC_TRY(reduce_rows8((const double*)h->partW.p, Bp, (const int64_t*)h->nodeg_base.p, (const int*)h->nodeg_nch.p,
+    XC_TRY(reduce_rows8(w.partW, Bp, (const int64_t*)h->nodeg_base.p, (const int*)h->nodeg_nch.p,
                         N, (const double*)h->wt.p, Y, ldy, (int)B, st));
-    XC_TRY(reduce_rows8((const double*)h->partW.p, Bp, (const int64_t*)h->nodeg_base_im.p,
+    XC_TRY(reduce_rows8(w.partW, Bp, (const int64_t*)h->nodeg_base_im.p,
                         (const int*)h->nodeg_nch.p, N, (const double*)h->wt.p, Y + (int64_t)N * ldy, ldy, (int)B, st));
     return mark(3);
   }
   SpmmSrcs s{};
   const int nb = (int)h->blocks.size();
   xc_status ferr;
-  const bool fork = fork_begin(h, st, B, ferr);
+  const bool fork = fork_begin(h, w, st, B, ferr);
   XC_TRY(ferr);
   for (int i = 0; i < nb; ++i) {
     BlockData& b = h->blocks[i];
-    double* zre = (double*)h->zpl.p + h->zoff[i];
+    double* zre = w.zpl + w.zoff[i];
     double* zim = zre + (int64_t)b.H * Bp;
     FftIO io{};
     io.X = X;
@@ -1634,40 +1732,53 @@ xc_status apply_impl(xc_op* h, xc_dir dir, const double* X, int64_t ldx, double*
     io.ldz = Bp;
     io.H = b.H;
     io.scale = 1.0 / sqrt((double)b.L);
-    XC_TRY(fft_run(b.fft, +1, PRO_XREAL, EPI_ZPLANES, io, (int)B, fork_scratch(h, fork, i),
-                   fork_stream(h, st, fork, i)));
+    XC_TRY(fft_run(b.fft, +1, PRO_XREAL, EPI_ZPLANES, io, (int)B, fork_scratch(w, fork, i),
+                   fork_stream(w, st, fork, i)));
     s.re[i] = zre;
     s.im[i] = zim;
     s.nrows[i] = b.H;
     s.ld[i] = Bp;
   }
-  XC_TRY(fork_end(h, st, fork));
+  XC_TRY(fork_end(h, w, st, fork));
   s.re[nb] = X;
   s.im[nb] = nullptr;
   s.nrows[nb] = h->tail;
   s.ld[nb] = ldx;
   XC_TRY(mark(1));
   XC_TRY(spmm_run(wins_for(h->winsW, h->nwinsW, B), h->nwinsW, (const SpmmItem*)h->itemsW.p,
-                  (const double*)h->tilesW.p, s, (double*)h->partW.p, Bp, (int)B, st));
+                  (const double*)h->tilesW.p, s, w.partW, Bp, (int)B, st));
   XC_TRY(mark(2));
-  XC_TRY(reduce_rows8((const double*)h->partW.p, Bp, (const int64_t*)h->nodeg_base.p, (const int*)h->nodeg_nch.p, N,
+  XC_TRY(reduce_rows8(w.partW, Bp, (const int64_t*)h->nodeg_base.p, (const int*)h->nodeg_nch.p, N,
                       (const double*)h->wt.p, Y, ldy, (int)B, st));
   return mark(3);
 }
 
+void ws_release(Ws& w) {
+  clear_graphs(w);
+  for (int i = 0; i < kAux; ++i)
+    if (w.s_aux[i]) {
+      cudaStreamSynchronize(w.s_aux[i]);
+      cudaStreamDestroy(w.s_aux[i]);
+      cudaEventDestroy(w.ev_join[i]);
+      w.s_aux[i] = nullptr;
+    }
+  if (w.ev_fork) cudaEventDestroy(w.ev_fork);
+  w.ev_fork = nullptr;
+  dev_free(w.own);
+  w.base = nullptr;
+  w.bytes = 0;
+  w.B = 0;
+}
+
 void destroy_impl(xc_op* h) {
-  clear_graphs(h);
   for (auto& e : h->ev) cudaEventDestroy(e);
   h->ev.clear();
-  for (int i = 0; i < xc_op::kAux; ++i) {
-    if (h->s_aux[i]) {
-      cudaStreamSynchronize(h->s_aux[i]);
-      cudaStreamDestroy(h->s_aux[i]);
-      cudaEventDestroy(h->ev_join[i]);
-    }
-    dev_free(h->scratch_aux[i]);
+  ws_release(h->def);
+  for (Ws* w : h->att) {
+    ws_release(*w);
+    delete w;
   }
-  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  h->att.clear();
   if (h->s_in) {
     cudaStreamSynchronize(h->s_in);
     cudaStreamSynchronize(h->s_out);
@@ -1690,11 +1801,11 @@ void destroy_impl(xc_op* h) {
     dev_free(b.grp_base); dev_free(b.grp_nch);
   }
   DevBuf* all[] = {&h->nodes, &h->wt, &h->tailP, &h->itemsA, &h->tilesA, &h->winsA, &h->tail_base, &h->tail_nch,
-                   &h->itemsW, &h->tilesW, &h->winsW, &h->nodeg_base, &h->nodeg_nch, &h->nodeg_base_im, &h->partA, &h->partW,
-                   &h->scratch, &h->zpl, &h->Xh, &h->Yh, &h->xsend, &h->xrecv, &h->djtab, &h->nodes_lo, &h->cscale,
-                   &h->tailR, &h->tailC, &h->ptr2d, &h->ent2d, &h->order2d, &h->tailpart,
+                   &h->itemsW, &h->tilesW, &h->winsW, &h->nodeg_base, &h->nodeg_nch, &h->nodeg_base_im,
+                   &h->Xh, &h->Yh, &h->xsend, &h->xrecv, &h->djtab, &h->nodes_lo, &h->cscale,
+                   &h->tailR, &h->tailC, &h->ptr2d, &h->ent2d, &h->order2d,
                    &h->bsr_sptr, &h->bsr_r4, &h->bsr_tiles, &h->bsr_srow, &h->bsr_snv, &h->bsr_sslot,
-                   &h->bsr_order, &h->bsr_rrow, &h->bsr_rnv, &h->bsr_rslot, &h->bsr_rcnt, &h->bsr_part};
+                   &h->bsr_order, &h->bsr_rrow, &h->bsr_rnv, &h->bsr_rslot, &h->bsr_rcnt};
   for (DevBuf* b : all) dev_free(*b);
 }
 
@@ -1981,28 +2092,36 @@ xc_status xc_apply(xc_handle h, xc_dir dir, const double* X, int64_t ldx, double
   }
   XC_CUDA(cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
-  if (!h->use_graphs || h->prof || h->xstage != 0) return apply_impl(h, dir, X, ldx, Y, ldy, B, st);
-  xc_op::GraphEntry* e = nullptr;
-  for (auto& g : h->graphs)
+  Ws* wp = &h->def;
+  {
+    std::lock_guard<std::mutex> lk(h->att_mu);
+    for (Ws* a : h->att)
+      if (a->bound == st) wp = a;
+  }
+  Ws& w = *wp;
+  if (wp != &h->def && B > w.B) XC_TRY(ws_carve(h, w, B));  // the caller's memory: no allocation
+  if (!h->use_graphs || h->prof || h->xstage != 0) return apply_impl(h, w, dir, X, ldx, Y, ldy, B, st);
+  GraphEntry* e = nullptr;
+  for (auto& g : w.graphs)
     if (g.X == X && g.Y == Y && g.ldx == ldx && g.ldy == ldy && g.B == B && g.dir == dir && g.st == st) e = &g;
   if (e && e->exec) {
     XC_CUDA(cudaGraphLaunch(e->exec, st));
     return XC_OK;
   }
-  if (!e) {  // first call with these arguments: run directly (lazy tables, workspace, attributes)
-    XC_TRY(apply_impl(h, dir, X, ldx, Y, ldy, B, st));
-    if (h->graphs.size() >= 16) clear_graphs(h);
-    h->graphs.push_back(xc_op::GraphEntry{X, Y, ldx, ldy, B, (int)dir, st, 1, nullptr});
+  if (!e) {  // first call with these arguments: run directly (one-time kernel attributes)
+    XC_TRY(apply_impl(h, w, dir, X, ldx, Y, ldy, B, st));
+    if (w.graphs.size() >= 16) clear_graphs(w);
+    w.graphs.push_back(GraphEntry{X, Y, ldx, ldy, B, (int)dir, st, 1, nullptr});
     return XC_OK;
   }
   // second call: capture the apply once, then replay it
   cudaStreamCaptureStatus cs;
   XC_CUDA(cudaStreamIsCapturing(st, &cs));
   if (cs != cudaStreamCaptureStatusNone || st == nullptr)  // caller is capturing, or legacy stream
-    return apply_impl(h, dir, X, ldx, Y, ldy, B, st);
+    return apply_impl(h, w, dir, X, ldx, Y, ldy, B, st);
   cudaGraph_t graph = nullptr;
   XC_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-  xc_status s = apply_impl(h, dir, X, ldx, Y, ldy, B, st);
+  xc_status s = apply_impl(h, w, dir, X, ldx, Y, ldy, B, st);
   cudaError_t ce = cudaStreamEndCapture(st, &graph);
   if (s != XC_OK) {
     if (graph) cudaGraphDestroy(graph);
@@ -2018,10 +2137,49 @@ xc_status xc_apply(xc_handle h, xc_dir dir, const double* X, int64_t ldx, double
   return XC_OK;
 }
 
+xc_status xc_attach_workspace(xc_handle h, void* stream, void* dptr, size_t bytes) {
+  if (!h) {
+    xc_set_error("null handle");
+    return XC_EINVAL;
+  }
+  XC_CUDA(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> lk(h->att_mu);
+  for (size_t i = 0; i < h->att.size(); ++i)
+    if (h->att[i]->bound == st) {  // replace (or detach): the old one's work must be done
+      XC_CUDA(cudaStreamSynchronize(st));
+      ws_release(*h->att[i]);
+      delete h->att[i];
+      h->att.erase(h->att.begin() + i);
+      break;
+    }
+  if (!dptr) return XC_OK;
+  if (bytes < 256 || ((uintptr_t)dptr & 255)) {
+    xc_set_error("attach_workspace: need a 256-byte aligned device range");
+    return XC_EINVAL;
+  }
+  Ws* w = new Ws();
+  w->bound = st;
+  w->base = (char*)dptr;
+  w->bytes = bytes;
+  xc_status s = ws_streams(*w);
+  if (s != XC_OK) {
+    ws_release(*w);
+    delete w;
+    return s;
+  }
+  h->att.push_back(w);
+  return XC_OK;
+}
+
 xc_status xc_set_graphs(xc_handle h, int enable) {
   if (!h) return XC_EINVAL;
   h->use_graphs = enable != 0;
-  if (!enable) clear_graphs(h);
+  if (!enable) {
+    clear_graphs(h->def);
+    std::lock_guard<std::mutex> lk(h->att_mu);
+    for (Ws* w : h->att) clear_graphs(*w);
+  }
   return XC_OK;
 }
 
@@ -2061,7 +2219,7 @@ xc_status host_enqueue(xc_op* h, xc_dir dir, const double* Xh, double* Yh, int64
   // slot i sits at i * N * Bc: a call with another chunk shape (B or direction) would move the
   // slots under chunks still in flight, so a shape change drains the pipeline first (as does a
   // reallocation)
-  if (h->Xh.bytes < NS * slot || Bc > h->ws_B || Bc != h->hBc || N != h->hN) {
+  if (h->Xh.bytes < NS * slot || Bc > h->def.B || Bc != h->hBc || N != h->hN) {
     XC_CUDA(cudaStreamSynchronize(h->s_in));
     XC_CUDA(cudaStreamSynchronize(h->s_out));
     if (h->hst_set) XC_CUDA(cudaStreamSynchronize(h->hst));
@@ -2096,7 +2254,7 @@ xc_status host_enqueue(xc_op* h, xc_dir dir, const double* Xh, double* Yh, int64
     XC_CUDA(cudaEventRecord(h->ev_in[i], h->s_in));
     XC_CUDA(cudaStreamWaitEvent(st, h->ev_in[i], 0));
     if (reused) XC_CUDA(cudaStreamWaitEvent(st, h->ev_out[i], 0));     // slot's Y copied out
-    XC_TRY(apply_impl(h, dir, xs, bc, ys, bc, bc, st));
+    XC_TRY(apply_impl(h, h->def, dir, xs, bc, ys, bc, bc, st));
     XC_CUDA(cudaEventRecord(h->ev_cmp[i], st));
     XC_CUDA(cudaStreamWaitEvent(h->s_out, h->ev_cmp[i], 0));
     XC_CUDA(cudaMemcpy2DAsync(Yh + c0, B * sizeof(double), ys, bc * sizeof(double), bc * sizeof(double), NO,
@@ -2149,35 +2307,15 @@ xc_status xc_reserve(xc_handle h, int64_t B) {
   return ensure_ws(h, B);
 }
 
+xc_status xc_launches(xc_handle h, xc_dir dir, int64_t B, int64_t* n) {
+  if (!h || !n || B < 1) return XC_EINVAL;
+  *n = count_launches(h, dir, B);
+  return XC_OK;
+}
+
 xc_status xc_workspace_query(xc_handle h, int64_t B, size_t* bytes) {
   if (!h || !bytes || B < 1) return XC_EINVAL;
-  int64_t Bp = pad_cols(B);
-  size_t s = 0, scr = 0;
-  const bool two_d = h->ukind == XC_LAG2D;
-  for (auto& b : h->blocks) {
-    if ((two_d || (h->dirs & XC_DIR_WAT)) && b.fft.L2 > 1) scr = std::max(scr, (size_t)b.L * B * sizeof(double2));
-    if ((h->dirs & XC_DIR_A) && b.fftM.L2 > 1) scr = std::max(scr, (size_t)b.fftM.L * B * sizeof(double2));
-    if ((h->dirs & XC_DIR_A) && h->kind == XC_EXP && b.fft.L2 > 1) scr = std::max(scr, (size_t)b.L * B * sizeof(double2));
-  }
-  s += scr;
-  if (h->kind != XC_EXP && h->blocks.size() > 1) {
-    size_t an[xc_op::kAux] = {};  // the forked streams' FFT scratch (ensure_ws)
-    for (size_t i = 1; i < h->blocks.size(); ++i) {
-      const BlockData& b = h->blocks[i];
-      size_t n = 0;
-      if (((h->dirs & XC_DIR_A) || two_d) && b.fftM.L2 > 1) n = std::max(n, (size_t)b.fftM.L * B * sizeof(double2));
-      if (((h->dirs & XC_DIR_WAT) || two_d) && b.fft.L2 > 1) n = std::max(n, (size_t)b.L * B * sizeof(double2));
-      for (int na : {2, (int)xc_op::kAux})  // scratch for either stream assignment (naux_for)
-        an[aux_of((int)i, na)] = std::max(an[aux_of((int)i, na)], n);
-    }
-    for (size_t a : an) s += a;
-  }
-  if (h->dirs & XC_DIR_A) s += (size_t)h->rowsA * Bp * 8;
-  if ((h->dirs & XC_DIR_WAT) || two_d) {
-    if (!two_d) s += (size_t)h->rowsW * Bp * 8;
-    for (auto& b : h->blocks) s += (size_t)2 * b.H * Bp * 8;
-  }
-  *bytes = s;
+  *bytes = ws_layout(h, B, nullptr, nullptr);
   return XC_OK;
 }
 

@@ -189,6 +189,10 @@ xc_status fft_run(const FftPlan& p, int sigma, FftPro pro, FftEpi epi, const Fft
 // Output-axis real-output inverse (c2r.cu): persistent prefetching passes, half spectrum
 // io.Uc (ldu) -> Y rows (io.Y, ldy) with the W^{-1}/truncate epilogue.  scratch: M*ncol double2.
 xc_status c2r_run(const FftPlan& p, const FftIO& io, int ncol, double2* scratch, cudaStream_t st);
+// two-pass lengths run in column chunks of c2r_chunk_cols(p, ncol) columns (scratch: M x that)
+int64_t c2r_chunk_cols(const FftPlan& p, int64_t ncol);
+// the length's twiddle tables (allocated once per device; call at build time, not in an apply)
+xc_status c2r_prepare(const FftPlan& p);
 // 1 if c2r.cu has a 512-thread big-tile kernel for this pass (mode 0 first / 1 second) and length
 bool c2r_has_big(int mode, int R);
 

@@ -51,6 +51,7 @@ class XcBlockInfo(ctypes.Structure):
 
 
 EXPORTS = ["xc_params_default", "xc_build_compressed", "xc_build_from_bands", "xc_build_local", "xc_build_step", "xc_apply", "xc_c2r_check", "xc_set_graphs", "xc_apply_host", "xc_apply_host_async", "xc_host_wait", "xc_reserve",
+           "xc_attach_workspace", "xc_launches",
            "xc_workspace_query", "xc_info", "xc_block_info", "xc_block_window", "xc_node_spectrum",
            "xc_gauss_rule", "xc_plan_chain", "xc_profile_enable", "xc_profile_read", "xc_destroy",
            "xc_last_error", "xc_version"]
@@ -88,6 +89,8 @@ def load():
     lib.xc_apply_host_async.argtypes = [vp, ctypes.c_int, vp, vp, _i64, vp]
     lib.xc_host_wait.argtypes = [vp]
     lib.xc_reserve.argtypes = [vp, _i64]
+    lib.xc_attach_workspace.argtypes = [vp, vp, vp, ctypes.c_size_t]
+    lib.xc_launches.argtypes = [vp, ctypes.c_int, _i64, ctypes.POINTER(_i64)]
     lib.xc_workspace_query.argtypes = [vp, _i64, ctypes.POINTER(ctypes.c_size_t)]
     lib.xc_info.argtypes = [vp, ctypes.POINTER(XcInfo)]
     lib.xc_block_info.argtypes = [vp, ctypes.c_int, ctypes.POINTER(XcBlockInfo)]
@@ -183,6 +186,7 @@ class Transform:
         lib = load()
         self._lib = lib
         self.kind = kind
+        self._reserved, self._attached = 0, {}
         x = np.ascontiguousarray(np.asarray(nodes, dtype=np.float64))
         self.N = x.size
         self.M = n_rows if n_rows > 0 else self.N   # degrees (rows of A)
@@ -227,6 +231,7 @@ class Transform:
         self = cls.__new__(cls)
         self._lib = lib
         self.kind = kind
+        self._reserved, self._attached = 0, {}
         x = np.ascontiguousarray(np.asarray(nodes, dtype=np.float64))
         self.N = x.size
         self.M = kw.get("n_rows", 0) or self.N
@@ -277,6 +282,8 @@ class Transform:
             raise XcError(f"out must be a CUDA float64 tensor of shape ({rout}, {B}) on {X.device} with "
                           f"unit column stride")
         st = stream if stream is not None else torch.cuda.current_stream(X.device).cuda_stream
+        if st not in self._attached and B > self._reserved:   # xc_apply itself never allocates
+            self.reserve(B)
         _check(self._lib.xc_apply(self._h, direction, ctypes.c_void_p(X.data_ptr()), X.stride(0),
                                   ctypes.c_void_p(out.data_ptr()), out.stride(0), B, ctypes.c_void_p(st)))
         return out
@@ -336,7 +343,27 @@ class Transform:
                 "n": n.value}
 
     def reserve(self, B: int):
+        """xc_reserve: the handle's own workspace for up to B columns (allocates)."""
         _check(self._lib.xc_reserve(self._h, B))
+        self._reserved = max(self._reserved, B)
+
+    def attach_workspace(self, stream: int, ws=None):
+        """xc_attach_workspace: bind a caller-owned CUDA tensor (>= workspace_bytes(B) bytes) as the
+        workspace of applies on `stream` (a cudaStream_t handle); ws=None detaches."""
+        if ws is None:
+            _check(self._lib.xc_attach_workspace(self._h, ctypes.c_void_p(stream), None, 0))
+            self._attached.pop(stream, None)
+            return
+        nbytes = ws.numel() * ws.element_size()
+        _check(self._lib.xc_attach_workspace(self._h, ctypes.c_void_p(stream), ctypes.c_void_p(ws.data_ptr()),
+                                             nbytes))
+        self._attached[stream] = ws   # keep the memory alive while attached
+
+    def launches(self, B: int, direction: int = XC_DIR_A) -> int:
+        """Kernel launches one xc_apply of B columns makes (xc_launches)."""
+        n = _i64()
+        _check(self._lib.xc_launches(self._h, direction, B, ctypes.byref(n)))
+        return n.value
 
     def workspace_bytes(self, B: int) -> int:
         n = ctypes.c_size_t()

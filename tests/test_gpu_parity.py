@@ -1005,3 +1005,60 @@ def test_extreme_parameters(case):
     dense = (w[:, None] * O.dense_apply_t(kind, x, X[:, :4])) if wat else O.dense_apply(kind, x, X[:, :4])
     assert O.rel_l2_cols(Y[:, :4], dense).max() <= 10 * eps, name
     T.close()
+
+
+def test_attached_workspaces_two_streams():
+    """xc_attach_workspace: two streams with their own caller-owned workspaces apply concurrently
+    (interleaved launches, then two host threads) with results bit-identical to the handle's own
+    workspace; a short workspace is XC_ENOMEM and an unreserved B is XC_ESTATE (no allocation in
+    xc_apply)."""
+    import ctypes
+    import threading
+    xc = _xc()
+    kt = (O.KIND_JACOBI, 0.5, -0.3)
+    N, B = 2048, 96
+    x, _ = _nodes(kt, N, 2)
+    T = xc.Transform(kt[0], x, 1e-12, alpha=0.5, beta=-0.3)
+    Xs = [_gpu(I.rhs(N, B, 60 + i)) for i in range(2)]
+    refs = [T.apply(X).clone() for X in Xs]
+    nbytes = T.workspace_bytes(B)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    wss = [torch.empty(nbytes // 8 + 64, dtype=torch.float64, device="cuda") for _ in range(2)]
+    for s, w in zip(streams, wss):
+        T.attach_workspace(s.cuda_stream, w)
+    outs = [torch.full_like(r, float("nan")) for r in refs]
+    torch.cuda.synchronize()
+    for _ in range(3):  # interleaved on the two streams (graph capture on the 2nd call included)
+        for s, X, Y in zip(streams, Xs, outs):
+            T.apply(X, out=Y, stream=s.cuda_stream)
+    torch.cuda.synchronize()
+    assert all(torch.equal(Y, r) for Y, r in zip(outs, refs))
+
+    def worker(i):
+        for _ in range(4):
+            T.apply(Xs[i], out=outs[i], stream=streams[i].cuda_stream)
+    for Y in outs:
+        Y.fill_(float("nan"))
+    torch.cuda.synchronize()
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    assert all(torch.equal(Y, r) for Y, r in zip(outs, refs))
+    # a workspace shorter than xc_workspace_query: XC_ENOMEM, nothing allocated behind the caller
+    s3 = torch.cuda.Stream()
+    small = torch.empty(4096, dtype=torch.float64, device="cuda")
+    T.attach_workspace(s3.cuda_stream, small)
+    with pytest.raises(xc.XcError, match="XC_ENOMEM"):
+        T.apply(Xs[0], stream=s3.cuda_stream)
+    for s in streams + [s3]:
+        T.attach_workspace(s.cuda_stream, None)
+    # the handle's own workspace: B beyond xc_reserve is XC_ESTATE at the C ABI
+    Yb = torch.empty((N, 4 * B), dtype=torch.float64, device="cuda")
+    Xb = _gpu(I.rhs(N, 4 * B, 70))
+    rc = T._lib.xc_apply(T._h, xc.XC_DIR_A, ctypes.c_void_p(Xb.data_ptr()), 4 * B, ctypes.c_void_p(Yb.data_ptr()),
+                         4 * B, 4 * B, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 3   # XC_ESTATE
+    T.close()
