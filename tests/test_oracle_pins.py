@@ -772,3 +772,124 @@ def test_2d_all_tail_is_the_direct_sum():
     assert not op.D2
     C = I.rhs(N, 2, 3)
     np.testing.assert_allclose(O.apply_2d(op, C), O.dense_apply_t(LAG, x, C), rtol=0, atol=1e-12)
+
+
+# --------------------------------------------------------------------------- c5-range pins
+# c5 evaluates degrees up to L_1 - 1 = 86399 (block 1 of N = 65536), where recurrence error grows
+# (P:475).  These pins reach those degrees with references that are not the oracle's recurrence:
+# closed forms at x = 0, +-1 and mpmath's hypergeometric series next to +-1 (where it converges).
+
+C5_DEGREES = (20000, 65534, 65535, 86398, 86399)
+
+
+def _h_jacobi(n, a, b):
+    """Squared norm of P_n^(a,b) (chi_n, read as the squared norm, R-4)."""
+    return mp.mpf(2) ** (a + b + 1) / (2 * n + a + b + 1) * mp.exp(
+        mp.loggamma(n + a + 1) + mp.loggamma(n + b + 1) - mp.loggamma(n + a + b + 1) - mp.loggamma(n + 1))
+
+
+@pytest.mark.parametrize("kind", [LEG, JAC], ids=["legendre", "jacobi_0.5_-0.3"])
+def test_jacobi_c5_degrees_closed_forms(kind):
+    """p_n(1) = C(n+a, n)/sqrt(h_n), p_n(-1) = (-1)^n C(n+b, n)/sqrt(h_n) at the c5 degrees; for
+    Legendre also p_n(0) = sqrt((2n+1)/2) (-1)^{n/2} C(n, n/2)/2^n (n even), 0 (n odd).  Relative
+    1e-14 of the row scale |p_n(1)|."""
+    mp.mp.dps = 40
+    a, b = kind.alpha, kind.beta
+    E = O.entries(kind, np.array([-1.0, 0.0, 1.0]), 0, max(C5_DEGREES) + 1)
+    for n in C5_DEGREES:
+        sh = mp.sqrt(_h_jacobi(n, a, b))
+        p1 = float(mp.binomial(n + a, n) / sh)
+        pm1 = float((-1) ** n * mp.binomial(n + b, n) / sh)
+        assert abs(E[2, n] - p1) <= 1e-14 * abs(p1), (n, E[2, n], p1)
+        assert abs(E[0, n] - pm1) <= 1e-14 * abs(p1), (n, E[0, n], pm1)
+        if a == 0.0 and b == 0.0:
+            p0 = 0.0 if n % 2 else float(mp.sqrt(mp.mpf(2 * n + 1) / 2) * (-1) ** (n // 2) * mp.binomial(n, n // 2)
+                                         / mp.mpf(2) ** n)
+            assert abs(E[1, n] - p0) <= 1e-14 * abs(p1), (n, E[1, n], p0)
+
+
+@pytest.mark.parametrize("kind", [LEG, JAC], ids=["legendre", "jacobi_0.5_-0.3"])
+def test_jacobi_c5_degrees_near_the_ends_vs_mpmath(kind):
+    """Next to x = +-1 (the outermost Gauss nodes of N = 65536 and two more) the hypergeometric series
+    of P_n^(a,b) converges fast even at n = 86399: mpmath (40 digits) vs the oracle's double-double
+    recurrence at the c5 degrees, 1e-14 of the row scale.  x -> -x via P_n^(a,b)(-x) = (-1)^n P_n^(b,a)(x)."""
+    mp.mp.dps = 40
+    a, b = kind.alpha, kind.beta
+    th = [2.404825557695773 / 65536.5, 5.520078110286311 / 65536.5, 3e-5]
+    xs = [math.cos(t) for t in th]
+    x = np.array(sorted([-v for v in xs] + xs))
+    E = O.entries(kind, x, 0, max(C5_DEGREES) + 1)
+    for n in C5_DEGREES:
+        sh = mp.sqrt(_h_jacobi(n, a, b))
+        scale = float(mp.binomial(n + a, n) / sh)
+        for i, xv in enumerate(x):
+            X = mp.mpf(float(xv))
+            if xv > 0:
+                ref = mp.jacobi(n, a, b, X, maxterms=10 ** 6) / sh
+            else:
+                ref = (-1) ** n * mp.jacobi(n, b, a, -X, maxterms=10 ** 6) / sh
+            assert abs(E[i, n] - float(ref)) <= 1e-14 * scale, (n, xv, E[i, n], float(ref))
+
+
+def _gauss_rows_orthogonality(x, w, rows, chunk=1024):
+    """G = A_S diag(w) A_S^T for the sampled degree rows S (entries in node chunks)."""
+    jmax = int(max(rows)) + 1
+    G = np.zeros((len(rows), len(rows)))
+    for k0 in range(0, x.size, chunk):
+        E = O.entries(LEG, x[k0:k0 + chunk], 0, jmax)[:, rows]      # E[k, s] = p_{rows[s]}(x_k)
+        G += E.T @ (w[k0:k0 + chunk, None] * E)
+    return G
+
+
+# Bar of the sampled-row orthogonality: N eps.  The Gauss nodes are rounded to fp64 (relative error
+# eps), and p_j(x~_k) moves by ~ j |x~_k - x_k| / sqrt(1 - x^2) per node, which leaves
+# A diag(w) A^T - I at ~ 0.5 N eps for every row (measured with 80-bit accumulation: 3.7e-13 at
+# N = 4096, 9.2e-13 at 16384, 7.5e-12 at 65536 -- growing as N, not the summation).  An fp64
+# (not double-double) recurrence misses this bar by two orders (3.6e-10 at N = 16384, SURVEY PR-10).
+
+
+def test_discrete_orthogonality_sampled_rows_16384():
+    """A diag(w) A^T = I on 64 sampled degree rows of the N = 16384 Gauss-Legendre transform
+    (both ends of the degree range included), N eps."""
+    N = 16384
+    x, w, _ = O.gauss_rule(LEG, N)
+    rows = np.unique(np.r_[0, 1, N - 2, N - 1, np.random.default_rng(1).integers(0, N, 60)])
+    G = _gauss_rows_orthogonality(x, w, rows)
+    assert np.abs(G - np.eye(len(rows))).max() <= N * np.finfo(float).eps
+
+
+def test_discrete_orthogonality_sampled_rows_65536():
+    """The same at N = 65536 (c5), with the oracle's Gauss rule from tools/make_c5_oracle.py's cache
+    (its N = 65536 Newton solve takes minutes; skipped without the cache)."""
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle_cache",
+                        "c5_oracle.npz")
+    if not os.path.exists(path):
+        pytest.skip("oracle cache missing: tools/make_c5_oracle.py")
+    z = np.load(path)
+    x, w = z["x"], z["w"]
+    N = x.size
+    rows = np.unique(np.r_[0, 1, N - 2, N - 1, np.random.default_rng(2).integers(0, N, 60)])
+    G = _gauss_rows_orthogonality(x, w, rows)
+    assert np.abs(G - np.eye(len(rows))).max() <= N * np.finfo(float).eps
+
+
+@pytest.mark.parametrize("L", [720, 2250, 2916])
+def test_dft_step_vs_naive_dft(L):
+    """The oracle's DFT step (numpy rfft, unitary: Eq. 1) at radix-3/5 block lengths of c1/c3/c5
+    against the naive O(L^2) sum in 80-bit arithmetic with exactly reduced twiddle indices
+    e^{-2 pi i ((p q) mod L) / L}: relative 1e-14 of the spectrum's max."""
+    blk = O.Block(L, 0, L // 4, L)
+    plan = O.Plan(LEG, 64, 1e-12, 1e-2, O.solve_zeta(1e-12), [blk], 0)
+    x = np.array([-0.93, -0.2, 0.41, 0.999])
+    S = O.node_spectra(plan, blk, x)
+    w = O.kaiser(plan.zeta, L - 1).astype(np.longdouble)
+    E = O.entries(LEG, x, 0, L).astype(np.longdouble) * w[None, :]
+    p = np.arange(L, dtype=np.int64)
+    H = L // 2 + 1
+    pq = (p[:, None] * p[None, :H]) % L
+    ang = -2 * np.pi * pq.astype(np.longdouble) / L
+    re = E @ np.cos(ang) / np.sqrt(np.longdouble(L))
+    im = E @ np.sin(ang) / np.sqrt(np.longdouble(L))
+    ref = (re + 1j * im).astype(np.complex128)
+    m = np.abs(ref).max(axis=1, keepdims=True)
+    assert np.all(np.abs(S - ref) <= 1e-14 * m)
