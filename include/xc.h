@@ -38,7 +38,9 @@ typedef enum {
   XC_ESTATE = 3,        /* direction applied that was not built                       */
   XC_ENOMEM = 4,        /* device allocation failed                                   */
   XC_ECUDA = 5,         /* CUDA runtime error                                         */
-  XC_EUNSUPPORTED = 6   /* size beyond the FFT engine's range (L > 1024^2, ...)       */
+  XC_EUNSUPPORTED = 6,  /* size beyond the FFT engine's range (L > 1024^2, ...)       */
+  XC_ENCCL = 7          /* distributed precompute: the caller's all-gather (NCCL) did not
+                           deliver every rank's part of the exchange in rank order      */
 } xc_status;
 
 typedef enum {
@@ -89,6 +91,12 @@ typedef struct {
                               with the 2Q+1 leading window coefficients, only the bins around each
                               node's peak evaluated; the truncated window W' is then the method's
                               window (xc_block_window returns it).  XC_EINVAL for other kinds.  */
+  int thresh_mode;         /* 0: per-node relative threshold |S| >= eps1 max_q |S[k,q]| (P:106,
+                              R-3; default); 1: the global threshold of Alg. 1/2 step 1.3,
+                              |S| >= eps1 max over the block's whole compressed matrix:
+                              two passes over the nodes (and one more exchange, of the block
+                              maxima, in a distributed build).  XC_LAG2D is always global (R-23);
+                              XC_EUNSUPPORTED with trig_precompute = 1.                       */
 } xc_params;
 
 typedef struct {
@@ -146,18 +154,40 @@ xc_status xc_build_from_bands(xc_kind kind, const xc_params* p, const double* no
                               const int* const* start, const int* const* len, const double* const* vals,
                               xc_handle* out);
 
+/* Operator persistence (checkpoint / resume of the precompute, which costs "several orders of
+ * magnitude" more than an apply).  xc_export writes the handle's compressed operator to
+ * `path`: a versioned little-endian file -- header (magic "XCOPER01", kind, thresh_mode,
+ * trig_precompute, dense_cutoff, dirs, block count, tail, N, M, alpha, beta, eta, eps1, eps2,
+ * zeta), the caller's nodes (and weights if XC_DIR_WAT was built), then per block (L, m_off,
+ * keep_lo, keep_hi, nnz), its window (L doubles), the node bands start[N], len[N] (int32) and the
+ * kept values (nnz complex, run-contiguous in node order: the layout of xc_build_from_bands).
+ * xc_import rebuilds the operator from such a file: the plan is recomputed from the file's
+ * parameters and must reproduce its chain, windows and counts (else XC_EINVAL); the kept values
+ * are the file's, so applies are bit-identical to the exporting handle's.  Only device, stream
+ * and node_chunk are taken from p (may be NULL).  Errors: XC_EINVAL (I/O, not an operator file,
+ * truncated, plan mismatch), XC_EUNSUPPORTED (export of XC_LAG2D), XC_ESTATE (export during a
+ * distributed build), XC_ECUDA / XC_ENOMEM. */
+xc_status xc_export(xc_handle h, const char* path);
+xc_status xc_import(const char* path, const xc_params* p, xc_handle* out);
+
 /* Distributed precompute (the node range of the operator is split over ranks).
- * One exchange: the caller copies `send` (bytes_per_rank device bytes) of every rank into
+ * Each exchange: the caller copies `send` (bytes_per_rank device bytes) of every rank into
  * `recv` in rank order (recv + r * bytes_per_rank), e.g. one NCCL all-gather.
  * xc_build_local: phase 1 and the node bands (entries, FFT, threshold; p2-p4) of nodes
  *   [rank * ceil(N/nranks), (rank + 1) * ceil(N/nranks)) only; *ex describes the first exchange
- *   (every node's band start and length).  Same arguments as xc_build_compressed.
- * xc_build_step: consumes the completed exchange; sets *ex to the next one (the kept values,
- *   padded to the largest rank's count) or, after the last, finishes the build (tiles of the
- *   whole operator, identical to xc_build_compressed's) and sets ex->bytes_per_rank = 0.
+ *   (every node's band start and length; with thresh_mode = 1 first the block maxima of this
+ *   rank's nodes, the reference of the global threshold).  Same arguments as xc_build_compressed.
+ * xc_build_step: consumes the completed exchange; sets *ex to the next one (the bands after the
+ *   maxima, the kept values, padded to the largest rank's count, after the bands) or, after the
+ *   last, finishes the build (tiles of the whole operator, identical to xc_build_compressed's)
+ *   and sets ex->bytes_per_rank = 0.
+ * Every rank's part starts with a 16-byte header (magic, stage, rank, nranks) that
+ * xc_build_step checks in every slot of `recv`.
  * The buffers in *ex are owned by the handle and valid until the next call on it.
  * Errors: XC_EINVAL (bad rank / nranks, as xc_build_compressed), XC_ESTATE (step outside a
- * distributed build).  The handle is unusable for xc_apply until the build has finished. */
+ * distributed build), XC_ENCCL (a slot of `recv` does not hold that rank's part of this
+ * exchange: the all-gather failed or ordered the ranks differently).  The handle is unusable for
+ * xc_apply until the build has finished. */
 typedef struct {
   void* send;             /* device, bytes_per_rank bytes                                   */
   void* recv;             /* device, nranks * bytes_per_rank bytes, rank-major              */

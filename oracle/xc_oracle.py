@@ -427,12 +427,28 @@ class Operator:
     P_tail: np.ndarray  # (tail x N) dense, phi_j(x_k) for j < tail
 
 
-def compress(plan: Plan, nodes: np.ndarray, node_chunk: int = 512) -> Operator:
+def threshold_global(S: np.ndarray, eps1: float, gmax2: float) -> np.ndarray:
+    """Global threshold of Algorithm 1/2 step 1.3: drop |S| < eps1 * ||A_e||_max, the max
+    over the block's whole compressed matrix (gmax2 = that max squared)."""
+    mag2 = S.real ** 2 + S.imag ** 2
+    return np.where(mag2 >= (eps1 * eps1) * gmax2, S, 0.0)
+
+
+def compress(plan: Plan, nodes: np.ndarray, node_chunk: int = 512, thresh_mode: int = 0) -> Operator:
+    """The compressed operator of every block.  thresh_mode 0: the per-node
+    relative threshold (reading R-3); 1: the global threshold of step 1.3 -- a first
+    pass over the nodes finds the block's max |S|, the second thresholds."""
     S_list, W_list = [], []
     for blk in plan.blocks:
         parts = []
+        gmax2 = 0.0
+        if thresh_mode == 1:
+            for k0 in range(0, plan.N, node_chunk):
+                S = node_spectra(plan, blk, nodes[k0:k0 + node_chunk])
+                gmax2 = max(gmax2, float((S.real ** 2 + S.imag ** 2).max()))
         for k0 in range(0, plan.N, node_chunk):
-            Sk = threshold(node_spectra(plan, blk, nodes[k0:k0 + node_chunk]), plan.eps1)
+            S = node_spectra(plan, blk, nodes[k0:k0 + node_chunk])
+            Sk = threshold_global(S, plan.eps1, gmax2) if thresh_mode == 1 else threshold(S, plan.eps1)
             parts.append(sp.csr_matrix(Sk))
         S_list.append(sp.vstack(parts).tocsr())
         W_list.append(kaiser(plan.zeta, blk.L - 1))

@@ -731,13 +731,15 @@ xc_status launch(C2RArgs& a, const FftIO& io, cudaStream_t st) {
 
 int c2r_launches(const FftPlan& p) { return p.L2 > 1 ? 2 : 1; }
 
-// Column chunk of a two-pass length: the four-step scratch of one chunk (M x chunk complex) is held
-// near XC_C2R_CHUNK_MB (default 40) MB so that pass 1 reads it from L2 (126 MB) right after pass 0
-// wrote it, instead of a round trip through HBM (c5 block 1: 5.6 GB per apply at B = 4096).
-// XC_C2R_CHUNK_MB=0: one chunk (the whole batch) -- the measurement switch.
+// Column chunk of a two-pass length: with XC_C2R_CHUNK_MB = m > 0 the four-step scratch of one chunk
+// (M x chunk complex) is held near m MB so that pass 1 could read it from L2 right after pass 0
+// wrote it.  Measured at c5 (B = 4096): the scratch traffic does leave HBM, but the FFT phase
+// grows 3.94 -> 4.70 / 4.79 / 4.92 ms at m = 20 / 40 / 80 (2 x 64 launches for block 1 instead of
+// 2, each a short persistent grid with its own ramp and tail; these passes are issue-bound, not
+// HBM-bound), so the default is one chunk (m = 0); the switch stays for measurements.
 int64_t c2r_chunk_cols(const FftPlan& p, int64_t B) {
   if (p.L2 <= 1 || B <= 64) return B;
-  static const int64_t mb = getenv("XC_C2R_CHUNK_MB") ? atoll(getenv("XC_C2R_CHUNK_MB")) : 40;
+  static const int64_t mb = getenv("XC_C2R_CHUNK_MB") ? atoll(getenv("XC_C2R_CHUNK_MB")) : 0;
   if (mb <= 0) return B;
   int64_t c = (mb << 20) / (16 * (int64_t)p.L) / 64 * 64;
   return std::min<int64_t>(B, std::max<int64_t>(64, c));

@@ -11,6 +11,8 @@
 //  * tile fill for the tensor-core SpMM (spmm.cu).
 #include <math.h>
 
+#include <algorithm>
+
 #include "xc_internal.cuh"
 
 namespace {
@@ -137,8 +139,8 @@ __global__ void gen_exp(GenParams g, double2* F, int64_t ld) {
 // circ (complex rows, full spectrum of L = H bins): the run is circular -- the shortest arc
 // holding every kept bin (the complement of the longest circular gap); start in [0, H),
 // start + len may exceed H (bins taken mod H).
-__global__ void band_detect_circ_k(const double2* __restrict__ spec, int H, int nc, double eps1, int* start,
-                                   int* len) {
+__global__ void band_detect_circ_k(const double2* __restrict__ spec, int H, int nc, double eps1, double thr_abs2,
+                                   int* start, int* len) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nc) return;
   double mx = 0.0;
@@ -146,7 +148,7 @@ __global__ void band_detect_circ_k(const double2* __restrict__ spec, int H, int 
     double2 v = spec[(int64_t)q * nc + k];
     mx = fmax(mx, v.x * v.x + v.y * v.y);
   }
-  const double thr = (eps1 * eps1) * mx;
+  const double thr = thr_abs2 > 0.0 ? thr_abs2 : (eps1 * eps1) * mx;  // global or per node
   int first = -1, prev = -1, gap = -1, gap_end = 0;
   if (mx > 0.0)
     for (int q = 0; q < H; ++q) {
@@ -175,7 +177,8 @@ __global__ void band_detect_circ_k(const double2* __restrict__ spec, int H, int 
   }
 }
 
-__global__ void band_detect_k(const double2* __restrict__ spec, int H, int nc, double eps1, int* start, int* len) {
+__global__ void band_detect_k(const double2* __restrict__ spec, int H, int nc, double eps1, double thr_abs2, int* start,
+                              int* len) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nc) return;
   double mx = 0.0;
@@ -183,7 +186,7 @@ __global__ void band_detect_k(const double2* __restrict__ spec, int H, int nc, d
     double2 v = spec[(int64_t)q * nc + k];
     mx = fmax(mx, v.x * v.x + v.y * v.y);
   }
-  double thr = (eps1 * eps1) * mx;
+  const double thr = thr_abs2 > 0.0 ? thr_abs2 : (eps1 * eps1) * mx;  // global or per node
   int first = -1, last = -1;
   if (mx > 0.0) {
     for (int q = 0; q < H; ++q) {
@@ -198,8 +201,8 @@ __global__ void band_detect_k(const double2* __restrict__ spec, int H, int nc, d
   len[k] = first < 0 ? 0 : last - first + 1;
 }
 
-__global__ void band_store_k(const double2* __restrict__ spec, int H, int nc, double eps1, const int* start,
-                             const int* len, const int64_t* off, double2* vals, bool circ) {
+__global__ void band_store_k(const double2* __restrict__ spec, int H, int nc, double eps1, double thr_abs2,
+                             const int* start, const int* len, const int64_t* off, double2* vals, bool circ) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nc) return;
   double mx = 0.0;
@@ -207,7 +210,7 @@ __global__ void band_store_k(const double2* __restrict__ spec, int H, int nc, do
     double2 v = spec[(int64_t)q * nc + k];
     mx = fmax(mx, v.x * v.x + v.y * v.y);
   }
-  double thr = (eps1 * eps1) * mx;
+  const double thr = thr_abs2 > 0.0 ? thr_abs2 : (eps1 * eps1) * mx;
   int s = start[k], n = len[k];
   int64_t o = off[k];
   for (int i = 0; i < n; ++i) {
@@ -219,7 +222,27 @@ __global__ void band_store_k(const double2* __restrict__ spec, int H, int nc, do
   }
 }
 
+// max |S|^2 over a spectrum chunk (the global threshold's reference, Alg. 1/2 step 1.3):
+// non-negative doubles order as their bit patterns, so the max is an exact integer atomicMax
+__global__ void spec_max2_k(const double2* __restrict__ spec, int64_t n, unsigned long long* out) {
+  double m = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = spec[i];
+    m = fmax(m, v.x * v.x + v.y * v.y);
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
 }  // namespace
+
+xc_status spec_max2(const double2* spec, int64_t n, unsigned long long* out, cudaStream_t st) {
+  if (n <= 0) return XC_OK;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 4 * sm_count());
+  spec_max2_k<<<grid, 256, 0, st>>>(spec, n, out);
+  XC_CUDA(cudaGetLastError());
+  return XC_OK;
+}
 
 xc_status gen_entries(const GenParams& g, double2* F, cudaStream_t st) {
   if (g.nc <= 0 || g.L <= 0) return XC_OK;
@@ -252,17 +275,17 @@ xc_status gen_entries_real(const GenParams& g, double* E, int64_t ldE, cudaStrea
   return XC_OK;
 }
 
-xc_status band_detect(const double2* spec, int H, int nc, double eps1, int* start, int* len, bool circ,
-                      cudaStream_t st) {
-  if (circ) band_detect_circ_k<<<(nc + 127) / 128, 128, 0, st>>>(spec, H, nc, eps1, start, len);
-  else band_detect_k<<<(nc + 127) / 128, 128, 0, st>>>(spec, H, nc, eps1, start, len);
+xc_status band_detect(const double2* spec, int H, int nc, double eps1, double thr_abs2, int* start, int* len,
+                      bool circ, cudaStream_t st) {
+  if (circ) band_detect_circ_k<<<(nc + 127) / 128, 128, 0, st>>>(spec, H, nc, eps1, thr_abs2, start, len);
+  else band_detect_k<<<(nc + 127) / 128, 128, 0, st>>>(spec, H, nc, eps1, thr_abs2, start, len);
   XC_CUDA(cudaGetLastError());
   return XC_OK;
 }
 
-xc_status band_store(const double2* spec, int H, int nc, double eps1, const int* start, const int* len,
-                     const int64_t* off, double2* vals, bool circ, cudaStream_t st) {
-  band_store_k<<<(nc + 127) / 128, 128, 0, st>>>(spec, H, nc, eps1, start, len, off, vals, circ);
+xc_status band_store(const double2* spec, int H, int nc, double eps1, double thr_abs2, const int* start,
+                     const int* len, const int64_t* off, double2* vals, bool circ, cudaStream_t st) {
+  band_store_k<<<(nc + 127) / 128, 128, 0, st>>>(spec, H, nc, eps1, thr_abs2, start, len, off, vals, circ);
   XC_CUDA(cudaGetLastError());
   return XC_OK;
 }

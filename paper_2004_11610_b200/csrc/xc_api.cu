@@ -14,6 +14,7 @@
 //               SpMM over all blocks + tail -> reduction times the weights.
 #include <math.h>
 #include <cmath>
+#include <stdio.h>
 #include <string.h>
 #include <stdlib.h>
 
@@ -74,6 +75,7 @@ struct BlockData {
   int64_t nnz = 0;
   int max_band = 0;
   int appQ = -1;  // Appendix A precompute: Q of the truncated window spectrum (-1: direct)
+  double gmax2 = 0;  // thresh_mode = 1: max |S|^2 over the whole block (all ranks)
   int ngroups = 0;
   int64_t loc_count = 0;  // values of the locally computed node range (distributed precompute)
   DevBuf grp_base, grp_nch;  // output axis groups
@@ -124,6 +126,10 @@ struct xc_op {
   int kind = 0;   // machinery kind (XC_LAGSPEC runs as XC_EXP, R-21)
   int ukind = 0;  // the kind the caller built
   bool appA = false;  // Appendix A trig precompute (R-22)
+  int thresh_mode = 0;  // 0: per-node relative threshold (R-3); 1: global
+  std::vector<double> user_nodes, user_wt;  // the caller's nodes / weights (xc_export)
+  double eta = 0;
+  int dense_cutoff = 32;
   DevBuf tailR, tailC;  // XC_LAG2D: direct-method tails (rows i < t: N x t; columns j < t: t x (N-t))
   DevBuf ptr2d, ent2d, order2d;  // XC_LAG2D: CSR of the Hermitian halves of sum_a D2_ab, time blocks
   int rows2d = 0;                 // stacked; order2d: rows longest first
@@ -175,6 +181,7 @@ struct xc_op {
   cudaStream_t bst = nullptr;
   int node_chunk = 0;
   int rank = 0, nranks = 1, npr = 0, xstage = 0;  // npr: nodes per rank (padded)
+  int xstage_next = 0;  // stage of the exchange being prepared (0 max, 1 bands, 2 values: 3, 1, 2)
   DevBuf xsend, xrecv;
   std::vector<int64_t> xmaxc;  // per block: max over ranks of the local value count
   // phase profiling (ring of event sets: start, after phase 1, after phase 2, end)
@@ -415,6 +422,73 @@ xc_status block_setup(xc_op* h, BlockData& b, DevBuf& dxq) {
   return XC_OK;
 }
 
+// The windowed extended rows of nodes [k0, k0 + n) and their unitary DFT (Eq. 1): spec[q * n + k],
+// q < H (the direct precompute, p2-p3).
+xc_status chunk_spectra(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int k0, int n, DevBuf& F, DevBuf& scr,
+                        DevBuf& spec, cudaStream_t st) {
+  GenParams g{};
+  g.kind = h->kind;
+  g.L = b.L;
+  g.m_off = b.m_off;
+  g.nodes = (const double*)h->nodes.p + k0;
+  if (h->nodes_lo.p) g.nodes_lo = (const double*)h->nodes_lo.p + k0;
+  if (h->cscale.p) g.cscale = (const double2*)h->cscale.p + k0;
+  g.nc = n;
+  g.w = (const double*)b.w.p;
+  g.jab = (const double2*)djtab.p;
+  g.p0 = p0;
+  XC_TRY(gen_entries(g, (double2*)F.p, st));
+  FftIO io{};
+  io.src = (const double2*)F.p;
+  io.lds = n;
+  io.dst = (double2*)spec.p;
+  io.ldd = n;
+  io.kmax = b.H;
+  io.scale = 1.0 / sqrt((double)b.L);  // unitary DFT of Eq. (1)
+  return fft_run(b.fft, -1, PRO_PLAIN, EPI_PLAIN, io, n, (double2*)scr.p, st);
+}
+
+// Nodes per precompute chunk of block b: F, the FFT scratch and the spectra (48 B per position and
+// node) take at most a third of the free device memory (capped at 48 GB): the entry recurrence runs
+// one thread per node, so the chunk is the generation's parallelism (c5 block 1: ~9K nodes per
+// chunk instead of 776 with a 3 GB budget -- 10x faster precompute)
+int chunk_nodes(const BlockData& b, int node_chunk, int64_t per_node, int N) {
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = 3ull << 30;
+  const int64_t budget = std::max<int64_t>(1LL << 30, std::min<int64_t>((int64_t)(fr / 3), 48LL << 30));
+  int nc = node_chunk > 0 ? node_chunk : (int)std::max<int64_t>(64, std::min<int64_t>(budget / per_node, 1 << 24));
+  return std::min(nc, std::max(1, N));
+}
+
+// Global threshold reference (thresh_mode = 1, Alg. 1/2 step 1.3): max |S|^2 over the block's
+// spectra of nodes [n0, n1) -- the first of the two passes over the nodes.
+xc_status block_max2(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int node_chunk, int n0, int n1,
+                     double& mx2, cudaStream_t st) {
+  DevBuf dxq;
+  XC_TRY(block_setup(h, b, dxq));
+  const int nc = chunk_nodes(b, node_chunk, (int64_t)b.L * 48, n1 - n0);
+  DevBuf F, scr, spec, dmx;
+  XC_TRY(dev_alloc(F, (size_t)b.L * nc * sizeof(double2)));
+  if (b.fft.L2 > 1) XC_TRY(dev_alloc(scr, (size_t)b.L * nc * sizeof(double2)));
+  XC_TRY(dev_alloc(spec, (size_t)b.H * nc * sizeof(double2)));
+  XC_TRY(dev_alloc(dmx, sizeof(unsigned long long)));
+  XC_CUDA(cudaMemsetAsync(dmx.p, 0, sizeof(unsigned long long), st));
+  for (int k0 = n0; k0 < n1; k0 += nc) {
+    const int n = std::min(nc, n1 - k0);
+    XC_TRY(chunk_spectra(h, b, djtab, p0, k0, n, F, scr, spec, st));
+    XC_TRY(spec_max2((const double2*)spec.p, (int64_t)b.H * n, (unsigned long long*)dmx.p, st));
+  }
+  unsigned long long bits = 0;
+  XC_CUDA(cudaMemcpyAsync(&bits, dmx.p, sizeof(bits), cudaMemcpyDeviceToHost, st));
+  XC_CUDA(cudaStreamSynchronize(st));
+  memcpy(&mx2, &bits, sizeof(double));
+  dev_free(F);
+  dev_free(scr);
+  dev_free(spec);
+  dev_free(dmx);
+  return XC_OK;
+}
+
 xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int node_chunk, int n0, int n1,
                       cudaStream_t st) {
   const int N = (int)h->N;
@@ -422,13 +496,8 @@ xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int n
   DevBuf dxq;
   XC_TRY(block_setup(h, b, dxq));
 
-  // chunk the nodes so that F, the FFT scratch and the spectra (48 B per position and node) take
-  // at most a third of the free device memory (capped at 48 GB): the entry recurrence runs one
-  // thread per node, so the chunk is the generation's parallelism (c5 block 1: ~9K nodes per
-  // chunk instead of 776 with a 3 GB budget -- 10x faster precompute)
-  size_t fr = 0, tot = 0;
-  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = 3ull << 30;
-  const int64_t budget = std::max<int64_t>(1LL << 30, std::min<int64_t>((int64_t)(fr / 3), 48LL << 30));
+  // global threshold (thresh_mode = 1): |S|^2 >= eps1^2 max over the whole block (set by the caller)
+  const double thr2 = h->thresh_mode == 1 ? (h->eps1 * h->eps1) * b.gmax2 : 0.0;
   // Appendix A, window mode: only 2W+1 bins per node are evaluated and kept in memory; for
   // complex rows the window must stay under half the circle (its linear span is then the
   // shortest arc holding the kept bins, R-18); short blocks take the full-spectrum mode
@@ -436,8 +505,7 @@ xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int n
   const int appWmax = cplx_rows ? (b.L / 2 - 1) / 2 : b.H;
   const bool app_win = h->appA && appW <= appWmax;
   int64_t per_node = app_win ? (int64_t)16 * 4 * (2 * appW + 1) + 32 : (int64_t)b.L * 48;
-  int nc = node_chunk > 0 ? node_chunk : (int)std::max<int64_t>(64, std::min<int64_t>(budget / per_node, 1 << 24));
-  nc = std::min(nc, N);
+  const int nc = chunk_nodes(b, node_chunk, per_node, N);
   DevBuf F, scr, spec, st_len, d_start, d_len, dflag, dwin, dwfirst, dthr;
   if (!h->appA) {
     XC_TRY(dev_alloc(F, (size_t)b.L * nc * sizeof(double2)));
@@ -500,30 +568,11 @@ xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int n
         appW = 2 * appW;  // a kept bin on the window's edge: widen and redo the chunk
       }
     } else {
-      GenParams g{};
-      g.kind = h->kind;
-      g.L = b.L;
-      g.m_off = b.m_off;
-      g.nodes = (const double*)h->nodes.p + k0;
-      if (h->nodes_lo.p) g.nodes_lo = (const double*)h->nodes_lo.p + k0;
-      if (h->cscale.p) g.cscale = (const double2*)h->cscale.p + k0;
-      g.nc = n;
-      g.w = (const double*)b.w.p;
-      g.jab = (const double2*)djtab.p;
-      g.p0 = p0;
-      XC_TRY(gen_entries(g, (double2*)F.p, st));
-      FftIO io{};
-      io.src = (const double2*)F.p;
-      io.lds = n;
-      io.dst = (double2*)spec.p;
-      io.ldd = n;
-      io.kmax = b.H;
-      io.scale = 1.0 / sqrt((double)b.L);  // unitary DFT of Eq. (1)
-      XC_TRY(fft_run(b.fft, -1, PRO_PLAIN, EPI_PLAIN, io, n, (double2*)scr.p, st));
+      XC_TRY(chunk_spectra(h, b, djtab, p0, k0, n, F, scr, spec, st));
     }
     int* ds = (int*)b.start.p + k0;
     int* dl = (int*)b.len.p + k0;
-    if (!app_win) XC_TRY(band_detect((const double2*)spec.p, b.H, n, h->eps1, ds, dl, cplx_rows, st));
+    if (!app_win) XC_TRY(band_detect((const double2*)spec.p, b.H, n, h->eps1, thr2, ds, dl, cplx_rows, st));
     XC_CUDA(cudaMemcpyAsync(b.h_start.data() + k0, ds, n * sizeof(int), cudaMemcpyDeviceToHost, st));
     XC_CUDA(cudaMemcpyAsync(b.h_len.data() + k0, dl, n * sizeof(int), cudaMemcpyDeviceToHost, st));
     XC_CUDA(cudaStreamSynchronize(st));
@@ -540,7 +589,7 @@ xc_status build_block(xc_op* h, BlockData& b, const DevBuf& djtab, ddv p0, int n
     if (app_win)
       XC_TRY(appa_store(wm, W, (const int64_t*)choff.p, (double2*)cv.p, n, st));
     else
-      XC_TRY(band_store((const double2*)spec.p, b.H, n, h->eps1, ds, dl, (const int64_t*)choff.p,
+      XC_TRY(band_store((const double2*)spec.p, b.H, n, h->eps1, thr2, ds, dl, (const int64_t*)choff.p,
                         (double2*)cv.p, cplx_rows, st));
     XC_CUDA(cudaStreamSynchronize(st));
     chunk_vals.push_back(cv);
@@ -1028,6 +1077,15 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
   h->kind = kind == XC_LAGSPEC ? XC_EXP : (kind == XC_LAG2D ? XC_LAGUERRE : kind);
   h->ukind = kind;
   h->appA = p.trig_precompute == 1;
+  if (p.thresh_mode != 0 && p.thresh_mode != 1) {
+    xc_set_error("thresh_mode: 0 (per node, P:106) or 1 (global, P:198)");
+    return XC_EINVAL;
+  }
+  if (p.thresh_mode == 1 && h->appA) {
+    xc_set_error("thresh_mode = 1 with the Appendix A precompute");
+    return XC_EUNSUPPORTED;
+  }
+  h->thresh_mode = kind == XC_LAG2D ? 1 : p.thresh_mode;  // the 2D blocks have no node axis (R-23)
   h->use_fork = getenv("XC_NO_FORK") == nullptr;  // A/B switch for measurements
   h->alpha = p.alpha;
   h->beta = p.beta;
@@ -1061,6 +1119,10 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
   }
   XC_TRY(validate_nodes(kind, nodes, N));
   XC_CUDA(cudaSetDevice(p.device));
+  h->user_nodes.assign(nodes, nodes + N);  // for xc_export
+  if (h->dirs & XC_DIR_WAT) h->user_wt.assign(p.weights, p.weights + N);
+  h->eta = p.eta;
+  h->dense_cutoff = p.dense_cutoff > 0 ? p.dense_cutoff : 32;
   cudaStream_t st = (cudaStream_t)p.stream;
 
   PlanOut plan;
@@ -1125,6 +1187,12 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
 // Phase 2 (p2-p4): node bands of the nodes [n0, n1) of every block.
 xc_status build_bands(xc_op* h, int n0, int n1) {
   for (auto& b : h->blocks) XC_TRY(build_block(h, b, h->djtab, h->p0, h->node_chunk, n0, n1, h->bst));
+  return XC_OK;
+}
+
+// Phase 2a (thresh_mode = 1): each block's max |S|^2 over the nodes [n0, n1) into gmax2.
+xc_status build_maxima(xc_op* h, int n0, int n1) {
+  for (auto& b : h->blocks) XC_TRY(block_max2(h, b, h->djtab, h->p0, h->node_chunk, n0, n1, b.gmax2, h->bst));
   return XC_OK;
 }
 
@@ -1423,6 +1491,7 @@ xc_status build_2d(xc_op* h) {
 xc_status build_impl(xc_kind kind, const xc_params* prm, const double* nodes, int64_t N, double eps, xc_op* h) {
   XC_TRY(build_begin(kind, prm, nodes, N, eps, h));
   if (h->ukind == XC_LAG2D) return build_2d(h);
+  if (h->thresh_mode == 1) XC_TRY(build_maxima(h, 0, (int)N));  // two passes: max, then threshold
   XC_TRY(build_bands(h, 0, (int)N));
   return build_end(h);
 }
@@ -1838,6 +1907,68 @@ xc_status xc_build_compressed(xc_kind kind, const xc_params* p, const double* no
   return XC_OK;
 }
 
+namespace {
+
+// The computation stage on given node bands (xc_build_from_bands, xc_import).  windows (import):
+// the exported per-block windows, which the rebuilt plan must reproduce bit for bit.
+xc_status from_bands_impl(xc_kind kind, const xc_params* p, const double* nodes, int64_t N, double eps,
+                          const int* const* start, const int* const* len, const double* const* vals,
+                          const std::vector<std::vector<double>>* windows, xc_op* h) {
+  XC_TRY(build_begin(kind, p, nodes, N, eps, h));
+  if (windows && windows->size() != h->blocks.size()) {
+    xc_set_error("import: the file's block chain differs from the plan of its parameters");
+    return XC_EINVAL;
+  }
+  for (size_t i = 0; i < h->blocks.size(); ++i) {
+    BlockData& b = h->blocks[i];
+    DevBuf none;
+    XC_TRY(block_setup(h, b, none));
+    if (windows && (*windows)[i] != b.h_w) {
+      xc_set_error("import: block " + std::to_string(i) + "'s window differs from the plan's");
+      return XC_EINVAL;
+    }
+    if (!start[i] || !len[i] || !vals[i]) {
+      xc_set_error("build_from_bands: null band arrays of block " + std::to_string(i));
+      return XC_EINVAL;
+    }
+    b.h_start.assign(start[i], start[i] + N);
+    b.h_len.assign(len[i], len[i] + N);
+    b.h_off.assign(N + 1, 0);
+    int64_t tot = 0;
+    for (int64_t k = 0; k < N; ++k) {
+      if (b.h_len[k] < 0 || b.h_len[k] > b.H || b.h_start[k] < 0 || b.h_start[k] >= std::max(1, b.H) ||
+          (h->kind != XC_EXP && b.h_start[k] + b.h_len[k] > b.H)) {
+        xc_set_error("build_from_bands: band out of range at block " + std::to_string(i) + ", node " +
+                     std::to_string(k));
+        return XC_EINVAL;
+      }
+      tot += b.h_len[k];
+    }
+    std::vector<double2> v(std::max<int64_t>(1, tot));
+    for (int64_t q = 0; q < tot; ++q) v[q] = make_double2(vals[i][2 * q], vals[i][2 * q + 1]);
+    XC_TRY(upload(b.vals, v));
+    XC_TRY(upload(b.start, b.h_start));
+    XC_TRY(upload(b.len, b.h_len));
+    b.loc_count = tot;
+  }
+  return build_end(h);
+}
+
+// ---- operator files (xc_export / xc_import), little-endian, version 1 -----------------------
+constexpr char kOpMagic[8] = {'X', 'C', 'O', 'P', 'E', 'R', '0', '1'};
+struct OpFileHdr {
+  char magic[8];
+  int32_t kind, thresh_mode, trig_precompute, dense_cutoff, dirs, n_blocks, tail, reserved;
+  int64_t N, M;
+  double alpha, beta, eta, eps1, eps2, zeta;
+};
+struct OpFileBlk {
+  int32_t L, m_off, keep_lo, keep_hi;
+  int64_t nnz;
+};
+
+}  // namespace
+
 xc_status xc_build_from_bands(xc_kind kind, const xc_params* p, const double* nodes, int64_t N, double eps,
                               const int* const* start, const int* const* len, const double* const* vals,
                               xc_handle* out) {
@@ -1851,48 +1982,236 @@ xc_status xc_build_from_bands(xc_kind kind, const xc_params* p, const double* no
     return XC_EUNSUPPORTED;
   }
   xc_op* h = new xc_op();
-  auto fail = [&](xc_status s) {
+  xc_status s = from_bands_impl(kind, p, nodes, N, eps, start, len, vals, nullptr, h);
+  if (s != XC_OK) {
     destroy_impl(h);
     delete h;
     return s;
-  };
-  xc_status s = build_begin(kind, p, nodes, N, eps, h);
-  if (s != XC_OK) return fail(s);
-  for (size_t i = 0; i < h->blocks.size(); ++i) {
-    BlockData& b = h->blocks[i];
-    DevBuf none;
-    if ((s = block_setup(h, b, none)) != XC_OK) return fail(s);
-    if (!start[i] || !len[i] || !vals[i]) {
-      xc_set_error("build_from_bands: null band arrays of block " + std::to_string(i));
-      return fail(XC_EINVAL);
-    }
-    b.h_start.assign(start[i], start[i] + N);
-    b.h_len.assign(len[i], len[i] + N);
-    b.h_off.assign(N + 1, 0);
-    int64_t tot = 0;
-    for (int64_t k = 0; k < N; ++k) {
-      if (b.h_len[k] < 0 || b.h_len[k] > b.H || b.h_start[k] < 0 || b.h_start[k] >= std::max(1, b.H) ||
-          (h->kind != XC_EXP && b.h_start[k] + b.h_len[k] > b.H)) {
-        xc_set_error("build_from_bands: band out of range at block " + std::to_string(i) + ", node " +
-                     std::to_string(k));
-        return fail(XC_EINVAL);
-      }
-      tot += b.h_len[k];
-    }
-    std::vector<double2> v(std::max<int64_t>(1, tot));
-    for (int64_t q = 0; q < tot; ++q) v[q] = make_double2(vals[i][2 * q], vals[i][2 * q + 1]);
-    if ((s = upload(b.vals, v)) != XC_OK) return fail(s);
-    if ((s = upload(b.start, b.h_start)) != XC_OK) return fail(s);
-    if ((s = upload(b.len, b.h_len)) != XC_OK) return fail(s);
-    b.loc_count = tot;
   }
-  if ((s = build_end(h)) != XC_OK) return fail(s);
+  *out = h;
+  return XC_OK;
+}
+
+xc_status xc_export(xc_handle h, const char* path) {
+  if (!h || !path) {
+    xc_set_error("export: null argument");
+    return XC_EINVAL;
+  }
+  if (h->ukind == XC_LAG2D || h->xstage != 0) {
+    xc_set_error(h->xstage ? "export: distributed build not finished" : "export: XC_LAG2D operators are not exported");
+    return h->xstage ? XC_ESTATE : XC_EUNSUPPORTED;
+  }
+  XC_CUDA(cudaSetDevice(h->device));
+  OpFileHdr hd{};
+  memcpy(hd.magic, kOpMagic, 8);
+  hd.kind = h->ukind;
+  hd.thresh_mode = h->thresh_mode;
+  hd.trig_precompute = h->appA ? 1 : 0;
+  hd.dense_cutoff = h->dense_cutoff;
+  hd.dirs = h->dirs;
+  hd.n_blocks = (int32_t)h->blocks.size();
+  hd.tail = h->tail;
+  hd.N = h->N;
+  hd.M = h->M;
+  hd.alpha = h->alpha;
+  hd.beta = h->beta;
+  hd.eta = h->eta;
+  hd.eps1 = h->eps1;
+  hd.eps2 = h->eps2;
+  hd.zeta = h->zeta;
+  FILE* f = fopen(path, "wb");
+  if (!f) {
+    xc_set_error(std::string("export: cannot open ") + path);
+    return XC_EINVAL;
+  }
+  bool ok = fwrite(&hd, sizeof(hd), 1, f) == 1;
+  ok = ok && fwrite(h->user_nodes.data(), sizeof(double), h->N, f) == (size_t)h->N;
+  if (h->dirs & XC_DIR_WAT) ok = ok && fwrite(h->user_wt.data(), sizeof(double), h->N, f) == (size_t)h->N;
+  for (auto& b : h->blocks) {
+    if (!ok) break;
+    OpFileBlk bk{b.L, b.m_off, b.keep_lo, b.keep_hi, b.nnz};
+    std::vector<double2> v(std::max<int64_t>(1, b.nnz));
+    if (b.nnz > 0) {
+      cudaError_t e = cudaMemcpy(v.data(), b.vals.p, b.nnz * sizeof(double2), cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) {
+        fclose(f);
+        xc_set_error(std::string("export: ") + cudaGetErrorString(e));
+        return XC_ECUDA;
+      }
+    }
+    ok = fwrite(&bk, sizeof(bk), 1, f) == 1;
+    ok = ok && fwrite(b.h_w.data(), sizeof(double), b.L, f) == (size_t)b.L;
+    ok = ok && fwrite(b.h_start.data(), sizeof(int), h->N, f) == (size_t)h->N;
+    ok = ok && fwrite(b.h_len.data(), sizeof(int), h->N, f) == (size_t)h->N;
+    ok = ok && (b.nnz == 0 || fwrite(v.data(), sizeof(double2), b.nnz, f) == (size_t)b.nnz);
+  }
+  if (fclose(f) != 0) ok = false;
+  if (!ok) {
+    xc_set_error(std::string("export: write failed: ") + path);
+    return XC_EINVAL;
+  }
+  return XC_OK;
+}
+
+xc_status xc_import(const char* path, const xc_params* prm, xc_handle* out) {
+  if (!path || !out) {
+    xc_set_error("import: null argument");
+    return XC_EINVAL;
+  }
+  *out = nullptr;
+  FILE* f = fopen(path, "rb");
+  if (!f) {
+    xc_set_error(std::string("import: cannot open ") + path);
+    return XC_EINVAL;
+  }
+  auto bad = [&](const std::string& m) {
+    fclose(f);
+    xc_set_error("import: " + m + " (" + path + ")");
+    return XC_EINVAL;
+  };
+  OpFileHdr hd{};
+  if (fread(&hd, sizeof(hd), 1, f) != 1 || memcmp(hd.magic, kOpMagic, 8) != 0) return bad("not an operator file");
+  if (hd.N < 2 || hd.N > (1 << 24) || hd.n_blocks < 0 || hd.n_blocks >= XC_MAX_BLOCKS) return bad("bad header");
+  const int64_t N = hd.N;
+  std::vector<double> nodes(N), wt;
+  if (fread(nodes.data(), sizeof(double), N, f) != (size_t)N) return bad("truncated nodes");
+  if (hd.dirs & XC_DIR_WAT) {
+    wt.resize(N);
+    if (fread(wt.data(), sizeof(double), N, f) != (size_t)N) return bad("truncated weights");
+  }
+  std::vector<std::vector<int>> st(hd.n_blocks), ln(hd.n_blocks);
+  std::vector<std::vector<double>> vals(hd.n_blocks), win(hd.n_blocks);
+  std::vector<OpFileBlk> bks(hd.n_blocks);
+  for (int i = 0; i < hd.n_blocks; ++i) {
+    OpFileBlk& bk = bks[i];
+    if (fread(&bk, sizeof(bk), 1, f) != 1 || bk.L < 2 || bk.nnz < 0) return bad("bad block header");
+    win[i].resize(bk.L);
+    st[i].resize(N);
+    ln[i].resize(N);
+    vals[i].resize(2 * std::max<int64_t>(1, bk.nnz));
+    if (fread(win[i].data(), sizeof(double), bk.L, f) != (size_t)bk.L ||
+        fread(st[i].data(), sizeof(int), N, f) != (size_t)N || fread(ln[i].data(), sizeof(int), N, f) != (size_t)N ||
+        (bk.nnz > 0 && fread(vals[i].data(), sizeof(double2), bk.nnz, f) != (size_t)bk.nnz))
+      return bad("truncated block " + std::to_string(i));
+  }
+  fclose(f);
+  xc_params p;
+  xc_params_default(&p);
+  if (prm) {  // device and stream from the caller; everything that shapes the operator from the file
+    p.device = prm->device;
+    p.stream = prm->stream;
+    p.node_chunk = prm->node_chunk;
+  }
+  p.alpha = hd.alpha;
+  p.beta = hd.beta;
+  p.eps1 = hd.eps1;
+  p.eps2 = hd.eps2;
+  p.eta = hd.eta;
+  p.dense_cutoff = hd.dense_cutoff;
+  p.dirs = hd.dirs;
+  p.n_rows = hd.M != N ? hd.M : 0;
+  p.trig_precompute = hd.trig_precompute;
+  p.thresh_mode = hd.thresh_mode;
+  p.weights = wt.empty() ? nullptr : wt.data();
+  std::vector<const int*> sp(hd.n_blocks), lp(hd.n_blocks);
+  std::vector<const double*> vp(hd.n_blocks);
+  for (int i = 0; i < hd.n_blocks; ++i) {
+    sp[i] = st[i].data();
+    lp[i] = ln[i].data();
+    vp[i] = vals[i].data();
+  }
+  xc_op* h = new xc_op();
+  xc_status s = from_bands_impl((xc_kind)hd.kind, &p, nodes.data(), N, hd.eps1, sp.data(), lp.data(), vp.data(),
+                                &win, h);
+  if (s == XC_OK) {
+    for (int i = 0; i < hd.n_blocks && s == XC_OK; ++i) {
+      const BlockData& b = h->blocks[i];
+      if (b.L != bks[i].L || b.m_off != bks[i].m_off || b.keep_lo != bks[i].keep_lo || b.keep_hi != bks[i].keep_hi ||
+          b.nnz != bks[i].nnz) {
+        xc_set_error("import: block " + std::to_string(i) + " differs from the plan of the file's parameters");
+        s = XC_EINVAL;
+      }
+    }
+    if (s == XC_OK && (h->tail != hd.tail || h->zeta != hd.zeta)) {
+      xc_set_error("import: the plan's tail or zeta differs from the file's");
+      s = XC_EINVAL;
+    }
+  }
+  if (s != XC_OK) {
+    destroy_impl(h);
+    delete h;
+    return s;
+  }
   *out = h;
   return XC_OK;
 }
 
 // ---- distributed precompute: node range per rank + two all-gathers ----------
 namespace {
+
+// Every rank's part of an exchange starts with this header; after the caller's all-gather the
+// slot of rank r must carry rank r's header of the current stage (else XC_ENCCL: the all-gather
+// was incomplete, out of rank order, or mixed stages).
+struct ExHdr {
+  uint32_t magic, stage, rank, nranks;
+};
+constexpr uint32_t kExMagic = 0x58434558u;  // "XCEX"
+constexpr size_t kExHdr = sizeof(ExHdr);     // 16 bytes: keeps the double2 payload aligned
+
+xc_status put_exchange(xc_op* h, const void* payload, size_t bytes, bool device_payload) {
+  ExHdr hd{kExMagic, (uint32_t)h->xstage_next, (uint32_t)h->rank, (uint32_t)h->nranks};
+  XC_TRY(dev_alloc(h->xsend, kExHdr + bytes));
+  XC_TRY(dev_alloc(h->xrecv, (kExHdr + bytes) * h->nranks));
+  XC_CUDA(cudaMemset(h->xsend.p, 0, kExHdr + bytes));
+  XC_CUDA(cudaMemcpy(h->xsend.p, &hd, kExHdr, cudaMemcpyHostToDevice));
+  if (bytes && payload)
+    XC_CUDA(cudaMemcpy((char*)h->xsend.p + kExHdr, payload, bytes,
+                       device_payload ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+  return XC_OK;
+}
+
+// Check the headers of the completed exchange (per = one rank's slot in bytes).
+xc_status check_exchange(xc_op* h, size_t per) {
+  for (int r = 0; r < h->nranks; ++r) {
+    ExHdr hd{};
+    XC_CUDA(cudaMemcpy(&hd, (const char*)h->xrecv.p + (size_t)r * per, kExHdr, cudaMemcpyDeviceToHost));
+    if (hd.magic != kExMagic || hd.stage != (uint32_t)h->xstage || hd.rank != (uint32_t)r ||
+        hd.nranks != (uint32_t)h->nranks) {
+      xc_set_error("exchange " + std::to_string(h->xstage) + ": slot " + std::to_string(r) + " holds rank " +
+                   std::to_string(hd.rank) + " of stage " + std::to_string(hd.stage) +
+                   " (the all-gather is incomplete or out of rank order)");
+      return XC_ENCCL;
+    }
+  }
+  return XC_OK;
+}
+
+// Exchange 0 (thresh_mode = 1): this rank's max |S|^2 per block (the global threshold's reference,
+// an all-reduce(max) done as an all-gather + max, so one exchange primitive serves all).
+xc_status stage_exchange0(xc_op* h) {
+  std::vector<double> mx;
+  for (auto& b : h->blocks) mx.push_back(b.gmax2);
+  h->xstage_next = 3;
+  return put_exchange(h, mx.data(), mx.size() * sizeof(double), false);
+}
+
+xc_status stage_maxima(xc_op* h) {
+  const int nb = (int)h->blocks.size();
+  const size_t per = kExHdr + (size_t)nb * sizeof(double);
+  XC_TRY(check_exchange(h, per));
+  std::vector<char> all(per * h->nranks);
+  XC_CUDA(cudaMemcpy(all.data(), h->xrecv.p, all.size(), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < nb; ++i) {
+    double m = 0.0;
+    for (int r = 0; r < h->nranks; ++r) {
+      double v;
+      memcpy(&v, all.data() + (size_t)r * per + kExHdr + (size_t)i * sizeof(double), sizeof(double));
+      m = std::max(m, v);
+    }
+    h->blocks[i].gmax2 = m;
+  }
+  return XC_OK;
+}
 
 // Exchange 1: per block, the (start, len) of this rank's nodes, padded to npr nodes.
 xc_status stage_exchange1(xc_op* h) {
@@ -1906,11 +2225,8 @@ xc_status stage_exchange1(xc_op* h) {
       buf[((size_t)i * 2 + 1) * h->npr + (k - n0)] = b.h_len[k];
     }
   }
-  const size_t bytes = buf.size() * sizeof(int);
-  XC_TRY(dev_alloc(h->xsend, bytes));
-  XC_TRY(dev_alloc(h->xrecv, bytes * h->nranks));
-  XC_CUDA(cudaMemcpy(h->xsend.p, buf.data(), bytes, cudaMemcpyHostToDevice));
-  return XC_OK;
+  h->xstage_next = 1;
+  return put_exchange(h, buf.data(), buf.size() * sizeof(int), false);
 }
 
 // After exchange 1: every node's band; exchange 2 carries each rank's values per block,
@@ -1918,14 +2234,17 @@ xc_status stage_exchange1(xc_op* h) {
 xc_status stage_exchange2(xc_op* h) {
   const int nb = (int)h->blocks.size();
   const int N = (int)h->N;
-  std::vector<int> all((size_t)h->nranks * nb * 2 * h->npr);
-  XC_CUDA(cudaMemcpy(all.data(), h->xrecv.p, all.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  const size_t per1 = kExHdr + (size_t)nb * 2 * h->npr * sizeof(int);
+  XC_TRY(check_exchange(h, per1));
+  std::vector<char> raw(per1 * h->nranks);
+  XC_CUDA(cudaMemcpy(raw.data(), h->xrecv.p, raw.size(), cudaMemcpyDeviceToHost));
   h->xmaxc.assign(nb, 1);
   for (int i = 0; i < nb; ++i) {
     BlockData& b = h->blocks[i];
     for (int r = 0; r < h->nranks; ++r) {
-      const int* st = all.data() + (((size_t)r * nb + i) * 2 + 0) * h->npr;
-      const int* ln = all.data() + (((size_t)r * nb + i) * 2 + 1) * h->npr;
+      const int* slot = reinterpret_cast<const int*>(raw.data() + (size_t)r * per1 + kExHdr);
+      const int* st = slot + ((size_t)i * 2 + 0) * h->npr;
+      const int* ln = slot + ((size_t)i * 2 + 1) * h->npr;
       int64_t cnt = 0;
       for (int j = 0; j < h->npr && r * h->npr + j < N; ++j) {
         b.h_start[r * h->npr + j] = st[j];
@@ -1937,10 +2256,9 @@ xc_status stage_exchange2(xc_op* h) {
   }
   size_t per = 0;
   for (int i = 0; i < nb; ++i) per += (size_t)h->xmaxc[i] * sizeof(double2);
-  XC_TRY(dev_alloc(h->xsend, per));
-  XC_TRY(dev_alloc(h->xrecv, per * h->nranks));
-  XC_CUDA(cudaMemset(h->xsend.p, 0, per));
-  size_t off = 0;
+  h->xstage_next = 2;
+  XC_TRY(put_exchange(h, nullptr, per, true));
+  size_t off = kExHdr;
   for (int i = 0; i < nb; ++i) {
     BlockData& b = h->blocks[i];
     if (b.loc_count > 0)
@@ -1954,9 +2272,10 @@ xc_status stage_exchange2(xc_op* h) {
 xc_status stage_finish(xc_op* h) {
   const int nb = (int)h->blocks.size();
   const int N = (int)h->N;
-  size_t per = 0;
+  size_t per = kExHdr;
   for (int i = 0; i < nb; ++i) per += (size_t)h->xmaxc[i] * sizeof(double2);
-  size_t boff = 0;
+  XC_TRY(check_exchange(h, per));
+  size_t boff = kExHdr;
   for (int i = 0; i < nb; ++i) {
     BlockData& b = h->blocks[i];
     int64_t total = 0;
@@ -2011,20 +2330,34 @@ xc_status xc_build_local(xc_kind kind, const xc_params* p, const double* nodes, 
   h->nranks = nranks;
   h->npr = (int)((N + nranks - 1) / nranks);
   const int n0 = std::min<int>((int)N, rank * h->npr), n1 = std::min<int>((int)N, n0 + h->npr);
-  if ((s = build_bands(h, n0, n1)) != XC_OK) return fail(s);
-  if ((s = stage_exchange1(h)) != XC_OK) return fail(s);
-  h->xstage = 1;
+  if (h->thresh_mode == 1) {  // global threshold: first the block maxima of every rank (exchange 0)
+    if ((s = build_maxima(h, n0, n1)) != XC_OK) return fail(s);
+    if ((s = stage_exchange0(h)) != XC_OK) return fail(s);
+  } else {
+    if ((s = build_bands(h, n0, n1)) != XC_OK) return fail(s);
+    if ((s = stage_exchange1(h)) != XC_OK) return fail(s);
+  }
+  h->xstage = h->xstage_next;
   set_exchange(h, ex);
   *out = h;
   return XC_OK;
 }
 
 xc_status xc_build_step(xc_handle h, xc_exchange_t* ex) {
-  if (!h || !ex || h->xstage < 1 || h->xstage > 2) {
+  if (!h || !ex || h->xstage < 1 || h->xstage > 3) {
     xc_set_error("build_step: handle is not in a distributed build");
     return XC_ESTATE;
   }
   XC_CUDA(cudaSetDevice(h->device));
+  if (h->xstage == 3) {  // block maxima of all ranks -> global thresholds -> this rank's bands
+    XC_TRY(stage_maxima(h));
+    const int n0 = std::min<int>((int)h->N, h->rank * h->npr), n1 = std::min<int>((int)h->N, n0 + h->npr);
+    XC_TRY(build_bands(h, n0, n1));
+    XC_TRY(stage_exchange1(h));
+    h->xstage = 1;
+    set_exchange(h, ex);
+    return XC_OK;
+  }
   if (h->xstage == 1) {
     XC_TRY(stage_exchange2(h));
     h->xstage = 2;

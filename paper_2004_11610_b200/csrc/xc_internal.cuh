@@ -317,10 +317,14 @@ xc_status lag2d_bsr(const Bsr2D& m, const double2* z, int64_t ldz, double2* U, i
 // a split-j pass with a deterministic second-pass reduction
 xc_status dense_tn(const double* E, int J, int K, int64_t ldE, const double* X, int64_t ldx, double* Y, int64_t ldy,
                    int B, bool acc, double* part, int64_t part_cap, cudaStream_t st);
-xc_status band_detect(const double2* spec, int H, int nc, double eps1, int* start, int* len, bool circ,
-                      cudaStream_t st);
-xc_status band_store(const double2* spec, int H, int nc, double eps1, const int* start, const int* len,
-                     const int64_t* off, double2* vals, bool circ, cudaStream_t st);
+// thr_abs2 > 0: the global threshold |S|^2 >= thr_abs2 (Alg. 1/2 step 1.3); else per node
+// |S|^2 >= eps1^2 max_q |S[k,q]|^2 (R-3)
+xc_status band_detect(const double2* spec, int H, int nc, double eps1, double thr_abs2, int* start, int* len,
+                      bool circ, cudaStream_t st);
+xc_status band_store(const double2* spec, int H, int nc, double eps1, double thr_abs2, const int* start,
+                     const int* len, const int64_t* off, double2* vals, bool circ, cudaStream_t st);
+// *out = max(*out, max_i |spec_i|^2) as the bit pattern of a non-negative double
+xc_status spec_max2(const double2* spec, int64_t n, unsigned long long* out, cudaStream_t st);
 
 // Gauss rules (gauss.cu)
 xc_status gauss_rule_device(int kind, double alpha, double beta, int64_t N, double* x, double* w,

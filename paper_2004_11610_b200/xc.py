@@ -18,7 +18,7 @@ XC_COS, XC_JACOBI, XC_LAGUERRE, XC_EXP, XC_LAGSPEC, XC_LAG2D = 1, 2, 3, 4, 5, 6
 COMPLEX_KINDS = (XC_EXP, XC_LAGSPEC)  # planar complex X / Y (real rows, then imaginary rows)
 XC_DIR_A, XC_DIR_WAT = 1, 2
 _STATUS = {0: "XC_OK", 1: "XC_EINVAL", 2: "XC_ENUMERIC", 3: "XC_ESTATE", 4: "XC_ENOMEM", 5: "XC_ECUDA",
-           6: "XC_EUNSUPPORTED"}
+           6: "XC_EUNSUPPORTED", 7: "XC_ENCCL"}
 
 _i64 = ctypes.c_int64
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -29,7 +29,7 @@ class XcParams(ctypes.Structure):
                 ("eps2", ctypes.c_double), ("dense_cutoff", ctypes.c_int), ("dirs", ctypes.c_int),
                 ("weights", _dp), ("device", ctypes.c_int), ("stream", ctypes.c_void_p),
                 ("node_chunk", ctypes.c_int), ("eta", ctypes.c_double), ("n_rows", _i64),
-                ("trig_precompute", ctypes.c_int)]
+                ("trig_precompute", ctypes.c_int), ("thresh_mode", ctypes.c_int)]
 
 
 class XcInfo(ctypes.Structure):
@@ -51,7 +51,7 @@ class XcBlockInfo(ctypes.Structure):
 
 
 EXPORTS = ["xc_params_default", "xc_build_compressed", "xc_build_from_bands", "xc_build_local", "xc_build_step", "xc_apply", "xc_c2r_check", "xc_set_graphs", "xc_apply_host", "xc_apply_host_async", "xc_host_wait", "xc_reserve",
-           "xc_attach_workspace", "xc_launches",
+           "xc_attach_workspace", "xc_launches", "xc_export", "xc_import",
            "xc_workspace_query", "xc_info", "xc_block_info", "xc_block_window", "xc_node_spectrum",
            "xc_gauss_rule", "xc_plan_chain", "xc_profile_enable", "xc_profile_read", "xc_destroy",
            "xc_last_error", "xc_version"]
@@ -91,6 +91,8 @@ def load():
     lib.xc_reserve.argtypes = [vp, _i64]
     lib.xc_attach_workspace.argtypes = [vp, vp, vp, ctypes.c_size_t]
     lib.xc_launches.argtypes = [vp, ctypes.c_int, _i64, ctypes.POINTER(_i64)]
+    lib.xc_export.argtypes = [vp, ctypes.c_char_p]
+    lib.xc_import.argtypes = [ctypes.c_char_p, ctypes.POINTER(XcParams), ctypes.POINTER(vp)]
     lib.xc_workspace_query.argtypes = [vp, _i64, ctypes.POINTER(ctypes.c_size_t)]
     lib.xc_info.argtypes = [vp, ctypes.POINTER(XcInfo)]
     lib.xc_block_info.argtypes = [vp, ctypes.c_int, ctypes.POINTER(XcBlockInfo)]
@@ -182,7 +184,7 @@ class Transform:
     def __init__(self, kind: int, nodes, eps: float, alpha: float = 0.0, beta: float = 0.0,
                  eps1: float = 0.0, eps2: float = 0.0, dense_cutoff: int = 0, dirs: int = XC_DIR_A,
                  weights=None, device: int = 0, node_chunk: int = 0, stream=None, dist=None,
-                 eta: float = 0.0, n_rows: int = 0, trig_precompute: int = 0):
+                 eta: float = 0.0, n_rows: int = 0, trig_precompute: int = 0, thresh_mode: int = 0):
         lib = load()
         self._lib = lib
         self.kind = kind
@@ -194,7 +196,7 @@ class Transform:
         lib.xc_params_default(ctypes.byref(p))
         p.alpha, p.beta, p.eps1, p.eps2 = alpha, beta, eps1, eps2
         p.dense_cutoff, p.dirs, p.device, p.node_chunk = dense_cutoff, dirs, device, node_chunk
-        p.eta, p.n_rows, p.trig_precompute = eta, n_rows, trig_precompute
+        p.eta, p.n_rows, p.trig_precompute, p.thresh_mode = eta, n_rows, trig_precompute, thresh_mode
         self._w = None
         if weights is not None:
             self._w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
@@ -218,8 +220,13 @@ class Transform:
             send = device_bytes(ex.send, n, device)
             recv = device_bytes(ex.recv, n * nranks, device)
             torch.cuda.synchronize(device)
-            allgather(send, recv)
-            torch.cuda.synchronize(device)
+            try:
+                allgather(send, recv)
+                torch.cuda.synchronize(device)
+            except Exception as e:   # the exchange failed (NCCL / process group error)
+                lib.xc_destroy(self._h)
+                self._h = None
+                raise XcError(f"XC_ENCCL: exchange all-gather failed: {e}") from e
             self.exchanges.append(n)
             _check(lib.xc_build_step(self._h, ctypes.byref(ex)))
 
@@ -261,6 +268,29 @@ class Transform:
         _check(lib.xc_build_from_bands(kind, ctypes.byref(p), _np_ptr(x), self.N, eps, st, ln, vl, ctypes.byref(h)))
         self._h = h
         return self
+
+    @classmethod
+    def load_file(cls, path: str, device: int = 0):
+        """xc_import: the operator of an xc_export file (plan recomputed and checked, kept values
+        from the file: applies bit-identical to the exporting handle's)."""
+        lib = load()
+        self = cls.__new__(cls)
+        self._lib = lib
+        self._reserved, self._attached = 0, {}
+        p = XcParams()
+        lib.xc_params_default(ctypes.byref(p))
+        p.device = device
+        h = ctypes.c_void_p()
+        _check(lib.xc_import(os.fsencode(path), ctypes.byref(p), ctypes.byref(h)))
+        self._h = h
+        self.device = device
+        inf = self.info()
+        self.kind, self.N, self.M = inf["kind"], inf["N"], inf["M"]
+        return self
+
+    def export(self, path: str):
+        """xc_export: write the compressed operator to `path` (versioned file, include/xc.h)."""
+        _check(self._lib.xc_export(self._h, os.fsencode(path)))
 
     # -- computation stage --------------------------------------------------------------
     def apply(self, X, direction: int = XC_DIR_A, out=None, stream=None):

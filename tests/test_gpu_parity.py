@@ -280,6 +280,8 @@ def _drive_ranks(lib, kind_t, x, eps, nranks, **extra):
         for h, e in zip(hs, exs):
             xc._check(lib.xc_build_step(h, ctypes.byref(e)))
         rounds += 1
+    for h in hs:
+        xc._check(lib.xc_reserve(h, 64))   # xc_apply never allocates
     return hs, rounds
 
 
@@ -1061,4 +1063,139 @@ def test_attached_workspaces_two_streams():
     rc = T._lib.xc_apply(T._h, xc.XC_DIR_A, ctypes.c_void_p(Xb.data_ptr()), 4 * B, ctypes.c_void_p(Yb.data_ptr()),
                          4 * B, 4 * B, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
     assert rc == 3   # XC_ESTATE
+    T.close()
+
+
+GLOBAL_CASES = [("c1", (O.KIND_JACOBI, 0.0, 0.0), 512, 1, 1e-12, 0),
+                ("c3_reduced", (O.KIND_JACOBI, 0.5, -0.3), 2048, 96, 1e-12, 2),
+                ("cos", (O.KIND_COS, 0.0, 0.0), 1000, 130, 1e-10, 1),
+                ("laguerre", (O.KIND_LAGUERRE, 0.0, 0.0), 512, 40, 1e-11, 3)]
+
+
+@pytest.mark.parametrize("case", GLOBAL_CASES, ids=[c[0] for c in GLOBAL_CASES])
+def test_global_threshold_parity(case):
+    """thresh_mode = 1 (the global threshold of Alg. 1/2 step 1.3; two passes over the nodes on
+    the GPU): both directions vs the oracle's compressed apply with the same mode (1e-12), and the
+    dense product within the mode's calibrated 1000 eps."""
+    xc = _xc()
+    name, kt, N, B, eps, seed = case
+    kind = O.Kind(*kt)
+    x, wt = _nodes(kt, N, seed)
+    dirs = xc.XC_DIR_A | (xc.XC_DIR_WAT if wt is not None else 0)
+    T = xc.Transform(kt[0], x, eps, alpha=kt[1], beta=kt[2], thresh_mode=1, dirs=dirs, weights=wt)
+    op = O.compress(O.make_plan(kind, N, eps), x, thresh_mode=1)
+    X = I.rhs(N, B, seed + 200)
+    Y = T.apply(_gpu(X)).cpu().numpy()
+    assert O.rel_l2_cols(Y, O.apply_output_axis(op, X)).max() <= 1e-12, name
+    assert O.rel_l2_cols(Y, O.dense_apply(kind, x, X)).max() <= 1000 * eps, name
+    if wt is not None:
+        Yw = T.apply(_gpu(X), xc.XC_DIR_WAT).cpu().numpy()
+        assert O.rel_l2_cols(Yw, O.apply_input_axis(op, X, wt)).max() <= 1e-12, name
+    T0 = xc.Transform(kt[0], x, eps, alpha=kt[1], beta=kt[2])
+    assert T.info()["nnz"] < T0.info()["nnz"]   # the global threshold keeps fewer entries
+    T.close()
+    T0.close()
+
+
+def test_distributed_global_threshold_and_enccl():
+    """Distributed precompute with thresh_mode = 1: an extra first exchange of the block maxima (3
+    rounds), then the single build's operator bit for bit; an all-gather that delivers the ranks
+    out of order is XC_ENCCL."""
+    import ctypes
+    xc = _xc()
+    lib = xc.load()
+    kt = (O.KIND_JACOBI, 0.5, -0.3)
+    N, B, eps = 1500, 24, 1e-12
+    x, _ = _nodes(kt, N, 2)
+    X = _gpu(I.rhs(N, B, 9))
+    T = xc.Transform(kt[0], x, eps, alpha=kt[1], beta=kt[2], thresh_mode=1)
+    Y = T.apply(X)
+    hs, rounds = _drive_ranks(lib, kt, x, eps, 3, thresh_mode=1)
+    assert rounds == 3
+    for h in hs:
+        Yd = torch.empty_like(Y)
+        xc._check(lib.xc_apply(h, xc.XC_DIR_A, ctypes.c_void_p(X.data_ptr()), B, ctypes.c_void_p(Yd.data_ptr()),
+                               B, B, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        torch.cuda.synchronize()
+        assert torch.equal(Yd, Y)
+        lib.xc_destroy(h)
+    # a broken exchange: rank order reversed in every recv buffer
+    p = xc.XcParams()
+    lib.xc_params_default(ctypes.byref(p))
+    p.alpha, p.beta = kt[1], kt[2]
+    hs, exs = [], []
+    for r in range(2):
+        h, ex = ctypes.c_void_p(), xc.XcExchange()
+        xc._check(lib.xc_build_local(kt[0], ctypes.byref(p), xc._np_ptr(x), N, eps, r, 2, ctypes.byref(h),
+                                     ctypes.byref(ex)))
+        hs.append(h)
+        exs.append(ex)
+    n = exs[0].bytes_per_rank
+    cat = torch.cat([xc.device_bytes(e.send, n) for e in reversed(exs)])
+    for e in exs:
+        xc.device_bytes(e.recv, 2 * n).copy_(cat)
+    torch.cuda.synchronize()
+    assert lib.xc_build_step(hs[0], ctypes.byref(exs[0])) == 7   # XC_ENCCL
+    assert "out of rank order" in lib.xc_last_error().decode()
+    for h in hs:
+        lib.xc_destroy(h)
+    T.close()
+
+
+EXPORT_CASES = ["jacobi_both_dirs", "cos_appendixA", "lagspec_rect", "global_threshold"]
+
+
+@pytest.mark.parametrize("which", EXPORT_CASES)
+def test_export_import_round_trip(which, tmp_path):
+    """xc_export / xc_import (operator persistence; the precompute costs orders of magnitude more
+    than an apply): the imported handle applies bit-identically in every built direction, its
+    node spectra are the exporter's, and the file header reads as documented in include/xc.h."""
+    xc = _xc()
+    B = 20
+    if which == "jacobi_both_dirs":
+        kt = (O.KIND_JACOBI, 0.5, -0.3)
+        x, _ = _nodes(kt, 1200, 2)
+        _, w, _ = O.gauss_rule(O.Kind(*kt), 1200)
+        T = xc.Transform(kt[0], x, 1e-12, alpha=0.5, beta=-0.3, dirs=xc.XC_DIR_A | xc.XC_DIR_WAT, weights=w)
+    elif which == "cos_appendixA":
+        T = xc.Transform(xc.XC_COS, I.cos_nodes(3000, 1), 1e-10, trig_precompute=1)
+    elif which == "lagspec_rect":
+        cfg = I.CONFIGS["c7"]
+        T = xc.Transform(xc.XC_LAGSPEC, I.lagspec_freqs(cfg.N, cfg.T), cfg.eps, eta=cfg.eta, n_rows=cfg.M,
+                         dirs=xc.XC_DIR_A | xc.XC_DIR_WAT, weights=np.ones(cfg.N))
+    else:
+        kt = (O.KIND_JACOBI, 0.0, 0.0)
+        x, _ = _nodes(kt, 900, 0)
+        T = xc.Transform(xc.XC_JACOBI, x, 1e-12, thresh_mode=1)
+    path = str(tmp_path / "op.xcop")
+    T.export(path)
+    raw = open(path, "rb").read()
+    assert raw[:8] == b"XCOPER01"
+    kind, tm, tp, cut, dirs, nb, tail, _ = np.frombuffer(raw[8:40], dtype="<i4")
+    N, M = np.frombuffer(raw[40:56], dtype="<i8")
+    inf = T.info()
+    assert (kind, dirs, nb, tail, N, M) == (inf["kind"], inf["dirs"], inf["n_blocks"], inf["tail"], inf["N"], inf["M"])
+    assert tm == (1 if which == "global_threshold" else 0) and tp == (1 if which == "cos_appendixA" else 0)
+    U = xc.Transform.load_file(path)
+    assert U.info()["nnz"] == inf["nnz"] and U.blocks() == T.blocks()
+    for d in (xc.XC_DIR_A, xc.XC_DIR_WAT):
+        if not (inf["dirs"] & d):
+            continue
+        X = _gpu(I.rhs(T.rows(d)[0], B, 31))
+        assert torch.equal(T.apply(X, d), U.apply(X, d))
+    for k in (0, int(N) // 2, int(N) - 1):
+        assert np.array_equal(T.node_spectrum(0, k), U.node_spectrum(0, k))
+    open(path + ".cut", "wb").write(raw[:len(raw) // 2])
+    with pytest.raises(xc.XcError, match="XC_EINVAL"):
+        xc.Transform.load_file(path + ".cut")
+    T.close()
+    U.close()
+
+
+def test_export_lag2d_unsupported(tmp_path):
+    xc = _xc()
+    cfg = I.CONFIGS["c8"]
+    T = xc.Transform(xc.XC_LAG2D, I.lag2d_grid(256, cfg.eta), 1e-10)
+    with pytest.raises(xc.XcError, match="XC_EUNSUPPORTED"):
+        T.export(str(tmp_path / "x.xcop"))
     T.close()

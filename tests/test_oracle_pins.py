@@ -893,3 +893,42 @@ def test_dft_step_vs_naive_dft(L):
     ref = (re + 1j * im).astype(np.complex128)
     m = np.abs(ref).max(axis=1, keepdims=True)
     assert np.all(np.abs(S - ref) <= 1e-14 * m)
+
+
+# --------------------------------------------------------------------------- global threshold
+def test_global_threshold_soundness_and_subset():
+    """thresh_mode = 1, the global threshold of Alg. 1/2 step 1.3: every kept |S| >= eps1 x the
+    max over the block's whole matrix, every dropped one below it (max taken here over all nodes at
+    once, the oracle takes it in a first pass over node chunks); the kept set is a subset of the
+    per-node threshold's (eps1 x a node's max <= eps1 x the block max)."""
+    N = 300
+    x, _, _ = O.gauss_rule(JAC, N)
+    plan = O.make_plan(JAC, N, 1e-10)
+    opg = O.compress(plan, x, node_chunk=64, thresh_mode=1)
+    opn = O.compress(plan, x, node_chunk=64)
+    for blk, Sg, Sn in zip(plan.blocks, opg.S, opn.S):
+        S = O.node_spectra(plan, blk, x)
+        tau = plan.eps1 * np.abs(S).max()
+        G = Sg.toarray()
+        assert np.all(np.abs(G[G != 0]) >= tau * (1 - 1e-12))
+        assert np.all(np.abs(S[G == 0]) < tau * (1 + 1e-12))
+        assert np.all((Sn.toarray() != 0) | (G == 0))          # subset of the per-node kept set
+        assert Sg.nnz < Sn.nnz
+
+
+def test_global_threshold_keep_all_and_error():
+    """Global threshold: eps1 -> 0 keeps everything (the dense product to 1e-13, as per node), and at
+    eps = 1e-12 the error against the dense product is larger than the per-node threshold's but
+    bounded (calibration, SURVEY PR-7: 7.1e-11 vs 2.3e-12 at N = 1024): <= 1000 eps."""
+    N = 512
+    x, _, _ = O.gauss_rule(JAC, N)
+    plan = O.make_plan(JAC, N, 1e-12)
+    X = I.rhs(N, 6, 12)
+    Yd = O.dense_apply(JAC, x, X)
+    eg = O.rel_l2_cols(O.apply_output_axis(O.compress(plan, x, thresh_mode=1), X), Yd).max()
+    en = O.rel_l2_cols(O.apply_output_axis(O.compress(plan, x), X), Yd).max()
+    assert en < eg <= 1000 * 1e-12, (en, eg)
+    plan0 = O.make_plan(JAC, N, 1e-12)
+    plan0.eps1 = 0.0
+    e0 = O.rel_l2_cols(O.apply_output_axis(O.compress(plan0, x, thresh_mode=1), X), Yd).max()
+    assert e0 < 1e-13
