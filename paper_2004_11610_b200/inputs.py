@@ -47,6 +47,10 @@ CONFIGS = {
     # NEXT-1: the time-domain Laguerre series sum D c, D[i,j] = l_j(eta t_i), t_i = 12 i / (N-1)
     # (P:528), by the 2D block method; eps2 = 0.1 (R-23: errors pass two window divisions)
     "c8": Config("c8_lag2d_4096", KIND_LAG2D, 4096, 256, 1e-10, 8, eps2=0.1, eta=100.0),
+    # off the configured lengths (c5's kind and batch at half and twice N): the generic C2R
+    # passes, no length-specialised kernel -- a check for performance cliffs (not BASELINE configs)
+    "c5n32k": Config("legendre_32768", KIND_JACOBI, 32768, 4096, 1e-12, 12),
+    "c5n128k": Config("legendre_131072", KIND_JACOBI, 131072, 4096, 1e-12, 13),
 }
 
 
