@@ -97,6 +97,13 @@ typedef struct {
                               two passes over the nodes (and one more exchange, of the block
                               maxima, in a distributed build).  XC_LAG2D is always global (R-23);
                               XC_EUNSUPPORTED with trig_precompute = 1.                       */
+  int apply_path;          /* XC_DIR_A of the real kinds: 0 = auto (the small-operator path when
+                              every block has L/2 <= 4096 in at most 8 blocks and the operator has
+                              <= 4M entries -- c1, c2 -- else tiled); 1 = tiled (tensor-core SpMM
+                              over node windows + C2R passes); 2 = the small-operator path (two
+                              launches: a bin-major gather for every u_i and the tail, then every
+                              block's C2R in shared memory; XC_EUNSUPPORTED if not eligible).
+                              The choice depends on the operator only, never on B.            */
 } xc_params;
 
 typedef struct {

@@ -1,0 +1,154 @@
+// small.cu -- the two-launch apply of small operators (XC_DIR_A, real kinds; c1, c2).
+//
+// The computation stage of Alg. 2 / its block form for operators whose every
+// block fits one CTA's shared memory: there the tiled path (DMMA SpMM over node windows, split-K
+// reductions, one or two C2R passes per block, the tail reduction) is launch-bound -- six to ten
+// dependent launches for a few microseconds of work.  Here:
+//   launch 1 (small_spmm_k): every block's half spectrum u_i[q] = sum_k S_i[k,q] x_k by a
+//     bin-major gather (the node bands transposed at build time; nodes ascending, so the sum order
+//     is fixed and independent of the batch), and the dense tail rows Y[j] = sum_k phi_j(x_k) x_k
+//      straight into Y;
+//   launch 2 (small_c2r_k): per (block, column) the real-output inverse DFT of length L = 2M from
+//     u in shared memory (the C2R pairing, then Stockham radix stages), times 1/(sqrt(L) w_p) on
+//     the kept positions only (W^{-1}, Fe2 discard: P:163-180).
+// The choice between this path and the tiled one depends on the operator only (never on B), so a
+// column's result does not depend on the batch it is applied in (sharding stays bit-identical).
+#include <algorithm>
+
+#include "bfly.cuh"
+#include "xc_internal.cuh"
+
+namespace {
+
+using namespace xcb;
+
+// launch 1: rows = every block's bins (complex rows of u) then the tail degrees (real Y rows).
+// A CTA of 256 threads takes RB = 256 / CT rows x CT columns.
+__global__ void __launch_bounds__(256) small_spmm_k(const SmallOp op, const double* __restrict__ X, int64_t ldx,
+                                                    double2* __restrict__ U, int64_t ldu, double* __restrict__ Y,
+                                                    int64_t ldy, int B, int CT) {
+  const int tid = threadIdx.x;
+  const int r = blockIdx.x * (256 / CT) + tid / CT;
+  const int c = blockIdx.y * CT + tid % CT;
+  if (r >= op.rows || c >= B) return;
+  const int64_t e0 = op.ptr[r], e1 = op.ptr[r + 1];
+  double re = 0.0, im = 0.0;
+  for (int64_t e = e0; e < e1; ++e) {
+    const double x = __ldg(X + (int64_t)__ldg(op.node + e) * ldx + c);
+    const double2 v = __ldg(op.val + e);
+    re = fma(v.x, x, re);
+    im = fma(v.y, x, im);
+  }
+  const int64_t o = op.out[r];
+  if (o >= 0) U[o * ldu + c] = make_double2(re, im);   // u row of a block
+  else Y[(-o - 1) * ldy + c] = re;                     // tail degree -o-1
+}
+
+// One Stockham radix-r stage over M points: in -> out, twiddles w_M^{t k M/(Ns r)} from tw (M entries).
+template <int r>
+__device__ __forceinline__ void small_stage(const double2* in, double2* out, const double2* __restrict__ tw, int M,
+                                            int Ns) {
+  const int Mr = M / r, step = M / (Ns * r);
+  for (int j = threadIdx.x; j < Mr; j += blockDim.x) {
+    const int k = j % Ns;
+    double2 v[r];
+#pragma unroll
+    for (int t = 0; t < r; ++t) v[t] = in[j + t * Mr];
+    if (Ns > 1) {
+#pragma unroll
+      for (int t = 1; t < r; ++t) v[t] = c_mul(v[t], __ldg(tw + (int64_t)t * k * step % M));
+    }
+    bfly<r>(v);
+    const int d = (j / Ns) * Ns * r + k;
+#pragma unroll
+    for (int t = 0; t < r; ++t) out[d + t * Ns] = v[t];
+  }
+}
+
+// launch 2: CTA (block i, column c).  Shared: A (H complex; u, then a ping-pong buffer), Bf (M).
+__global__ void __launch_bounds__(256) small_c2r_k(const SmallBlocks sb, const double2* __restrict__ U, int64_t ldu,
+                                                   double* __restrict__ Y, int64_t ldy) {
+  extern __shared__ double2 sm[];
+  const SmallBlk b = sb.blk[blockIdx.x];
+  const int c = blockIdx.y;
+  const int M = b.M;
+  double2* A = sm;
+  double2* Bf = sm + b.M + 1;
+  const double2* u = U + b.urow * ldu + c;
+  for (int q = threadIdx.x; q <= M; q += blockDim.x) A[q] = u[(int64_t)q * ldu];
+  __syncthreads();
+  // pairing: Z[n] = (u_n + conj u_{M-n}) + i e^{i pi n / M} (u_n - conj u_{M-n})
+  for (int n = threadIdx.x; n < M; n += blockDim.x) {
+    const double2 a = A[n], p = A[M - n], w = __ldg(b.twh + n);
+    const double evr = a.x + p.x, evi = a.y - p.y, dr = a.x - p.x, di = a.y + p.y;
+    const double odr = dr * w.x - di * w.y, odi = dr * w.y + di * w.x;
+    Bf[n] = make_double2(evr - odi, evi + odr);
+  }
+  __syncthreads();
+  double2* in = Bf;
+  double2* out = A;
+  int Ns = 1;
+  for (int s = 0; s < b.nf; ++s) {
+    const int r = b.f[s];
+    switch (r) {
+      case 2: small_stage<2>(in, out, b.twM, M, Ns); break;
+      case 3: small_stage<3>(in, out, b.twM, M, Ns); break;
+      case 4: small_stage<4>(in, out, b.twM, M, Ns); break;
+      case 5: small_stage<5>(in, out, b.twM, M, Ns); break;
+      case 6: small_stage<6>(in, out, b.twM, M, Ns); break;
+      case 9: small_stage<9>(in, out, b.twM, M, Ns); break;
+      default: small_stage<8>(in, out, b.twM, M, Ns); break;
+    }
+    Ns *= r;
+    __syncthreads();
+    double2* t = in;
+    in = out;
+    out = t;
+  }
+  // z_k = in[k]: v[2k] = Re z_k, v[2k+1] = Im z_k; Y[p + m_off] = v[p] yscale[p], p in [keep_lo, keep_hi)
+  for (int p = b.keep_lo + threadIdx.x; p < b.keep_hi; p += blockDim.x) {
+    const double2 z = in[p >> 1];
+    Y[(int64_t)(p + b.m_off) * ldy + c] = ((p & 1) ? z.y : z.x) * __ldg(b.yscale + p);
+  }
+}
+
+}  // namespace
+
+xc_status small_spmm(const SmallOp& op, const double* X, int64_t ldx, double2* U, int64_t ldu, double* Y, int64_t ldy,
+                     int B, cudaStream_t st) {
+  int CT = 1;
+  while (CT < 32 && CT < B) CT *= 2;
+  for (int c0 = 0; c0 < B; c0 += 65535 * CT) {  // grid.y limit
+    const int bc = std::min(B - c0, 65535 * CT);
+    dim3 g1((op.rows + 256 / CT - 1) / (256 / CT), (bc + CT - 1) / CT);
+    small_spmm_k<<<g1, 256, 0, st>>>(op, X + c0, ldx, U + c0, ldu, Y + c0, ldy, bc, CT);
+    XC_CUDA(cudaGetLastError());
+  }
+  return XC_OK;
+}
+
+xc_status small_c2r(const SmallBlocks& sb, const double2* U, int64_t ldu, double* Y, int64_t ldy, int B,
+                    cudaStream_t st) {
+  if (sb.nb == 0) return XC_OK;
+  const size_t smem = (size_t)(2 * sb.maxM + 1) * sizeof(double2);
+  static std::atomic<unsigned long long> once{0};
+  if (first_on_device(once))
+    XC_CUDA(cudaFuncSetAttribute(small_c2r_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (2 * kSmallMaxM + 1) * (int)sizeof(double2)));
+  for (int c0 = 0; c0 < B; c0 += 65535) {  // grid.y limit
+    small_c2r_k<<<dim3(sb.nb, std::min(B - c0, 65535)), 256, smem, st>>>(sb, U + c0, ldu, Y + c0, ldy);
+    XC_CUDA(cudaGetLastError());
+  }
+  return XC_OK;
+}
+
+bool small_radices(int M, int* f, int& nf) {
+  nf = 0;
+  int x = M;
+  for (int r : {8, 9, 6, 4, 2, 5, 3})
+    while (x % r == 0 && nf < 16) {
+      f[nf++] = r;
+      x /= r;
+    }
+  return x == 1;
+}

@@ -127,6 +127,11 @@ struct xc_op {
   int ukind = 0;  // the kind the caller built
   bool appA = false;  // Appendix A trig precompute (R-22)
   int thresh_mode = 0;  // 0: per-node relative threshold (R-3); 1: global
+  int apply_path = 0;   // xc_params.apply_path: 0 auto, 1 tiled, 2 small (two launches)
+  bool small_on = false;   // XC_DIR_A runs the small-operator path (small.cu)
+  DevBuf sm_ptr, sm_node, sm_val, sm_out, sm_twM;  // its bin-major operator and stage twiddles
+  SmallOp sm_op{};
+  SmallBlocks sm_blocks{};
   std::vector<double> user_nodes, user_wt;  // the caller's nodes / weights (xc_export)
   double eta = 0;
   int dense_cutoff = 32;
@@ -340,6 +345,11 @@ int64_t count_launches(const xc_op* h, int dir, int64_t B) {
   if (h->ukind == XC_LAG2D) {
     for (auto& b : h->blocks) n += ((b.fft.L2 > 1) ? 2 : 1) + c2r_launches_b(b, B);
     return n + 1 + (h->bsr_nred > 0 ? 1 : 0) + (h->tail > 0 ? 2 + (h->N > 128 ? 1 : 0) : 0);
+  }
+  if (dir == XC_DIR_A && h->small_on) {  // small_spmm / small_c2r grid.y chunks
+    int64_t ct = 1;
+    while (ct < 32 && ct < B) ct *= 2;
+    return (B + 65535 * ct - 1) / (65535 * ct) + (B + 65534) / 65535;
   }
   if (dir == XC_DIR_A) {
     if (!(h->dirs & XC_DIR_A)) return 0;
@@ -1086,6 +1096,11 @@ xc_status build_begin(xc_kind kind, const xc_params* prm, const double* nodes, i
     return XC_EUNSUPPORTED;
   }
   h->thresh_mode = kind == XC_LAG2D ? 1 : p.thresh_mode;  // the 2D blocks have no node axis (R-23)
+  if (p.apply_path < 0 || p.apply_path > 2) {
+    xc_set_error("apply_path: 0 (auto), 1 (tiled) or 2 (small-operator path)");
+    return XC_EINVAL;
+  }
+  h->apply_path = p.apply_path;
   h->use_fork = getenv("XC_NO_FORK") == nullptr;  // A/B switch for measurements
   h->alpha = p.alpha;
   h->beta = p.beta;
@@ -1196,6 +1211,114 @@ xc_status build_maxima(xc_op* h, int n0, int n1) {
   return XC_OK;
 }
 
+// The small-operator path (small.cu): eligible when XC_DIR_A of a real kind has at most
+// kSmallMaxBlocks blocks, each with M = L/2 <= kSmallMaxM (one CTA's shared memory) and a
+// 2-3-5 radix plan, and at most 4M entries in all (bins and tail); the choice depends on the
+// operator only.  Builds the bin-major transpose of the node bands (nodes ascending per bin) and
+// the tail rows, and the per-block tables of the in-shared-memory C2R.
+xc_status build_small(xc_op* h, cudaStream_t st) {
+  h->small_on = false;
+  if (h->apply_path == 1 || !(h->dirs & XC_DIR_A) || h->kind == XC_EXP || h->ukind == XC_LAG2D) return XC_OK;
+  bool ok = (int)h->blocks.size() <= kSmallMaxBlocks;
+  int64_t ents = (int64_t)h->tail * h->N;
+  for (auto& b : h->blocks) {
+    ok = ok && b.L / 2 <= kSmallMaxM;
+    ents += b.nnz;
+  }
+  ok = ok && ents <= (4LL << 20);
+  SmallBlocks sb{};
+  for (size_t i = 0; ok && i < h->blocks.size(); ++i) {
+    ok = small_radices(h->blocks[i].L / 2, sb.blk[i].f, sb.blk[i].nf);
+  }
+  if (!ok) {
+    if (h->apply_path == 2) {
+      xc_set_error("apply_path = 2: the operator is too large for the small-operator path");
+      return XC_EUNSUPPORTED;
+    }
+    return XC_OK;
+  }
+  const int N = (int)h->N;
+  // rows: every block's bins q < H (complex u rows), then the tail degrees
+  std::vector<int64_t> cnt, out;
+  for (auto& b : h->blocks) {
+    for (int q = 0; q < b.H; ++q) out.push_back(b.ubase / 2 + q);
+  }
+  for (int j = 0; j < h->tail; ++j) out.push_back(-(int64_t)j - 1);
+  const int rows = (int)out.size();
+  std::vector<int64_t> ptr(rows + 1, 0);
+  int64_t r0 = 0;
+  for (auto& b : h->blocks) {
+    for (int k = 0; k < N; ++k)
+      for (int j = 0; j < b.h_len[k]; ++j) ptr[r0 + b.h_start[k] + j + 1]++;
+    r0 += b.H;
+  }
+  for (int j = 0; j < h->tail; ++j) ptr[r0 + j + 1] = N;
+  for (int r = 0; r < rows; ++r) ptr[r + 1] += ptr[r];
+  std::vector<int> node(std::max<int64_t>(1, ptr[rows]));
+  std::vector<double2> val(std::max<int64_t>(1, ptr[rows]));
+  std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
+  r0 = 0;
+  for (auto& b : h->blocks) {
+    std::vector<double2> v(std::max<int64_t>(1, b.nnz));
+    if (b.nnz > 0) XC_CUDA(cudaMemcpy(v.data(), b.vals.p, b.nnz * sizeof(double2), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < N; ++k)  // nodes ascending: the fixed summation order of every bin
+      for (int j = 0; j < b.h_len[k]; ++j) {
+        const int64_t e = fill[r0 + b.h_start[k] + j]++;
+        node[e] = k;
+        val[e] = v[b.h_off[k] + j];
+      }
+    r0 += b.H;
+  }
+  if (h->tail > 0) {
+    std::vector<double> P((size_t)h->tail * N);
+    XC_CUDA(cudaMemcpy(P.data(), h->tailP.p, P.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    for (int j = 0; j < h->tail; ++j)
+      for (int k = 0; k < N; ++k) {
+        const int64_t e = fill[r0 + j]++;
+        node[e] = k;
+        val[e] = make_double2(P[(size_t)j * N + k], 0.0);
+      }
+  }
+  XC_TRY(upload(h->sm_ptr, ptr));
+  XC_TRY(upload(h->sm_node, node));
+  XC_TRY(upload(h->sm_val, val));
+  XC_TRY(upload(h->sm_out, out));
+  h->sm_op = SmallOp{(const int64_t*)h->sm_ptr.p, (const int*)h->sm_node.p, (const double2*)h->sm_val.p,
+                     (const int64_t*)h->sm_out.p, rows};
+  // stage twiddles e^{+2 pi i n / M} of every block, concatenated
+  std::vector<double2> tw;
+  std::vector<size_t> twoff;
+  const long double PI2 = 6.283185307179586476925286766559005768L;
+  for (auto& b : h->blocks) {
+    const int M = b.L / 2;
+    twoff.push_back(tw.size());
+    for (int n = 0; n < M; ++n) {
+      const long double a = PI2 * (long double)n / (long double)M;
+      tw.push_back(make_double2((double)cosl(a), (double)sinl(a)));
+    }
+  }
+  XC_TRY(upload(h->sm_twM, tw));
+  sb.nb = (int)h->blocks.size();
+  sb.maxM = 0;
+  for (int i = 0; i < sb.nb; ++i) {
+    const BlockData& b = h->blocks[i];
+    SmallBlk& k = sb.blk[i];
+    k.M = b.L / 2;
+    k.m_off = b.m_off;
+    k.keep_lo = b.keep_lo;
+    k.keep_hi = b.keep_hi;
+    k.urow = b.ubase / 2;
+    k.twh = (const double2*)b.twh.p;
+    k.twM = (const double2*)h->sm_twM.p + twoff[i];
+    k.yscale = (const double*)b.yscale.p;
+    sb.maxM = std::max(sb.maxM, k.M);
+  }
+  h->sm_blocks = sb;
+  h->small_on = true;
+  (void)st;
+  return XC_OK;
+}
+
 // Phase 3: global band offsets, dense tail entries, tensor-core tiles, info.
 xc_status build_end(xc_op* h) {
   const int64_t N = h->N;
@@ -1221,6 +1344,7 @@ xc_status build_end(xc_op* h) {
   if (h->dirs & XC_DIR_WAT) XC_TRY(build_input_axis(h, st));
   if ((h->dirs & XC_DIR_A) && h->kind != XC_EXP)  // C2R twiddle tables now, not inside an apply
     for (auto& b : h->blocks) XC_TRY(c2r_prepare(b.fftM));
+  XC_TRY(build_small(h, st));
   dev_free(h->djtab);
   XC_CUDA(cudaStreamSynchronize(st));
 
@@ -1704,6 +1828,13 @@ xc_status apply_impl(xc_op* h, Ws& w, xc_dir dir, const double* X, int64_t ldx, 
     XC_TRY(mark(2));
     return mark(3);
   }
+  if (dir == XC_DIR_A && h->small_on) {  // small operators: two launches (small.cu)
+    XC_TRY(small_spmm(h->sm_op, X, ldx, (double2*)w.partA, Bp, Y, ldy, (int)B, st));
+    XC_TRY(mark(1));
+    XC_TRY(small_c2r(h->sm_blocks, (const double2*)w.partA, Bp, Y, ldy, (int)B, st));
+    XC_TRY(mark(2));
+    return mark(3);
+  }
   if (dir == XC_DIR_A) {
     SpmmSrcs s{};
     s.re[0] = X;
@@ -1874,7 +2005,8 @@ void destroy_impl(xc_op* h) {
                    &h->Xh, &h->Yh, &h->xsend, &h->xrecv, &h->djtab, &h->nodes_lo, &h->cscale,
                    &h->tailR, &h->tailC, &h->ptr2d, &h->ent2d, &h->order2d,
                    &h->bsr_sptr, &h->bsr_r4, &h->bsr_tiles, &h->bsr_srow, &h->bsr_snv, &h->bsr_sslot,
-                   &h->bsr_order, &h->bsr_rrow, &h->bsr_rnv, &h->bsr_rslot, &h->bsr_rcnt};
+                   &h->bsr_order, &h->bsr_rrow, &h->bsr_rnv, &h->bsr_rslot, &h->bsr_rcnt,
+                   &h->sm_ptr, &h->sm_node, &h->sm_val, &h->sm_out, &h->sm_twM};
   for (DevBuf* b : all) dev_free(*b);
 }
 
@@ -2101,6 +2233,7 @@ xc_status xc_import(const char* path, const xc_params* prm, xc_handle* out) {
     p.device = prm->device;
     p.stream = prm->stream;
     p.node_chunk = prm->node_chunk;
+    p.apply_path = prm->apply_path;
   }
   p.alpha = hd.alpha;
   p.beta = hd.beta;

@@ -333,3 +333,35 @@ xc_status gauss_rule_device(int kind, double alpha, double beta, int64_t N, doub
 // Host-side Jacobi recurrence coefficients in double-double (plan.cu)
 void jacobi_coeffs(double alpha, double beta, int nmax, std::vector<double2>& tab, ddv& p0);
 double jacobi_mu0(double alpha, double beta);
+
+// ---------------------------------------------------------------------------
+// Small operators (small.cu): the two-launch apply of XC_DIR_A for real kinds when every block's
+// M = L/2 <= kSmallMaxM: a bin-major gather for all u_i and the tail, then every block's C2R in
+// shared memory.
+// ---------------------------------------------------------------------------
+constexpr int kSmallMaxM = 4096;
+constexpr int kSmallMaxBlocks = 8;
+struct SmallOp {
+  const int64_t* ptr;   // rows + 1: entries of row r at [ptr[r], ptr[r+1])
+  const int* node;      // node index of each entry (ascending within a row)
+  const double2* val;   // S_i[k, q] (block bins) or (phi_j(x_k), 0) (tail degrees)
+  const int64_t* out;   // >= 0: complex u row (double2 units, ld = ldu); < 0: tail degree -out-1
+  int rows;
+};
+struct SmallBlk {
+  int M, nf, f[16];
+  int m_off, keep_lo, keep_hi;
+  int64_t urow;           // first complex u row of the block
+  const double2* twh;     // e^{+i pi n / M}, n < M (pairing)
+  const double2* twM;     // e^{+2 pi i n / M}, n < M (stage twiddles)
+  const double* yscale;   // 1 / (sqrt(L) w_p)
+};
+struct SmallBlocks {
+  SmallBlk blk[kSmallMaxBlocks];
+  int nb, maxM;
+};
+xc_status small_spmm(const SmallOp& op, const double* X, int64_t ldx, double2* U, int64_t ldu, double* Y, int64_t ldy,
+                     int B, cudaStream_t st);
+xc_status small_c2r(const SmallBlocks& sb, const double2* U, int64_t ldu, double* Y, int64_t ldy, int B,
+                    cudaStream_t st);
+bool small_radices(int M, int* f, int& nf);

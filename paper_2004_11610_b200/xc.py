@@ -29,7 +29,8 @@ class XcParams(ctypes.Structure):
                 ("eps2", ctypes.c_double), ("dense_cutoff", ctypes.c_int), ("dirs", ctypes.c_int),
                 ("weights", _dp), ("device", ctypes.c_int), ("stream", ctypes.c_void_p),
                 ("node_chunk", ctypes.c_int), ("eta", ctypes.c_double), ("n_rows", _i64),
-                ("trig_precompute", ctypes.c_int), ("thresh_mode", ctypes.c_int)]
+                ("trig_precompute", ctypes.c_int), ("thresh_mode", ctypes.c_int),
+                ("apply_path", ctypes.c_int)]
 
 
 class XcInfo(ctypes.Structure):
@@ -184,7 +185,8 @@ class Transform:
     def __init__(self, kind: int, nodes, eps: float, alpha: float = 0.0, beta: float = 0.0,
                  eps1: float = 0.0, eps2: float = 0.0, dense_cutoff: int = 0, dirs: int = XC_DIR_A,
                  weights=None, device: int = 0, node_chunk: int = 0, stream=None, dist=None,
-                 eta: float = 0.0, n_rows: int = 0, trig_precompute: int = 0, thresh_mode: int = 0):
+                 eta: float = 0.0, n_rows: int = 0, trig_precompute: int = 0, thresh_mode: int = 0,
+                 apply_path: int = 0):
         lib = load()
         self._lib = lib
         self.kind = kind
@@ -197,6 +199,7 @@ class Transform:
         p.alpha, p.beta, p.eps1, p.eps2 = alpha, beta, eps1, eps2
         p.dense_cutoff, p.dirs, p.device, p.node_chunk = dense_cutoff, dirs, device, node_chunk
         p.eta, p.n_rows, p.trig_precompute, p.thresh_mode = eta, n_rows, trig_precompute, thresh_mode
+        p.apply_path = apply_path
         self._w = None
         if weights is not None:
             self._w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))

@@ -1199,3 +1199,37 @@ def test_export_lag2d_unsupported(tmp_path):
     with pytest.raises(xc.XcError, match="XC_EUNSUPPORTED"):
         T.export(str(tmp_path / "x.xcop"))
     T.close()
+
+
+SMALL_CASES = [("c1", (O.KIND_JACOBI, 0.0, 0.0), 512, 1, 1e-12, 0),
+               ("c1_ragged", (O.KIND_JACOBI, 0.0, 0.0), 512, 37, 1e-12, 0),
+               ("c2", (O.KIND_COS, 0.0, 0.0), 4096, 64, 1e-10, 1),
+               ("jacobi_2048", (O.KIND_JACOBI, 0.5, -0.3), 2048, 96, 1e-12, 2),
+               ("laguerre_1024", (O.KIND_LAGUERRE, 0.0, 0.0), 1024, 33, 1e-11, 3),
+               ("tiny_N7", (O.KIND_JACOBI, 0.0, 0.0), 7, 3, 1e-12, 4)]
+
+
+@pytest.mark.parametrize("case", SMALL_CASES, ids=[c[0] for c in SMALL_CASES])
+def test_small_path_parity(case):
+    """The small-operator path (apply_path = 2: a bin-major gather, then every block's C2R in
+    shared memory; two launches) and the tiled path (apply_path = 1) both meet 1e-12 against the
+    oracle's compressed apply; auto picks the small path for these operators; column results do
+    not depend on the batch (shards equal the full run bit for bit)."""
+    xc = _xc()
+    name, kt, N, B, eps, seed = case
+    kind = O.Kind(*kt)
+    x, _ = _nodes(kt, N, seed)
+    X = I.rhs(N, B, seed + 300)
+    Ya = O.apply_output_axis(O.compress(O.make_plan(kind, N, eps), x), X)
+    Ys = []
+    for path in (1, 2, 0):
+        T = xc.Transform(kt[0], x, eps, alpha=kt[1], beta=kt[2], apply_path=path)
+        Y = T.apply(_gpu(X))
+        assert O.rel_l2_cols(Y.cpu().numpy(), Ya).max() <= 1e-12, (name, path)
+        if path != 1:
+            assert T.launches(B) == 2
+            if B > 1:
+                assert torch.equal(T.apply(_gpu(X[:, 1:2])), Y[:, 1:2])
+        Ys.append(Y)
+        T.close()
+    assert torch.equal(Ys[1], Ys[2])   # auto = small here
