@@ -23,18 +23,80 @@ namespace {
 using namespace xcb;
 
 // launch 1: rows = every block's bins (complex rows of u) then the tail degrees (real Y rows).
-// A CTA of 256 threads takes RB = 256 / CT rows x CT columns.
+// One launch, two kinds of CTAs (blockIdx.x < nshort: short rows; else long rows):
+// * short rows: a CTA of 256 threads takes RB = 256 / CT rows x CT columns (column tile blockIdx.x %
+//   ntile); with STAGE it first copies its CT columns of X to shared memory (N x CT doubles).  A
+//   thread sums its row's entries in entry order (nodes ascending), the loads of 4 entries issued
+//   ahead of their FMAs (no dependent-load chain per entry);
+// * long rows (more than kSmallLong entries: the dense tail degrees, the bins of the short blocks
+//   that every node touches): one warp per (row, column), lane l sums entries l, l + 32, ... in
+//   order, then a fixed shuffle tree.
+// Either way the order depends on the row only, never on B: a column's bits do not depend on the
+// batch it is applied in.
+template <bool STAGE>
 __global__ void __launch_bounds__(256) small_spmm_k(const SmallOp op, const double* __restrict__ X, int64_t ldx,
                                                     double2* __restrict__ U, int64_t ldu, double* __restrict__ Y,
-                                                    int64_t ldy, int B, int CT) {
+                                                    int64_t ldy, int B, int CT, int N, int nshort, int ntile) {
+  extern __shared__ double xs[];
   const int tid = threadIdx.x;
-  const int r = blockIdx.x * (256 / CT) + tid / CT;
-  const int c = blockIdx.y * CT + tid % CT;
+  if ((int)blockIdx.x >= nshort) {  // long rows
+    const int64_t pair = (int64_t)(blockIdx.x - nshort) * 8 + (tid >> 5);
+    const int lane = tid & 31;
+    if (pair >= (int64_t)op.nlong * B) return;
+    const int r = op.longrows[pair / B];
+    const int c = (int)(pair % B);
+    const int64_t e0 = op.ptr[r], e1 = op.ptr[r + 1];
+    double re = 0.0, im = 0.0;
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const double x = __ldg(X + (int64_t)__ldg(op.node + e) * ldx + c);
+      const double2 v = __ldg(op.val + e);
+      re = fma(v.x, x, re);
+      im = fma(v.y, x, im);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      re += __shfl_xor_sync(0xffffffffu, re, o);
+      im += __shfl_xor_sync(0xffffffffu, im, o);
+    }
+    if (lane == 0) {
+      const int64_t o = op.out[r];
+      if (o >= 0) U[o * ldu + c] = make_double2(re, im);
+      else Y[(-o - 1) * ldy + c] = re;
+    }
+    return;
+  }
+  const int c0 = ((int)blockIdx.x % ntile) * CT;
+  if (STAGE) {
+    for (int i = tid; i < N * CT; i += 256) {
+      const int k = i / CT, lc = i - k * CT;
+      xs[i] = (c0 + lc < B) ? __ldg(X + (int64_t)k * ldx + c0 + lc) : 0.0;
+    }
+    __syncthreads();
+  }
+  const int r = ((int)blockIdx.x / ntile) * (256 / CT) + tid / CT;
+  const int lc = tid % CT, c = c0 + lc;
   if (r >= op.rows || c >= B) return;
   const int64_t e0 = op.ptr[r], e1 = op.ptr[r + 1];
+  if (e1 - e0 > kSmallLong) return;  // a long row
+  auto xv = [&](int k) { return STAGE ? xs[k * CT + lc] : __ldg(X + (int64_t)k * ldx + c); };
   double re = 0.0, im = 0.0;
-  for (int64_t e = e0; e < e1; ++e) {
-    const double x = __ldg(X + (int64_t)__ldg(op.node + e) * ldx + c);
+  int64_t e = e0;
+  for (; e + 4 <= e1; e += 4) {
+    const int k0 = __ldg(op.node + e), k1 = __ldg(op.node + e + 1), k2 = __ldg(op.node + e + 2),
+              k3 = __ldg(op.node + e + 3);
+    const double2 v0 = __ldg(op.val + e), v1 = __ldg(op.val + e + 1), v2 = __ldg(op.val + e + 2),
+                  v3 = __ldg(op.val + e + 3);
+    const double x0 = xv(k0), x1 = xv(k1), x2 = xv(k2), x3 = xv(k3);
+    re = fma(v0.x, x0, re);
+    im = fma(v0.y, x0, im);
+    re = fma(v1.x, x1, re);
+    im = fma(v1.y, x1, im);
+    re = fma(v2.x, x2, re);
+    im = fma(v2.y, x2, im);
+    re = fma(v3.x, x3, re);
+    im = fma(v3.y, x3, im);
+  }
+  for (; e < e1; ++e) {
+    const double x = xv(__ldg(op.node + e));
     const double2 v = __ldg(op.val + e);
     re = fma(v.x, x, re);
     im = fma(v.y, x, im);
@@ -46,7 +108,7 @@ __global__ void __launch_bounds__(256) small_spmm_k(const SmallOp op, const doub
 
 // One Stockham radix-r stage over M points: in -> out, twiddles w_M^{t k M/(Ns r)} from tw (M entries).
 template <int r>
-__device__ __forceinline__ void small_stage(const double2* in, double2* out, const double2* __restrict__ tw, int M,
+__device__ __forceinline__ void small_stage(const double2* in, double2* out, const double2* tw, int M,
                                             int Ns) {
   const int Mr = M / r, step = M / (Ns * r);
   for (int j = threadIdx.x; j < Mr; j += blockDim.x) {
@@ -56,7 +118,7 @@ __device__ __forceinline__ void small_stage(const double2* in, double2* out, con
     for (int t = 0; t < r; ++t) v[t] = in[j + t * Mr];
     if (Ns > 1) {
 #pragma unroll
-      for (int t = 1; t < r; ++t) v[t] = c_mul(v[t], __ldg(tw + (int64_t)t * k * step % M));
+      for (int t = 1; t < r; ++t) v[t] = c_mul(v[t], tw[t * k * step]);
     }
     bfly<r>(v);
     const int d = (j / Ns) * Ns * r + k;
@@ -66,7 +128,7 @@ __device__ __forceinline__ void small_stage(const double2* in, double2* out, con
 }
 
 // launch 2: CTA (block i, column c).  Shared: A (H complex; u, then a ping-pong buffer), Bf (M).
-__global__ void __launch_bounds__(256) small_c2r_k(const SmallBlocks sb, const double2* __restrict__ U, int64_t ldu,
+__global__ void __launch_bounds__(1024) small_c2r_k(const SmallBlocks sb, const double2* __restrict__ U, int64_t ldu,
                                                    double* __restrict__ Y, int64_t ldy) {
   extern __shared__ double2 sm[];
   const SmallBlk b = sb.blk[blockIdx.x];
@@ -74,8 +136,10 @@ __global__ void __launch_bounds__(256) small_c2r_k(const SmallBlocks sb, const d
   const int M = b.M;
   double2* A = sm;
   double2* Bf = sm + b.M + 1;
+  double2* tw = Bf + b.M;  // the stage twiddles e^{2 pi i n / M}, staged once (one coalesced pass)
   const double2* u = U + b.urow * ldu + c;
   for (int q = threadIdx.x; q <= M; q += blockDim.x) A[q] = u[(int64_t)q * ldu];
+  for (int n = threadIdx.x; n < M; n += blockDim.x) tw[n] = __ldg(b.twM + n);
   __syncthreads();
   // pairing: Z[n] = (u_n + conj u_{M-n}) + i e^{i pi n / M} (u_n - conj u_{M-n})
   for (int n = threadIdx.x; n < M; n += blockDim.x) {
@@ -91,13 +155,13 @@ __global__ void __launch_bounds__(256) small_c2r_k(const SmallBlocks sb, const d
   for (int s = 0; s < b.nf; ++s) {
     const int r = b.f[s];
     switch (r) {
-      case 2: small_stage<2>(in, out, b.twM, M, Ns); break;
-      case 3: small_stage<3>(in, out, b.twM, M, Ns); break;
-      case 4: small_stage<4>(in, out, b.twM, M, Ns); break;
-      case 5: small_stage<5>(in, out, b.twM, M, Ns); break;
-      case 6: small_stage<6>(in, out, b.twM, M, Ns); break;
-      case 9: small_stage<9>(in, out, b.twM, M, Ns); break;
-      default: small_stage<8>(in, out, b.twM, M, Ns); break;
+      case 2: small_stage<2>(in, out, tw, M, Ns); break;
+      case 3: small_stage<3>(in, out, tw, M, Ns); break;
+      case 4: small_stage<4>(in, out, tw, M, Ns); break;
+      case 5: small_stage<5>(in, out, tw, M, Ns); break;
+      case 6: small_stage<6>(in, out, tw, M, Ns); break;
+      case 9: small_stage<9>(in, out, tw, M, Ns); break;
+      default: small_stage<8>(in, out, tw, M, Ns); break;
     }
     Ns *= r;
     __syncthreads();
@@ -115,13 +179,23 @@ __global__ void __launch_bounds__(256) small_c2r_k(const SmallBlocks sb, const d
 }  // namespace
 
 xc_status small_spmm(const SmallOp& op, const double* X, int64_t ldx, double2* U, int64_t ldu, double* Y, int64_t ldy,
-                     int B, cudaStream_t st) {
+                     int B, int N, cudaStream_t st) {
   int CT = 1;
   while (CT < 32 && CT < B) CT *= 2;
-  for (int c0 = 0; c0 < B; c0 += 65535 * CT) {  // grid.y limit
-    const int bc = std::min(B - c0, 65535 * CT);
-    dim3 g1((op.rows + 256 / CT - 1) / (256 / CT), (bc + CT - 1) / CT);
-    small_spmm_k<<<g1, 256, 0, st>>>(op, X + c0, ldx, U + c0, ldu, Y + c0, ldy, bc, CT);
+  // stage the CTA's columns of X in shared memory when they fit 48 KB (c1: 4 KB), else L1/L2
+  const bool stage = (size_t)N * CT * sizeof(double) <= 48 * 1024;
+  for (int c0 = 0; c0 < B; c0 += 65535) {  // keeps the 1D grid small
+    const int bc = std::min(B - c0, 65535);
+    const int ntile = (bc + CT - 1) / CT;
+    const int64_t nshort = (int64_t)((op.rows + 256 / CT - 1) / (256 / CT)) * ntile;
+    const int64_t nlong = ((int64_t)op.nlong * bc + 7) / 8;
+    const unsigned grid = (unsigned)(nshort + nlong);
+    if (stage)
+      small_spmm_k<true><<<grid, 256, (size_t)N * CT * sizeof(double), st>>>(op, X + c0, ldx, U + c0, ldu, Y + c0,
+                                                                              ldy, bc, CT, N, (int)nshort, ntile);
+    else
+      small_spmm_k<false><<<grid, 256, 0, st>>>(op, X + c0, ldx, U + c0, ldu, Y + c0, ldy, bc, CT, N, (int)nshort,
+                                                 ntile);
     XC_CUDA(cudaGetLastError());
   }
   return XC_OK;
@@ -130,13 +204,14 @@ xc_status small_spmm(const SmallOp& op, const double* X, int64_t ldx, double2* U
 xc_status small_c2r(const SmallBlocks& sb, const double2* U, int64_t ldu, double* Y, int64_t ldy, int B,
                     cudaStream_t st) {
   if (sb.nb == 0) return XC_OK;
-  const size_t smem = (size_t)(2 * sb.maxM + 1) * sizeof(double2);
+  const size_t smem = (size_t)(3 * sb.maxM + 1) * sizeof(double2);
   static std::atomic<unsigned long long> once{0};
   if (first_on_device(once))
     XC_CUDA(cudaFuncSetAttribute(small_c2r_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (2 * kSmallMaxM + 1) * (int)sizeof(double2)));
+                                 (3 * kSmallMaxM + 1) * (int)sizeof(double2)));
+  const int nth = sb.maxM >= 2048 ? 1024 : (sb.maxM >= 512 ? 512 : 256);  // one CTA per column: latency
   for (int c0 = 0; c0 < B; c0 += 65535) {  // grid.y limit
-    small_c2r_k<<<dim3(sb.nb, std::min(B - c0, 65535)), 256, smem, st>>>(sb, U + c0, ldu, Y + c0, ldy);
+    small_c2r_k<<<dim3(sb.nb, std::min(B - c0, 65535)), nth, smem, st>>>(sb, U + c0, ldu, Y + c0, ldy);
     XC_CUDA(cudaGetLastError());
   }
   return XC_OK;

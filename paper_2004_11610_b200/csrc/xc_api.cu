@@ -129,7 +129,7 @@ struct xc_op {
   int thresh_mode = 0;  // 0: per-node relative threshold (R-3); 1: global
   int apply_path = 0;   // xc_params.apply_path: 0 auto, 1 tiled, 2 small (two launches)
   bool small_on = false;   // XC_DIR_A runs the small-operator path (small.cu)
-  DevBuf sm_ptr, sm_node, sm_val, sm_out, sm_twM;  // its bin-major operator and stage twiddles
+  DevBuf sm_ptr, sm_node, sm_val, sm_out, sm_twM, sm_long;  // its bin-major operator and stage twiddles
   SmallOp sm_op{};
   SmallBlocks sm_blocks{};
   std::vector<double> user_nodes, user_wt;  // the caller's nodes / weights (xc_export)
@@ -347,9 +347,7 @@ int64_t count_launches(const xc_op* h, int dir, int64_t B) {
     return n + 1 + (h->bsr_nred > 0 ? 1 : 0) + (h->tail > 0 ? 2 + (h->N > 128 ? 1 : 0) : 0);
   }
   if (dir == XC_DIR_A && h->small_on) {  // small_spmm / small_c2r grid.y chunks
-    int64_t ct = 1;
-    while (ct < 32 && ct < B) ct *= 2;
-    return (B + 65535 * ct - 1) / (65535 * ct) + (B + 65534) / 65535;
+    return 2 * ((B + 65534) / 65535);
   }
   if (dir == XC_DIR_A) {
     if (!(h->dirs & XC_DIR_A)) return 0;
@@ -1221,8 +1219,11 @@ xc_status build_small(xc_op* h, cudaStream_t st) {
   if (h->apply_path == 1 || !(h->dirs & XC_DIR_A) || h->kind == XC_EXP || h->ukind == XC_LAG2D) return XC_OK;
   bool ok = (int)h->blocks.size() <= kSmallMaxBlocks;
   int64_t ents = (int64_t)h->tail * h->N;
+  // auto: blocks with M <= 1024 (c1); a longer block (c2: M = 3600) is faster on the tiled path
+  // (two C2R passes spread over the SMs beat one shared-memory FFT per CTA and column: 27 vs 33 us)
+  const int maxM = h->apply_path == 2 ? kSmallMaxM : 1024;
   for (auto& b : h->blocks) {
-    ok = ok && b.L / 2 <= kSmallMaxM;
+    ok = ok && b.L / 2 <= maxM;
     ents += b.nnz;
   }
   ok = ok && ents <= (4LL << 20);
@@ -1283,8 +1284,12 @@ xc_status build_small(xc_op* h, cudaStream_t st) {
   XC_TRY(upload(h->sm_node, node));
   XC_TRY(upload(h->sm_val, val));
   XC_TRY(upload(h->sm_out, out));
+  std::vector<int> lr;
+  for (int r = 0; r < rows; ++r)
+    if (ptr[r + 1] - ptr[r] > kSmallLong) lr.push_back(r);
+  XC_TRY(upload(h->sm_long, lr));
   h->sm_op = SmallOp{(const int64_t*)h->sm_ptr.p, (const int*)h->sm_node.p, (const double2*)h->sm_val.p,
-                     (const int64_t*)h->sm_out.p, rows};
+                     (const int64_t*)h->sm_out.p, rows, (const int*)h->sm_long.p, (int)lr.size()};
   // stage twiddles e^{+2 pi i n / M} of every block, concatenated
   std::vector<double2> tw;
   std::vector<size_t> twoff;
@@ -1829,7 +1834,7 @@ xc_status apply_impl(xc_op* h, Ws& w, xc_dir dir, const double* X, int64_t ldx, 
     return mark(3);
   }
   if (dir == XC_DIR_A && h->small_on) {  // small operators: two launches (small.cu)
-    XC_TRY(small_spmm(h->sm_op, X, ldx, (double2*)w.partA, Bp, Y, ldy, (int)B, st));
+    XC_TRY(small_spmm(h->sm_op, X, ldx, (double2*)w.partA, Bp, Y, ldy, (int)B, N, st));
     XC_TRY(mark(1));
     XC_TRY(small_c2r(h->sm_blocks, (const double2*)w.partA, Bp, Y, ldy, (int)B, st));
     XC_TRY(mark(2));
@@ -2006,7 +2011,7 @@ void destroy_impl(xc_op* h) {
                    &h->tailR, &h->tailC, &h->ptr2d, &h->ent2d, &h->order2d,
                    &h->bsr_sptr, &h->bsr_r4, &h->bsr_tiles, &h->bsr_srow, &h->bsr_snv, &h->bsr_sslot,
                    &h->bsr_order, &h->bsr_rrow, &h->bsr_rnv, &h->bsr_rslot, &h->bsr_rcnt,
-                   &h->sm_ptr, &h->sm_node, &h->sm_val, &h->sm_out, &h->sm_twM};
+                   &h->sm_ptr, &h->sm_node, &h->sm_val, &h->sm_out, &h->sm_twM, &h->sm_long};
   for (DevBuf* b : all) dev_free(*b);
 }
 

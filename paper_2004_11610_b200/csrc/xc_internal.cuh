@@ -347,7 +347,10 @@ struct SmallOp {
   const double2* val;   // S_i[k, q] (block bins) or (phi_j(x_k), 0) (tail degrees)
   const int64_t* out;   // >= 0: complex u row (double2 units, ld = ldu); < 0: tail degree -out-1
   int rows;
+  const int* longrows;  // rows with more than kSmallLong entries (one warp each)
+  int nlong;
 };
+constexpr int kSmallLong = 64;
 struct SmallBlk {
   int M, nf, f[16];
   int m_off, keep_lo, keep_hi;
@@ -361,7 +364,7 @@ struct SmallBlocks {
   int nb, maxM;
 };
 xc_status small_spmm(const SmallOp& op, const double* X, int64_t ldx, double2* U, int64_t ldu, double* Y, int64_t ldy,
-                     int B, cudaStream_t st);
+                     int B, int N, cudaStream_t st);
 xc_status small_c2r(const SmallBlocks& sb, const double2* U, int64_t ldu, double* Y, int64_t ldy, int B,
                     cudaStream_t st);
 bool small_radices(int M, int* f, int& nf);
