@@ -533,6 +533,7 @@ struct Spec {
 // BIG (512 threads, 64 KB tiles, 1 CTA / SM): the longest passes, so that a tile row is >= 128 B
 const Spec kSpecs[] = {
     XC_BIG(0, 200, 4),
+    XC_BIG(1, 432, 3), XC_BIG(1, 512, 3),  // second passes of M = 86400 = 200 x 432, 27648 = 54 x 512 (N = 131072)
     XC_SPEC(1, 216, 3), XC_SPEC(0, 54, 5),  XC_SPEC(1, 256, 3), XC_SPEC(0, 45, 5), XC_SPEC(1, 100, 4),
     XC_SPEC(0, 27, 6),  XC_SPEC(1, 54, 5),  XC_SPEC(1, 240, 3), XC_SPEC(1, 64, 5), XC_SPEC(0, 32, 6),
     XC_SPEC(0, 36, 5),  XC_SPEC(0, 9, 7),
@@ -549,20 +550,36 @@ const Spec kSpecs[] = {
 
 }  // namespace
 
-bool c2r_has_big(int mode, int R) {
+namespace {
+bool has_big(int mode, int R);
+}
+
+bool c2r_has_big(int mode, int R) { return has_big(mode, R); }
+
+bool c2r_has_spec(int mode, int R) {
   for (const Spec& sp : kSpecs)
-    if (sp.mode == mode && sp.R == R && sp.big) return true;
+    if (sp.mode == mode && sp.R == R) return true;
   return false;
 }
 
 namespace {
 
+// Big tiles (512 threads, 4096 points) for pass `mode` of length R: where a specialised big kernel
+// exists, and for the lengths the specialised kernels do not cover whenever the 2048-point tile
+// would leave rows narrower than 8 columns (128 B; R > 128 with paired sub-sequences, R > 256
+// otherwise): the generic big kernel then doubles the row width (the passes' HBM throughput tracks
+// it: 64 B rows 2.35 TB/s, 128 B 3.7 TB/s; tools/stride_probe.cu).
 bool has_big(int mode, int R) {
   static const bool off = getenv("XC_C2R_GENERIC") || getenv("XC_C2R_NOBIG");  // measurement switches
   if (off) return false;
+  bool spec = false;
   for (const Spec& sp : kSpecs)
-    if (sp.mode == mode && sp.R == R && sp.big) return true;
-  return false;
+    if (sp.mode == mode && sp.R == R) {
+      if (sp.big) return true;
+      spec = true;
+    }
+  if (spec || mode == 2) return false;
+  return R > (mode == 0 ? 128 : 256);
 }
 
 template <int MODE>
@@ -570,6 +587,7 @@ xc_status launch(C2RArgs& a, const FftIO& io, cudaStream_t st) {
   static std::atomic<unsigned long long> once{0};
   if (first_on_device(once)) {
     XC_CUDA(cudaFuncSetAttribute(c2r_pass<MODE, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    XC_CUDA(cudaFuncSetAttribute(c2r_pass<MODE, 0, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     for (const Spec& sp : kSpecs)
       if (sp.mode == MODE)
         XC_CUDA(cudaFuncSetAttribute((const void*)sp.k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -591,8 +609,8 @@ xc_status launch(C2RArgs& a, const FftIO& io, cudaStream_t st) {
     xc_set_error("c2r: tile does not fit shared memory");
     return XC_EUNSUPPORTED;
   }
-  C2RKernel k = (C2RKernel)c2r_pass<MODE, 0, 0>;
-  int nt = NTH;
+  C2RKernel k = a.big ? (C2RKernel)c2r_pass<MODE, 0, 0, 1> : (C2RKernel)c2r_pass<MODE, 0, 0>;
+  int nt = a.big ? 2 * NTH : NTH;
   static const bool generic = getenv("XC_C2R_GENERIC") != nullptr;
   if (!generic)
     for (const Spec& sp : kSpecs)
@@ -601,7 +619,7 @@ xc_status launch(C2RArgs& a, const FftIO& io, cudaStream_t st) {
         nt = sp.big ? 2 * NTH : NTH;
       }
   static const bool log_generic = getenv("XC_C2R_LOG") != nullptr;  // which passes run generic
-  if (log_generic && k == (C2RKernel)c2r_pass<MODE, 0, 0>)
+  if (log_generic && (k == (C2RKernel)c2r_pass<MODE, 0, 0> || k == (C2RKernel)c2r_pass<MODE, 0, 0, 1>))
     fprintf(stderr, "c2r generic: mode %d R %d lgn %d big %d\n", MODE, a.R, a.lgn, a.big);
   if (a.big && nt == NTH) {
     xc_set_error("c2r: big tile without a big kernel");

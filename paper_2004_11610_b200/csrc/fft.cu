@@ -395,7 +395,7 @@ double c2r_pass_cost(int R, int smin, int mode) {
         if (e0min + b * estep < Rr) warps += 1;
       }
   }
-  return warps * 32.0 / ((double)R * nseq) * pen;
+  return warps * 32.0 / ((double)R * nseq) * pen * (c2r_has_spec(mode, R) ? 1.0 : 1.4);
 }
 
 xc_status fft_plan_make(FftPlan& p, int L, bool c2r) {
@@ -407,8 +407,10 @@ xc_status fft_plan_make(FftPlan& p, int L, bool c2r) {
     int best = -1;
     if (c2r) {  // the split with the cheapest pair of C2R passes (first pass pairs sub-sequences)
       double bc = 1e30;
+      // first pass (paired sub-sequences) <= 256 points, second <= 512: every M up to 131072
+      // splits (c5 at N = 131072: M = 86400 = 200 x 432, both passes on 128-B tile rows)
       for (int d = 2; d <= 256; ++d) {
-        if (L % d || L / d > 256) continue;
+        if (L % d || L / d > 512) continue;
         const double c = c2r_pass_cost(d, 2, 0) + c2r_pass_cost(L / d, 1, 1);
         if (c < bc - 1e-9) {
           bc = c;

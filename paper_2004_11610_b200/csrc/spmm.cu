@@ -42,8 +42,7 @@ constexpr int WARPS = XC_WARPS;  // warps per CTA
 template <int NT>
 __global__ void __launch_bounds__(WARPS * 32, 2)
     spmm_win(const SpmmWin* __restrict__ wins, const SpmmItem* __restrict__ items,
-             const double* __restrict__ tiles, SpmmSrcs srcs, double* __restrict__ part, int64_t ldp, int ncols,
-             int pf) {
+             const double* __restrict__ tiles, SpmmSrcs srcs, double* __restrict__ part, int64_t ldp, int ncols) {
   constexpr int CW = 8 * NT;   // columns per tile
   constexpr int CWP = CW + 4;  // padded smem row: the 4 rows of a B fragment fall in distinct banks
   extern __shared__ double2 xs2[];
@@ -110,14 +109,6 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
   const int iw0 = W.i0 + __ldg(&wins[blockIdx.y].wo[warp]), iw1 = W.i0 + __ldg(&wins[blockIdx.y].wo[warp + 1]);
   for (int ii = iw0; ii < iw1; ++ii) {
     const SpmmItem it = its[ii - W.i0];
-    // the next item's first two A steps into L1 while this item runs (its loads then hit L1 instead
-    // of waiting an L2 round trip at the item start; the later steps are 4 steps ahead anyway)
-    if (ii + 1 < iw1 && pf) {
-      const SpmmItem& nx = its[ii + 1 - W.i0];
-      const double2* np = reinterpret_cast<const double2*>(tiles + nx.a_off) + lane;
-      if (nx.nsteps > 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(np));
-      if (nx.nsteps > 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(np + 32));
-    }
     double acc[2][NT][2];
 #pragma unroll
     for (int m = 0; m < 2; ++m)
@@ -254,8 +245,7 @@ xc_status launch(const SpmmWin* wins, int nwins, const SpmmItem* items, const do
   for (int w0 = 0; w0 < nwins; w0 += 65535) {
     int nw = std::min(65535, nwins - w0);
     dim3 grid((ncols + 8 * NT - 1) / (8 * NT), nw);
-    static const int pf = getenv("XC_SPMM_NOPF") ? 0 : 1;  // measurement switch (next-item prefetch)
-    spmm_win<NT><<<grid, WARPS * 32, sm, st>>>(wins + w0, items, tiles, srcs, part, ldp, ncols, pf);
+    spmm_win<NT><<<grid, WARPS * 32, sm, st>>>(wins + w0, items, tiles, srcs, part, ldp, ncols);
     XC_CUDA(cudaGetLastError());
   }
   return XC_OK;

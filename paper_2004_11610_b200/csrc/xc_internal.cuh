@@ -195,6 +195,9 @@ int64_t c2r_chunk_cols(const FftPlan& p, int64_t ncol);
 xc_status c2r_prepare(const FftPlan& p);
 // 1 if c2r.cu has a 512-thread big-tile kernel for this pass (mode 0 first / 1 second) and length
 bool c2r_has_big(int mode, int R);
+// 1 if c2r.cu has a compile-time specialised kernel for this pass and length (the generic one runs
+// ~1.4x the instructions)
+bool c2r_has_spec(int mode, int R);
 
 // ---------------------------------------------------------------------------
 // SpMM on the FP64 tensor cores (spmm.cu)
