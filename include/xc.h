@@ -262,6 +262,13 @@ xc_status xc_reserve(xc_handle h, int64_t B);
  * the two-pass inverse DFTs run in column chunks, so the count grows with B). */
 xc_status xc_launches(xc_handle h, xc_dir dir, int64_t B, int64_t* n);
 
+/* Debug aid (the GPU pool's compute-sanitizer is closed): with the environment variable
+ * XC_WS_GUARD=1 set before the first call, every workspace part is followed by a 64 KB guard zone
+ * filled with 0x7F when it is carved; this synchronises the device and returns in *bad the number
+ * of guard bytes some kernel overwrote (0: no write past a workspace part) and in *checked (may be
+ * NULL) the guard bytes examined (0 when guards are off). */
+xc_status xc_debug_guards(xc_handle h, int64_t* bad, int64_t* checked);
+
 /* Bytes of workspace xc_apply needs for B right-hand sides (what xc_attach_workspace must get). */
 xc_status xc_workspace_query(xc_handle h, int64_t B, size_t* bytes);
 

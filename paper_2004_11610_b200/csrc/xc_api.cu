@@ -120,6 +120,7 @@ struct Ws {
   cudaEvent_t ev_fork = nullptr, ev_join[kAux] = {};
   int naux = 2;               // forked streams of the current apply (naux_for)
   std::vector<GraphEntry> graphs;
+  std::vector<std::pair<size_t, size_t>> guards;  // debug guard zones (XC_WS_GUARD): offset, bytes
 };
 
 struct xc_op {
@@ -236,13 +237,27 @@ size_t block_scratch(const xc_op* h, const BlockData& b, int64_t B) {
 
 // The workspace of B columns: part sizes in carve order (256-byte aligned), total returned.  With
 // w and base it also sets w's pointers into [base, base + total).  xc_workspace_query is this total.
+// Debug guard zones (XC_WS_GUARD=1, read once): kGuard bytes after every workspace part, filled with
+// 0x7F at carve time; xc_debug_guards counts the bytes a kernel overwrote (an out-of-bounds write
+// past a part).  compute-sanitizer is closed on the GPU pool, so this is the write check the tests run.
+constexpr size_t kGuard = 64 * 1024;
+bool ws_guard() {
+  static const bool on = getenv("XC_WS_GUARD") && atoi(getenv("XC_WS_GUARD")) != 0;
+  return on;
+}
+
 size_t ws_layout(const xc_op* h, int64_t B, Ws* w, char* base) {
   const int64_t Bp = pad_cols(B);
   const bool two_d = h->ukind == XC_LAG2D;
   size_t off = 0;
+  std::vector<std::pair<size_t, size_t>> guards;
   auto take = [&](size_t bytes) -> char* {
     char* p = base ? base + off : nullptr;
     off += (std::max<size_t>(bytes, 16) + 255) / 256 * 256;
+    if (ws_guard()) {
+      guards.push_back({off, kGuard});
+      off += kGuard;
+    }
     return p;
   };
   size_t scr = 1;
@@ -287,6 +302,7 @@ size_t ws_layout(const xc_op* h, int64_t B, Ws* w, char* base) {
     w->partW = p_partW;
     w->zpl = p_zpl;
     w->zoff = zoff;
+    w->guards = guards;
   }
   return off;
 }
@@ -314,6 +330,7 @@ xc_status ws_carve(const xc_op* h, Ws& w, int64_t B) {
   }
   ws_layout(h, B, &w, w.base);
   w.B = B;
+  for (auto& g : w.guards) XC_CUDA(cudaMemset(w.base + g.first, 0x7F, g.second));  // debug mode only
   clear_graphs(w);  // captured graphs reference the old layout
   return XC_OK;
 }
@@ -2776,6 +2793,27 @@ xc_status xc_reserve(xc_handle h, int64_t B) {
   if (!h || B < 1) return XC_EINVAL;
   XC_CUDA(cudaSetDevice(h->device));
   return ensure_ws(h, B);
+}
+
+xc_status xc_debug_guards(xc_handle h, int64_t* bad, int64_t* checked) {
+  if (!h || !bad) return XC_EINVAL;
+  XC_CUDA(cudaSetDevice(h->device));
+  XC_CUDA(cudaDeviceSynchronize());
+  int64_t nb = 0, nc = 0;
+  std::vector<unsigned char> buf;
+  std::lock_guard<std::mutex> lk(h->att_mu);
+  std::vector<Ws*> all{&h->def};
+  for (Ws* w : h->att) all.push_back(w);
+  for (Ws* w : all)
+    for (auto& g : w->guards) {
+      buf.resize(g.second);
+      XC_CUDA(cudaMemcpy(buf.data(), w->base + g.first, g.second, cudaMemcpyDeviceToHost));
+      for (unsigned char c : buf) nb += c != 0x7F;
+      nc += (int64_t)g.second;
+    }
+  *bad = nb;
+  if (checked) *checked = nc;
+  return XC_OK;
 }
 
 xc_status xc_launches(xc_handle h, xc_dir dir, int64_t B, int64_t* n) {

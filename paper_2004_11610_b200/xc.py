@@ -53,6 +53,7 @@ class XcBlockInfo(ctypes.Structure):
 
 EXPORTS = ["xc_params_default", "xc_build_compressed", "xc_build_from_bands", "xc_build_local", "xc_build_step", "xc_apply", "xc_c2r_check", "xc_set_graphs", "xc_apply_host", "xc_apply_host_async", "xc_host_wait", "xc_reserve",
            "xc_attach_workspace", "xc_launches", "xc_export", "xc_import",
+           "xc_debug_guards",
            "xc_workspace_query", "xc_info", "xc_block_info", "xc_block_window", "xc_node_spectrum",
            "xc_gauss_rule", "xc_plan_chain", "xc_profile_enable", "xc_profile_read", "xc_destroy",
            "xc_last_error", "xc_version"]
@@ -93,6 +94,7 @@ def load():
     lib.xc_attach_workspace.argtypes = [vp, vp, vp, ctypes.c_size_t]
     lib.xc_launches.argtypes = [vp, ctypes.c_int, _i64, ctypes.POINTER(_i64)]
     lib.xc_export.argtypes = [vp, ctypes.c_char_p]
+    lib.xc_debug_guards.argtypes = [vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]
     lib.xc_import.argtypes = [ctypes.c_char_p, ctypes.POINTER(XcParams), ctypes.POINTER(vp)]
     lib.xc_workspace_query.argtypes = [vp, _i64, ctypes.POINTER(ctypes.c_size_t)]
     lib.xc_info.argtypes = [vp, ctypes.POINTER(XcInfo)]
@@ -391,6 +393,12 @@ class Transform:
         _check(self._lib.xc_attach_workspace(self._h, ctypes.c_void_p(stream), ctypes.c_void_p(ws.data_ptr()),
                                              nbytes))
         self._attached[stream] = ws   # keep the memory alive while attached
+
+    def debug_guards(self):
+        """xc_debug_guards: (overwritten guard bytes, guard bytes checked); needs XC_WS_GUARD=1."""
+        bad, chk = _i64(), _i64()
+        _check(self._lib.xc_debug_guards(self._h, ctypes.byref(bad), ctypes.byref(chk)))
+        return bad.value, chk.value
 
     def launches(self, B: int, direction: int = XC_DIR_A) -> int:
         """Kernel launches one xc_apply of B columns makes (xc_launches)."""

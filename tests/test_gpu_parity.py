@@ -209,22 +209,34 @@ def test_determinism_and_sharding():
     T.close()
 
 
-def test_strided_and_host_api():
-    """ldx, ldy > B (strided views) and the host-buffer entry point give the same numbers."""
+@pytest.mark.parametrize("which", ["small", "tiled", "laguerre_wat", "exp_wat"])
+def test_strided_and_host_api(which):
+    """ldx, ldy > B (strided views) and the host-buffer entry point give the same numbers, and no
+    kernel writes outside Y's B columns (the sentinel padding around them stays untouched) -- on the
+    small-operator path, the tiled path, the input axis and the complex kind."""
     xc = _xc()
-    kt = (O.KIND_JACOBI, 0.0, 0.0)
-    N, B = 512, 24
-    x, _ = _nodes(kt, N, 0)
-    Xn = I.rhs(N, B, 1)
-    T = xc.Transform(xc.XC_JACOBI, x, 1e-12)
-    Y = T.apply(_gpu(Xn)).cpu().numpy()
-    big = torch.zeros((N, 40), dtype=torch.float64, device="cuda")
+    N, B, d = 512, 24, xc.XC_DIR_A
+    if which in ("small", "tiled"):
+        x, _ = _nodes((O.KIND_JACOBI, 0.0, 0.0), N, 0)
+        T = xc.Transform(xc.XC_JACOBI, x, 1e-12, apply_path=2 if which == "small" else 1)
+    elif which == "laguerre_wat":
+        x, wt = _nodes((O.KIND_LAGUERRE, 0.0, 0.0), N, 3)
+        T = xc.Transform(xc.XC_LAGUERRE, x, 1e-11, dirs=xc.XC_DIR_A | xc.XC_DIR_WAT, weights=wt)
+        d = xc.XC_DIR_WAT
+    else:
+        T = xc.Transform(xc.XC_EXP, I.exp_nodes(N, 4), 1e-12, dirs=xc.XC_DIR_A | xc.XC_DIR_WAT,
+                         weights=np.ones(N))
+        d = xc.XC_DIR_WAT
+    rin, rout = T.rows(d)
+    Xn = I.rhs(rin, B, 1)
+    Y = T.apply(_gpu(Xn), d).cpu().numpy()
+    big = torch.zeros((rin, 40), dtype=torch.float64, device="cuda")
     big[:, 3:3 + B] = _gpu(Xn)
-    out = torch.full((N, 50), 7.0, dtype=torch.float64, device="cuda")
-    T.apply(big[:, 3:3 + B], out=out[:, 5:5 + B])
+    out = torch.full((rout, 50), 7.0, dtype=torch.float64, device="cuda")
+    T.apply(big[:, 3:3 + B], d, out=out[:, 5:5 + B])
     assert np.array_equal(out[:, 5:5 + B].cpu().numpy(), Y)
     assert torch.all(out[:, :5] == 7.0) and torch.all(out[:, 5 + B:] == 7.0)
-    Yh = T.apply_host(Xn)
+    Yh = T.apply_host(Xn, d)
     assert np.array_equal(Yh, Y)
     T.close()
 
@@ -1236,3 +1248,18 @@ def test_small_path_parity(case):
         Ys.append(Y)
         T.close()
     assert torch.equal(Ys[2], Ys[1]) or torch.equal(Ys[2], Ys[0])   # auto = one of the two paths
+
+
+def test_workspace_guard_zones():
+    """No kernel writes past a workspace part (compute-sanitizer is closed on the GPU pool): every
+    case of tools/sanitize_cases.py -- all kinds, both directions, the small and tiled paths, the 2D
+    method, degenerate sizes, an attached workspace and the host pipeline, each at its batch and at
+    B = 1 -- runs with XC_WS_GUARD=1 (64 KB guard zones after every part) and leaves them intact."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, XC_WS_GUARD="1")
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "sanitize_cases.py")], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "all cases done" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])

@@ -3,8 +3,11 @@
 # usage: PYTEST_K="expr" VARIANTS="XC_C2R_CHUNK_MB=0;XC_C2R_CHUNK_MB=20" tools/gpu_iter.sh [bench args]
 mkdir -p gpurun_out
 if [ -n "$PYTEST_K" ]; then
-  if [ "$PYTEST_K" = "all" ]; then K=""; else K="-k $PYTEST_K"; fi
-  timeout 1800 python -m pytest tests -m gpu -x -q -p no:cacheprovider $K > gpurun_out/pytest_iter.log 2>&1; echo "pytest rc=$?"
+  if [ "$PYTEST_K" = "all" ]; then
+    timeout 1800 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_iter.log 2>&1; echo "pytest rc=$?"
+  else
+    timeout 1800 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "$PYTEST_K" > gpurun_out/pytest_iter.log 2>&1; echo "pytest rc=$?"
+  fi
   tail -4 gpurun_out/pytest_iter.log
 fi
 timeout 300 python bench.py --steps 20 --warmup 5 --e2e-steps 0 --no-cpu-baseline "$@" > gpurun_out/bench_iter.json 2> gpurun_out/bench_iter.err; echo "bench rc=$?"

@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""Small cases of every kernel family for compute-sanitizer (memcheck / racecheck / synccheck):
+"""Small cases of every kernel family (for compute-sanitizer where it is open; on the B200 pool it is
+closed, so with XC_WS_GUARD=1 every case also checks the workspace guard zones, xc_debug_guards):
 Legendre c1 (B = 1) and a reduced c3 (block chain, split-K, tail, forked streams), both directions
 of Laguerre, the exp and spectral-Laguerre kinds (complex SpMM, C2C), the 2D block method, the
 Appendix-A precompute, the global threshold, degenerate sizes N = 2..64, the host-buffer pipeline,
@@ -16,17 +17,32 @@ from paper_2004_11610_b200 import inputs as I  # noqa: E402
 from paper_2004_11610_b200 import xc  # noqa: E402
 
 
+GUARD = os.environ.get("XC_WS_GUARD") == "1"
+
+
+def check_guards(name, T):
+    if GUARD:
+        bad, checked = T.debug_guards()
+        assert checked > 0 and bad == 0, (name, bad, checked)
+
+
 def run(name, T, X, dirs=(xc.XC_DIR_A,)):
     for d in dirs:
-        Y = T.apply(torch.from_numpy(X).cuda(), d)
-        torch.cuda.synchronize()
-        assert torch.isfinite(Y).all(), name
+        for path_B in (X.shape[1], 1):   # the batch, then one column (other grid shapes)
+            Y = T.apply(torch.from_numpy(np.ascontiguousarray(X[:, :path_B])).cuda(), d)
+            torch.cuda.synchronize()
+            assert torch.isfinite(Y).all(), name
+    check_guards(name, T)
     print("ok", name, flush=True)
 
 
 def main():
     x, w, wt = xc.gauss_rule(xc.XC_JACOBI, 512)
     run("c1", xc.Transform(xc.XC_JACOBI, x, 1e-12), I.rhs(512, 1, 0))
+    run("c1_tiled", xc.Transform(xc.XC_JACOBI, x, 1e-12, apply_path=1), I.rhs(512, 33, 0))
+    x2 = I.cos_nodes(4096, 1)
+    run("c2", xc.Transform(xc.XC_COS, x2, 1e-10), I.rhs(4096, 64, 1))
+    run("c2_small", xc.Transform(xc.XC_COS, x2, 1e-10, apply_path=2), I.rhs(4096, 70, 1))
     x, w, wt = xc.gauss_rule(xc.XC_JACOBI, 2048, 0.5, -0.3)
     T = xc.Transform(xc.XC_JACOBI, x, 1e-12, alpha=0.5, beta=-0.3, dirs=3, weights=w)
     run("c3_reduced", T, I.rhs(2048, 96, 2), (1, 2))
@@ -35,10 +51,13 @@ def main():
     T.attach_workspace(s.cuda_stream, ws)
     Y = T.apply(torch.from_numpy(I.rhs(2048, 96, 3)).cuda(), stream=s.cuda_stream)
     torch.cuda.synchronize()
+    check_guards("attached_workspace", T)
     print("ok attached_workspace", flush=True)
     Xh = I.rhs(2048, 130, 4)
     Yh = T.apply_host(Xh)
-    print("ok host_pipeline", np.isfinite(Yh).all(), flush=True)
+    assert np.isfinite(Yh).all()
+    check_guards("host_pipeline", T)
+    print("ok host_pipeline", flush=True)
     x, w, wt = xc.gauss_rule(xc.XC_LAGUERRE, 1024)
     run("laguerre_both", xc.Transform(xc.XC_LAGUERRE, x, 1e-11, dirs=3, weights=wt), I.rhs(1024, 40, 3), (1, 2))
     t = I.exp_nodes(96, 2)
