@@ -344,9 +344,7 @@ xc_status ensure_ws(xc_op* h, int64_t B) {
   XC_TRY(dev_alloc(h->def.own, need));
   h->def.base = (char*)h->def.own.p;
   h->def.bytes = need;
-  XC_TRY(ws_carve(h, h->def, B));
-  if (h->def.zpl && h->ukind == XC_LAG2D)  // finite padding rows (read by the DMMA blocks, times 0)
-    XC_CUDA(cudaMemset(h->def.zpl, 0, need - (size_t)((char*)h->def.zpl - h->def.base)));
+  XC_TRY(ws_carve(h, h->def, B));  // (the 2D padding rows are zeroed by every apply)
   return XC_OK;
 }
 
