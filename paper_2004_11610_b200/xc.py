@@ -176,6 +176,21 @@ def nccl_allgather(group=None):
     return ag
 
 
+def host_allgather(group=None):
+    """The same exchange through host memory (a gloo process group): device send -> host, all-gather,
+    host -> device recv.  For process groups without a GPU transport (tests of two processes on
+    one GPU; no kernel waits on another process, the exchange is host-mediated)."""
+    import torch
+    import torch.distributed as dist
+
+    def ag(send, recv):
+        h = send.cpu()
+        parts = [torch.empty_like(h) for _ in range(dist.get_world_size(group))]
+        dist.all_gather(parts, h, group=group)
+        recv.copy_(torch.cat(parts).to(recv.device))
+    return ag
+
+
 class Transform:
     """A compressed special-function transform (handle of xc_build_compressed).
 

@@ -792,12 +792,14 @@ def test_lag2d_errors():
 
 @pytest.mark.parametrize("L,B", [(86400, 64), (27648, 64), (9000, 96), (2916, 64), (960, 64), (360, 8),
                                  (21600, 32), (10800, 64), (7200, 64), (1152, 40), (720, 1), (60, 3),
-                                 (172800, 64), (55296, 64), (43200, 72), (36000, 64), (262144, 16)])
+                                 (172800, 64), (55296, 64), (43200, 72), (36000, 64), (262144, 16),
+                                 (86400, 128), (86400, 160), (86400, 1024), (172800, 256)])
 def test_c2r_engine_vs_numpy(L, B):
     """The output-axis inverse DFT engine (c2r.cu) alone at the block lengths of c1-c5 -- including
     the specialised and big-tile passes of c5 (86400 = 2 x 200 x 216, 27648, 9000, 2916), the off-config
     lengths of N = 131072 (172800 = 2 x 200 x 432, 55296 = 2 x 54 x 512), generic big-tile passes
-    (36000, 43200) and the longest splittable length M = 131072 = 256 x 512 -- against
+    (36000, 43200), the longest splittable length M = 131072 = 256 x 512, and the fused two-pass kernel
+    (86400 and 172800 at B >= 128: both passes in one launch, chunks of 32 columns) -- against
     numpy's unitary irfft (Eq. 1 convention, pinned in test_oracle_pins), 1e-13 relative."""
     xc = _xc()
     rng = np.random.default_rng(L + B)
@@ -1263,3 +1265,48 @@ def test_workspace_guard_zones():
     r = subprocess.run([sys.executable, os.path.join(root, "tools", "sanitize_cases.py")], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "all cases done" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
+
+
+def _dist_build_worker(rank, world, port, out_dir):
+    import os
+    import torch.distributed as dist
+    xc = _xc()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    kt = (O.KIND_JACOBI, 0.5, -0.3)
+    N, B, eps = 3000, 40, 1e-12
+    x, _, _ = O.gauss_rule(O.Kind(*kt), N)
+    X = _gpu(I.rhs(N, B, 17))
+    for tm in (0, 1):
+        Td = xc.Transform(kt[0], x, eps, alpha=kt[1], beta=kt[2], thresh_mode=tm,
+                          dist=(rank, world, xc.host_allgather()))
+        np.save(f"{out_dir}/y{rank}_{tm}.npy", Td.apply(X).cpu().numpy())
+        np.save(f"{out_dir}/n{rank}_{tm}.npy", np.array(Td.exchanges))
+        Td.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_process_distributed_build(tmp_path):
+    """p5 with two real processes (one GPU, host-mediated gloo all-gathers; no kernel waits on the
+    other process): both ranks end with the single-process operator, bit-identical applies, for the
+    per-node and the global threshold (2 and 3 exchanges)."""
+    import socket
+    import torch.multiprocessing as tmp
+    xc = _xc()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    tmp.spawn(_dist_build_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    kt = (O.KIND_JACOBI, 0.5, -0.3)
+    x, _, _ = O.gauss_rule(O.Kind(*kt), 3000)
+    X = _gpu(I.rhs(3000, 40, 17))
+    for tm in (0, 1):
+        T = xc.Transform(kt[0], x, 1e-12, alpha=kt[1], beta=kt[2], thresh_mode=tm)
+        Y = T.apply(X).cpu().numpy()
+        T.close()
+        for r in range(2):
+            assert np.array_equal(np.load(tmp_path / f"y{r}_{tm}.npy"), Y), (r, tm)
+            assert len(np.load(tmp_path / f"n{r}_{tm}.npy")) == 2 + tm
