@@ -420,183 +420,6 @@ __global__ void __launch_bounds__(BIG ? 2 * NTH : NTH, BIG ? 1 : 3)
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
-// ---- fused two-pass C2R: both passes of a long length in one persistent kernel ----------------
-// The batch is cut into chunks of cw columns; chunk c's four-step scratch (M x cw complex) lives
-// in buffer c % nbuf (nbuf x ~22 MB: L2-resident), so pass 1 reads what pass 0 wrote from L2 and
-// the 2 x 2.8 GB scratch round trip of c5's block 1 never reaches HBM.  CTAs claim tiles from one
-// counter in the order P0(0), P0(1), P1(0), P0(2), P1(1), ..., P1(n-1) (Pp(c): the pass-p tiles of
-// chunk c); a pass-1 tile waits until every pass-0 tile of its chunk is done, a pass-0 tile until
-// the pass-1 tiles of the chunk nbuf before it (same buffer) are done.  Every tile it waits for
-// was claimed earlier by a running CTA, so the waits end (no inter-launch dependency; one launch
-// instead of 2 per chunk -- the per-launch ramps made the chunked two-launch form slower).
-struct FusedCtl {
-  unsigned* counter;  // tile claims (zeroed before the launch)
-  unsigned* done0;    // per chunk: finished pass-0 tiles
-  unsigned* done1;    // per chunk: finished pass-1 tiles
-  int nchunk, cw, n0, n1, nbuf;
-  unsigned sstride;   // elements between scratch buffers (M x cw)
-};
-
-__device__ __forceinline__ void fused_decode(const FusedCtl& f, int t, int& pass, int& c, int& lt) {
-  if (t < f.n0) {
-    pass = 0;
-    c = 0;
-    lt = t;
-    return;
-  }
-  const int u = t - f.n0, blk = f.n0 + f.n1, k = u / blk, r = u - k * blk;
-  if (k < f.nchunk - 1) {
-    if (r < f.n0) {
-      pass = 0;
-      c = k + 1;
-      lt = r;
-    } else {
-      pass = 1;
-      c = k;
-      lt = r - f.n0;
-    }
-  } else {
-    pass = 1;
-    c = f.nchunk - 1;
-    lt = r;
-  }
-}
-
-__device__ __forceinline__ bool fused_ready(const FusedCtl& f, int pass, int c) {
-  if (pass == 1) return *(volatile unsigned*)(f.done0 + c) >= (unsigned)f.n0;
-  return c < f.nbuf || *(volatile unsigned*)(f.done1 + c - f.nbuf) >= (unsigned)f.n1;
-}
-
-// One tile of pass MODE (sub-length RC, 2^LGNC sequences) with the next tile's loads issued after
-// its first stage when ready.  Returns whether they were.
-template <int MODE, int RC, int LGNC>
-__device__ __forceinline__ bool fused_tile(const C2RArgs& a, const C2RArgs& an, int pn, const FftIO& io,
-                                           const Smem& sp, int lt, int coff, unsigned soff, double2* aux,
-                                           int ln, int cn_off, unsigned sn_off, double2* auxn, const Smem& spn,
-                                           int lgnn, int* s_flag, bool next_ok) {
-  constexpr int NT = 2 * NTH;
-  const Geo g{RC, LGNC};
-  const int tid = threadIdx.x;
-  const int sq = tid & ((1 << LGNC) - 1), e0 = tid >> LGNC, estep = NT >> LGNC;
-  constexpr int IN0 = (MODE == 1) ? IN_LD : IN_Z;
-  const Slot s = slot_of<MODE>(a, lt, sq);
-  Epi ep;
-  if (MODE == 0) {
-    ep.base = (int)(soff + (unsigned)(s.sub * a.lds + s.col));
-    ep.kstep = a.L2 * a.lds;
-  } else {
-    ep.base = io.m_off * (int)io.ldy + s.col + coff;
-    ep.kstep = 0;
-  }
-  constexpr StagePlan P = stages_of(RC);
-  constexpr StageC c0 = P.st[0];
-  static_assert(P.nf >= 2, "fused passes have two or more radix stages");
-  stage<c0.r, IN0, OUT_WK, MODE, true>(a, io, g, sp, aux, s, ep, sq, e0, estep, c0);
-  __syncthreads();  // LD consumed, WK written; s_flag set by thread 0 before this barrier
-  const bool go = next_ok && *s_flag;
-  if (go) {
-    const int sqn = tid & ((1 << lgnn) - 1), e0n = tid >> lgnn, esn = NT >> lgnn;
-    if (pn == 0) issue_loads<0>(an, io, ln, spn, 0, sqn, e0n, esn, NT, cn_off, sn_off);
-    else issue_loads<1>(an, io, ln, spn, 0, sqn, e0n, esn, NT, cn_off, sn_off);
-  }
-  stages_ct<MODE, RC, 1>(a, io, g, sp, aux, s, ep, sq, e0, estep);
-  (void)auxn;
-  return go;
-}
-
-template <int R0, int L0, int R1, int L1>
-__global__ void __launch_bounds__(2 * NTH, 1)
-    c2r_fused(const __grid_constant__ C2RArgs a0, const __grid_constant__ C2RArgs a1,
-              const __grid_constant__ FftIO io, const FusedCtl f) {
-  constexpr int NT = 2 * NTH;
-  constexpr int T0 = R0 << L0, T1 = R1 << L1, TT = T0 > T1 ? T0 : T1;
-  constexpr int NQ = (1 << (L0 > L1 ? L0 : L1));
-  extern __shared__ double2 smem[];
-  __shared__ int s_tile, s_flag;
-  const int naxm = a0.naux > a1.naux ? a0.naux : a1.naux;
-  Smem b0, b1;  // the two passes' views of one layout: LD | WK | nyq | stw0 | stw1 | ptw | 2 aux slots
-  b0.ld = b1.ld = smem;
-  b0.wk = b1.wk = smem + TT;
-  b0.nyq = b1.nyq = smem + 2 * TT;
-  b0.stw = b0.nyq + NQ;
-  b1.stw = b0.stw + a0.nstw;
-  b0.ptw = b1.ptw = b1.stw + a1.nstw;
-  double2* auxbase = b0.ptw + a0.naux;
-  b0.aux2 = b1.aux2 = auxbase;
-  const int tid = threadIdx.x;
-  for (int i = tid; i < a0.nstw; i += NT) cp16(b0.stw + i, a0.stw + i, true);
-  for (int i = tid; i < a1.nstw; i += NT) cp16(b1.stw + i, a1.stw + i, true);
-  const int total = f.nchunk * (f.n0 + f.n1);
-  auto slot_view = [&](const Smem& b, int ab) {
-    Smem v = b;
-    v.aux2 = auxbase + ab * naxm;
-    return v;
-  };
-  if (tid == 0) s_tile = (int)atomicAdd(f.counter, 1u);
-  __syncthreads();
-  int t = s_tile, abuf = 0;
-  bool loaded = false;
-  // the first tile's loads (after its dependency)
-  if (t < total) {
-    int p, c, lt;
-    fused_decode(f, t, p, c, lt);
-    if (tid == 0)
-      while (!fused_ready(f, p, c)) __nanosleep(200);
-    __threadfence();
-    __syncthreads();
-    const Smem v = slot_view(p == 0 ? b0 : b1, 0);
-    const int lg = p == 0 ? L0 : L1;
-    const int sq = tid & ((1 << lg) - 1), e0 = tid >> lg, es = NT >> lg;
-    if (p == 0) issue_loads<0>(a0, io, lt, v, 0, sq, e0, es, NT, c * f.cw, (unsigned)(c % f.nbuf) * f.sstride);
-    else issue_loads<1>(a1, io, lt, v, 0, sq, e0, es, NT, c * f.cw, (unsigned)(c % f.nbuf) * f.sstride);
-    loaded = true;
-  }
-  while (t < total) {
-    int p, c, lt;
-    fused_decode(f, t, p, c, lt);
-    __syncthreads();  // every thread has read s_tile of this tile
-    if (tid == 0) s_tile = (int)atomicAdd(f.counter, 1u);  // claim the next tile now
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-    __syncthreads();  // this tile's data in; s_tile = the next tile
-    const int tn = s_tile;
-    int pn = 0, cn = 0, ln = 0;
-    const bool has_next = tn < total;
-    if (has_next) fused_decode(f, tn, pn, cn, ln);
-    if (tid == 0) s_flag = has_next && fused_ready(f, pn, cn);  // read before the tile's first barrier
-    const Smem cur = slot_view(p == 0 ? b0 : b1, abuf);
-    const Smem nxt = slot_view(pn == 0 ? b0 : b1, abuf ^ 1);
-    const int coff = c * f.cw, cnoff = cn * f.cw;
-    const unsigned soff = (unsigned)(c % f.nbuf) * f.sstride, snoff = (unsigned)(cn % f.nbuf) * f.sstride;
-    bool went;
-    if (p == 0)
-      went = fused_tile<0, R0, L0>(a0, pn == 0 ? a0 : a1, pn, io, cur, lt, coff, soff, cur.aux2, ln, cnoff, snoff,
-                                   nxt.aux2, nxt, pn == 0 ? L0 : L1, &s_flag, has_next);
-    else
-      went = fused_tile<1, R1, L1>(a1, pn == 0 ? a0 : a1, pn, io, cur, lt, coff, soff, cur.aux2, ln, cnoff, snoff,
-                                   nxt.aux2, nxt, pn == 0 ? L0 : L1, &s_flag, has_next);
-    // this tile's results visible device-wide, then count it
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) atomicAdd(p == 0 ? f.done0 + c : f.done1 + c, 1u);
-    if (has_next && !went) {  // its dependency was not met at the first stage: wait, then load
-      if (tid == 0)
-        while (!fused_ready(f, pn, cn)) __nanosleep(200);
-      __threadfence();
-      __syncthreads();
-      const int lg = pn == 0 ? L0 : L1;
-      const int sq = tid & ((1 << lg) - 1), e0 = tid >> lg, es = NT >> lg;
-      if (pn == 0) issue_loads<0>(a0, io, ln, nxt, 0, sq, e0, es, NT, cnoff, snoff);
-      else issue_loads<1>(a1, io, ln, nxt, 0, sq, e0, es, NT, cnoff, snoff);
-    } else if (has_next) {
-      __threadfence();  // acquire side of the ready flag read by thread 0 (loads already issued)
-    }
-    t = tn;
-    abuf ^= 1;
-  }
-  (void)loaded;
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-}
-
 int ilog2i(int v) {
   int l = 0;
   while ((1 << (l + 1)) <= v) ++l;
@@ -837,114 +660,13 @@ xc_status c2r_prepare(const FftPlan& p) {
 
 static xc_status c2r_run_cols(const FftPlan& p, const FftIO& io, int ncol, double2* scratch, cudaStream_t st);
 
-// Fused instances (first pass R0 with 2^L0 sequences, second R1 with 2^L1; 512 threads, big tiles)
-typedef void (*FusedKernel)(C2RArgs, C2RArgs, FftIO, FusedCtl);
-struct FusedSpec {
-  int R0, L0, R1, L1;
-  FusedKernel k;
-};
-const FusedSpec kFused[] = {
-    {200, 4, 216, 4, (FusedKernel)c2r_fused<200, 4, 216, 4>},   // c5 block 1: M = 43200
-    {200, 4, 432, 3, (FusedKernel)c2r_fused<200, 4, 432, 3>},   // N = 131072 block 1: M = 86400
-};
-
-// Geometry of one pass for ncol columns with big tiles (launch<MODE>'s tile counts, no launch)
-void pass_geometry(C2RArgs& a, int mode, int ncol) {
-  a.mode = mode;
-  a.ncol = ncol;
-  a.lds = ncol;
-  a.big = 1;
-  set_radices(a);
-  choose(a, mode == 0 ? 2 : 1);
-  a.ntx = (a.ncol + a.cb - 1) / a.cb;
-  const int nty = mode == 0 ? (a.P + a.sc / 2 - 1) / (a.sc / 2) : (a.S + a.sc - 1) / a.sc;
-  a.ntiles = a.ntx * nty;
-  a.naux = a.sc * a.R;
-}
-
-// The fused two-pass C2R when an instance exists for the plan's split and the batch has at least
-// nbuf + 1 chunks (the control words sit in the scratch after the nbuf chunk buffers).
-// XC_FUSED=0 turns it off; XC_FUSED_CW (columns per chunk, default 32), XC_FUSED_CTAS (grid).
-xc_status c2r_fused_run(const FftPlan& p, const FftIO& io, int ncol, double2* scratch, cudaStream_t st, bool& done,
-                        bool dry = false) {
-  done = false;
-  static const bool off = getenv("XC_FUSED") && atoi(getenv("XC_FUSED")) == 0;
-  static const int cw_env = getenv("XC_FUSED_CW") ? atoi(getenv("XC_FUSED_CW")) : 32;
-  static const int ctas_env = getenv("XC_FUSED_CTAS") ? atoi(getenv("XC_FUSED_CTAS")) : 0;
-  if (off || p.L2 <= 1 || (!scratch && !dry)) return XC_OK;
-  const int cw = std::max(16, cw_env / 16 * 16), nbuf = 3;
-  if (ncol % cw != 0 || ncol < (nbuf + 1) * cw) return XC_OK;
-  const C2RTables* tb = nullptr;
-  XC_TRY(tables_for(p, &tb));
-  C2RArgs a0{}, a1{};
-  for (C2RArgs* a : {&a0, &a1}) {
-    a->ptw = (const double2*)tb->ptw.p;
-    a->ftw = (const double2*)tb->ftw.p;
-    a->M = p.L;
-    a->L1 = p.L1;
-    a->L2 = p.L2;
-    a->scr = scratch;
-  }
-  a0.R = p.L1;
-  a0.S = p.L2;
-  a0.P = (a0.S & 1) ? (a0.S + 1) / 2 : a0.S / 2;
-  a0.stw = (const double2*)tb->stw0.p;
-  pass_geometry(a0, 0, cw);
-  a1.R = p.L2;
-  a1.S = p.L1;
-  a1.stw = (const double2*)tb->stw1.p;
-  pass_geometry(a1, 1, cw);
-  FusedKernel k = nullptr;
-  for (const FusedSpec& f : kFused)
-    if (f.R0 == a0.R && f.L0 == a0.lgn && f.R1 == a1.R && f.L1 == a1.lgn) k = f.k;
-  if (!k || a0.sc < 2) return XC_OK;
-  if ((int64_t)p.L * nbuf * cw >= (1LL << 31)) return XC_OK;
-  if (dry) {
-    done = true;
-    return XC_OK;
-  }
-  FusedCtl f{};
-  f.nchunk = ncol / cw;
-  f.cw = cw;
-  f.n0 = a0.ntiles;
-  f.n1 = a1.ntiles;
-  f.nbuf = nbuf;
-  f.sstride = (unsigned)((int64_t)p.L * cw);
-  unsigned* ctl = reinterpret_cast<unsigned*>(scratch + (size_t)nbuf * f.sstride);
-  f.counter = ctl;
-  f.done0 = ctl + 1;
-  f.done1 = ctl + 1 + f.nchunk;
-  XC_CUDA(cudaMemsetAsync(ctl, 0, (1 + 2 * (size_t)f.nchunk) * sizeof(unsigned), st));
-  const int TT = std::max(a0.R << a0.lgn, a1.R << a1.lgn), NQ = 1 << std::max(a0.lgn, a1.lgn);
-  const size_t sm = (size_t)(2 * TT + NQ + a0.nstw + a1.nstw + a0.naux + 2 * std::max(a0.naux, a1.naux)) *
-                    sizeof(double2);
-  if (sm > 220 * 1024) return XC_OK;
-  static std::atomic<unsigned long long> once{0};
-  if (first_on_device(once))
-    for (const FusedSpec& fs : kFused)
-      XC_CUDA(cudaFuncSetAttribute((const void*)fs.k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-  const int nsm = sm_count();
-  const int total = f.nchunk * (f.n0 + f.n1);
-  const int grid = std::min(total, ctas_env > 0 ? ctas_env : nsm);
-  k<<<grid, 2 * NTH, sm, st>>>(a0, a1, io, f);
-  XC_CUDA(cudaGetLastError());
-  done = true;
-  return XC_OK;
-}
-
 int64_t c2r_launch_count(const FftPlan& p, int64_t ncol) {
   if (p.L2 <= 1) return 1;
-  bool fused = false;
-  FftIO io{};
-  if (c2r_fused_run(p, io, (int)ncol, nullptr, nullptr, fused, true) == XC_OK && fused) return 1;
   const int64_t cw = c2r_chunk_cols(p, ncol);
   return 2 * ((ncol + cw - 1) / cw);
 }
 
 xc_status c2r_run(const FftPlan& p, const FftIO& io, int ncol, double2* scratch, cudaStream_t st) {
-  bool fused = false;
-  XC_TRY(c2r_fused_run(p, io, ncol, scratch, st, fused));
-  if (fused) return XC_OK;
   const int64_t cw = c2r_chunk_cols(p, ncol);
   if (cw >= ncol) return c2r_run_cols(p, io, ncol, scratch, st);
   for (int64_t c0 = 0; c0 < ncol; c0 += cw) {  // columns are independent: chunk by chunk

@@ -191,7 +191,7 @@ xc_status fft_run(const FftPlan& p, int sigma, FftPro pro, FftEpi epi, const Fft
 xc_status c2r_run(const FftPlan& p, const FftIO& io, int ncol, double2* scratch, cudaStream_t st);
 // two-pass lengths run in column chunks of c2r_chunk_cols(p, ncol) columns (scratch: M x that)
 int64_t c2r_chunk_cols(const FftPlan& p, int64_t ncol);
-// kernel launches of c2r_run for ncol columns (1 when the fused two-pass kernel takes the length)
+// kernel launches of c2r_run for ncol columns
 int64_t c2r_launch_count(const FftPlan& p, int64_t ncol);
 // the length's twiddle tables (allocated once per device; call at build time, not in an apply)
 xc_status c2r_prepare(const FftPlan& p);

@@ -793,13 +793,12 @@ def test_lag2d_errors():
 @pytest.mark.parametrize("L,B", [(86400, 64), (27648, 64), (9000, 96), (2916, 64), (960, 64), (360, 8),
                                  (21600, 32), (10800, 64), (7200, 64), (1152, 40), (720, 1), (60, 3),
                                  (172800, 64), (55296, 64), (43200, 72), (36000, 64), (262144, 16),
-                                 (86400, 128), (86400, 160), (86400, 1024), (172800, 256)])
+                                 (86400, 128), (172800, 256)])
 def test_c2r_engine_vs_numpy(L, B):
     """The output-axis inverse DFT engine (c2r.cu) alone at the block lengths of c1-c5 -- including
     the specialised and big-tile passes of c5 (86400 = 2 x 200 x 216, 27648, 9000, 2916), the off-config
     lengths of N = 131072 (172800 = 2 x 200 x 432, 55296 = 2 x 54 x 512), generic big-tile passes
-    (36000, 43200), the longest splittable length M = 131072 = 256 x 512, and the fused two-pass kernel
-    (86400 and 172800 at B >= 128: both passes in one launch, chunks of 32 columns) -- against
+    (36000, 43200) and the longest splittable length M = 131072 = 256 x 512 -- against
     numpy's unitary irfft (Eq. 1 convention, pinned in test_oracle_pins), 1e-13 relative."""
     xc = _xc()
     rng = np.random.default_rng(L + B)
