@@ -536,6 +536,8 @@ struct Spec {
 const Spec kSpecs[] = {
     XC_BIG(0, 200, 4),
     XC_BIG(1, 432, 3), XC_BIG(1, 512, 3),  // second passes of M = 86400 = 200 x 432, 27648 = 54 x 512 (N = 131072)
+    XC_BIG(0, 100, 5),  // first pass of M = 43200 = 100 x 432 with 16-column (256-B) tile rows
+                        // (c5 block 1 10.92 -> 10.74 ms, N = 32768 5.13 -> 5.00 ms vs 200 x 216)
     XC_SPEC(1, 216, 3), XC_SPEC(0, 54, 5),  XC_SPEC(1, 256, 3), XC_SPEC(0, 45, 5), XC_SPEC(1, 100, 4),
     XC_SPEC(0, 27, 6),  XC_SPEC(1, 54, 5),  XC_SPEC(1, 240, 3), XC_SPEC(1, 64, 5), XC_SPEC(0, 32, 6),
     XC_SPEC(0, 36, 5),  XC_SPEC(0, 9, 7),

@@ -217,7 +217,11 @@ void clear_graphs(Ws& w) {
 // naux - 1 streams.  Large batches use naux = 2 (blocks 3.. in one stream: more concurrent
 // streams slowed c5's FFT phase 3.94 -> 4.09 ms), small ones all four (c3 0.255 -> 0.225 ms).
 inline int aux_of(int ib, int naux) { return ib == 1 ? 0 : 1 + (ib - 2) % (naux - 1); }
-inline int naux_for(int64_t N, int64_t B) { return N * B <= (32LL << 20) ? kAux : 2; }
+inline int naux_for(int64_t N, int64_t B) {
+  static const int force = getenv("XC_NAUX") ? atoi(getenv("XC_NAUX")) : 0;  // measurement switch
+  if (force >= 2 && force <= kAux) return force;
+  return N * B <= (32LL << 20) ? kAux : 2;
+}
 
 // Columns of one C2R column chunk of a two-pass block (c2r_run): the four-step scratch of a chunk
 // (M x chunk complex) is kept near 40 MB so that it stays in L2 between the two passes.
