@@ -244,9 +244,12 @@ def run_reference(args, cfg, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+COLL_DEVICE = "cuda"   # where the timing collectives' tensors live ("cpu" with the gloo test backend)
+
+
 def sum_cols(B):
     from paper_2004_11610_b200.shard import sum_over_ranks
-    return sum_over_ranks(B, device="cuda")
+    return sum_over_ranks(B, device=COLL_DEVICE)
 
 
 def main():
@@ -262,6 +265,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--direction", default="", help="A or WAT (default: the config's first)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process group backend (gloo: host-mediated exchanges, for the 2-rank test on one GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = I.CONFIGS[args.config]
@@ -285,11 +290,20 @@ def main():
 
     import torch
     from paper_2004_11610_b200 import xc
+    global COLL_DEVICE
+    # XC_BENCH_ONE_DEVICE=1 (tests only): every rank on cuda:0 with the gloo backend -- the exchanges
+    # and timing collectives then run on the host, no kernel waits on another rank
+    if os.environ.get("XC_BENCH_ONE_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "gloo":
+            dist.init_process_group("gloo")
+            COLL_DEVICE = "cpu"
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     direction = xc.XC_DIR_WAT if (args.direction or cfg.dirs[0]) == "WAT" else xc.XC_DIR_A
     B_global = args.batch or cfg.B
@@ -303,7 +317,8 @@ def main():
     t0 = time.perf_counter()
     # N > 1: distributed precompute (node range per rank, NCCL all-gather of the node bands)
     T = xc.Transform(cfg.kind, x, cfg.eps, alpha=cfg.alpha, beta=cfg.beta, dirs=dirs, weights=wt, device=local,
-                     dist=(rank, ws, xc.nccl_allgather()) if ws > 1 else None,
+                     dist=(rank, ws, xc.nccl_allgather() if args.dist_backend == "nccl" else xc.host_allgather())
+                     if ws > 1 else None,
                      eta=cfg.eta, n_rows=cfg.M, eps2=cfg.eps2 if cfg.eps2 != 1e-2 else 0.0)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
@@ -348,7 +363,7 @@ def main():
         dist.barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
     clk = clocks.stop() if clocks else None
-    ms = max_over_ranks(ms, device="cuda")
+    ms = max_over_ranks(ms, device=COLL_DEVICE)
     total_cols = int(round(sum_cols(B)))
     value = total_cols / (ms / 1e3)
 
@@ -365,7 +380,7 @@ def main():
     torch.cuda.nvtx.range_pop()
     prof = T.profile_read()
     T.profile(False)
-    ems = max_over_ranks(p0.elapsed_time(p1) / args.steps, device="cuda")
+    ems = max_over_ranks(p0.elapsed_time(p1) / args.steps, device=COLL_DEVICE)
     graph = {"eager_ms_per_step": ems, "eager_value": total_cols / (ems / 1e3), "unit": "transforms/s",
              "note": "value/ms_per_step: xc_apply's default CUDA-graph replay; eager: the same steps "
                      "launched kernel by kernel with per-phase events (the roofline's kernel times)"}
@@ -410,7 +425,7 @@ def main():
             T.apply_host_async_ptr(Xp.data_ptr(), Yp.data_ptr(), B, direction, stream=stream.cuda_stream)
         T.host_wait()
         ems = (time.perf_counter() - tw0) * 1e3 / args.e2e_steps
-        ems = max_over_ranks(ems, device="cuda")
+        ems = max_over_ranks(ems, device=COLL_DEVICE)
         e2e = {"value": total_cols / (ems / 1e3), "unit": "transforms/s",
                "h2d_bytes_per_step": int(sum_cols(Xh.nbytes)), "d2h_bytes_per_step": int(sum_cols(8 * Y.numel())),
                "ms_per_step": ems,
@@ -456,7 +471,8 @@ def main():
             "graph": graph,
             "gpu_launches": info["launches_A" if direction == xc.XC_DIR_A else "launches_WAT"] * args.steps,
             "clocks": clk,
-            "comm": ({"backend": "nccl", "world_size": ws, "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
+            "comm": ({"backend": args.dist_backend, "world_size": ws,
+                      "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
                       "data_path_collectives": 0, "precompute": "2 all-gathers of node bands (xc_build_local/step)"}
                      if ws > 1 else None),
             "precompute_s": {"gauss_nodes": t_nodes, "build": t_build,

@@ -1309,3 +1309,31 @@ def test_two_process_distributed_build(tmp_path):
         for r in range(2):
             assert np.array_equal(np.load(tmp_path / f"y{r}_{tm}.npy"), Y), (r, tm)
             assert len(np.load(tmp_path / f"n{r}_{tm}.npy")) == 2 + tm
+
+
+def test_bench_two_ranks_one_gpu():
+    """The multi-rank bench path end to end (launcher, rank-local column shards of the seeded global
+    batch, distributed precompute through the rank exchange, max-over-ranks timing, one JSON line)
+    with 2 ranks on one GPU: gloo backend, so the exchanges and the timing collectives run on the
+    host and no kernel waits on another rank."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, XC_BENCH_ONE_DEVICE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", f"--master-port={port}", os.path.join(root, "bench.py"), "--gpus", "2", "--config", "c3",
+           "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1", "--dist-backend", "gloo"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong" and line["value"] > 0
+    assert line["config"]["global_batch"] == 256 and line["config"]["columns_of_rank0"] == [0, 128]
+    assert line["comm"]["world_size"] == 2 and line["comm"]["data_path_collectives"] == 0
+    assert "2 ranks" in line["precompute_s"]["mode"]
