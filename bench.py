@@ -400,7 +400,7 @@ def main():
     # DRAM traffic of the SpMM launch from the committed ncu --set full capture (same workload)
     traffic, traffic_src = None, None
     try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "r01_spmm_traffic.json")))
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r02_spmm_traffic.json")))
         if tr.get("workload") == cfg.name and tr.get("B_per_gpu") == B and direction == xc.XC_DIR_A:
             traffic = float(tr["dram_bytes_read_per_launch"] + tr["dram_bytes_write_per_launch"])
             traffic_src = tr["source"]
