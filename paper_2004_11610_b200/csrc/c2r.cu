@@ -266,13 +266,13 @@ enum { OUT_WK = 0, OUT_G = 1 };
 // One Stockham radix-r stage for this thread's sequence: butterflies j = e0 + b*estep < R/r.
 // Out-of-range butterflies of the last round are computed on a clamped (valid) index and
 // their stores suppressed, so there is no divergent control flow inside the stage.
-template <int r, int IN, int OUT, int MODE, bool FIRST>
+template <int r, int IN, int OUT, int MODE, bool FIRST, int PPT = TILE / NTH>
 __device__ __forceinline__ void stage(const C2RArgs& a, const FftIO& io, const Geo g, const Smem& sp,
                                       const double2* aux, const Slot& s, const Epi& ep, int sq, int e0, int estep,
                                       const StageC c) {
   const double2* ld = sp.ld;
   double2* wk = sp.wk;
-  constexpr int MB = (TILE / NTH + r - 1) / r;  // butterflies per thread (R * nseq <= TILE)
+  constexpr int MB = (PPT + r - 1) / r;  // butterflies per thread (R * nseq <= PPT * threads)
   const int lgn = g.lgn;
   double2 v[MB][r];
   bool act[MB], wact[MB];
@@ -335,27 +335,32 @@ __device__ __forceinline__ void stage_r(const C2RArgs& a, const FftIO& io, const
 }
 
 // Compile-time stage sequence (specialised kernels): stages ST .. NF-2 in place, then the last.
-template <int MODE, int RC, int ST>
+template <int MODE, int RC, int ST, int PPT = TILE / NTH>
 __device__ __forceinline__ void stages_ct(const C2RArgs& a, const FftIO& io, const Geo g, const Smem& sp,
                                           const double2* aux, const Slot& s, const Epi& ep, int sq, int e0,
                                           int estep) {
   constexpr StagePlan P = stages_of(RC);
   constexpr StageC c = P.st[ST];
   if constexpr (ST + 1 < P.nf) {
-    stage<c.r, IN_WK, OUT_WK, MODE, false>(a, io, g, sp, aux, s, ep, sq, e0, estep, c);
+    stage<c.r, IN_WK, OUT_WK, MODE, false, PPT>(a, io, g, sp, aux, s, ep, sq, e0, estep, c);
     __syncthreads();
-    stages_ct<MODE, RC, ST + 1>(a, io, g, sp, aux, s, ep, sq, e0, estep);
+    stages_ct<MODE, RC, ST + 1, PPT>(a, io, g, sp, aux, s, ep, sq, e0, estep);
   } else {
-    stage<c.r, IN_WK, OUT_G, MODE, false>(a, io, g, sp, aux, s, ep, sq, e0, estep, c);
+    stage<c.r, IN_WK, OUT_G, MODE, false, PPT>(a, io, g, sp, aux, s, ep, sq, e0, estep, c);
   }
 }
 
 // RC = 0: generic kernel (runtime length and radix plan); RC > 0: specialised for sub-length
 // RC with 2^LGNC sequences per tile.
+// BIG = 1: 512 threads, tiles up to 2 TILE points (one CTA per SM); BIG = 2 ("wide"): 512 threads,
+// tiles up to kWide points (~200 KB of double-buffered tiles), so that a first pass of 200 points
+// has 32 sequences = 16 columns (256-B rows)
+constexpr int kWide = 6400;
 template <int MODE, int RC, int LGNC, int BIG = 0>
 __global__ void __launch_bounds__(BIG ? 2 * NTH : NTH, BIG ? 1 : 3)
     c2r_pass(const __grid_constant__ C2RArgs a, const __grid_constant__ FftIO io) {
-  constexpr int NT = BIG ? 2 * NTH : NTH;  // BIG: 512 threads, tiles up to 2 TILE (one CTA per SM)
+  constexpr int NT = BIG ? 2 * NTH : NTH;
+  constexpr int PPT = BIG == 2 ? (kWide + 2 * NTH - 1) / (2 * NTH) : TILE / NTH;  // points per thread
   extern __shared__ double2 smem[];
   const Smem sp = smem_parts(a, smem);
   const Geo g = RC ? Geo{RC, LGNC >= 0 ? LGNC : a.lgn} : Geo{a.R, a.lgn};  // LGNC < 0: runtime
@@ -391,14 +396,14 @@ __global__ void __launch_bounds__(BIG ? 2 * NTH : NTH, BIG ? 1 : 3)
       constexpr StagePlan P = stages_of(RC);
       constexpr StageC c0 = P.st[0];
       if constexpr (P.nf == 1) {
-        stage<c0.r, IN0, OUT_G, MODE, true>(a, io, g, sp, aux, s, ep, sq, e0, estep, c0);
+        stage<c0.r, IN0, OUT_G, MODE, true, PPT>(a, io, g, sp, aux, s, ep, sq, e0, estep, c0);
         __syncthreads();
         if (more) issue_loads<MODE>(a, io, tile + gridDim.x, sp, abuf ^ 1, sq, e0, estep, NT);
       } else {
-        stage<c0.r, IN0, OUT_WK, MODE, true>(a, io, g, sp, aux, s, ep, sq, e0, estep, c0);
+        stage<c0.r, IN0, OUT_WK, MODE, true, PPT>(a, io, g, sp, aux, s, ep, sq, e0, estep, c0);
         __syncthreads();  // LD and the pairing slice consumed, WK written
         if (more) issue_loads<MODE>(a, io, tile + gridDim.x, sp, abuf ^ 1, sq, e0, estep, NT);
-        stages_ct<MODE, RC, 1>(a, io, g, sp, aux, s, ep, sq, e0, estep);
+        stages_ct<MODE, RC, 1, PPT>(a, io, g, sp, aux, s, ep, sq, e0, estep);
       }
     } else {
       if (a.nf == 1) {
@@ -509,7 +514,7 @@ xc_status tables_for(const FftPlan& p, const C2RTables** out) {
 
 // nseq = cb * sc (powers of two) with R * nseq <= TILE; columns first (cb <= 16), sc >= smin.
 void choose(C2RArgs& a, int smin) {
-  const int tile = a.big ? 2 * TILE : TILE, nth = a.big ? 2 * NTH : NTH;
+  const int tile = a.big == 2 ? kWide : (a.big ? 2 * TILE : TILE), nth = a.big ? 2 * NTH : NTH;
   int nseq = 1;
   while (2 * nseq * a.R <= tile && nseq < nth && nseq < smin * a.S * std::max(1, a.ncol)) nseq *= 2;
   int cb = 1;
@@ -532,9 +537,10 @@ struct Spec {
 };
 #define XC_SPEC(M, R, L) {M, R, L, 0, (C2RKernel)c2r_pass<M, R, L>}
 #define XC_BIG(M, R, L) {M, R, L, 1, (C2RKernel)c2r_pass<M, R, L, 1>}
+#define XC_WIDE(M, R, L) {M, R, L, 2, (C2RKernel)c2r_pass<M, R, L, 2>}
 // BIG (512 threads, 64 KB tiles, 1 CTA / SM): the longest passes, so that a tile row is >= 128 B
 const Spec kSpecs[] = {
-    XC_BIG(0, 200, 4),
+    XC_BIG(0, 200, 4), XC_WIDE(0, 200, 5),
     XC_BIG(1, 432, 3), XC_BIG(1, 512, 3),  // second passes of M = 86400 = 200 x 432, 27648 = 54 x 512 (N = 131072)
     XC_BIG(0, 100, 5),  // first pass of M = 43200 = 100 x 432 with 16-column (256-B) tile rows
                         // (c5 block 1 10.92 -> 10.74 ms, N = 32768 5.13 -> 5.00 ms vs 200 x 216)
@@ -551,6 +557,7 @@ const Spec kSpecs[] = {
 };
 #undef XC_SPEC
 #undef XC_BIG
+#undef XC_WIDE
 
 }  // namespace
 
@@ -559,6 +566,14 @@ bool has_big(int mode, int R);
 }
 
 bool c2r_has_big(int mode, int R) { return has_big(mode, R); }
+
+bool c2r_has_wide(int mode, int R) {
+  static const bool off = getenv("XC_C2R_GENERIC") || getenv("XC_C2R_NOBIG") || getenv("XC_C2R_NOWIDE");
+  if (off) return false;
+  for (const Spec& sp : kSpecs)
+    if (sp.mode == mode && sp.R == R && sp.big == 2) return true;
+  return false;
+}
 
 bool c2r_has_spec(int mode, int R) {
   for (const Spec& sp : kSpecs)
@@ -590,11 +605,11 @@ template <int MODE>
 xc_status launch(C2RArgs& a, const FftIO& io, cudaStream_t st) {
   static std::atomic<unsigned long long> once{0};
   if (first_on_device(once)) {
-    XC_CUDA(cudaFuncSetAttribute(c2r_pass<MODE, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    XC_CUDA(cudaFuncSetAttribute(c2r_pass<MODE, 0, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    XC_CUDA(cudaFuncSetAttribute(c2r_pass<MODE, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    XC_CUDA(cudaFuncSetAttribute(c2r_pass<MODE, 0, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     for (const Spec& sp : kSpecs)
       if (sp.mode == MODE)
-        XC_CUDA(cudaFuncSetAttribute((const void*)sp.k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        XC_CUDA(cudaFuncSetAttribute((const void*)sp.k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   }
   const int nsm = sm_count();
   a.mode = MODE;
@@ -609,7 +624,7 @@ xc_status launch(C2RArgs& a, const FftIO& io, cudaStream_t st) {
   const size_t ent = 2 * (size_t)a.R * nseq + nseq + a.nstw + (MODE == 1 ? 0 : a.naux) +
                      (MODE == 2 ? 1 : 2) * (size_t)a.naux;
   const size_t sm = ent * sizeof(double2);
-  if (sm > 200 * 1024) {
+  if (sm > 227 * 1024) {
     xc_set_error("c2r: tile does not fit shared memory");
     return XC_EUNSUPPORTED;
   }
@@ -727,9 +742,9 @@ static xc_status c2r_run_cols(const FftPlan& p, const FftIO& io, int ncol, doubl
   a.P = (a.S & 1) ? (a.S + 1) / 2 : a.S / 2;
   set_radices(a);
   a.stw = (const double2*)tb->stw0.p;
-  a.big = has_big(0, a.R) && ncol >= 64;
+  a.big = ncol >= 64 ? (c2r_has_wide(0, a.R) && ncol >= 128 ? 2 : (has_big(0, a.R) ? 1 : 0)) : 0;
   choose(a, 2);
-  if (a.sc < 2 || a.R * (1 << a.lgn) > (a.big ? 2 : 1) * TILE) {
+  if (a.sc < 2 || a.R * (1 << a.lgn) > (a.big == 2 ? kWide : (a.big ? 2 : 1) * TILE)) {
     xc_set_error("c2r: first-pass length too long");
     return XC_EUNSUPPORTED;
   }

@@ -20,6 +20,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <stdio.h>
+
 #include "xc_internal.cuh"
 
 namespace {
@@ -377,8 +379,8 @@ void set_stages(PassArgs& a, int nf, const int* f) {
 double c2r_pass_cost(int R, int smin, int mode) {
   const C2RRadices pl = c2r_radices(R);
   if (pl.nf < 0) return 1e30;
-  const bool big = c2r_has_big(mode, R);
-  const int tile = big ? 4096 : 2048, nth = big ? 512 : 256;
+  const bool wide = c2r_has_wide(mode, R), big = wide || c2r_has_big(mode, R);
+  const int tile = wide ? 6400 : (big ? 4096 : 2048), nth = big ? 512 : 256;
   int nseq = 1;
   while (2 * nseq * R <= tile && nseq < nth) nseq *= 2;
   if (nseq < smin) return 1e30;
@@ -388,14 +390,19 @@ double c2r_pass_cost(int R, int smin, int mode) {
   const int estep = nth >> lgn;
   double warps = 0;
   for (int i = 0; i < pl.nf; ++i) {
-    const int r = pl.f[i], Rr = R / r, MB = (8 + r - 1) / r;
+    const int ppt = wide ? 13 : 8;  // points per thread of the tile (c2r.cu: TILE / NTH, or kWide / 512)
+    const int r = pl.f[i], Rr = R / r, MB = (ppt + r - 1) / r;
     for (int b = 0; b < MB; ++b)
       for (int w = 0; w < nth / 32; ++w) {
         const int e0min = (32 * w) >> lgn;
         if (e0min + b * estep < Rr) warps += 1;
       }
   }
-  return warps * 32.0 / ((double)R * nseq) * pen * (c2r_has_spec(mode, R) ? 1.0 : 1.4);
+  // a big second pass runs one 512-thread CTA per SM against three 256-thread ones: measured
+  // slower than the model's rounds say (c5 block 1: 432-point big pass 1.17 ms vs 216-point pass
+  // 0.96 ms), hence the occupancy factor 1.7
+  const double occ = (mode == 1 && big) ? 1.7 : 1.0;
+  return warps * 32.0 / ((double)R * nseq) * pen * occ * (c2r_has_spec(mode, R) ? 1.0 : 1.4);
 }
 
 xc_status fft_plan_make(FftPlan& p, int L, bool c2r) {
@@ -405,7 +412,18 @@ xc_status fft_plan_make(FftPlan& p, int L, bool c2r) {
     p.L2 = 1;
   } else {
     int best = -1;
-    if (c2r) {  // the split with the cheapest pair of C2R passes (first pass pairs sub-sequences)
+    // XC_C2R_SPLIT="M:L1[,M:L1...]" forces the split of the listed C2R lengths (measurement switch)
+    static const char* forced = getenv("XC_C2R_SPLIT");
+    if (c2r && forced) {
+      const char* q = forced;
+      while (*q) {
+        int m = 0, l1 = 0;
+        if (sscanf(q, "%d:%d", &m, &l1) == 2 && m == L && l1 > 1 && L % l1 == 0) best = l1;
+        while (*q && *q != ',') ++q;
+        if (*q == ',') ++q;
+      }
+    }
+    if (c2r && best < 0) {  // the split with the cheapest pair of C2R passes (first pass pairs sub-sequences)
       double bc = 1e30;
       // first pass (paired sub-sequences) <= 256 points, second <= 512: every M up to 131072
       // splits (c5 at N = 131072: M = 86400 = 200 x 432, both passes on 128-B tile rows)

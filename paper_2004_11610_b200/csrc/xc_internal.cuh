@@ -200,6 +200,8 @@ bool c2r_has_big(int mode, int R);
 // 1 if c2r.cu has a compile-time specialised kernel for this pass and length (the generic one runs
 // ~1.4x the instructions)
 bool c2r_has_spec(int mode, int R);
+// 1 if c2r.cu has a "wide" kernel (512 threads, 6400-point tiles) for this pass and length
+bool c2r_has_wide(int mode, int R);
 
 // ---------------------------------------------------------------------------
 // SpMM on the FP64 tensor cores (spmm.cu)
