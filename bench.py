@@ -299,6 +299,10 @@ def main():
     dist = None
     if ws > 1:
         import torch.distributed as dist
+        # the NCCL communicator lines (ranks, devices, transport) on stderr, also under the driver's
+        # own torchrun launch
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if args.dist_backend == "gloo":
             dist.init_process_group("gloo")
             COLL_DEVICE = "cpu"
