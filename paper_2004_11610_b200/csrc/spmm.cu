@@ -39,7 +39,7 @@ constexpr int WARPS = XC_WARPS;  // warps per CTA
 // B rows lie inside it) are spread over the warps.  Each item holds 2 M-tiles sharing the B
 // fragments (2 x NT DMMAs per 4-row step).  B fragments come from shared memory (one step
 // ahead), A fragments stream from global memory two steps ahead.
-template <int NT>
+template <int NT, bool PF>
 __global__ void __launch_bounds__(WARPS * 32, 2)
     spmm_win(const SpmmWin* __restrict__ wins, const SpmmItem* __restrict__ items,
              const double* __restrict__ tiles, SpmmSrcs srcs, double* __restrict__ part, int64_t ldp, int ncols) {
@@ -109,6 +109,19 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
   const int iw0 = W.i0 + __ldg(&wins[blockIdx.y].wo[warp]), iw1 = W.i0 + __ldg(&wins[blockIdx.y].wo[warp + 1]);
   for (int ii = iw0; ii < iw1; ++ii) {
     const SpmmItem it = its[ii - W.i0];
+    // PF (grids of a few waves, c3): at an item's start its A stream beyond the first 4 steps and
+    // the next item's first 4 steps are prefetched into L2 (128-B lines, lane l takes lines l,
+    // l + 32, ...): the 4-step register prefetch does not cover a DRAM first touch (c3 SpMM
+    // 0.120 -> 0.111 ms; on the long c5 grid it costs more than it gains: 6.65 -> 6.82 ms)
+    if constexpr (PF) {
+      const char* ab = reinterpret_cast<const char*>(tiles + it.a_off);
+      for (int q = 16 + lane; q < 4 * it.nsteps; q += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(ab + 128 * q));
+      if (ii + 1 < iw1 && lane < 16) {
+        const SpmmItem& nx = its[ii + 1 - W.i0];
+        if (lane < 4 * nx.nsteps)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(tiles + nx.a_off) + 128 * lane));
+      }
+    }
     double acc[2][NT][2];
 #pragma unroll
     for (int m = 0; m < 2; ++m)
@@ -240,12 +253,20 @@ xc_status launch(const SpmmWin* wins, int nwins, const SpmmItem* items, const do
                  double* part, int64_t ldp, int ncols, cudaStream_t st) {
   const size_t sm = (size_t)XC_WMAX * (8 * NT + 4) * sizeof(double) + (size_t)XC_WIN_ITEMS * sizeof(SpmmItem);
   static std::atomic<unsigned long long> once{0};
-  if (first_on_device(once))
-    XC_CUDA(cudaFuncSetAttribute(spmm_win<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  if (first_on_device(once)) {
+    XC_CUDA(cudaFuncSetAttribute(spmm_win<NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    XC_CUDA(cudaFuncSetAttribute(spmm_win<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  }
+  // the A-stream L2 prefetch for grids of 1 to 16 waves of 2 CTAs per SM (c3 +3 %, c4 +0.5 %, its
+  // input axis +1.3 %; not the µs-scale grids of c2/c6/c7 nor the long c5 grid); XC_SPMM_PF=0/1 forces
+  const int64_t ctas = (int64_t)nwins * ((ncols + 8 * NT - 1) / (8 * NT)), wave = 2 * (int64_t)sm_count();
+  static const int force = getenv("XC_SPMM_PF") ? atoi(getenv("XC_SPMM_PF")) : -1;
+  const bool pf = force >= 0 ? force != 0 : (ctas >= wave && ctas < 16 * wave);
   for (int w0 = 0; w0 < nwins; w0 += 65535) {
     int nw = std::min(65535, nwins - w0);
     dim3 grid((ncols + 8 * NT - 1) / (8 * NT), nw);
-    spmm_win<NT><<<grid, WARPS * 32, sm, st>>>(wins + w0, items, tiles, srcs, part, ldp, ncols);
+    if (pf) spmm_win<NT, true><<<grid, WARPS * 32, sm, st>>>(wins + w0, items, tiles, srcs, part, ldp, ncols);
+    else spmm_win<NT, false><<<grid, WARPS * 32, sm, st>>>(wins + w0, items, tiles, srcs, part, ldp, ncols);
     XC_CUDA(cudaGetLastError());
   }
   return XC_OK;
