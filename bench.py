@@ -398,7 +398,7 @@ def main():
     if cfg.kind == I.KIND_LAG2D:   # no dense tail inside the product launch (separate kernels)
         spmm_flops = 8.0 * nnz * B
     achieved = spmm_flops / (spmm_ms / 1e3) / 1e12
-    alg_bytes = 16.0 * N * B + 20.0 * nnz + 8.0 * tail * N   # X in, Y out, operator once (SURVEY d.3)
+    alg_bytes = info["alg_bytes_per_col"] * B + info["alg_bytes_fixed"]   # X in, Y out, operator once (SURVEY d.3)
     peaks = _peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     # DRAM traffic of the SpMM launch from the committed ncu --set full capture (same workload)

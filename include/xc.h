@@ -123,6 +123,10 @@ typedef struct {
   int launches_A;          /* kernel launches per xc_apply(XC_DIR_A)                         */
   int launches_WAT;        /* kernel launches per xc_apply(XC_DIR_WAT)                       */
   int64_t M;               /* degrees (rows of A): N unless rectangular (complex kinds)       */
+  double alg_bytes_per_col;  /* algorithmic HBM bytes per RHS column of an apply:
+                                X read + Y written (16 N, planar complex twice)                 */
+  double alg_bytes_fixed;    /* ... and per apply: the operator once (20 B per kept entry:
+                                complex value + index) and the dense tail (8 t N)               */
 } xc_info_t;
 
 typedef struct {

@@ -1405,6 +1405,8 @@ xc_status build_end(xc_op* h) {
   in.op_bytes_WAT = h->tilesW_n * 8 + (int64_t)h->nitemsW * sizeof(SpmmItem);
   in.launches_A = (int)count_launches(h, XC_DIR_A, 1);
   in.launches_WAT = (int)count_launches(h, XC_DIR_WAT, 1);
+  in.alg_bytes_per_col = (kind == XC_EXP ? 16.0 : 8.0) * (double)(h->N + h->M);
+  in.alg_bytes_fixed = 20.0 * (double)nnz + 8.0 * h->tail * (double)N;
   return XC_OK;
 }
 
@@ -1639,6 +1641,8 @@ xc_status build_2d(xc_op* h) {
   in.flops_per_col_WAT = 0;
   in.op_bytes_A = total * (int64_t)sizeof(Ent2D);
   in.launches_A = (int)count_launches(h, XC_DIR_A, 1);
+  in.alg_bytes_per_col = 16.0 * (double)N;
+  in.alg_bytes_fixed = 24.0 * (double)total + 8.0 * (2.0 * t * N - (double)t * t);  // Ent2D values + indices
   return XC_OK;
 }
 

@@ -39,7 +39,8 @@ class XcInfo(ctypes.Structure):
                 ("dirs", ctypes.c_int), ("nnz", _i64), ("op_bytes_A", _i64), ("op_bytes_WAT", _i64),
                 ("flops_per_col_A", ctypes.c_double), ("flops_per_col_WAT", ctypes.c_double),
                 ("dmma_flops_per_col_A", ctypes.c_double), ("dmma_flops_per_col_WAT", ctypes.c_double),
-                ("launches_A", ctypes.c_int), ("launches_WAT", ctypes.c_int), ("M", _i64)]
+                ("launches_A", ctypes.c_int), ("launches_WAT", ctypes.c_int), ("M", _i64),
+                ("alg_bytes_per_col", ctypes.c_double), ("alg_bytes_fixed", ctypes.c_double)]
 
 
 class XcExchange(ctypes.Structure):
