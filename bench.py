@@ -473,7 +473,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "graph": graph,
-            "gpu_launches": info["launches_A" if direction == xc.XC_DIR_A else "launches_WAT"] * args.steps,
+            "gpu_launches": T.launches(B, direction) * args.steps,   # xc_launches: kernels of one apply of B
             "clocks": clk,
             "comm": ({"backend": args.dist_backend, "world_size": ws,
                       "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
