@@ -176,116 +176,6 @@ __global__ void __launch_bounds__(1024) small_c2r_k(const SmallBlocks sb, const 
   }
 }
 
-// Sums of the rows [r0, r1) (long rows: longrows[l0, l1)) for column c, x_k from shared memory:
-// short rows one thread each in entry order (4-entry load batches), long rows one warp each (lane
-// sums, then the xor tree) -- exactly small_spmm_k's arithmetic.  Result of row r: put(r, re, im).
-template <typename Put>
-__device__ __forceinline__ void small_rows(const SmallOp& op, const double* xs, int r0, int r1, int l0, int l1,
-                                           Put put) {
-  for (int r = r0 + (int)threadIdx.x; r < r1; r += blockDim.x) {
-    const int64_t e0 = op.ptr[r], e1 = op.ptr[r + 1];
-    if (e1 - e0 > kSmallLong) continue;
-    double re = 0.0, im = 0.0;
-    int64_t e = e0;
-    for (; e + 4 <= e1; e += 4) {
-      const int k0 = __ldg(op.node + e), k1 = __ldg(op.node + e + 1), k2 = __ldg(op.node + e + 2),
-                k3 = __ldg(op.node + e + 3);
-      const double2 v0 = __ldg(op.val + e), v1 = __ldg(op.val + e + 1), v2 = __ldg(op.val + e + 2),
-                    v3 = __ldg(op.val + e + 3);
-      const double x0 = xs[k0], x1 = xs[k1], x2 = xs[k2], x3 = xs[k3];
-      re = fma(v0.x, x0, re);
-      im = fma(v0.y, x0, im);
-      re = fma(v1.x, x1, re);
-      im = fma(v1.y, x1, im);
-      re = fma(v2.x, x2, re);
-      im = fma(v2.y, x2, im);
-      re = fma(v3.x, x3, re);
-      im = fma(v3.y, x3, im);
-    }
-    for (; e < e1; ++e) {
-      const double x = xs[__ldg(op.node + e)];
-      const double2 v = __ldg(op.val + e);
-      re = fma(v.x, x, re);
-      im = fma(v.y, x, im);
-    }
-    put(r, re, im);
-  }
-  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int l = l0 + (int)(threadIdx.x >> 5); l < l1; l += nw) {
-    const int r = op.longrows[l];
-    const int64_t e0 = op.ptr[r], e1 = op.ptr[r + 1];
-    double re = 0.0, im = 0.0;
-    for (int64_t e = e0 + lane; e < e1; e += 32) {
-      const double x = xs[__ldg(op.node + e)];
-      const double2 v = __ldg(op.val + e);
-      re = fma(v.x, x, re);
-      im = fma(v.y, x, im);
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      re += __shfl_xor_sync(0xffffffffu, re, o);
-      im += __shfl_xor_sync(0xffffffffu, im, o);
-    }
-    if (lane == 0) put(r, re, im);
-  }
-}
-
-// One launch: CTA (i, c).  i < nb: block i's u in shared memory, then its C2R; i == nb: the tail.
-// Shared: x column (N) | A (M + 1) | Bf (M) | tw (M).
-__global__ void __launch_bounds__(256) small_fused_k(const SmallOp op, const SmallBlocks sb,
-                                                     const double* __restrict__ X, int64_t ldx,
-                                                     double* __restrict__ Y, int64_t ldy, int N) {
-  extern __shared__ double2 sm2[];
-  double* xs = reinterpret_cast<double*>(sm2);
-  const int c = blockIdx.y;
-  for (int k = threadIdx.x; k < N; k += blockDim.x) xs[k] = __ldg(X + (int64_t)k * ldx + c);
-  __syncthreads();
-  if ((int)blockIdx.x == sb.nb) {  // the dense tail straight to Y
-    small_rows(op, xs, sb.tr0, sb.tr1, sb.tl0, sb.tl1, [&](int r, double re, double) {
-      Y[(-op.out[r] - 1) * ldy + c] = re;
-    });
-    return;
-  }
-  const SmallBlk b = sb.blk[blockIdx.x];
-  const int M = b.M;
-  double2* A = sm2 + (N + 1) / 2;
-  double2* Bf = A + M + 1;
-  double2* tw = Bf + M;
-  for (int n = threadIdx.x; n < M; n += blockDim.x) tw[n] = __ldg(b.twM + n);
-  small_rows(op, xs, b.r0, b.r1, b.l0, b.l1, [&](int r, double re, double im) { A[r - b.r0] = make_double2(re, im); });
-  __syncthreads();
-  for (int n = threadIdx.x; n < M; n += blockDim.x) {  // pairing, as small_c2r_k
-    const double2 a = A[n], p = A[M - n], w = __ldg(b.twh + n);
-    const double evr = a.x + p.x, evi = a.y - p.y, dr = a.x - p.x, di = a.y + p.y;
-    const double odr = dr * w.x - di * w.y, odi = dr * w.y + di * w.x;
-    Bf[n] = make_double2(evr - odi, evi + odr);
-  }
-  __syncthreads();
-  double2* in = Bf;
-  double2* out = A;
-  int Ns = 1;
-  for (int s = 0; s < b.nf; ++s) {
-    const int r = b.f[s];
-    switch (r) {
-      case 2: small_stage<2>(in, out, tw, M, Ns); break;
-      case 3: small_stage<3>(in, out, tw, M, Ns); break;
-      case 4: small_stage<4>(in, out, tw, M, Ns); break;
-      case 5: small_stage<5>(in, out, tw, M, Ns); break;
-      case 6: small_stage<6>(in, out, tw, M, Ns); break;
-      case 9: small_stage<9>(in, out, tw, M, Ns); break;
-      default: small_stage<8>(in, out, tw, M, Ns); break;
-    }
-    Ns *= r;
-    __syncthreads();
-    double2* t = in;
-    in = out;
-    out = t;
-  }
-  for (int p = b.keep_lo + threadIdx.x; p < b.keep_hi; p += blockDim.x) {
-    const double2 z = in[p >> 1];
-    Y[(int64_t)(p + b.m_off) * ldy + c] = ((p & 1) ? z.y : z.x) * __ldg(b.yscale + p);
-  }
-}
-
 }  // namespace
 
 xc_status small_spmm(const SmallOp& op, const double* X, int64_t ldx, double2* U, int64_t ldu, double* Y, int64_t ldy,
@@ -336,19 +226,4 @@ bool small_radices(int M, int* f, int& nf) {
       x /= r;
     }
   return x == 1;
-}
-
-xc_status small_fused(const SmallOp& op, const SmallBlocks& sb, const double* X, int64_t ldx, double* Y, int64_t ldy,
-                      int B, int N, cudaStream_t st) {
-  const size_t smem = (size_t)((N + 1) / 2 + 3 * sb.maxM + 1) * sizeof(double2);
-  static std::atomic<unsigned long long> once{0};
-  if (first_on_device(once))
-    XC_CUDA(cudaFuncSetAttribute(small_fused_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(((kSmallFusedN + 1) / 2 + 3 * 1024 + 1) * sizeof(double2))));
-  const int nx = sb.nb + (sb.tr1 > sb.tr0 ? 1 : 0);
-  for (int c0 = 0; c0 < B; c0 += 65535) {
-    small_fused_k<<<dim3(nx, std::min(B - c0, 65535)), 256, smem, st>>>(op, sb, X + c0, ldx, Y + c0, ldy, N);
-    XC_CUDA(cudaGetLastError());
-  }
-  return XC_OK;
 }

@@ -356,15 +356,6 @@ xc_status ensure_ws(xc_op* h, int64_t B) {
   return XC_OK;
 }
 
-// The small path's one-launch form for B <= 8 columns (XC_SMALL_FUSED=0/1 forces): a CTA per
-// (block, column) stages its X column once -- beyond a few columns the two-launch form, whose
-// gather reads X rows coalesced across columns, is cheaper.  Both forms give the same bits.
-bool small_fused_for(const xc_op* h, int64_t B) {
-  static const int force = getenv("XC_SMALL_FUSED") ? atoi(getenv("XC_SMALL_FUSED")) : -1;
-  if (!h->small_on || h->N > kSmallFusedN) return false;
-  return force >= 0 ? force != 0 : B <= 8;
-}
-
 // Kernel launches of one apply of B columns (xc_launches; xc_info's counts are for B = 1).
 int64_t c2r_launches_b(const BlockData& b, int64_t B) { return c2r_launch_count(b.fftM, B); }
 int64_t count_launches(const xc_op* h, int dir, int64_t B) {
@@ -374,8 +365,9 @@ int64_t count_launches(const xc_op* h, int dir, int64_t B) {
     for (auto& b : h->blocks) n += ((b.fft.L2 > 1) ? 2 : 1) + c2r_launches_b(b, B);
     return n + 1 + (h->bsr_nred > 0 ? 1 : 0) + (h->tail > 0 ? 2 + (h->N > 128 ? 1 : 0) : 0);
   }
-  if (dir == XC_DIR_A && h->small_on)  // small_fused, or small_spmm + small_c2r (grid.y chunks)
-    return (small_fused_for(h, B) ? 1 : 2) * ((B + 65534) / 65535);
+  if (dir == XC_DIR_A && h->small_on) {  // small_spmm / small_c2r grid.y chunks
+    return 2 * ((B + 65534) / 65535);
+  }
   if (dir == XC_DIR_A) {
     if (!(h->dirs & XC_DIR_A)) return 0;
     n = spmm_launches(h->nwinsA) + (h->tail > 0 ? 1 : 0);
@@ -1320,21 +1312,6 @@ xc_status build_small(xc_op* h, cudaStream_t st) {
   std::vector<int> lr;
   for (int r = 0; r < rows; ++r)
     if (ptr[r + 1] - ptr[r] > kSmallLong) lr.push_back(r);
-  auto lrank = [&](int r) { return (int)(std::lower_bound(lr.begin(), lr.end(), r) - lr.begin()); };
-  {  // row and long-row ranges of every block and of the tail (the one-launch form)
-    int rb = 0;
-    for (size_t i = 0; i < h->blocks.size(); ++i) {
-      sb.blk[i].r0 = rb;
-      sb.blk[i].r1 = rb + h->blocks[i].H;
-      sb.blk[i].l0 = lrank(sb.blk[i].r0);
-      sb.blk[i].l1 = lrank(sb.blk[i].r1);
-      rb += h->blocks[i].H;
-    }
-    sb.tr0 = rb;
-    sb.tr1 = rows;
-    sb.tl0 = lrank(rb);
-    sb.tl1 = lrank(rows);
-  }
   XC_TRY(upload(h->sm_long, lr));
   h->sm_op = SmallOp{(const int64_t*)h->sm_ptr.p, (const int*)h->sm_node.p, (const double2*)h->sm_val.p,
                      (const int64_t*)h->sm_out.p, rows, (const int*)h->sm_long.p, (int)lr.size()};
@@ -1885,13 +1862,7 @@ xc_status apply_impl(xc_op* h, Ws& w, xc_dir dir, const double* X, int64_t ldx, 
     XC_TRY(mark(2));
     return mark(3);
   }
-  if (dir == XC_DIR_A && h->small_on) {  // small operators (small.cu)
-    if (small_fused_for(h, B)) {  // one launch (same bits as the two-launch form)
-      XC_TRY(small_fused(h->sm_op, h->sm_blocks, X, ldx, Y, ldy, (int)B, N, st));
-      XC_TRY(mark(1));
-      XC_TRY(mark(2));
-      return mark(3);
-    }
+  if (dir == XC_DIR_A && h->small_on) {  // small operators: two launches (small.cu)
     XC_TRY(small_spmm(h->sm_op, X, ldx, (double2*)w.partA, Bp, Y, ldy, (int)B, N, st));
     XC_TRY(mark(1));
     XC_TRY(small_c2r(h->sm_blocks, (const double2*)w.partA, Bp, Y, ldy, (int)B, st));

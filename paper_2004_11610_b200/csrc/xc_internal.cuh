@@ -362,8 +362,6 @@ struct SmallBlk {
   int M, nf, f[16];
   int m_off, keep_lo, keep_hi;
   int64_t urow;           // first complex u row of the block
-  int r0, r1;             // its rows in SmallOp (bins q = r - r0), and its long rows longrows[l0, l1)
-  int l0, l1;
   const double2* twh;     // e^{+i pi n / M}, n < M (pairing)
   const double2* twM;     // e^{+2 pi i n / M}, n < M (stage twiddles)
   const double* yscale;   // 1 / (sqrt(L) w_p)
@@ -371,16 +369,9 @@ struct SmallBlk {
 struct SmallBlocks {
   SmallBlk blk[kSmallMaxBlocks];
   int nb, maxM;
-  int tr0, tr1, tl0, tl1;  // the tail degrees' rows and long rows
 };
 xc_status small_spmm(const SmallOp& op, const double* X, int64_t ldx, double2* U, int64_t ldu, double* Y, int64_t ldy,
                      int B, int N, cudaStream_t st);
 xc_status small_c2r(const SmallBlocks& sb, const double2* U, int64_t ldu, double* Y, int64_t ldy, int B,
                     cudaStream_t st);
 bool small_radices(int M, int* f, int& nf);
-// The same computation in ONE launch for small batches: a CTA per (block, column) forms the block's
-// u in shared memory (the same per-row summation order, so the bits equal the two-launch form's)
-// and runs its C2R there; one more CTA per column forms the tail degrees.  N <= kSmallFusedN.
-constexpr int kSmallFusedN = 6144;
-xc_status small_fused(const SmallOp& op, const SmallBlocks& sb, const double* X, int64_t ldx, double* Y, int64_t ldy,
-                      int B, int N, cudaStream_t st);

@@ -1228,7 +1228,7 @@ SMALL_CASES = [("c1", (O.KIND_JACOBI, 0.0, 0.0), 512, 1, 1e-12, 0),
 @pytest.mark.parametrize("case", SMALL_CASES, ids=[c[0] for c in SMALL_CASES])
 def test_small_path_parity(case):
     """The small-operator path (apply_path = 2: a bin-major gather, then every block's C2R in
-    shared memory; one launch for B <= 8, two beyond, the same bits) and the tiled path (apply_path = 1) both meet 1e-12 against the
+    shared memory; two launches) and the tiled path (apply_path = 1) both meet 1e-12 against the
     oracle's compressed apply; auto is one of the two (small for M <= 1024); column results do not
     depend on the batch (shards equal the full run bit for bit)."""
     xc = _xc()
@@ -1243,7 +1243,7 @@ def test_small_path_parity(case):
         Y = T.apply(_gpu(X))
         assert O.rel_l2_cols(Y.cpu().numpy(), Ya).max() <= 1e-12, (name, path)
         if path == 2:
-            assert T.launches(B) == (1 if B <= 8 else 2)   # one launch for small batches
+            assert T.launches(B) == 2
             if B > 1:
                 assert torch.equal(T.apply(_gpu(X[:, 1:2])), Y[:, 1:2])
         Ys.append(Y)
