@@ -34,7 +34,7 @@ using namespace xcb;
 // Either way the order depends on the row only, never on B: a column's bits do not depend on the
 // batch it is applied in.
 template <bool STAGE>
-__global__ void __launch_bounds__(256) small_spmm_k(const SmallOp op, const double* __restrict__ X, int64_t ldx,
+__global__ void __launch_bounds__(256, 2) small_spmm_k(const SmallOp op, const double* __restrict__ X, int64_t ldx,
                                                     double2* __restrict__ U, int64_t ldu, double* __restrict__ Y,
                                                     int64_t ldy, int B, int CT, int N, int nshort, int ntile) {
   extern __shared__ double xs[];
@@ -47,7 +47,24 @@ __global__ void __launch_bounds__(256) small_spmm_k(const SmallOp op, const doub
     const int c = (int)(pair % B);
     const int64_t e0 = op.ptr[r], e1 = op.ptr[r + 1];
     double re = 0.0, im = 0.0;
-    for (int64_t e = e0 + lane; e < e1; e += 32) {
+    int64_t e = e0 + lane;
+    for (; e + 96 < e1; e += 128) {  // four of this lane's entries in flight, summed in order
+      const int k0 = __ldg(op.node + e), k1 = __ldg(op.node + e + 32), k2 = __ldg(op.node + e + 64),
+                k3 = __ldg(op.node + e + 96);
+      const double2 v0 = __ldg(op.val + e), v1 = __ldg(op.val + e + 32), v2 = __ldg(op.val + e + 64),
+                    v3 = __ldg(op.val + e + 96);
+      const double x0 = __ldg(X + (int64_t)k0 * ldx + c), x1 = __ldg(X + (int64_t)k1 * ldx + c);
+      const double x2 = __ldg(X + (int64_t)k2 * ldx + c), x3 = __ldg(X + (int64_t)k3 * ldx + c);
+      re = fma(v0.x, x0, re);
+      im = fma(v0.y, x0, im);
+      re = fma(v1.x, x1, re);
+      im = fma(v1.y, x1, im);
+      re = fma(v2.x, x2, re);
+      im = fma(v2.y, x2, im);
+      re = fma(v3.x, x3, re);
+      im = fma(v3.y, x3, im);
+    }
+    for (; e < e1; e += 32) {
       const double x = __ldg(X + (int64_t)__ldg(op.node + e) * ldx + c);
       const double2 v = __ldg(op.val + e);
       re = fma(v.x, x, re);
@@ -80,6 +97,23 @@ __global__ void __launch_bounds__(256) small_spmm_k(const SmallOp op, const doub
   auto xv = [&](int k) { return STAGE ? xs[k * CT + lc] : __ldg(X + (int64_t)k * ldx + c); };
   double re = 0.0, im = 0.0;
   int64_t e = e0;
+  for (; e + 8 <= e1; e += 8) {  // eight entries' loads in flight, summed in order
+    int k[8];
+    double2 v[8];
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      k[i] = __ldg(op.node + e + i);
+      v[i] = __ldg(op.val + e + i);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = xv(k[i]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      re = fma(v[i].x, x[i], re);
+      im = fma(v[i].y, x[i], im);
+    }
+  }
   for (; e + 4 <= e1; e += 4) {
     const int k0 = __ldg(op.node + e), k1 = __ldg(op.node + e + 1), k2 = __ldg(op.node + e + 2),
               k3 = __ldg(op.node + e + 3);
