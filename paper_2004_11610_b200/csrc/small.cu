@@ -39,22 +39,47 @@ __global__ void __launch_bounds__(256, 2) small_spmm_k(const SmallOp op, const d
                                                     int64_t ldy, int B, int CT, int N, int nshort, int ntile) {
   extern __shared__ double xs[];
   const int tid = threadIdx.x;
+  // launch 2 may start now: it only loads its tables before waiting for this grid to complete
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if ((int)blockIdx.x >= nshort) {  // long rows
     const int64_t pair = (int64_t)(blockIdx.x - nshort) * 8 + (tid >> 5);
     const int lane = tid & 31;
+    // a single column (B = 1, c1): X staged in shared memory like the short rows' CTAs
+    const bool stx = STAGE && B == 1;
+    if (stx) {
+      for (int i = tid; i < N; i += 256) xs[i] = __ldg(X + (int64_t)i * ldx);
+      __syncthreads();
+    }
     if (pair >= (int64_t)op.nlong * B) return;
     const int r = op.longrows[pair / B];
     const int c = (int)(pair % B);
+    auto xl = [&](int k) { return stx ? xs[k] : __ldg(X + (int64_t)k * ldx + c); };
     const int64_t e0 = op.ptr[r], e1 = op.ptr[r + 1];
     double re = 0.0, im = 0.0;
     int64_t e = e0 + lane;
-    for (; e + 96 < e1; e += 128) {  // four of this lane's entries in flight, summed in order
+    for (; e + 224 < e1; e += 256) {  // eight of this lane's entries in flight, summed in order
+      int k[8];
+      double2 v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        k[i] = __ldg(op.node + e + 32 * i);
+        v[i] = __ldg(op.val + e + 32 * i);
+      }
+      double x[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = xl(k[i]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        re = fma(v[i].x, x[i], re);
+        im = fma(v[i].y, x[i], im);
+      }
+    }
+    for (; e + 96 < e1; e += 128) {  // four in flight
       const int k0 = __ldg(op.node + e), k1 = __ldg(op.node + e + 32), k2 = __ldg(op.node + e + 64),
                 k3 = __ldg(op.node + e + 96);
       const double2 v0 = __ldg(op.val + e), v1 = __ldg(op.val + e + 32), v2 = __ldg(op.val + e + 64),
                     v3 = __ldg(op.val + e + 96);
-      const double x0 = __ldg(X + (int64_t)k0 * ldx + c), x1 = __ldg(X + (int64_t)k1 * ldx + c);
-      const double x2 = __ldg(X + (int64_t)k2 * ldx + c), x3 = __ldg(X + (int64_t)k3 * ldx + c);
+      const double x0 = xl(k0), x1 = xl(k1), x2 = xl(k2), x3 = xl(k3);
       re = fma(v0.x, x0, re);
       im = fma(v0.y, x0, im);
       re = fma(v1.x, x1, re);
@@ -65,7 +90,7 @@ __global__ void __launch_bounds__(256, 2) small_spmm_k(const SmallOp op, const d
       im = fma(v3.y, x3, im);
     }
     for (; e < e1; e += 32) {
-      const double x = __ldg(X + (int64_t)__ldg(op.node + e) * ldx + c);
+      const double x = xl(__ldg(op.node + e));
       const double2 v = __ldg(op.val + e);
       re = fma(v.x, x, re);
       im = fma(v.y, x, im);
@@ -161,7 +186,11 @@ __device__ __forceinline__ void small_stage(const double2* in, double2* out, con
   }
 }
 
-// launch 2: CTA (block i, column c).  Shared: A (H complex; u, then a ping-pong buffer), Bf (M).
+// launch 2: CTA (block i, column c).  Shared: A (H complex; u, then a ping-pong buffer), Bf (M), the
+// stage twiddles (M) and, with STG, the pairing twiddles (M) and the kept positions' scales.
+// Launched with programmatic dependent launch: everything that does not depend on u (the tables)
+// is loaded before griddepcontrol.wait, i.e. while launch 1 still runs.
+template <bool STG>
 __global__ void __launch_bounds__(1024) small_c2r_k(const SmallBlocks sb, const double2* __restrict__ U, int64_t ldu,
                                                    double* __restrict__ Y, int64_t ldy) {
   extern __shared__ double2 sm[];
@@ -171,13 +200,21 @@ __global__ void __launch_bounds__(1024) small_c2r_k(const SmallBlocks sb, const 
   double2* A = sm;
   double2* Bf = sm + b.M + 1;
   double2* tw = Bf + b.M;  // the stage twiddles e^{2 pi i n / M}, staged once (one coalesced pass)
+  double2* th = tw + b.M;  // STG: the pairing twiddles e^{i pi n / M}
+  double* ys = reinterpret_cast<double*>(th + b.M);  // STG: yscale[keep_lo + i]
+  for (int n = threadIdx.x; n < M; n += blockDim.x) {
+    tw[n] = __ldg(b.twM + n);
+    if (STG) th[n] = __ldg(b.twh + n);
+  }
+  if (STG)
+    for (int p = b.keep_lo + threadIdx.x; p < b.keep_hi; p += blockDim.x) ys[p - b.keep_lo] = __ldg(b.yscale + p);
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // launch 1's u (and tail rows) complete
   const double2* u = U + b.urow * ldu + c;
   for (int q = threadIdx.x; q <= M; q += blockDim.x) A[q] = u[(int64_t)q * ldu];
-  for (int n = threadIdx.x; n < M; n += blockDim.x) tw[n] = __ldg(b.twM + n);
   __syncthreads();
   // pairing: Z[n] = (u_n + conj u_{M-n}) + i e^{i pi n / M} (u_n - conj u_{M-n})
   for (int n = threadIdx.x; n < M; n += blockDim.x) {
-    const double2 a = A[n], p = A[M - n], w = __ldg(b.twh + n);
+    const double2 a = A[n], p = A[M - n], w = STG ? th[n] : __ldg(b.twh + n);
     const double evr = a.x + p.x, evi = a.y - p.y, dr = a.x - p.x, di = a.y + p.y;
     const double odr = dr * w.x - di * w.y, odi = dr * w.y + di * w.x;
     Bf[n] = make_double2(evr - odi, evi + odr);
@@ -206,7 +243,7 @@ __global__ void __launch_bounds__(1024) small_c2r_k(const SmallBlocks sb, const 
   // z_k = in[k]: v[2k] = Re z_k, v[2k+1] = Im z_k; Y[p + m_off] = v[p] yscale[p], p in [keep_lo, keep_hi)
   for (int p = b.keep_lo + threadIdx.x; p < b.keep_hi; p += blockDim.x) {
     const double2 z = in[p >> 1];
-    Y[(int64_t)(p + b.m_off) * ldy + c] = ((p & 1) ? z.y : z.x) * __ldg(b.yscale + p);
+    Y[(int64_t)(p + b.m_off) * ldy + c] = ((p & 1) ? z.y : z.x) * (STG ? ys[p - b.keep_lo] : __ldg(b.yscale + p));
   }
 }
 
@@ -238,15 +275,33 @@ xc_status small_spmm(const SmallOp& op, const double* X, int64_t ldx, double2* U
 xc_status small_c2r(const SmallBlocks& sb, const double2* U, int64_t ldu, double* Y, int64_t ldy, int B,
                     cudaStream_t st) {
   if (sb.nb == 0) return XC_OK;
-  const size_t smem = (size_t)(3 * sb.maxM + 1) * sizeof(double2);
+  int maxk = 0;  // the longest kept range
+  for (int i = 0; i < sb.nb; ++i) maxk = std::max(maxk, sb.blk[i].keep_hi - sb.blk[i].keep_lo);
+  const size_t base = (size_t)(3 * sb.maxM + 1) * sizeof(double2);
+  const size_t full = base + (size_t)sb.maxM * sizeof(double2) + (size_t)maxk * sizeof(double);
+  const bool stg = full <= 200 * 1024;
+  const size_t smem = stg ? full : base;
   static std::atomic<unsigned long long> once{0};
-  if (first_on_device(once))
-    XC_CUDA(cudaFuncSetAttribute(small_c2r_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (first_on_device(once)) {
+    XC_CUDA(cudaFuncSetAttribute(small_c2r_k<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (3 * kSmallMaxM + 1) * (int)sizeof(double2)));
+    XC_CUDA(cudaFuncSetAttribute(small_c2r_k<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  }
   const int nth = sb.maxM >= 2048 ? 1024 : (sb.maxM >= 512 ? 512 : 256);  // one CTA per column: latency
   for (int c0 = 0; c0 < B; c0 += 65535) {  // grid.y limit
-    small_c2r_k<<<dim3(sb.nb, std::min(B - c0, 65535)), nth, smem, st>>>(sb, U + c0, ldu, Y + c0, ldy);
-    XC_CUDA(cudaGetLastError());
+    // programmatic dependent launch on the gather (launch 1) that precedes it on the stream
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(sb.nb, std::min(B - c0, 65535));
+    cfg.blockDim = dim3(nth);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (stg) XC_CUDA(cudaLaunchKernelEx(&cfg, small_c2r_k<true>, sb, U + c0, ldu, Y + c0, ldy));
+    else XC_CUDA(cudaLaunchKernelEx(&cfg, small_c2r_k<false>, sb, U + c0, ldu, Y + c0, ldy));
   }
   return XC_OK;
 }

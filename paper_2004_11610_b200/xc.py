@@ -317,6 +317,8 @@ class Transform:
     def apply(self, X, direction: int = XC_DIR_A, out=None, stream=None):
         """Y = A X (XC_DIR_A) or diag(wt) A^T X (XC_DIR_WAT); X a CUDA fp64 tensor (N x B)."""
         import torch
+        # argument checks only (cheap attribute reads: for the microsecond-scale configs the
+        # binding's own cost is part of every call)
         if not (isinstance(X, torch.Tensor) and X.is_cuda and X.dtype == torch.float64 and X.dim() == 2):
             raise XcError("X must be a 2-D CUDA float64 tensor")
         if X.stride(1) != 1:
@@ -325,25 +327,31 @@ class Transform:
         rin, rout = self.rows(direction)
         if N != rin:
             raise XcError(f"X has {N} rows, transform needs {rin}")
+        dev = X.get_device()
         if out is None:
             out = torch.empty((rout, B), dtype=torch.float64, device=X.device)
         elif not (isinstance(out, torch.Tensor) and out.is_cuda and out.dtype == torch.float64 and out.dim() == 2
-                  and tuple(out.shape) == (rout, B) and out.device == X.device and out.stride(1) == 1
-                  and out.stride(0) >= B):
+                  and out.shape[0] == rout and out.shape[1] == B and out.get_device() == dev
+                  and out.stride(1) == 1 and out.stride(0) >= B):
             raise XcError(f"out must be a CUDA float64 tensor of shape ({rout}, {B}) on {X.device} with "
                           f"unit column stride")
-        st = stream if stream is not None else torch.cuda.current_stream(X.device).cuda_stream
-        if st not in self._attached and B > self._reserved:   # xc_apply itself never allocates
+        st = stream if stream is not None else torch._C._cuda_getCurrentRawStream(dev)
+        if B > self._reserved and st not in self._attached:   # xc_apply itself never allocates
             self.reserve(B)
-        _check(self._lib.xc_apply(self._h, direction, ctypes.c_void_p(X.data_ptr()), X.stride(0),
-                                  ctypes.c_void_p(out.data_ptr()), out.stride(0), B, ctypes.c_void_p(st)))
+        rc = self._lib.xc_apply(self._h, direction, X.data_ptr(), X.stride(0), out.data_ptr(), out.stride(0), B, st)
+        if rc:
+            _check(rc)
         return out
 
     def rows(self, direction: int = XC_DIR_A):
         """(rows of X, rows of Y) of an apply: nodes N / degrees M by direction, twice for the
         planar complex kinds."""
-        cf = 2 if self.kind in COMPLEX_KINDS else 1
-        return (cf * self.N, cf * self.M) if direction == XC_DIR_A else (cf * self.M, cf * self.N)
+        r = self.__dict__.get("_rows_cache")
+        if r is None or r[0] != (self.kind, self.N, self.M):
+            cf = 2 if self.kind in COMPLEX_KINDS else 1
+            r = ((self.kind, self.N, self.M), (cf * self.N, cf * self.M), (cf * self.M, cf * self.N))
+            self._rows_cache = r
+        return r[1] if direction == XC_DIR_A else r[2]
 
     def apply_complex(self, Xc, direction: int = XC_DIR_A, stream=None):
         """Complex kinds with a complex128 CUDA tensor: marshalled to and from the planar layout
