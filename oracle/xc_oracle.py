@@ -395,18 +395,69 @@ def make_plan(kind: Kind, N: int, eps: float, eps1: float | None = None, eps2: f
 # ---------------------------------------------------------------------------
 # Compression (precomputation stage)
 # ---------------------------------------------------------------------------
-def node_spectra(plan: Plan, blk: Block, nodes: np.ndarray) -> np.ndarray:
+# ---------------------------------------------------------------------------
+# The DFT step written out (BASELINE north star: "the compressed algorithm with a naive DFT").
+# Eq. 1: (F f)_q = (1/sqrt(L)) sum_p f_p e^{-2 pi i p q / L}; F* has the + sign.  The
+# twiddle of p q is taken at the exactly reduced index (p q mod L) from a table evaluated in long
+# double, and the O(L^2) sum is one matrix product.  dft="fft" (default) uses numpy's FFT for the
+# same step; the two are pinned against each other in tests/test_oracle_pins.py.
+# ---------------------------------------------------------------------------
+NAIVE_MAX_L = 4096
+
+
+@functools.lru_cache(maxsize=6)
+def _dft_matrix(L: int, sign: int) -> np.ndarray:
+    """F[q, p] = e^{sign 2 pi i (p q mod L) / L} / sqrt(L) (L x L, complex128)."""
+    if L > NAIVE_MAX_L:
+        raise ValueError(f"naive DFT limited to L <= {NAIVE_MAX_L} (O(L^2) memory)")
+    m = np.arange(L, dtype=np.longdouble)
+    # angles in long double: 2 pi m / L with pi to long-double precision
+    pi_l = np.longdouble("3.14159265358979323846264338327950288")
+    ang = 2 * pi_l * m / np.longdouble(L)
+    tw = (np.cos(ang) + sign * 1j * np.sin(ang)).astype(np.complex128)
+    idx = np.outer(np.arange(L, dtype=np.int64), np.arange(L, dtype=np.int64)) % L
+    return tw[idx] / math.sqrt(L)
+
+
+def naive_dft(x: np.ndarray, sign: int, axis: int = 0) -> np.ndarray:
+    """Unitary DFT of length L = x.shape[axis] by the direct sum (sign -1: F, +1: F*)."""
+    x = np.moveaxis(np.asarray(x, dtype=np.complex128), axis, 0)
+    y = _dft_matrix(x.shape[0], sign) @ x.reshape(x.shape[0], -1)
+    return np.moveaxis(y.reshape(x.shape), 0, axis)
+
+
+def _half_to_real_inverse(u: np.ndarray, L: int, dft: str) -> np.ndarray:
+    """v = F* U (real), U the Hermitian spectrum whose bins 0..L/2 are u (rows)."""
+    if dft == "fft":
+        return np.fft.irfft(u, n=L, axis=0, norm="ortho")
+    H = u.shape[0]
+    U = np.zeros((L,) + u.shape[1:], dtype=np.complex128)
+    U[:H] = u
+    U[0] = U[0].real                                   # bins 0 and L/2 of a real signal are real
+    if L % 2 == 0:
+        U[L // 2] = U[L // 2].real
+    U[L - np.arange(1, (L + 1) // 2)] = np.conj(u[1:(L + 1) // 2])
+    return naive_dft(U, +1, axis=0).real
+
+
+def node_spectra(plan: Plan, blk: Block, nodes: np.ndarray, dft: str = "fft") -> np.ndarray:
     """S[k, q] = (F W e_k)_q: unitary DFT (Eq. 1) of the windowed extended row of node k.
 
     Returns the half spectrum q in [0, H) (real rows).  Bins 0 and L/2
     are real by symmetry and their imaginary part is set to exactly 0.  Kind EXP (complex
-    rows): the full spectrum q in [0, L).
+    rows): the full spectrum q in [0, L).  dft="naive": the direct sum (naive_dft).
     """
     w = kaiser(plan.zeta, blk.L - 1)
     E = entries(plan.kind, nodes, 0, blk.L, blk.m_off)          # E[k, p] = phi_{p+m_off}(x_k)
-    if is_complex(plan.kind):                                   # complex rows: the full spectrum
+    if dft == "naive":
+        S = naive_dft(E * w[None, :], -1, axis=1)
+        if is_complex(plan.kind):
+            return S
+        S = S[:, :blk.H].copy()
+    elif is_complex(plan.kind):                                 # complex rows: the full spectrum
         return np.fft.fft(E * w[None, :], axis=1, norm="ortho")
-    S = np.fft.rfft(E * w[None, :], axis=1, norm="ortho")      # e^{-2 pi i p q / L} / sqrt(L)
+    else:
+        S = np.fft.rfft(E * w[None, :], axis=1, norm="ortho")  # e^{-2 pi i p q / L} / sqrt(L)
     S[:, 0] = S[:, 0].real
     S[:, -1] = S[:, -1].real
     return S
@@ -434,7 +485,8 @@ def threshold_global(S: np.ndarray, eps1: float, gmax2: float) -> np.ndarray:
     return np.where(mag2 >= (eps1 * eps1) * gmax2, S, 0.0)
 
 
-def compress(plan: Plan, nodes: np.ndarray, node_chunk: int = 512, thresh_mode: int = 0) -> Operator:
+def compress(plan: Plan, nodes: np.ndarray, node_chunk: int = 512, thresh_mode: int = 0,
+             dft: str = "fft") -> Operator:
     """The compressed operator of every block.  thresh_mode 0: the per-node
     relative threshold (reading R-3); 1: the global threshold of step 1.3 -- a first
     pass over the nodes finds the block's max |S|, the second thresholds."""
@@ -444,10 +496,10 @@ def compress(plan: Plan, nodes: np.ndarray, node_chunk: int = 512, thresh_mode: 
         gmax2 = 0.0
         if thresh_mode == 1:
             for k0 in range(0, plan.N, node_chunk):
-                S = node_spectra(plan, blk, nodes[k0:k0 + node_chunk])
+                S = node_spectra(plan, blk, nodes[k0:k0 + node_chunk], dft)
                 gmax2 = max(gmax2, float((S.real ** 2 + S.imag ** 2).max()))
         for k0 in range(0, plan.N, node_chunk):
-            S = node_spectra(plan, blk, nodes[k0:k0 + node_chunk])
+            S = node_spectra(plan, blk, nodes[k0:k0 + node_chunk], dft)
             Sk = threshold_global(S, plan.eps1, gmax2) if thresh_mode == 1 else threshold(S, plan.eps1)
             parts.append(sp.csr_matrix(Sk))
         S_list.append(sp.vstack(parts).tocsr())
@@ -634,19 +686,20 @@ def nnz_2d(op: Operator2D, half: bool = True) -> int:
 # ---------------------------------------------------------------------------
 # Computation stage
 # ---------------------------------------------------------------------------
-def apply_output_axis(op: Operator, X: np.ndarray) -> np.ndarray:
+def apply_output_axis(op: Operator, X: np.ndarray, dft: str = "fft") -> np.ndarray:
     """Y = A X, output indexed by degree (Alg. 2; block form P:281).
 
     Per block: u = S^T X (sparse), v = F* u (unitary inverse DFT, real
     output), Y[kept] = v[kept] / w[kept]; the extra positions are discarded
-    (Fe2).  Tail degrees by the direct method.
+    (Fe2).  Tail degrees by the direct method.  dft="naive": the inverse
+    DFT by the direct sum (naive_dft), blocks with L <= NAIVE_MAX_L.
     """
     if is_complex(op.plan.kind):                                # complex input and output
         X = np.asarray(X, dtype=np.complex128)
         Y = np.zeros((op.plan.rows, X.shape[1]), dtype=np.complex128)
         for blk, S, w in zip(op.plan.blocks, op.S, op.windows):
             u = S.T @ X                                         # (L x B): full spectrum
-            v = np.fft.ifft(u, axis=0, norm="ortho")            # e^{+2 pi i p q / L} / sqrt(L)
+            v = naive_dft(u, +1) if dft == "naive" else np.fft.ifft(u, axis=0, norm="ortho")
             lo, hi = blk.keep_lo, blk.keep_hi
             Y[lo + blk.m_off:hi + blk.m_off] = v[lo:hi] / w[lo:hi, None]
         return Y
@@ -655,7 +708,7 @@ def apply_output_axis(op: Operator, X: np.ndarray) -> np.ndarray:
     Y = np.zeros((N, B))
     for blk, S, w in zip(op.plan.blocks, op.S, op.windows):
         u = S.T @ X                                             # (H x B) complex
-        v = np.fft.irfft(u, n=blk.L, axis=0, norm="ortho")      # e^{+2 pi i p q / L} / sqrt(L)
+        v = _half_to_real_inverse(u, blk.L, dft)                # e^{+2 pi i p q / L} / sqrt(L)
         lo, hi = blk.keep_lo, blk.keep_hi
         Y[lo + blk.m_off:hi + blk.m_off] = v[lo:hi] / w[lo:hi, None]
     if op.plan.tail:
@@ -663,7 +716,7 @@ def apply_output_axis(op: Operator, X: np.ndarray) -> np.ndarray:
     return Y
 
 
-def apply_input_axis(op: Operator, C: np.ndarray, wt: np.ndarray | None = None) -> np.ndarray:
+def apply_input_axis(op: Operator, C: np.ndarray, wt: np.ndarray | None = None, dft: str = "fft") -> np.ndarray:
     """Y = diag(wt) A^T C, input indexed by degree (Alg. 1; block form P:281-301).
 
     Per block: z = pad(C) / w (zeros outside the kept range, Fe1/Fe3), z' = F* z,
@@ -678,7 +731,8 @@ def apply_input_axis(op: Operator, C: np.ndarray, wt: np.ndarray | None = None) 
             z = np.zeros((blk.L, B), dtype=np.complex128)
             lo, hi = blk.keep_lo, blk.keep_hi
             z[lo:hi] = C[lo + blk.m_off:hi + blk.m_off] / w[lo:hi, None]
-            Y += S @ np.fft.ifft(z, axis=0, norm="ortho")       # sum_q S[k,q] (F* z)_q
+            zf = naive_dft(z, +1) if dft == "naive" else np.fft.ifft(z, axis=0, norm="ortho")
+            Y += S @ zf                                         # sum_q S[k,q] (F* z)_q
         if wt is not None:
             Y *= wt[:, None]
         return Y
@@ -689,7 +743,10 @@ def apply_input_axis(op: Operator, C: np.ndarray, wt: np.ndarray | None = None) 
         z = np.zeros((blk.L, B))
         lo, hi = blk.keep_lo, blk.keep_hi
         z[lo:hi] = C[lo + blk.m_off:hi + blk.m_off] / w[lo:hi, None]
-        zq = np.conj(np.fft.rfft(z, axis=0, norm="ortho"))     # (F* z)_q, q in [0, H)
+        if dft == "naive":
+            zq = naive_dft(z, +1)[:blk.H]                       # (F* z)_q, q in [0, H)
+        else:
+            zq = np.conj(np.fft.rfft(z, axis=0, norm="ortho"))  # (F* z)_q, q in [0, H)
         c = np.full(blk.H, 2.0)
         c[0] = 1.0
         c[-1] = 1.0

@@ -151,6 +151,37 @@ def test_input_axis_parity_small(kt, N):
     T.close()
 
 
+NAIVE_CASES = [
+    ("c1", (O.KIND_JACOBI, 0.0, 0.0), 512, 1, 1e-12, 0, "A"),
+    ("c1_ragged", (O.KIND_JACOBI, 0.0, 0.0), 512, 37, 1e-12, 0, "A"),
+    ("jacobi_wat", (O.KIND_JACOBI, 0.5, -0.3), 600, 21, 1e-12, 2, "WAT"),
+    ("cos_1000", (O.KIND_COS, 0.0, 0.0), 1000, 33, 1e-10, 1, "A"),
+]
+
+
+@pytest.mark.parametrize("case", NAIVE_CASES, ids=[c[0] for c in NAIVE_CASES])
+def test_vs_naive_dft_oracle(case):
+    """BASELINE's oracle to the letter: the compressed algorithm with a NAIVE DFT (O(L^2) sums of
+    Eq. 1) in the precompute and in the computation stage (P:201 / P:218); the
+    GPU apply (its own precompute, through the C ABI) meets 1e-12 against it."""
+    xc = _xc()
+    name, kt, N, B, eps, seed, d = case
+    x, w = _nodes(kt, N, seed)
+    op = O.compress(O.make_plan(O.Kind(*kt), N, eps), x, dft="naive")
+    X = I.rhs(N, B, seed + 300)
+    if d == "A":
+        T = xc.Transform(kt[0], x, eps, alpha=kt[1], beta=kt[2])
+        Y = T.apply(_gpu(X)).cpu().numpy()
+        ref = O.apply_output_axis(op, X, dft="naive")
+    else:
+        w = np.ones(N) if w is None else w
+        T = xc.Transform(kt[0], x, eps, alpha=kt[1], beta=kt[2], dirs=xc.XC_DIR_WAT, weights=w)
+        Y = T.apply(_gpu(X), xc.XC_DIR_WAT).cpu().numpy()
+        ref = O.apply_input_axis(op, X, w, dft="naive")
+    assert O.rel_l2_cols(Y, ref).max() <= 1e-12, name
+    T.close()
+
+
 @pytest.mark.slow
 def test_c5_sampled():
     """c5 at full size (N = 65536, bench launch configuration B = 4096): 16 sampled columns

@@ -932,3 +932,54 @@ def test_global_threshold_keep_all_and_error():
     plan0.eps1 = 0.0
     e0 = O.rel_l2_cols(O.apply_output_axis(O.compress(plan0, x, thresh_mode=1), X), Yd).max()
     assert e0 < 1e-13
+
+
+# --------------------------------------------------------------------------- naive DFT step
+@pytest.mark.parametrize("L", [30, 108, 288, 720, 2250])
+def test_naive_dft_vs_library_fft(L):
+    """The oracle's written-out DFT step (naive_dft: the O(L^2) sum of Eq. 1, exactly reduced
+    twiddle indices) against numpy's FFT, both signs, and the unitary round trip F* F = I."""
+    rng = np.random.default_rng(L)
+    x = rng.standard_normal((L, 3)) + 1j * rng.standard_normal((L, 3))
+    f = O.naive_dft(x, -1)
+    g = O.naive_dft(x, +1)
+    assert np.abs(f - np.fft.fft(x, axis=0, norm="ortho")).max() <= 1e-14 * np.abs(f).max() * math.log2(L)
+    assert np.abs(g - np.fft.ifft(x, axis=0, norm="ortho")).max() <= 1e-14 * np.abs(g).max() * math.log2(L)
+    assert np.abs(O.naive_dft(f, +1) - x).max() <= 1e-13
+    d = np.zeros(L, complex)
+    d[1] = 1.0
+    assert np.allclose(O.naive_dft(d, -1), np.exp(-2j * np.pi * np.arange(L) / L) / math.sqrt(L), atol=1e-15)
+
+
+@pytest.mark.parametrize("kind,dirs", [(LEG, "A"), (JAC, "AW"), (COS, "A")])
+def test_compressed_algorithm_with_naive_dft(kind, dirs):
+    """BASELINE's oracle as written: the compressed algorithm with a naive DFT, in both steps where
+    the method takes one (precompute S = F W e_k; apply v = F* u, P:218 / z' = F* z,
+    P:201).  At c1's size (N = 512, blocks L = 720, 288, 108) it builds the same kept sets as the
+    library-FFT form (up to threshold ties) with entries equal to 1e-14 of each node's max, applies
+    to 1e-14 of it on either operator, and meets the 10 eps bar against the dense product."""
+    N, eps = 512, 1e-12
+    if kind.kind == O.KIND_COS:
+        x, wt = I.cos_nodes(N, 1), None
+    else:
+        x, _, wt = O.gauss_rule(kind, N)
+    plan = O.make_plan(kind, N, eps)
+    opf = O.compress(plan, x)
+    opn = O.compress(plan, x, dft="naive")
+    for Sf, Sn in zip(opf.S, opn.S):
+        A, B = Sf.toarray(), Sn.toarray()
+        m = np.abs(A).max(axis=1, keepdims=True)
+        both = (A != 0) & (B != 0)
+        assert np.all(np.abs(A - B)[both] <= 1e-14 * np.broadcast_to(m, A.shape)[both])
+        flip = (A != 0) != (B != 0)                                # ties at the threshold only
+        assert np.all(np.abs(np.where(flip, A + B, 0)) <= plan.eps1 * m * (1 + 1e-10))
+    X = I.rhs(N, 4, 0)
+    ref = O.apply_output_axis(opf, X)
+    Yn = O.apply_output_axis(opn, X, dft="naive")
+    assert O.rel_l2_cols(O.apply_output_axis(opf, X, dft="naive"), ref).max() <= 1e-14
+    assert O.rel_l2_cols(Yn, ref).max() <= 1e-13
+    assert O.rel_l2_cols(Yn, O.dense_apply(kind, x, X)).max() <= 10 * eps
+    if "W" in dirs:
+        C = I.rhs(N, 4, 1)
+        r = O.apply_input_axis(opf, C, wt)
+        assert O.rel_l2_cols(O.apply_input_axis(opf, C, wt, dft="naive"), r).max() <= 1e-14
