@@ -220,13 +220,11 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
             double v2 = acc[mt][2 * m][1], v3 = acc[mt][2 * m + 1][1];
             double s0 = odd ? v0 : v2, s1 = odd ? v1 : v3;
             double r0 = __shfl_xor_sync(0xffffffffu, s0, 4), r1 = __shfl_xor_sync(0xffffffffu, s1, 4);
-            if (!odd) {
-              __stcs(crow + c, make_double2(v0, r0));
-              __stcs(crow + c + 1, make_double2(v1, r1));
-            } else {
-              __stcs(crow + c + 2, make_double2(r0, v2));
-              __stcs(crow + c + 3, make_double2(r1, v3));
-            }
+            // one 32-byte store per lane (two adjacent complex numbers; STG.256 on sm_100)
+            double* q = reinterpret_cast<double*>(crow + c + (odd ? 2 : 0));
+            const double q0 = odd ? r0 : v0, q1 = odd ? v2 : r0, q2 = odd ? r1 : v1, q3 = odd ? v3 : r1;
+            asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(q), "d"(q0), "d"(q1), "d"(q2), "d"(q3)
+                         : "memory");
           }
         }
       } else {
@@ -239,8 +237,9 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
 #pragma unroll
           for (int m = 0; m < NT / 2; ++m) {
             int c = tile0 + 16 * m + 4 * t;
-            __stcs(reinterpret_cast<double2*>(orow + c), make_double2(acc[mt][2 * m][0], acc[mt][2 * m + 1][0]));
-            __stcs(reinterpret_cast<double2*>(orow + c + 2), make_double2(acc[mt][2 * m][1], acc[mt][2 * m + 1][1]));
+            asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(orow + c), "d"(acc[mt][2 * m][0]),
+                         "d"(acc[mt][2 * m + 1][0]), "d"(acc[mt][2 * m][1]), "d"(acc[mt][2 * m + 1][1])
+                         : "memory");
           }
         }
       }
