@@ -11,7 +11,10 @@
 //     node = 8g + row, q = k0 + 2s + kk/2
 // and its tail A[row][kk] = phi_{k0+4s+kk}(x_{8g+row}).
 // In every case lane l of a warp holds A[l/4][l%4] (spmm.cu); an item carries two M-tiles
-// (or one), interleaved per lane; each M-tile is filled from its own family's bands.
+// (or one), interleaved per lane; each M-tile is filled from its own family's bands.  Steps come
+// in pairs: steps 2k, 2k+1 of lane l are the 4 doubles at a_off + 128 k + 4 l (slot 0, slot 1 of
+// step 2k, then of step 2k+1), one 32-byte load per lane for two steps (an odd step count is
+// padded with a zero step).
 #include "build.h"
 #include "xc_internal.cuh"
 
@@ -31,6 +34,10 @@ __device__ __forceinline__ double band_val(int k, int q, int comp, int H, const 
   return comp ? v.y : v.x;
 }
 
+__device__ __forceinline__ int64_t tile_at(int64_t a_off, int s, int lane, int mt) {
+  return a_off + 64 * (s & ~1) + 4 * lane + 2 * (s & 1) + mt;
+}
+
 // lane l of a warp holds A[l/4][l%4] of each M-tile: row r = l/4, B row R = k0 + 4s + l%4
 template <int MODE>
 __global__ void fill_k(const FillItem* fi, const int* start, const int* len, const int64_t* off,
@@ -42,7 +49,7 @@ __global__ void fill_k(const FillItem* fi, const int* start, const int* len, con
     const int R = it.k0 + 4 * s + (lane & 3);
     const int r = lane >> 2;
     if (R < it.lo || R >= it.hi) {
-      tiles[it.a_off + 64 * s + 2 * lane + it.mt] = 0.0;
+      tiles[tile_at(it.a_off, s, lane, it.mt)] = 0.0;
       continue;
     }
     if (MODE == FILL_OUT_CPLX) {        // node R, bin 4 gm + r/2, component r&1
@@ -76,7 +83,7 @@ __global__ void fill_k(const FillItem* fi, const int* start, const int* len, con
       int node = 8 * gm + r;
       if (node < N && R < t) v = P[(int64_t)R * N + node];
     }
-    tiles[it.a_off + 64 * s + 2 * lane + it.mt] = v;
+    tiles[tile_at(it.a_off, s, lane, it.mt)] = v;
   }
 }
 

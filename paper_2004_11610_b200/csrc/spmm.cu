@@ -34,6 +34,13 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 
 constexpr int WARPS = XC_WARPS;  // warps per CTA
 
+// 32-byte read-only load (LDG.256 on sm_100)
+__device__ __forceinline__ double4 ldg4(const double* p) {
+  double4 v;
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+
 // One CTA = one window of B rows [r0, r1) (<= XC_WMAX) x one tile of 8*NT right-hand sides.
 // The window's rows are staged once in shared memory; the window's items (all families whose
 // B rows lie inside it) are spread over the warps.  Each item holds 2 M-tiles sharing the B
@@ -148,49 +155,45 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
     if (n > 0) lds_b(0, b0);
     if (it.out_row[1] >= 0) {
       // two M-tiles sharing the B fragments
-      // A fragments streamed four steps ahead
-      const double2* ap = reinterpret_cast<const double2*>(tiles + it.a_off) + lane;
-      const double2 z2 = make_double2(0.0, 0.0);
-      double2 a0 = n > 0 ? __ldg(ap) : z2, a1 = n > 1 ? __ldg(ap + 32) : z2;
-      double2 a2 = n > 2 ? __ldg(ap + 64) : z2, a3 = n > 3 ? __ldg(ap + 96) : z2;
+      // A fragments streamed four steps ahead, two steps per 32-byte load (the tile stream holds
+      // steps 2k, 2k+1 of a lane as (slot 0, slot 1, slot 0, slot 1): build.cu)
+      const double* ap = tiles + it.a_off + 4 * lane;
+      const double4 z4 = make_double4(0.0, 0.0, 0.0, 0.0);
+      double4 a01 = n > 0 ? ldg4(ap) : z4, a23 = n > 2 ? ldg4(ap + 128) : z4;
       for (int s = 0; s < n; s += 2) {
         if (s + 1 < n) lds_b(s + 1, b1);
 #pragma unroll
         for (int i = 0; i < NT; ++i) {
-          dmma(acc[0][i][0], acc[0][i][1], a0.x, b0[i]);
-          dmma(acc[1][i][0], acc[1][i][1], a0.y, b0[i]);
+          dmma(acc[0][i][0], acc[0][i][1], a01.x, b0[i]);
+          dmma(acc[1][i][0], acc[1][i][1], a01.y, b0[i]);
         }
-        a0 = a2;
-        a2 = (s + 4 < n) ? __ldg(ap + 32 * (s + 4)) : z2;
         if (s + 1 < n) {
           if (s + 2 < n) lds_b(s + 2, b0);
 #pragma unroll
           for (int i = 0; i < NT; ++i) {
-            dmma(acc[0][i][0], acc[0][i][1], a1.x, b1[i]);
-            dmma(acc[1][i][0], acc[1][i][1], a1.y, b1[i]);
+            dmma(acc[0][i][0], acc[0][i][1], a01.z, b1[i]);
+            dmma(acc[1][i][0], acc[1][i][1], a01.w, b1[i]);
           }
-          a1 = a3;
-          a3 = (s + 5 < n) ? __ldg(ap + 32 * (s + 5)) : z2;
         }
+        a01 = a23;
+        a23 = (s + 4 < n) ? ldg4(ap + 64 * (s + 4)) : z4;
       }
     } else {
-      // one M-tile (slot 0 of the A stream), A fragments streamed 4 steps ahead
-      const double* ap = tiles + it.a_off + 2 * lane;
-      double a0 = n > 0 ? __ldg(ap) : 0.0, a1 = n > 1 ? __ldg(ap + 64) : 0.0;
-      double a2 = n > 2 ? __ldg(ap + 128) : 0.0, a3 = n > 3 ? __ldg(ap + 192) : 0.0;
+      // one M-tile (slot 0 of the A stream), A fragments streamed 4 steps ahead, two per load
+      const double* ap = tiles + it.a_off + 4 * lane;
+      const double4 z4 = make_double4(0.0, 0.0, 0.0, 0.0);
+      double4 a01 = n > 0 ? ldg4(ap) : z4, a23 = n > 2 ? ldg4(ap + 128) : z4;
       for (int s = 0; s < n; s += 2) {
         if (s + 1 < n) lds_b(s + 1, b1);
 #pragma unroll
-        for (int i = 0; i < NT; ++i) dmma(acc[0][i][0], acc[0][i][1], a0, b0[i]);
-        a0 = a2;
-        a2 = (s + 4 < n) ? __ldg(ap + 64 * (s + 4)) : 0.0;
+        for (int i = 0; i < NT; ++i) dmma(acc[0][i][0], acc[0][i][1], a01.x, b0[i]);
         if (s + 1 < n) {
           if (s + 2 < n) lds_b(s + 2, b0);
 #pragma unroll
-          for (int i = 0; i < NT; ++i) dmma(acc[0][i][0], acc[0][i][1], a1, b1[i]);
-          a1 = a3;
-          a3 = (s + 5 < n) ? __ldg(ap + 64 * (s + 5)) : 0.0;
+          for (int i = 0; i < NT; ++i) dmma(acc[0][i][0], acc[0][i][1], a01.z, b1[i]);
         }
+        a01 = a23;
+        a23 = (s + 4 < n) ? ldg4(ap + 64 * (s + 4)) : z4;
       }
     }
 

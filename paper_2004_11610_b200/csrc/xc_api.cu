@@ -720,7 +720,7 @@ void emit_item(const MTile& a, const MTile* b, int src, ItemSet& out) {
     out.fills.push_back(FillItem{out.aoff, it.k0, it.nsteps, b->g, 1, b->k0, b->k1});
     out.fam.push_back(b->fam);
   }
-  out.aoff += 64LL * it.nsteps;
+  out.aoff += 64LL * ((it.nsteps + 1) & ~1);  // steps in pairs (build.cu)
 }
 
 // Pair neighbours of an ordered list greedily where worth it.
