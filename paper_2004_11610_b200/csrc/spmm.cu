@@ -33,6 +33,9 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 
 constexpr int WARPS = XC_WARPS;  // warps per CTA
+// zero rows staged after every window: a step past an item's end (the zero A step that pads an odd
+// step count, the B-fragment load one step ahead) reads them, so the step loop has no branches
+constexpr int kPadRows = 8;
 
 // 32-byte read-only load (LDG.256 on sm_100)
 __device__ __forceinline__ double4 ldg4(const double* p) {
@@ -61,7 +64,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
   W.i1 = wins[blockIdx.y].i1;
   W.src = wins[blockIdx.y].src;
   // the window's item descriptors, staged next to the X window (8-byte cp.async pieces)
-  SpmmItem* its = reinterpret_cast<SpmmItem*>(xs2 + XC_WMAX * ((8 * NT + 4) / 2));
+  SpmmItem* its = reinterpret_cast<SpmmItem*>(xs2 + (XC_WMAX + kPadRows) * ((8 * NT + 4) / 2));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = lane & 3, g = lane >> 2;
   const int tile0 = blockIdx.x * CW;
@@ -78,24 +81,25 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
     if (vec) {
       // cp.async: every 16-byte piece of the window in flight at once (no register round trip;
       // rows past the source are zero-filled)
-      for (int idx = tid; idx < nr * (CW / 2); idx += WARPS * 32) {
+      for (int idx = tid; idx < (nr + kPadRows) * (CW / 2); idx += WARPS * 32) {
         int rl = idx / (CW / 2), c2 = idx - rl * (CW / 2);
         int R = W.r0 + rl;
         int row = im ? (R >> 1) : R;
         const double* src = (im && (R & 1)) ? im : re;
-        const bool ok = row < nrows;
+        const bool ok = row < nrows && rl < nr;
         const double2* g = reinterpret_cast<const double2*>(src + (int64_t)(ok ? row : 0) * ld + tile0) + c2;
         const unsigned sa = (unsigned)__cvta_generic_to_shared(&xs2[rl * (CWP / 2) + c2]);
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 16 : 0));
       }
     } else {
       double* xw = reinterpret_cast<double*>(xs2);
-      for (int idx = tid; idx < nr * CW; idx += WARPS * 32) {
+      for (int idx = tid; idx < (nr + kPadRows) * CW; idx += WARPS * 32) {
         int rl = idx / CW, c = idx - rl * CW;
         int R = W.r0 + rl;
         int row = im ? (R >> 1) : R;
         const double* src = (im && (R & 1)) ? im : re;
-        xw[rl * CWP + c] = (row < nrows && tile0 + c < ncols) ? __ldg(src + (int64_t)row * ld + tile0 + c) : 0.0;
+        xw[rl * CWP + c] =
+            (rl < nr && row < nrows && tile0 + c < ncols) ? __ldg(src + (int64_t)row * ld + tile0 + c) : 0.0;
       }
     }
     constexpr int IW = sizeof(SpmmItem) / 8;
@@ -160,20 +164,18 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
       const double* ap = tiles + it.a_off + 4 * lane;
       const double4 z4 = make_double4(0.0, 0.0, 0.0, 0.0);
       double4 a01 = n > 0 ? ldg4(ap) : z4, a23 = n > 2 ? ldg4(ap + 128) : z4;
-      for (int s = 0; s < n; s += 2) {
-        if (s + 1 < n) lds_b(s + 1, b1);
+      for (int s = 0; s < n; s += 2) {  // an odd n ends on the zero A step (pad rows for B)
+        lds_b(s + 1, b1);
 #pragma unroll
         for (int i = 0; i < NT; ++i) {
           dmma(acc[0][i][0], acc[0][i][1], a01.x, b0[i]);
           dmma(acc[1][i][0], acc[1][i][1], a01.y, b0[i]);
         }
-        if (s + 1 < n) {
-          if (s + 2 < n) lds_b(s + 2, b0);
+        lds_b(s + 2, b0);
 #pragma unroll
-          for (int i = 0; i < NT; ++i) {
-            dmma(acc[0][i][0], acc[0][i][1], a01.z, b1[i]);
-            dmma(acc[1][i][0], acc[1][i][1], a01.w, b1[i]);
-          }
+        for (int i = 0; i < NT; ++i) {
+          dmma(acc[0][i][0], acc[0][i][1], a01.z, b1[i]);
+          dmma(acc[1][i][0], acc[1][i][1], a01.w, b1[i]);
         }
         a01 = a23;
         a23 = (s + 4 < n) ? ldg4(ap + 64 * (s + 4)) : z4;
@@ -184,14 +186,12 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
       const double4 z4 = make_double4(0.0, 0.0, 0.0, 0.0);
       double4 a01 = n > 0 ? ldg4(ap) : z4, a23 = n > 2 ? ldg4(ap + 128) : z4;
       for (int s = 0; s < n; s += 2) {
-        if (s + 1 < n) lds_b(s + 1, b1);
+        lds_b(s + 1, b1);
 #pragma unroll
         for (int i = 0; i < NT; ++i) dmma(acc[0][i][0], acc[0][i][1], a01.x, b0[i]);
-        if (s + 1 < n) {
-          if (s + 2 < n) lds_b(s + 2, b0);
+        lds_b(s + 2, b0);
 #pragma unroll
-          for (int i = 0; i < NT; ++i) dmma(acc[0][i][0], acc[0][i][1], a01.z, b1[i]);
-        }
+        for (int i = 0; i < NT; ++i) dmma(acc[0][i][0], acc[0][i][1], a01.z, b1[i]);
         a01 = a23;
         a23 = (s + 4 < n) ? ldg4(ap + 64 * (s + 4)) : z4;
       }
@@ -253,7 +253,8 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
 template <int NT>
 xc_status launch(const SpmmWin* wins, int nwins, const SpmmItem* items, const double* tiles, const SpmmSrcs& srcs,
                  double* part, int64_t ldp, int ncols, cudaStream_t st) {
-  const size_t sm = (size_t)XC_WMAX * (8 * NT + 4) * sizeof(double) + (size_t)XC_WIN_ITEMS * sizeof(SpmmItem);
+  const size_t sm =
+      (size_t)(XC_WMAX + kPadRows) * (8 * NT + 4) * sizeof(double) + (size_t)XC_WIN_ITEMS * sizeof(SpmmItem);
   static std::atomic<unsigned long long> once{0};
   if (first_on_device(once)) {
     XC_CUDA(cudaFuncSetAttribute(spmm_win<NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
