@@ -260,11 +260,11 @@ xc_status launch(const SpmmWin* wins, int nwins, const SpmmItem* items, const do
     XC_CUDA(cudaFuncSetAttribute(spmm_win<NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     XC_CUDA(cudaFuncSetAttribute(spmm_win<NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   }
-  // the A-stream L2 prefetch for grids of 1 to 16 waves of 2 CTAs per SM (c3 +3 %, c4 +0.5 %, its
-  // input axis +1.3 %; not the µs-scale grids of c2/c6/c7 nor the long c5 grid); XC_SPMM_PF=0/1 forces
-  const int64_t ctas = (int64_t)nwins * ((ncols + 8 * NT - 1) / (8 * NT)), wave = 2 * (int64_t)sm_count();
+  // the A-stream L2 prefetch instance (XC_SPMM_PF=1; measurement switch).  It paid on grids of 1 to
+  // 16 waves with 16-byte A loads (c3 +3 %); with the 32-byte step-pair loads it no longer does
+  // (c3 0.1045 vs 0.1049 ms, c4 1.267 vs 1.245 ms without it), so it is off by default
   static const int force = getenv("XC_SPMM_PF") ? atoi(getenv("XC_SPMM_PF")) : -1;
-  const bool pf = force >= 0 ? force != 0 : (ctas >= wave && ctas < 16 * wave);
+  const bool pf = force > 0;
   for (int w0 = 0; w0 < nwins; w0 += 65535) {
     int nw = std::min(65535, nwins - w0);
     dim3 grid((ncols + 8 * NT - 1) / (8 * NT), nw);
