@@ -672,7 +672,11 @@ xc_status finalize_bands(xc_op* h, BlockData& b) {
 // same rows may be paired into one item: they then share the B fragments (half the shared-
 // memory traffic per DMMA) but both run over the union of the ranges.  Pairing is used only
 // where the union adds little (kPairSlack); otherwise the item carries one M-tile.
-constexpr double kPairSlack = 1.08;
+constexpr double kPairSlackDefault = 1.08;
+double pair_slack() {  // XC_PAIR_SLACK overrides (measurement switch)
+  static const double v = getenv("XC_PAIR_SLACK") ? atof(getenv("XC_PAIR_SLACK")) : kPairSlackDefault;
+  return v;
+}
 
 struct MTile {
   int fam;        // block index, or -1 for the dense tail
@@ -695,7 +699,7 @@ bool worth_pairing(const MTile& a, const MTile& b) {
   if (la == 0 || lb == 0) return false;
   const int u0 = std::min(a.k0, b.k0), u1 = std::max(a.k1, b.k1);
   if (u1 - u0 > XC_WMAX - 3) return false;  // the pair must fit one shared-memory window
-  return 2.0 * (u1 - u0) <= kPairSlack * (la + lb);
+  return 2.0 * (u1 - u0) <= pair_slack() * (la + lb);
 }
 
 // Emit one item for M-tile a (and b, if non-null) reading operand source `src`.
