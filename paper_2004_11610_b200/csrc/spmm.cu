@@ -164,7 +164,8 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
       const double* ap = tiles + it.a_off + 4 * lane;
       const double4 z4 = make_double4(0.0, 0.0, 0.0, 0.0);
       double4 a01 = n > 0 ? ldg4(ap) : z4, a23 = n > 2 ? ldg4(ap + 128) : z4;
-      for (int s = 0; s < n; s += 2) {  // an odd n ends on the zero A step (pad rows for B)
+      int s = 0;
+      for (; s + 1 < n; s += 2) {  // step pairs, no bounds branches (the B load one step ahead may read pad rows)
         lds_b(s + 1, b1);
 #pragma unroll
         for (int i = 0; i < NT; ++i) {
@@ -180,12 +181,20 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
         a01 = a23;
         a23 = (s + 4 < n) ? ldg4(ap + 64 * (s + 4)) : z4;
       }
+      if (s < n) {  // odd n: the last step alone (b0 and a01.xy hold it)
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+          dmma(acc[0][i][0], acc[0][i][1], a01.x, b0[i]);
+          dmma(acc[1][i][0], acc[1][i][1], a01.y, b0[i]);
+        }
+      }
     } else {
       // one M-tile (slot 0 of the A stream), A fragments streamed 4 steps ahead, two per load
       const double* ap = tiles + it.a_off + 4 * lane;
       const double4 z4 = make_double4(0.0, 0.0, 0.0, 0.0);
       double4 a01 = n > 0 ? ldg4(ap) : z4, a23 = n > 2 ? ldg4(ap + 128) : z4;
-      for (int s = 0; s < n; s += 2) {
+      int s = 0;
+      for (; s + 1 < n; s += 2) {
         lds_b(s + 1, b1);
 #pragma unroll
         for (int i = 0; i < NT; ++i) dmma(acc[0][i][0], acc[0][i][1], a01.x, b0[i]);
@@ -194,6 +203,10 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
         for (int i = 0; i < NT; ++i) dmma(acc[0][i][0], acc[0][i][1], a01.z, b1[i]);
         a01 = a23;
         a23 = (s + 4 < n) ? ldg4(ap + 64 * (s + 4)) : z4;
+      }
+      if (s < n) {
+#pragma unroll
+        for (int i = 0; i < NT; ++i) dmma(acc[0][i][0], acc[0][i][1], a01.x, b0[i]);
       }
     }
 
