@@ -6,6 +6,6 @@ one() {
   python -c "
 import json;d=json.load(open('gpurun_out/exp.json'));r=d['roofline'];print('%-22s'%'$1','ms %.4f'%d['ms_per_step'],'spmm %.4f fft %.4f frac %.3f eff %.3f'%(r['spmm_ms'],r['fft_ms'],r['frac'],r.get('dmma_issue_efficiency',0)))"
 }
-for v in 1.0 1.08 1.2 1.35 1.6; do
+for v in ${SLACKS:-1.0 1.08 1.2}; do
   for c in c5 c3 c4; do one "$c slack=$v" "XC_PAIR_SLACK=$v" "--config $c"; done
 done
