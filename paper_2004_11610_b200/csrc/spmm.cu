@@ -288,6 +288,10 @@ xc_status launch(const SpmmWin* wins, int nwins, const SpmmItem* items, const do
   return XC_OK;
 }
 
+constexpr int kRedBatch = 16;
+constexpr int kRedDeepMin = 48;  // chains at least this long take the deep instance
+
+template <bool DEEP>
 __global__ void reduce_rows8_kernel(const double* __restrict__ part, int64_t ldp, const int64_t* __restrict__ base,
                                     const int* __restrict__ nch, int nrows, const double* __restrict__ rowscale,
                                     double* __restrict__ Y, int64_t ldy, int ncols) {
@@ -298,11 +302,29 @@ __global__ void reduce_rows8_kernel(const double* __restrict__ part, int64_t ldp
     int64_t r0 = base[g] + (row & 7);
     double sc = rowscale ? rowscale[row] : 1.0;
     for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < ncols; col += gridDim.x * blockDim.x) {
-      // four loads in flight, summed in chunk order (the same rounding as the plain loop)
+      // summed in chunk order (the same rounding as the plain loop).  Long chains (the small-L
+      // blocks and the tail: up to N / 184 chunks) are latency bound, so the loads run two
+      // batches of 16 ahead of the adds (c5 block 8: 356 chunks, 72 us at four in flight)
       const double* p = part + r0 * ldp + col;
       const int64_t st = 8 * ldp;
       double s = 0.0;
       int c = 0;
+      if (DEEP && n >= 2 * kRedBatch) {
+        double a[kRedBatch];
+#pragma unroll
+        for (int i = 0; i < kRedBatch; ++i) a[i] = __ldcs(p + (c + i) * st);
+        for (c = kRedBatch; c + kRedBatch <= n; c += kRedBatch) {
+          double b[kRedBatch];
+#pragma unroll
+          for (int i = 0; i < kRedBatch; ++i) b[i] = __ldcs(p + (c + i) * st);
+#pragma unroll
+          for (int i = 0; i < kRedBatch; ++i) s += a[i];
+#pragma unroll
+          for (int i = 0; i < kRedBatch; ++i) a[i] = b[i];
+        }
+#pragma unroll
+        for (int i = 0; i < kRedBatch; ++i) s += a[i];
+      }
       for (; c + 4 <= n; c += 4) {
         const double v0 = __ldcs(p + c * st), v1 = __ldcs(p + (c + 1) * st);
         const double v2 = __ldcs(p + (c + 2) * st), v3 = __ldcs(p + (c + 3) * st);
@@ -345,11 +367,16 @@ xc_status spmm_run(const SpmmWin* wins, int nwins, const SpmmItem* items, const 
 }
 
 xc_status reduce_rows8(const double* part, int64_t ldp, const int64_t* base, const int* nch, int nrows,
-                       const double* rowscale, double* Y, int64_t ldy, int ncols, cudaStream_t st) {
+                       const double* rowscale, double* Y, int64_t ldy, int ncols, int maxn, cudaStream_t st) {
   if (nrows <= 0) return XC_OK;
   int th = ncols >= 256 ? 256 : (ncols >= 64 ? 64 : 32);
   dim3 grid(std::min((ncols + th - 1) / th, 64), std::min(nrows, 65535));
-  reduce_rows8_kernel<<<grid, th, 0, st>>>(part, ldp, base, nch, nrows, rowscale, Y, ldy, ncols);
+  // the deep instance (86 registers) only where chains are long: short chains (c5 block 3, ~2
+  // chunks, HBM bound) need the occupancy of the 32-register one
+  if (maxn >= kRedDeepMin)
+    reduce_rows8_kernel<true><<<grid, th, 0, st>>>(part, ldp, base, nch, nrows, rowscale, Y, ldy, ncols);
+  else
+    reduce_rows8_kernel<false><<<grid, th, 0, st>>>(part, ldp, base, nch, nrows, rowscale, Y, ldy, ncols);
   XC_CUDA(cudaGetLastError());
   return XC_OK;
 }

@@ -79,6 +79,7 @@ struct BlockData {
   int ngroups = 0;
   int64_t loc_count = 0;  // values of the locally computed node range (distributed precompute)
   DevBuf grp_base, grp_nch;  // output axis groups
+  int grp_nch_max = 0;       // the longest chunk chain (reduce_rows8's instance)
 };
 
 template <typename T>
@@ -157,11 +158,13 @@ struct xc_op {
   int64_t rowsA = 0, tilesA_n = 0, mtstepsA = 0;  // M-tile steps issued (DMMA accounting)
   int ntailg = 0;
   DevBuf tail_base, tail_nch;
+  int tail_nch_max = 0;
   // input axis
   DevBuf itemsW, tilesW, winsW;
   int nitemsW = 0, nwinsW = 0;
   int64_t rowsW = 0, tilesW_n = 0, mtstepsW = 0;
   DevBuf nodeg_base, nodeg_nch;
+  int nodeg_nch_max = 0;
   DevBuf nodeg_base_im;  // XC_EXP: partial rows of the imaginary parts per node group
   // workspaces: the handle's own (xc_reserve; also the host-buffer pipeline's) and the ones the
   // caller attaches to streams (xc_attach_workspace); xc_apply uses the one bound to its stream
@@ -925,6 +928,7 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
     if (b.split) {
       XC_TRY(upload(b.grp_base, gbase));
       XC_TRY(upload(b.grp_nch, gnch));
+      b.grp_nch_max = gnch.empty() ? 0 : *std::max_element(gnch.begin(), gnch.end());
     }
     pair_list(mt, 0, S);  // the direct groups, consecutive in g
   }
@@ -952,6 +956,7 @@ xc_status build_output_axis(xc_op* h, cudaStream_t st) {
   pair_list(mt, 0, S);
   XC_TRY(upload(h->tail_base, tbase));
   XC_TRY(upload(h->tail_nch, tnch));
+  h->tail_nch_max = tnch.empty() ? 0 : *std::max_element(tnch.begin(), tnch.end());
   h->rowsA = rows;
   return upload_and_fill(h, S, false, h->itemsA, h->winsA, h->tilesA, h->nitemsA, h->nwinsA, h->tilesA_n, st);
 }
@@ -1010,6 +1015,7 @@ xc_status build_input_axis_cc(xc_op* h, cudaStream_t st) {
   XC_TRY(upload(h->nodeg_base, gbase));
   XC_TRY(upload(h->nodeg_base_im, gbase_im));
   XC_TRY(upload(h->nodeg_nch, gnch));
+  h->nodeg_nch_max = gnch.empty() ? 0 : *std::max_element(gnch.begin(), gnch.end());
   h->rowsW = rows;
   return upload_and_fill(h, S, true, h->itemsW, h->winsW, h->tilesW, h->nitemsW, h->nwinsW, h->tilesW_n, st);
 }
@@ -1073,6 +1079,7 @@ xc_status build_input_axis(xc_op* h, cudaStream_t st) {
   }
   XC_TRY(upload(h->nodeg_base, gbase));
   XC_TRY(upload(h->nodeg_nch, gnch));
+  h->nodeg_nch_max = gnch.empty() ? 0 : *std::max_element(gnch.begin(), gnch.end());
   h->rowsW = rows;
   return upload_and_fill(h, S, true, h->itemsW, h->winsW, h->tilesW, h->nitemsW, h->nwinsW, h->tilesW_n, st);
 }
@@ -1849,7 +1856,7 @@ xc_status apply_impl(xc_op* h, Ws& w, xc_dir dir, const double* X, int64_t ldx, 
       double* U = w.partA + b.ubase * Bp;
       if (b.split)
         XC_TRY(reduce_rows8(w.partA, Bp, (const int64_t*)b.grp_base.p, (const int*)b.grp_nch.p,
-                            8 * b.ngroups, nullptr, U, Bp, (int)Bp, st));
+                            8 * b.ngroups, nullptr, U, Bp, (int)Bp, b.grp_nch_max, st));
       // v = F* u over all L bins (complex inverse DFT), then Fe2 discard and W^{-1}
       FftIO io{};
       io.src = reinterpret_cast<const double2*>(U);
@@ -1893,7 +1900,7 @@ xc_status apply_impl(xc_op* h, Ws& w, xc_dir dir, const double* X, int64_t ldx, 
       double* U = w.partA + b.ubase * Bp;
       if (b.split)  // interleaved complex rows: reduce all Bp doubles of each double row
         XC_TRY(reduce_rows8(w.partA, Bp, (const int64_t*)b.grp_base.p, (const int*)b.grp_nch.p,
-                            8 * b.ngroups, nullptr, U, Bp, (int)Bp, sb));
+                            8 * b.ngroups, nullptr, U, Bp, (int)Bp, b.grp_nch_max, sb));
       FftIO io{};
       io.Uc = reinterpret_cast<const double2*>(U);
       io.ldu = Bp;
@@ -1907,12 +1914,18 @@ xc_status apply_impl(xc_op* h, Ws& w, xc_dir dir, const double* X, int64_t ldx, 
       io.keep_hi = b.keep_hi;
       io.m_off = b.m_off;
       XC_TRY(c2r_run(b.fftM, io, (int)B, scr, sb));
+      // the dense tail's rows [0, t) are disjoint from every block's kept rows [s_i, e_i) (the
+      // chain ends at s = t, m_off = 0), so its reduction runs beside the FFT phase, after block
+      // 2 on that block's stream (the lightest), instead of after the join (c3: 19 us at the end)
+      if (ib == std::min(1, nb - 1) && h->tail > 0)
+        XC_TRY(reduce_rows8(w.partA, Bp, (const int64_t*)h->tail_base.p, (const int*)h->tail_nch.p,
+                            h->tail, nullptr, Y, ldy, (int)B, h->tail_nch_max, sb));
     }
     XC_TRY(fork_end(h, w, st, fork));
     XC_TRY(mark(2));
-    if (h->tail > 0)
+    if (nb == 0 && h->tail > 0)  // a tail-only operator (N <= the dense cutoff)
       XC_TRY(reduce_rows8(w.partA, Bp, (const int64_t*)h->tail_base.p, (const int*)h->tail_nch.p,
-                          h->tail, nullptr, Y, ldy, (int)B, st));
+                          h->tail, nullptr, Y, ldy, (int)B, h->tail_nch_max, st));
     return mark(3);
   }
   // XC_DIR_WAT
@@ -1944,9 +1957,9 @@ xc_status apply_impl(xc_op* h, Ws& w, xc_dir dir, const double* X, int64_t ldx, 
                     (const double*)h->tilesW.p, s, w.partW, Bp, (int)B, st));
     XC_TRY(mark(2));
     XC_TRY(reduce_rows8(w.partW, Bp, (const int64_t*)h->nodeg_base.p, (const int*)h->nodeg_nch.p,
-                        N, (const double*)h->wt.p, Y, ldy, (int)B, st));
+                        N, (const double*)h->wt.p, Y, ldy, (int)B, h->nodeg_nch_max, st));
     XC_TRY(reduce_rows8(w.partW, Bp, (const int64_t*)h->nodeg_base_im.p,
-                        (const int*)h->nodeg_nch.p, N, (const double*)h->wt.p, Y + (int64_t)N * ldy, ldy, (int)B, st));
+                        (const int*)h->nodeg_nch.p, N, (const double*)h->wt.p, Y + (int64_t)N * ldy, ldy, (int)B, h->nodeg_nch_max, st));
     return mark(3);
   }
   SpmmSrcs s{};
@@ -1987,7 +2000,7 @@ xc_status apply_impl(xc_op* h, Ws& w, xc_dir dir, const double* X, int64_t ldx, 
                   (const double*)h->tilesW.p, s, w.partW, Bp, (int)B, st));
   XC_TRY(mark(2));
   XC_TRY(reduce_rows8(w.partW, Bp, (const int64_t*)h->nodeg_base.p, (const int*)h->nodeg_nch.p, N,
-                      (const double*)h->wt.p, Y, ldy, (int)B, st));
+                      (const double*)h->wt.p, Y, ldy, (int)B, h->nodeg_nch_max, st));
   return mark(3);
 }
 

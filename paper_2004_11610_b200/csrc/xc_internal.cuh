@@ -246,7 +246,7 @@ int spmm_nt_for(int64_t B);
 // ---------------------------------------------------------------------------
 // Y[deg][b] = sum_c part[(base(g) + 8c + deg % 8)][b], g = deg / 8, deg in [0, t)
 xc_status reduce_rows8(const double* part, int64_t ldp, const int64_t* base, const int* nch, int nrows,
-                       const double* rowscale, double* Y, int64_t ldy, int ncols, cudaStream_t st);
+                       const double* rowscale, double* Y, int64_t ldy, int ncols, int maxn, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // Precompute kernels (gen.cu)
