@@ -24,10 +24,11 @@ using namespace xcb;
 
 // launch 1: rows = every block's bins (complex rows of u) then the tail degrees (real Y rows).
 // One launch, two kinds of CTAs (blockIdx.x < nshort: short rows; else long rows):
-// * short rows: a CTA of 256 threads takes RB = 256 / CT rows x CT columns (column tile blockIdx.x %
-//   ntile); with STAGE it first copies its CT columns of X to shared memory (N x CT doubles).  A
-//   thread sums its row's entries in entry order (nodes ascending), the loads of 4 entries issued
-//   ahead of their FMAs (no dependent-load chain per entry);
+// * short rows: a CTA of 256 threads takes RB = 256 / (4 CT) rows x CT columns (column tile
+//   blockIdx.x % ntile); with STAGE it first copies its CT columns of X to shared memory (N x CT
+//   doubles).  Four lanes share a (row, column): each sums a quarter of the row's entries in entry
+//   order (nodes ascending) with all its loads issued in one batch, then two shuffles add the
+//   quarters as (s0 + s1) + (s2 + s3);
 // * long rows (more than kSmallLong entries: the dense tail degrees, the bins of the short blocks
 //   that every node touches): one warp per (row, column), lane l sums entries l, l + 32, ... in
 //   order, then a fixed shuffle tree.
@@ -114,52 +115,49 @@ __global__ void __launch_bounds__(256, 2) small_spmm_k(const SmallOp op, const d
     }
     __syncthreads();
   }
-  const int r = ((int)blockIdx.x / ntile) * (256 / CT) + tid / CT;
-  const int lc = tid % CT, c = c0 + lc;
-  if (r >= op.rows || c >= B) return;
-  const int64_t e0 = op.ptr[r], e1 = op.ptr[r + 1];
-  if (e1 - e0 > kSmallLong) return;  // a long row
+  // kSmallSub adjacent lanes per (row, column): sub-lane j sums the j-th quarter of the row's
+  // entries in entry order (all of its loads in one batch), then (s0 + s1) + (s2 + s3) by two xor
+  // shuffles -- a fixed order per row, independent of B and of the CTA shape
+  const int sub = tid % kSmallSub, t = tid / kSmallSub;
+  const int r = ((int)blockIdx.x / ntile) * (256 / (CT * kSmallSub)) + t / CT;
+  const int lc = t % CT, c = c0 + lc;
+  const bool live = r < op.rows && c < B;
+  int64_t e0 = 0, e1 = 0;
+  if (live) {
+    e0 = op.ptr[r];
+    e1 = op.ptr[r + 1];
+  }
+  const bool longrow = e1 - e0 > kSmallLong;  // a long row (the warp CTAs take it)
   auto xv = [&](int k) { return STAGE ? xs[k * CT + lc] : __ldg(X + (int64_t)k * ldx + c); };
+  const int q = (int)((e1 - e0 + kSmallSub - 1) / kSmallSub);  // <= kSmallLong / kSmallSub
+  const int64_t s0 = e0 + (int64_t)sub * q, s1 = min(e1, s0 + q);
   double re = 0.0, im = 0.0;
-  int64_t e = e0;
-  for (; e + 8 <= e1; e += 8) {  // eight entries' loads in flight, summed in order
-    int k[8];
-    double2 v[8];
-    double x[8];
+  if (live && !longrow) {
+    constexpr int Q = kSmallLong / kSmallSub;
+    int k[Q];
+    double2 v[Q];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      k[i] = __ldg(op.node + e + i);
-      v[i] = __ldg(op.val + e + i);
+    for (int i = 0; i < Q; ++i) {
+      const bool in = s0 + i < s1;
+      k[i] = in ? __ldg(op.node + s0 + i) : 0;
+      v[i] = in ? __ldg(op.val + s0 + i) : make_double2(0.0, 0.0);
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = xv(k[i]);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      re = fma(v[i].x, x[i], re);
-      im = fma(v[i].y, x[i], im);
+    for (int i = 0; i < Q; ++i) {
+      if (s0 + i < s1) {
+        const double x = xv(k[i]);
+        re = fma(v[i].x, x, re);
+        im = fma(v[i].y, x, im);
+      }
     }
   }
-  for (; e + 4 <= e1; e += 4) {
-    const int k0 = __ldg(op.node + e), k1 = __ldg(op.node + e + 1), k2 = __ldg(op.node + e + 2),
-              k3 = __ldg(op.node + e + 3);
-    const double2 v0 = __ldg(op.val + e), v1 = __ldg(op.val + e + 1), v2 = __ldg(op.val + e + 2),
-                  v3 = __ldg(op.val + e + 3);
-    const double x0 = xv(k0), x1 = xv(k1), x2 = xv(k2), x3 = xv(k3);
-    re = fma(v0.x, x0, re);
-    im = fma(v0.y, x0, im);
-    re = fma(v1.x, x1, re);
-    im = fma(v1.y, x1, im);
-    re = fma(v2.x, x2, re);
-    im = fma(v2.y, x2, im);
-    re = fma(v3.x, x3, re);
-    im = fma(v3.y, x3, im);
-  }
-  for (; e < e1; ++e) {
-    const double x = xv(__ldg(op.node + e));
-    const double2 v = __ldg(op.val + e);
-    re = fma(v.x, x, re);
-    im = fma(v.y, x, im);
-  }
+  // lanes of one (row, column) are adjacent and share live / longrow, so whole groups of
+  // kSmallSub lanes take part in each shuffle
+  re += __shfl_xor_sync(0xffffffffu, re, 1);
+  im += __shfl_xor_sync(0xffffffffu, im, 1);
+  re += __shfl_xor_sync(0xffffffffu, re, 2);
+  im += __shfl_xor_sync(0xffffffffu, im, 2);
+  if (!live || longrow || sub != 0) return;
   const int64_t o = op.out[r];
   if (o >= 0) U[o * ldu + c] = make_double2(re, im);   // u row of a block
   else Y[(-o - 1) * ldy + c] = re;                     // tail degree -o-1
@@ -258,7 +256,8 @@ xc_status small_spmm(const SmallOp& op, const double* X, int64_t ldx, double2* U
   for (int c0 = 0; c0 < B; c0 += 65535) {  // keeps the 1D grid small
     const int bc = std::min(B - c0, 65535);
     const int ntile = (bc + CT - 1) / CT;
-    const int64_t nshort = (int64_t)((op.rows + 256 / CT - 1) / (256 / CT)) * ntile;
+    const int rb = 256 / (CT * kSmallSub);  // short rows per CTA
+    const int64_t nshort = (int64_t)((op.rows + rb - 1) / rb) * ntile;
     const int64_t nlong = ((int64_t)op.nlong * bc + 7) / 8;
     const unsigned grid = (unsigned)(nshort + nlong);
     if (stage)

@@ -358,6 +358,7 @@ struct SmallOp {
   int nlong;
 };
 constexpr int kSmallLong = 64;
+constexpr int kSmallSub = 4;  // lanes per short (row, column) of the gather (kSmallLong / kSmallSub loads each)
 struct SmallBlk {
   int M, nf, f[16];
   int m_off, keep_lo, keep_hi;
