@@ -110,6 +110,12 @@ def _timing_nodes(cfg):
         return I.lag2d_grid(cfg.N, cfg.eta)
     if cfg.kind == I.KIND_LAGUERRE:
         return np.linspace(0.0, 4.0 * cfg.N, cfg.N)   # scipy's Laguerre rule overflows at this N
+    if cfg.N > 8192:
+        # scipy's rules are an O(N^2) banded eigenvalue solve (minutes at N = 65536, which once ran
+        # the reference arm into its time limit): the classical first-order estimate of the Gauss-
+        # Jacobi nodes, theta_k = pi (2k + alpha - 1/2) / (2N + alpha + beta + 1), serves the timing
+        k = np.arange(1, cfg.N + 1, dtype=np.float64)
+        return np.sort(np.cos(np.pi * (2.0 * k + cfg.alpha - 0.5) / (2.0 * cfg.N + cfg.alpha + cfg.beta + 1.0)))
     if cfg.alpha == 0.0 and cfg.beta == 0.0:
         return scipy.special.roots_legendre(cfg.N)[0]
     return scipy.special.roots_jacobi(cfg.N, cfg.alpha, cfg.beta)[0]
