@@ -57,6 +57,15 @@ class Clocks:
         except Exception:
             self.p = None
 
+    def wait_ready(self, timeout=8.0):
+        """Block until the sampler has written its first line (a cold nvidia-smi can take longer to
+        start than a short timed region lasts)."""
+        t0 = time.perf_counter()
+        while self.p is not None and time.perf_counter() - t0 < timeout:
+            if os.path.getsize(self.f.name) > 0:
+                return
+            time.sleep(0.05)
+
     def stop(self):
         if self.p is None:
             return None
@@ -354,7 +363,8 @@ def main():
     if dist:
         dist.barrier()
     clocks = Clocks(local) if rank == 0 else None
-    time.sleep(0.3 if clocks else 0)
+    if clocks:
+        clocks.wait_ready()
     # ---- timed region: xc_apply as a user calls it (its default CUDA-graph replay: a call
     # repeated with the same arguments is captured on its 2nd occurrence and replayed after) ----
     for _ in range(2):
